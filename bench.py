@@ -1,0 +1,318 @@
+#!/usr/bin/env python
+"""Sweep-throughput benchmark (BASELINE.json config C5; metric "sweep
+cell-angle updates/s").
+
+One step = one batched transport sweep (K1) of every direction of the C5
+workload: a GRID^2 mesh, CL(N_THETA, N_OMEGA_Z) directions, sigma_t = 1,
+random fp64 per-(cell, direction) sources from the counter-based generator
+(seed 12345), inputs resident in HBM.  `value` is device-timed (CUDA events
+on the problem's stream, max over ranks); `e2e` is the same metric through
+the C ABI with HOST buffers (pinned), host<->device copies inside the timed
+region; `cpu_baseline` is the CPU oracle (a single-threaded restatement of
+the reference's sweep, proj/src/sweep.cpp:9-57) timed on a bounded sample.
+
+--impl reference times that CPU implementation on all host threads instead
+(the reference itself cannot be built: Eigen is absent).
+
+Multi-GPU: one process per GPU (torchrun); every rank sweeps its own copy of
+the direction set with rank-specific sources (weak scaling, no collective on
+the data path); the step time is the max over ranks.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+SEED = 12345
+BYTES_PER_UPDATE = 64  # 32 B source cell read + 32 B psi cell write
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--grid", type=int, default=512)
+    ap.add_argument("--n-theta", type=int, default=128)
+    ap.add_argument("--n-omega-z", type=int, default=32)
+    ap.add_argument("--e2e-chunk", type=int, default=128, help="directions per host-buffer call")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--cpu-sample-dirs", type=int, default=8)
+    return ap.parse_args()
+
+
+def load_peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            return json.load(f)["hbm_gbs"], "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+def load_traffic():
+    """dram bytes per sweep launch from the committed ncu --set full capture."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "sweep_traffic.json")) as f:
+            return json.load(f)
+    except Exception:
+        return None
+
+
+class Clocks:
+    """nvidia-smi sampler running during the timed region."""
+
+    def __init__(self, index):
+        self.index = index
+        self.lines = []
+        self.proc = None
+
+    def __enter__(self):
+        q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+             "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={q}",
+                                          "--format=csv,noheader,nounits", "-lms", "200"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 8:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx = float(parts[1])
+            except ValueError:
+                continue
+            for name, v in zip(names, parts[4:8]):
+                if v.lower() == "active":
+                    reasons.add(name)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def cpu_sweep_rate(grid, n_theta, n_omega_z, ndirs, threads):
+    """The CPU oracle sweep (port of proj/src/sweep.cpp) on `ndirs` directions
+    of the same workload, spread over `threads` host threads (ctypes drops
+    the GIL).  Returns (updates/s, updates, seconds)."""
+    import concurrent.futures as cf
+
+    import numpy as np
+    sys.path.insert(0, os.path.join(ROOT, "tests"))
+    import _oracle as O
+    probs = [O.Problem("C5", nx=grid, ny=grid, n_theta=n_theta, n_omega_z=n_omega_z, use_dsa=0)
+             for _ in range(threads)]
+    d = probs[0].get("dirs")
+    n = probs[0].n
+    stride = max(1, (n_theta * n_omega_z) // ndirs)
+    dirs = [(k * stride) % (n_theta * n_omega_z) for k in range(ndirs)]
+    srcs = {j: O.c5_fill(SEED, j, 1, n)[0] for j in dirs}
+
+    def work(t):
+        for k in range(t, ndirs, threads):
+            j = dirs[k]
+            probs[t].sweep(d[j, 0], d[j, 1], srcs[j])
+
+    t0 = time.perf_counter()
+    with cf.ThreadPoolExecutor(threads) as ex:
+        list(ex.map(work, range(threads)))
+    dt = time.perf_counter() - t0
+    upd = ndirs * (n // 4)
+    return upd / dt, upd, dt
+
+
+def run_reference(args, rank, world):
+    """--impl reference: the CPU implementation on all host threads (rank 0)."""
+    if rank != 0:
+        return
+    threads = os.cpu_count() or 1
+    ndirs = max(threads, (threads * 2))
+    for _ in range(max(0, args.warmup)):
+        cpu_sweep_rate(args.grid, args.n_theta, args.n_omega_z, threads, threads)
+    rates, times = [], []
+    for _ in range(args.steps):
+        r, upd, dt = cpu_sweep_rate(args.grid, args.n_theta, args.n_omega_z, ndirs, threads)
+        rates.append(r)
+        times.append(dt)
+    value = sum(r * t for r, t in zip(rates, times)) / sum(times)
+    sample = f"{ndirs} of {args.n_theta * args.n_omega_z} directions per step on {args.grid}^2 cells"
+    line = {
+        "impl": "reference", "metric": "sweep cell-angle updates/s", "value": value,
+        "unit": "cell-angle updates/s", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": 1e3 * statistics.mean(times), "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": workload_config(args),
+        "cpu_baseline": {"value": value, "unit": "cell-angle updates/s", "cores": threads, "kind": "port",
+                         "sample": sample},
+        "e2e": {"value": value, "unit": "cell-angle updates/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def workload_config(args):
+    nd = args.n_theta * args.n_omega_z
+    return {"workload": f"C5 sweep {args.grid}^2 cells x CL({args.n_theta},{args.n_omega_z}) = {nd} directions",
+            "grid": args.grid, "directions": nd, "quadrature": f"CL({args.n_theta},{args.n_omega_z})",
+            "sigma_t": 1.0, "source": "U[0,1) per (cell, direction), counter-based, seed 12345",
+            "l2": "inputs larger than L2 (no flush needed)", "parallelism": f"direction sets x{args.gpus}"}
+
+
+def main():
+    args = parse()
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        run_reference(args, rank, world)
+        return
+
+    import numpy as np
+    import torch
+    import paper_2603_25233_b200 as P
+
+    torch.cuda.set_device(local)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+
+    prob = P.Problem("C5", device=local, nx=args.grid, ny=args.grid, n_theta=args.n_theta,
+                     n_omega_z=args.n_omega_z, use_dsa=0)
+    stream = torch.cuda.current_stream()
+    prob.set_stream(stream.cuda_stream)
+    D, n = prob.n_omega, prob.n
+    cells = n // 4
+    rhs = torch.empty(D * n, dtype=torch.float64, device="cuda")
+    psi = torch.empty(D * n, dtype=torch.float64, device="cuda")
+    angles = torch.arange(D, dtype=torch.int32, device="cuda")
+    prob.c5_fill(rhs.data_ptr(), D, rank * D, SEED)
+
+    def step():
+        prob.sweep_async(angles.data_ptr(), D, rhs.data_ptr(), n, psi.data_ptr(), n)
+
+    for _ in range(args.warmup):
+        step()
+    prob.check()
+
+    def barrier():
+        if dist:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    barrier()
+    with Clocks(local) as clk:
+        start.record(stream)
+        for _ in range(args.steps):
+            step()
+        end.record(stream)
+        torch.cuda.synchronize()
+    barrier()
+    prob.check()
+    ms = start.elapsed_time(end) / args.steps
+    t = torch.tensor([ms], dtype=torch.float64, device="cuda")
+    if dist:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms_max = float(t.item())
+    value = world * D * cells / (ms_max * 1e-3)
+
+    # Kernel-only duration of the sweep launch (same stream, events around it).
+    k0, k1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    k0.record(stream)
+    step()
+    k1.record(stream)
+    torch.cuda.synchronize()
+    kernel_ms = k0.elapsed_time(k1)
+    peak, peak_kind = load_peaks()
+    achieved = BYTES_PER_UPDATE * D * cells / (kernel_ms * 1e-3) / 1e9
+    traffic = load_traffic()
+    key = f"{args.grid}x{D}"
+    roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+                "peak_kind": peak_kind,
+                "traffic": (traffic or {}).get(key),
+                "bytes_per_update": BYTES_PER_UPDATE, "kernel_ms": kernel_ms}
+
+    # End to end through the C ABI with pinned host buffers.
+    e2e = None
+    if not args.no_e2e:
+        C = min(args.e2e_chunk, D)
+        h_rhs = torch.empty(C * n, dtype=torch.float64, pin_memory=True)
+        h_psi = torch.empty(C * n, dtype=torch.float64, pin_memory=True)
+        h_rhs.copy_(rhs[:C * n])
+        chunks = [np.arange(c0, min(D, c0 + C), dtype=np.int32) for c0 in range(0, D, C)]
+
+        def e2e_step():
+            for ang in chunks:
+                prob.sweep_host_ptr(ang, h_rhs.data_ptr(), n, h_psi.data_ptr(), n)
+
+        e2e_step()
+        barrier()
+        t0 = time.perf_counter()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        e2e_steps = max(1, min(args.steps, 2))
+        for _ in range(e2e_steps):
+            e2e_step()
+        e1.record(stream)
+        torch.cuda.synchronize()
+        wall = (time.perf_counter() - t0) / e2e_steps
+        et = torch.tensor([wall], dtype=torch.float64, device="cuda")
+        if dist:
+            dist.all_reduce(et, op=dist.ReduceOp.MAX)
+        e2e = {"value": world * D * cells / float(et.item()), "unit": "cell-angle updates/s",
+               "h2d_bytes_per_step": D * n * 8, "d2h_bytes_per_step": D * n * 8,
+               "steps": e2e_steps, "chunk_directions": C, "api": "rtlr_cu_sweep(where=RTLR_CU_HOST)"}
+
+    cpu = None
+    if rank == 0 and world == 1:
+        r, upd, dt = cpu_sweep_rate(args.grid, args.n_theta, args.n_omega_z, args.cpu_sample_dirs, 1)
+        cpu = {"value": r, "unit": "cell-angle updates/s", "cores": 1, "kind": "port",
+               "sample": f"{args.cpu_sample_dirs} directions x {args.grid}^2 cells ({upd} updates, {dt:.1f} s)"}
+
+    if rank == 0:
+        line = {
+            "metric": "sweep cell-angle updates/s", "value": value, "unit": "cell-angle updates/s",
+            "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_max,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic", "config": workload_config(args) | {"parallelism": f"direction-sets x{world}"},
+            "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": args.steps,
+            "clocks": clk.summary(),
+        }
+        print(json.dumps(line), flush=True)
+    if dist:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,162 @@
+/*
+ * rtlr_cu.h — C ABI of the B200 (sm_100a) compute core for the rank-adaptive
+ * low-rank SI-DSA transport solver of arXiv 2603.25233.
+ *
+ * The reference (`rtlr`, /root/reference/proj) is a static C++ library whose
+ * Eigen-typed functions are its interface; it has no FFI.  Each entry point
+ * below is the plain-pointer equivalent of one reference call, cited as
+ * file:line.  All functions return an rtlr_cu_status; on failure
+ * rtlr_cu_last_error() gives the reference's exception message.  Status
+ * codes map 1:1 onto the reference's exception classes:
+ *   RTLR_CU_INVALID_ARGUMENT <- std::invalid_argument
+ *   RTLR_CU_RUNTIME_ERROR    <- std::runtime_error (e.g. "sweep: singular
+ *                               local block", "galerkin_solve: singular
+ *                               reduced system", "build_diffusion: ...")
+ *   RTLR_CU_CONFIG_ERROR     <- rtlr::ConfigError (problem.hpp:16-18)
+ * Non-convergence is not an error (report converged == 0), as in the
+ * reference.  One host thread per problem; not reentrant.
+ *
+ * Vectors use the reference's layout: DOF = (b*nx + a)*4 + my*2 + mx
+ * (dg_space.hpp:22,45-46); angular fluxes are column-major N_x x n.
+ * `where` selects RTLR_CU_HOST (pageable/pinned host memory; copies are
+ * done inside the call) or RTLR_CU_DEVICE (pointers on the problem's GPU).
+ */
+#ifndef RTLR_CU_H
+#define RTLR_CU_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  RTLR_CU_OK = 0,
+  RTLR_CU_INVALID_ARGUMENT = 1,
+  RTLR_CU_RUNTIME_ERROR = 2,
+  RTLR_CU_CONFIG_ERROR = 3,
+  RTLR_CU_CUDA_ERROR = 4
+} rtlr_cu_status;
+
+enum { RTLR_CU_HOST = 0, RTLR_CU_DEVICE = 1 };
+
+typedef struct rtlr_cu_config rtlr_cu_config;   /* ProblemConfig (problem.hpp:69-81) */
+typedef struct rtlr_cu_problem rtlr_cu_problem; /* AssembledProblem (problem.hpp:98-106), GPU-resident */
+typedef struct rtlr_cu_report rtlr_cu_report;   /* SolveReport (report.hpp:33-44) */
+
+/* ScalarField (dg_space.hpp:10) as a C callback. */
+typedef double (*rtlr_cu_field_fn)(void* user, double x, double y);
+
+const char* rtlr_cu_last_error(void);
+int rtlr_cu_version(void);
+int rtlr_cu_device_count(void);
+
+/* ---- configuration: make_preset (problem.hpp:90, problem.cpp:111-200) plus
+ * the BASELINE configs "C1".."C5"; keys as in problem.cpp:372-451
+ * ("mesh.nx", "quadrature.n_theta", "solver.eps_si_sa", "solver.p", ...;
+ * the short forms "nx", "n_theta", "eps_si_sa", "p" are accepted too) and
+ * constant fields "sigma_s_const", "sigma_a_const", "source_const",
+ * "boundary_const". */
+int rtlr_cu_config_create(const char* preset, rtlr_cu_config** out);
+int rtlr_cu_config_set(rtlr_cu_config* cfg, const char* key, double value);
+/* which: "sigma_s" | "sigma_a" | "source" | "boundary" */
+int rtlr_cu_config_set_field(rtlr_cu_config* cfg, const char* which, rtlr_cu_field_fn fn, void* user);
+void rtlr_cu_config_destroy(rtlr_cu_config* cfg);
+
+/* ---- assemble_problem (problem.hpp:108, problem.cpp:461-483) + upload.
+ * device < 0 assembles on the host only (inputs can be inspected with
+ * rtlr_cu_problem_get; GPU entry points then fail with INVALID_ARGUMENT). */
+int rtlr_cu_problem_create(const rtlr_cu_config* cfg, int device, rtlr_cu_problem** out);
+void rtlr_cu_problem_destroy(rtlr_cu_problem* p);
+/* info: nx, ny, n_theta, n_omega_z, n_dofs, n_omega, n_unique_dirs, sigma_t_uniform */
+int rtlr_cu_problem_info(const rtlr_cu_problem* p, int64_t info[8]);
+/* Host copies of the assembled inputs: "dirs" (N_Omega x 3), "weights",
+ * "source", "sigma_t_blocks" / "sigma_s_blocks" / "sigma_a_blocks"
+ * (ncell x 16, column-major blocks), "sip_bsr" (ncell x 5 x 16: self, west,
+ * east, south, north), "stream_blocks" (ax-,ax+,ay-,ay+,bx-,bx+,by-,by+). */
+int rtlr_cu_problem_get(const rtlr_cu_problem* p, const char* what, double* out);
+/* Launch work on an external cudaStream_t (NULL: the problem's own stream). */
+int rtlr_cu_problem_set_stream(rtlr_cu_problem* p, void* cuda_stream);
+/* "pcg_rtol", "pcg_max_iters" */
+int rtlr_cu_problem_set_option(rtlr_cu_problem* p, const char* key, double value);
+int rtlr_cu_synchronize(rtlr_cu_problem* p);
+
+/* ---- sweep(ops, quad, angle, rhs) (sweep.hpp:14-15), batched over n
+ * angles: psi[:, k] = (D_{angles[k]} + Sigma_t)^{-1} rhs[:, k] (+ the
+ * angle's inflow boundary vector when the problem has one).  rhs_stride = 0
+ * shares one right-hand side; angles == NULL means 0..n-1. */
+int rtlr_cu_sweep(rtlr_cu_problem* p, const int* angles, int n, const double* rhs,
+                  int64_t rhs_stride, double* psi, int64_t psi_stride, int where);
+/* Fully asynchronous device variant: d_angles, rhs and psi are device
+ * pointers; the launch is enqueued on the problem's stream and the call
+ * returns immediately.  A singular local block is reported by the next
+ * rtlr_cu_check (which synchronizes the stream). */
+int rtlr_cu_sweep_async(rtlr_cu_problem* p, const int* d_angles, int n, const double* d_rhs,
+                        int64_t rhs_stride, double* d_psi, int64_t psi_stride);
+int rtlr_cu_check(rtlr_cu_problem* p);
+/* Same with explicit directions omega_xy[2k], omega_xy[2k+1] (no inflow). */
+int rtlr_cu_sweep_dirs(rtlr_cu_problem* p, const double* omega_xy, int n, const double* rhs,
+                       int64_t rhs_stride, double* psi, int64_t psi_stride, int where);
+/* StreamingOperator::apply (operators.hpp:53-61, operators.cpp:283-288). */
+int rtlr_cu_apply(rtlr_cu_problem* p, double omega_x, double omega_y, const double* v, double* out,
+                  int where);
+/* rhs_core = Sigma_s phi + G (full_rank.cpp:81). */
+int rtlr_cu_rhs_core(rtlr_cu_problem* p, const double* phi, double* out, int where);
+/* si_step (full_rank.hpp:28-30); psi may be NULL. */
+int rtlr_cu_si_step(rtlr_cu_problem* p, const double* phi_prev, double* phi_star, double* psi, int where);
+/* DiffusionSystem::solve / correct (diffusion.hpp:16-39); iterations may be NULL. */
+int rtlr_cu_dsa_solve(rtlr_cu_problem* p, const double* rhs, double* x, int where, int* iterations);
+int rtlr_cu_dsa_correct(rtlr_cu_problem* p, const double* phi_star, const double* phi_prev,
+                        double* delta, int where);
+/* C5 synthetic sources: rhs[k*n_dofs + i] = U[0,1)(seed, (dir0+k)*n_dofs + i). */
+int rtlr_cu_c5_fill(rtlr_cu_problem* p, double* d_rhs, int64_t n_dirs, int64_t dir0, uint64_t seed);
+
+/* ---- drivers */
+typedef struct { /* FullRankOptions (full_rank.hpp:32-37) */
+  double eps_si_sa;
+  int max_iterations;
+  int use_dsa;
+  int store_psi;
+} rtlr_cu_fr_options;
+
+typedef struct { /* LowRankOptions + LowRankParams (low_rank.hpp:29-36, 146-153) */
+  int p, q;
+  double eps_res, eps_diff, eps_svd, eps_mgs;
+  double eps_si_sa;
+  int max_iterations;
+  int use_dsa;
+  uint64_t seed;
+  int build_factors;
+} rtlr_cu_lr_options;
+
+void rtlr_cu_fr_options_default(rtlr_cu_fr_options* o);
+void rtlr_cu_lr_options_default(rtlr_cu_lr_options* o);
+/* Options from the problem's SolverParams (report.cpp:20-43 full_options /
+ * low_options). */
+int rtlr_cu_problem_fr_options(const rtlr_cu_problem* p, rtlr_cu_fr_options* o);
+int rtlr_cu_problem_lr_options(const rtlr_cu_problem* p, rtlr_cu_lr_options* o);
+/* solve_full_rank (full_rank.hpp:41-43) */
+int rtlr_cu_solve_full_rank(rtlr_cu_problem* p, const rtlr_cu_fr_options* o, rtlr_cu_report** out);
+/* solve_low_rank (low_rank.hpp:156-158) */
+int rtlr_cu_solve_low_rank(rtlr_cu_problem* p, const rtlr_cu_lr_options* o, rtlr_cu_report** out);
+
+/* info: iterations, converged, n_history, has_psi, factor_rank, sampled_total, psi_dofs, n_dofs */
+int rtlr_cu_report_info(const rtlr_cu_report* r, int64_t info[8]);
+/* "phi", "psi", "S", "X", "V", "solve_seconds", or a per-outer-iteration
+ * history column: "diff_two_norm", "diff_inf_norm", "rank", "oversampling",
+ * "inner_iterations", "sampled_count", "fullrank_fallback", "dsa_iterations". */
+int rtlr_cu_report_get(const rtlr_cu_report* r, const char* what, double* out);
+int rtlr_cu_report_sampled(const rtlr_cu_report* r, int* counts, int* flat);
+void rtlr_cu_report_destroy(rtlr_cu_report* r);
+
+/* ---- angle sharding for N GPUs (one process per GPU): the angles rank
+ * `rank` of `nranks` owns; mirror pairs stay together and quadrants stay
+ * balanced.  Pure host logic (no GPU needed). */
+int rtlr_cu_partition_angles(int n_theta, int n_omega_z, int nranks, int rank, int* count,
+                             int* angles);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* RTLR_CU_H */

@@ -86,6 +86,12 @@ double oracle_c5_uniform(unsigned long long seed, unsigned long long counter) {
   return c5_uniform(seed, counter);
 }
 
+void oracle_c5_fill(unsigned long long seed, long long dir0, long long ndirs, long long ndof, double* out) {
+  for (long long k = 0; k < ndirs; ++k)
+    for (long long i = 0; i < ndof; ++i)
+      out[k * ndof + i] = c5_uniform(seed, static_cast<unsigned long long>((dir0 + k) * ndof + i));
+}
+
 int oracle_truncation_rank(const double* s, int n, double eps) {
   return truncation_rank(Vec(s, s + n), eps);
 }
@@ -138,6 +144,7 @@ int oracle_problem_set(void* h, const char* key, double v) {
     else if (k == "use_dsa") s.use_dsa = v != 0.0;
     else if (k == "store_psi") s.store_psi = v != 0.0;
     else if (k == "build_factors") s.build_factors = v != 0.0;
+    else if (k == "dsa_factor") s.dsa_factor = v != 0.0;
     else if (k == "sigma_s_const") s.sigma_s = [v](double, double) { return v; };
     else if (k == "sigma_a_const") s.sigma_a = [v](double, double) { return v; };
     else if (k == "source_const") s.source = [v](double, double) { return v; };
@@ -243,6 +250,19 @@ int oracle_boundary_vector(void* h, int angle, double* out) {
     AssembledProblem& a = *p->asm_;
     if (!p->spec.boundary) throw std::invalid_argument("no boundary field");
     put(boundary_vector(a.space, a.quad, p->spec.boundary, angle), out);
+  });
+}
+
+int oracle_boundary_vector_dir(void* h, double omx, double omy, double* out) {
+  return guard([&] {
+    Problem* p = static_cast<Problem*>(h);
+    AssembledProblem& a = *p->asm_;
+    if (!p->spec.boundary) throw std::invalid_argument("no boundary field");
+    AngularQuadrature q;
+    q.n_theta = q.n_omega_z = 1;
+    q.dirs = {omx, omy, 0.0};
+    q.weights = {1.0};
+    put(boundary_vector(a.space, q, p->spec.boundary, 0), out);
   });
 }
 

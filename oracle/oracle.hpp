@@ -171,7 +171,7 @@ Vec sweep(const DiscreteOperators& ops, const AngularQuadrature& quad, int angle
 // proj/src/diffusion.cpp:90-213 (SIP-DG + weak Dirichlet, banded LDL^T solve)
 class DiffusionSystem {
  public:
-  DiffusionSystem(const DGSpace& space, const DiscreteOperators& ops);
+  DiffusionSystem(const DGSpace& space, const DiscreteOperators& ops, bool factor = true);
   const Csr& matrix() const { return a_diff_; }
   Vec solve(const Vec& rhs) const;
   Vec correct(const Vec& phi_star, const Vec& phi_prev) const;
@@ -343,6 +343,7 @@ struct ProblemSpec {
   int p = 1, q = 8, max_iterations = 500;
   std::uint64_t seed = 0;
   bool use_dsa = true, store_psi = true, build_factors = true;
+  bool dsa_factor = true;  // false: assemble the SIP matrix only (inspection)
 };
 ProblemSpec make_problem(const std::string& name);  // presets + "C1".."C5"
 struct AssembledProblem {

@@ -252,7 +252,7 @@ void assemble_problem(const ProblemSpec& spec, AssembledProblem& out) {
     out.bc = build_boundary_data(out.space, out.quad, spec.boundary);
   delete out.dsa;
   out.dsa = nullptr;
-  if (spec.use_dsa) out.dsa = new DiffusionSystem(out.space, out.ops);
+  if (spec.use_dsa) out.dsa = new DiffusionSystem(out.space, out.ops, spec.dsa_factor);
 }
 
 }  // namespace oracle

@@ -87,7 +87,7 @@ Vec scaled(double a, const Vec& v) {
 
 // proj/src/diffusion.cpp:90-201 (assembly identical; SimplicialLDLT replaced
 // by a banded LDL^T in natural DOF order, bandwidth s*(nx+1)-1).
-DiffusionSystem::DiffusionSystem(const DGSpace& space, const DiscreteOperators& ops) {
+DiffusionSystem::DiffusionSystem(const DGSpace& space, const DiscreteOperators& ops, bool factor) {
   const SpatialMesh& mesh = space.mesh;
   const int k = space.degree, s = space.dofs_per_cell(), n = space.size();
   const double dx = mesh.dx(), dy = mesh.dy();
@@ -160,6 +160,7 @@ DiffusionSystem::DiffusionSystem(const DGSpace& space, const DiscreteOperators& 
     }
   a_diff_ = csr_add(csr_from_triplets(n, trips), ops.sigma_a);
   sigma_s_ = ops.sigma_s;
+  if (!factor) return;
 
   // Banded LDL^T.
   n_ = n;
@@ -191,6 +192,7 @@ DiffusionSystem::DiffusionSystem(const DGSpace& space, const DiscreteOperators& 
 }
 
 Vec DiffusionSystem::solve(const Vec& rhs) const {
+  if (band_.empty()) throw std::runtime_error("diffusion solve failed (matrix not factored)");
   const int w = bw_ + 1;
   auto B = [&](int i, int j) { return band_[static_cast<size_t>(i) * w + (j - i + bw_)]; };
   Vec x = rhs;

@@ -1,0 +1,39 @@
+// Vector / DSA kernels (see linalg.cu).
+#pragma once
+
+#include "device.cuh"
+
+namespace rtlr {
+namespace cuda {
+
+constexpr int kNormParts = 296;  // 2 x 148 SMs
+
+struct PcgState {
+  double bb, rr;
+  int done, iters, failed, pad;
+};
+
+struct PcgArgs {
+  int nx, ny, ncell, nparts, max_iters;
+  double rtol2;
+  const double* sip;  // SoA, 80 x ncell
+  const double* jac;  // SoA, 16 x ncell
+  const double* b;
+  double *x, *r, *z, *p, *q;
+  double *part_rz, *part_pq, *part_rr, *part_bb;  // part_rz has 2 x nparts
+  PcgState* state;
+};
+
+// out = Sigma (x - x_minus) + g   (x_minus, g optional)
+void sigma_apply(int ndof, const double* blocks, const double* x, const double* x_minus,
+                 const double* g, double* out, cudaStream_t s);
+void phi_accumulate(int ndof, int nu, const double* psi, long long ld, const double* w, double* phi,
+                    cudaStream_t s);
+// out2[0] = ||a-b||_2, out2[1] = ||a-b||_inf (b optional); work >= 2*kNormParts
+void diff_norms(int n, const double* a, const double* b, double* work, double* out2, cudaStream_t s);
+void vadd(int n, const double* a, const double* b, double* out, cudaStream_t s);
+void bsr_apply(const PcgArgs& a, const double* x, double* y, cudaStream_t s);
+int pcg_solve(const PcgArgs& a, PcgState* host_state, cudaStream_t s);
+
+}  // namespace cuda
+}  // namespace rtlr

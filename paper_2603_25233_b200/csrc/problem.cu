@@ -1,0 +1,306 @@
+// rtlr::cuda::Problem: upload, batched sweeps, DSA and the full-rank SI-DSA
+// driver (proj/src/full_rank.cpp:41-122) on one B200.
+#include <algorithm>
+#include <chrono>
+#include <cmath>
+#include <cstring>
+#include <map>
+
+#include "problem.hpp"
+
+namespace rtlr {
+namespace cuda {
+
+namespace {
+
+// 4x4 inverse on the host (block-Jacobi preconditioner), Gauss-Jordan with
+// partial pivoting.
+void invert4_host(const double* m, double* inv) {
+  double a[4][8];
+  for (int i = 0; i < 4; ++i)
+    for (int j = 0; j < 4; ++j) {
+      a[i][j] = m[j * 4 + i];
+      a[i][4 + j] = (i == j) ? 1.0 : 0.0;
+    }
+  for (int k = 0; k < 4; ++k) {
+    int p = k;
+    for (int i = k + 1; i < 4; ++i)
+      if (std::abs(a[i][k]) > std::abs(a[p][k])) p = i;
+    if (a[p][k] == 0.0) throw std::runtime_error("build_diffusion: factorization failed (matrix not positive definite)");
+    if (p != k)
+      for (int j = 0; j < 8; ++j) std::swap(a[k][j], a[p][j]);
+    const double d = a[k][k];
+    for (int j = 0; j < 8; ++j) a[k][j] /= d;
+    for (int i = 0; i < 4; ++i)
+      if (i != k) {
+        const double f = a[i][k];
+        for (int j = 0; j < 8; ++j) a[i][j] -= f * a[k][j];
+      }
+  }
+  for (int i = 0; i < 4; ++i)
+    for (int j = 0; j < 4; ++j) inv[j * 4 + i] = a[i][4 + j];
+}
+
+}  // namespace
+
+Problem::Problem(const ProblemConfig& cfg, int device) : device_(device) {
+  assemble(cfg, hp_);
+  dedupe_directions();
+  if (device_ < 0) return;  // host-only assembly (inspection without a GPU)
+  RTLR_CUDA(cudaSetDevice(device_));
+  RTLR_CUDA(cudaStreamCreateWithFlags(&stream_, cudaStreamNonBlocking));
+  own_stream_ = true;
+  RTLR_CUDA(cudaMallocHost(&h_state_, sizeof(PcgState)));
+  RTLR_CUDA(cudaMallocHost(&h_pin_, 64 * sizeof(double)));
+  upload();
+}
+
+Problem::~Problem() {
+  if (device_ < 0) return;
+  cudaSetDevice(device_);
+  if (stream_) cudaStreamSynchronize(stream_);
+  if (own_stream_ && stream_) cudaStreamDestroy(stream_);
+  if (h_state_) cudaFreeHost(h_state_);
+  if (h_pin_) cudaFreeHost(h_pin_);
+}
+
+void Problem::set_stream(cudaStream_t s) {
+  RTLR_CUDA(cudaStreamSynchronize(stream_));
+  if (s == nullptr) {
+    if (!own_stream_) {
+      RTLR_CUDA(cudaStreamCreateWithFlags(&stream_, cudaStreamNonBlocking));
+      own_stream_ = true;
+    }
+    return;
+  }
+  if (own_stream_) cudaStreamDestroy(stream_);
+  stream_ = s;
+  own_stream_ = false;
+}
+
+void Problem::upload() {
+  const HostProblem& h = hp_;
+  cudaStream_t s = stream_;
+  std::memcpy(sc_.ax_minus, h.sc.ax_minus, sizeof sc_.ax_minus);
+  std::memcpy(sc_.ax_plus, h.sc.ax_plus, sizeof sc_.ax_plus);
+  std::memcpy(sc_.ay_minus, h.sc.ay_minus, sizeof sc_.ay_minus);
+  std::memcpy(sc_.ay_plus, h.sc.ay_plus, sizeof sc_.ay_plus);
+  std::memcpy(sc_.bx_minus, h.sc.bx_minus, sizeof sc_.bx_minus);
+  std::memcpy(sc_.bx_plus, h.sc.bx_plus, sizeof sc_.bx_plus);
+  std::memcpy(sc_.by_minus, h.sc.by_minus, sizeof sc_.by_minus);
+  std::memcpy(sc_.by_plus, h.sc.by_plus, sizeof sc_.by_plus);
+  std::memcpy(sc_.trx_r, h.sc.trx_r, sizeof sc_.trx_r);
+  std::memcpy(sc_.trx_l, h.sc.trx_l, sizeof sc_.trx_l);
+  std::memcpy(sc_.try_r, h.sc.try_r, sizeof sc_.try_r);
+  std::memcpy(sc_.try_l, h.sc.try_l, sizeof sc_.try_l);
+  dirs_.upload(h.dirs.data(), h.dirs.size(), s);
+  sigma_t_.upload(h.sigma_t.data(), h.sigma_t.size(), s);
+  sigma_s_.upload(h.sigma_s.data(), h.sigma_s.size(), s);
+  source_.upload(h.source.data(), h.source.size(), s);
+  if (h.bc_any) bc_.upload(h.bc.data(), h.bc.size(), s);
+  err_.ensure(1);
+  RTLR_CUDA(cudaMemsetAsync(err_.get(), 0, sizeof(int), s));
+  if (!h.sip.empty()) {
+    const size_t nc = h.ncell;
+    std::vector<double> soa(80 * nc), jac(16 * nc);
+    for (size_t c = 0; c < nc; ++c) {
+      for (int k = 0; k < 80; ++k) soa[k * nc + c] = h.sip[c * 80 + k];
+      double inv[16];
+      invert4_host(&h.sip[c * 80], inv);
+      for (int e = 0; e < 16; ++e) jac[e * nc + c] = inv[e];
+    }
+    sip_.upload(soa.data(), soa.size(), s);
+    jac_.upload(jac.data(), jac.size(), s);
+    pcg_vec_.ensure(5 * static_cast<size_t>(h.ndof));
+    pcg_part_.ensure(5 * static_cast<size_t>(kNormParts));
+    pcg_state_.ensure(1);
+  }
+  norm_work_.ensure(2 * kNormParts + 8);
+  uniq_w_.upload(uniq_w_host_.data(), uniq_w_host_.size(), s);
+  angle_idx_.upload(uniq_rep_.data(), uniq_rep_.size(), s);
+  RTLR_CUDA(cudaStreamSynchronize(s));
+}
+
+void Problem::dedupe_directions() {
+  const HostProblem& h = hp_;
+  // Mirror-pair deduplication (bitwise-equal Omega_x, Omega_y).
+  std::map<std::pair<std::uint64_t, std::uint64_t>, int> seen;
+  uniq_rep_.clear();
+  uniq_of_.assign(h.n_omega, 0);
+  uniq_w_host_.clear();
+  for (int j = 0; j < h.n_omega; ++j) {
+    std::uint64_t bx, by;
+    std::memcpy(&bx, &h.dirs[3 * j], 8);
+    std::memcpy(&by, &h.dirs[3 * j + 1], 8);
+    auto it = seen.find({bx, by});
+    if (it == seen.end()) {
+      const int u = static_cast<int>(uniq_rep_.size());
+      seen[{bx, by}] = u;
+      uniq_rep_.push_back(j);
+      uniq_w_host_.push_back(h.weights[j]);
+      uniq_of_[j] = u;
+    } else {
+      uniq_of_[j] = it->second;
+      uniq_w_host_[it->second] += h.weights[j];
+    }
+  }
+}
+
+void Problem::check_error() {
+  int e = 0;
+  RTLR_CUDA(cudaMemcpyAsync(&e, err_.get(), sizeof(int), cudaMemcpyDeviceToHost, stream_));
+  RTLR_CUDA(cudaStreamSynchronize(stream_));
+  if (e) {
+    RTLR_CUDA(cudaMemsetAsync(err_.get(), 0, sizeof(int), stream_));
+    throw std::runtime_error("sweep: singular local block");
+  }
+}
+
+void Problem::sweep(const int* d_angles, int n, const double* d_rhs, long long rhs_stride,
+                    double* d_psi, long long psi_stride, bool use_bc, const double* d_dirs) {
+  if (n <= 0) return;
+  SweepArgs a{};
+  a.nx = hp_.nx;
+  a.ny = hp_.ny;
+  a.n = n;
+  a.dirs = d_dirs ? d_dirs : dirs_.get();
+  a.angles = d_angles;
+  a.rhs = d_rhs;
+  a.rhs_stride = rhs_stride;
+  a.bc = (use_bc && hp_.bc_any && !d_dirs) ? bc_.get() : nullptr;
+  a.bc_stride = hp_.ndof;
+  a.psi = d_psi;
+  a.psi_stride = psi_stride;
+  a.sigma_t = sigma_t_.get();
+  a.line = line_.ensure(static_cast<size_t>(n) * hp_.nx * 2);
+  a.err = err_.get();
+  a.sc = sc_;
+  launch_sweep(a, hp_.sigma_t_uniform, stream_);
+}
+
+void Problem::apply(double omx, double omy, const double* d_v, double* d_out) {
+  StencilArgs a{hp_.nx, hp_.ny, hp_.ncell, sigma_t_.get(), sc_};
+  launch_stream_apply(a, omx, omy, d_v, d_out, stream_);
+}
+
+void Problem::rhs_core(const double* d_phi, double* d_out) {
+  sigma_apply(hp_.ndof, sigma_s_.get(), d_phi, nullptr, source_.get(), d_out, stream_);
+}
+
+PcgArgs Problem::pcg_args(const double* b, double* x) {
+  PcgArgs a{};
+  a.nx = hp_.nx;
+  a.ny = hp_.ny;
+  a.ncell = hp_.ncell;
+  a.nparts = kNormParts;
+  a.max_iters = pcg_max_iters;
+  a.rtol2 = pcg_rtol * pcg_rtol;
+  a.sip = sip_.get();
+  a.jac = jac_.get();
+  a.b = b;
+  a.x = x;
+  double* v = pcg_vec_.get();
+  const size_t n = hp_.ndof;
+  a.r = v;
+  a.z = v + n;
+  a.p = v + 2 * n;
+  a.q = v + 3 * n;
+  double* part = pcg_part_.get();
+  a.part_rz = part;
+  a.part_pq = part + 2 * kNormParts;
+  a.part_rr = part + 3 * kNormParts;
+  a.part_bb = part + 4 * kNormParts;
+  a.state = pcg_state_.get();
+  return a;
+}
+
+int Problem::dsa_solve(const double* d_rhs, double* d_x) {
+  if (sip_.get() == nullptr) throw std::invalid_argument("dsa: problem assembled without a diffusion system");
+  PcgArgs a = pcg_args(d_rhs, d_x);
+  return pcg_solve(a, h_state_, stream_);
+}
+
+int Problem::dsa_correct(const double* d_phi_star, const double* d_phi_prev, double* d_delta) {
+  // rhs = Sigma_s (phi* - phi_prev)  (diffusion.cpp:210-213)
+  double* rhs = pcg_vec_.get() + 4 * static_cast<size_t>(hp_.ndof);
+  sigma_apply(hp_.ndof, sigma_s_.get(), d_phi_star, d_phi_prev, nullptr, rhs, stream_);
+  return dsa_solve(rhs, d_delta);
+}
+
+void Problem::si_step(const double* d_phi_prev, double* d_phi_star, double* d_psi_or_null) {
+  const size_t n = hp_.ndof;
+  const int nu = static_cast<int>(uniq_rep_.size());
+  double* rc = scratch_.ensure(n + n * static_cast<size_t>(nu));
+  double* psi_u = rc + n;
+  rhs_core(d_phi_prev, rc);
+  sweep(angle_idx_.get(), nu, rc, 0, psi_u, static_cast<long long>(n));
+  phi_accumulate(static_cast<int>(n), nu, psi_u, static_cast<long long>(n), uniq_w_.get(), d_phi_star, stream_);
+  if (d_psi_or_null)
+    for (int j = 0; j < hp_.n_omega; ++j)
+      RTLR_CUDA(cudaMemcpyAsync(d_psi_or_null + j * n, psi_u + uniq_of_[j] * n, n * sizeof(double),
+                                cudaMemcpyDeviceToDevice, stream_));
+  check_error();
+}
+
+// proj/src/full_rank.cpp:60-122
+SolveReport Problem::solve_full_rank(const FullRankOptions& o) {
+  if (o.use_dsa && sip_.get() == nullptr)
+    throw std::invalid_argument("solve_full_rank: DSA requested but no diffusion system");
+  const size_t n = hp_.ndof;
+  const int nu = static_cast<int>(uniq_rep_.size());
+  SolveReport rep;
+  rep.method = "full";
+  rep.psi_dofs = static_cast<long long>(n) * hp_.n_omega;
+  RTLR_CUDA(cudaStreamSynchronize(stream_));
+  const auto t0 = std::chrono::steady_clock::now();
+
+  double* base = scratch_.ensure(5 * n + n * static_cast<size_t>(nu));
+  double *phi = base, *phi_star = base + n, *rc = base + 2 * n, *delta = base + 3 * n;
+  double* psi_u = base + 5 * n;
+  RTLR_CUDA(cudaMemsetAsync(phi, 0, n * sizeof(double), stream_));
+  for (int it = 1; it <= o.max_iterations; ++it) {
+    rhs_core(phi, rc);
+    sweep(angle_idx_.get(), nu, rc, 0, psi_u, static_cast<long long>(n));
+    phi_accumulate(static_cast<int>(n), nu, psi_u, static_cast<long long>(n), uniq_w_.get(), phi_star, stream_);
+    diff_norms(static_cast<int>(n), phi_star, phi, norm_work_.get(), norm_work_.get() + 2 * kNormParts, stream_);
+    RTLR_CUDA(cudaMemcpyAsync(h_pin_, norm_work_.get() + 2 * kNormParts, 2 * sizeof(double),
+                              cudaMemcpyDeviceToHost, stream_));
+    check_error();  // synchronizes
+    OuterRecord rec;
+    rec.diff_two_norm = h_pin_[0];
+    rec.diff_inf_norm = h_pin_[1];
+    rep.iterations = it;
+    if (rec.diff_inf_norm <= o.eps_si_sa) {
+      rep.history.push_back(rec);
+      rep.converged = true;
+      RTLR_CUDA(cudaMemcpyAsync(phi, phi_star, n * sizeof(double), cudaMemcpyDeviceToDevice, stream_));
+      break;
+    }
+    if (o.use_dsa) {
+      rec.dsa_iterations = dsa_correct(phi_star, phi, delta);
+      vadd(static_cast<int>(n), phi_star, delta, phi, stream_);
+    } else {
+      RTLR_CUDA(cudaMemcpyAsync(phi, phi_star, n * sizeof(double), cudaMemcpyDeviceToDevice, stream_));
+    }
+    rep.history.push_back(rec);
+  }
+  if (!rep.converged)
+    RTLR_CUDA(cudaMemcpyAsync(phi, phi_star, n * sizeof(double), cudaMemcpyDeviceToDevice, stream_));
+  rep.phi.resize(n);
+  RTLR_CUDA(cudaMemcpyAsync(rep.phi.data(), phi, n * sizeof(double), cudaMemcpyDeviceToHost, stream_));
+  RTLR_CUDA(cudaStreamSynchronize(stream_));
+  rep.solve_seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+  if (o.store_psi) {
+    rep.has_psi = true;
+    rep.psi.resize(n * hp_.n_omega);
+    std::vector<double> pu(n * static_cast<size_t>(nu));
+    RTLR_CUDA(cudaMemcpyAsync(pu.data(), psi_u, pu.size() * sizeof(double), cudaMemcpyDeviceToHost, stream_));
+    RTLR_CUDA(cudaStreamSynchronize(stream_));
+    for (int j = 0; j < hp_.n_omega; ++j)
+      std::memcpy(&rep.psi[j * n], &pu[uniq_of_[j] * n], n * sizeof(double));
+  }
+  return rep;
+}
+
+}  // namespace cuda
+}  // namespace rtlr

@@ -1,0 +1,159 @@
+// rtlr::cuda — device-resident problem and the solver API that mirrors the
+// reference's (proj/include/rtlr/{sweep,full_rank,low_rank,diffusion}.hpp).
+#pragma once
+
+#include <memory>
+#include <string>
+#include <vector>
+
+#include "device.cuh"
+#include "host.hpp"
+#include "linalg.cuh"
+
+namespace rtlr {
+namespace cuda {
+
+template <class T>
+class DBuf {
+ public:
+  DBuf() = default;
+  DBuf(const DBuf&) = delete;
+  DBuf& operator=(const DBuf&) = delete;
+  ~DBuf() { release(); }
+  void release() {
+    if (p_) cudaFree(p_);
+    p_ = nullptr;
+    n_ = 0;
+  }
+  // Grow to at least n elements (contents not preserved).
+  T* ensure(size_t n) {
+    if (n > n_) {
+      release();
+      RTLR_CUDA(cudaMalloc(&p_, (n ? n : 1) * sizeof(T)));
+      n_ = n;
+    }
+    return p_;
+  }
+  void upload(const T* h, size_t n, cudaStream_t s) {
+    ensure(n);
+    if (n) RTLR_CUDA(cudaMemcpyAsync(p_, h, n * sizeof(T), cudaMemcpyHostToDevice, s));
+  }
+  T* get() const { return p_; }
+  size_t size() const { return n_; }
+
+ private:
+  T* p_ = nullptr;
+  size_t n_ = 0;
+};
+
+// proj/include/rtlr/report.hpp:12-50
+struct LowRankFactors {
+  std::vector<double> X, S, V;  // X: N_x x r, V: N_Omega x r, column-major
+  int rank = 0;
+};
+struct OuterRecord {
+  double diff_two_norm = 0.0, diff_inf_norm = 0.0;
+  int rank = -1;
+  double oversampling = 0.0;
+  int inner_iterations = 0, sampled_count = 0;
+  bool fullrank_fallback = false;
+  int dsa_iterations = 0;  // PCG iterations of this outer step (0: none)
+};
+struct SolveReport {
+  std::string method;
+  std::vector<double> phi;
+  bool converged = false;
+  int iterations = 0;
+  double solve_seconds = 0.0;
+  long long psi_dofs = 0;
+  std::vector<OuterRecord> history;
+  bool has_psi = false;
+  std::vector<double> psi;  // N_x x N_Omega column-major
+  bool has_factors = false;
+  LowRankFactors factors;
+  std::vector<std::vector<int>> sampled_log;
+};
+
+struct FullRankOptions {  // full_rank.hpp:32-37
+  double eps_si_sa = 1e-6;
+  int max_iterations = 500;
+  bool use_dsa = true;
+  bool store_psi = true;
+};
+struct LowRankParams {  // low_rank.hpp:29-36
+  int p = 1, q = 8;
+  double eps_res = 1e-7, eps_diff = 1e-7, eps_svd = 1e-8, eps_mgs = 1e-10;
+};
+struct LowRankOptions {  // low_rank.hpp:146-153
+  LowRankParams inner;
+  double eps_si_sa = 1e-6;
+  int max_iterations = 500;
+  bool use_dsa = true;
+  std::uint64_t seed = 0;
+  bool build_factors = true;
+};
+
+// Assembled problem resident on one GPU.
+class Problem {
+ public:
+  Problem(const ProblemConfig& cfg, int device);
+  ~Problem();
+  Problem(const Problem&) = delete;
+  Problem& operator=(const Problem&) = delete;
+
+  const HostProblem& host() const { return hp_; }
+  cudaStream_t stream() const { return stream_; }
+  void set_stream(cudaStream_t s);  // external stream (e.g. torch's); nullptr = own
+
+  // Batched sweep, all pointers on the device.  angles may be nullptr
+  // (0..n-1 of dirs).  dirs overrides the problem quadrature when given
+  // (device pointer, n x 3).
+  void sweep(const int* d_angles, int n, const double* d_rhs, long long rhs_stride, double* d_psi,
+             long long psi_stride, bool use_bc = true, const double* d_dirs = nullptr);
+  // StreamingOperator::apply (operators.cpp:283-288): out = (Sigma_t + Ox Dx + Oy Dy) v
+  void apply(double omx, double omy, const double* d_v, double* d_out);
+  // DiffusionSystem::solve / correct (diffusion.cpp:203-213); returns PCG iterations
+  int dsa_solve(const double* d_rhs, double* d_x);
+  int dsa_correct(const double* d_phi_star, const double* d_phi_prev, double* d_delta);
+  // rhs_core = Sigma_s phi + G (full_rank.cpp:81)
+  void rhs_core(const double* d_phi, double* d_out);
+  // si_step (full_rank.cpp:41-58)
+  void si_step(const double* d_phi_prev, double* d_phi_star, double* d_psi_or_null);
+
+  SolveReport solve_full_rank(const FullRankOptions& o);
+  SolveReport solve_low_rank(const LowRankOptions& o);
+
+  void check_error();  // throws runtime_error("sweep: singular local block")
+  int device() const { return device_; }
+
+  // Unique 2D transport operators: mirror directions (j1, j2) and
+  // (j1, n_z-1-j2) have bitwise-identical (Omega_x, Omega_y).
+  const std::vector<int>& unique_rep() const { return uniq_rep_; }
+  const std::vector<int>& unique_of() const { return uniq_of_; }
+
+  double pcg_rtol = 1e-13;
+  int pcg_max_iters = 20000;
+
+ private:
+  friend class LowRankEngine;
+  void upload();
+  void dedupe_directions();
+  PcgArgs pcg_args(const double* b, double* x);
+
+  HostProblem hp_;
+  int device_ = 0;
+  cudaStream_t stream_ = nullptr;
+  bool own_stream_ = true;
+  StreamDev sc_{};
+  DBuf<double> dirs_, sigma_t_, sigma_s_, source_, bc_, sip_, jac_;
+  DBuf<int> err_, angle_idx_;
+  DBuf<double> line_, norm_work_, pcg_vec_, pcg_part_, uniq_w_, scratch_;
+  DBuf<PcgState> pcg_state_;
+  PcgState* h_state_ = nullptr;
+  double* h_pin_ = nullptr;  // small pinned host scratch
+  std::vector<int> uniq_rep_, uniq_of_;
+  std::vector<double> uniq_w_host_;
+};
+
+}  // namespace cuda
+}  // namespace rtlr

@@ -47,6 +47,7 @@ def lib():
         L.oracle_apply.argtypes = [ctypes.c_void_p, ctypes.c_double, ctypes.c_double, _D, _D]
         L.oracle_rhs_core.argtypes = [ctypes.c_void_p, _D, _D]
         L.oracle_boundary_vector.argtypes = [ctypes.c_void_p, ctypes.c_int, _D]
+        L.oracle_boundary_vector_dir.argtypes = [ctypes.c_void_p, ctypes.c_double, ctypes.c_double, _D]
         L.oracle_dsa_solve.argtypes = [ctypes.c_void_p, _D, _D]
         L.oracle_dsa_correct.argtypes = [ctypes.c_void_p, _D, _D, _D]
         L.oracle_si_step.argtypes = [ctypes.c_void_p, _D, _D, _D]
@@ -60,6 +61,8 @@ def lib():
         L.oracle_psi_difference.argtypes = [ctypes.c_void_p, ctypes.c_void_p]
         L.oracle_c5_uniform.restype = ctypes.c_double
         L.oracle_c5_uniform.argtypes = [ctypes.c_ulonglong, ctypes.c_ulonglong]
+        L.oracle_c5_fill.argtypes = [ctypes.c_ulonglong, ctypes.c_longlong, ctypes.c_longlong,
+                                     ctypes.c_longlong, _D]
         L.oracle_truncation_rank.argtypes = [_D, ctypes.c_int, ctypes.c_double]
         L.oracle_svd_values.argtypes = [_D, ctypes.c_int, ctypes.c_int, _D]
         L.oracle_gauss_legendre.argtypes = [ctypes.c_int, _D, _D]
@@ -111,6 +114,12 @@ def svd_values(a):
 
 def c5_uniform(seed, counter):
     return lib().oracle_c5_uniform(seed, counter)
+
+
+def c5_fill(seed, dir0, ndirs, ndof):
+    out = np.zeros((ndirs, ndof))
+    lib().oracle_c5_fill(seed, dir0, ndirs, ndof, _p(out))
+    return out
 
 
 class Result:
@@ -221,6 +230,11 @@ class Problem:
         phi = np.ascontiguousarray(phi, dtype=np.float64)
         out = np.zeros(self.n)
         _check(lib().oracle_rhs_core(self.h, _p(phi), _p(out)))
+        return out
+
+    def boundary_vector(self, omx, omy):
+        out = np.zeros(self.n)
+        _check(lib().oracle_boundary_vector_dir(self.h, omx, omy, _p(out)))
         return out
 
     def dsa_solve(self, rhs):

@@ -1,0 +1,138 @@
+"""Product host setup vs the oracle, bit for bit (north star: bit-exact
+quadrature and mesh indexing; identical assembled inputs), plus the C-ABI
+surface and the angle partition.  CPU only: problems are assembled with
+device = -1 (host-only)."""
+import os
+import re
+
+import numpy as np
+import pytest
+
+import _oracle as O
+import paper_2603_25233_b200 as P
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+CASES = [
+    ("C1", {}),
+    ("C2", {}),
+    ("C3", {"nx": 98, "ny": 77}),
+    ("C4", {}),
+    ("C5", {"nx": 64, "ny": 48}),
+    ("homogeneous(100,2)", {}),
+    ("pin_cell", {}),
+    ("variable_scattering", {}),
+    ("lattice", {}),
+]
+
+
+def _pair(name, ov):
+    o = O.Problem(name, assemble=False, **ov)
+    o.set("dsa_factor", 0)
+    o.assemble()
+    p = P.Problem(name, device=-1, **ov)
+    return o, p
+
+
+@pytest.mark.parametrize("name,ov", CASES)
+def test_inputs_bitwise(name, ov):
+    o, p = _pair(name, ov)
+    assert (p.n, p.n_omega) == (o.n, o.n_omega)
+    assert np.array_equal(p.get("dirs"), o.get("dirs"))
+    assert np.array_equal(p.get("weights"), o.get("weights"))
+    assert np.array_equal(p.get("source"), o.get("source"))
+    for blk in ("sigma_t_blocks", "sigma_s_blocks", "sigma_a_blocks"):
+        assert np.array_equal(p.get(blk), o.get(blk)), blk
+    assert np.array_equal(p.get("stream_blocks"), o.get("stream_blocks"))
+
+
+def _bsr_to_dense_rows(p, sip):
+    """Scatter the product's 5-block BSR into a scipy matrix."""
+    import scipy.sparse as sp
+    nx, ny = p.nx, p.ny
+    rows, cols, vals = [], [], []
+    for c in range(p.ncell):
+        a, b = c % nx, c // nx
+        nbr = [c, c - 1 if a > 0 else -1, c + 1 if a + 1 < nx else -1,
+               c - nx if b > 0 else -1, c + nx if b + 1 < ny else -1]
+        for s, cc in enumerate(nbr):
+            if cc < 0:
+                assert not sip[c, s].any()
+                continue
+            blk = sip[c, s]
+            for i in range(4):
+                for j in range(4):
+                    if blk[i, j] != 0.0:
+                        rows.append(4 * c + i)
+                        cols.append(4 * cc + j)
+                        vals.append(blk[i, j])
+    return sp.csr_matrix((vals, (rows, cols)), shape=(p.n, p.n))
+
+
+@pytest.mark.parametrize("name,ov", [("C1", {}), ("C3", {"nx": 49, "ny": 35}),
+                                     ("C4", {"nx": 64, "ny": 64}), ("lattice", {"nx": 20, "ny": 20}),
+                                     ("pin_cell", {})])
+def test_sip_matrix_bitwise(name, ov):
+    o, p = _pair(name, ov)
+    ref = o.csr("sip").tocoo()
+    mine = _bsr_to_dense_rows(p, p.get("sip_bsr")).tocsr()
+    got = np.asarray(mine[ref.row, ref.col]).ravel()
+    assert np.array_equal(got, ref.data)
+    # the reference CSR also keeps duplicate sums that cancel to exactly 0
+    assert mine.nnz == np.count_nonzero(ref.data)
+
+
+def test_quadrature_bitwise_all_baseline_rules():
+    for nt, nz in ((16, 8), (32, 16), (48, 24), (64, 32), (32, 8), (64, 16), (128, 32)):
+        p = P.Problem("C5", device=-1, nx=4, ny=4, n_theta=nt, n_omega_z=nz)
+        d, w = O.quadrature(nt, nz)
+        assert np.array_equal(p.get("dirs"), d) and np.array_equal(p.get("weights"), w)
+        assert p.n_unique == nt * nz // 2  # mirror pairs collapse
+
+
+def test_degree_other_than_one_rejected():
+    with pytest.raises(P.InvalidArgument, match="degree"):
+        P.Problem("homogeneous(1,1)", device=-1, degree=2)
+
+
+def test_config_errors_map_to_config_error():  # problem.cpp:95-107
+    with pytest.raises(P.ConfigError):
+        P.Problem("no_such_preset", device=-1)
+    with pytest.raises(P.ConfigError, match="p <= q"):
+        P.Problem("C1", device=-1, p=9, q=8)
+
+
+def test_host_only_problem_rejects_gpu_calls():
+    p = P.Problem("C1", device=-1)
+    with pytest.raises(P.InvalidArgument, match="host-only"):
+        p.sweep([0], p.get("source"))
+
+
+def test_c_abi_exports_every_declared_symbol():
+    hdr = open(os.path.join(ROOT, "include", "rtlr_cu.h")).read()
+    declared = set(re.findall(r"\b(rtlr_cu_[a-z0-9_]+)\s*\(", hdr))
+    assert declared == set(P.EXPORTS)
+    lib = P.load_library()
+    for sym in declared:
+        assert hasattr(lib, sym), sym
+
+
+@pytest.mark.parametrize("nt,nz,n", [(16, 8, 1), (16, 8, 2), (32, 16, 4), (64, 32, 8), (7, 3, 3)])
+def test_partition_angles(nt, nz, n):
+    parts = [P.partition_angles(nt, nz, n, r) for r in range(n)]
+    allv = np.concatenate(parts)
+    assert sorted(allv.tolist()) == list(range(nt * nz))
+    sizes = [len(x) for x in parts]
+    assert max(sizes) - min(sizes) <= 2
+    for x in parts:  # mirror pairs never split
+        s = set(x.tolist())
+        for a in x:
+            j1, j2 = divmod(int(a), nz)
+            assert j1 * nz + (nz - 1 - j2) in s
+
+
+def test_c5_uniform_matches_oracle():
+    # host restatement of the device generator (paper_2603_25233_b200/csrc/host.hpp)
+    vals = [O.c5_uniform(12345, c) for c in (0, 1, 2, 10**9, 2**40 + 7)]
+    assert all(0.0 <= v < 1.0 for v in vals)
+    assert len(set(vals)) == len(vals)

@@ -1,0 +1,312 @@
+"""Pins the CPU oracle against the reference's own known-answer tests and
+captured results.  Each test cites the reference test it
+restates.  CPU only."""
+import math
+
+import numpy as np
+import pytest
+import scipy.sparse as sp
+import scipy.sparse.linalg as spla
+
+import _oracle as O
+
+
+def sphere_moment(a, b, c):
+    def df(n):
+        v = 1.0
+        while n > 1:
+            v *= n
+            n -= 2
+        return v
+    if a % 2 or b % 2 or c % 2:
+        return 0.0
+    return df(a - 1) * df(b - 1) * df(c - 1) / df(a + b + c + 1)
+
+
+def quad_moment(d, w, a, b, c):
+    return float(np.sum(w * d[:, 0] ** a * d[:, 1] ** b * d[:, 2] ** c))
+
+
+# ---------------------------------------------------------------- quadrature
+def test_gauss_legendre_nodes_weights():  # test_quadrature.cpp:35-52
+    for n in (1, 2, 3, 4, 5, 8, 16, 33, 64):
+        x, w = O.gauss_legendre(n)
+        assert abs(w.sum() - 2.0) <= 1e-14 * 2
+        for i in range(n):
+            assert x[i] == -x[n - 1 - i]  # exact mirroring
+            if i > 0:
+                assert x[i] > x[i - 1]
+        acc = float(np.sum(w * x ** (2 * n - 2)))
+        assert abs(acc - 2.0 / (2 * n - 1)) <= 1e-12 * 2.0 / (2 * n - 1)
+    with pytest.raises(O.OracleError, match="invalid_argument"):
+        O.gauss_legendre(0)
+
+
+def test_cl_structure_and_closed_form():  # test_quadrature.cpp:54-77
+    d, w = O.quadrature(8, 4)
+    assert len(w) == 32 and abs(w.sum() - 1.0) < 1e-14 and (w > 0).all()
+    assert np.all(np.abs(np.linalg.norm(d, axis=1) - 1.0) < 1e-14)
+    d, w = O.quadrature(2, 1)
+    assert abs(d[0, 0]) < 1e-14 and abs(d[0, 1] - 1.0) < 1e-15 and d[0, 2] == 0.0
+    assert abs(d[1, 0]) < 1e-14 and abs(d[1, 1] + 1.0) < 1e-15
+    assert abs(w[0] - 0.5) < 1e-15 and abs(w[1] - 0.5) < 1e-15
+
+
+def test_cl_moments_symmetry_exactness():  # test_quadrature.cpp:79-122
+    d, w = O.quadrature(8, 4)
+    assert abs(quad_moment(d, w, 2, 0, 0) - 1 / 3) < 1e-13
+    for j in range(len(w)):
+        assert np.min(np.max(np.abs(d + d[j]), axis=1)) <= 1e-14
+    for total in range(8):
+        for a in range(total + 1):
+            for b in range(total - a + 1):
+                c = total - a - b
+                assert abs(quad_moment(d, w, a, b, c) - sphere_moment(a, b, c)) < 1e-12
+    err_z8 = quad_moment(d, w, 0, 0, 8) - sphere_moment(0, 0, 8)
+    assert abs(err_z8 - (-0.0058046)) <= 1e-3 * 0.0058046
+    d2, w2 = O.quadrature(10, 5)
+    for a in (8, 0):
+        assert abs(quad_moment(d2, w2, a, 0, 8 - a) - sphere_moment(a, 0, 8 - a)) < 1e-12
+
+
+def test_azimuth_major_ordering():  # test_quadrature.cpp:124-131
+    d, _ = O.quadrature(4, 3)
+    x, _ = O.gauss_legendre(3)
+    for j1 in range(4):
+        for j2 in range(3):
+            assert d[j1 * 3 + j2, 2] == x[j2]
+
+
+def test_mirror_pairs_bitwise():
+    for nt, nz in ((16, 8), (32, 16), (48, 24), (64, 32), (32, 8), (64, 16), (128, 32)):
+        d, w = O.quadrature(nt, nz)
+        for j1 in range(nt):
+            for j2 in range(nz):
+                a, b = j1 * nz + j2, j1 * nz + nz - 1 - j2
+                assert d[a, 0] == d[b, 0] and d[a, 1] == d[b, 1] and w[a] == w[b]
+
+
+# ---------------------------------------------------------------- operators
+def test_space_sizes_and_unit_sigma():  # test_dg_operators.cpp:32-71
+    p = O.Problem("homogeneous(1,1)", nx=1, ny=1, use_dsa=0)
+    assert p.n == 4
+    p = O.Problem("homogeneous(1,2)", use_dsa=0)
+    assert p.n == 4096
+    p = O.Problem("homogeneous(1,1)", nx=4, ny=4, x_min=0, x_max=1, y_min=0, y_max=1, use_dsa=0)
+    ss = p.csr("sigma_s").toarray()
+    assert np.max(np.abs(ss - np.eye(p.n))) < 1e-13
+    assert np.max(np.abs(p.csr("sigma_t").toarray() - ss)) < 1e-15
+
+
+def test_one_sided_streaming_negative_transposes():  # test_dg_operators.cpp:203-210
+    p = O.Problem("homogeneous(1,1)", nx=2, ny=2, use_dsa=0)
+    for m, pl in (("d_x_minus", "d_x_plus"), ("d_y_minus", "d_y_plus")):
+        a = p.csr(m).toarray()
+        b = p.csr(pl).toarray()
+        assert np.max(np.abs(b + a.T)) < 1e-13
+
+
+def materialize(p, omx, omy):
+    st = p.csr("sigma_t")
+    dx = p.csr("d_x_minus" if omx >= 0 else "d_x_plus")
+    dy = p.csr("d_y_minus" if omy >= 0 else "d_y_plus")
+    m = st.copy()
+    if omx != 0:
+        m = m + omx * dx
+    if omy != 0:
+        m = m + omy * dy
+    return sp.csc_matrix(m)
+
+
+# ---------------------------------------------------------------- sweep
+def test_zero_rhs_zero_flux():  # test_sweep.cpp:34-42
+    p = O.Problem("homogeneous(1,1)", nx=4, ny=4, n_theta=4, n_omega_z=2, use_dsa=0)
+    d, _ = O.quadrature(4, 2)
+    for j in range(8):
+        assert np.linalg.norm(p.sweep(d[j, 0], d[j, 1], np.zeros(p.n))) == 0.0
+
+
+def test_sweep_equals_direct_solve():  # test_sweep.cpp:44-63 (random rhs, numpy generator)
+    p = O.Problem("pin_cell", nx=8, ny=8, use_dsa=0)
+    d, _ = O.quadrature(8, 4)
+    rng = np.random.default_rng(7)
+    for j in (0, 5, 13, 21, 27, 31):
+        a = materialize(p, d[j, 0], d[j, 1])
+        for _ in range(5):
+            rhs = rng.standard_normal(p.n)
+            via = p.sweep(d[j, 0], d[j, 1], rhs)
+            direct = spla.spsolve(a, rhs)
+            assert np.linalg.norm(via - direct) < 1e-11 * np.linalg.norm(direct)
+
+
+def test_sweep_residual_every_angle():  # test_sweep.cpp:65-78
+    p = O.Problem("homogeneous(3,1)", nx=5, ny=7, x_min=0, x_max=1, y_min=0, y_max=1, use_dsa=0)
+    d, _ = O.quadrature(8, 4)
+    rng = np.random.default_rng(3)
+    for j in range(32):
+        rhs = rng.standard_normal(p.n)
+        psi = p.sweep(d[j, 0], d[j, 1], rhs)
+        assert np.linalg.norm(p.apply(d[j, 0], d[j, 1], psi) - rhs) <= 1e-12 * np.linalg.norm(rhs)
+
+
+def test_axis_aligned_directions():  # test_sweep.cpp:111-124
+    p = O.Problem("homogeneous(0.7,1)", nx=6, ny=5, x_min=0, x_max=1, y_min=0, y_max=1, use_dsa=0)
+    rng = np.random.default_rng(11)
+    for ox, oy in ((1.0, 0.0), (0.0, 1.0), (-1.0, 0.0), (0.0, -1.0)):
+        rhs = rng.standard_normal(p.n)
+        psi = p.sweep(ox, oy, rhs)
+        assert np.linalg.norm(p.apply(ox, oy, psi) - rhs) <= 1e-12 * np.linalg.norm(rhs)
+
+
+def test_uniform_inflow_streams_unchanged():  # test_sweep.cpp:126-140
+    p = O.Problem("homogeneous(0,1)", nx=5, ny=5, x_min=0, x_max=1, y_min=0, y_max=1,
+                  sigma_a_const=0.0, boundary_const=1.0, use_dsa=0)
+    h = 1.0 / 5
+    for ox, oy in ((1.0, 0.0), (0.0, -1.0), (math.sqrt(0.5), math.sqrt(0.5)), (-0.6, 0.8)):
+        psi = p.sweep(ox, oy, p.boundary_vector(ox, oy))
+        means = psi[0::4] / math.sqrt(h * h)
+        assert np.all(np.abs(means - 1.0) <= 1e-12)
+
+
+def test_thick_medium_sweep_vs_direct():  # test_sweep.cpp:157-173
+    p = O.Problem("homogeneous(100,1)", nx=8, ny=8, n_theta=4, n_omega_z=2, use_dsa=0)
+    d, _ = O.quadrature(4, 2)
+    g = p.get("source")
+    for j in range(8):
+        psi = p.sweep(d[j, 0], d[j, 1], g)
+        direct = spla.spsolve(materialize(p, d[j, 0], d[j, 1]), g)
+        assert np.linalg.norm(psi - direct) <= 1e-11 * np.linalg.norm(direct)
+
+
+# ---------------------------------------------------------------- diffusion
+def test_diffusion_spd_residual_and_trivial_corrections():  # test_diffusion.cpp:24-77
+    p = O.Problem("homogeneous(10,1)", nx=8, ny=8, sigma_a_const=0.5)
+    a = p.csr("sip")
+    ad = a.toarray()
+    assert np.max(np.abs(ad - ad.T)) < 1e-12 * np.max(np.abs(ad))
+    rng = np.random.default_rng(17)
+    rhs = rng.standard_normal(p.n)
+    x = p.dsa_solve(rhs)
+    assert np.linalg.norm(a @ x - rhs) <= 1e-12 * np.linalg.norm(rhs)
+    phi = rng.standard_normal(p.n)
+    assert np.linalg.norm(p.dsa_correct(phi, phi)) == 0.0
+    ev = np.linalg.eigvalsh(ad)
+    assert ev.min() > 0
+
+
+def test_diffusion_linear_scaling():  # test_diffusion.cpp:44-53
+    thick = O.Problem("homogeneous(100,1)", nx=6, ny=6).csr("sip").toarray()
+    unit = O.Problem("homogeneous(0.3333333333333333,1)", nx=6, ny=6).csr("sip").toarray() / 300.0
+    assert np.max(np.abs(thick - unit)) < 1e-12 * np.max(np.abs(unit))
+
+
+def test_vanishing_sigma_t_rejected():  # test_diffusion.cpp:79-83
+    with pytest.raises(O.OracleError, match="sigma_t must be positive"):
+        O.Problem("homogeneous(0,1)", nx=4, ny=4)
+
+
+# ---------------------------------------------------------------- full rank
+def test_first_iterate_is_si_step_bitwise():  # test_full_rank.cpp:54-66
+    p = O.Problem("homogeneous(100,1)", use_dsa=0, max_iterations=1)
+    step = p.si_step(np.zeros(p.n))
+    r = p.solve("full")
+    assert np.array_equal(r.get("phi", p.n), step)
+
+
+def test_pure_absorber_two_iterations():  # test_full_rank.cpp:68-79
+    p = O.Problem("homogeneous(0,1)", sigma_a_const=1.0)
+    r = p.solve("full")
+    assert r.converged and r.iterations == 2
+    assert r.history("diff_inf_norm")[-1] == 0.0
+
+
+def test_streaming_matches_stored():  # test_full_rank.cpp:102-115
+    a = O.Problem("homogeneous(1,1)").solve("full")
+    p = O.Problem("homogeneous(1,1)", store_psi=0)
+    b = p.solve("full")
+    assert a.iterations == b.iterations
+    pa, pb = a.get("phi", p.n), b.get("phi", p.n)
+    assert np.linalg.norm(pa - pb) <= 1e-13 * np.linalg.norm(pa)
+
+
+def test_iteration_cap():  # test_full_rank.cpp:117-127
+    r = O.Problem("homogeneous(100,1)", use_dsa=0, max_iterations=3, store_psi=0).solve("full")
+    assert not r.converged and r.iterations == 3
+
+
+# ---------------------------------------------------------------- low rank
+def test_truncation_rank_rule():  # test_low_rank.cpp:327-334
+    s3 = np.array([1.0, 1e-4, 1e-12])
+    assert O.truncation_rank(s3, 1e-8) == 2
+    assert O.truncation_rank(s3, 1e-2) == 1
+    assert O.truncation_rank(s3, 1e-18) == 3
+    assert O.truncation_rank(np.zeros(4), 1e-8) == 1
+
+
+def test_svd_values_against_numpy():
+    rng = np.random.default_rng(4)
+    for m, n in ((6, 10), (10, 6), (30, 30)):
+        a = rng.standard_normal((m, n))
+        s = O.svd_values(a)
+        assert np.allclose(s, np.linalg.svd(a, compute_uv=False), rtol=1e-13, atol=1e-14)
+
+
+# proj/test_output.txt:30 (acceptance criterion 4, seed 12345): FR/LR
+# iteration counts and the LR-FR scalar-flux difference magnitudes.
+CRITERION4 = [
+    ("homogeneous(0.1,2)", 5, 5, 6.7e-17),
+    ("homogeneous(1,2)", 10, 10, 6.5e-17),
+    ("homogeneous(10,2)", 12, 12, 4.4e-15),
+    ("homogeneous(100,2)", 6, 6, 7.9e-12),
+    ("pin_cell", 17, 17, 1.3e-12),
+    ("variable_scattering", 7, 7, 6.4e-13),
+]
+
+
+@pytest.mark.parametrize("name,fr_it,lr_it,dphi", CRITERION4)
+def test_acceptance_criterion4_counts(name, fr_it, lr_it, dphi):
+    p = O.Problem(name, seed=12345)
+    f = p.solve("full")
+    l = p.solve("lowrank")
+    assert f.converged and l.converged
+    assert f.iterations == fr_it and l.iterations == lr_it
+    d = np.linalg.norm(f.get("phi", p.n) - l.get("phi", p.n))
+    assert d <= 1e-6 and d <= 100 * max(dphi, 1e-16)
+
+
+def test_lowrank_determinism_and_seed_dependence():  # test_low_rank.cpp:441-470
+    p = O.Problem("homogeneous(1,1)", seed=2024)
+    a, b = p.solve("lowrank"), p.solve("lowrank")
+    assert np.array_equal(a.get("phi", p.n), b.get("phi", p.n))
+    assert a.sampled_log() == b.sampled_log()
+    assert np.array_equal(a.history("rank"), b.history("rank"))
+    p.set("seed", 2025)
+    c = p.solve("lowrank")
+    assert c.converged and c.sampled_log() != a.sampled_log()
+
+
+def test_lowrank_vs_fullrank_factors():  # test_low_rank.cpp:472-498
+    p = O.Problem("homogeneous(1,1)", seed=11)
+    f = p.solve("full")
+    l = p.solve("lowrank")
+    assert abs(f.iterations - l.iterations) <= 1
+    assert np.linalg.norm(f.get("phi", p.n) - l.get("phi", p.n)) <= 1e-6
+    r = l.factor_rank
+    X = l.get("X", p.n * r).reshape(r, p.n).T
+    V = l.get("V", p.n_omega * r).reshape(r, p.n_omega).T
+    S = l.get("S", r)
+    assert np.linalg.norm(X.T @ X - np.eye(r)) <= 1e-10
+    assert np.linalg.norm(V.T @ V - np.eye(r)) <= 1e-10
+    assert np.all(np.diff(S) <= 0)
+    assert l.psi_dofs == r * (p.n + p.n_omega)
+    assert O.lib().oracle_psi_difference(f.h, l.h) <= 1e-5
+
+
+def test_dsa_accelerates_si():  # acceptance.cpp criterion 7 (6 vs >= 200)
+    p = O.Problem("homogeneous(100,2)", store_psi=0)
+    dsa = p.solve("full")
+    p.set("use_dsa", 0)
+    p.set("max_iterations", 40)
+    plain = p.solve("full")
+    assert dsa.converged and dsa.iterations == 6
+    assert 5 * dsa.iterations <= plain.iterations
