@@ -209,7 +209,10 @@ def main():
 
     prob = P.Problem("C5", device=local, nx=args.grid, ny=args.grid, n_theta=args.n_theta,
                      n_omega_z=args.n_omega_z, use_dsa=0)
-    stream = torch.cuda.current_stream()
+    # A dedicated (non-default) torch stream: the kernels and the CUDA events
+    # that time them are on the same stream.
+    stream = torch.cuda.Stream()
+    torch.cuda.set_stream(stream)
     prob.set_stream(stream.cuda_stream)
     D, n = prob.n_omega, prob.n
     cells = n // 4

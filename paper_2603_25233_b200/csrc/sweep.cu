@@ -134,125 +134,260 @@ __device__ __forceinline__ bool invert4(const double* M, double* Minv) {
 
 #undef A_
 
+// Position of a lane in its warp's stream of (band, column) work items:
+// k-th band owned by this warp (band = w + k*W), column col (may be
+// negative during the initial skew, or >= nx in the padding of S).
+struct Pos {
+  int k, col;
+};
+
+__device__ __forceinline__ void advance(Pos& p, int S) {
+  if (++p.col == S) {
+    p.col = 0;
+    ++p.k;
+  }
+}
+
+struct Geo {
+  int nx, ny, nb, S, w, W, lane;
+  bool xu, yu;
+  // returns true and the cell index when the position is a real cell
+  __device__ __forceinline__ bool cell(const Pos& p, size_t& c, int& band) const {
+    band = w + p.k * W;
+    const int row = band * 32 + lane;
+    if (p.col < 0 || p.col >= nx || band >= nb || row >= ny) return false;
+    const int ca = xu ? p.col : nx - 1 - p.col;
+    const int cb = yu ? row : ny - 1 - row;
+    c = static_cast<size_t>(cb) * nx + ca;
+    return true;
+  }
+};
+
+constexpr int kPrefetch = 4;   // rhs cells in flight per lane
+
+// Shared-memory load the compiler may not hoist out of the step loop (keeps
+// the per-direction 4x4 inverse out of the register file).
+__device__ __forceinline__ double2 lds2(const double* p) {
+  double2 v;
+  const unsigned a = static_cast<unsigned>(__cvta_generic_to_shared(p));
+  asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];" : "=d"(v.x), "=d"(v.y) : "r"(a));
+  return v;
+}
+constexpr int kRing = 64;      // columns per inter-warp trace ring
+
+// Shared memory of one direction group (W warps).
+struct GroupSmem {
+  double* consts;      // 40: minv / dstream (16), kx ky tx ty (8), spare
+  double* ring;        // W x kRing x 2
+  volatile int* prod;  // W: columns published by warp w's lane 31
+  volatile int* cons;  // W: columns of warp w's ring consumed by warp w+1
+};
+
+__host__ __device__ constexpr int group_smem_doubles(int W) { return 40 + W * kRing * 2 + W; }
+
 template <bool UNIFORM>
-__global__ void __launch_bounds__(128) sweep_kernel(const SweepArgs a) {
+__global__ void __launch_bounds__(256, 2) sweep_kernel(const SweepArgs a, int W) {
+  extern __shared__ double smem[];
   const int lane = threadIdx.x & 31;
-  const int w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  if (w >= a.n) return;  // whole warp exits together
-  const int ang = a.angles ? a.angles[w] : w;
+  const int wib = threadIdx.x >> 5;
+  const int groups = (blockDim.x >> 5) / W;
+  const int g = wib / W, w = wib % W;
+  const int slot = blockIdx.x * groups + g;
+  if (slot >= a.n || g >= groups) return;  // a whole direction group exits together
+  GroupSmem sm;
+  {
+    double* base = smem + static_cast<size_t>(g) * group_smem_doubles(W);
+    sm.consts = base;
+    sm.ring = base + 40;
+    int* ctr = reinterpret_cast<int*>(base + 40 + W * kRing * 2);
+    sm.prod = ctr;
+    sm.cons = ctr + W;
+  }
+  const int ang = a.angles ? a.angles[slot] : slot;
   const double omx = a.dirs[3 * ang], omy = a.dirs[3 * ang + 1];
   const bool xu = omx >= 0.0, yu = omy >= 0.0;  // sweep.cpp:37-38
-  const double* ax = xu ? a.sc.ax_minus : a.sc.ax_plus;
-  const double* ay = yu ? a.sc.ay_minus : a.sc.ay_plus;
-  // Upwind couplings: (B psi_up)[my,mx] = c[mx] * (t . psi_up[my,:]) with
+  // Per-direction constants, computed once by warp 0 into shared memory:
+  // the cell block Omega_x Ax + Omega_y Ay (general path) or the inverse of
+  // Omega_x Ax + Omega_y Ay + Sigma_t (uniform medium), and the upwind
+  // couplings (B psi_up)[my,mx] = c[mx] * (t . psi_up[my,:]) with
   // (c, t) = (-t_L, t_R) for the "minus" blocks and (t_R, t_L) for "plus".
-  double kx[2], tx[2], ky[2], ty[2];
+  if (w == 0) {
+    const double* ax = xu ? a.sc.ax_minus : a.sc.ax_plus;
+    const double* ay = yu ? a.sc.ay_minus : a.sc.ay_plus;
+    if (lane < 16) {
+      const double d = omx * ax[lane] + omy * ay[lane];
+      sm.consts[lane] = UNIFORM ? d + a.sigma_t[lane] : d;
+    }
+    if (lane < 2) {
+      sm.consts[16 + lane] = omx * (xu ? -a.sc.trx_l[lane] : a.sc.trx_r[lane]);
+      sm.consts[18 + lane] = xu ? a.sc.trx_r[lane] : a.sc.trx_l[lane];
+      sm.consts[20 + lane] = omy * (yu ? -a.sc.try_l[lane] : a.sc.try_r[lane]);
+      sm.consts[22 + lane] = yu ? a.sc.try_r[lane] : a.sc.try_l[lane];
+    }
+    __syncwarp();
+    if (UNIFORM && lane == 0) {
+      double M[16], Mi[16];
 #pragma unroll
-  for (int m = 0; m < 2; ++m) {
-    kx[m] = omx * (xu ? -a.sc.trx_l[m] : a.sc.trx_r[m]);
-    tx[m] = xu ? a.sc.trx_r[m] : a.sc.trx_l[m];
-    ky[m] = omy * (yu ? -a.sc.try_l[m] : a.sc.try_r[m]);
-    ty[m] = yu ? a.sc.try_r[m] : a.sc.try_l[m];
+      for (int k = 0; k < 16; ++k) M[k] = sm.consts[k];
+      if (!invert4(M, Mi)) atomicExch(a.err, 1);
+#pragma unroll
+      for (int k = 0; k < 16; ++k) sm.consts[k] = Mi[k];
+    }
+    if (lane < W) {
+      sm.prod[lane] = 0;
+      sm.cons[lane] = 0;
+    }
   }
-  double dstream[16];
-#pragma unroll
-  for (int k = 0; k < 16; ++k) dstream[k] = omx * ax[k] + omy * ay[k];
+  // all W warps of the group see the constants and initialised counters
+  asm volatile("bar.sync %0, %1;" ::"r"(g + 1), "r"(W * 32) : "memory");
+  const double* cst = sm.consts;
+  const double kx[2] = {cst[16], cst[17]}, tx[2] = {cst[18], cst[19]};
+  const double ky[2] = {cst[20], cst[21]}, ty[2] = {cst[22], cst[23]};
 
-  double minv[16];
-  if (UNIFORM) {
-    double M[16];
-#pragma unroll
-    for (int k = 0; k < 16; ++k) M[k] = dstream[k] + a.sigma_t[k];
-    if (!invert4(M, minv) && lane == 0) atomicExch(a.err, 1);
-  }
-
-  const int nx = a.nx, ny = a.ny;
-  const int S = nx > 32 ? nx : 32;
-  const int nb = (ny + 31) >> 5;
-  const int total = nb * S + 31;
-  double* line = a.line + static_cast<size_t>(w) * nx * 2;
-  const double* rhs = a.rhs + static_cast<long long>(w) * a.rhs_stride;
+  Geo geo;
+  geo.nx = a.nx;
+  geo.ny = a.ny;
+  geo.nb = (a.ny + 31) >> 5;
+  geo.S = a.nx > 32 ? a.nx : 32;
+  geo.w = w;
+  geo.W = W;
+  geo.lane = lane;
+  geo.xu = xu;
+  geo.yu = yu;
+  const int S = geo.S, nx = a.nx;
+  const int kw = (w < geo.nb) ? (geo.nb - w + W - 1) / W : 0;  // bands of this warp
+  const int total = kw * S + 31;
+  const double* rhs = a.rhs + static_cast<long long>(slot) * a.rhs_stride;
   const double* bc = a.bc ? a.bc + static_cast<long long>(ang) * a.bc_stride : nullptr;
-  double* psi = a.psi + static_cast<long long>(w) * a.psi_stride;
+  double* psi = a.psi + static_cast<long long>(slot) * a.psi_stride;
+  const int pw = (w + W - 1) % W;  // producer of our lane 0's traces
+
+  // prefetch queue: rhs of steps t .. t+kPrefetch-1 (slot = step % kPrefetch)
+  double q0[kPrefetch], q1[kPrefetch], q2[kPrefetch], q3[kPrefetch];
+  Pos cur{0, -lane}, pre{0, -lane};
+#pragma unroll
+  for (int s = 0; s < kPrefetch; ++s) {
+    size_t c;
+    int band;
+    q0[s] = q1[s] = q2[s] = q3[s] = 0.0;
+    if (geo.cell(pre, c, band)) {
+      double v[4];
+      ld_cell(rhs + 4 * c, v);
+      q0[s] = v[0];
+      q1[s] = v[1];
+      q2[s] = v[2];
+      q3[s] = v[3];
+    }
+    advance(pre, S);
+  }
 
   double txi0 = 0.0, txi1 = 0.0;  // x traces of the previous cell in the row
   double tyo0 = 0.0, tyo1 = 0.0;  // y traces produced last step
-  int col = -lane, band = 0;
-  for (int t = 0; t < total; ++t) {
-    double yi0 = __shfl_up_sync(0xffffffffu, tyo0, 1);
-    double yi1 = __shfl_up_sync(0xffffffffu, tyo1, 1);
-    const int row = band * 32 + lane;
-    const bool act = col >= 0 && col < nx && band < nb && row < ny;
-    tyo0 = 0.0;
-    tyo1 = 0.0;
-    if (act) {
-      if (lane == 0) {
-        if (band > 0) {
-          yi0 = __ldcg(line + 2 * col);
-          yi1 = __ldcg(line + 2 * col + 1);
+  for (int t0 = 0; t0 < total; t0 += kPrefetch) {
+#pragma unroll
+    for (int s = 0; s < kPrefetch; ++s) {
+      if (t0 + s >= total) break;  // warp-uniform
+      double v[4] = {q0[s], q1[s], q2[s], q3[s]};
+      // refill this queue slot with the step kPrefetch ahead
+      {
+        size_t c;
+        int band;
+        q0[s] = q1[s] = q2[s] = q3[s] = 0.0;
+        if (geo.cell(pre, c, band)) {
+          double u[4];
+          ld_cell(rhs + 4 * c, u);
+          q0[s] = u[0];
+          q1[s] = u[1];
+          q2[s] = u[2];
+          q3[s] = u[3];
+        }
+        advance(pre, S);
+      }
+      double yi0 = __shfl_up_sync(0xffffffffu, tyo0, 1);
+      double yi1 = __shfl_up_sync(0xffffffffu, tyo1, 1);
+      tyo0 = 0.0;
+      tyo1 = 0.0;
+      size_t cell;
+      int band;
+      if (geo.cell(cur, cell, band)) {
+        const int col = cur.col;
+        if (lane == 0) {
+          if (band == 0) {
+            yi0 = yi1 = 0.0;
+          } else {
+            // traces of band-1, column col, from the producer warp's ring
+            const int gidx = ((band - 1 - pw) / W) * nx + col;
+            while (sm.prod[pw] <= gidx) __nanosleep(32);
+            __threadfence_block();
+            const double* r = sm.ring + (static_cast<size_t>(pw) * kRing + (gidx % kRing)) * 2;
+            yi0 = r[0];
+            yi1 = r[1];
+            __threadfence_block();
+            sm.cons[pw] = gidx + 1;
+          }
+        }
+        if (col == 0) {
+          txi0 = 0.0;
+          txi1 = 0.0;
+        }
+        if (bc) {
+          double gb[4];
+          ld_cell(bc + 4 * cell, gb);
+#pragma unroll
+          for (int k = 0; k < 4; ++k) v[k] += gb[k];
+        }
+        // local = rhs - Omega_x Bx psi_x - Omega_y By psi_y   (sweep.cpp:40-46)
+        v[0] = v[0] - kx[0] * txi0;
+        v[1] = v[1] - kx[1] * txi0;
+        v[2] = v[2] - kx[0] * txi1;
+        v[3] = v[3] - kx[1] * txi1;
+        v[0] = v[0] - ky[0] * yi0;
+        v[1] = v[1] - ky[0] * yi1;
+        v[2] = v[2] - ky[1] * yi0;
+        v[3] = v[3] - ky[1] * yi1;
+        double p[4];
+        if (UNIFORM) {
+          p[0] = p[1] = p[2] = p[3] = 0.0;
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {  // column j of the inverse
+            const double2 lo = lds2(cst + 4 * j), hi = lds2(cst + 4 * j + 2);
+            p[0] += lo.x * v[j];
+            p[1] += lo.y * v[j];
+            p[2] += hi.x * v[j];
+            p[3] += hi.y * v[j];
+          }
         } else {
-          yi0 = 0.0;
-          yi1 = 0.0;
+          double A[16];
+          const double2* sb = reinterpret_cast<const double2*>(a.sigma_t + 16 * cell);
+#pragma unroll
+          for (int k = 0; k < 8; ++k) {
+            const double2 s2 = __ldg(sb + k);
+            A[2 * k] = cst[2 * k] + s2.x;
+            A[2 * k + 1] = cst[2 * k + 1] + s2.y;
+          }
+          if (!lu_solve4(A, v)) atomicExch(a.err, 1);
+#pragma unroll
+          for (int r = 0; r < 4; ++r) p[r] = v[r];
+        }
+        st_cell(psi + 4 * cell, p);
+        // outflow traces: x (per y-mode) for the next cell of this row,
+        // y (per x-mode) for the row above (next lane / next band).
+        txi0 = tx[0] * p[0] + tx[1] * p[1];
+        txi1 = tx[0] * p[2] + tx[1] * p[3];
+        tyo0 = ty[0] * p[0] + ty[1] * p[2];
+        tyo1 = ty[0] * p[1] + ty[1] * p[3];
+        if (lane == 31 && band + 1 < geo.nb) {
+          const int gidx = ((band - w) / W) * nx + col;
+          while (gidx - sm.cons[w] >= kRing) __nanosleep(32);
+          double* r = sm.ring + (static_cast<size_t>(w) * kRing + (gidx % kRing)) * 2;
+          r[0] = tyo0;
+          r[1] = tyo1;
+          __threadfence_block();
+          sm.prod[w] = gidx + 1;
         }
       }
-      if (col == 0) {
-        txi0 = 0.0;
-        txi1 = 0.0;
-      }
-      const int ca = xu ? col : nx - 1 - col;
-      const int cb = yu ? row : ny - 1 - row;
-      const size_t cell = static_cast<size_t>(cb) * nx + ca;
-      double v[4];
-      ld_cell(rhs + 4 * cell, v);
-      if (bc) {
-        double g[4];
-        ld_cell(bc + 4 * cell, g);
-#pragma unroll
-        for (int k = 0; k < 4; ++k) v[k] += g[k];
-      }
-      // local = rhs - Omega_x Bx psi_x - Omega_y By psi_y   (sweep.cpp:40-46)
-      v[0] = v[0] - kx[0] * txi0;
-      v[1] = v[1] - kx[1] * txi0;
-      v[2] = v[2] - kx[0] * txi1;
-      v[3] = v[3] - kx[1] * txi1;
-      v[0] = v[0] - ky[0] * yi0;
-      v[1] = v[1] - ky[0] * yi1;
-      v[2] = v[2] - ky[1] * yi0;
-      v[3] = v[3] - ky[1] * yi1;
-      double p[4];
-      if (UNIFORM) {
-#pragma unroll
-        for (int r = 0; r < 4; ++r)
-          p[r] = minv[r] * v[0] + minv[4 + r] * v[1] + minv[8 + r] * v[2] + minv[12 + r] * v[3];
-      } else {
-        double A[16];
-        const double2* sb = reinterpret_cast<const double2*>(a.sigma_t + 16 * cell);
-#pragma unroll
-        for (int k = 0; k < 8; ++k) {
-          const double2 s2 = __ldg(sb + k);
-          A[2 * k] = dstream[2 * k] + s2.x;
-          A[2 * k + 1] = dstream[2 * k + 1] + s2.y;
-        }
-        if (!lu_solve4(A, v)) atomicExch(a.err, 1);
-#pragma unroll
-        for (int r = 0; r < 4; ++r) p[r] = v[r];
-      }
-      st_cell(psi + 4 * cell, p);
-      // outflow traces: x (per y-mode) for the next cell of this row,
-      // y (per x-mode) for the row above (next lane / next band).
-      txi0 = tx[0] * p[0] + tx[1] * p[1];
-      txi1 = tx[0] * p[2] + tx[1] * p[3];
-      tyo0 = ty[0] * p[0] + ty[1] * p[2];
-      tyo1 = ty[0] * p[1] + ty[1] * p[3];
-      if (lane == 31) {
-        __stcg(line + 2 * col, tyo0);
-        __stcg(line + 2 * col + 1, tyo1);
-      }
-    }
-    __syncwarp();
-    if (++col == S) {
-      col = 0;
-      ++band;
+      __syncwarp();
+      advance(cur, S);
     }
   }
 }
@@ -275,12 +410,19 @@ __global__ void c5_fill_kernel(double* rhs, long long total, long long base, std
 
 void launch_sweep(const SweepArgs& a, bool uniform, cudaStream_t s) {
   if (a.n <= 0) return;
-  const int warps_per_block = 4;
-  const int blocks = (a.n + warps_per_block - 1) / warps_per_block;
+  // Warps per direction: enough concurrent warps to fill 148 SMs x 16, at
+  // most one per 32-row band, at most 8.
+  const int nb = (a.ny + 31) / 32;
+  int W = nb >= 2 ? 2 : 1;
+  while (W < 8 && static_cast<long long>(a.n) * W * 2 <= 148 * 16 && 2 * W <= nb) W *= 2;
+  const int warps_per_block = 8;
+  const int groups = warps_per_block / W;
+  const int blocks = (a.n + groups - 1) / groups;
+  const size_t smem = static_cast<size_t>(groups) * group_smem_doubles(W) * sizeof(double);
   if (uniform)
-    sweep_kernel<true><<<blocks, warps_per_block * 32, 0, s>>>(a);
+    sweep_kernel<true><<<blocks, warps_per_block * 32, smem, s>>>(a, W);
   else
-    sweep_kernel<false><<<blocks, warps_per_block * 32, 0, s>>>(a);
+    sweep_kernel<false><<<blocks, warps_per_block * 32, smem, s>>>(a, W);
   RTLR_CUDA(cudaGetLastError());
 }
 
