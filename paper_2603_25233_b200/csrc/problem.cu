@@ -172,7 +172,7 @@ void Problem::sweep(const int* d_angles, int n, const double* d_rhs, long long r
   a.psi = d_psi;
   a.psi_stride = psi_stride;
   a.sigma_t = sigma_t_.get();
-  a.line = line_.ensure(static_cast<size_t>(n) * hp_.nx * 2);
+  a.line = line_.ensure(static_cast<size_t>(n) * 8 * hp_.nx * 2);  // up to 8 warps per direction
   a.err = err_.get();
   a.sc = sc_;
   launch_sweep(a, hp_.sigma_t_uniform, stream_);

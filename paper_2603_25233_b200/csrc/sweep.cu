@@ -35,6 +35,16 @@ __device__ __forceinline__ void ld_cell(const double* p, double v[4]) {
   v[3] = b.y;
 }
 
+// Streaming source read: each lane walks its mesh row 32 B per step, so ask
+// L2 to fetch 256 B per miss (the lane's next 8 cells) instead of one 32-B
+// sector; consecutive steps then hit L2 and DRAM sees full bursts.
+__device__ __forceinline__ void ld_cell_stream(const double* p, double v[4]) {
+  asm volatile("ld.global.nc.L2::256B.v2.f64 {%0, %1}, [%4];\n\t"
+               "ld.global.nc.L2::256B.v2.f64 {%2, %3}, [%4+16];"
+               : "=d"(v[0]), "=d"(v[1]), "=d"(v[2]), "=d"(v[3])
+               : "l"(p));
+}
+
 __device__ __forceinline__ void st_cell(double* p, const double v[4]) {
   double2* q = reinterpret_cast<double2*>(p);
   __stcs(q, make_double2(v[0], v[1]));
@@ -164,6 +174,7 @@ struct Geo {
 };
 
 constexpr int kPrefetch = 4;   // rhs cells in flight per lane
+constexpr int kLineSmemBudget = 96 * 1024;  // bytes of trace lines per block kept in smem
 
 // Shared-memory load the compiler may not hoist out of the step loop (keeps
 // the per-direction 4x4 inverse out of the register file).
@@ -173,20 +184,26 @@ __device__ __forceinline__ double2 lds2(const double* p) {
   asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];" : "=d"(v.x), "=d"(v.y) : "r"(a));
   return v;
 }
-constexpr int kRing = 64;      // columns per inter-warp trace ring
-
-// Shared memory of one direction group (W warps).
+// Shared memory of one direction group (W warps).  Warp w hands the top
+// traces of each of its bands to warp (w+1) % W through a full-row trace
+// line (nx x 2 doubles, in smem when it fits, else in L2) plus a progress
+// counter: slot col of line w is only rewritten (band b+W) after warp w+1
+// read it for band b+1, because that rewrite depends on the read through
+// the upwind chain band b+1 -> ... -> b+W.  Readers therefore only wait for
+// data to be published; there are no space waits and no cycles.
 struct GroupSmem {
   double* consts;      // 40: minv / dstream (16), kx ky tx ty (8), spare
-  double* ring;        // W x kRing x 2
   volatile int* prod;  // W: columns published by warp w's lane 31
-  volatile int* cons;  // W: columns of warp w's ring consumed by warp w+1
+  double* lines;       // W x nx x 2 (shared or global)
 };
 
-__host__ __device__ constexpr int group_smem_doubles(int W) { return 40 + W * kRing * 2 + W; }
+__host__ __device__ constexpr int group_smem_doubles(int W, int nx, bool smem_lines) {
+  // even, so every group's constants stay 16-byte aligned for ld.shared.v2
+  return 40 + 2 * ((W + 3) / 4) + (smem_lines ? W * nx * 2 : 0);
+}
 
 template <bool UNIFORM>
-__global__ void __launch_bounds__(256, 2) sweep_kernel(const SweepArgs a, int W) {
+__global__ void __launch_bounds__(256, 2) sweep_kernel(const SweepArgs a, int W, bool smem_lines) {
   extern __shared__ double smem[];
   const int lane = threadIdx.x & 31;
   const int wib = threadIdx.x >> 5;
@@ -196,12 +213,10 @@ __global__ void __launch_bounds__(256, 2) sweep_kernel(const SweepArgs a, int W)
   if (slot >= a.n || g >= groups) return;  // a whole direction group exits together
   GroupSmem sm;
   {
-    double* base = smem + static_cast<size_t>(g) * group_smem_doubles(W);
+    double* base = smem + static_cast<size_t>(g) * group_smem_doubles(W, a.nx, smem_lines);
     sm.consts = base;
-    sm.ring = base + 40;
-    int* ctr = reinterpret_cast<int*>(base + 40 + W * kRing * 2);
-    sm.prod = ctr;
-    sm.cons = ctr + W;
+    sm.prod = reinterpret_cast<int*>(base + 40);
+    sm.lines = smem_lines ? base + 40 + 2 * ((W + 3) / 4) : a.line + static_cast<size_t>(slot) * W * a.nx * 2;
   }
   const int ang = a.angles ? a.angles[slot] : slot;
   const double omx = a.dirs[3 * ang], omy = a.dirs[3 * ang + 1];
@@ -233,10 +248,7 @@ __global__ void __launch_bounds__(256, 2) sweep_kernel(const SweepArgs a, int W)
 #pragma unroll
       for (int k = 0; k < 16; ++k) sm.consts[k] = Mi[k];
     }
-    if (lane < W) {
-      sm.prod[lane] = 0;
-      sm.cons[lane] = 0;
-    }
+    if (lane < W) sm.prod[lane] = 0;
   }
   // all W warps of the group see the constants and initialised counters
   asm volatile("bar.sync %0, %1;" ::"r"(g + 1), "r"(W * 32) : "memory");
@@ -272,7 +284,7 @@ __global__ void __launch_bounds__(256, 2) sweep_kernel(const SweepArgs a, int W)
     q0[s] = q1[s] = q2[s] = q3[s] = 0.0;
     if (geo.cell(pre, c, band)) {
       double v[4];
-      ld_cell(rhs + 4 * c, v);
+      ld_cell_stream(rhs + 4 * c, v);
       q0[s] = v[0];
       q1[s] = v[1];
       q2[s] = v[2];
@@ -295,7 +307,7 @@ __global__ void __launch_bounds__(256, 2) sweep_kernel(const SweepArgs a, int W)
         q0[s] = q1[s] = q2[s] = q3[s] = 0.0;
         if (geo.cell(pre, c, band)) {
           double u[4];
-          ld_cell(rhs + 4 * c, u);
+          ld_cell_stream(rhs + 4 * c, u);
           q0[s] = u[0];
           q1[s] = u[1];
           q2[s] = u[2];
@@ -315,15 +327,18 @@ __global__ void __launch_bounds__(256, 2) sweep_kernel(const SweepArgs a, int W)
           if (band == 0) {
             yi0 = yi1 = 0.0;
           } else {
-            // traces of band-1, column col, from the producer warp's ring
+            // traces of band-1, column col, from the producer warp's line
             const int gidx = ((band - 1 - pw) / W) * nx + col;
-            while (sm.prod[pw] <= gidx) __nanosleep(32);
+            while (sm.prod[pw] <= gidx) __nanosleep(20);
             __threadfence_block();
-            const double* r = sm.ring + (static_cast<size_t>(pw) * kRing + (gidx % kRing)) * 2;
-            yi0 = r[0];
-            yi1 = r[1];
-            __threadfence_block();
-            sm.cons[pw] = gidx + 1;
+            const double* r = sm.lines + (static_cast<size_t>(pw) * nx + col) * 2;
+            if (smem_lines) {
+              yi0 = r[0];
+              yi1 = r[1];
+            } else {
+              yi0 = __ldcg(r);
+              yi1 = __ldcg(r + 1);
+            }
           }
         }
         if (col == 0) {
@@ -378,10 +393,14 @@ __global__ void __launch_bounds__(256, 2) sweep_kernel(const SweepArgs a, int W)
         tyo1 = ty[0] * p[1] + ty[1] * p[3];
         if (lane == 31 && band + 1 < geo.nb) {
           const int gidx = ((band - w) / W) * nx + col;
-          while (gidx - sm.cons[w] >= kRing) __nanosleep(32);
-          double* r = sm.ring + (static_cast<size_t>(w) * kRing + (gidx % kRing)) * 2;
-          r[0] = tyo0;
-          r[1] = tyo1;
+          double* r = sm.lines + (static_cast<size_t>(w) * nx + col) * 2;
+          if (smem_lines) {
+            r[0] = tyo0;
+            r[1] = tyo1;
+          } else {
+            __stcg(r, tyo0);
+            __stcg(r + 1, tyo1);
+          }
           __threadfence_block();
           sm.prod[w] = gidx + 1;
         }
@@ -413,16 +432,24 @@ void launch_sweep(const SweepArgs& a, bool uniform, cudaStream_t s) {
   // Warps per direction: enough concurrent warps to fill 148 SMs x 16, at
   // most one per 32-row band, at most 8.
   const int nb = (a.ny + 31) / 32;
-  int W = nb >= 2 ? 2 : 1;
-  while (W < 8 && static_cast<long long>(a.n) * W * 2 <= 148 * 16 && 2 * W <= nb) W *= 2;
+  // Deadlock-free only when a band row is longer than the lane skew of the
+  // whole warp chain: S > 32 W (warp j at step t needs warp j-1 past step
+  // t + 32; warp 0's next band needs warp W-1, i.e. itself 32 W steps back).
+  const int S = a.nx > 32 ? a.nx : 32;
+  int W = 1;
+  while (W < 8 && static_cast<long long>(a.n) * W * 2 <= 148 * 16 && 2 * W <= nb && 32 * (2 * W) < S) W *= 2;
   const int warps_per_block = 8;
   const int groups = warps_per_block / W;
   const int blocks = (a.n + groups - 1) / groups;
-  const size_t smem = static_cast<size_t>(groups) * group_smem_doubles(W) * sizeof(double);
-  if (uniform)
-    sweep_kernel<true><<<blocks, warps_per_block * 32, smem, s>>>(a, W);
-  else
-    sweep_kernel<false><<<blocks, warps_per_block * 32, smem, s>>>(a, W);
+  const bool smem_lines = static_cast<size_t>(8) * a.nx * 2 * sizeof(double) <= kLineSmemBudget;
+  const size_t smem = static_cast<size_t>(groups) * group_smem_doubles(W, a.nx, smem_lines) * sizeof(double);
+  if (uniform) {
+    RTLR_CUDA(cudaFuncSetAttribute(sweep_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+    sweep_kernel<true><<<blocks, warps_per_block * 32, smem, s>>>(a, W, smem_lines);
+  } else {
+    RTLR_CUDA(cudaFuncSetAttribute(sweep_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+    sweep_kernel<false><<<blocks, warps_per_block * 32, smem, s>>>(a, W, smem_lines);
+  }
   RTLR_CUDA(cudaGetLastError());
 }
 
