@@ -1,0 +1,613 @@
+// Dense fp64 kernels of the low-rank path (see dense.cuh).
+#include <algorithm>
+#include <cmath>
+#include <vector>
+
+#include "dense.cuh"
+
+namespace rtlr {
+namespace cuda {
+
+namespace {
+
+constexpr int BM = 64, BN = 64, BK = 16;
+
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+// Block-wide sum (blockDim.x multiple of 32, <= 1024); result valid in all threads.
+__device__ __forceinline__ double block_sum_all(double v, double* sh) {
+  v = warp_sum(v);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+  __syncthreads();
+  if (lane == 0) sh[warp] = v;
+  __syncthreads();
+  double s = 0.0;
+  for (int i = 0; i < nw; ++i) s += sh[i];  // fixed order
+  __syncthreads();
+  return s;
+}
+
+// ------------------------------------------------------------ GEMM A^T B
+// grid (tilesM, tilesN, splits); each CTA accumulates a 64x64 tile over its
+// K range into part[split] (M x N col-major) or directly into C.
+__global__ void __launch_bounds__(256) gemm_tn_kernel(int M, int N, long long K, long long kchunk,
+                                                      const double* __restrict__ A, long long lda,
+                                                      const double* __restrict__ B, long long ldb,
+                                                      double* __restrict__ out, long long ldo, long long split_stride) {
+  __shared__ double As[BK][BM + 1];
+  __shared__ double Bs[BK][BN + 1];
+  const int tid = threadIdx.x;
+  const int tm = tid % 16, tn = tid / 16;  // 16 x 16 threads, 4 x 4 outputs each
+  const int m0 = blockIdx.x * BM, n0 = blockIdx.y * BN;
+  const long long k0 = blockIdx.z * kchunk;
+  const long long k1 = min(K, k0 + kchunk);
+  double acc[4][4] = {};
+  for (long long kb = k0; kb < k1; kb += BK) {
+    // load A[kb:kb+16, m0:m0+64] -> As[k][m]; 1024 elements, 4 per thread
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      const int idx = tid + e * 256;
+      const int kk = idx % BK, mm = idx / BK;
+      const long long k = kb + kk;
+      const int m = m0 + mm;
+      As[kk][mm] = (k < k1 && m < M) ? A[k + m * lda] : 0.0;
+      const int n = n0 + mm;
+      Bs[kk][mm] = (k < k1 && n < N) ? B[k + n * ldb] : 0.0;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int kk = 0; kk < BK; ++kk) {
+      double a[4], b[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) a[i] = As[kk][tm + 16 * i];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) b[j] = Bs[kk][tn + 16 * j];
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) acc[i][j] += a[i] * b[j];
+    }
+    __syncthreads();
+  }
+  double* o = out + blockIdx.z * split_stride;
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int m = m0 + tm + 16 * i, n = n0 + tn + 16 * j;
+      if (m < M && n < N) o[m + n * ldo] = acc[i][j];
+    }
+}
+
+__global__ void splitk_reduce(int M, int N, int splits, const double* __restrict__ part, double* __restrict__ C,
+                              long long ldc) {
+  const long long total = static_cast<long long>(M) * N;
+  for (long long e = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; e < total;
+       e += static_cast<long long>(gridDim.x) * blockDim.x) {
+    double s = 0.0;
+    for (int z = 0; z < splits; ++z) s += part[z * total + e];
+    const int m = static_cast<int>(e % M), n = static_cast<int>(e / M);
+    C[m + n * ldc] = s;
+  }
+}
+
+int tn_splits(int M, int N, long long K) {
+  const long long tiles = static_cast<long long>((M + BM - 1) / BM) * ((N + BN - 1) / BN);
+  long long s = (2 * 148 * 2 + tiles - 1) / tiles;  // ~4 CTAs per SM
+  s = std::min<long long>(s, std::max<long long>(1, K / 256));
+  s = std::min<long long>(s, 1024);
+  return static_cast<int>(std::max<long long>(1, s));
+}
+
+// ------------------------------------------------------------ GEMM A B
+__global__ void __launch_bounds__(256) gemm_nn_kernel(long long M, int N, int K, const double* __restrict__ A,
+                                                      long long lda, const double* __restrict__ B, long long ldb,
+                                                      double* __restrict__ C, long long ldc) {
+  __shared__ double As[BK][BM + 1];
+  __shared__ double Bs[BK][BN + 1];
+  const int tid = threadIdx.x;
+  const int tm = tid % 16, tn = tid / 16;
+  const long long m0 = blockIdx.x * static_cast<long long>(BM);
+  const int n0 = blockIdx.y * BN;
+  double acc[4][4] = {};
+  for (int kb = 0; kb < K; kb += BK) {
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      const int idx = tid + e * 256;
+      const int mm = idx % BM, kk = idx / BM;  // A is M-contiguous
+      const long long m = m0 + mm;
+      const int k = kb + kk;
+      As[kk][mm] = (k < K && m < M) ? A[m + k * lda] : 0.0;
+      const int kk2 = idx % BK, nn = idx / BK;  // B is K-contiguous
+      const int k2 = kb + kk2, n = n0 + nn;
+      Bs[kk2][nn] = (k2 < K && n < N) ? B[k2 + n * ldb] : 0.0;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int kk = 0; kk < BK; ++kk) {
+      double a[4], b[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) a[i] = As[kk][tm + 16 * i];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) b[j] = Bs[kk][tn + 16 * j];
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) acc[i][j] += a[i] * b[j];
+    }
+    __syncthreads();
+  }
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const long long m = m0 + tm + 16 * i;
+      const int n = n0 + tn + 16 * j;
+      if (m < M && n < N) C[m + n * ldc] = acc[i][j];
+    }
+}
+
+// ------------------------------------------------------------ vectors
+__global__ void gemv_n_kernel(long long n, int k, const double* __restrict__ A, long long lda,
+                              const double* __restrict__ x, double alpha, double* __restrict__ y) {
+  for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<long long>(gridDim.x) * blockDim.x) {
+    double s = 0.0;
+    for (int j = 0; j < k; ++j) s += A[i + j * lda] * x[j];
+    y[i] += alpha * s;
+  }
+}
+
+constexpr int kDotParts = 296;
+
+__global__ void dot_partials(long long n, const double* __restrict__ a, const double* __restrict__ b,
+                             double* __restrict__ part) {
+  __shared__ double sh[32];
+  double s = 0.0;
+  for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<long long>(gridDim.x) * blockDim.x)
+    s += a[i] * b[i];
+  s = block_sum_all(s, sh);
+  if (threadIdx.x == 0) part[blockIdx.x] = s;
+}
+
+__global__ void dot_finish(int parts, const double* __restrict__ part, double* __restrict__ out) {
+  __shared__ double sh[32];
+  double s = 0.0;
+  for (int i = threadIdx.x; i < parts; i += blockDim.x) s += part[i];
+  s = block_sum_all(s, sh);
+  if (threadIdx.x == 0) *out = s;
+}
+
+__global__ void scale_copy_kernel(long long n, const double* __restrict__ x, const double* __restrict__ h,
+                                  double* __restrict__ y) {
+  const double d = *h;
+  for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<long long>(gridDim.x) * blockDim.x)
+    y[i] = x[i] / d;
+}
+
+__global__ void axpy_kernel(long long n, const double* __restrict__ alpha, double sign, const double* __restrict__ x,
+                            double* __restrict__ y) {
+  const double a = sign * *alpha;
+  for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<long long>(gridDim.x) * blockDim.x)
+    y[i] += a * x[i];
+}
+
+int grid1d(long long n) {
+  long long g = (n + 255) / 256;
+  return static_cast<int>(std::max<long long>(1, std::min<long long>(g, 148 * 16)));
+}
+
+// ------------------------------------------------------------ stencils
+__device__ __forceinline__ double row_mv(const double* B, int i, const double* v) {
+  return B[i] * v[0] + B[4 + i] * v[1] + B[8 + i] * v[2] + B[12 + i] * v[3];
+}
+__device__ __forceinline__ double col_mv(const double* B, int i, const double* v) {  // (B^T v)_i
+  return B[4 * i] * v[0] + B[4 * i + 1] * v[1] + B[4 * i + 2] * v[2] + B[4 * i + 3] * v[3];
+}
+
+__global__ void stream_products_kernel(const StencilArgs A, int p, const double* __restrict__ P, long long ldp,
+                                       double* __restrict__ W, long long ldw) {
+  const long long ndof = 4LL * A.ncell;
+  const long long total = ndof * p;
+  for (long long e = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; e < total;
+       e += static_cast<long long>(gridDim.x) * blockDim.x) {
+    const int j = static_cast<int>(e / ndof);
+    const long long r = e % ndof;
+    const int c = static_cast<int>(r >> 2), i = static_cast<int>(r & 3);
+    const int a = c % A.nx, b = c / A.nx;
+    const double* pc = P + j * ldp + 4LL * c;
+    const long long up = 4LL * A.nx;
+    double dxm = row_mv(A.sc.ax_minus, i, pc);
+    if (a > 0) dxm += row_mv(A.sc.bx_minus, i, pc - 4);
+    double dxmt = col_mv(A.sc.ax_minus, i, pc);
+    if (a + 1 < A.nx) dxmt += col_mv(A.sc.bx_minus, i, pc + 4);
+    double dym = row_mv(A.sc.ay_minus, i, pc);
+    if (b > 0) dym += row_mv(A.sc.by_minus, i, pc - up);
+    double dymt = col_mv(A.sc.ay_minus, i, pc);
+    if (b + 1 < A.ny) dymt += col_mv(A.sc.by_minus, i, pc + up);
+    const double st = row_mv(A.sigma_t + 16LL * c, i, pc);
+    const long long o = r + j * ldw;
+    const long long blk = p * ldw;
+    W[o] = dxm;
+    W[o + blk] = dxmt;
+    W[o + 2 * blk] = dym;
+    W[o + 3 * blk] = dymt;
+    W[o + 4 * blk] = st;
+  }
+}
+
+// ------------------------------------------------------------ Galerkin LU
+// One CTA per angle.  A (r x r, column-major, leading dimension r) lives in
+// shared memory (r <= kSmemLuMax) or in the global workspace.
+__device__ void lu_solve_block(double* Am, double* b, int r, double* shv, int* shi) {
+  const int tid = threadIdx.x, nt = blockDim.x;
+  for (int k = 0; k < r; ++k) {
+    // pivot: first maximum of |A[i,k]|, i >= k
+    double best = -1.0;
+    int bi = r;
+    for (int i = k + tid; i < r; i += nt) {
+      const double v = fabs(Am[i + k * r]);
+      if (v > best) {
+        best = v;
+        bi = i;
+      }
+    }
+    // warp then block argmax, ties -> smaller index
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const double ov = __shfl_xor_sync(0xffffffffu, best, o);
+      const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+      if (ov > best || (ov == best && oi < bi)) {
+        best = ov;
+        bi = oi;
+      }
+    }
+    const int warp = tid >> 5, lane = tid & 31;
+    if (lane == 0) {
+      shv[warp] = best;
+      shi[warp] = bi;
+    }
+    __syncthreads();
+    if (tid == 0) {
+      double bv = shv[0];
+      int bix = shi[0];
+      for (int w = 1; w < (nt >> 5); ++w)
+        if (shv[w] > bv || (shv[w] == bv && shi[w] < bix)) {
+          bv = shv[w];
+          bix = shi[w];
+        }
+      shi[32] = bix;
+      shv[32] = bv;
+    }
+    __syncthreads();
+    const int p = shi[32];
+    const bool nonzero = shv[32] > 0.0;
+    if (nonzero && p != k) {
+      for (int j = tid; j < r; j += nt) {
+        const double t = Am[k + j * r];
+        Am[k + j * r] = Am[p + j * r];
+        Am[p + j * r] = t;
+      }
+      if (tid == 0) {
+        const double t = b[k];
+        b[k] = b[p];
+        b[p] = t;
+      }
+    }
+    __syncthreads();
+    if (nonzero) {
+      const double d = Am[k + k * r];
+      for (int i = k + 1 + tid; i < r; i += nt) Am[i + k * r] /= d;
+    }
+    __syncthreads();
+    // trailing update and forward substitution on b
+    const int rr = r - k - 1;
+    for (int e = tid; e < rr * rr; e += nt) {
+      const int i = k + 1 + e % rr, j = k + 1 + e / rr;
+      Am[i + j * r] -= Am[i + k * r] * Am[k + j * r];
+    }
+    for (int i = k + 1 + tid; i < r; i += nt) b[i] -= b[k] * Am[i + k * r];
+    __syncthreads();
+  }
+  // back substitution (column oriented)
+  for (int i = r - 1; i >= 0; --i) {
+    if (tid == 0) b[i] = b[i] / Am[i + i * r];
+    __syncthreads();
+    const double bi = b[i];
+    for (int j = tid; j < i; j += nt) b[j] -= bi * Am[j + i * r];
+    __syncthreads();
+  }
+}
+
+__global__ void __launch_bounds__(256) galerkin_kernel(int r, const int* __restrict__ angles,
+                                                       const double* __restrict__ dirs, const double* __restrict__ proj,
+                                                       long long ldp, long long pstride, const double* __restrict__ prhs,
+                                                       const double* __restrict__ extra, double* __restrict__ sol,
+                                                       long long ldsol, int* __restrict__ flags, double* __restrict__ work,
+                                                       bool in_smem) {
+  extern __shared__ double sm[];
+  __shared__ double shv[33];
+  __shared__ int shi[33];
+  __shared__ double bvec_small[kSmemLuMax];
+  const int jb = blockIdx.x;
+  const int ang = angles[jb];
+  const double omx = dirs[3 * ang], omy = dirs[3 * ang + 1];
+  const double* px = proj + (omx >= 0.0 ? 0 : 1) * pstride;
+  const double* py = proj + (omy >= 0.0 ? 2 : 3) * pstride;
+  const double* pt = proj + 4 * pstride;
+  double* Am = in_smem ? sm : work + static_cast<size_t>(jb) * r * r;
+  double* b = in_smem ? bvec_small : sol + jb * ldsol;
+  // reduced_streaming (low_rank.cpp:176-183): omx*Px + omy*Py + Pt
+  for (int e = threadIdx.x; e < r * r; e += blockDim.x) {
+    const int i = e % r, j = e / r;
+    Am[i + j * r] = omx * px[i + j * ldp] + omy * py[i + j * ldp] + pt[i + j * ldp];
+  }
+  for (int i = threadIdx.x; i < r; i += blockDim.x) b[i] = prhs[i] + (extra ? extra[i + jb * ldsol] : 0.0);
+  __syncthreads();
+  lu_solve_block(Am, b, r, shv, shi);
+  int bad = 0;
+  for (int i = threadIdx.x; i < r; i += blockDim.x) {
+    if (!isfinite(b[i])) bad = 1;
+    if (in_smem) sol[i + jb * ldsol] = b[i];
+  }
+  bad = __syncthreads_or(bad);
+  if (threadIdx.x == 0) flags[jb] = bad;
+}
+
+// ------------------------------------------------------------ Householder QR
+// column tail norms: out[0] = sum_{i>k} x_i^2 over column k (rows k+1..m-1)
+__global__ void hh_tail(long long m, int k, const double* __restrict__ a, long long lda, double* __restrict__ part) {
+  __shared__ double sh[32];
+  double s = 0.0;
+  for (long long i = k + 1 + blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < m;
+       i += static_cast<long long>(gridDim.x) * blockDim.x) {
+    const double v = a[i + k * lda];
+    s += v * v;
+  }
+  s = block_sum_all(s, sh);
+  if (threadIdx.x == 0) part[blockIdx.x] = s;
+}
+
+// beta / tau (Eigen makeHouseholder) from the partials; store in scal[0..2]
+__global__ void hh_make(int parts, int k, double* a, long long lda, const double* part, double* tau, double* scal) {
+  __shared__ double sh[32];
+  double s = 0.0;
+  for (int i = threadIdx.x; i < parts; i += blockDim.x) s += part[i];
+  s = block_sum_all(s, sh);
+  if (threadIdx.x == 0) {
+    const double c0 = a[k + k * lda];
+    double beta, t, denom;
+    if (s <= 2.2250738585072014e-308) {
+      t = 0.0;
+      beta = c0;
+      denom = 0.0;  // tail zeroed
+    } else {
+      beta = sqrt(c0 * c0 + s);
+      if (c0 >= 0.0) beta = -beta;
+      denom = c0 - beta;
+      t = (beta - c0) / beta;
+    }
+    tau[k] = t;
+    scal[0] = denom;
+    scal[1] = beta;
+  }
+}
+
+__global__ void hh_scale_tail(long long m, int k, double* a, long long lda, const double* scal) {
+  const double denom = scal[0];
+  for (long long i = k + 1 + blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < m;
+       i += static_cast<long long>(gridDim.x) * blockDim.x)
+    a[i + k * lda] = denom == 0.0 ? 0.0 : a[i + k * lda] / denom;
+}
+
+// w_j = a[k,j] + sum_{i>k} v_i a[i,j] for j in [j0, j1): one CTA per column,
+// then a[:,j] -= tau w_j v   (v_0 = 1, v_i = a[i,k] for i > k)
+__global__ void hh_apply(long long m, int k, const double* __restrict__ v, long long ldv, const double* tau,
+                         double* a, long long lda, int j0) {
+  __shared__ double sh[32];
+  const int j = j0 + blockIdx.x;
+  double* col = a + j * lda;
+  double s = 0.0;
+  for (long long i = k + 1 + threadIdx.x; i < m; i += blockDim.x) s += v[i + k * ldv] * col[i];
+  s = block_sum_all(s, sh);
+  const double w = tau[k] * (col[k] + s);
+  if (threadIdx.x == 0) col[k] -= w;
+  for (long long i = k + 1 + threadIdx.x; i < m; i += blockDim.x) col[i] -= w * v[i + k * ldv];
+}
+
+__global__ void set_beta(int k, double* a, long long lda, const double* scal) {
+  if (threadIdx.x == 0 && blockIdx.x == 0) a[k + k * lda] = scal[1];
+}
+
+__global__ void eye_cols(long long m, int n, double* q, long long ldq) {
+  const long long total = m * n;
+  for (long long e = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; e < total;
+       e += static_cast<long long>(gridDim.x) * blockDim.x) {
+    const long long i = e % m, j = e / m;
+    q[i + j * ldq] = (i == j) ? 1.0 : 0.0;
+  }
+}
+
+__global__ void extract_r(int n, const double* a, long long lda, double* r) {
+  for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < n * n; e += gridDim.x * blockDim.x) {
+    const int i = e % n, j = e / n;
+    r[i + j * n] = (i <= j) ? a[i + j * lda] : 0.0;
+  }
+}
+
+// ------------------------------------------------------------ Jacobi SVD
+__device__ __forceinline__ int rr_player(int k, int t, int n) {  // round-robin schedule
+  return k == 0 ? 0 : ((k - 1 + t) % (n - 1)) + 1;
+}
+
+__global__ void __launch_bounds__(256) jacobi_round(long long m, int n, int npad, int t, double* __restrict__ w,
+                                                    long long ldw, double* __restrict__ v, int* __restrict__ rotated) {
+  __shared__ double sh[32];
+  const int pi = blockIdx.x;
+  int p = rr_player(pi, t, npad), q = rr_player(npad - 1 - pi, t, npad);
+  if (p > q) {
+    const int tmp = p;
+    p = q;
+    q = tmp;
+  }
+  if (q >= n) return;  // padding player
+  double* wp = w + p * ldw;
+  double* wq = w + q * ldw;
+  double al = 0.0, be = 0.0, ga = 0.0;
+  for (long long i = threadIdx.x; i < m; i += blockDim.x) {
+    const double x = wp[i], y = wq[i];
+    al += x * x;
+    be += y * y;
+    ga += x * y;
+  }
+  al = block_sum_all(al, sh);
+  be = block_sum_all(be, sh);
+  ga = block_sum_all(ga, sh);
+  if (ga == 0.0 || fabs(ga) <= 1e-15 * sqrt(al * be)) return;
+  if (threadIdx.x == 0) atomicAdd(rotated, 1);
+  const double zeta = (be - al) / (2.0 * ga);
+  const double tt = (zeta >= 0 ? 1.0 : -1.0) / (fabs(zeta) + sqrt(1.0 + zeta * zeta));
+  const double c = 1.0 / sqrt(1.0 + tt * tt), s = c * tt;
+  for (long long i = threadIdx.x; i < m; i += blockDim.x) {
+    const double x = wp[i], y = wq[i];
+    wp[i] = c * x - s * y;
+    wq[i] = s * x + c * y;
+  }
+  if (v) {
+    double* vp = v + static_cast<long long>(p) * n;
+    double* vq = v + static_cast<long long>(q) * n;
+    for (int i = threadIdx.x; i < n; i += blockDim.x) {
+      const double x = vp[i], y = vq[i];
+      vp[i] = c * x - s * y;
+      vq[i] = s * x + c * y;
+    }
+  }
+}
+
+}  // namespace
+
+size_t gemm_tn_work(int M, int N, long long K) {
+  return static_cast<size_t>(tn_splits(M, N, K)) * M * N;
+}
+
+void gemm_tn(int M, int N, long long K, const double* A, long long lda, const double* B, long long ldb, double* C,
+             long long ldc, double* work, size_t work_doubles, cudaStream_t s) {
+  if (M <= 0 || N <= 0) return;
+  int splits = tn_splits(M, N, K);
+  while (splits > 1 && static_cast<size_t>(splits) * M * N > work_doubles) splits /= 2;
+  long long kchunk = (K + splits - 1) / splits;
+  kchunk = ((kchunk + BK - 1) / BK) * BK;
+  splits = static_cast<int>((K + kchunk - 1) / kchunk);
+  if (splits < 1) splits = 1;
+  dim3 grid((M + BM - 1) / BM, (N + BN - 1) / BN, splits);
+  if (splits == 1) {
+    gemm_tn_kernel<<<grid, 256, 0, s>>>(M, N, K, kchunk, A, lda, B, ldb, C, ldc, 0);
+  } else {
+    gemm_tn_kernel<<<grid, 256, 0, s>>>(M, N, K, kchunk, A, lda, B, ldb, work, M, static_cast<long long>(M) * N);
+    splitk_reduce<<<grid1d(static_cast<long long>(M) * N), 256, 0, s>>>(M, N, splits, work, C, ldc);
+  }
+  RTLR_CUDA(cudaGetLastError());
+}
+
+void gemm_nn(long long M, int N, int K, const double* A, long long lda, const double* B, long long ldb, double* C,
+             long long ldc, cudaStream_t s) {
+  if (M <= 0 || N <= 0) return;
+  if (K <= 0) {
+    for (int j = 0; j < N; ++j) RTLR_CUDA(cudaMemsetAsync(C + j * ldc, 0, M * sizeof(double), s));
+    return;
+  }
+  dim3 grid(static_cast<unsigned>((M + BM - 1) / BM), (N + BN - 1) / BN);
+  gemm_nn_kernel<<<grid, 256, 0, s>>>(M, N, K, A, lda, B, ldb, C, ldc);
+  RTLR_CUDA(cudaGetLastError());
+}
+
+void gemv_n(long long n, int k, const double* A, long long lda, const double* x, double alpha, double* y,
+            cudaStream_t s) {
+  if (k <= 0) return;
+  gemv_n_kernel<<<grid1d(n), 256, 0, s>>>(n, k, A, lda, x, alpha, y);
+  RTLR_CUDA(cudaGetLastError());
+}
+
+void dot(long long n, const double* a, const double* b, double* work, double* out, cudaStream_t s) {
+  dot_partials<<<kDotParts, 256, 0, s>>>(n, a, b, work);
+  dot_finish<<<1, 256, 0, s>>>(kDotParts, work, out);
+  RTLR_CUDA(cudaGetLastError());
+}
+
+void scale_copy(long long n, const double* x, const double* h, double* y, cudaStream_t s) {
+  scale_copy_kernel<<<grid1d(n), 256, 0, s>>>(n, x, h, y);
+  RTLR_CUDA(cudaGetLastError());
+}
+
+void axpy_dev(long long n, const double* alpha, double sign, const double* x, double* y, cudaStream_t s) {
+  axpy_kernel<<<grid1d(n), 256, 0, s>>>(n, alpha, sign, x, y);
+  RTLR_CUDA(cudaGetLastError());
+}
+
+void stream_products(const StencilArgs& a, int p, const double* P, long long ldp, double* W, long long ldw,
+                     cudaStream_t s) {
+  if (p <= 0) return;
+  stream_products_kernel<<<grid1d(4LL * a.ncell * p), 256, 0, s>>>(a, p, P, ldp, W, ldw);
+  RTLR_CUDA(cudaGetLastError());
+}
+
+void galerkin_batch(int r, int m, const int* angles, const double* dirs, const double* proj, long long ldp,
+                    long long proj_stride, const double* prhs, const double* extra, double* sol, long long ldsol,
+                    int* flags, double* work, cudaStream_t s) {
+  if (m <= 0 || r <= 0) return;
+  const bool in_smem = r <= kSmemLuMax;
+  const size_t smem = in_smem ? static_cast<size_t>(r) * r * sizeof(double) : 0;
+  if (in_smem)
+    RTLR_CUDA(cudaFuncSetAttribute(galerkin_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   kSmemLuMax * kSmemLuMax * 8));
+  galerkin_kernel<<<m, 256, smem, s>>>(r, angles, dirs, proj, ldp, proj_stride, prhs, extra, sol, ldsol, flags,
+                                       work, in_smem);
+  RTLR_CUDA(cudaGetLastError());
+}
+
+void householder_qr(long long m, int n, double* a, long long lda, double* tau, double* q, long long ldq, double* r,
+                    double* work, cudaStream_t s) {
+  // work: kDotParts + 4 doubles
+  double* part = work;
+  double* scal = work + kDotParts;
+  for (int k = 0; k < n && k < m; ++k) {
+    hh_tail<<<kDotParts, 256, 0, s>>>(m, k, a, lda, part);
+    hh_make<<<1, 256, 0, s>>>(kDotParts, k, a, lda, part, tau, scal);
+    hh_scale_tail<<<grid1d(m), 256, 0, s>>>(m, k, a, lda, scal);
+    if (k + 1 < n) hh_apply<<<n - k - 1, 256, 0, s>>>(m, k, a, lda, tau, a, lda, k + 1);
+    set_beta<<<1, 32, 0, s>>>(k, a, lda, scal);
+  }
+  RTLR_CUDA(cudaGetLastError());
+  extract_r<<<grid1d(static_cast<long long>(n) * n), 256, 0, s>>>(n, a, lda, r);
+  // Q = H_0 ... H_{n-1} I[:, :n], applied backwards.  v_k lives below the
+  // diagonal of a (v_0 = 1 implicit; the diagonal now holds beta).
+  eye_cols<<<grid1d(m * n), 256, 0, s>>>(m, n, q, ldq);
+  for (int k = std::min<long long>(n, m) - 1; k >= 0; --k)
+    hh_apply<<<n, 256, 0, s>>>(m, k, a, lda, tau, q, ldq, 0);
+  RTLR_CUDA(cudaGetLastError());
+}
+
+void jacobi_svd(long long m, int n, double* w, long long ldw, double* v, int max_sweeps, int* host_rotated,
+                double* work, cudaStream_t s) {
+  if (n < 2) return;
+  const int npad = n + (n & 1);
+  int* d_rot = reinterpret_cast<int*>(work);
+  for (int sweep = 0; sweep < max_sweeps; ++sweep) {
+    RTLR_CUDA(cudaMemsetAsync(d_rot, 0, sizeof(int), s));
+    for (int t = 0; t < npad - 1; ++t) jacobi_round<<<npad / 2, 256, 0, s>>>(m, n, npad, t, w, ldw, v, d_rot);
+    RTLR_CUDA(cudaGetLastError());
+    RTLR_CUDA(cudaMemcpyAsync(host_rotated, d_rot, sizeof(int), cudaMemcpyDeviceToHost, s));
+    RTLR_CUDA(cudaStreamSynchronize(s));
+    if (*host_rotated == 0) break;
+  }
+}
+
+}  // namespace cuda
+}  // namespace rtlr

@@ -1,0 +1,59 @@
+// Dense fp64 kernels of the low-rank path (K4-K11): tall-skinny GEMMs with
+// deterministic split-K, GEMV/dot/norm reductions, the transposed streaming
+// stencils for border extension, batched Galerkin LU solves, Householder
+// QR and one-sided Jacobi SVD.  All reductions use fixed partitions and
+// fixed summation orders (bitwise reproducible across runs).
+#pragma once
+
+#include "device.cuh"
+
+namespace rtlr {
+namespace cuda {
+
+// C[M x N] (ldc) = A^T B with A: K x M (lda), B: K x N (ldb), K large.
+// work >= splits * M * N doubles.  beta_add: C += result instead of C =.
+void gemm_tn(int M, int N, long long K, const double* A, long long lda, const double* B, long long ldb,
+             double* C, long long ldc, double* work, size_t work_doubles, cudaStream_t s);
+// C[M x N] (ldc) = A B with A: M x K (lda, M large), B: K x N (ldb), K small.
+void gemm_nn(long long M, int N, int K, const double* A, long long lda, const double* B, long long ldb,
+             double* C, long long ldc, cudaStream_t s);
+size_t gemm_tn_work(int M, int N, long long K);
+
+// out[i] = sum_k A[i, k] x[k] for A: n x k (lda) — accumulating into y (y += A x * alpha)
+void gemv_n(long long n, int k, const double* A, long long lda, const double* x, double alpha, double* y,
+            cudaStream_t s);
+
+// Deterministic dot products / norms: out = sum a*b (partials then fixed-order sum)
+void dot(long long n, const double* a, const double* b, double* work, double* out, cudaStream_t s);
+void scale_copy(long long n, const double* x, const double* h, double* y, cudaStream_t s);  // y = x / *h
+void axpy_dev(long long n, const double* alpha, double sign, const double* x, double* y, cudaStream_t s);
+
+// Transposed / plain streaming matrices on p columns (border extension):
+// W = [Dx^- P, (Dx^-)^T P, Dy^- P, (Dy^-)^T P, Sigma_t P], each N_x x p,
+// written at W + k*p*ldw.
+void stream_products(const StencilArgs& a, int p, const double* P, long long ldp, double* W, long long ldw,
+                     cudaStream_t s);
+
+// Batched Galerkin solves (low_rank.cpp:176-200): for each of m angles,
+// A_j = omx Px + omy Py + Pt (r x r, from the 5 projections with leading
+// dimension ldp), LU with partial pivoting, c_j = A_j^{-1} (prhs + extra_j).
+// sol: r x m (ldsol); extra optional r x m (Xt g_j).  flags[j] = 1 if the
+// solution is not finite.  work >= m * r * r doubles for r > kSmemLuMax.
+constexpr int kSmemLuMax = 96;
+void galerkin_batch(int r, int m, const int* angles, const double* dirs, const double* proj, long long ldp,
+                    long long proj_stride, const double* prhs, const double* extra, double* sol,
+                    long long ldsol, int* flags, double* work, cudaStream_t s);
+
+// Householder QR of an m x n (m >= n) column-major matrix (lda), in place;
+// tau (n).  Q formed explicitly into q (m x n).  r (n x n) upper.
+void householder_qr(long long m, int n, double* a, long long lda, double* tau, double* q, long long ldq,
+                    double* r, double* work, cudaStream_t s);
+
+// One-sided Jacobi on the columns of w (m x n, ld), accumulating the
+// rotations in v (n x n) when given.  Afterwards columns of w are mutually
+// orthogonal: w = U diag(s), s = column norms.
+void jacobi_svd(long long m, int n, double* w, long long ldw, double* v, int max_sweeps, int* host_rotated,
+                double* work, cudaStream_t s);
+
+}  // namespace cuda
+}  // namespace rtlr

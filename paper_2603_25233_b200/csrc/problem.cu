@@ -94,6 +94,7 @@ void Problem::upload() {
   std::memcpy(sc_.try_r, h.sc.try_r, sizeof sc_.try_r);
   std::memcpy(sc_.try_l, h.sc.try_l, sizeof sc_.try_l);
   dirs_.upload(h.dirs.data(), h.dirs.size(), s);
+  weights_.upload(h.weights.data(), h.weights.size(), s);
   sigma_t_.upload(h.sigma_t.data(), h.sigma_t.size(), s);
   sigma_s_.upload(h.sigma_s.data(), h.sigma_s.size(), s);
   source_.upload(h.source.data(), h.source.size(), s);

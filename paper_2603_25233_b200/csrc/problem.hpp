@@ -3,6 +3,7 @@
 #pragma once
 
 #include <memory>
+#include <utility>
 #include <string>
 #include <vector>
 
@@ -40,6 +41,10 @@ class DBuf {
   }
   T* get() const { return p_; }
   size_t size() const { return n_; }
+  void swap(DBuf& o) noexcept {
+    std::swap(p_, o.p_);
+    std::swap(n_, o.n_);
+  }
 
  private:
   T* p_ = nullptr;
@@ -145,7 +150,7 @@ class Problem {
   cudaStream_t stream_ = nullptr;
   bool own_stream_ = true;
   StreamDev sc_{};
-  DBuf<double> dirs_, sigma_t_, sigma_s_, source_, bc_, sip_, jac_;
+  DBuf<double> dirs_, weights_, sigma_t_, sigma_s_, source_, bc_, sip_, jac_;
   DBuf<int> err_, angle_idx_;
   DBuf<double> line_, norm_work_, pcg_vec_, pcg_part_, uniq_w_, scratch_;
   DBuf<PcgState> pcg_state_;

@@ -144,37 +144,9 @@ __device__ __forceinline__ bool invert4(const double* M, double* Minv) {
 
 #undef A_
 
-// Position of a lane in its warp's stream of (band, column) work items:
-// k-th band owned by this warp (band = w + k*W), column col (may be
-// negative during the initial skew, or >= nx in the padding of S).
-struct Pos {
-  int k, col;
-};
-
-__device__ __forceinline__ void advance(Pos& p, int S) {
-  if (++p.col == S) {
-    p.col = 0;
-    ++p.k;
-  }
-}
-
-struct Geo {
-  int nx, ny, nb, S, w, W, lane;
-  bool xu, yu;
-  // returns true and the cell index when the position is a real cell
-  __device__ __forceinline__ bool cell(const Pos& p, size_t& c, int& band) const {
-    band = w + p.k * W;
-    const int row = band * 32 + lane;
-    if (p.col < 0 || p.col >= nx || band >= nb || row >= ny) return false;
-    const int ca = xu ? p.col : nx - 1 - p.col;
-    const int cb = yu ? row : ny - 1 - row;
-    c = static_cast<size_t>(cb) * nx + ca;
-    return true;
-  }
-};
-
-constexpr int kPrefetch = 4;   // rhs cells in flight per lane
+constexpr int kPrefetch = 4;               // rhs cells in flight per lane
 constexpr int kLineSmemBudget = 96 * 1024;  // bytes of trace lines per block kept in smem
+constexpr int kPublish = 8;                 // columns per published progress update
 
 // Shared-memory load the compiler may not hoist out of the step loop (keeps
 // the per-direction 4x4 inverse out of the register file).
@@ -184,13 +156,15 @@ __device__ __forceinline__ double2 lds2(const double* p) {
   asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];" : "=d"(v.x), "=d"(v.y) : "r"(a));
   return v;
 }
+
 // Shared memory of one direction group (W warps).  Warp w hands the top
 // traces of each of its bands to warp (w+1) % W through a full-row trace
 // line (nx x 2 doubles, in smem when it fits, else in L2) plus a progress
 // counter: slot col of line w is only rewritten (band b+W) after warp w+1
 // read it for band b+1, because that rewrite depends on the read through
 // the upwind chain band b+1 -> ... -> b+W.  Readers therefore only wait for
-// data to be published; there are no space waits and no cycles.
+// data to be published; there are no space waits and no cycles.  With a
+// single warp per direction the line is the warp's own and needs no counter.
 struct GroupSmem {
   double* consts;      // 40: minv / dstream (16), kx ky tx ty (8), spare
   volatile int* prod;  // W: columns published by warp w's lane 31
@@ -202,7 +176,40 @@ __host__ __device__ constexpr int group_smem_doubles(int W, int nx, bool smem_li
   return 40 + 2 * ((W + 3) / 4) + (smem_lines ? W * nx * 2 : 0);
 }
 
-template <bool UNIFORM>
+// A lane's position in its warp's stream of work: the k-th band owned by
+// the warp (band = w + k W) and a column (negative during the initial lane
+// skew, >= nx in the padding up to S).  cell is linear in col, so it is
+// advanced incrementally and only recomputed at band changes.
+struct Stream {
+  long long cell;
+  int col, k, band;
+  bool rowok;
+};
+
+struct Walk {
+  int nx, ny, nb, S, w, W, lane, xs;
+  bool xu, yu;
+  __device__ __forceinline__ void seek(Stream& s, int k, int col) const {
+    s.k = k;
+    s.col = col;
+    s.band = w + k * W;
+    const int row = s.band * 32 + lane;
+    s.rowok = s.band < nb && row < ny;
+    const int cb = yu ? row : ny - 1 - row;
+    const int ca = xu ? col : nx - 1 - col;
+    s.cell = static_cast<long long>(cb) * nx + ca;
+  }
+  __device__ __forceinline__ void step(Stream& s) const {
+    ++s.col;
+    s.cell += xs;
+    if (s.col == S) seek(s, s.k + 1, 0);
+  }
+  __device__ __forceinline__ bool active(const Stream& s) const {
+    return s.rowok && s.col >= 0 && s.col < nx;
+  }
+};
+
+template <bool UNIFORM, bool MULTI>
 __global__ void __launch_bounds__(256, 2) sweep_kernel(const SweepArgs a, int W, bool smem_lines) {
   extern __shared__ double smem[];
   const int lane = threadIdx.x & 31;
@@ -256,82 +263,84 @@ __global__ void __launch_bounds__(256, 2) sweep_kernel(const SweepArgs a, int W,
   const double kx[2] = {cst[16], cst[17]}, tx[2] = {cst[18], cst[19]};
   const double ky[2] = {cst[20], cst[21]}, ty[2] = {cst[22], cst[23]};
 
-  Geo geo;
-  geo.nx = a.nx;
-  geo.ny = a.ny;
-  geo.nb = (a.ny + 31) >> 5;
-  geo.S = a.nx > 32 ? a.nx : 32;
-  geo.w = w;
-  geo.W = W;
-  geo.lane = lane;
-  geo.xu = xu;
-  geo.yu = yu;
-  const int S = geo.S, nx = a.nx;
-  const int kw = (w < geo.nb) ? (geo.nb - w + W - 1) / W : 0;  // bands of this warp
+  Walk walk;
+  walk.nx = a.nx;
+  walk.ny = a.ny;
+  walk.nb = (a.ny + 31) >> 5;
+  walk.S = a.nx > 32 ? a.nx : 32;
+  walk.w = w;
+  walk.W = W;
+  walk.lane = lane;
+  walk.xu = xu;
+  walk.yu = yu;
+  walk.xs = xu ? 1 : -1;
+  const int S = walk.S, nx = a.nx, nb = walk.nb;
+  const int kw = (w < nb) ? (nb - w + W - 1) / W : 0;  // bands of this warp
   const int total = kw * S + 31;
   const double* rhs = a.rhs + static_cast<long long>(slot) * a.rhs_stride;
   const double* bc = a.bc ? a.bc + static_cast<long long>(ang) * a.bc_stride : nullptr;
   double* psi = a.psi + static_cast<long long>(slot) * a.psi_stride;
   const int pw = (w + W - 1) % W;  // producer of our lane 0's traces
+  double* my_line = sm.lines + static_cast<size_t>(w) * nx * 2;
+  const double* in_line = sm.lines + static_cast<size_t>(pw) * nx * 2;
 
   // prefetch queue: rhs of steps t .. t+kPrefetch-1 (slot = step % kPrefetch)
   double q0[kPrefetch], q1[kPrefetch], q2[kPrefetch], q3[kPrefetch];
-  Pos cur{0, -lane}, pre{0, -lane};
+  Stream cur, pre;
+  walk.seek(cur, 0, -lane);
+  walk.seek(pre, 0, -lane);
 #pragma unroll
   for (int s = 0; s < kPrefetch; ++s) {
-    size_t c;
-    int band;
     q0[s] = q1[s] = q2[s] = q3[s] = 0.0;
-    if (geo.cell(pre, c, band)) {
+    if (walk.active(pre)) {
       double v[4];
-      ld_cell_stream(rhs + 4 * c, v);
+      ld_cell_stream(rhs + 4 * pre.cell, v);
       q0[s] = v[0];
       q1[s] = v[1];
       q2[s] = v[2];
       q3[s] = v[3];
     }
-    advance(pre, S);
+    walk.step(pre);
   }
 
   double txi0 = 0.0, txi1 = 0.0;  // x traces of the previous cell in the row
   double tyo0 = 0.0, tyo1 = 0.0;  // y traces produced last step
+  int seen = 0;                   // MULTI: producer progress already observed by lane 0
   for (int t0 = 0; t0 < total; t0 += kPrefetch) {
 #pragma unroll
     for (int s = 0; s < kPrefetch; ++s) {
       if (t0 + s >= total) break;  // warp-uniform
       double v[4] = {q0[s], q1[s], q2[s], q3[s]};
       // refill this queue slot with the step kPrefetch ahead
-      {
-        size_t c;
-        int band;
-        q0[s] = q1[s] = q2[s] = q3[s] = 0.0;
-        if (geo.cell(pre, c, band)) {
-          double u[4];
-          ld_cell_stream(rhs + 4 * c, u);
-          q0[s] = u[0];
-          q1[s] = u[1];
-          q2[s] = u[2];
-          q3[s] = u[3];
-        }
-        advance(pre, S);
+      if (walk.active(pre)) {
+        double u[4];
+        ld_cell_stream(rhs + 4 * pre.cell, u);
+        q0[s] = u[0];
+        q1[s] = u[1];
+        q2[s] = u[2];
+        q3[s] = u[3];
       }
+      walk.step(pre);
       double yi0 = __shfl_up_sync(0xffffffffu, tyo0, 1);
       double yi1 = __shfl_up_sync(0xffffffffu, tyo1, 1);
       tyo0 = 0.0;
       tyo1 = 0.0;
-      size_t cell;
-      int band;
-      if (geo.cell(cur, cell, band)) {
-        const int col = cur.col;
+      const bool act = walk.active(cur);
+      const int col = cur.col;
+      if (act) {
         if (lane == 0) {
-          if (band == 0) {
+          if (cur.band == 0) {
             yi0 = yi1 = 0.0;
           } else {
             // traces of band-1, column col, from the producer warp's line
-            const int gidx = ((band - 1 - pw) / W) * nx + col;
-            while (sm.prod[pw] <= gidx) __nanosleep(20);
-            __threadfence_block();
-            const double* r = sm.lines + (static_cast<size_t>(pw) * nx + col) * 2;
+            if (MULTI) {
+              const int gidx = ((cur.band - 1 - pw) / W) * nx + col;
+              if (seen <= gidx) {
+                while ((seen = sm.prod[pw]) <= gidx) __nanosleep(20);
+                __threadfence_block();
+              }
+            }
+            const double* r = in_line + 2 * col;
             if (smem_lines) {
               yi0 = r[0];
               yi1 = r[1];
@@ -347,7 +356,7 @@ __global__ void __launch_bounds__(256, 2) sweep_kernel(const SweepArgs a, int W,
         }
         if (bc) {
           double gb[4];
-          ld_cell(bc + 4 * cell, gb);
+          ld_cell(bc + 4 * cur.cell, gb);
 #pragma unroll
           for (int k = 0; k < 4; ++k) v[k] += gb[k];
         }
@@ -373,7 +382,7 @@ __global__ void __launch_bounds__(256, 2) sweep_kernel(const SweepArgs a, int W,
           }
         } else {
           double A[16];
-          const double2* sb = reinterpret_cast<const double2*>(a.sigma_t + 16 * cell);
+          const double2* sb = reinterpret_cast<const double2*>(a.sigma_t + 16 * cur.cell);
 #pragma unroll
           for (int k = 0; k < 8; ++k) {
             const double2 s2 = __ldg(sb + k);
@@ -384,16 +393,15 @@ __global__ void __launch_bounds__(256, 2) sweep_kernel(const SweepArgs a, int W,
 #pragma unroll
           for (int r = 0; r < 4; ++r) p[r] = v[r];
         }
-        st_cell(psi + 4 * cell, p);
+        st_cell(psi + 4 * cur.cell, p);
         // outflow traces: x (per y-mode) for the next cell of this row,
         // y (per x-mode) for the row above (next lane / next band).
         txi0 = tx[0] * p[0] + tx[1] * p[1];
         txi1 = tx[0] * p[2] + tx[1] * p[3];
         tyo0 = ty[0] * p[0] + ty[1] * p[2];
         tyo1 = ty[0] * p[1] + ty[1] * p[3];
-        if (lane == 31 && band + 1 < geo.nb) {
-          const int gidx = ((band - w) / W) * nx + col;
-          double* r = sm.lines + (static_cast<size_t>(w) * nx + col) * 2;
+        if (lane == 31 && cur.band + 1 < nb) {
+          double* r = my_line + 2 * col;
           if (smem_lines) {
             r[0] = tyo0;
             r[1] = tyo1;
@@ -401,15 +409,50 @@ __global__ void __launch_bounds__(256, 2) sweep_kernel(const SweepArgs a, int W,
             __stcg(r, tyo0);
             __stcg(r + 1, tyo1);
           }
-          __threadfence_block();
-          sm.prod[w] = gidx + 1;
+          if (MULTI && ((col + 1) % kPublish == 0 || col + 1 == nx)) {
+            __threadfence_block();
+            sm.prod[w] = ((cur.band - w) / W) * nx + col + 1;
+          }
         }
       }
       __syncwarp();
-      advance(cur, S);
+      walk.step(cur);
     }
   }
 }
+
+// Handoff is deadlock free only when a band row is longer than the lane
+// skew of the warp chain: warp j at step t needs warp j-1 past step t+32
+// (plus the publish granularity), and warp 0's next band needs warp W-1.
+__host__ __device__ constexpr bool multi_ok(int W, int S) { return 32 * W + 2 * kPublish < S; }
+
+}  // namespace
+
+void launch_sweep(const SweepArgs& a, bool uniform, cudaStream_t s) {
+  if (a.n <= 0) return;
+  // Warps per direction: enough concurrent warps to fill 148 SMs x 16, at
+  // most one per 32-row band, at most 8, and within the deadlock bound.
+  const int nb = (a.ny + 31) / 32;
+  const int S = a.nx > 32 ? a.nx : 32;
+  int W = 1;
+  while (W < 8 && static_cast<long long>(a.n) * W * 2 <= 148 * 16 && 2 * W <= nb && multi_ok(2 * W, S)) W *= 2;
+  const int warps_per_block = 8;
+  const int groups = warps_per_block / W;
+  const int blocks = (a.n + groups - 1) / groups;
+  const bool smem_lines = static_cast<size_t>(8) * a.nx * 2 * sizeof(double) <= kLineSmemBudget;
+  const size_t smem = static_cast<size_t>(groups) * group_smem_doubles(W, a.nx, smem_lines) * sizeof(double);
+  auto go = [&](auto kern) {
+    RTLR_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+    kern<<<blocks, warps_per_block * 32, smem, s>>>(a, W, smem_lines);
+  };
+  if (uniform)
+    W > 1 ? go(sweep_kernel<true, true>) : go(sweep_kernel<true, false>);
+  else
+    W > 1 ? go(sweep_kernel<false, true>) : go(sweep_kernel<false, false>);
+  RTLR_CUDA(cudaGetLastError());
+}
+
+namespace {
 
 __device__ __forceinline__ double c5u(std::uint64_t seed, std::uint64_t counter) {
   std::uint64_t z = counter * 0x9E3779B97F4A7C15ull + seed;
@@ -426,32 +469,6 @@ __global__ void c5_fill_kernel(double* rhs, long long total, long long base, std
 }
 
 }  // namespace
-
-void launch_sweep(const SweepArgs& a, bool uniform, cudaStream_t s) {
-  if (a.n <= 0) return;
-  // Warps per direction: enough concurrent warps to fill 148 SMs x 16, at
-  // most one per 32-row band, at most 8.
-  const int nb = (a.ny + 31) / 32;
-  // Deadlock-free only when a band row is longer than the lane skew of the
-  // whole warp chain: S > 32 W (warp j at step t needs warp j-1 past step
-  // t + 32; warp 0's next band needs warp W-1, i.e. itself 32 W steps back).
-  const int S = a.nx > 32 ? a.nx : 32;
-  int W = 1;
-  while (W < 8 && static_cast<long long>(a.n) * W * 2 <= 148 * 16 && 2 * W <= nb && 32 * (2 * W) < S) W *= 2;
-  const int warps_per_block = 8;
-  const int groups = warps_per_block / W;
-  const int blocks = (a.n + groups - 1) / groups;
-  const bool smem_lines = static_cast<size_t>(8) * a.nx * 2 * sizeof(double) <= kLineSmemBudget;
-  const size_t smem = static_cast<size_t>(groups) * group_smem_doubles(W, a.nx, smem_lines) * sizeof(double);
-  if (uniform) {
-    RTLR_CUDA(cudaFuncSetAttribute(sweep_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
-    sweep_kernel<true><<<blocks, warps_per_block * 32, smem, s>>>(a, W, smem_lines);
-  } else {
-    RTLR_CUDA(cudaFuncSetAttribute(sweep_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
-    sweep_kernel<false><<<blocks, warps_per_block * 32, smem, s>>>(a, W, smem_lines);
-  }
-  RTLR_CUDA(cudaGetLastError());
-}
 
 void launch_c5_fill(double* rhs, long long n_dirs, long long dir0, long long ndof, std::uint64_t seed,
                     cudaStream_t s) {
