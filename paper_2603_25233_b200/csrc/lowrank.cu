@@ -14,6 +14,9 @@
 #include <cmath>
 #include <cstring>
 #include <numeric>
+#include <cstdlib>
+#include <cstdio>
+#include <string>
 
 #include "dense.cuh"
 #include "problem.hpp"
@@ -135,6 +138,33 @@ struct DMat {
   double* col(int j) const { return buf.get() + static_cast<size_t>(ld) * j; }
 };
 
+// Per-phase wall-clock accounting (RTLR_PROFILE=1): synchronizes the stream
+// at phase boundaries, so it is off by default.
+struct PhaseTimer {
+  bool on = false;
+  cudaStream_t s = nullptr;
+  std::vector<std::pair<std::string, double>> acc;
+  std::chrono::steady_clock::time_point t0;
+  std::string cur;
+  void start(const char* name) {
+    if (!on) return;
+    RTLR_CUDA(cudaStreamSynchronize(s));
+    t0 = std::chrono::steady_clock::now();
+    cur = name;
+  }
+  void stop() {
+    if (!on) return;
+    RTLR_CUDA(cudaStreamSynchronize(s));
+    const double dt = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+    for (auto& e : acc)
+      if (e.first == cur) {
+        e.second += dt;
+        return;
+      }
+    acc.push_back({cur, dt});
+  }
+};
+
 }  // namespace
 
 struct InnerResult {
@@ -162,8 +192,12 @@ class LowRankEngine {
     dirs_ = P.dirs_.get();
     sa_ = StencilArgs{hp_.nx, hp_.ny, hp_.ncell, P.sigma_t_.get(), P.sc_};
     RTLR_CUDA(cudaMallocHost(&hbuf_, 64 * sizeof(double)));
+    const char* e = std::getenv("RTLR_PROFILE");
+    pt_.on = e && e[0] == '1';
+    pt_.s = s_;
   }
   ~LowRankEngine() { cudaFreeHost(hbuf_); }
+  PhaseTimer pt_;
 
   InnerResult inner(const double* d_phi_prev, SubsampleRng& rng);
   int rank() const { return rank_; }
@@ -468,14 +502,20 @@ InnerResult LowRankEngine::inner(const double* d_phi_prev, SubsampleRng& rng) {
     const int p_now = static_cast<int>(next.size());
     double* S = snaps_.ensure(static_cast<size_t>(n_) * p_now);
     int* d_next = upload_ints(ang2_, next);
+    pt_.start("sweep");
     P_.sweep(d_next, p_now, rhs_core_.get(), 0, S, n_);
     P_.check_error();
+    pt_.stop();
     for (int j : next) {
       sampled[j] = 1;
       out.sampled_order.push_back(j);
     }
+    pt_.start("cgs");
     const bool reorth = mgs_ro_update(S, next);
+    pt_.stop();
+    pt_.start("projections");
     update_projections(reorth);
+    pt_.stop();
     if (reorth) ++out.reorthogonalizations;
     const bool any_unsampled = std::any_of(sampled.begin(), sampled.end(), [](char c) { return !c; });
     if (!any_unsampled) {
@@ -491,8 +531,12 @@ InnerResult LowRankEngine::inner(const double* d_phi_prev, SubsampleRng& rng) {
     std::vector<int> cands = rng.sample_without_replacement(std::move(pool), prm_.q);
     const int m = static_cast<int>(cands.size());
     double* csol = cand_.ensure(static_cast<size_t>(rank_) * m);
+    pt_.start("galerkin_q");
     galerkin(cands, csol, rank_);
+    pt_.stop();
+    pt_.start("residual_q");
     std::vector<double> norms = residual_norms(cands, csol, rank_);
+    pt_.stop();
     std::vector<int> order(m);
     std::iota(order.begin(), order.end(), 0);
     std::sort(order.begin(), order.end(), [&](int a, int b) {
@@ -504,8 +548,10 @@ InnerResult LowRankEngine::inner(const double* d_phi_prev, SubsampleRng& rng) {
     for (int i = 0; i < std::min(prm_.p, m); ++i) next.push_back(cands[order[i]]);
 
     if (max_residual < prm_.eps_res) {
+      pt_.start("build_C");
       build_full_coefficients(&cands, csol);
       phi_from_C();
+      pt_.stop();
       // ||phi - phi_old||_2
       double* w = work(2 * kNormParts + 8);
       diff_norms(static_cast<int>(n_), phi_.get(), phi_old_.get(), w, w + 2 * kNormParts, s_);
@@ -520,7 +566,9 @@ InnerResult LowRankEngine::inner(const double* d_phi_prev, SubsampleRng& rng) {
         int* du = upload_ints(ang2_, unsampled);
         gather_cols<<<g1(static_cast<long long>(rank_) * unsampled.size()), 256, 0, s_>>>(
             rank_, static_cast<int>(unsampled.size()), du, C_.get(), rank_, Cu, rank_);
+        pt_.start("verify");
         std::vector<double> vn = residual_norms(unsampled, Cu, rank_);
+        pt_.stop();
         std::vector<std::pair<double, int>> outstanding;
         for (size_t i = 0; i < unsampled.size(); ++i)
           if (vn[i] >= prm_.eps_res) outstanding.push_back({vn[i], unsampled[i]});
@@ -631,7 +679,9 @@ SolveReport Problem::solve_low_rank(const LowRankOptions& o) {
   int final_rank = 0;
   for (int it = 1; it <= o.max_iterations; ++it) {
     inner = eng.inner(phi, rng);
+    eng.pt_.start("svd");
     const std::vector<double> sv = eng.svd(false, 0, nullptr, nullptr);
+    eng.pt_.stop();
     const int rp = truncation_rank(sv, o.inner.eps_svd);
     diff_norms(static_cast<int>(n), eng.phi(), phi, norm_work_.get(), norm_work_.get() + 2 * kNormParts, stream_);
     RTLR_CUDA(cudaMemcpyAsync(h_pin_, norm_work_.get() + 2 * kNormParts, 2 * sizeof(double), cudaMemcpyDeviceToHost,
@@ -655,8 +705,10 @@ SolveReport Problem::solve_low_rank(const LowRankOptions& o) {
       break;
     }
     if (o.use_dsa) {
+      eng.pt_.start("dsa");
       rec.dsa_iterations = dsa_correct(eng.phi(), phi, delta);
       vadd(static_cast<int>(n), eng.phi(), delta, phi, stream_);
+      eng.pt_.stop();
     } else {
       RTLR_CUDA(cudaMemcpyAsync(phi, eng.phi(), n * sizeof(double), cudaMemcpyDeviceToDevice, stream_));
     }
@@ -664,6 +716,11 @@ SolveReport Problem::solve_low_rank(const LowRankOptions& o) {
   }
   if (!rep.converged)
     RTLR_CUDA(cudaMemcpyAsync(phi, eng.phi(), n * sizeof(double), cudaMemcpyDeviceToDevice, stream_));
+  if (eng.pt_.on) {
+    std::fprintf(stderr, "[rtlr profile] low-rank phases (s):");
+    for (auto& e : eng.pt_.acc) std::fprintf(stderr, " %s=%.4f", e.first.c_str(), e.second);
+    std::fprintf(stderr, "\n");
+  }
   rep.phi.resize(n);
   RTLR_CUDA(cudaMemcpyAsync(rep.phi.data(), phi, n * sizeof(double), cudaMemcpyDeviceToHost, stream_));
   RTLR_CUDA(cudaStreamSynchronize(stream_));

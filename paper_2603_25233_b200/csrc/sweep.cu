@@ -144,9 +144,25 @@ __device__ __forceinline__ bool invert4(const double* M, double* Minv) {
 
 #undef A_
 
-constexpr int kPrefetch = 4;               // rhs cells in flight per lane
-constexpr int kLineSmemBudget = 96 * 1024;  // bytes of trace lines per block kept in smem
-constexpr int kPublish = 8;                 // columns per published progress update
+constexpr int kPrefetch = 6;               // rhs cells in flight per lane (smem queue)
+
+// Source cells stream through a per-warp shared-memory queue filled with
+// cp.async: in-flight data costs no registers and the wait is explicit.
+__device__ __forceinline__ void cp_cell_async(double* dst_smem, const double* src) {
+  const unsigned d = static_cast<unsigned>(__cvta_generic_to_shared(dst_smem));
+  asm volatile(
+      "cp.async.cg.shared.global.L2::256B [%0], [%1], 16;\n\t"
+      "cp.async.cg.shared.global.L2::256B [%2], [%3], 16;\n\t"
+      "cp.async.commit_group;" ::"r"(d),
+      "l"(src), "r"(d + 16), "l"(src + 2)
+      : "memory");
+}
+template <int N>
+__device__ __forceinline__ void cp_wait() {
+  asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
+}
+constexpr int kLineSmemBudget = 64 * 1024;  // bytes of trace lines per block kept in smem
+constexpr int kPublish = 2;                 // columns per published progress update
 
 // Shared-memory load the compiler may not hoist out of the step loop (keeps
 // the per-direction 4x4 inverse out of the register file).
@@ -155,6 +171,14 @@ __device__ __forceinline__ double2 lds2(const double* p) {
   const unsigned a = static_cast<unsigned>(__cvta_generic_to_shared(p));
   asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];" : "=d"(v.x), "=d"(v.y) : "r"(a));
   return v;
+}
+
+__device__ __forceinline__ void lds_cell(const double* p, double v[4]) {
+  const double2 a = lds2(p), b = lds2(p + 2);
+  v[0] = a.x;
+  v[1] = a.y;
+  v[2] = b.x;
+  v[3] = b.y;
 }
 
 // Shared memory of one direction group (W warps).  Warp w hands the top
@@ -218,9 +242,12 @@ __global__ void __launch_bounds__(256, 2) sweep_kernel(const SweepArgs a, int W,
   const int g = wib / W, w = wib % W;
   const int slot = blockIdx.x * groups + g;
   if (slot >= a.n || g >= groups) return;  // a whole direction group exits together
+  // per-warp source queue: kPrefetch slots x 32 lanes x 4 doubles
+  double* queue = smem + static_cast<size_t>(wib) * kPrefetch * 32 * 4 + static_cast<size_t>(lane) * 4;
   GroupSmem sm;
   {
-    double* base = smem + static_cast<size_t>(g) * group_smem_doubles(W, a.nx, smem_lines);
+    double* base = smem + static_cast<size_t>(blockDim.x >> 5) * kPrefetch * 32 * 4 +
+                   static_cast<size_t>(g) * group_smem_doubles(W, a.nx, smem_lines);
     sm.consts = base;
     sm.prod = reinterpret_cast<int*>(base + 40);
     sm.lines = smem_lines ? base + 40 + 2 * ((W + 3) / 4) : a.line + static_cast<size_t>(slot) * W * a.nx * 2;
@@ -284,22 +311,14 @@ __global__ void __launch_bounds__(256, 2) sweep_kernel(const SweepArgs a, int W,
   double* my_line = sm.lines + static_cast<size_t>(w) * nx * 2;
   const double* in_line = sm.lines + static_cast<size_t>(pw) * nx * 2;
 
-  // prefetch queue: rhs of steps t .. t+kPrefetch-1 (slot = step % kPrefetch)
-  double q0[kPrefetch], q1[kPrefetch], q2[kPrefetch], q3[kPrefetch];
+  // prefetch queue: rhs of steps t .. t+kPrefetch-1 (slot = step % kPrefetch).
+  // Idle positions load a valid dummy cell (never consumed).
   Stream cur, pre;
   walk.seek(cur, 0, -lane);
   walk.seek(pre, 0, -lane);
 #pragma unroll
   for (int s = 0; s < kPrefetch; ++s) {
-    q0[s] = q1[s] = q2[s] = q3[s] = 0.0;
-    if (walk.active(pre)) {
-      double v[4];
-      ld_cell_stream(rhs + 4 * pre.cell, v);
-      q0[s] = v[0];
-      q1[s] = v[1];
-      q2[s] = v[2];
-      q3[s] = v[3];
-    }
+    cp_cell_async(queue + s * 128, rhs + (walk.active(pre) ? 4 * pre.cell : 0));
     walk.step(pre);
   }
 
@@ -310,16 +329,12 @@ __global__ void __launch_bounds__(256, 2) sweep_kernel(const SweepArgs a, int W,
 #pragma unroll
     for (int s = 0; s < kPrefetch; ++s) {
       if (t0 + s >= total) break;  // warp-uniform
-      double v[4] = {q0[s], q1[s], q2[s], q3[s]};
+      // the oldest of kPrefetch groups (this step's cell) has landed
+      cp_wait<kPrefetch - 1>();
+      double v[4];
+      lds_cell(queue + s * 128, v);
       // refill this queue slot with the step kPrefetch ahead
-      if (walk.active(pre)) {
-        double u[4];
-        ld_cell_stream(rhs + 4 * pre.cell, u);
-        q0[s] = u[0];
-        q1[s] = u[1];
-        q2[s] = u[2];
-        q3[s] = u[3];
-      }
+      cp_cell_async(queue + s * 128, rhs + (walk.active(pre) ? 4 * pre.cell : 0));
       walk.step(pre);
       double yi0 = __shfl_up_sync(0xffffffffu, tyo0, 1);
       double yi1 = __shfl_up_sync(0xffffffffu, tyo1, 1);
@@ -336,7 +351,8 @@ __global__ void __launch_bounds__(256, 2) sweep_kernel(const SweepArgs a, int W,
             if (MULTI) {
               const int gidx = ((cur.band - 1 - pw) / W) * nx + col;
               if (seen <= gidx) {
-                while ((seen = sm.prod[pw]) <= gidx) __nanosleep(20);
+                while ((seen = sm.prod[pw]) <= gidx) {
+                }
                 __threadfence_block();
               }
             }
@@ -419,6 +435,7 @@ __global__ void __launch_bounds__(256, 2) sweep_kernel(const SweepArgs a, int W,
       walk.step(cur);
     }
   }
+  cp_wait<0>();
 }
 
 // Handoff is deadlock free only when a band row is longer than the lane
@@ -440,7 +457,9 @@ void launch_sweep(const SweepArgs& a, bool uniform, cudaStream_t s) {
   const int groups = warps_per_block / W;
   const int blocks = (a.n + groups - 1) / groups;
   const bool smem_lines = static_cast<size_t>(8) * a.nx * 2 * sizeof(double) <= kLineSmemBudget;
-  const size_t smem = static_cast<size_t>(groups) * group_smem_doubles(W, a.nx, smem_lines) * sizeof(double);
+  const size_t smem = (static_cast<size_t>(warps_per_block) * kPrefetch * 32 * 4 +
+                      static_cast<size_t>(groups) * group_smem_doubles(W, a.nx, smem_lines)) *
+                     sizeof(double);
   auto go = [&](auto kern) {
     RTLR_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
     kern<<<blocks, warps_per_block * 32, smem, s>>>(a, W, smem_lines);
