@@ -144,7 +144,11 @@ __device__ __forceinline__ bool invert4(const double* M, double* Minv) {
 
 #undef A_
 
-constexpr int kPrefetch = 6;               // rhs cells in flight per lane (smem queue)
+// rhs cells in flight per lane (smem queue): deeper for the single-warp
+// throughput kernel, shallower when trace lines share the smem budget.
+template <bool MULTI>
+__host__ __device__ constexpr int prefetch_depth() { return MULTI ? 4 : 8; }
+constexpr int kQueueSlotDoubles = 32 * 4 + 2;  // 32 lanes x one cell + the lane-0 trace pair
 
 // Source cells stream through a per-warp shared-memory queue filled with
 // cp.async: in-flight data costs no registers and the wait is explicit.
@@ -152,11 +156,15 @@ __device__ __forceinline__ void cp_cell_async(double* dst_smem, const double* sr
   const unsigned d = static_cast<unsigned>(__cvta_generic_to_shared(dst_smem));
   asm volatile(
       "cp.async.cg.shared.global.L2::256B [%0], [%1], 16;\n\t"
-      "cp.async.cg.shared.global.L2::256B [%2], [%3], 16;\n\t"
-      "cp.async.commit_group;" ::"r"(d),
+      "cp.async.cg.shared.global.L2::256B [%2], [%3], 16;" ::"r"(d),
       "l"(src), "r"(d + 16), "l"(src + 2)
       : "memory");
 }
+__device__ __forceinline__ void cp16_async(double* dst_smem, const double* src) {
+  const unsigned d = static_cast<unsigned>(__cvta_generic_to_shared(dst_smem));
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(d), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
 template <int N>
 __device__ __forceinline__ void cp_wait() {
   asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
@@ -233,8 +241,9 @@ struct Walk {
   }
 };
 
-template <bool UNIFORM, bool MULTI>
+template <bool UNIFORM, bool MULTI, bool HAS_BC>
 __global__ void __launch_bounds__(256, 2) sweep_kernel(const SweepArgs a, int W, bool smem_lines) {
+  constexpr int kPrefetch = prefetch_depth<MULTI>();
   extern __shared__ double smem[];
   const int lane = threadIdx.x & 31;
   const int wib = threadIdx.x >> 5;
@@ -242,11 +251,12 @@ __global__ void __launch_bounds__(256, 2) sweep_kernel(const SweepArgs a, int W,
   const int g = wib / W, w = wib % W;
   const int slot = blockIdx.x * groups + g;
   if (slot >= a.n || g >= groups) return;  // a whole direction group exits together
-  // per-warp source queue: kPrefetch slots x 32 lanes x 4 doubles
-  double* queue = smem + static_cast<size_t>(wib) * kPrefetch * 32 * 4 + static_cast<size_t>(lane) * 4;
+  // per-warp source queue: kPrefetch slots x (32 lanes x 4 doubles + 2)
+  double* wqueue = smem + static_cast<size_t>(wib) * kPrefetch * kQueueSlotDoubles;
+  double* queue = wqueue + static_cast<size_t>(lane) * 4;
   GroupSmem sm;
   {
-    double* base = smem + static_cast<size_t>(blockDim.x >> 5) * kPrefetch * 32 * 4 +
+    double* base = smem + static_cast<size_t>(blockDim.x >> 5) * kPrefetch * kQueueSlotDoubles +
                    static_cast<size_t>(g) * group_smem_doubles(W, a.nx, smem_lines);
     sm.consts = base;
     sm.prod = reinterpret_cast<int*>(base + 40);
@@ -305,11 +315,14 @@ __global__ void __launch_bounds__(256, 2) sweep_kernel(const SweepArgs a, int W,
   const int kw = (w < nb) ? (nb - w + W - 1) / W : 0;  // bands of this warp
   const int total = kw * S + 31;
   const double* rhs = a.rhs + static_cast<long long>(slot) * a.rhs_stride;
-  const double* bc = a.bc ? a.bc + static_cast<long long>(ang) * a.bc_stride : nullptr;
+  const double* bc = HAS_BC ? a.bc + static_cast<long long>(ang) * a.bc_stride : nullptr;
   double* psi = a.psi + static_cast<long long>(slot) * a.psi_stride;
   const int pw = (w + W - 1) % W;  // producer of our lane 0's traces
   double* my_line = sm.lines + static_cast<size_t>(w) * nx * 2;
   const double* in_line = sm.lines + static_cast<size_t>(pw) * nx * 2;
+  // single warp: lane 0's traces (written by its own lane 31, S-31 steps
+  // earlier) ride in the same cp.async group as the source cell
+  const bool line_pf = !MULTI && (S - 31 > kPrefetch);
 
   // prefetch queue: rhs of steps t .. t+kPrefetch-1 (slot = step % kPrefetch).
   // Idle positions load a valid dummy cell (never consumed).
@@ -318,7 +331,10 @@ __global__ void __launch_bounds__(256, 2) sweep_kernel(const SweepArgs a, int W,
   walk.seek(pre, 0, -lane);
 #pragma unroll
   for (int s = 0; s < kPrefetch; ++s) {
-    cp_cell_async(queue + s * 128, rhs + (walk.active(pre) ? 4 * pre.cell : 0));
+    cp_cell_async(queue + s * kQueueSlotDoubles, rhs + (walk.active(pre) ? 4 * pre.cell : 0));
+    if (line_pf && lane == 0 && walk.active(pre) && pre.band > 0)
+      cp16_async(wqueue + s * kQueueSlotDoubles + 128, in_line + 2 * pre.col);
+    cp_commit();
     walk.step(pre);
   }
 
@@ -332,9 +348,15 @@ __global__ void __launch_bounds__(256, 2) sweep_kernel(const SweepArgs a, int W,
       // the oldest of kPrefetch groups (this step's cell) has landed
       cp_wait<kPrefetch - 1>();
       double v[4];
-      lds_cell(queue + s * 128, v);
+      lds_cell(queue + s * kQueueSlotDoubles, v);
+      double2 lq = make_double2(0.0, 0.0);
+      if (line_pf && lane == 0) lq = lds2(wqueue + s * kQueueSlotDoubles + 128);
+      __syncwarp();
       // refill this queue slot with the step kPrefetch ahead
-      cp_cell_async(queue + s * 128, rhs + (walk.active(pre) ? 4 * pre.cell : 0));
+      cp_cell_async(queue + s * kQueueSlotDoubles, rhs + (walk.active(pre) ? 4 * pre.cell : 0));
+      if (line_pf && lane == 0 && walk.active(pre) && pre.band > 0)
+        cp16_async(wqueue + s * kQueueSlotDoubles + 128, in_line + 2 * pre.col);
+      cp_commit();
       walk.step(pre);
       double yi0 = __shfl_up_sync(0xffffffffu, tyo0, 1);
       double yi1 = __shfl_up_sync(0xffffffffu, tyo1, 1);
@@ -357,7 +379,10 @@ __global__ void __launch_bounds__(256, 2) sweep_kernel(const SweepArgs a, int W,
               }
             }
             const double* r = in_line + 2 * col;
-            if (smem_lines) {
+            if (line_pf) {
+              yi0 = lq.x;
+              yi1 = lq.y;
+            } else if (smem_lines) {
               yi0 = r[0];
               yi1 = r[1];
             } else {
@@ -370,7 +395,7 @@ __global__ void __launch_bounds__(256, 2) sweep_kernel(const SweepArgs a, int W,
           txi0 = 0.0;
           txi1 = 0.0;
         }
-        if (bc) {
+        if (HAS_BC) {
           double gb[4];
           ld_cell(bc + 4 * cur.cell, gb);
 #pragma unroll
@@ -456,18 +481,29 @@ void launch_sweep(const SweepArgs& a, bool uniform, cudaStream_t s) {
   const int warps_per_block = 8;
   const int groups = warps_per_block / W;
   const int blocks = (a.n + groups - 1) / groups;
-  const bool smem_lines = static_cast<size_t>(8) * a.nx * 2 * sizeof(double) <= kLineSmemBudget;
-  const size_t smem = (static_cast<size_t>(warps_per_block) * kPrefetch * 32 * 4 +
-                      static_cast<size_t>(groups) * group_smem_doubles(W, a.nx, smem_lines)) *
-                     sizeof(double);
+  // W == 1 keeps its trace line in L2 (prefetched through the queue);
+  // multi-warp groups share lines in smem when they fit.
+  const bool smem_lines = W > 1 && static_cast<size_t>(8) * a.nx * 2 * sizeof(double) <= kLineSmemBudget;
+  const int pf = W > 1 ? prefetch_depth<true>() : prefetch_depth<false>();
+  const size_t smem = (static_cast<size_t>(warps_per_block) * pf * kQueueSlotDoubles +
+                       static_cast<size_t>(groups) * group_smem_doubles(W, a.nx, smem_lines)) *
+                      sizeof(double);
   auto go = [&](auto kern) {
     RTLR_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
     kern<<<blocks, warps_per_block * 32, smem, s>>>(a, W, smem_lines);
   };
-  if (uniform)
-    W > 1 ? go(sweep_kernel<true, true>) : go(sweep_kernel<true, false>);
-  else
-    W > 1 ? go(sweep_kernel<false, true>) : go(sweep_kernel<false, false>);
+  const bool bc = a.bc != nullptr;
+  if (uniform) {
+    if (W > 1)
+      bc ? go(sweep_kernel<true, true, true>) : go(sweep_kernel<true, true, false>);
+    else
+      bc ? go(sweep_kernel<true, false, true>) : go(sweep_kernel<true, false, false>);
+  } else {
+    if (W > 1)
+      bc ? go(sweep_kernel<false, true, true>) : go(sweep_kernel<false, true, false>);
+    else
+      bc ? go(sweep_kernel<false, false, true>) : go(sweep_kernel<false, false, false>);
+  }
   RTLR_CUDA(cudaGetLastError());
 }
 
