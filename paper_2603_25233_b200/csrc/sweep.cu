@@ -152,17 +152,26 @@ constexpr int kQueueSlotDoubles = 32 * 4 + 2;  // 32 lanes x one cell + the lane
 
 // Source cells stream through a per-warp shared-memory queue filled with
 // cp.async: in-flight data costs no registers and the wait is explicit.
+// dst: this lane's slot entry; the two 16-byte halves of the cell go 512
+// bytes apart so a warp's LDS.128 / smem fill is contiguous (no conflicts)
 __device__ __forceinline__ void cp_cell_async(double* dst_smem, const double* src) {
   const unsigned d = static_cast<unsigned>(__cvta_generic_to_shared(dst_smem));
   asm volatile(
       "cp.async.cg.shared.global.L2::256B [%0], [%1], 16;\n\t"
       "cp.async.cg.shared.global.L2::256B [%2], [%3], 16;" ::"r"(d),
-      "l"(src), "r"(d + 16), "l"(src + 2)
+      "l"(src), "r"(d + 512), "l"(src + 2)
       : "memory");
 }
 __device__ __forceinline__ void cp16_async(double* dst_smem, const double* src) {
   const unsigned d = static_cast<unsigned>(__cvta_generic_to_shared(dst_smem));
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(d), "l"(src) : "memory");
+}
+__device__ __forceinline__ void st_cell256(double* p, const double v[4]) {
+  // one 32-byte cell per lane per instruction (STG.E.ENL2.256): lanes walk
+  // different rows, so L1TEX wavefronts per warp store halve vs 2 x 128-bit
+  asm volatile("st.global.cs.v4.f64 [%0], {%1, %2, %3, %4};" ::"l"(p), "d"(v[0]), "d"(v[1]), "d"(v[2]),
+               "d"(v[3])
+               : "memory");
 }
 __device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
 template <int N>
@@ -182,7 +191,7 @@ __device__ __forceinline__ double2 lds2(const double* p) {
 }
 
 __device__ __forceinline__ void lds_cell(const double* p, double v[4]) {
-  const double2 a = lds2(p), b = lds2(p + 2);
+  const double2 a = lds2(p), b = lds2(p + 64);
   v[0] = a.x;
   v[1] = a.y;
   v[2] = b.x;
@@ -253,7 +262,7 @@ __global__ void __launch_bounds__(256, 2) sweep_kernel(const SweepArgs a, int W,
   if (slot >= a.n || g >= groups) return;  // a whole direction group exits together
   // per-warp source queue: kPrefetch slots x (32 lanes x 4 doubles + 2)
   double* wqueue = smem + static_cast<size_t>(wib) * kPrefetch * kQueueSlotDoubles;
-  double* queue = wqueue + static_cast<size_t>(lane) * 4;
+  double* queue = wqueue + static_cast<size_t>(lane) * 2;  // halves at +0 and +64 doubles
   GroupSmem sm;
   {
     double* base = smem + static_cast<size_t>(blockDim.x >> 5) * kPrefetch * kQueueSlotDoubles +
@@ -434,7 +443,7 @@ __global__ void __launch_bounds__(256, 2) sweep_kernel(const SweepArgs a, int W,
 #pragma unroll
           for (int r = 0; r < 4; ++r) p[r] = v[r];
         }
-        st_cell(psi + 4 * cur.cell, p);
+        st_cell256(psi + 4 * cur.cell, p);
         // outflow traces: x (per y-mode) for the next cell of this row,
         // y (per x-mode) for the row above (next lane / next band).
         txi0 = tx[0] * p[0] + tx[1] * p[1];
