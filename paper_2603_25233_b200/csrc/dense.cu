@@ -106,7 +106,7 @@ int tn_splits(int M, int N, long long K) {
 // ------------------------------------------------------------ GEMM A B
 __global__ void __launch_bounds__(256) gemm_nn_kernel(long long M, int N, int K, const double* __restrict__ A,
                                                       long long lda, const double* __restrict__ B, long long ldb,
-                                                      double* __restrict__ C, long long ldc) {
+                                                      double* __restrict__ C, long long ldc, bool subtract) {
   __shared__ double As[BK][BM + 1];
   __shared__ double Bs[BK][BN + 1];
   const int tid = threadIdx.x;
@@ -147,7 +147,12 @@ __global__ void __launch_bounds__(256) gemm_nn_kernel(long long M, int N, int K,
     for (int j = 0; j < 4; ++j) {
       const long long m = m0 + tm + 16 * i;
       const int n = n0 + tn + 16 * j;
-      if (m < M && n < N) C[m + n * ldc] = acc[i][j];
+      if (m < M && n < N) {
+        if (subtract)
+          C[m + n * ldc] -= acc[i][j];
+        else
+          C[m + n * ldc] = acc[i][j];
+      }
     }
 }
 
@@ -491,6 +496,190 @@ __global__ void __launch_bounds__(256) jacobi_round(long long m, int n, int npad
   }
 }
 
+
+// ------------------------------------------------------------ blocked batched LU
+// Right-looking LU with partial pivoting (first maximum, as Eigen's
+// PartialPivLU) of the augmented systems [A_j | b_j] (r x (r+1), column-
+// major, ld r) in panels of kNb columns: panel factorisation (one CTA per
+// system), row swaps + unit-lower TRSM of the panel rows, a tiled GEMM
+// trailing update over many CTAs, then back substitution.  Forward
+// substitution on b happens through the augmented column.
+constexpr int kNb = 16;
+
+__global__ void __launch_bounds__(256) lu_assemble(int r, const int* __restrict__ angles, const double* __restrict__ dirs,
+                                                   const double* __restrict__ proj, long long ldp, long long pstride,
+                                                   const double* __restrict__ prhs, const double* __restrict__ extra,
+                                                   long long ldx, double* __restrict__ M) {
+  const int jb = blockIdx.y;
+  const int ang = angles[jb];
+  const double omx = dirs[3 * ang], omy = dirs[3 * ang + 1];
+  const double* px = proj + (omx >= 0.0 ? 0 : 1) * pstride;
+  const double* py = proj + (omy >= 0.0 ? 2 : 3) * pstride;
+  const double* pt = proj + 4 * pstride;
+  double* A = M + static_cast<size_t>(jb) * r * (r + 1);
+  const long long total = static_cast<long long>(r) * (r + 1);
+  for (long long e = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; e < total;
+       e += static_cast<long long>(gridDim.x) * blockDim.x) {
+    const int i = static_cast<int>(e % r), j = static_cast<int>(e / r);
+    A[e] = j < r ? omx * px[i + j * ldp] + omy * py[i + j * ldp] + pt[i + j * ldp]
+                 : prhs[i] + (extra ? extra[i + jb * ldx] : 0.0);
+  }
+}
+
+__global__ void __launch_bounds__(256) lu_panel(int r, int k0, int jb, double* __restrict__ M, int* __restrict__ piv) {
+  __shared__ double shv[33];
+  __shared__ int shi[33];
+  double* A = M + static_cast<size_t>(blockIdx.x) * r * (r + 1);
+  int* pv = piv + static_cast<size_t>(blockIdx.x) * r;
+  const int tid = threadIdx.x, nt = blockDim.x;
+  for (int j = k0; j < k0 + jb; ++j) {
+    double best = -1.0;
+    int bi = r;
+    for (int i = j + tid; i < r; i += nt) {
+      const double v = fabs(A[i + static_cast<size_t>(j) * r]);
+      if (v > best) {
+        best = v;
+        bi = i;
+      }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const double ov = __shfl_xor_sync(0xffffffffu, best, o);
+      const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+      if (ov > best || (ov == best && oi < bi)) {
+        best = ov;
+        bi = oi;
+      }
+    }
+    if ((tid & 31) == 0) {
+      shv[tid >> 5] = best;
+      shi[tid >> 5] = bi;
+    }
+    __syncthreads();
+    if (tid == 0) {
+      double bv = shv[0];
+      int bix = shi[0];
+      for (int w = 1; w < (nt >> 5); ++w)
+        if (shv[w] > bv || (shv[w] == bv && shi[w] < bix)) {
+          bv = shv[w];
+          bix = shi[w];
+        }
+      shi[32] = bv > 0.0 ? bix : j;  // all-zero column: no swap (first zero pivot)
+      shv[32] = bv;
+      pv[j] = shi[32];
+    }
+    __syncthreads();
+    const int p = shi[32];
+    const bool nonzero = shv[32] > 0.0;
+    if (p != j)
+      for (int c = k0 + tid; c < k0 + jb; c += nt) {
+        const double t = A[j + static_cast<size_t>(c) * r];
+        A[j + static_cast<size_t>(c) * r] = A[p + static_cast<size_t>(c) * r];
+        A[p + static_cast<size_t>(c) * r] = t;
+      }
+    __syncthreads();
+    if (nonzero) {
+      const double d = A[j + static_cast<size_t>(j) * r];
+      for (int i = j + 1 + tid; i < r; i += nt) A[i + static_cast<size_t>(j) * r] /= d;
+    }
+    __syncthreads();
+    const int rows = r - j - 1, cols = k0 + jb - j - 1;
+    for (int e = tid; e < rows * cols; e += nt) {
+      const int i = j + 1 + e % rows, c = j + 1 + e / rows;
+      A[i + static_cast<size_t>(c) * r] -= A[i + static_cast<size_t>(j) * r] * A[j + static_cast<size_t>(c) * r];
+    }
+    __syncthreads();
+  }
+}
+
+// row swaps of the panel applied to the trailing columns, then U12 = L11^-1 A12
+__global__ void __launch_bounds__(256) lu_swap_trsm(int r, int k0, int jb, double* __restrict__ M,
+                                                    const int* __restrict__ piv) {
+  double* A = M + static_cast<size_t>(blockIdx.y) * r * (r + 1);
+  const int* pv = piv + static_cast<size_t>(blockIdx.y) * r;
+  const int c = k0 + jb + blockIdx.x * blockDim.x + threadIdx.x;
+  if (c > r) return;  // columns k0+jb .. r (r is the augmented rhs)
+  double* col = A + static_cast<size_t>(c) * r;
+  for (int j = k0; j < k0 + jb; ++j) {
+    const int p = pv[j];
+    if (p != j) {
+      const double t = col[j];
+      col[j] = col[p];
+      col[p] = t;
+    }
+  }
+  double u[kNb];
+#pragma unroll
+  for (int i = 0; i < kNb; ++i) {
+    if (i >= jb) break;
+    double s = col[k0 + i];
+    for (int l = 0; l < i; ++l) s -= A[k0 + i + static_cast<size_t>(k0 + l) * r] * u[l];
+    u[i] = s;
+    col[k0 + i] = s;
+  }
+}
+
+// A22 -= L21 U12 over rows k0+jb..r-1, columns k0+jb..r; grid (tilesM, tilesN, m)
+__global__ void __launch_bounds__(256) lu_update(int r, int k0, int jb, double* __restrict__ M) {
+  __shared__ double Ls[kNb][BM + 1];
+  __shared__ double Us[kNb][BN + 1];
+  double* A = M + static_cast<size_t>(blockIdx.z) * r * (r + 1);
+  const int row0 = k0 + jb + blockIdx.x * BM, col0 = k0 + jb + blockIdx.y * BN;
+  const int tid = threadIdx.x, tm = tid % 16, tn = tid / 16;
+  for (int e = tid; e < kNb * BM; e += 256) {
+    const int kk = e / BM, mm = e % BM;
+    const int i = row0 + mm;
+    Ls[kk][mm] = (kk < jb && i < r) ? A[i + static_cast<size_t>(k0 + kk) * r] : 0.0;
+    const int nn = e % BN, kk2 = e / BN;
+    const int c = col0 + nn;
+    Us[kk2][nn] = (kk2 < jb && c <= r) ? A[k0 + kk2 + static_cast<size_t>(c) * r] : 0.0;
+  }
+  __syncthreads();
+  double acc[4][4] = {};
+#pragma unroll
+  for (int kk = 0; kk < kNb; ++kk) {
+    double a[4], b[4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) a[i] = Ls[kk][tm + 16 * i];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) b[j] = Us[kk][tn + 16 * j];
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+      for (int j = 0; j < 4; ++j) acc[i][j] += a[i] * b[j];
+  }
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int row = row0 + tm + 16 * i, c = col0 + tn + 16 * j;
+      if (row < r && c <= r) A[row + static_cast<size_t>(c) * r] -= acc[i][j];
+    }
+}
+
+// back substitution with U (column oriented, as Eigen), solution to sol
+__global__ void __launch_bounds__(256) lu_backsolve(int r, const double* __restrict__ M, double* __restrict__ sol,
+                                                    long long ldsol, int* __restrict__ flags) {
+  extern __shared__ double xs[];
+  const double* A = M + static_cast<size_t>(blockIdx.x) * r * (r + 1);
+  for (int i = threadIdx.x; i < r; i += blockDim.x) xs[i] = A[i + static_cast<size_t>(r) * r];
+  __syncthreads();
+  for (int i = r - 1; i >= 0; --i) {
+    if (threadIdx.x == 0) xs[i] = xs[i] / A[i + static_cast<size_t>(i) * r];
+    __syncthreads();
+    const double xi = xs[i];
+    for (int j = threadIdx.x; j < i; j += blockDim.x) xs[j] -= xi * A[j + static_cast<size_t>(i) * r];
+    __syncthreads();
+  }
+  int bad = 0;
+  for (int i = threadIdx.x; i < r; i += blockDim.x) {
+    sol[i + blockIdx.x * ldsol] = xs[i];
+    if (!isfinite(xs[i])) bad = 1;
+  }
+  bad = __syncthreads_or(bad);
+  if (threadIdx.x == 0) flags[blockIdx.x] = bad;
+}
+
 }  // namespace
 
 size_t gemm_tn_work(int M, int N, long long K) {
@@ -517,14 +706,15 @@ void gemm_tn(int M, int N, long long K, const double* A, long long lda, const do
 }
 
 void gemm_nn(long long M, int N, int K, const double* A, long long lda, const double* B, long long ldb, double* C,
-             long long ldc, cudaStream_t s) {
+             long long ldc, cudaStream_t s, bool subtract) {
   if (M <= 0 || N <= 0) return;
   if (K <= 0) {
-    for (int j = 0; j < N; ++j) RTLR_CUDA(cudaMemsetAsync(C + j * ldc, 0, M * sizeof(double), s));
+    if (!subtract)
+      for (int j = 0; j < N; ++j) RTLR_CUDA(cudaMemsetAsync(C + j * ldc, 0, M * sizeof(double), s));
     return;
   }
   dim3 grid(static_cast<unsigned>((M + BM - 1) / BM), (N + BN - 1) / BN);
-  gemm_nn_kernel<<<grid, 256, 0, s>>>(M, N, K, A, lda, B, ldb, C, ldc);
+  gemm_nn_kernel<<<grid, 256, 0, s>>>(M, N, K, A, lda, B, ldb, C, ldc, subtract);
   RTLR_CUDA(cudaGetLastError());
 }
 
@@ -558,10 +748,35 @@ void stream_products(const StencilArgs& a, int p, const double* P, long long ldp
   RTLR_CUDA(cudaGetLastError());
 }
 
+size_t galerkin_work_doubles(int r, int m) {
+  if (r <= kSmemLuMax) return 0;
+  return static_cast<size_t>(m) * (static_cast<size_t>(r) * (r + 1) + r);
+}
+
 void galerkin_batch(int r, int m, const int* angles, const double* dirs, const double* proj, long long ldp,
                     long long proj_stride, const double* prhs, const double* extra, double* sol, long long ldsol,
                     int* flags, double* work, cudaStream_t s) {
   if (m <= 0 || r <= 0) return;
+  if (r > kSmemLuMax) {
+    double* M = work;
+    int* piv = reinterpret_cast<int*>(work + static_cast<size_t>(m) * r * (r + 1));
+    lu_assemble<<<dim3(std::max(1, std::min(64, (r * (r + 1) + 255) / 256)), m), 256, 0, s>>>(
+        r, angles, dirs, proj, ldp, proj_stride, prhs, extra, ldsol, M);
+    for (int k0 = 0; k0 < r; k0 += kNb) {
+      const int jb = std::min(kNb, r - k0);
+      lu_panel<<<m, 256, 0, s>>>(r, k0, jb, M, piv);
+      const int ntrail = r + 1 - (k0 + jb);
+      if (ntrail > 0) {
+        lu_swap_trsm<<<dim3((ntrail + 127) / 128, m), 128, 0, s>>>(r, k0, jb, M, piv);
+        const int rows = r - (k0 + jb);
+        if (rows > 0)
+          lu_update<<<dim3((rows + BM - 1) / BM, (ntrail + BN - 1) / BN, m), 256, 0, s>>>(r, k0, jb, M);
+      }
+    }
+    lu_backsolve<<<m, 256, static_cast<size_t>(r) * sizeof(double), s>>>(r, M, sol, ldsol, flags);
+    RTLR_CUDA(cudaGetLastError());
+    return;
+  }
   const bool in_smem = r <= kSmemLuMax;
   const size_t smem = in_smem ? static_cast<size_t>(r) * r * sizeof(double) : 0;
   if (in_smem)

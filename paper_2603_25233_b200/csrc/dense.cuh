@@ -14,9 +14,9 @@ namespace cuda {
 // work >= splits * M * N doubles.  beta_add: C += result instead of C =.
 void gemm_tn(int M, int N, long long K, const double* A, long long lda, const double* B, long long ldb,
              double* C, long long ldc, double* work, size_t work_doubles, cudaStream_t s);
-// C[M x N] (ldc) = A B with A: M x K (lda, M large), B: K x N (ldb), K small.
+// C[M x N] (ldc) = A B (or C -= A B) with A: M x K (lda, M large), B: K x N (ldb), K small.
 void gemm_nn(long long M, int N, int K, const double* A, long long lda, const double* B, long long ldb,
-             double* C, long long ldc, cudaStream_t s);
+             double* C, long long ldc, cudaStream_t s, bool subtract = false);
 size_t gemm_tn_work(int M, int N, long long K);
 
 // out[i] = sum_k A[i, k] x[k] for A: n x k (lda) — accumulating into y (y += A x * alpha)
@@ -40,6 +40,7 @@ void stream_products(const StencilArgs& a, int p, const double* P, long long ldp
 // sol: r x m (ldsol); extra optional r x m (Xt g_j).  flags[j] = 1 if the
 // solution is not finite.  work >= m * r * r doubles for r > kSmemLuMax.
 constexpr int kSmemLuMax = 96;
+size_t galerkin_work_doubles(int r, int m);
 void galerkin_batch(int r, int m, const int* angles, const double* dirs, const double* proj, long long ldp,
                     long long proj_stride, const double* prhs, const double* extra, double* sol,
                     long long ldsol, int* flags, double* work, cudaStream_t s);

@@ -269,34 +269,66 @@ bool LowRankEngine::mgs_ro_update(const double* snaps, const std::vector<int>& a
   const int m0 = n_snap_;
   X_.reserve(n_, rank_ + p_in, s_);
   std::vector<int> accepted;
-  double* chat = vec_.get();
+  // Block classical Gram-Schmidt, equivalent to the reference's per-snapshot
+  // CGS up to rounding: every snapshot is projected against the basis that
+  // existed before this batch in one GEMM (twice: "twice is enough", the
+  // second pass is unconditional for the old basis, which only adds
+  // accuracy), then sequentially against the vectors this batch accepted,
+  // where the reference's conditional second pass (rem < 0.5 norm0) is
+  // kept.  X_old is read 4 times per batch instead of up to 4 times per
+  // snapshot.
+  const int r_old = rank_;
+  double* Rm = rem_.ensure(static_cast<size_t>(n_) * p_in);
+  RTLR_CUDA(cudaMemcpyAsync(Rm, snaps, static_cast<size_t>(n_) * p_in * sizeof(double), cudaMemcpyDeviceToDevice, s_));
+  double* nr = nrm_.ensure(std::max(p_in, 128));
+  col_norms_kernel<<<p_in, 256, 0, s_>>>(n_, p_in, snaps, n_, nr);
+  std::vector<double> norm0(p_in), cold;
+  RTLR_CUDA(cudaMemcpyAsync(norm0.data(), nr, p_in * sizeof(double), cudaMemcpyDeviceToHost, s_));
+  if (r_old > 0) {
+    double* C1 = gbuf_.ensure(static_cast<size_t>(2) * r_old * p_in);
+    double* C2 = C1 + static_cast<size_t>(r_old) * p_in;
+    gemm_tn(r_old, p_in, n_, X_.col(0), X_.ld, snaps, n_, C1, r_old, work(gemm_tn_work(r_old, p_in, n_)),
+            work_.size(), s_);
+    gemm_nn(n_, p_in, r_old, X_.col(0), X_.ld, C1, r_old, Rm, n_, s_, /*subtract=*/true);
+    gemm_tn(r_old, p_in, n_, X_.col(0), X_.ld, Rm, n_, C2, r_old, work(gemm_tn_work(r_old, p_in, n_)),
+            work_.size(), s_);
+    gemm_nn(n_, p_in, r_old, X_.col(0), X_.ld, C2, r_old, Rm, n_, s_, /*subtract=*/true);
+    std::vector<double> h1(static_cast<size_t>(r_old) * p_in), h2(h1.size());
+    RTLR_CUDA(cudaMemcpyAsync(h1.data(), C1, h1.size() * sizeof(double), cudaMemcpyDeviceToHost, s_));
+    RTLR_CUDA(cudaMemcpyAsync(h2.data(), C2, h2.size() * sizeof(double), cudaMemcpyDeviceToHost, s_));
+    RTLR_CUDA(cudaStreamSynchronize(s_));
+    cold.resize(h1.size());
+    for (size_t k = 0; k < h1.size(); ++k) cold[k] = h1[k] + h2[k];
+  } else {
+    RTLR_CUDA(cudaStreamSynchronize(s_));
+  }
+  double* cnew = vec_.get();
   double* corr = vec_.get() + rmax_;
-  std::vector<double> hchat;
+  std::vector<double> hc(p_in), hc2(p_in);
   for (int i = 0; i < p_in; ++i) {
-    const double* sn = snaps + static_cast<size_t>(i) * n_;
-    const double norm0 = std::sqrt(host_dot(sn, sn, n_));
-    RTLR_CUDA(cudaMemcpyAsync(rem_.get(), sn, n_ * sizeof(double), cudaMemcpyDeviceToDevice, s_));
+    double* rem = Rm + static_cast<size_t>(i) * n_;
+    const int k_new = rank_ - r_old;
     std::vector<double> reccol(rank_ + 1, 0.0);
-    if (rank_ > 0) {
-      // c = X^T psi; rem = psi - X c; second pass when mass was removed
-      gemm_tn(rank_, 1, n_, X_.col(0), X_.ld, sn, n_, chat, rank_, work(gemm_tn_work(rank_, 1, n_)),
+    for (int k = 0; k < r_old; ++k) reccol[k] = cold[k + static_cast<size_t>(i) * r_old];
+    if (k_new > 0) {
+      gemm_tn(k_new, 1, n_, X_.col(r_old), X_.ld, rem, n_, cnew, k_new, work(gemm_tn_work(k_new, 1, n_)),
               work_.size(), s_);
-      gemv_n(n_, rank_, X_.col(0), X_.ld, chat, -1.0, rem_.get(), s_);
-      const double rn = std::sqrt(host_dot(rem_.get(), rem_.get(), n_));
-      if (rn < 0.5 * norm0) {
-        gemm_tn(rank_, 1, n_, X_.col(0), X_.ld, rem_.get(), n_, corr, rank_, work(gemm_tn_work(rank_, 1, n_)),
+      gemv_n(n_, k_new, X_.col(r_old), X_.ld, cnew, -1.0, rem, s_);
+      RTLR_CUDA(cudaMemcpyAsync(hc.data(), cnew, k_new * sizeof(double), cudaMemcpyDeviceToHost, s_));
+      const double rn = std::sqrt(host_dot(rem, rem, n_));
+      if (rn < 0.5 * norm0[i]) {
+        gemm_tn(k_new, 1, n_, X_.col(r_old), X_.ld, rem, n_, corr, k_new, work(gemm_tn_work(k_new, 1, n_)),
                 work_.size(), s_);
-        gemv_n(n_, rank_, X_.col(0), X_.ld, corr, -1.0, rem_.get(), s_);
-        add_vec<<<1, 256, 0, s_>>>(rank_, chat, corr);
+        gemv_n(n_, k_new, X_.col(r_old), X_.ld, corr, -1.0, rem, s_);
+        RTLR_CUDA(cudaMemcpyAsync(hc2.data(), corr, k_new * sizeof(double), cudaMemcpyDeviceToHost, s_));
+        RTLR_CUDA(cudaStreamSynchronize(s_));
+        for (int k = 0; k < k_new; ++k) hc[k] += hc2[k];
       }
-      hchat.resize(rank_);
-      RTLR_CUDA(cudaMemcpyAsync(hchat.data(), chat, rank_ * sizeof(double), cudaMemcpyDeviceToHost, s_));
-      RTLR_CUDA(cudaStreamSynchronize(s_));
-      for (int k = 0; k < rank_; ++k) reccol[k] = hchat[k];
+      for (int k = 0; k < k_new; ++k) reccol[r_old + k] = hc[k];
     }
-    const double h = std::sqrt(host_dot(rem_.get(), rem_.get(), n_));
-    if (norm0 > 0.0 && h > 1e-12 * norm0) {  // drop_tol (low_rank.hpp:61-62)
-      scale_val_kernel<<<g1(n_), 256, 0, s_>>>(n_, rem_.get(), h, X_.col(rank_));
+    const double h = std::sqrt(host_dot(rem, rem, n_));
+    if (norm0[i] > 0.0 && h > 1e-12 * norm0[i]) {  // drop_tol (low_rank.hpp:61-62)
+      scale_val_kernel<<<g1(n_), 256, 0, s_>>>(n_, rem, h, X_.col(rank_));
       reccol[rank_] = h;
       accepted.push_back(i);
       ++rank_;
@@ -382,7 +414,7 @@ void LowRankEngine::galerkin(const std::vector<int>& angles, double* d_sol, long
   if (rank_ < 1) throw std::runtime_error("galerkin_solve: empty basis");
   const int m = static_cast<int>(angles.size());
   const long long rr = static_cast<long long>(rank_) * rank_;
-  const int chunk = rank_ > kSmemLuMax ? static_cast<int>(std::max<long long>(1, (64LL << 20) / rr)) : 4096;
+  const int chunk = rank_ > kSmemLuMax ? static_cast<int>(std::max<long long>(1, (128LL << 20) / rr)) : 4096;
   for (int j0 = 0; j0 < m; j0 += chunk) {
     const int mc = std::min(chunk, m - j0);
     std::vector<int> sub(angles.begin() + j0, angles.begin() + j0 + mc);
@@ -398,7 +430,7 @@ void LowRankEngine::galerkin(const std::vector<int>& angles, double* d_sol, long
       extra = out;
     }
     int* flags = flags_.ensure(mc);
-    double* lw = rank_ > kSmemLuMax ? luw_.ensure(static_cast<size_t>(mc) * rr) : nullptr;
+    double* lw = rank_ > kSmemLuMax ? luw_.ensure(galerkin_work_doubles(rank_, mc)) : nullptr;
     galerkin_batch(rank_, mc, d_ang, dirs_, proj_.get(), ldp_, ldp_ * ldp_, prhs_.get(), extra, out, ldsol, flags, lw,
                    s_);
     std::vector<int> hf(mc);
