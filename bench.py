@@ -45,7 +45,8 @@ def parse():
     ap.add_argument("--grid", type=int, default=512)
     ap.add_argument("--n-theta", type=int, default=128)
     ap.add_argument("--n-omega-z", type=int, default=32)
-    ap.add_argument("--e2e-chunk", type=int, default=128, help="directions per host-buffer call")
+    ap.add_argument("--e2e-chunk", type=int, default=256, help="directions per host-buffer call")
+    ap.add_argument("--no-solvers", action="store_true", help="skip the C1/C2 time-to-tol extras")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--cpu-sample-dirs", type=int, default=8)
     return ap.parse_args()
@@ -297,6 +298,23 @@ def main():
                "h2d_bytes_per_step": D * n * 8, "d2h_bytes_per_step": D * n * 8,
                "steps": e2e_steps, "chunk_directions": C, "api": "rtlr_cu_sweep(where=RTLR_CU_HOST)"}
 
+    # Secondary BASELINE metric: solver time-to-tol through the public API
+    # (assembly + upload excluded, as the reference's solve_seconds).
+    solvers = None
+    if rank == 0 and not args.no_solvers:
+        solvers = {}
+        for name, method in (("C1", "full"), ("C2", "lowrank")):
+            sp = P.Problem(name, device=local)
+            t0 = time.perf_counter()
+            rep = sp.solve_full_rank(store_psi=0) if method == "full" else sp.solve_low_rank(build_factors=0)
+            wall = time.perf_counter() - t0
+            entry = {"method": method, "time_to_tol_s": float(rep.get("solve_seconds", 1)[0]), "wall_s": wall,
+                     "iterations": rep.iterations, "converged": rep.converged}
+            if method == "lowrank":
+                entry["final_rank"] = int(rep.history("rank")[-1])
+            solvers[name] = entry
+            del sp
+
     cpu = None
     if rank == 0 and world == 1:
         r, upd, dt = cpu_sweep_rate(args.grid, args.n_theta, args.n_omega_z, args.cpu_sample_dirs, 1)
@@ -310,7 +328,7 @@ def main():
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic", "config": workload_config(args) | {"parallelism": f"direction-sets x{world}"},
             "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": args.steps,
-            "clocks": clk.summary(),
+            "clocks": clk.summary(), "solvers": solvers,
         }
         print(json.dumps(line), flush=True)
     if dist:

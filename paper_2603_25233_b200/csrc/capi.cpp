@@ -289,6 +289,10 @@ int rtlr_cu_sweep(rtlr_cu_problem* p, const int* angles, int n, const double* rh
       ang[k] = angles ? angles[k] : k;
       if (ang[k] < 0 || ang[k] >= h.n_omega) throw std::invalid_argument("sweep: angle index out of range");
     }
+    if (where == RTLR_CU_HOST) {  // chunked, H2D / sweep / D2H overlapped
+      P.sweep_host(ang.data(), n, rhs, rhs_stride, psi, psi_stride);
+      return;
+    }
     cudaStream_t s = P.stream();
     int* d_ang = nullptr;
     RTLR_CUDA(cudaMallocAsync(&d_ang, n * sizeof(int), s));

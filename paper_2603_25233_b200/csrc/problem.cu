@@ -58,6 +58,8 @@ Problem::Problem(const ProblemConfig& cfg, int device) : device_(device) {
 Problem::~Problem() {
   if (device_ < 0) return;
   cudaSetDevice(device_);
+  if (copy_in_) cudaStreamDestroy(copy_in_);
+  if (copy_out_) cudaStreamDestroy(copy_out_);
   if (stream_) cudaStreamSynchronize(stream_);
   if (own_stream_ && stream_) cudaStreamDestroy(stream_);
   if (h_state_) cudaFreeHost(h_state_);
@@ -177,6 +179,57 @@ void Problem::sweep(const int* d_angles, int n, const double* d_rhs, long long r
   a.err = err_.get();
   a.sc = sc_;
   launch_sweep(a, hp_.sigma_t_uniform, stream_);
+}
+
+void Problem::sweep_host(const int* h_angles, int n, const double* h_rhs, long long rhs_stride, double* h_psi,
+                         long long psi_stride) {
+  if (n <= 0) return;
+  const size_t nd = hp_.ndof;
+  if (!copy_in_) RTLR_CUDA(cudaStreamCreateWithFlags(&copy_in_, cudaStreamNonBlocking));
+  if (!copy_out_) RTLR_CUDA(cudaStreamCreateWithFlags(&copy_out_, cudaStreamNonBlocking));
+  const int chunk = static_cast<int>(std::max<size_t>(1, std::min<size_t>(n, (size_t{256} << 20) / (nd * 8))));
+  int* d_ang = hang_.ensure(n);
+  RTLR_CUDA(cudaMemcpyAsync(d_ang, h_angles, n * sizeof(int), cudaMemcpyHostToDevice, stream_));
+  const bool shared = rhs_stride == 0;
+  for (int b = 0; b < 2; ++b) {
+    hin_[b].ensure(shared ? nd : nd * chunk);
+    hout_[b].ensure(nd * chunk);
+  }
+  cudaEvent_t in_done[2], comp_done[2], out_done[2];
+  for (int b = 0; b < 2; ++b) {
+    RTLR_CUDA(cudaEventCreateWithFlags(&in_done[b], cudaEventDisableTiming));
+    RTLR_CUDA(cudaEventCreateWithFlags(&comp_done[b], cudaEventDisableTiming));
+    RTLR_CUDA(cudaEventCreateWithFlags(&out_done[b], cudaEventDisableTiming));
+  }
+  RTLR_CUDA(cudaStreamSynchronize(stream_));
+  if (shared) RTLR_CUDA(cudaMemcpyAsync(hin_[0].get(), h_rhs, nd * 8, cudaMemcpyHostToDevice, copy_in_));
+  int k = 0;
+  for (int c0 = 0; c0 < n; c0 += chunk, ++k) {
+    const int b = k & 1, c = std::min(chunk, n - c0);
+    if (!shared) {
+      if (k >= 2) RTLR_CUDA(cudaStreamWaitEvent(copy_in_, comp_done[b], 0));  // buffer b consumed
+      RTLR_CUDA(cudaMemcpy2DAsync(hin_[b].get(), nd * 8, h_rhs + static_cast<size_t>(c0) * rhs_stride,
+                                  static_cast<size_t>(rhs_stride) * 8, nd * 8, c, cudaMemcpyHostToDevice, copy_in_));
+    }
+    RTLR_CUDA(cudaEventRecord(in_done[b], copy_in_));
+    RTLR_CUDA(cudaStreamWaitEvent(stream_, in_done[b], 0));
+    if (k >= 2) RTLR_CUDA(cudaStreamWaitEvent(stream_, out_done[b], 0));  // output buffer drained
+    sweep(d_ang + c0, c, shared ? hin_[0].get() : hin_[b].get(), shared ? 0 : static_cast<long long>(nd),
+          hout_[b].get(), static_cast<long long>(nd));
+    RTLR_CUDA(cudaEventRecord(comp_done[b], stream_));
+    RTLR_CUDA(cudaStreamWaitEvent(copy_out_, comp_done[b], 0));
+    RTLR_CUDA(cudaMemcpy2DAsync(h_psi + static_cast<size_t>(c0) * psi_stride, static_cast<size_t>(psi_stride) * 8,
+                                hout_[b].get(), nd * 8, nd * 8, c, cudaMemcpyDeviceToHost, copy_out_));
+    RTLR_CUDA(cudaEventRecord(out_done[b], copy_out_));
+  }
+  RTLR_CUDA(cudaStreamSynchronize(copy_out_));
+  RTLR_CUDA(cudaStreamSynchronize(stream_));
+  for (int b = 0; b < 2; ++b) {
+    cudaEventDestroy(in_done[b]);
+    cudaEventDestroy(comp_done[b]);
+    cudaEventDestroy(out_done[b]);
+  }
+  check_error();
 }
 
 void Problem::apply(double omx, double omy, const double* d_v, double* d_out) {

@@ -115,6 +115,11 @@ class Problem {
   // (device pointer, n x 3).
   void sweep(const int* d_angles, int n, const double* d_rhs, long long rhs_stride, double* d_psi,
              long long psi_stride, bool use_bc = true, const double* d_dirs = nullptr);
+  // Same with host rhs / psi (pinned for overlap): directions are streamed
+  // through device buffers in chunks, H2D / sweep / D2H pipelined on three
+  // streams.  h_angles on the host.
+  void sweep_host(const int* h_angles, int n, const double* h_rhs, long long rhs_stride, double* h_psi,
+                  long long psi_stride);
   // StreamingOperator::apply (operators.cpp:283-288): out = (Sigma_t + Ox Dx + Oy Dy) v
   void apply(double omx, double omy, const double* d_v, double* d_out);
   // DiffusionSystem::solve / correct (diffusion.cpp:203-213); returns PCG iterations
@@ -152,7 +157,9 @@ class Problem {
   StreamDev sc_{};
   DBuf<double> dirs_, weights_, sigma_t_, sigma_s_, source_, bc_, sip_, jac_;
   DBuf<int> err_, angle_idx_;
-  DBuf<double> line_, norm_work_, pcg_vec_, pcg_part_, uniq_w_, scratch_;
+  DBuf<double> line_, norm_work_, pcg_vec_, pcg_part_, uniq_w_, scratch_, hin_[2], hout_[2];
+  DBuf<int> hang_;
+  cudaStream_t copy_in_ = nullptr, copy_out_ = nullptr;
   DBuf<PcgState> pcg_state_;
   PcgState* h_state_ = nullptr;
   double* h_pin_ = nullptr;  // small pinned host scratch
