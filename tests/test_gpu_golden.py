@@ -1,0 +1,39 @@
+"""GPU solvers at the BASELINE configs' full size against golden fixtures
+produced by the CPU oracle (tests/golden/make_golden.py).  Bars from the
+north star: scalar flux rel. L2 <= 1e-10 (full rank) / 1e-8 (low rank),
+outer iterations +-1, final rank reported side by side (+-2)."""
+import os
+
+import numpy as np
+import pytest
+
+import paper_2603_25233_b200 as P
+
+pytestmark = pytest.mark.gpu
+GOLD = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden")
+
+
+def load(tag):
+    path = os.path.join(GOLD, tag + ".npz")
+    if not os.path.exists(path):
+        pytest.skip(f"no golden fixture {tag}")
+    return np.load(path)
+
+
+@pytest.mark.parametrize("name,method", [("C1", "full"), ("C2", "full"), ("C2", "lowrank"),
+                                         ("C3", "full"), ("C3", "lowrank")])
+def test_baseline_config_matches_oracle(name, method):
+    g = load(f"{name}_{method}")
+    p = P.Problem(name)
+    r = p.solve_full_rank(store_psi=0) if method == "full" else p.solve_low_rank(build_factors=0)
+    ref = g["phi"]
+    err = np.linalg.norm(r.phi - ref) / np.linalg.norm(ref)
+    tol = 1e-10 if method == "full" else 1e-8
+    print(f"{name} {method}: it {r.iterations} vs {int(g['iterations'])}, rel {err:.2e}")
+    assert r.converged and bool(g["converged"])
+    assert abs(r.iterations - int(g["iterations"])) <= 1
+    assert err <= tol
+    if method == "lowrank":
+        ranks, ref_ranks = r.history("rank"), g["rank"]
+        print(f"  ranks GPU {list(map(int, ranks))} oracle {list(map(int, ref_ranks))}")
+        assert abs(int(ranks[-1]) - int(ref_ranks[-1])) <= 2
