@@ -154,6 +154,13 @@ void rtlr_cu_report_destroy(rtlr_cu_report* r);
  * balanced.  Pure host logic (no GPU needed). */
 int rtlr_cu_partition_angles(int n_theta, int n_omega_z, int nranks, int rank, int* count,
                              int* angles);
+/* NCCL (over NVLink / NVSwitch) for the sharded drivers: rank 0 creates the
+ * 128-byte id, the launcher broadcasts it, every rank attaches its problem.
+ * solve_full_rank then sweeps this rank's directions and sums the scalar-
+ * flux partials with ncclAllReduce (full_rank.cpp:89 psi * w); the DSA
+ * correction is replicated.  nranks == 1 with id == NULL detaches. */
+int rtlr_cu_nccl_unique_id(unsigned char* id);
+int rtlr_cu_problem_set_comm(rtlr_cu_problem* p, int nranks, int rank, const unsigned char* id);
 
 #ifdef __cplusplus
 }

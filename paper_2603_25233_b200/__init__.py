@@ -37,7 +37,7 @@ EXPORTS = [
     "rtlr_cu_solve_full_rank", "rtlr_cu_solve_low_rank", "rtlr_cu_report_info",
     "rtlr_cu_report_get", "rtlr_cu_report_sampled", "rtlr_cu_report_destroy",
     "rtlr_cu_partition_angles", "rtlr_cu_problem_fr_options", "rtlr_cu_problem_lr_options",
-    "rtlr_cu_sweep_async", "rtlr_cu_check",
+    "rtlr_cu_sweep_async", "rtlr_cu_check", "rtlr_cu_nccl_unique_id", "rtlr_cu_problem_set_comm",
 ]
 
 
@@ -97,6 +97,8 @@ def load_library(path: str = LIB_PATH):
     L.rtlr_cu_sweep_async.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int, ctypes.c_void_p,
                                       ctypes.c_int64, ctypes.c_void_p, ctypes.c_int64]
     L.rtlr_cu_check.argtypes = [ctypes.c_void_p]
+    L.rtlr_cu_nccl_unique_id.argtypes = [ctypes.c_char_p]
+    L.rtlr_cu_problem_set_comm.argtypes = [ctypes.c_void_p, ctypes.c_int, ctypes.c_int, ctypes.c_char_p]
     L.rtlr_cu_sweep_dirs.argtypes =[ctypes.c_void_p, _D, ctypes.c_int, ctypes.c_void_p, ctypes.c_int64,
                                      ctypes.c_void_p, ctypes.c_int64, ctypes.c_int]
     L.rtlr_cu_apply.argtypes = [ctypes.c_void_p, ctypes.c_double, ctypes.c_double, ctypes.c_void_p,
@@ -138,6 +140,13 @@ def _dp(a: np.ndarray):
 
 def device_count() -> int:
     return load_library().rtlr_cu_device_count()
+
+
+def nccl_unique_id() -> bytes:
+    """128-byte NCCL unique id (create on rank 0, broadcast to the others)."""
+    buf = ctypes.create_string_buffer(128)
+    _check(load_library().rtlr_cu_nccl_unique_id(buf))
+    return buf.raw
 
 
 def partition_angles(n_theta: int, n_omega_z: int, nranks: int, rank: int) -> np.ndarray:
@@ -239,6 +248,10 @@ class Problem:
 
     def set_stream(self, cuda_stream: int):
         _check(load_library().rtlr_cu_problem_set_stream(self.h, ctypes.c_void_p(cuda_stream)))
+
+    def set_comm(self, nranks: int, rank: int, nccl_id: bytes | None):
+        """Attach an NCCL communicator: the drivers then shard directions."""
+        _check(load_library().rtlr_cu_problem_set_comm(self.h, nranks, rank, nccl_id))
 
     def set_option(self, key: str, value: float):
         _check(load_library().rtlr_cu_problem_set_option(self.h, key.encode(), float(value)))

@@ -539,25 +539,22 @@ void rtlr_cu_report_destroy(rtlr_cu_report* r) { delete r; }
 
 int rtlr_cu_partition_angles(int n_theta, int n_omega_z, int nranks, int rank, int* count, int* angles) {
   return guard([&] {
-    need(n_theta >= 1 && n_omega_z >= 1 && nranks >= 1 && rank >= 0 && rank < nranks && count,
-         "partition_angles: bad argument");
-    // Units are mirror pairs {(j1, j2), (j1, n_z-1-j2)}, listed azimuth-
-    // major so a round-robin deal spreads every rank over all quadrants.
-    const int half = (n_omega_z + 1) / 2;
-    int k = 0, u = 0;
-    for (int j2 = 0; j2 < half; ++j2)
-      for (int j1 = 0; j1 < n_theta; ++j1, ++u) {
-        if (u % nranks != rank) continue;
-        const int a = j1 * n_omega_z + j2, b = j1 * n_omega_z + (n_omega_z - 1 - j2);
-        if (angles) angles[k] = a;
-        ++k;
-        if (b != a) {
-          if (angles) angles[k] = b;
-          ++k;
-        }
-      }
-    *count = k;
+    need(count != nullptr, "partition_angles: bad argument");
+    const std::vector<int> a = partition_angles(n_theta, n_omega_z, nranks, rank);
+    *count = static_cast<int>(a.size());
+    if (angles) std::memcpy(angles, a.data(), a.size() * sizeof(int));
   });
+}
+
+int rtlr_cu_nccl_unique_id(unsigned char* out) {
+  return guard([&] {
+    need(out != nullptr, "nccl_unique_id: null argument");
+    nccl_unique_id(out);
+  });
+}
+
+int rtlr_cu_problem_set_comm(rtlr_cu_problem* p, int nranks, int rank, const unsigned char* id) {
+  return guard([&] { gpu(p).set_comm(nranks, rank, id); });
 }
 
 }  // extern "C"

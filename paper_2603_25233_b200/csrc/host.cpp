@@ -705,6 +705,22 @@ std::vector<int> SubsampleRng::sample_without_replacement(std::vector<int> pool,
   return pool;
 }
 
+std::vector<int> partition_angles(int n_theta, int n_omega_z, int nranks, int rank) {
+  if (n_theta < 1 || n_omega_z < 1 || nranks < 1 || rank < 0 || rank >= nranks)
+    throw std::invalid_argument("partition_angles: bad argument");
+  std::vector<int> out;
+  const int half = (n_omega_z + 1) / 2;
+  int u = 0;
+  for (int j2 = 0; j2 < half; ++j2)
+    for (int j1 = 0; j1 < n_theta; ++j1, ++u) {
+      if (u % nranks != rank) continue;
+      const int a = j1 * n_omega_z + j2, b = j1 * n_omega_z + (n_omega_z - 1 - j2);
+      out.push_back(a);
+      if (b != a) out.push_back(b);
+    }
+  return out;
+}
+
 int truncation_rank(const std::vector<double>& s, double eps_svd) {  // low_rank.cpp:254-266
   const int n = static_cast<int>(s.size());
   if (n == 0) return 0;

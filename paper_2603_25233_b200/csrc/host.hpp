@@ -103,6 +103,11 @@ class SubsampleRng {
 // proj/src/low_rank.cpp:254-266
 int truncation_rank(const std::vector<double>& s, double eps_svd);
 
+// Directions owned by `rank` of `nranks`: units are mirror pairs
+// {(j1, j2), (j1, n_z-1-j2)} listed pair-index-major / azimuth-minor and dealt
+// round-robin, so every rank spans all quadrants and pairs never split.
+std::vector<int> partition_angles(int n_theta, int n_omega_z, int nranks, int rank);
+
 // Counter-based U[0,1) generator for the C5 per-(cell, direction) sources
 // (SURVEY.md §8(d)); bit-identical on host and device.
 inline double c5_uniform(std::uint64_t seed, std::uint64_t counter) {

@@ -6,10 +6,62 @@
 #include <cstring>
 #include <map>
 
+#include <nccl.h>
+
 #include "problem.hpp"
 
 namespace rtlr {
 namespace cuda {
+
+#define RTLR_NCCL(call)                                                                        \
+  do {                                                                                         \
+    ncclResult_t r_ = (call);                                                                  \
+    if (r_ != ncclSuccess)                                                                     \
+      throw ::rtlr::cuda::CudaError(std::string("NCCL error ") + ncclGetErrorString(r_) + " at " + \
+                                    __FILE__ + ":" + std::to_string(__LINE__));               \
+  } while (0)
+
+void nccl_unique_id(unsigned char* out) {
+  ncclUniqueId id;
+  RTLR_NCCL(ncclGetUniqueId(&id));
+  std::memcpy(out, id.internal, NCCL_UNIQUE_ID_BYTES);
+}
+
+void Problem::set_comm(int nranks, int rank, const void* id) {
+  if (nranks < 1 || rank < 0 || rank >= nranks) throw std::invalid_argument("set_comm: bad rank layout");
+  if (comm_) {
+    ncclCommDestroy(static_cast<ncclComm_t>(comm_));
+    comm_ = nullptr;
+  }
+  nranks_ = nranks;
+  rank_ = rank;
+  if (nranks > 1 || id != nullptr) {
+    if (id == nullptr) throw std::invalid_argument("set_comm: nranks > 1 needs an NCCL unique id");
+    ncclUniqueId uid;
+    std::memcpy(uid.internal, id, NCCL_UNIQUE_ID_BYTES);
+    ncclComm_t c;
+    RTLR_CUDA(cudaSetDevice(device_));
+    RTLR_NCCL(ncclCommInitRank(&c, nranks, uid, rank));
+    comm_ = c;
+  }
+  // this rank's unique directions (mirror pairs never split, so the unique
+  // representatives of the owned angles are exactly this rank's share)
+  const std::vector<int> mine = partition_angles(hp_.cfg.n_theta, hp_.cfg.n_omega_z, nranks, rank);
+  std::vector<char> seen(uniq_rep_.size(), 0);
+  std::vector<int> reps;
+  std::vector<double> w;
+  for (int a : mine) {
+    const int u = uniq_of_[a];
+    if (seen[u]) continue;
+    seen[u] = 1;
+    reps.push_back(uniq_rep_[u]);
+    w.push_back(uniq_w_host_[u]);
+  }
+  my_n_ = static_cast<int>(reps.size());
+  my_idx_.upload(reps.data(), reps.size(), stream_);
+  my_w_.upload(w.data(), w.size(), stream_);
+  RTLR_CUDA(cudaStreamSynchronize(stream_));
+}
 
 namespace {
 
@@ -58,6 +110,7 @@ Problem::Problem(const ProblemConfig& cfg, int device) : device_(device) {
 Problem::~Problem() {
   if (device_ < 0) return;
   cudaSetDevice(device_);
+  if (comm_) ncclCommDestroy(static_cast<ncclComm_t>(comm_));
   if (copy_in_) cudaStreamDestroy(copy_in_);
   if (copy_out_) cudaStreamDestroy(copy_out_);
   if (stream_) cudaStreamSynchronize(stream_);
@@ -312,10 +365,19 @@ SolveReport Problem::solve_full_rank(const FullRankOptions& o) {
   double *phi = base, *phi_star = base + n, *rc = base + 2 * n, *delta = base + 3 * n;
   double* psi_u = base + 5 * n;
   RTLR_CUDA(cudaMemsetAsync(phi, 0, n * sizeof(double), stream_));
+  // Direction sharding: with a communicator this rank sweeps only its share
+  // of the unique directions and the partial scalar fluxes are summed
+  // (ncclAllReduce); everything after (norms, DSA) is replicated.
+  const bool sharded = comm_ != nullptr;
+  const int nsweep = sharded ? my_n_ : nu;
+  const int* sweep_idx = sharded ? my_idx_.get() : angle_idx_.get();
+  const double* sweep_w = sharded ? my_w_.get() : uniq_w_.get();
   for (int it = 1; it <= o.max_iterations; ++it) {
     rhs_core(phi, rc);
-    sweep(angle_idx_.get(), nu, rc, 0, psi_u, static_cast<long long>(n));
-    phi_accumulate(static_cast<int>(n), nu, psi_u, static_cast<long long>(n), uniq_w_.get(), phi_star, stream_);
+    sweep(sweep_idx, nsweep, rc, 0, psi_u, static_cast<long long>(n));
+    phi_accumulate(static_cast<int>(n), nsweep, psi_u, static_cast<long long>(n), sweep_w, phi_star, stream_);
+    if (sharded)
+      RTLR_NCCL(ncclAllReduce(phi_star, phi_star, n, ncclDouble, ncclSum, static_cast<ncclComm_t>(comm_), stream_));
     diff_norms(static_cast<int>(n), phi_star, phi, norm_work_.get(), norm_work_.get() + 2 * kNormParts, stream_);
     RTLR_CUDA(cudaMemcpyAsync(h_pin_, norm_work_.get() + 2 * kNormParts, 2 * sizeof(double),
                               cudaMemcpyDeviceToHost, stream_));
@@ -344,7 +406,7 @@ SolveReport Problem::solve_full_rank(const FullRankOptions& o) {
   RTLR_CUDA(cudaMemcpyAsync(rep.phi.data(), phi, n * sizeof(double), cudaMemcpyDeviceToHost, stream_));
   RTLR_CUDA(cudaStreamSynchronize(stream_));
   rep.solve_seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
-  if (o.store_psi) {
+  if (o.store_psi && !sharded) {  // sharded runs keep psi distributed (not gathered)
     rep.has_psi = true;
     rep.psi.resize(n * hp_.n_omega);
     std::vector<double> pu(n * static_cast<size_t>(nu));

@@ -98,6 +98,10 @@ struct LowRankOptions {  // low_rank.hpp:146-153
   bool build_factors = true;
 };
 
+// 128-byte NCCL unique id for a new communicator (rank 0 creates it and
+// broadcasts it to the other processes).
+void nccl_unique_id(unsigned char* out);
+
 // Assembled problem resident on one GPU.
 class Problem {
  public:
@@ -134,6 +138,12 @@ class Problem {
   SolveReport solve_low_rank(const LowRankOptions& o);
 
   void check_error();  // throws runtime_error("sweep: singular local block")
+
+  // Direction sharding over ranks (one process per GPU): this rank sweeps
+  // its share of the unique directions and the scalar-flux partials are
+  // summed with ncclAllReduce.  nranks == 1 restores the unsharded path.
+  void set_comm(int nranks, int rank, const void* nccl_unique_id);
+  int nranks() const { return nranks_; }
   int device() const { return device_; }
 
   // Unique 2D transport operators: mirror directions (j1, j2) and
@@ -165,6 +175,11 @@ class Problem {
   double* h_pin_ = nullptr;  // small pinned host scratch
   std::vector<int> uniq_rep_, uniq_of_;
   std::vector<double> uniq_w_host_;
+  int nranks_ = 1, rank_ = 0;
+  void* comm_ = nullptr;  // ncclComm_t
+  DBuf<int> my_idx_;      // this rank's unique-direction representatives
+  DBuf<double> my_w_;
+  int my_n_ = 0;
 };
 
 }  // namespace cuda

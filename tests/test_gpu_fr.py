@@ -145,3 +145,15 @@ def test_c5_device_sources_match_host_generator():
     idx = [0, 1, g.n - 1, 2 * g.n + 17]
     for i in idx:
         assert host[i] == O.c5_uniform(12345, 5 * g.n + i)
+
+
+def test_sharded_full_rank_single_rank_nccl():
+    """The direction-sharded FR driver (partial phi + ncclAllReduce) on a
+    one-rank NCCL communicator reproduces the unsharded solve."""
+    a = P.Problem("C1")
+    ra = a.solve_full_rank(store_psi=0)
+    b = P.Problem("C1")
+    b.set_comm(1, 0, P.nccl_unique_id())
+    rb = b.solve_full_rank(store_psi=0)
+    assert rb.iterations == ra.iterations
+    assert rel(rb.phi, ra.phi) <= 1e-13
