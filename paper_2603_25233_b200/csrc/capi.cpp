@@ -267,6 +267,7 @@ int rtlr_cu_problem_set_option(rtlr_cu_problem* p, const char* key, double v) {
     std::string k = key;
     if (k == "pcg_rtol") p->p->pcg_rtol = v;
     else if (k == "pcg_max_iters") p->p->pcg_max_iters = static_cast<int>(v);
+    else if (k == "pcg_multigrid") p->p->pcg_multigrid = v != 0.0;
     else throw std::invalid_argument("unknown option '" + k + "'");
   });
 }

@@ -156,6 +156,90 @@ __global__ void __launch_bounds__(256) gemm_nn_kernel(long long M, int N, int K,
     }
 }
 
+// ------------------------------------------------------------ skinny GEMMs
+// N <= 16 columns (CGS batches, candidate blocks): the 64-wide tiles above
+// would waste up to 8x the flops.
+constexpr int kSkinny = 16;
+
+// C[M x N] = A^T B, A: K x M, split-K partials like gemm_tn_kernel.
+__global__ void __launch_bounds__(256) gemm_tn_skinny_kernel(int M, int N, long long K, long long kchunk,
+                                                             const double* __restrict__ A, long long lda,
+                                                             const double* __restrict__ B, long long ldb,
+                                                             double* __restrict__ out, long long ldo,
+                                                             long long split_stride) {
+  constexpr int SK = 32;
+  __shared__ double As[SK][BM + 1];
+  __shared__ double Bs[SK][kSkinny + 1];
+  const int tid = threadIdx.x, tm = tid % 16, tn = tid / 16;
+  const int m0 = blockIdx.x * BM;
+  const long long k0 = blockIdx.y * kchunk, k1 = min(K, k0 + kchunk);
+  double acc[4] = {0.0, 0.0, 0.0, 0.0};
+  for (long long kb = k0; kb < k1; kb += SK) {
+#pragma unroll
+    for (int e = 0; e < 8; ++e) {  // 32 x 64 tile of A, k fastest
+      const int idx = tid + e * 256, kk = idx % SK, mm = idx / SK;
+      const long long k = kb + kk;
+      As[kk][mm] = (k < k1 && m0 + mm < M) ? A[k + static_cast<long long>(m0 + mm) * lda] : 0.0;
+    }
+#pragma unroll
+    for (int e = 0; e < 2; ++e) {
+      const int idx = tid + e * 256, kk = idx % SK, nn = idx / SK;
+      const long long k = kb + kk;
+      Bs[kk][nn] = (k < k1 && nn < N) ? B[k + static_cast<long long>(nn) * ldb] : 0.0;
+    }
+    __syncthreads();
+    if (tn < N) {
+#pragma unroll
+      for (int kk = 0; kk < SK; ++kk) {
+        const double b = Bs[kk][tn];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) acc[i] += As[kk][tm + 16 * i] * b;
+      }
+    }
+    __syncthreads();
+  }
+  if (tn < N) {
+    double* o = out + blockIdx.y * split_stride;
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const int m = m0 + tm + 16 * i;
+      if (m < M) o[m + static_cast<long long>(tn) * ldo] = acc[i];
+    }
+  }
+}
+
+// C[M x N] (-)= A B, A: M x K (M large), B: K x N; one row per thread.
+__global__ void __launch_bounds__(256) gemm_nn_skinny_kernel(long long M, int N, int K, const double* __restrict__ A,
+                                                             long long lda, const double* __restrict__ B, long long ldb,
+                                                             double* __restrict__ C, long long ldc, bool subtract) {
+  constexpr int KC = 128;
+  __shared__ double Bs[KC][kSkinny];
+  const long long m = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x;
+  double acc[kSkinny];
+#pragma unroll
+  for (int j = 0; j < kSkinny; ++j) acc[j] = 0.0;
+  for (int kb = 0; kb < K; kb += KC) {
+    const int kc = min(KC, K - kb);
+    for (int e = threadIdx.x; e < KC * kSkinny; e += blockDim.x) {
+      const int kk = e % KC, nn = e / KC;
+      Bs[kk][nn] = (kk < kc && nn < N) ? B[kb + kk + static_cast<long long>(nn) * ldb] : 0.0;
+    }
+    __syncthreads();
+    if (m < M)
+      for (int kk = 0; kk < kc; ++kk) {
+        const double a = A[m + static_cast<long long>(kb + kk) * lda];
+#pragma unroll
+        for (int j = 0; j < kSkinny; ++j) acc[j] += a * Bs[kk][j];
+      }
+    __syncthreads();
+  }
+  if (m < M)
+    for (int j = 0; j < N; ++j) {
+      double* c = C + m + static_cast<long long>(j) * ldc;
+      *c = subtract ? *c - acc[j] : acc[j];
+    }
+}
+
 // ------------------------------------------------------------ vectors
 __global__ void gemv_n_kernel(long long n, int k, const double* __restrict__ A, long long lda,
                               const double* __restrict__ x, double alpha, double* __restrict__ y) {
@@ -692,9 +776,21 @@ void gemm_tn(int M, int N, long long K, const double* A, long long lda, const do
   int splits = tn_splits(M, N, K);
   while (splits > 1 && static_cast<size_t>(splits) * M * N > work_doubles) splits /= 2;
   long long kchunk = (K + splits - 1) / splits;
-  kchunk = ((kchunk + BK - 1) / BK) * BK;
+  kchunk = ((kchunk + 31) / 32) * 32;
   splits = static_cast<int>((K + kchunk - 1) / kchunk);
   if (splits < 1) splits = 1;
+  if (N <= kSkinny) {
+    dim3 grid((M + BM - 1) / BM, splits);
+    if (splits == 1) {
+      gemm_tn_skinny_kernel<<<grid, 256, 0, s>>>(M, N, K, kchunk, A, lda, B, ldb, C, ldc, 0);
+    } else {
+      gemm_tn_skinny_kernel<<<grid, 256, 0, s>>>(M, N, K, kchunk, A, lda, B, ldb, work, M,
+                                                 static_cast<long long>(M) * N);
+      splitk_reduce<<<grid1d(static_cast<long long>(M) * N), 256, 0, s>>>(M, N, splits, work, C, ldc);
+    }
+    RTLR_CUDA(cudaGetLastError());
+    return;
+  }
   dim3 grid((M + BM - 1) / BM, (N + BN - 1) / BN, splits);
   if (splits == 1) {
     gemm_tn_kernel<<<grid, 256, 0, s>>>(M, N, K, kchunk, A, lda, B, ldb, C, ldc, 0);
@@ -711,6 +807,12 @@ void gemm_nn(long long M, int N, int K, const double* A, long long lda, const do
   if (K <= 0) {
     if (!subtract)
       for (int j = 0; j < N; ++j) RTLR_CUDA(cudaMemsetAsync(C + j * ldc, 0, M * sizeof(double), s));
+    return;
+  }
+  if (N <= kSkinny) {
+    gemm_nn_skinny_kernel<<<static_cast<unsigned>((M + 255) / 256), 256, 0, s>>>(M, N, K, A, lda, B, ldb, C, ldc,
+                                                                                  subtract);
+    RTLR_CUDA(cudaGetLastError());
     return;
   }
   dim3 grid(static_cast<unsigned>((M + BM - 1) / BM), (N + BN - 1) / BN);

@@ -7,6 +7,7 @@
 // block and consumers sum the partials in a fixed order, so reruns are
 // bitwise identical (proj/tests/test_low_rank.cpp:441-470 contract).
 #include "linalg.cuh"
+#include "mg.cuh"
 
 namespace rtlr {
 namespace cuda {
@@ -301,6 +302,79 @@ __global__ void pcg_direction(const PcgArgs a, int it) {
   }
 }
 
+// ---- multigrid-preconditioned variants: the preconditioner application is
+// a separate V-cycle between these kernels.
+// x = 0, r = b; partials of b.b
+__global__ void pcg_init_mg(const PcgArgs a) {
+  __shared__ double sh[40];
+  double bb = 0.0;
+  for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < a.ncell; c += gridDim.x * blockDim.x) {
+    double r[4], zero[4] = {0, 0, 0, 0};
+    ld4(a.b + 4 * static_cast<size_t>(c), r);
+    st4(a.x + 4 * static_cast<size_t>(c), zero);
+    st4(a.r + 4 * static_cast<size_t>(c), r);
+#pragma unroll
+    for (int i = 0; i < 4; ++i) bb += r[i] * r[i];
+  }
+  bb = block_sum(bb, sh);
+  if (threadIdx.x == 0) a.part_bb[blockIdx.x] = bb;
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    a.state->done = 0;
+    a.state->iters = 0;
+    a.state->failed = 0;
+  }
+}
+// p = z (init) ; partials of r.z into part_rz[slot]
+__global__ void pcg_rz(const PcgArgs a, int slot, bool copy_p) {
+  if (a.state->done) return;
+  __shared__ double sh[40];
+  double rz = 0.0;
+  for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < a.ncell; c += gridDim.x * blockDim.x) {
+    double r[4], z[4];
+    ld4(a.r + 4 * static_cast<size_t>(c), r);
+    ld4(a.z + 4 * static_cast<size_t>(c), z);
+    if (copy_p) st4(a.p + 4 * static_cast<size_t>(c), z);
+#pragma unroll
+    for (int i = 0; i < 4; ++i) rz += r[i] * z[i];
+  }
+  rz = block_sum(rz, sh);
+  if (threadIdx.x == 0) a.part_rz[slot * a.nparts + blockIdx.x] = rz;
+}
+// alpha = rz/pq; x += alpha p; r -= alpha q; partials r.r
+__global__ void pcg_update_mg(const PcgArgs a, int it) {
+  if (a.state->done) return;
+  __shared__ double sh[40];
+  const double rz = sum_partials(a.part_rz + (it & 1) * a.nparts, a.nparts, sh);
+  const double pq = sum_partials(a.part_pq, a.nparts, sh);
+  if (!(pq > 0.0)) {
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+      a.state->failed = 1;
+      a.state->done = 1;
+    }
+    return;
+  }
+  const double alpha = rz / pq;
+  double rr = 0.0;
+  for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < a.ncell; c += gridDim.x * blockDim.x) {
+    const size_t o = 4 * static_cast<size_t>(c);
+    double x[4], r[4], p[4], q[4];
+    ld4(a.x + o, x);
+    ld4(a.r + o, r);
+    ld4(a.p + o, p);
+    ld4(a.q + o, q);
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      x[i] += alpha * p[i];
+      r[i] -= alpha * q[i];
+      rr += r[i] * r[i];
+    }
+    st4(a.x + o, x);
+    st4(a.r + o, r);
+  }
+  rr = block_sum(rr, sh);
+  if (threadIdx.x == 0) a.part_rr[blockIdx.x] = rr;
+}
+
 __global__ void bsr_apply_kernel(const PcgArgs a, const double* x, double* y) {
   for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < a.ncell; c += gridDim.x * blockDim.x) {
     double v[4];
@@ -348,14 +422,27 @@ void bsr_apply(const PcgArgs& a, const double* x, double* y, cudaStream_t s) {
 
 int pcg_solve(const PcgArgs& a, PcgState* host_state, cudaStream_t s) {
   const int g = a.nparts;
-  pcg_init<<<g, kThreads, 0, s>>>(a);
-  pcg_check_zero<<<1, kThreads, 0, s>>>(a);
+  if (a.mg) {
+    pcg_init_mg<<<g, kThreads, 0, s>>>(a);
+    pcg_check_zero<<<1, kThreads, 0, s>>>(a);
+    mg_vcycle(a, *a.mg, a.r, a.z, a.tmp4, s);
+    pcg_rz<<<g, kThreads, 0, s>>>(a, 0, true);
+  } else {
+    pcg_init<<<g, kThreads, 0, s>>>(a);
+    pcg_check_zero<<<1, kThreads, 0, s>>>(a);
+  }
   RTLR_CUDA(cudaGetLastError());
-  const int chunk = 32;
+  const int chunk = a.mg ? 8 : 32;
   for (int it0 = 0; it0 < a.max_iters; it0 += chunk) {
     for (int it = it0; it < it0 + chunk && it < a.max_iters; ++it) {
       pcg_spmv<<<g, kThreads, 0, s>>>(a);
-      pcg_update<<<g, kThreads, 0, s>>>(a, it);
+      if (a.mg) {
+        pcg_update_mg<<<g, kThreads, 0, s>>>(a, it);
+        mg_vcycle(a, *a.mg, a.r, a.z, a.tmp4, s);
+        pcg_rz<<<g, kThreads, 0, s>>>(a, (it + 1) & 1, false);
+      } else {
+        pcg_update<<<g, kThreads, 0, s>>>(a, it);
+      }
       pcg_direction<<<g, kThreads, 0, s>>>(a, it);
     }
     RTLR_CUDA(cudaGetLastError());

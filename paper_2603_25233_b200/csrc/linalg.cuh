@@ -22,6 +22,8 @@ struct PcgArgs {
   double *x, *r, *z, *p, *q;
   double *part_rz, *part_pq, *part_rr, *part_bb;  // part_rz has 2 x nparts
   PcgState* state;
+  const struct MgDevice* mg = nullptr;  // multigrid preconditioner (nullptr: block Jacobi)
+  double* tmp4 = nullptr;               // N_x scratch for the V-cycle
 };
 
 // out = Sigma (x - x_minus) + g   (x_minus, g optional)

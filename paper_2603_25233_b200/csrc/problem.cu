@@ -167,7 +167,32 @@ void Problem::upload() {
     }
     sip_.upload(soa.data(), soa.size(), s);
     jac_.upload(jac.data(), jac.size(), s);
-    pcg_vec_.ensure(5 * static_cast<size_t>(h.ndof));
+    pcg_vec_.ensure(6 * static_cast<size_t>(h.ndof));
+    // multigrid hierarchy for the preconditioner (mg.cuh)
+    std::vector<double> cinv;
+    const std::vector<MgLevelHost> lv = build_mg_hierarchy(h.nx, h.ny, h.sip, 64, cinv);
+    mg_bufs_.clear();
+    mg_ = MgDevice{};
+    mg_.nlev = static_cast<int>(lv.size());
+    auto alloc = [&](size_t n) {
+      mg_bufs_.push_back(std::make_unique<DBuf<double>>());
+      return mg_bufs_.back()->ensure(n);
+    };
+    for (const MgLevelHost& L : lv) {
+      const size_t n = static_cast<size_t>(L.nx) * L.ny;
+      mg_.nx.push_back(L.nx);
+      mg_.ny.push_back(L.ny);
+      double* st = alloc(5 * n);
+      RTLR_CUDA(cudaMemcpyAsync(st, L.st.data(), 5 * n * sizeof(double), cudaMemcpyHostToDevice, s));
+      mg_.st.push_back(st);
+      mg_.x.push_back(alloc(n));
+      mg_.b.push_back(alloc(n));
+      mg_.t.push_back(alloc(n));
+    }
+    mg_.ncoarse = lv.back().nx * lv.back().ny;
+    mg_.cinv = alloc(cinv.size());
+    RTLR_CUDA(cudaMemcpyAsync(mg_.cinv, cinv.data(), cinv.size() * sizeof(double), cudaMemcpyHostToDevice, s));
+    RTLR_CUDA(cudaStreamSynchronize(s));
     pcg_part_.ensure(5 * static_cast<size_t>(kNormParts));
     pcg_state_.ensure(1);
   }
@@ -318,6 +343,10 @@ PcgArgs Problem::pcg_args(const double* b, double* x) {
   a.part_rr = part + 3 * kNormParts;
   a.part_bb = part + 4 * kNormParts;
   a.state = pcg_state_.get();
+  if (pcg_multigrid) {
+    a.mg = &mg_;
+    a.tmp4 = v + 5 * n;
+  }
   return a;
 }
 

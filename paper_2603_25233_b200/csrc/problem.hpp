@@ -10,6 +10,7 @@
 #include "device.cuh"
 #include "host.hpp"
 #include "linalg.cuh"
+#include "mg.cuh"
 
 namespace rtlr {
 namespace cuda {
@@ -153,6 +154,7 @@ class Problem {
 
   double pcg_rtol = 1e-13;
   int pcg_max_iters = 20000;
+  bool pcg_multigrid = true;  // false: block-Jacobi PCG
 
  private:
   friend class LowRankEngine;
@@ -171,6 +173,8 @@ class Problem {
   DBuf<int> hang_;
   cudaStream_t copy_in_ = nullptr, copy_out_ = nullptr;
   DBuf<PcgState> pcg_state_;
+  std::vector<std::unique_ptr<DBuf<double>>> mg_bufs_;
+  MgDevice mg_;
   PcgState* h_state_ = nullptr;
   double* h_pin_ = nullptr;  // small pinned host scratch
   std::vector<int> uniq_rep_, uniq_of_;
