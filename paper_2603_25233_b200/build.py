@@ -51,6 +51,22 @@ def _compile(src: str, verbose: bool) -> str:
     return obj
 
 
+def _nccl_link():
+    """Link the NCCL that torch itself loads (the venv's nvidia-nccl wheel)
+    when present: a process that loads this library before `import torch`
+    would otherwise bind the older system libnccl.so.2 first and torch's
+    libtorch_cuda.so then fails on symbols only the newer NCCL exports."""
+    try:
+        import nvidia.nccl  # type: ignore
+        for root in nvidia.nccl.__path__:
+            d = os.path.join(root, "lib")
+            if os.path.exists(os.path.join(d, "libnccl.so.2")):
+                return ["-L" + d, "-l:libnccl.so.2", "-Xlinker", "-rpath=" + d]
+    except ImportError:
+        pass
+    return ["-L/usr/lib/x86_64-linux-gnu", "-lnccl"]
+
+
 def build(verbose: bool = False) -> str:
     os.makedirs(OBJ_DIR, exist_ok=True)
     with cf.ThreadPoolExecutor(max_workers=min(8, os.cpu_count() or 1)) as ex:
@@ -58,7 +74,7 @@ def build(verbose: bool = False) -> str:
     newest = max(os.path.getmtime(o) for o in objs)
     if not os.path.exists(LIB) or os.path.getmtime(LIB) < newest:
         cmd = [NVCC, *GENCODE, "-shared", "-o", LIB, *objs, "-lcudart_static", "-lrt", "-ldl", "-lpthread",
-               "-L/usr/lib/x86_64-linux-gnu", "-lnccl"]
+               *_nccl_link()]
         r = subprocess.run(cmd, capture_output=True, text=True)
         if r.returncode != 0:
             raise RuntimeError(f"link failed:\n{r.stdout}\n{r.stderr}")

@@ -65,7 +65,11 @@ struct SweepArgs {
   StreamDev sc;
 };
 
+// Skewed lane-per-row wavefront (sweep.cu) and row-chunk affine-scan
+// (sweep_scan.cu) formulations of K1; Problem::sweep picks the scan kernel
+// unless RTLR_SWEEP=skew.
 void launch_sweep(const SweepArgs& a, bool uniform_sigma_t, cudaStream_t s);
+void launch_sweep_scan(const SweepArgs& a, bool uniform_sigma_t, cudaStream_t s);
 
 // Generates C5 sources: rhs[k][dof] = U[0,1)(seed, (dir0+k)*ndof + dof).
 void launch_c5_fill(double* rhs, long long n_dirs, long long dir0, long long ndof,

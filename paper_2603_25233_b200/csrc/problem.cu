@@ -3,6 +3,7 @@
 #include <algorithm>
 #include <chrono>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 
@@ -253,10 +254,17 @@ void Problem::sweep(const int* d_angles, int n, const double* d_rhs, long long r
   a.psi = d_psi;
   a.psi_stride = psi_stride;
   a.sigma_t = sigma_t_.get();
-  a.line = line_.ensure(static_cast<size_t>(n) * 8 * hp_.nx * 2);  // up to 8 warps per direction
+  a.line = line_.ensure(static_cast<size_t>(n) * 8 * (hp_.nx + 1) * 2);  // up to 8 warps per direction
   a.err = err_.get();
   a.sc = sc_;
-  launch_sweep(a, hp_.sigma_t_uniform, stream_);
+  static const bool skew = [] {
+    const char* e = std::getenv("RTLR_SWEEP");
+    return e && std::string(e) == "skew";
+  }();
+  if (skew)
+    launch_sweep(a, hp_.sigma_t_uniform, stream_);
+  else
+    launch_sweep_scan(a, hp_.sigma_t_uniform, stream_);
 }
 
 void Problem::sweep_host(const int* h_angles, int n, const double* h_rhs, long long rhs_stride, double* h_psi,
