@@ -48,7 +48,9 @@ def parse():
     ap.add_argument("--e2e-chunk", type=int, default=256, help="directions per host-buffer call")
     ap.add_argument("--no-solvers", action="store_true", help="skip the C1/C2 time-to-tol extras")
     ap.add_argument("--no-e2e", action="store_true")
-    ap.add_argument("--cpu-sample-dirs", type=int, default=8)
+    ap.add_argument("--no-cpu", action="store_true", help="skip the CPU baseline sample")
+    ap.add_argument("--cpu-sample-updates", type=float, default=8e7,
+                    help="CPU baseline sample size in cell-angle updates (~10 s of one core)")
     return ap.parse_args()
 
 
@@ -317,10 +319,11 @@ def main():
             del sp
 
     cpu = None
-    if rank == 0 and world == 1:
-        r, upd, dt = cpu_sweep_rate(args.grid, args.n_theta, args.n_omega_z, args.cpu_sample_dirs, 1)
+    if rank == 0 and world == 1 and not args.no_cpu:
+        ndirs = max(1, min(D, int(args.cpu_sample_updates // cells)))
+        r, upd, dt = cpu_sweep_rate(args.grid, args.n_theta, args.n_omega_z, ndirs, 1)
         cpu = {"value": r, "unit": "cell-angle updates/s", "cores": 1, "kind": "port",
-               "sample": f"{args.cpu_sample_dirs} directions x {args.grid}^2 cells ({upd} updates, {dt:.1f} s)"}
+               "sample": f"{ndirs} directions x {args.grid}^2 cells ({upd} updates, {dt:.1f} s)"}
 
     if rank == 0:
         line = {

@@ -385,21 +385,36 @@ __global__ void __launch_bounds__(256, 2) sweep_scan_kernel(const SweepArgs a, i
     v1[3] -= ky1 * y11;
 
     double ps0[4], ps1[4];
+    // Constants are re-read from shared memory every step as 16-byte
+    // broadcasts (one wavefront each); registers hold only the stream state.
+    const double2* c2 = reinterpret_cast<const double2*>(cst);
     if (UNIFORM) {
       double u0[4], u1[4];
 #pragma unroll
-      for (int i = 0; i < 4; ++i) {
-        u0[i] = cst[i] * v0[0] + cst[4 + i] * v0[1] + cst[8 + i] * v0[2] + cst[12 + i] * v0[3];
-        u1[i] = cst[i] * v1[0] + cst[4 + i] * v1[1] + cst[8 + i] * v1[2] + cst[12 + i] * v1[3];
+      for (int c = 0; c < 4; ++c) {  // u = M^-1 v, column by column
+        const double2 lo = c2[2 * c], hi = c2[2 * c + 1];
+        if (c == 0) {
+          u0[0] = lo.x * v0[0], u0[1] = lo.y * v0[0], u0[2] = hi.x * v0[0], u0[3] = hi.y * v0[0];
+          u1[0] = lo.x * v1[0], u1[1] = lo.y * v1[0], u1[2] = hi.x * v1[0], u1[3] = hi.y * v1[0];
+        } else {
+          u0[0] += lo.x * v0[c], u0[1] += lo.y * v0[c], u0[2] += hi.x * v0[c], u0[3] += hi.y * v0[c];
+          u1[0] += lo.x * v1[c], u1[1] += lo.y * v1[c], u1[2] += hi.x * v1[c], u1[3] += hi.y * v1[c];
+        }
       }
-      // f = T_x u (per y-mode); lane map over its two cells: tau -> G^2 tau + (G f0 + f1)
+      // f = T_x u (per y-mode); lane map over its two cells: tau -> G^2 tau + (G f0 + f1).
+      // The chunk's carry enters lane 0's map before the scan, so the
+      // inclusive scan yields tau after each lane's last cell directly.
       const double f00 = tx0 * u0[0] + tx1 * u0[1], f01 = tx0 * u0[2] + tx1 * u0[3];
       const double f10 = tx0 * u1[0] + tx1 * u1[1], f11 = tx0 * u1[2] + tx1 * u1[3];
-      const double* Gc = cst + kG;
-      double s0, s1;
-      mat2_vec(Gc, f00, f01, s0, s1);
-      s0 += f10;
-      s1 += f11;
+      const double2 g01 = c2[kG / 2], g23 = c2[kG / 2 + 1];
+      double s0 = f10 + g01.x * f00 + g23.x * f01;
+      double s1 = f11 + g01.y * f00 + g23.y * f01;
+      {
+        const double2 p01 = c2[kGP / 2], p23 = c2[kGP / 2 + 1];  // G^2
+        const double t0 = lane == 0 ? tc0 : 0.0, t1 = lane == 0 ? tc1 : 0.0;
+        s0 += p01.x * t0 + p23.x * t1;
+        s1 += p01.y * t0 + p23.y * t1;
+      }
       // inclusive scan over the lanes: s_l <- s_l + G^(2d) s_{l-d}
 #pragma unroll
       for (int l = 0; l < 5; ++l) {
@@ -408,28 +423,24 @@ __global__ void __launch_bounds__(256, 2) sweep_scan_kernel(const SweepArgs a, i
         double o1 = __shfl_up_sync(0xffffffffu, s1, d);
         o0 = lane >= d ? o0 : 0.0;
         o1 = lane >= d ? o1 : 0.0;
-        const double* P = cst + kGP + 4 * (d - 1);
-        s0 += P[0] * o0 + P[2] * o1;
-        s1 += P[1] * o0 + P[3] * o1;
+        const double2 p01 = c2[(kGP + 4 * (d - 1)) / 2], p23 = c2[(kGP + 4 * (d - 1)) / 2 + 1];
+        s0 += p01.x * o0 + p23.x * o1;
+        s1 += p01.y * o0 + p23.y * o1;
       }
-      double e0, e1;  // tau after this lane's last cell = s + G^(2(l+1)) tau_c
-      mat2_vec(cst + kGP + 4 * lane, tc0, tc1, e0, e1);
-      e0 += s0;
-      e1 += s1;
-      double ti0 = __shfl_up_sync(0xffffffffu, e0, 1), ti1 = __shfl_up_sync(0xffffffffu, e1, 1);
+      double ti0 = __shfl_up_sync(0xffffffffu, s0, 1), ti1 = __shfl_up_sync(0xffffffffu, s1, 1);
       if (lane == 0) ti0 = tc0, ti1 = tc1;
-      tc0 = __shfl_sync(0xffffffffu, e0, 31);
-      tc1 = __shfl_sync(0xffffffffu, e1, 31);
+      tc0 = __shfl_sync(0xffffffffu, s0, 31);
+      tc1 = __shfl_sync(0xffffffffu, s1, 31);
       // psi = u + Q tau_in, cell by cell
-      const double* Q = cst + kQ;
+      const double m0 = f00 + g01.x * ti0 + g23.x * ti1, m1 = f01 + g01.y * ti0 + g23.y * ti1;
 #pragma unroll
-      for (int i = 0; i < 4; ++i) ps0[i] = u0[i] + Q[i] * ti0 + Q[4 + i] * ti1;
-      double m0, m1;
-      mat2_vec(Gc, ti0, ti1, m0, m1);
-      m0 += f00;
-      m1 += f01;
-#pragma unroll
-      for (int i = 0; i < 4; ++i) ps1[i] = u1[i] + Q[i] * m0 + Q[4 + i] * m1;
+      for (int h = 0; h < 2; ++h) {
+        const double2 qa = c2[kQ / 2 + h], qb = c2[kQ / 2 + 2 + h];  // Q[2h..2h+1], Q[4+2h..]
+        ps0[2 * h] = u0[2 * h] + qa.x * ti0 + qb.x * ti1;
+        ps0[2 * h + 1] = u0[2 * h + 1] + qa.y * ti0 + qb.y * ti1;
+        ps1[2 * h] = u1[2 * h] + qa.x * m0 + qb.x * m1;
+        ps1[2 * h + 1] = u1[2 * h + 1] + qa.y * m0 + qb.y * m1;
+      }
     } else {
       // per cell: [u | Qc] = M_a^-1 [local | -K_x], G_a = T_x Qc, f_a = T_x u
       double Qc0[8], Qc1[8];
@@ -439,9 +450,9 @@ __global__ void __launch_bounds__(256, 2) sweep_scan_kernel(const SweepArgs a, i
         const double2* sb = reinterpret_cast<const double2*>(a.sigma_t + 16 * cell0);
 #pragma unroll
         for (int e = 0; e < 8; ++e) {
-          const double2 s2 = __ldg(sb + e);
-          A[2 * e] = cst[2 * e] + s2.x;
-          A[2 * e + 1] = cst[2 * e + 1] + s2.y;
+          const double2 s2 = __ldg(sb + e), m2 = c2[e];
+          A[2 * e] = m2.x + s2.x;
+          A[2 * e + 1] = m2.y + s2.y;
         }
         double b1[4] = {-kx0, -kx1, 0.0, 0.0}, b2[4] = {0.0, 0.0, -kx0, -kx1};
         ok0 = lu_solve4x3(A, v0, b1, b2);
@@ -453,9 +464,9 @@ __global__ void __launch_bounds__(256, 2) sweep_scan_kernel(const SweepArgs a, i
         const double2* sb = reinterpret_cast<const double2*>(a.sigma_t + 16 * cell1);
 #pragma unroll
         for (int e = 0; e < 8; ++e) {
-          const double2 s2 = __ldg(sb + e);
-          A[2 * e] = cst[2 * e] + s2.x;
-          A[2 * e + 1] = cst[2 * e + 1] + s2.y;
+          const double2 s2 = __ldg(sb + e), m2 = c2[e];
+          A[2 * e] = m2.x + s2.x;
+          A[2 * e + 1] = m2.y + s2.y;
         }
         double b1[4] = {-kx0, -kx1, 0.0, 0.0}, b2[4] = {0.0, 0.0, -kx0, -kx1};
         ok1 = lu_solve4x3(A, v1, b1, b2);
@@ -480,6 +491,11 @@ __global__ void __launch_bounds__(256, 2) sweep_scan_kernel(const SweepArgs a, i
       mat2_vec(G1, f00, f01, s0, s1);
       s0 += f10;
       s1 += f11;
+      {  // the chunk's carry enters lane 0's map
+        const double t0 = lane == 0 ? tc0 : 0.0, t1 = lane == 0 ? tc1 : 0.0;
+        s0 += A0 * t0 + A2 * t1;
+        s1 += A1 * t0 + A3 * t1;
+      }
 #pragma unroll
       for (int l = 0; l < 5; ++l) {
         const int d = 1 << l;
@@ -503,11 +519,10 @@ __global__ void __launch_bounds__(256, 2) sweep_scan_kernel(const SweepArgs a, i
         A2 = n2;
         A3 = n3;
       }
-      const double e0 = s0 + A0 * tc0 + A2 * tc1, e1 = s1 + A1 * tc0 + A3 * tc1;
-      double ti0 = __shfl_up_sync(0xffffffffu, e0, 1), ti1 = __shfl_up_sync(0xffffffffu, e1, 1);
+      double ti0 = __shfl_up_sync(0xffffffffu, s0, 1), ti1 = __shfl_up_sync(0xffffffffu, s1, 1);
       if (lane == 0) ti0 = tc0, ti1 = tc1;
-      tc0 = __shfl_sync(0xffffffffu, e0, 31);
-      tc1 = __shfl_sync(0xffffffffu, e1, 31);
+      tc0 = __shfl_sync(0xffffffffu, s0, 31);
+      tc1 = __shfl_sync(0xffffffffu, s1, 31);
 #pragma unroll
       for (int i = 0; i < 4; ++i) ps0[i] = v0[i] + Qc0[i] * ti0 + Qc0[4 + i] * ti1;
       double m0, m1;
