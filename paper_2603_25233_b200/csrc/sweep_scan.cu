@@ -11,14 +11,22 @@
 // in chunks of 64 consecutive cells, two adjacent cells per lane (so every
 // warp-wide load/store covers one contiguous 2 KB segment), composes its two
 // cells' maps locally and resolves the recurrence across the lanes with a
-// 5-level branch-free shuffle scan of affine maps; the carry tau passes from
-// chunk to chunk.  Rows run in upwind order; the y-upwind traces of the
-// previous row live in a per-warp trace line (two planes, one per x-mode;
-// shared memory, or L2 for very wide rows).  Sources stream in one chunk
-// ahead through registers and kAhead chunks ahead through bulk L2 prefetches.
-// With W > 1 warps per direction, warp w owns rows w, w+W, ... and reads the
-// line of warp w-1 behind a per-chunk progress counter (data-ready waits
-// only, along the sweep DAG: no cycles).
+// 5-level shuffle scan of affine maps (predicated FMAs, no selects); the
+// chunk's carry tau enters lane 0's map, so the scan yields every lane's tau
+// directly.  Rows run in upwind order; the y-upwind traces of the previous
+// row live in a per-warp trace line (two planes, one per x-mode; shared
+// memory, or L2 for very wide rows).  Sources stream in one step ahead
+// through registers (two register sets, the loop unrolled by two) and a few
+// chunks ahead through bulk L2 prefetches.  With W > 1 warps per direction,
+// warp w owns rows w, w+W, ... and reads the line of warp w-1 behind a
+// per-chunk progress counter (acquire/release; data-ready waits only, along
+// the sweep DAG: no cycles).
+//
+// The sweep loop is specialised on the x-direction sign, so cell addresses
+// advance by a compile-time stride and a lane's second cell is an immediate
+// +-32 B offset.  Everything per step is sized to keep SM-side work (issue
+// slots, shared-memory wavefronts) low: the kernel must stay HBM-bound when
+// the board power cap pulls the SM clock down under sustained load.
 //
 // Uniform media (every Sigma_t block bitwise equal) use one per-direction
 // inverse M^-1, so G is constant and only the 2-vector f is scanned; general
@@ -132,17 +140,19 @@ __device__ __forceinline__ void st_cell256(double* p, const double v[4]) {
                "d"(v[3])
                : "memory");
 }
-// Bulk prefetch of [p, p + bytes) into L2 (one instruction per chunk).
+// Bulk prefetch of [p, p + bytes) into L2 (one instruction per unit).
 __device__ __forceinline__ void prefetch_l2(const double* p, unsigned bytes) {
   asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ unsigned smem_u32(const void* p) {
+  return static_cast<unsigned>(__cvta_generic_to_shared(p));
 }
 // Trace-line access: explicit shared-memory or L2 (.cg) instructions, so the
 // compiler never falls back to generic loads for the smem case.
 __device__ __forceinline__ double2 ld_line(const double* p, bool smem) {
   double2 v;
   if (smem) {
-    const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(p));
-    asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];" : "=d"(v.x), "=d"(v.y) : "r"(s) : "memory");
+    asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];" : "=d"(v.x), "=d"(v.y) : "r"(smem_u32(p)) : "memory");
   } else {
     asm volatile("ld.global.cg.v2.f64 {%0, %1}, [%2];" : "=d"(v.x), "=d"(v.y) : "l"(p) : "memory");
   }
@@ -150,18 +160,54 @@ __device__ __forceinline__ double2 ld_line(const double* p, bool smem) {
 }
 __device__ __forceinline__ void st_line(double* p, double x, double y, bool smem) {
   if (smem) {
-    const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(p));
-    asm volatile("st.shared.v2.f64 [%0], {%1, %2};" ::"r"(s), "d"(x), "d"(y) : "memory");
+    asm volatile("st.shared.v2.f64 [%0], {%1, %2};" ::"r"(smem_u32(p)), "d"(x), "d"(y) : "memory");
   } else {
     asm volatile("st.global.cg.v2.f64 [%0], {%1, %2};" ::"l"(p), "d"(x), "d"(y) : "memory");
   }
+}
+// Progress counters (shared memory), CTA-scope acquire/release: the
+// producer and consumer warps share the CTA, whichever state space (shared
+// memory or L2) holds the trace lines.
+__device__ __forceinline__ void wait_progress(const int* p, int need) {
+  int v;
+  do {
+    asm volatile("ld.acquire.cta.shared.b32 %0, [%1];" : "=r"(v) : "r"(smem_u32(p)) : "memory");
+  } while (v < need);
+}
+__device__ __forceinline__ void publish_progress(int* p, int v) {
+  asm volatile("st.release.cta.shared.b32 [%0], %1;" ::"r"(smem_u32(p)), "r"(v) : "memory");
+}
+// fp64 shuffles as two 32-bit shuffles on the register pair (keeps the
+// compiler from reshuffling the halves).
+__device__ __forceinline__ double shfl_up_f64(double x, int d) {
+  double r;
+  asm("{\n\t.reg .b32 lo, hi;\n\tmov.b64 {lo, hi}, %1;\n\t"
+      "shfl.sync.up.b32 lo, lo, %2, 0, -1;\n\tshfl.sync.up.b32 hi, hi, %2, 0, -1;\n\t"
+      "mov.b64 %0, {lo, hi};\n\t}"
+      : "=d"(r)
+      : "d"(x), "r"(d));
+  return r;
+}
+__device__ __forceinline__ double shfl_idx_f64(double x, int src) {
+  double r;
+  asm("{\n\t.reg .b32 lo, hi;\n\tmov.b64 {lo, hi}, %1;\n\t"
+      "shfl.sync.idx.b32 lo, lo, %2, 31, -1;\n\tshfl.sync.idx.b32 hi, hi, %2, 31, -1;\n\t"
+      "mov.b64 %0, {lo, hi};\n\t}"
+      : "=d"(r)
+      : "d"(x), "r"(src));
+  return r;
+}
+// s += P o (2 x 2, P column-major as two double2).
+__device__ __forceinline__ void fma2(double& s0, double& s1, double2 p01, double2 p23, double o0, double o1) {
+  s0 = fma(p23.x, o1, fma(p01.x, o0, s0));
+  s1 = fma(p23.y, o1, fma(p01.y, o0, s1));
 }
 
 constexpr int kLineSmemBudget = 96 * 1024;  // bytes of trace lines per block kept in smem
 constexpr int kWarps = 8;                   // warps per block
 constexpr int kCpl = 2;                     // adjacent cells per lane
 constexpr int kChunk = 32 * kCpl;           // cells per warp step
-constexpr int kAhead = 4;                   // chunks prefetched into L2 ahead of the sweep
+constexpr int kAheadChunks = 4;             // minimum L2 prefetch distance (chunks)
 
 // Per-direction constants (shared memory, written by warp 0 of the group):
 //   [0..16)   M^-1 (uniform) or Omega_x Ax + Omega_y Ay (general), column-major
@@ -177,197 +223,104 @@ __host__ __device__ constexpr int group_doubles(int W, int nx, bool smem_lines) 
   return kConsts + 2 * ((W + 3) / 4) + (smem_lines ? W * 2 * line_pitch(nx) : 0);
 }
 
-struct Group {
-  double* c;           // kConsts
-  volatile int* prod;  // W progress counters (chunks published)
-  double* lines;       // W x 2 planes x pitch
-};
-
 __device__ __forceinline__ void mat2_vec(const double* G, double x0, double x1, double& y0, double& y1) {
   y0 = G[0] * x0 + G[2] * x1;  // column-major 2 x 2
   y1 = G[1] * x0 + G[3] * x1;
 }
 
-template <bool UNIFORM, bool MULTI, bool HAS_BC>
-__global__ void __launch_bounds__(256, 2) sweep_scan_kernel(const SweepArgs a, int W, bool smem_lines) {
-  extern __shared__ double smem[];
+// One warp's share of one direction.
+struct Dir {
+  const double* rhs;
+  const double* bc;
+  double* psi;
+  const double* sigma_t;
+  const double* cst;  // shared memory, kConsts
+  int* prod;          // shared memory, W progress counters
+  double* my_line;
+  const double* in_line;
+  int* err;
+  int nx, ny, W, w, pw, nchunk, nrows, pitch;
+  bool yu, smem_lines;
+};
+
+template <bool UNIFORM, bool MULTI, bool HAS_BC, bool XU>
+__device__ __forceinline__ void sweep_dir(const Dir& d) {
+  constexpr int kDx = XU ? 1 : -1;  // cell index step along the sweep
   const int lane = threadIdx.x & 31;
-  const int wib = threadIdx.x >> 5;
-  const int groups = kWarps / W;
-  const int g = wib / W, w = wib % W;
-  const int slot = blockIdx.x * groups + g;
-  if (slot >= a.n) return;  // a whole direction group exits together
-  const int nx = a.nx, ny = a.ny;
-  const int pitch = line_pitch(nx);
-  Group G;
-  {
-    double* base = smem + static_cast<size_t>(g) * group_doubles(W, nx, smem_lines);
-    G.c = base;
-    G.prod = reinterpret_cast<int*>(base + kConsts);
-    G.lines = smem_lines ? base + kConsts + 2 * ((W + 3) / 4)
-                         : a.line + static_cast<size_t>(slot) * W * 2 * pitch;
-  }
-  const int ang = a.angles ? a.angles[slot] : slot;
-  const double omx = a.dirs[3 * ang], omy = a.dirs[3 * ang + 1];
-  const bool xu = omx >= 0.0, yu = omy >= 0.0;  // sweep.cpp:37-38
-  if (w == 0) {
-    const double* ax = xu ? a.sc.ax_minus : a.sc.ax_plus;
-    const double* ay = yu ? a.sc.ay_minus : a.sc.ay_plus;
-    if (lane < 16) {
-      const double d = omx * ax[lane] + omy * ay[lane];
-      G.c[lane] = UNIFORM ? d + a.sigma_t[lane] : d;
-    }
-    if (lane < 2) {
-      // (B psi_up)[my,mx] = c[mx] (t . psi_up[my,:]), (c,t) = (-t_L,t_R) minus / (t_R,t_L) plus
-      G.c[kKT + lane] = omx * (xu ? -a.sc.trx_l[lane] : a.sc.trx_r[lane]);
-      G.c[kKT + 2 + lane] = xu ? a.sc.trx_r[lane] : a.sc.trx_l[lane];
-      G.c[kKT + 4 + lane] = omy * (yu ? -a.sc.try_l[lane] : a.sc.try_r[lane]);
-      G.c[kKT + 6 + lane] = yu ? a.sc.try_r[lane] : a.sc.try_l[lane];
-    }
-    __syncwarp();
-    if (UNIFORM && lane == 0) {
-      // M^-1 columns via the reference LU; Q = -M^-1 K_x; G = T_x Q; (G^2)^(l+1)
-      double Mi[16];
-      for (int c = 0; c < 4; c += 3) {
-        double A[16], e0[4] = {0, 0, 0, 0}, e1[4] = {0, 0, 0, 0}, e2[4] = {0, 0, 0, 0};
-        for (int k = 0; k < 16; ++k) A[k] = G.c[k];
-        e0[c] = 1.0;
-        if (c + 1 < 4) e1[c + 1] = 1.0;
-        if (c + 2 < 4) e2[c + 2] = 1.0;
-        if (!lu_solve4x3(A, e0, e1, e2)) atomicExch(a.err, 1);
-        for (int r = 0; r < 4; ++r) {
-          Mi[c * 4 + r] = e0[r];
-          if (c + 1 < 4) Mi[(c + 1) * 4 + r] = e1[r];
-          if (c + 2 < 4) Mi[(c + 2) * 4 + r] = e2[r];
-        }
-      }
-      const double kx0 = G.c[kKT], kx1 = G.c[kKT + 1], tx0 = G.c[kKT + 2], tx1 = G.c[kKT + 3];
-      // K_x (4 x 2): column my has kx[mx] at rows (my, mx)
-      double Q[8];
-      for (int my = 0; my < 2; ++my)
-        for (int r = 0; r < 4; ++r)
-          Q[my * 4 + r] = -(Mi[(my * 2 + 0) * 4 + r] * kx0 + Mi[(my * 2 + 1) * 4 + r] * kx1);
-      // G = T_x Q (2 x 2): row m = tx . Q[(m,0..1), :]
-      double Gm[4];
-      for (int col = 0; col < 2; ++col)
-        for (int m = 0; m < 2; ++m) Gm[col * 2 + m] = tx0 * Q[col * 4 + m * 2] + tx1 * Q[col * 4 + m * 2 + 1];
-      for (int k = 0; k < 16; ++k) G.c[k] = Mi[k];
-      for (int k = 0; k < 8; ++k) G.c[kQ + k] = Q[k];
-      for (int e = 0; e < 4; ++e) G.c[kG + e] = Gm[e];
-      double G2[4];
-      for (int col = 0; col < 2; ++col)
-        for (int m = 0; m < 2; ++m) G2[col * 2 + m] = Gm[m] * Gm[col * 2] + Gm[2 + m] * Gm[col * 2 + 1];
-      double P[4] = {G2[0], G2[1], G2[2], G2[3]};
-      for (int k = 0; k < 32; ++k) {
-        for (int e = 0; e < 4; ++e) G.c[kGP + 4 * k + e] = P[e];
-        double N[4];
-        for (int col = 0; col < 2; ++col)
-          for (int m = 0; m < 2; ++m) N[col * 2 + m] = G2[m] * P[col * 2] + G2[2 + m] * P[col * 2 + 1];
-        for (int e = 0; e < 4; ++e) P[e] = N[e];
-      }
-    }
-    if (lane < W) G.prod[lane] = 0;
-  }
-  asm volatile("bar.sync %0, %1;" ::"r"(g + 1), "r"(W * 32) : "memory");
-
-  const double* cst = G.c;
-  const double kx0 = cst[kKT], kx1 = cst[kKT + 1], tx0 = cst[kKT + 2], tx1 = cst[kKT + 3];
-  const double ky0 = cst[kKT + 4], ky1 = cst[kKT + 5], ty0 = cst[kKT + 6], ty1 = cst[kKT + 7];
-
-  const int nchunk = (nx + kChunk - 1) / kChunk;
-  const int nrows = (ny - w + W - 1) / W;  // rows w, w+W, ... of this warp
-  const int nsteps = nrows * nchunk;
-  const double* rhs = a.rhs + static_cast<long long>(slot) * a.rhs_stride;
-  const double* bc = HAS_BC ? a.bc + static_cast<long long>(ang) * a.bc_stride : nullptr;
-  double* psi = a.psi + static_cast<long long>(slot) * a.psi_stride;
-  const int pw = (w + W - 1) % W;
-  double* my_line = G.lines + static_cast<size_t>(w) * 2 * pitch;
-  const double* in_line = G.lines + static_cast<size_t>(pw) * 2 * pitch;
+  const int nx = d.nx, nchunk = d.nchunk, nrows = d.nrows;
   const int c0 = kCpl * lane;  // this lane's first sweep column within a chunk
+  const double kx0 = d.cst[kKT], kx1 = d.cst[kKT + 1], tx0 = d.cst[kKT + 2], tx1 = d.cst[kKT + 3];
+  const double ky0 = d.cst[kKT + 4], ky1 = d.cst[kKT + 5], ty0 = d.cst[kKT + 6], ty1 = d.cst[kKT + 7];
+  const double2* c2 = reinterpret_cast<const double2*>(d.cst);
 
-  auto row_base = [&](int rowk) -> long long {
-    const int r = w + rowk * W;
-    return static_cast<long long>(yu ? r : ny - 1 - r) * nx;
+  auto row0_of = [&](int rowk) -> long long {
+    const int r = d.w + rowk * d.W;
+    return static_cast<long long>(d.yu ? r : d.ny - 1 - r) * nx;
   };
-  // cell of sweep column col (clamped to a valid cell past the row end)
-  auto cell_of = [&](long long row0, int col) -> long long {
-    return row0 + (col < nx ? (xu ? col : nx - 1 - col) : 0);
-  };
-  auto prefetch_chunk = [&](int rowk, int k) {
-    const long long r0 = row_base(rowk);
-    const int lo = k * kChunk, cnt = min(kChunk, nx - lo);
-    const long long first = xu ? r0 + lo : r0 + nx - lo - cnt;
-    prefetch_l2(rhs + 4 * first, static_cast<unsigned>(cnt) * 32u);
-    if (HAS_BC) prefetch_l2(bc + 4 * first, static_cast<unsigned>(cnt) * 32u);
-  };
+  // this lane's first cell in row ordinal rowk
+  auto first_cell = [&](int rowk) -> long long { return row0_of(rowk) + (XU ? c0 : nx - 1 - c0); };
 
-  int prow = 0, pk = 0;  // L2 prefetch position, kAhead chunks in front
-  if (lane == 0) {
-    for (int t = 0; t < kAhead + 1 && prow < nrows; ++t) {
-      prefetch_chunk(prow, pk);
-      if (++pk == nchunk) pk = 0, ++prow;
+  // L2 prefetch, one chunk per step kAheadChunks ahead, issued by lane 0;
+  // (prow, pk) walks the chunks in sweep order.
+  int prow = 0, pk = 0;
+  long long prow0 = row0_of(0);
+  auto prefetch_next = [&]() {
+    if (prow >= nrows) return;
+    const int lo = pk * kChunk, cnt = min(kChunk, nx - lo);
+    const long long first = prow0 + (XU ? lo : nx - lo - cnt);
+    prefetch_l2(d.rhs + 4 * first, static_cast<unsigned>(cnt) * 32u);
+    if (HAS_BC) prefetch_l2(d.bc + 4 * first, static_cast<unsigned>(cnt) * 32u);
+    if (++pk == nchunk) {
+      pk = 0;
+      if (++prow < nrows) prow0 = row0_of(prow);
     }
-  }
-  double nv0[4], nv1[4];  // next step's sources
-  long long row0 = row_base(0);
-  ld_cell256(rhs + 4 * cell_of(row0, c0), nv0);
-  ld_cell256(rhs + 4 * cell_of(row0, c0 + 1), nv1);
+  };
+  if (lane == 0)
+    for (int u = 0; u < kAheadChunks; ++u) prefetch_next();
 
+  const int nsteps = nrows * nchunk;
+  long long cell = first_cell(0);  // this lane's first cell of the current step
+  long long next_row = nrows > 1 ? first_cell(1) : 0;
   int rowk = 0, k = 0;
-  double tc0 = 0.0, tc1 = 0.0;  // x-trace carry into the chunk
-  for (int t = 0; t < nsteps; ++t) {
-    if (k == 0) tc0 = tc1 = 0.0;  // vacuum x-inflow at the row start
+  double tc0 = 0.0, tc1 = 0.0;  // x-trace carry into the chunk (lane 0)
+
+  double ra0[4], ra1[4], rb0[4], rb1[4];  // two register sets of sources
+  if (c0 < nx) ld_cell256(d.rhs + 4 * cell, ra0);
+  if (c0 + 1 < nx) ld_cell256(d.rhs + 4 * (cell + kDx), ra1);
+
+  auto step = [&](int t, double (&v0)[4], double (&v1)[4], double (&n0)[4], double (&n1)[4]) {
     const int col = k * kChunk + c0;
     const bool act0 = col < nx, act1 = col + 1 < nx;
-    const long long cell0 = cell_of(row0, col), cell1 = cell_of(row0, col + 1);
-    double v0[4], v1[4];
-#pragma unroll
-    for (int i = 0; i < 4; ++i) {
-      v0[i] = nv0[i];
-      v1[i] = nv1[i];
-    }
-    int nk = k + 1, nrowk = rowk;
-    long long nrow0 = row0;
-    if (nk == nchunk) {
-      nk = 0;
-      ++nrowk;
-      if (nrowk < nrows) nrow0 = row_base(nrowk);
-    }
+    // next step's sources into the other register set
+    const bool last = k + 1 == nchunk;
+    const long long ncell = last ? next_row : cell + kDx * kChunk;
+    const int ncol = last ? c0 : col + kChunk;
     if (t + 1 < nsteps) {
-      const int ncol = nk * kChunk + c0;
-      ld_cell256(rhs + 4 * cell_of(nrow0, ncol), nv0);
-      ld_cell256(rhs + 4 * cell_of(nrow0, ncol + 1), nv1);
+      if (ncol < nx) ld_cell256(d.rhs + 4 * ncell, n0);
+      if (ncol + 1 < nx) ld_cell256(d.rhs + 4 * (ncell + kDx), n1);
     }
-    if (lane == 0 && prow < nrows) {
-      prefetch_chunk(prow, pk);
-      if (++pk == nchunk) pk = 0, ++prow;
-    }
+    if (lane == 0) prefetch_next();
+    if (k == 0) tc0 = tc1 = 0.0;  // vacuum x-inflow at the row start
     if (HAS_BC) {
       double g0[4], g1[4];
-      ld_cell256(bc + 4 * cell0, g0);
-      ld_cell256(bc + 4 * cell1, g1);
+      if (act0) ld_cell256(d.bc + 4 * cell, g0);
+      if (act1) ld_cell256(d.bc + 4 * (cell + kDx), g1);
 #pragma unroll
       for (int i = 0; i < 4; ++i) {
-        v0[i] += g0[i];
-        v1[i] += g1[i];
+        v0[i] += act0 ? g0[i] : 0.0;
+        v1[i] += act1 ? g1[i] : 0.0;
       }
     }
     // y-upwind traces (per x-mode) of these columns from the previous row
     double y00 = 0.0, y01 = 0.0, y10 = 0.0, y11 = 0.0;  // y{cell}{x-mode}
-    const int r = w + rowk * W;
-    if (r > 0) {
+    if (d.w + rowk * d.W > 0) {
       if (MULTI) {
-        if (lane == 0) {
-          const int need = (w == 0 ? rowk - 1 : rowk) * nchunk + k + 1;
-          while (G.prod[pw] < need) {
-          }
-          __threadfence_block();
-        }
+        if (lane == 0) wait_progress(d.prod + d.pw, (d.w == 0 ? rowk - 1 : rowk) * nchunk + k + 1);
         __syncwarp();
       }
       if (act0) {
-        const double2 p0 = ld_line(in_line + col, smem_lines);
-        const double2 p1 = ld_line(in_line + pitch + col, smem_lines);
+        const double2 p0 = ld_line(d.in_line + col, d.smem_lines);
+        const double2 p1 = ld_line(d.in_line + d.pitch + col, d.smem_lines);
         y00 = p0.x;
         y01 = p1.x;
         y10 = act1 ? p0.y : 0.0;  // the padding column of an odd row is never written
@@ -385,9 +338,6 @@ __global__ void __launch_bounds__(256, 2) sweep_scan_kernel(const SweepArgs a, i
     v1[3] -= ky1 * y11;
 
     double ps0[4], ps1[4];
-    // Constants are re-read from shared memory every step as 16-byte
-    // broadcasts (one wavefront each); registers hold only the stream state.
-    const double2* c2 = reinterpret_cast<const double2*>(cst);
     if (UNIFORM) {
       double u0[4], u1[4];
 #pragma unroll
@@ -401,36 +351,33 @@ __global__ void __launch_bounds__(256, 2) sweep_scan_kernel(const SweepArgs a, i
           u1[0] += lo.x * v1[c], u1[1] += lo.y * v1[c], u1[2] += hi.x * v1[c], u1[3] += hi.y * v1[c];
         }
       }
-      // f = T_x u (per y-mode); lane map over its two cells: tau -> G^2 tau + (G f0 + f1).
-      // The chunk's carry enters lane 0's map before the scan, so the
-      // inclusive scan yields tau after each lane's last cell directly.
+      // f = T_x u (per y-mode); lane map over its two cells: tau -> G^2 tau + (G f0 + f1);
+      // lane 0 also applies its map to the chunk's carry.
       const double f00 = tx0 * u0[0] + tx1 * u0[1], f01 = tx0 * u0[2] + tx1 * u0[3];
       const double f10 = tx0 * u1[0] + tx1 * u1[1], f11 = tx0 * u1[2] + tx1 * u1[3];
       const double2 g01 = c2[kG / 2], g23 = c2[kG / 2 + 1];
       double s0 = f10 + g01.x * f00 + g23.x * f01;
       double s1 = f11 + g01.y * f00 + g23.y * f01;
-      {
-        const double2 p01 = c2[kGP / 2], p23 = c2[kGP / 2 + 1];  // G^2
-        const double t0 = lane == 0 ? tc0 : 0.0, t1 = lane == 0 ? tc1 : 0.0;
-        s0 += p01.x * t0 + p23.x * t1;
-        s1 += p01.y * t0 + p23.y * t1;
-      }
+      fma2(s0, s1, c2[kGP / 2], c2[kGP / 2 + 1], tc0, tc1);  // tc = 0 off lane 0
       // inclusive scan over the lanes: s_l <- s_l + G^(2d) s_{l-d}
 #pragma unroll
       for (int l = 0; l < 5; ++l) {
-        const int d = 1 << l;
-        double o0 = __shfl_up_sync(0xffffffffu, s0, d);
-        double o1 = __shfl_up_sync(0xffffffffu, s1, d);
-        o0 = lane >= d ? o0 : 0.0;
-        o1 = lane >= d ? o1 : 0.0;
-        const double2 p01 = c2[(kGP + 4 * (d - 1)) / 2], p23 = c2[(kGP + 4 * (d - 1)) / 2 + 1];
-        s0 += p01.x * o0 + p23.x * o1;
-        s1 += p01.y * o0 + p23.y * o1;
+        const int dd = 1 << l;
+        double o0 = shfl_up_f64(s0, dd);
+        double o1 = shfl_up_f64(s1, dd);
+        o0 = lane >= dd ? o0 : 0.0;
+        o1 = lane >= dd ? o1 : 0.0;
+        fma2(s0, s1, c2[(kGP + 4 * (dd - 1)) / 2], c2[(kGP + 4 * (dd - 1)) / 2 + 1], o0, o1);
       }
-      double ti0 = __shfl_up_sync(0xffffffffu, s0, 1), ti1 = __shfl_up_sync(0xffffffffu, s1, 1);
-      if (lane == 0) ti0 = tc0, ti1 = tc1;
-      tc0 = __shfl_sync(0xffffffffu, s0, 31);
-      tc1 = __shfl_sync(0xffffffffu, s1, 31);
+      // One rotation: lane l > 0 receives tau_in from lane l-1; lane 0
+      // receives lane 31's tau, the next chunk's carry (only lane 0 keeps one).
+      double ti0 = shfl_idx_f64(s0, (lane + 31) & 31);
+      double ti1 = shfl_idx_f64(s1, (lane + 31) & 31);
+      if (lane == 0) {
+        const double n0 = ti0, n1 = ti1;
+        ti0 = tc0, ti1 = tc1;
+        tc0 = n0, tc1 = n1;
+      }
       // psi = u + Q tau_in, cell by cell
       const double m0 = f00 + g01.x * ti0 + g23.x * ti1, m1 = f01 + g01.y * ti0 + g23.y * ti1;
 #pragma unroll
@@ -447,7 +394,7 @@ __global__ void __launch_bounds__(256, 2) sweep_scan_kernel(const SweepArgs a, i
       bool ok0, ok1;
       {
         double A[16];
-        const double2* sb = reinterpret_cast<const double2*>(a.sigma_t + 16 * cell0);
+        const double2* sb = reinterpret_cast<const double2*>(d.sigma_t + 16 * cell);
 #pragma unroll
         for (int e = 0; e < 8; ++e) {
           const double2 s2 = __ldg(sb + e), m2 = c2[e];
@@ -461,7 +408,7 @@ __global__ void __launch_bounds__(256, 2) sweep_scan_kernel(const SweepArgs a, i
       }
       {
         double A[16];
-        const double2* sb = reinterpret_cast<const double2*>(a.sigma_t + 16 * cell1);
+        const double2* sb = reinterpret_cast<const double2*>(d.sigma_t + 16 * (act1 ? cell + kDx : cell));
 #pragma unroll
         for (int e = 0; e < 8; ++e) {
           const double2 s2 = __ldg(sb + e), m2 = c2[e];
@@ -473,7 +420,7 @@ __global__ void __launch_bounds__(256, 2) sweep_scan_kernel(const SweepArgs a, i
 #pragma unroll
         for (int i = 0; i < 4; ++i) Qc1[i] = b1[i], Qc1[4 + i] = b2[i];
       }
-      if ((!ok0 && act0) || (!ok1 && act1)) atomicExch(a.err, 1);
+      if ((!ok0 && act0) || (!ok1 && act1)) atomicExch(d.err, 1);
       double G0[4], G1[4];
 #pragma unroll
       for (int c = 0; c < 2; ++c) {
@@ -491,19 +438,15 @@ __global__ void __launch_bounds__(256, 2) sweep_scan_kernel(const SweepArgs a, i
       mat2_vec(G1, f00, f01, s0, s1);
       s0 += f10;
       s1 += f11;
-      {  // the chunk's carry enters lane 0's map
-        const double t0 = lane == 0 ? tc0 : 0.0, t1 = lane == 0 ? tc1 : 0.0;
-        s0 += A0 * t0 + A2 * t1;
-        s1 += A1 * t0 + A3 * t1;
-      }
+      fma2(s0, s1, make_double2(A0, A1), make_double2(A2, A3), tc0, tc1);  // the carry (0 off lane 0)
 #pragma unroll
       for (int l = 0; l < 5; ++l) {
-        const int d = 1 << l;
-        const bool in = lane >= d;
-        double p0 = __shfl_up_sync(0xffffffffu, A0, d), p1 = __shfl_up_sync(0xffffffffu, A1, d);
-        double p2 = __shfl_up_sync(0xffffffffu, A2, d), p3 = __shfl_up_sync(0xffffffffu, A3, d);
-        double o0 = __shfl_up_sync(0xffffffffu, s0, d), o1 = __shfl_up_sync(0xffffffffu, s1, d);
-        p0 = in ? p0 : 1.0;
+        const int dd = 1 << l;
+        const bool in = lane >= dd;
+        double p0 = shfl_up_f64(A0, dd), p1 = shfl_up_f64(A1, dd);
+        double p2 = shfl_up_f64(A2, dd), p3 = shfl_up_f64(A3, dd);
+        double o0 = shfl_up_f64(s0, dd), o1 = shfl_up_f64(s1, dd);
+        p0 = in ? p0 : 1.0;  // identity map below lane dd
         p1 = in ? p1 : 0.0;
         p2 = in ? p2 : 0.0;
         p3 = in ? p3 : 1.0;
@@ -519,10 +462,13 @@ __global__ void __launch_bounds__(256, 2) sweep_scan_kernel(const SweepArgs a, i
         A2 = n2;
         A3 = n3;
       }
-      double ti0 = __shfl_up_sync(0xffffffffu, s0, 1), ti1 = __shfl_up_sync(0xffffffffu, s1, 1);
-      if (lane == 0) ti0 = tc0, ti1 = tc1;
-      tc0 = __shfl_sync(0xffffffffu, s0, 31);
-      tc1 = __shfl_sync(0xffffffffu, s1, 31);
+      double ti0 = shfl_idx_f64(s0, (lane + 31) & 31);
+      double ti1 = shfl_idx_f64(s1, (lane + 31) & 31);
+      if (lane == 0) {
+        const double n0 = ti0, n1 = ti1;
+        ti0 = tc0, ti1 = tc1;
+        tc0 = n0, tc1 = n1;
+      }
 #pragma unroll
       for (int i = 0; i < 4; ++i) ps0[i] = v0[i] + Qc0[i] * ti0 + Qc0[4 + i] * ti1;
       double m0, m1;
@@ -533,31 +479,141 @@ __global__ void __launch_bounds__(256, 2) sweep_scan_kernel(const SweepArgs a, i
       for (int i = 0; i < 4; ++i) ps1[i] = v1[i] + Qc1[i] * m0 + Qc1[4 + i] * m1;
     }
     if (act0) {
-      st_cell256(psi + 4 * cell0, ps0);
-      if (act1) st_cell256(psi + 4 * cell1, ps1);
+      double* p = d.psi + 4 * cell;
+      st_cell256(p, ps0);
+      if (act1) st_cell256(p + 4 * kDx, ps1);
       // y-outflow traces (per x-mode) for the next row
-      st_line(my_line + col, ty0 * ps0[0] + ty1 * ps0[2], ty0 * ps1[0] + ty1 * ps1[2], smem_lines);
-      st_line(my_line + pitch + col, ty0 * ps0[1] + ty1 * ps0[3], ty0 * ps1[1] + ty1 * ps1[3], smem_lines);
+      st_line(d.my_line + col, ty0 * ps0[0] + ty1 * ps0[2], ty0 * ps1[0] + ty1 * ps1[2], d.smem_lines);
+      st_line(d.my_line + d.pitch + col, ty0 * ps0[1] + ty1 * ps0[3], ty0 * ps1[1] + ty1 * ps1[3],
+              d.smem_lines);
     }
-    if (MULTI) {
-      __syncwarp();
-      if (lane == 0) {
-        __threadfence_block();
-        G.prod[w] = t + 1;
-      }
+    __syncwarp();  // (own line: the next row reads what this row wrote)
+    if (MULTI && lane == 0) publish_progress(d.prod + d.w, t + 1);
+    // advance
+    cell = ncell;
+    if (last) {
+      k = 0;
+      ++rowk;
+      next_row = rowk + 1 < nrows ? first_cell(rowk + 1) : 0;
     } else {
-      __syncwarp();  // own line: the next row reads what this row wrote
+      ++k;
     }
-    k = nk;
-    rowk = nrowk;
-    row0 = nrow0;
+  };
+
+  for (int t = 0; t < nsteps; t += 2) {
+    step(t, ra0, ra1, rb0, rb1);
+    if (t + 1 < nsteps) step(t + 1, rb0, rb1, ra0, ra1);
   }
+}
+
+template <bool UNIFORM, bool MULTI, bool HAS_BC>
+__global__ void __launch_bounds__(256, 2) sweep_scan_kernel(const SweepArgs a, int W, bool smem_lines) {
+  extern __shared__ double smem[];
+  const int lane = threadIdx.x & 31;
+  const int wib = threadIdx.x >> 5;
+  const int groups = kWarps / W;
+  const int g = wib / W, w = wib % W;
+  const int slot = blockIdx.x * groups + g;
+  if (slot >= a.n) return;  // a whole direction group exits together
+  const int nx = a.nx, ny = a.ny;
+  const int pitch = line_pitch(nx);
+  double* base = smem + static_cast<size_t>(g) * group_doubles(W, nx, smem_lines);
+  double* cst = base;
+  int* prod = reinterpret_cast<int*>(base + kConsts);
+  double* lines = smem_lines ? base + kConsts + 2 * ((W + 3) / 4) : a.line + static_cast<size_t>(slot) * W * 2 * pitch;
+  const int ang = a.angles ? a.angles[slot] : slot;
+  const double omx = a.dirs[3 * ang], omy = a.dirs[3 * ang + 1];
+  const bool xu = omx >= 0.0, yu = omy >= 0.0;  // sweep.cpp:37-38
+  if (w == 0) {
+    const double* ax = xu ? a.sc.ax_minus : a.sc.ax_plus;
+    const double* ay = yu ? a.sc.ay_minus : a.sc.ay_plus;
+    if (lane < 16) {
+      const double dv = omx * ax[lane] + omy * ay[lane];
+      cst[lane] = UNIFORM ? dv + a.sigma_t[lane] : dv;
+    }
+    if (lane < 2) {
+      // (B psi_up)[my,mx] = c[mx] (t . psi_up[my,:]), (c,t) = (-t_L,t_R) minus / (t_R,t_L) plus
+      cst[kKT + lane] = omx * (xu ? -a.sc.trx_l[lane] : a.sc.trx_r[lane]);
+      cst[kKT + 2 + lane] = xu ? a.sc.trx_r[lane] : a.sc.trx_l[lane];
+      cst[kKT + 4 + lane] = omy * (yu ? -a.sc.try_l[lane] : a.sc.try_r[lane]);
+      cst[kKT + 6 + lane] = yu ? a.sc.try_r[lane] : a.sc.try_l[lane];
+    }
+    __syncwarp();
+    if (UNIFORM && lane == 0) {
+      // M^-1 columns via the reference LU; Q = -M^-1 K_x; G = T_x Q; (G^2)^(l+1)
+      double Mi[16];
+      for (int c = 0; c < 4; c += 3) {
+        double A[16], e0[4] = {0, 0, 0, 0}, e1[4] = {0, 0, 0, 0}, e2[4] = {0, 0, 0, 0};
+        for (int k = 0; k < 16; ++k) A[k] = cst[k];
+        e0[c] = 1.0;
+        if (c + 1 < 4) e1[c + 1] = 1.0;
+        if (c + 2 < 4) e2[c + 2] = 1.0;
+        if (!lu_solve4x3(A, e0, e1, e2)) atomicExch(a.err, 1);
+        for (int r = 0; r < 4; ++r) {
+          Mi[c * 4 + r] = e0[r];
+          if (c + 1 < 4) Mi[(c + 1) * 4 + r] = e1[r];
+          if (c + 2 < 4) Mi[(c + 2) * 4 + r] = e2[r];
+        }
+      }
+      const double kx0 = cst[kKT], kx1 = cst[kKT + 1], tx0 = cst[kKT + 2], tx1 = cst[kKT + 3];
+      // K_x (4 x 2): column my has kx[mx] at rows (my, mx)
+      double Q[8];
+      for (int my = 0; my < 2; ++my)
+        for (int r = 0; r < 4; ++r)
+          Q[my * 4 + r] = -(Mi[(my * 2 + 0) * 4 + r] * kx0 + Mi[(my * 2 + 1) * 4 + r] * kx1);
+      // G = T_x Q (2 x 2): row m = tx . Q[(m,0..1), :]
+      double Gm[4];
+      for (int col = 0; col < 2; ++col)
+        for (int m = 0; m < 2; ++m) Gm[col * 2 + m] = tx0 * Q[col * 4 + m * 2] + tx1 * Q[col * 4 + m * 2 + 1];
+      for (int k = 0; k < 16; ++k) cst[k] = Mi[k];
+      for (int k = 0; k < 8; ++k) cst[kQ + k] = Q[k];
+      for (int e = 0; e < 4; ++e) cst[kG + e] = Gm[e];
+      double G2[4];
+      for (int col = 0; col < 2; ++col)
+        for (int m = 0; m < 2; ++m) G2[col * 2 + m] = Gm[m] * Gm[col * 2] + Gm[2 + m] * Gm[col * 2 + 1];
+      double P[4] = {G2[0], G2[1], G2[2], G2[3]};
+      for (int k = 0; k < 32; ++k) {
+        for (int e = 0; e < 4; ++e) cst[kGP + 4 * k + e] = P[e];
+        double N[4];
+        for (int col = 0; col < 2; ++col)
+          for (int m = 0; m < 2; ++m) N[col * 2 + m] = G2[m] * P[col * 2] + G2[2 + m] * P[col * 2 + 1];
+        for (int e = 0; e < 4; ++e) P[e] = N[e];
+      }
+    }
+    if (lane < W) prod[lane] = 0;
+  }
+  asm volatile("bar.sync %0, %1;" ::"r"(g + 1), "r"(W * 32) : "memory");
+
+  Dir d;
+  d.rhs = a.rhs + static_cast<long long>(slot) * a.rhs_stride;
+  d.bc = HAS_BC ? a.bc + static_cast<long long>(ang) * a.bc_stride : nullptr;
+  d.psi = a.psi + static_cast<long long>(slot) * a.psi_stride;
+  d.sigma_t = a.sigma_t;
+  d.cst = cst;
+  d.prod = prod;
+  d.pw = (w + W - 1) % W;
+  d.my_line = lines + static_cast<size_t>(w) * 2 * pitch;
+  d.in_line = lines + static_cast<size_t>(d.pw) * 2 * pitch;
+  d.err = a.err;
+  d.nx = nx;
+  d.ny = ny;
+  d.W = W;
+  d.w = w;
+  d.nchunk = (nx + kChunk - 1) / kChunk;
+  d.nrows = (ny - w + W - 1) / W;  // rows w, w+W, ... of this warp
+  d.pitch = pitch;
+  d.yu = yu;
+  d.smem_lines = smem_lines;
+  if (xu)
+    sweep_dir<UNIFORM, MULTI, HAS_BC, true>(d);
+  else
+    sweep_dir<UNIFORM, MULTI, HAS_BC, false>(d);
 }
 
 int sm_count() {
   static const int n = [] {
-    int d = 0, v = 148;
-    if (cudaGetDevice(&d) == cudaSuccess) cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, d);
+    int dev = 0, v = 148;
+    if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
     return v;
   }();
   return n;
