@@ -154,6 +154,11 @@ void rtlr_cu_report_destroy(rtlr_cu_report* r);
  * balanced.  Pure host logic (no GPU needed). */
 int rtlr_cu_partition_angles(int n_theta, int n_omega_z, int nranks, int rank, int* count,
                              int* angles);
+/* Low-rank sharding of one phase's list of m angles (sampled sweeps, Galerkin
+ * solves, residual norms): rank `rank` owns items [*begin, *end), blocks of
+ * *bsz = ceil(m / nranks) items, gathered back in order with one in-place
+ * all-gather.  Pure host logic (no GPU needed). */
+int rtlr_cu_shard_block(int m, int nranks, int rank, int* begin, int* end, int* bsz);
 /* NCCL (over NVLink / NVSwitch) for the sharded drivers: rank 0 creates the
  * 128-byte id, the launcher broadcasts it, every rank attaches its problem.
  * solve_full_rank then sweeps this rank's directions and sums the scalar-

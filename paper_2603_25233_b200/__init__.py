@@ -38,6 +38,7 @@ EXPORTS = [
     "rtlr_cu_report_get", "rtlr_cu_report_sampled", "rtlr_cu_report_destroy",
     "rtlr_cu_partition_angles", "rtlr_cu_problem_fr_options", "rtlr_cu_problem_lr_options",
     "rtlr_cu_sweep_async", "rtlr_cu_check", "rtlr_cu_nccl_unique_id", "rtlr_cu_problem_set_comm",
+    "rtlr_cu_shard_block",
 ]
 
 
@@ -124,6 +125,8 @@ def load_library(path: str = LIB_PATH):
     L.rtlr_cu_report_sampled.argtypes = [ctypes.c_void_p, _I, _I]
     L.rtlr_cu_report_destroy.argtypes = [ctypes.c_void_p]
     L.rtlr_cu_partition_angles.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int, _I, _I]
+    _ip = ctypes.POINTER(ctypes.c_int)
+    L.rtlr_cu_shard_block.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.c_int, _ip, _ip, _ip]
     _lib = L
     return L
 
@@ -158,6 +161,14 @@ def partition_angles(n_theta: int, n_omega_z: int, nranks: int, rank: int) -> np
     _check(L.rtlr_cu_partition_angles(n_theta, n_omega_z, nranks, rank, ctypes.byref(cnt),
                                       out.ctypes.data_as(_I)))
     return out[:cnt.value]
+
+
+def shard_block(m: int, nranks: int, rank: int) -> tuple[int, int, int]:
+    """(begin, end, bsz): rank's contiguous block of an m-item low-rank phase."""
+    L = load_library()
+    b, e, z = ctypes.c_int(0), ctypes.c_int(0), ctypes.c_int(0)
+    _check(L.rtlr_cu_shard_block(m, nranks, rank, ctypes.byref(b), ctypes.byref(e), ctypes.byref(z)))
+    return b.value, e.value, z.value
 
 
 class Report:

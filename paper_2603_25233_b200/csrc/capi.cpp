@@ -547,6 +547,16 @@ int rtlr_cu_partition_angles(int n_theta, int n_omega_z, int nranks, int rank, i
   });
 }
 
+int rtlr_cu_shard_block(int m, int nranks, int rank, int* begin, int* end, int* bsz) {
+  return guard([&] {
+    need(begin != nullptr && end != nullptr && bsz != nullptr, "shard_block: null argument");
+    const ShardBlock b = shard_block(m, nranks, rank);
+    *begin = b.begin;
+    *end = b.end;
+    *bsz = b.bsz;
+  });
+}
+
 int rtlr_cu_nccl_unique_id(unsigned char* out) {
   return guard([&] {
     need(out != nullptr, "nccl_unique_id: null argument");

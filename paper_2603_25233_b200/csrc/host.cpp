@@ -721,6 +721,15 @@ std::vector<int> partition_angles(int n_theta, int n_omega_z, int nranks, int ra
   return out;
 }
 
+ShardBlock shard_block(int m, int nranks, int rank) {
+  if (m < 0 || nranks < 1 || rank < 0 || rank >= nranks) throw std::invalid_argument("shard_block: bad argument");
+  ShardBlock b;
+  b.bsz = (m + nranks - 1) / nranks;
+  b.begin = std::min(m, rank * b.bsz);
+  b.end = std::min(m, b.begin + b.bsz);
+  return b;
+}
+
 int truncation_rank(const std::vector<double>& s, double eps_svd) {  // low_rank.cpp:254-266
   const int n = static_cast<int>(s.size());
   if (n == 0) return 0;

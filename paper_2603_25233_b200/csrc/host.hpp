@@ -108,6 +108,15 @@ int truncation_rank(const std::vector<double>& s, double eps_svd);
 // round-robin, so every rank spans all quadrants and pairs never split.
 std::vector<int> partition_angles(int n_theta, int n_omega_z, int nranks, int rank);
 
+// Low-rank sharding of a list of m work items (angles of one LR phase):
+// rank k owns the contiguous block [k*bsz, min(m, (k+1)*bsz)), bsz =
+// ceil(m / nranks), so an in-place all-gather of bsz-item segments restores
+// the whole list in order on every rank.
+struct ShardBlock {
+  int begin = 0, end = 0, bsz = 0;
+};
+ShardBlock shard_block(int m, int nranks, int rank);
+
 // Counter-based U[0,1) generator for the C5 per-(cell, direction) sources
 // (SURVEY.md §8(d)); bit-identical on host and device.
 inline double c5_uniform(std::uint64_t seed, std::uint64_t counter) {

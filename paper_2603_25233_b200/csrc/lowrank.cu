@@ -217,6 +217,13 @@ class LowRankEngine {
   double host_dot(const double* a, const double* b, long long n);
   int* upload_ints(DBuf<int>& buf, const std::vector<int>& a);
   double* work(size_t need) { return work_.ensure(std::max<size_t>(need, 4096)); }
+  // Angle sharding of one phase's m items over the communicator's ranks
+  // (the whole list without one); padded(m) = items incl. the all-gather pad.
+  ShardBlock blk(int m) const {
+    if (!P_.sharded()) return ShardBlock{0, m, m};
+    return shard_block(m, P_.nranks(), P_.rank());
+  }
+  int padded(int m) const { return P_.sharded() ? blk(m).bsz * P_.nranks() : m; }
 
   Problem& P_;
   LowRankParams prm_;
@@ -410,13 +417,17 @@ void LowRankEngine::update_projections(bool reorth) {
 }
 
 // galerkin_solve for a list of angles (low_rank.cpp:192-200), batched.
+// Sharded: this rank solves its block of the angles and one all-gather
+// assembles every column on every rank (d_sol holds padded(m) columns).
 void LowRankEngine::galerkin(const std::vector<int>& angles, double* d_sol, long long ldsol) {
   if (rank_ < 1) throw std::runtime_error("galerkin_solve: empty basis");
   const int m = static_cast<int>(angles.size());
+  const ShardBlock sb = blk(m);
   const long long rr = static_cast<long long>(rank_) * rank_;
   const int chunk = rank_ > kSmemLuMax ? static_cast<int>(std::max<long long>(1, (128LL << 20) / rr)) : 4096;
-  for (int j0 = 0; j0 < m; j0 += chunk) {
-    const int mc = std::min(chunk, m - j0);
+  int bad = 0;
+  for (int j0 = sb.begin; j0 < sb.end; j0 += chunk) {
+    const int mc = std::min(chunk, sb.end - j0);
     std::vector<int> sub(angles.begin() + j0, angles.begin() + j0 + mc);
     int* d_ang = upload_ints(ang_, sub);
     double* out = d_sol + static_cast<long long>(j0) * ldsol;
@@ -436,30 +447,47 @@ void LowRankEngine::galerkin(const std::vector<int>& angles, double* d_sol, long
     std::vector<int> hf(mc);
     RTLR_CUDA(cudaMemcpyAsync(hf.data(), flags, mc * sizeof(int), cudaMemcpyDeviceToHost, s_));
     RTLR_CUDA(cudaStreamSynchronize(s_));
-    for (int v : hf)
-      if (v) throw std::runtime_error("galerkin_solve: singular reduced system");
+    for (int v : hf) bad |= v;
   }
+  if (P_.sharded()) {
+    // every rank learns of a singular system before anyone throws
+    int* d = flags_.ensure(1);
+    RTLR_CUDA(cudaMemcpyAsync(d, &bad, sizeof(int), cudaMemcpyHostToDevice, s_));
+    P_.allreduce_max(d, 1);
+    RTLR_CUDA(cudaMemcpyAsync(&bad, d, sizeof(int), cudaMemcpyDeviceToHost, s_));
+    RTLR_CUDA(cudaStreamSynchronize(s_));
+    if (!bad) {
+      if (ldsol != rank_) throw std::logic_error("galerkin: sharded solutions must be packed (ldsol == rank)");
+      P_.allgather_inplace(d_sol, static_cast<size_t>(sb.bsz) * ldsol);
+    }
+  }
+  if (bad) throw std::runtime_error("galerkin_solve: singular reduced system");
 }
 
 // ||rhs_j - (D_j + Sigma_t) X c_j|| for the listed angles, expanded block-
 // wise (low_rank.cpp:283-307); coefficient column k belongs to angles[k].
 std::vector<double> LowRankEngine::residual_norms(const std::vector<int>& angles, const double* coeffs,
                                                   long long ldc) {
+  // Sharded: this rank evaluates its block of the angles; the norms are
+  // all-gathered (every rank then takes the same greedy decisions).
   const int m = static_cast<int>(angles.size());
   std::vector<double> out(m);
+  if (m == 0) return out;
+  const ShardBlock sb = blk(m);
+  double* nr_all = nrm_.ensure(std::max(padded(m), 128));
   const int block = 128;
-  for (int i0 = 0; i0 < m; i0 += block) {
-    const int nb = std::min(block, m - i0);
+  for (int i0 = sb.begin; i0 < sb.end; i0 += block) {
+    const int nb = std::min(block, sb.end - i0);
     std::vector<int> sub(angles.begin() + i0, angles.begin() + i0 + nb);
     double* Y = ybuf_.ensure(static_cast<size_t>(n_) * block);
     gemm_nn(n_, nb, rank_, X_.col(0), X_.ld, coeffs + static_cast<long long>(i0) * ldc, ldc, Y, n_, s_);
     int* d_ang = upload_ints(ang_, sub);
-    double* nr = nrm_.ensure(block);
     launch_residual_norms(sa_, nb, d_ang, dirs_, Y, n_, rhs_core_.get(), hp_.bc_any ? P_.bc_.get() : nullptr, n_,
-                          work(static_cast<size_t>(block) * kResidParts), nr, s_);
-    RTLR_CUDA(cudaMemcpyAsync(out.data() + i0, nr, nb * sizeof(double), cudaMemcpyDeviceToHost, s_));
-    RTLR_CUDA(cudaStreamSynchronize(s_));
+                          work(static_cast<size_t>(block) * kResidParts), nr_all + i0, s_);
   }
+  P_.allgather_inplace(nr_all, sb.bsz);
+  RTLR_CUDA(cudaMemcpyAsync(out.data(), nr_all, m * sizeof(double), cudaMemcpyDeviceToHost, s_));
+  RTLR_CUDA(cudaStreamSynchronize(s_));
   return out;
 }
 
@@ -502,7 +530,7 @@ void LowRankEngine::build_full_coefficients(const std::vector<int>* cand, const 
   for (int j = 0; j < nomega_; ++j)
     if (!done[j]) rest.push_back(j);
   if (!rest.empty()) {
-    double* S = sol_.ensure(static_cast<size_t>(r) * rest.size());
+    double* S = sol_.ensure(static_cast<size_t>(r) * padded(static_cast<int>(rest.size())));
     galerkin(rest, S, r);
     int* dr = upload_ints(ang2_, rest);
     scatter_cols<<<g1(static_cast<long long>(r) * rest.size()), 256, 0, s_>>>(r, static_cast<int>(rest.size()), dr, S,
@@ -532,11 +560,19 @@ InnerResult LowRankEngine::inner(const double* d_phi_prev, SubsampleRng& rng) {
   while (true) {
     ++out.iterations;
     const int p_now = static_cast<int>(next.size());
-    double* S = snaps_.ensure(static_cast<size_t>(n_) * p_now);
+    double* S = snaps_.ensure(static_cast<size_t>(n_) * padded(p_now));
     int* d_next = upload_ints(ang2_, next);
     pt_.start("sweep");
-    P_.sweep(d_next, p_now, rhs_core_.get(), 0, S, n_);
-    P_.check_error();
+    {  // sharded: this rank's block of the sampled sweeps, then one all-gather
+      const ShardBlock sb = blk(p_now);
+      P_.sweep(d_next + sb.begin, sb.end - sb.begin, rhs_core_.get(), 0, S + static_cast<size_t>(sb.begin) * n_, n_);
+      if (P_.sharded()) {
+        P_.check_error_all();
+        P_.allgather_inplace(S, static_cast<size_t>(sb.bsz) * n_);
+      } else {
+        P_.check_error();
+      }
+    }
     pt_.stop();
     for (int j : next) {
       sampled[j] = 1;
@@ -562,7 +598,7 @@ InnerResult LowRankEngine::inner(const double* d_phi_prev, SubsampleRng& rng) {
       if (!sampled[j]) pool.push_back(j);
     std::vector<int> cands = rng.sample_without_replacement(std::move(pool), prm_.q);
     const int m = static_cast<int>(cands.size());
-    double* csol = cand_.ensure(static_cast<size_t>(rank_) * m);
+    double* csol = cand_.ensure(static_cast<size_t>(rank_) * padded(m));
     pt_.start("galerkin_q");
     galerkin(cands, csol, rank_);
     pt_.stop();

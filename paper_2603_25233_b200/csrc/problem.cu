@@ -238,6 +238,22 @@ void Problem::check_error() {
   }
 }
 
+void Problem::check_error_all() {
+  allreduce_max(err_.get(), 1);
+  check_error();
+}
+
+void Problem::allgather_inplace(double* buf, size_t count_per_rank) {
+  if (!comm_ || count_per_rank == 0) return;
+  RTLR_NCCL(ncclAllGather(buf + static_cast<size_t>(rank_) * count_per_rank, buf, count_per_rank, ncclDouble,
+                          static_cast<ncclComm_t>(comm_), stream_));
+}
+
+void Problem::allreduce_max(int* d_buf, int n) {
+  if (!comm_ || n <= 0) return;
+  RTLR_NCCL(ncclAllReduce(d_buf, d_buf, n, ncclInt, ncclMax, static_cast<ncclComm_t>(comm_), stream_));
+}
+
 void Problem::sweep(const int* d_angles, int n, const double* d_rhs, long long rhs_stride,
                     double* d_psi, long long psi_stride, bool use_bc, const double* d_dirs) {
   if (n <= 0) return;
@@ -418,7 +434,10 @@ SolveReport Problem::solve_full_rank(const FullRankOptions& o) {
     diff_norms(static_cast<int>(n), phi_star, phi, norm_work_.get(), norm_work_.get() + 2 * kNormParts, stream_);
     RTLR_CUDA(cudaMemcpyAsync(h_pin_, norm_work_.get() + 2 * kNormParts, 2 * sizeof(double),
                               cudaMemcpyDeviceToHost, stream_));
-    check_error();  // synchronizes
+    if (sharded)
+      check_error_all();  // synchronizes
+    else
+      check_error();
     OuterRecord rec;
     rec.diff_two_norm = h_pin_[0];
     rec.diff_inf_norm = h_pin_[1];

@@ -145,7 +145,16 @@ class Problem {
   // summed with ncclAllReduce.  nranks == 1 restores the unsharded path.
   void set_comm(int nranks, int rank, const void* nccl_unique_id);
   int nranks() const { return nranks_; }
+  int rank() const { return rank_; }
   int device() const { return device_; }
+  bool sharded() const { return comm_ != nullptr; }
+  // Collectives on the problem stream (no-ops without a communicator):
+  // in-place all-gather of count_per_rank doubles per rank; max over ranks.
+  void allgather_inplace(double* buf, size_t count_per_rank);
+  void allreduce_max(int* d_buf, int n);
+  // check_error() with the singular-block flag max-reduced over the ranks
+  // first, so every rank throws together (no rank left in a collective).
+  void check_error_all();
 
   // Unique 2D transport operators: mirror directions (j1, j2) and
   // (j1, n_z-1-j2) have bitwise-identical (Omega_x, Omega_y).

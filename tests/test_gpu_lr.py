@@ -110,3 +110,19 @@ def test_baseline_c2_reduced(name):
     rg = g.solve_low_rank()
     assert abs(rg.iterations - ro.iterations) <= 1
     assert rel(rg.phi, ro.get("phi", o.n)) <= 1e-8
+
+
+def test_sharded_low_rank_single_rank_nccl_is_bitwise():
+    """The angle-sharded LR driver (sampled sweeps, Galerkin solves and
+    residual norms per rank block + NCCL all-gathers) on a one-rank
+    communicator: every per-angle result is computed exactly as unsharded, so
+    phi, ranks and the sampled sets are bitwise identical."""
+    a = P.Problem("C1")
+    ra = a.solve_low_rank(build_factors=0)
+    b = P.Problem("C1")
+    b.set_comm(1, 0, P.nccl_unique_id())
+    rb = b.solve_low_rank(build_factors=0)
+    assert rb.iterations == ra.iterations
+    assert np.array_equal(rb.phi, ra.phi)
+    assert list(rb.history("rank")) == list(ra.history("rank"))
+    assert rb.sampled_log() == ra.sampled_log()

@@ -88,3 +88,84 @@ def test_two_rank_sharded_si_dsa(name):
         assert err_step <= 1e-13
         assert err_solve <= 1e-12
         assert abs(its - fr_its) <= 1
+
+
+def test_shard_block_covers_every_item_once_in_order():
+    import sys
+    sys.path.insert(0, os.path.dirname(HERE))
+    import paper_2603_25233_b200 as P
+    for m in (0, 1, 2, 7, 8, 16, 100, 1023):
+        for world in (1, 2, 3, 4, 8):
+            got = []
+            for r in range(world):
+                b, e, bsz = P.shard_block(m, world, r)
+                assert bsz == -(-m // world)
+                assert 0 <= b <= e <= m and e - b <= bsz
+                if e > b:
+                    assert b == r * bsz  # in-place all-gather offset
+                got.extend(range(b, e))
+            assert got == list(range(m))
+    with pytest.raises(P.RtlrError):
+        P.shard_block(4, 2, 2)
+
+
+def _lr_worker(rank, world, port, q):
+    """One low-rank phase, sharded as the GPU driver shards it: this rank
+    sweeps its block of the sampled angles into a padded buffer, the blocks
+    are all-gathered in place, and per-angle residual norms of the gathered
+    snapshots (an angle-sharded phase of its own) are all-gathered too."""
+    import sys
+    sys.path.insert(0, HERE)
+    sys.path.insert(0, os.path.dirname(HERE))
+    import _oracle as O
+    import paper_2603_25233_b200 as P
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        o = O.Problem("pin_cell")
+        d, _ = O.quadrature(o.n_theta, o.n_omega_z)
+        rng = np.random.default_rng(7)
+        rhs = o.rhs_core(rng.random(o.n))
+        n_om = o.n_theta * o.n_omega_z
+        out = []
+        for m in (1, 5, 8, 13):
+            angles = rng.choice(n_om, size=m, replace=False)
+            b, e, bsz = P.shard_block(m, world, rank)
+            buf = torch.zeros(world * bsz, o.n, dtype=torch.float64)
+            for k in range(b, e):
+                j = angles[k]
+                buf[k] = torch.from_numpy(o.sweep(d[j, 0], d[j, 1], rhs))
+            mine = buf[rank * bsz:(rank + 1) * bsz].clone()
+            dist.all_gather_into_tensor(buf, mine)
+            snaps = buf[:m].numpy()
+            ref = np.stack([o.sweep(d[j, 0], d[j, 1], rhs) for j in angles])
+            # residual norms ||rhs - A_j psi_j|| on this rank's block, gathered
+            nb = torch.zeros(world * bsz, dtype=torch.float64)
+            for k in range(b, e):
+                j = angles[k]
+                nb[k] = float(np.linalg.norm(rhs - o.apply(d[j, 0], d[j, 1], snaps[k])))
+            mine_n = nb[rank * bsz:(rank + 1) * bsz].clone()
+            dist.all_gather_into_tensor(nb, mine_n)
+            ref_n = [np.linalg.norm(rhs - o.apply(d[j, 0], d[j, 1], ref[k])) for k, j in enumerate(angles)]
+            out.append((m, bool(np.array_equal(snaps, ref)), bool(np.array_equal(nb[:m].numpy(), ref_n))))
+        q.put((rank, out))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_sharded_low_rank_phase_gathers_bitwise(world):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_lr_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    for p in procs:
+        p.join(timeout=300)
+        assert p.exitcode == 0
+    for _ in range(world):
+        _, out = q.get()
+        for m, snaps_ok, norms_ok in out:
+            assert snaps_ok and norms_ok, m
