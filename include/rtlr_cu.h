@@ -159,6 +159,12 @@ int rtlr_cu_partition_angles(int n_theta, int n_omega_z, int nranks, int rank, i
  * *bsz = ceil(m / nranks) items, gathered back in order with one in-place
  * all-gather.  Pure host logic (no GPU needed). */
 int rtlr_cu_shard_block(int m, int nranks, int rank, int* begin, int* end, int* bsz);
+/* ---- dense kernels of the truncation path, host buffers in and out (for
+ * tests and tools): the blocked Householder QR of the low-rank basis rebuild
+ * (low_rank.cpp:112-130): a (m x n, m >= n, column-major) = q r, q m x n with
+ * orthonormal columns, r n x n upper triangular (Eigen sign conventions). */
+int rtlr_cu_dense_qr(int device, int64_t m, int n, const double* a, double* q, double* r);
+
 /* NCCL (over NVLink / NVSwitch) for the sharded drivers: rank 0 creates the
  * 128-byte id, the launcher broadcasts it, every rank attaches its problem.
  * solve_full_rank then sweeps this rank's directions and sums the scalar-

@@ -38,7 +38,7 @@ EXPORTS = [
     "rtlr_cu_report_get", "rtlr_cu_report_sampled", "rtlr_cu_report_destroy",
     "rtlr_cu_partition_angles", "rtlr_cu_problem_fr_options", "rtlr_cu_problem_lr_options",
     "rtlr_cu_sweep_async", "rtlr_cu_check", "rtlr_cu_nccl_unique_id", "rtlr_cu_problem_set_comm",
-    "rtlr_cu_shard_block",
+    "rtlr_cu_shard_block", "rtlr_cu_dense_qr",
 ]
 
 
@@ -127,6 +127,8 @@ def load_library(path: str = LIB_PATH):
     L.rtlr_cu_partition_angles.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int, _I, _I]
     _ip = ctypes.POINTER(ctypes.c_int)
     L.rtlr_cu_shard_block.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.c_int, _ip, _ip, _ip]
+    L.rtlr_cu_dense_qr.argtypes = [ctypes.c_int, ctypes.c_int64, ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p,
+                                   ctypes.c_void_p]
     _lib = L
     return L
 
@@ -169,6 +171,16 @@ def shard_block(m: int, nranks: int, rank: int) -> tuple[int, int, int]:
     b, e, z = ctypes.c_int(0), ctypes.c_int(0), ctypes.c_int(0)
     _check(L.rtlr_cu_shard_block(m, nranks, rank, ctypes.byref(b), ctypes.byref(e), ctypes.byref(z)))
     return b.value, e.value, z.value
+
+
+def dense_qr(a: np.ndarray, device: int = 0):
+    """(q, r) of the GPU blocked Householder QR (the basis-rebuild kernel)."""
+    a = np.asfortranarray(a, dtype=np.float64)
+    m, n = a.shape
+    q = np.zeros((m, n), dtype=np.float64, order="F")
+    r = np.zeros((n, n), dtype=np.float64, order="F")
+    _check(load_library().rtlr_cu_dense_qr(device, m, n, _dp(a), _dp(q), _dp(r)))
+    return q, r
 
 
 class Report:

@@ -6,6 +6,7 @@
 #include <string>
 
 #include "../../include/rtlr_cu.h"
+#include "dense.cuh"
 #include "problem.hpp"
 
 using namespace rtlr::cuda;
@@ -544,6 +545,25 @@ int rtlr_cu_partition_angles(int n_theta, int n_omega_z, int nranks, int rank, i
     const std::vector<int> a = partition_angles(n_theta, n_omega_z, nranks, rank);
     *count = static_cast<int>(a.size());
     if (angles) std::memcpy(angles, a.data(), a.size() * sizeof(int));
+  });
+}
+
+int rtlr_cu_dense_qr(int device, int64_t m, int n, const double* a, double* q, double* r) {
+  return guard([&] {
+    need(m >= n && n >= 1 && a && q && r, "dense_qr: need m >= n >= 1 and host buffers");
+    RTLR_CUDA(cudaSetDevice(device));
+    cudaStream_t s;
+    RTLR_CUDA(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+    const size_t mn = static_cast<size_t>(m) * n;
+    DBuf<double> da, dq, dr, dt, dw;
+    da.upload(a, mn, s);
+    const size_t nw = householder_qr_work(m, n);
+    householder_qr(m, n, da.get(), m, dt.ensure(n), dq.ensure(mn), m, dr.ensure(static_cast<size_t>(n) * n),
+                   dw.ensure(nw), nw, s);
+    RTLR_CUDA(cudaMemcpyAsync(q, dq.get(), mn * sizeof(double), cudaMemcpyDeviceToHost, s));
+    RTLR_CUDA(cudaMemcpyAsync(r, dr.get(), static_cast<size_t>(n) * n * sizeof(double), cudaMemcpyDeviceToHost, s));
+    RTLR_CUDA(cudaStreamSynchronize(s));
+    RTLR_CUDA(cudaStreamDestroy(s));
   });
 }
 

@@ -1,6 +1,7 @@
 // Dense fp64 kernels of the low-rank path (see dense.cuh).
 #include <algorithm>
 #include <cmath>
+#include <stdexcept>
 #include <vector>
 
 #include "dense.cuh"
@@ -83,6 +84,10 @@ __global__ void __launch_bounds__(256) gemm_tn_kernel(int M, int N, long long K,
     }
 }
 
+// C = sum over the split-K partials.  Few outputs with many splits (the
+// CGS GEMVs): one warp per output, lanes stride the splits, fixed shuffle
+// tree; many outputs: one thread per output, splits in order.  Both orders
+// are fixed, so results are bitwise reproducible.
 __global__ void splitk_reduce(int M, int N, int splits, const double* __restrict__ part, double* __restrict__ C,
                               long long ldc) {
   const long long total = static_cast<long long>(M) * N;
@@ -93,6 +98,33 @@ __global__ void splitk_reduce(int M, int N, int splits, const double* __restrict
     const int m = static_cast<int>(e % M), n = static_cast<int>(e / M);
     C[m + n * ldc] = s;
   }
+}
+
+__global__ void splitk_reduce_warp(int M, int N, int splits, const double* __restrict__ part, double* __restrict__ C,
+                                   long long ldc) {
+  const long long total = static_cast<long long>(M) * N;
+  const int lane = threadIdx.x & 31;
+  for (long long e = (blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x) >> 5; e < total;
+       e += (static_cast<long long>(gridDim.x) * blockDim.x) >> 5) {
+    double s = 0.0;
+    for (int z = lane; z < splits; z += 32) s += part[z * total + e];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    if (lane == 0) {
+      const int m = static_cast<int>(e % M), n = static_cast<int>(e / M);
+      C[m + n * ldc] = s;
+    }
+  }
+}
+
+int grid1d(long long n);
+
+void launch_splitk_reduce(int M, int N, int splits, const double* part, double* C, long long ldc, cudaStream_t s) {
+  const long long total = static_cast<long long>(M) * N;
+  if (splits >= 64 && total <= 4096)
+    splitk_reduce_warp<<<static_cast<unsigned>((total * 32 + 255) / 256), 256, 0, s>>>(M, N, splits, part, C, ldc);
+  else
+    splitk_reduce<<<grid1d(total), 256, 0, s>>>(M, N, splits, part, C, ldc);
 }
 
 int tn_splits(int M, int N, long long K) {
@@ -511,6 +543,45 @@ __global__ void hh_apply(long long m, int k, const double* __restrict__ v, long 
   for (long long i = k + 1 + threadIdx.x; i < m; i += blockDim.x) col[i] -= w * v[i + k * ldv];
 }
 
+// Panel-column reflector application for tall columns, spread over
+// (column, row chunk) CTAs: partial dots v^T a_j per chunk, then every CTA
+// of column j sums the chunk partials in a fixed order (deterministic),
+// w_j = tau (a[k,j] + sum), and updates its rows.
+constexpr int kHhChunks = 32;
+__global__ void hh_dot_chunks(long long m, int k, const double* __restrict__ v, long long ldv,
+                              const double* __restrict__ a, long long lda, int j0, double* __restrict__ part) {
+  __shared__ double sh[32];
+  const int j = j0 + blockIdx.x, c = blockIdx.y;
+  const long long rows = m - (k + 1), per = (rows + kHhChunks - 1) / kHhChunks;
+  const long long r0 = k + 1 + c * per, r1 = min(m, r0 + per);
+  const double* col = a + j * lda;
+  double s = 0.0;
+  for (long long i = r0 + threadIdx.x; i < r1; i += blockDim.x) s += v[i + k * ldv] * col[i];
+  s = block_sum_all(s, sh);
+  if (threadIdx.x == 0) part[blockIdx.x * kHhChunks + c] = s;
+}
+__global__ void hh_update_chunks(long long m, int k, const double* __restrict__ v, long long ldv, const double* tau,
+                                 double* a, long long lda, int j0, const double* __restrict__ part) {
+  const int j = j0 + blockIdx.x, c = blockIdx.y;
+  double* col = a + j * lda;
+  double s = 0.0;
+  for (int z = 0; z < kHhChunks; ++z) s += part[blockIdx.x * kHhChunks + z];
+  const double w = tau[k] * (col[k] + s);
+  const long long rows = m - (k + 1), per = (rows + kHhChunks - 1) / kHhChunks;
+  const long long r0 = k + 1 + c * per, r1 = min(m, r0 + per);
+  for (long long i = r0 + threadIdx.x; i < r1; i += blockDim.x) col[i] -= w * v[i + k * ldv];
+}
+// row k of the updated columns, after every chunk CTA has read a[k, j]
+__global__ void hh_update_diag(int k, const double* tau, double* a, long long lda, int j0, int ncols,
+                               const double* __restrict__ part) {
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= ncols) return;
+  double* col = a + (j0 + t) * lda;
+  double s = 0.0;
+  for (int z = 0; z < kHhChunks; ++z) s += part[t * kHhChunks + z];
+  col[k] -= tau[k] * (col[k] + s);
+}
+
 __global__ void set_beta(int k, double* a, long long lda, const double* scal) {
   if (threadIdx.x == 0 && blockIdx.x == 0) a[k + k * lda] = scal[1];
 }
@@ -521,6 +592,61 @@ __global__ void eye_cols(long long m, int n, double* q, long long ldq) {
        e += static_cast<long long>(gridDim.x) * blockDim.x) {
     const long long i = e % m, j = e / m;
     q[i + j * ldq] = (i == j) ? 1.0 : 0.0;
+  }
+}
+
+// Explicit reflector block V (rows k0.., jb columns): unit diagonal, zeros
+// above, the stored v_i below (the factored panel keeps beta on its diagonal).
+__global__ void hh_panel_v(long long m, int k0, int jb, const double* __restrict__ a, long long lda,
+                           double* __restrict__ v, long long ldv) {
+  const long long rows = m - k0, total = rows * jb;
+  for (long long e = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; e < total;
+       e += static_cast<long long>(gridDim.x) * blockDim.x) {
+    const long long i = e % rows;
+    const int j = static_cast<int>(e / rows);
+    v[i + j * ldv] = i < j ? 0.0 : (i == j ? 1.0 : a[k0 + i + (k0 + j) * lda]);
+  }
+}
+
+// Forward column-wise block-reflector factor (H_0 ... H_{jb-1} = I - V T V^T):
+// T[i][i] = tau_i, T[0:i, i] = -tau_i T[0:i, 0:i] (V^T V)[0:i, i].  One block.
+__global__ void hh_form_t(int jb, const double* __restrict__ gram, const double* __restrict__ tau,
+                          double* __restrict__ t) {
+  __shared__ double T[32][33];
+  const int j = threadIdx.x;
+  if (j < jb)
+    for (int i = 0; i < jb; ++i) T[j][i] = 0.0;
+  __syncthreads();
+  for (int i = 0; i < jb; ++i) {
+    if (j < i) {
+      double s = 0.0;
+      for (int l = j; l < i; ++l) s += T[j][l] * gram[l + i * jb];
+      T[j][i] = -tau[i] * s;
+    } else if (j == i) {
+      T[i][i] = tau[i];
+    }
+    __syncthreads();
+  }
+  if (j < jb)
+    for (int i = 0; i < jb; ++i) t[j + i * jb] = T[j][i];
+}
+
+// W (jb x n) <- op(T) W, T upper triangular jb x jb; trans: T^T.
+__global__ void trmm_small(int jb, int n, const double* __restrict__ t, bool trans, double* __restrict__ w) {
+  __shared__ double col[32];
+  for (int c = blockIdx.x; c < n; c += gridDim.x) {
+    const int i = threadIdx.x;
+    if (i < jb) col[i] = w[i + c * jb];
+    __syncthreads();
+    if (i < jb) {
+      double s = 0.0;
+      if (trans)
+        for (int l = 0; l <= i; ++l) s += t[l + i * jb] * col[l];  // (T^T)[i][l] = T[l][i]
+      else
+        for (int l = i; l < jb; ++l) s += t[i + l * jb] * col[l];
+      w[i + c * jb] = s;
+    }
+    __syncthreads();
   }
 }
 
@@ -773,8 +899,12 @@ size_t gemm_tn_work(int M, int N, long long K) {
 void gemm_tn(int M, int N, long long K, const double* A, long long lda, const double* B, long long ldb, double* C,
              long long ldc, double* work, size_t work_doubles, cudaStream_t s) {
   if (M <= 0 || N <= 0) return;
+  // The split count (hence the summation order) is a function of the shape
+  // alone, never of the work buffer's capacity: results are reproducible
+  // whatever buffers earlier calls left behind.
   int splits = tn_splits(M, N, K);
-  while (splits > 1 && static_cast<size_t>(splits) * M * N > work_doubles) splits /= 2;
+  if (static_cast<size_t>(splits) * M * N > work_doubles)
+    throw std::invalid_argument("gemm_tn: work buffer smaller than gemm_tn_work(M, N, K)");
   long long kchunk = (K + splits - 1) / splits;
   kchunk = ((kchunk + 31) / 32) * 32;
   splits = static_cast<int>((K + kchunk - 1) / kchunk);
@@ -786,7 +916,7 @@ void gemm_tn(int M, int N, long long K, const double* A, long long lda, const do
     } else {
       gemm_tn_skinny_kernel<<<grid, 256, 0, s>>>(M, N, K, kchunk, A, lda, B, ldb, work, M,
                                                  static_cast<long long>(M) * N);
-      splitk_reduce<<<grid1d(static_cast<long long>(M) * N), 256, 0, s>>>(M, N, splits, work, C, ldc);
+      launch_splitk_reduce(M, N, splits, work, C, ldc, s);
     }
     RTLR_CUDA(cudaGetLastError());
     return;
@@ -796,7 +926,7 @@ void gemm_tn(int M, int N, long long K, const double* A, long long lda, const do
     gemm_tn_kernel<<<grid, 256, 0, s>>>(M, N, K, kchunk, A, lda, B, ldb, C, ldc, 0);
   } else {
     gemm_tn_kernel<<<grid, 256, 0, s>>>(M, N, K, kchunk, A, lda, B, ldb, work, M, static_cast<long long>(M) * N);
-    splitk_reduce<<<grid1d(static_cast<long long>(M) * N), 256, 0, s>>>(M, N, splits, work, C, ldc);
+    launch_splitk_reduce(M, N, splits, work, C, ldc, s);
   }
   RTLR_CUDA(cudaGetLastError());
 }
@@ -889,25 +1019,80 @@ void galerkin_batch(int r, int m, const int* angles, const double* dirs, const d
   RTLR_CUDA(cudaGetLastError());
 }
 
+constexpr size_t kQrPart = 1024;  // >= max(kDotParts, kQrBlock * kHhChunks)
+static_assert(kQrPart >= kQrBlock * kHhChunks && kQrPart >= kDotParts, "QR partials");
+
+size_t householder_qr_work(long long m, int n) {
+  constexpr int nb = kQrBlock;
+  size_t gemm = 0;  // the largest split-K workspace of any trailing / Q update
+  for (int c = 1; c <= n; ++c) gemm = std::max(gemm, gemm_tn_work(nb, c, m));
+  return kQrPart + 8 + static_cast<size_t>(m) * nb + 2 * static_cast<size_t>(nb) * n + 2 * nb * nb + gemm;
+}
+
+// Blocked Householder QR (LAPACK dgeqrf/dorgqr structure): each panel of
+// kQrBlock columns is factored column by column (Eigen's makeHouseholder
+// conventions, kernels above) and the trailing columns take the panel's
+// block reflector I - V T V^T through two tall GEMMs, so the trailing matrix
+// is read once per panel instead of once per column.  Q is formed the same
+// way, backwards.
 void householder_qr(long long m, int n, double* a, long long lda, double* tau, double* q, long long ldq, double* r,
-                    double* work, cudaStream_t s) {
-  // work: kDotParts + 4 doubles
+                    double* work, size_t work_doubles, cudaStream_t s) {
+  constexpr int nb = kQrBlock;
+  if (work_doubles < householder_qr_work(m, n))
+    throw std::invalid_argument("householder_qr: work buffer smaller than householder_qr_work(m, n)");
   double* part = work;
-  double* scal = work + kDotParts;
-  for (int k = 0; k < n && k < m; ++k) {
-    hh_tail<<<kDotParts, 256, 0, s>>>(m, k, a, lda, part);
-    hh_make<<<1, 256, 0, s>>>(kDotParts, k, a, lda, part, tau, scal);
-    hh_scale_tail<<<grid1d(m), 256, 0, s>>>(m, k, a, lda, scal);
-    if (k + 1 < n) hh_apply<<<n - k - 1, 256, 0, s>>>(m, k, a, lda, tau, a, lda, k + 1);
-    set_beta<<<1, 32, 0, s>>>(k, a, lda, scal);
+  double* scal = work + kQrPart;
+  double* V = scal + 8;
+  double* W = V + static_cast<size_t>(m) * nb;
+  double* G = W + 2 * static_cast<size_t>(nb) * n;
+  double* T = G + nb * nb;
+  double* gw = T + nb * nb;
+  const size_t gw_n = work_doubles - (gw - work);
+  const int kmax = static_cast<int>(std::min<long long>(n, m));
+  auto form_block = [&](int k0, int jb) {  // V (rows k0..m-1) and T of panel k0
+    const long long rows = m - k0;
+    hh_panel_v<<<grid1d(rows * jb), 256, 0, s>>>(m, k0, jb, a, lda, V, rows);
+    gemm_tn(jb, jb, rows, V, rows, V, rows, G, jb, gw, gw_n, s);
+    hh_form_t<<<1, 32, 0, s>>>(jb, G, tau + k0, T);
+  };
+  for (int k0 = 0; k0 < kmax; k0 += nb) {
+    const int jb = std::min(nb, kmax - k0);
+    for (int k = k0; k < k0 + jb; ++k) {
+      hh_tail<<<kDotParts, 256, 0, s>>>(m, k, a, lda, part);
+      hh_make<<<1, 256, 0, s>>>(kDotParts, k, a, lda, part, tau, scal);
+      hh_scale_tail<<<grid1d(m), 256, 0, s>>>(m, k, a, lda, scal);
+      const int nc = k0 + jb - k - 1;  // panel columns right of k
+      if (nc > 0) {
+        hh_dot_chunks<<<dim3(nc, kHhChunks), 256, 0, s>>>(m, k, a, lda, a, lda, k + 1, part);
+        hh_update_chunks<<<dim3(nc, kHhChunks), 256, 0, s>>>(m, k, a, lda, tau, a, lda, k + 1, part);
+        hh_update_diag<<<1, 32, 0, s>>>(k, tau, a, lda, k + 1, nc, part);
+      }
+      set_beta<<<1, 32, 0, s>>>(k, a, lda, scal);
+    }
+    const int nt = n - k0 - jb;
+    if (nt > 0) {  // A_trail -= V T^T (V^T A_trail)
+      const long long rows = m - k0;
+      form_block(k0, jb);
+      double* At = a + k0 + static_cast<long long>(k0 + jb) * lda;
+      gemm_tn(jb, nt, rows, V, rows, At, lda, W, jb, gw, gw_n, s);
+      trmm_small<<<std::min(nt, 4096), 32, 0, s>>>(jb, nt, T, true, W);
+      gemm_nn(rows, nt, jb, V, rows, W, jb, At, lda, s, /*subtract=*/true);
+    }
   }
   RTLR_CUDA(cudaGetLastError());
   extract_r<<<grid1d(static_cast<long long>(n) * n), 256, 0, s>>>(n, a, lda, r);
-  // Q = H_0 ... H_{n-1} I[:, :n], applied backwards.  v_k lives below the
-  // diagonal of a (v_0 = 1 implicit; the diagonal now holds beta).
+  // Q = H_0 ... H_{n-1} I[:, :n]: blocks applied backwards, Q_blk -= V T (V^T Q_blk)
   eye_cols<<<grid1d(m * n), 256, 0, s>>>(m, n, q, ldq);
-  for (int k = std::min<long long>(n, m) - 1; k >= 0; --k)
-    hh_apply<<<n, 256, 0, s>>>(m, k, a, lda, tau, q, ldq, 0);
+  for (int k0 = ((kmax - 1) / nb) * nb; k0 >= 0; k0 -= nb) {
+    const int jb = std::min(nb, kmax - k0);
+    const long long rows = m - k0;
+    const int nq = n - k0;
+    form_block(k0, jb);
+    double* Qb = q + k0 + static_cast<long long>(k0) * ldq;
+    gemm_tn(jb, nq, rows, V, rows, Qb, ldq, W, jb, gw, gw_n, s);
+    trmm_small<<<std::min(nq, 4096), 32, 0, s>>>(jb, nq, T, false, W);
+    gemm_nn(rows, nq, jb, V, rows, W, jb, Qb, ldq, s, /*subtract=*/true);
+  }
   RTLR_CUDA(cudaGetLastError());
 }
 

@@ -46,9 +46,13 @@ void galerkin_batch(int r, int m, const int* angles, const double* dirs, const d
                     long long ldsol, int* flags, double* work, cudaStream_t s);
 
 // Householder QR of an m x n (m >= n) column-major matrix (lda), in place;
-// tau (n).  Q formed explicitly into q (m x n).  r (n x n) upper.
+// tau (n).  Q formed explicitly into q (m x n).  r (n x n) upper.  Blocked
+// (panels of kQrBlock columns, block reflectors through tall GEMMs);
+// work >= householder_qr_work(m, n) doubles.
+constexpr int kQrBlock = 32;
+size_t householder_qr_work(long long m, int n);
 void householder_qr(long long m, int n, double* a, long long lda, double* tau, double* q, long long ldq,
-                    double* r, double* work, cudaStream_t s);
+                    double* r, double* work, size_t work_doubles, cudaStream_t s);
 
 // One-sided Jacobi on the columns of w (m x n, ld), accumulating the
 // rotations in v (n x n) when given.  Afterwards columns of w are mutually

@@ -198,6 +198,8 @@ class LowRankEngine {
   }
   ~LowRankEngine() { cudaFreeHost(hbuf_); }
   PhaseTimer pt_;
+  int reorth_count_ = 0;        // Householder rebuilds (all inner loops)
+  double reorth_seconds_ = 0.0;  // their wall time (meaningful with RTLR_PROFILE=1)
 
   InnerResult inner(const double* d_phi_prev, SubsampleRng& rng);
   int rank() const { return rank_; }
@@ -211,12 +213,18 @@ class LowRankEngine {
   bool mgs_ro_update(const double* snaps, const std::vector<int>& angles);
   void update_projections(bool reorth);
   void galerkin(const std::vector<int>& angles, double* d_sol, long long ldsol);
+  void galerkin_solve(const std::vector<int>& angles, double* d_sol, long long ldsol);
   std::vector<double> residual_norms(const std::vector<int>& angles, const double* coeffs, long long ldc);
   void build_full_coefficients(const std::vector<int>* cand, const double* cand_sol);
   void phi_from_C();
   double host_dot(const double* a, const double* b, long long n);
   int* upload_ints(DBuf<int>& buf, const std::vector<int>& a);
   double* work(size_t need) { return work_.ensure(std::max<size_t>(need, 4096)); }
+  // C = A^T B (K = N_x) with its split-K workspace
+  void tn(int M, int N, const double* A, long long lda, const double* B, long long ldb, double* C, long long ldc) {
+    double* w = work(gemm_tn_work(M, N, n_));
+    gemm_tn(M, N, n_, A, lda, B, ldb, C, ldc, w, work_.size(), s_);
+  }
   // Angle sharding of one phase's m items over the communicator's ranks
   // (the whole list without one); padded(m) = items incl. the all-gather pad.
   ShardBlock blk(int m) const {
@@ -236,8 +244,8 @@ class LowRankEngine {
   const double* dirs_;
   DMat X_;
   DBuf<double> proj_, prhs_, rhs_core_, phi_, phi_old_, rem_, vec_, C_, work_, snaps_, wbuf_, gbuf_, sol_, cand_,
-      ybuf_, nrm_, qa_, qq_, qr_, tau_, hrec_, luw_;
-  DBuf<int> ang_, ang2_, flags_;
+      ybuf_, nrm_, qa_, qq_, qr_, tau_, hrec_, luw_, gsol_;
+  DBuf<int> ang_, ang2_, flags_, pos_;
   double* hbuf_ = nullptr;
   int rank_ = 0, n_snap_ = 0, prev_rank_ = 0;
   std::vector<std::vector<double>> rec_;
@@ -294,11 +302,9 @@ bool LowRankEngine::mgs_ro_update(const double* snaps, const std::vector<int>& a
   if (r_old > 0) {
     double* C1 = gbuf_.ensure(static_cast<size_t>(2) * r_old * p_in);
     double* C2 = C1 + static_cast<size_t>(r_old) * p_in;
-    gemm_tn(r_old, p_in, n_, X_.col(0), X_.ld, snaps, n_, C1, r_old, work(gemm_tn_work(r_old, p_in, n_)),
-            work_.size(), s_);
+    tn(r_old, p_in, X_.col(0), X_.ld, snaps, n_, C1, r_old);
     gemm_nn(n_, p_in, r_old, X_.col(0), X_.ld, C1, r_old, Rm, n_, s_, /*subtract=*/true);
-    gemm_tn(r_old, p_in, n_, X_.col(0), X_.ld, Rm, n_, C2, r_old, work(gemm_tn_work(r_old, p_in, n_)),
-            work_.size(), s_);
+    tn(r_old, p_in, X_.col(0), X_.ld, Rm, n_, C2, r_old);
     gemm_nn(n_, p_in, r_old, X_.col(0), X_.ld, C2, r_old, Rm, n_, s_, /*subtract=*/true);
     std::vector<double> h1(static_cast<size_t>(r_old) * p_in), h2(h1.size());
     RTLR_CUDA(cudaMemcpyAsync(h1.data(), C1, h1.size() * sizeof(double), cudaMemcpyDeviceToHost, s_));
@@ -318,14 +324,12 @@ bool LowRankEngine::mgs_ro_update(const double* snaps, const std::vector<int>& a
     std::vector<double> reccol(rank_ + 1, 0.0);
     for (int k = 0; k < r_old; ++k) reccol[k] = cold[k + static_cast<size_t>(i) * r_old];
     if (k_new > 0) {
-      gemm_tn(k_new, 1, n_, X_.col(r_old), X_.ld, rem, n_, cnew, k_new, work(gemm_tn_work(k_new, 1, n_)),
-              work_.size(), s_);
+      tn(k_new, 1, X_.col(r_old), X_.ld, rem, n_, cnew, k_new);
       gemv_n(n_, k_new, X_.col(r_old), X_.ld, cnew, -1.0, rem, s_);
       RTLR_CUDA(cudaMemcpyAsync(hc.data(), cnew, k_new * sizeof(double), cudaMemcpyDeviceToHost, s_));
       const double rn = std::sqrt(host_dot(rem, rem, n_));
       if (rn < 0.5 * norm0[i]) {
-        gemm_tn(k_new, 1, n_, X_.col(r_old), X_.ld, rem, n_, corr, k_new, work(gemm_tn_work(k_new, 1, n_)),
-                work_.size(), s_);
+        tn(k_new, 1, X_.col(r_old), X_.ld, rem, n_, corr, k_new);
         gemv_n(n_, k_new, X_.col(r_old), X_.ld, corr, -1.0, rem, s_);
         RTLR_CUDA(cudaMemcpyAsync(hc2.data(), corr, k_new * sizeof(double), cudaMemcpyDeviceToHost, s_));
         RTLR_CUDA(cudaStreamSynchronize(s_));
@@ -352,6 +356,9 @@ bool LowRankEngine::mgs_ro_update(const double* snaps, const std::vector<int>& a
     reorth = overlap > prm_.eps_mgs;
   }
   if (reorth) {
+    ++reorth_count_;
+    if (pt_.on) RTLR_CUDA(cudaStreamSynchronize(s_));
+    const auto tq0 = std::chrono::steady_clock::now();
     const int n_acc = static_cast<int>(accepted.size());
     const int r_new = prev_rank_ + n_acc;
     double* M = qa_.ensure(static_cast<size_t>(n_) * r_new);
@@ -365,11 +372,12 @@ bool LowRankEngine::mgs_ro_update(const double* snaps, const std::vector<int>& a
     double* Q = qq_.ensure(static_cast<size_t>(n_) * r_new);
     double* R = qr_.ensure(static_cast<size_t>(r_new) * r_new);
     double* tau = tau_.ensure(r_new);
-    householder_qr(n_, r_new, M, n_, tau, Q, n_, R, work(4096), s_);
+    double* qw = work(householder_qr_work(n_, r_new));
+    householder_qr(n_, r_new, M, n_, tau, Q, n_, R, qw, work_.size(), s_);
     std::vector<double> hR(static_cast<size_t>(r_new) * r_new);
     RTLR_CUDA(cudaMemcpyAsync(hR.data(), R, hR.size() * sizeof(double), cudaMemcpyDeviceToHost, s_));
     double* B = gbuf_.ensure(static_cast<size_t>(r_new) * p_in);
-    gemm_tn(r_new, p_in, n_, Q, n_, snaps, n_, B, r_new, work(gemm_tn_work(r_new, p_in, n_)), work_.size(), s_);
+    tn(r_new, p_in, Q, n_, snaps, n_, B, r_new);
     std::vector<double> hB(static_cast<size_t>(r_new) * p_in);
     RTLR_CUDA(cudaMemcpyAsync(hB.data(), B, hB.size() * sizeof(double), cudaMemcpyDeviceToHost, s_));
     RTLR_CUDA(cudaMemcpyAsync(X_.col(0), Q, static_cast<size_t>(n_) * r_new * sizeof(double),
@@ -389,6 +397,7 @@ bool LowRankEngine::mgs_ro_update(const double* snaps, const std::vector<int>& a
         }
     for (int j = 0; j < p_in; ++j)
       for (int i = 0; i < rank_; ++i) rec_[m0 + j][i] = hB[i + static_cast<size_t>(j) * r_new];
+    reorth_seconds_ += std::chrono::duration<double>(std::chrono::steady_clock::now() - tq0).count();
   }
   return reorth;
 }
@@ -406,21 +415,46 @@ void LowRankEngine::update_projections(bool reorth) {
     double* W = wbuf_.ensure(static_cast<size_t>(n_) * 5 * chunk);
     stream_products(sa_, pc, X_.col(r0 + c0), X_.ld, W, n_, s_);
     double* G = gbuf_.ensure(static_cast<size_t>(rank_) * 5 * chunk);
-    gemm_tn(rank_, 5 * pc, n_, X_.col(0), X_.ld, W, n_, G, rank_, work(gemm_tn_work(rank_, 5 * pc, n_)),
-            work_.size(), s_);
+    tn(rank_, 5 * pc, X_.col(0), X_.ld, W, n_, G, rank_);
     proj_border_kernel<<<g1(static_cast<long long>(rank_) * pc), 256, 0, s_>>>(r0, pn, c0, pc, G, rank_, proj_.get(),
                                                                              ldp_, ldp_ * ldp_, rank_);
     RTLR_CUDA(cudaGetLastError());
   }
-  gemm_tn(pn, 1, n_, X_.col(r0), X_.ld, rhs_core_.get(), n_, prhs_.get() + r0, pn, work(gemm_tn_work(pn, 1, n_)),
-          work_.size(), s_);
+  tn(pn, 1, X_.col(r0), X_.ld, rhs_core_.get(), n_, prhs_.get() + r0, pn);
 }
 
 // galerkin_solve for a list of angles (low_rank.cpp:192-200), batched.
-// Sharded: this rank solves its block of the angles and one all-gather
-// assembles every column on every rank (d_sol holds padded(m) columns).
+// Mirror directions share (Omega_x, Omega_y) bitwise and, without inflow
+// data, the reduced right-hand side, so each distinct system is solved once
+// and its solution copied (bitwise the per-angle result).
 void LowRankEngine::galerkin(const std::vector<int>& angles, double* d_sol, long long ldsol) {
   if (rank_ < 1) throw std::runtime_error("galerkin_solve: empty basis");
+  if (!hp_.bc_any) {
+    std::vector<int> reps, pos(angles.size()), seen(P_.uniq_rep_.size(), -1);
+    for (size_t k = 0; k < angles.size(); ++k) {
+      const int u = P_.uniq_of_[angles[k]];
+      if (seen[u] < 0) {
+        seen[u] = static_cast<int>(reps.size());
+        reps.push_back(angles[k]);
+      }
+      pos[k] = seen[u];
+    }
+    if (reps.size() < angles.size()) {
+      double* tmp = gsol_.ensure(static_cast<size_t>(rank_) * padded(static_cast<int>(reps.size())));
+      galerkin_solve(reps, tmp, rank_);
+      int* dpos = upload_ints(pos_, pos);
+      const int m = static_cast<int>(angles.size());
+      gather_cols<<<g1(static_cast<long long>(rank_) * m), 256, 0, s_>>>(rank_, m, dpos, tmp, rank_, d_sol, ldsol);
+      RTLR_CUDA(cudaGetLastError());
+      return;
+    }
+  }
+  galerkin_solve(angles, d_sol, ldsol);
+}
+
+// Sharded: this rank solves its block of the angles and one all-gather
+// assembles every column on every rank (d_sol holds padded(m) columns).
+void LowRankEngine::galerkin_solve(const std::vector<int>& angles, double* d_sol, long long ldsol) {
   const int m = static_cast<int>(angles.size());
   const ShardBlock sb = blk(m);
   const long long rr = static_cast<long long>(rank_) * rank_;
@@ -437,7 +471,7 @@ void LowRankEngine::galerkin(const std::vector<int>& angles, double* d_sol, long
       for (int j = 0; j < mc; ++j)
         RTLR_CUDA(cudaMemcpyAsync(Gb + static_cast<size_t>(j) * n_, P_.bc_.get() + static_cast<size_t>(sub[j]) * n_,
                                   n_ * sizeof(double), cudaMemcpyDeviceToDevice, s_));
-      gemm_tn(rank_, mc, n_, X_.col(0), X_.ld, Gb, n_, out, ldsol, work(gemm_tn_work(rank_, mc, n_)), work_.size(), s_);
+      tn(rank_, mc, X_.col(0), X_.ld, Gb, n_, out, ldsol);
       extra = out;
     }
     int* flags = flags_.ensure(mc);
@@ -787,7 +821,7 @@ SolveReport Problem::solve_low_rank(const LowRankOptions& o) {
   if (eng.pt_.on) {
     std::fprintf(stderr, "[rtlr profile] low-rank phases (s):");
     for (auto& e : eng.pt_.acc) std::fprintf(stderr, " %s=%.4f", e.first.c_str(), e.second);
-    std::fprintf(stderr, "\n");
+    std::fprintf(stderr, " | reorth: %d rebuilds, %.4f s (inside cgs)\n", eng.reorth_count_, eng.reorth_seconds_);
   }
   rep.phi.resize(n);
   RTLR_CUDA(cudaMemcpyAsync(rep.phi.data(), phi, n * sizeof(double), cudaMemcpyDeviceToHost, stream_));

@@ -2,6 +2,7 @@
 // reference's (proj/include/rtlr/{sweep,full_rank,low_rank,diffusion}.hpp).
 #pragma once
 
+#include <algorithm>
 #include <memory>
 #include <utility>
 #include <string>
@@ -27,12 +28,16 @@ class DBuf {
     p_ = nullptr;
     n_ = 0;
   }
-  // Grow to at least n elements (contents not preserved).
+  // Grow to at least n elements (contents not preserved).  A buffer that
+  // grows again gets 1.5x headroom, so steadily growing work buffers (the
+  // low-rank basis raises r every inner iteration) reallocate O(log) times:
+  // cudaFree synchronizes the device.
   T* ensure(size_t n) {
     if (n > n_) {
+      const size_t want = n_ ? std::max(n, n_ + n_ / 2) : n;
       release();
-      RTLR_CUDA(cudaMalloc(&p_, (n ? n : 1) * sizeof(T)));
-      n_ = n;
+      RTLR_CUDA(cudaMalloc(&p_, (want ? want : 1) * sizeof(T)));
+      n_ = want;
     }
     return p_;
   }

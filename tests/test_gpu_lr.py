@@ -126,3 +126,18 @@ def test_sharded_low_rank_single_rank_nccl_is_bitwise():
     assert np.array_equal(rb.phi, ra.phi)
     assert list(rb.history("rank")) == list(ra.history("rank"))
     assert rb.sampled_log() == ra.sampled_log()
+
+
+@pytest.mark.parametrize("m,n", [(5000, 70), (3000, 33), (2048, 32), (777, 1), (4096, 96)])
+def test_blocked_householder_qr(m, n):
+    """Blocked Householder QR (basis rebuild, low_rank.cpp:112-130): q r = a,
+    q orthonormal, r upper, |r| equal to LAPACK's (signs follow Eigen)."""
+    rng = np.random.default_rng(m + n)
+    a = rng.standard_normal((m, n))
+    a[:, n // 2] = a[:, 0] + 1e-9 * rng.standard_normal(m)  # a nearly dependent column
+    q, r = P.dense_qr(a)
+    assert np.allclose(np.triu(r), r, rtol=0, atol=0)
+    assert np.linalg.norm(q @ r - a) / np.linalg.norm(a) <= 1e-14
+    assert np.linalg.norm(q.T @ q - np.eye(n)) <= 1e-13
+    r_ref = np.linalg.qr(a, mode="r")
+    assert np.allclose(np.abs(np.diag(r)), np.abs(np.diag(r_ref)), rtol=1e-8, atol=1e-12)
