@@ -46,7 +46,8 @@ def parse():
     ap.add_argument("--n-theta", type=int, default=128)
     ap.add_argument("--n-omega-z", type=int, default=32)
     ap.add_argument("--e2e-chunk", type=int, default=256, help="directions per host-buffer call")
-    ap.add_argument("--no-solvers", action="store_true", help="skip the C1/C2 time-to-tol extras")
+    ap.add_argument("--no-solvers", action="store_true", help="skip the solver time-to-tol leg")
+    ap.add_argument("--solver-timeout", type=float, default=420.0, help="watchdog for the solver leg (s)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true", help="skip the CPU baseline sample")
     ap.add_argument("--cpu-sample-updates", type=float, default=8e7,
@@ -183,6 +184,51 @@ def run_reference(args, rank, world):
     print(json.dumps(line), flush=True)
 
 
+SOLVER_JOBS = (("C2", "lowrank"), ("C4", "full"), ("C4", "lowrank"))
+
+
+def solver_leg(P, local, rank, world, dist):
+    """BASELINE's second metric: SI-DSA time-to-tol on the solver configs,
+    angle-sharded over the run's GPUs (one process per GPU, NCCL): FR sums
+    the phi partials of each rank's directions; LR shards the sampled sweeps,
+    Galerkin solves and residual norms and all-gathers them.  Every rank
+    returns the same report; rank 0's times are reported."""
+    import torch
+    out = {}
+    for name, method in SOLVER_JOBS:
+        sp = P.Problem(name, device=local)
+        if world > 1:  # a fresh NCCL id per communicator, from rank 0
+            buf = torch.zeros(128, dtype=torch.uint8, device="cuda")
+            if rank == 0:
+                buf.copy_(torch.tensor(list(P.nccl_unique_id()), dtype=torch.uint8))
+            dist.broadcast(buf, 0)
+            sp.set_comm(world, rank, bytes(buf.cpu().tolist()))
+        t0 = time.perf_counter()
+        rep = sp.solve_full_rank(store_psi=0) if method == "full" else sp.solve_low_rank(build_factors=0)
+        wall = time.perf_counter() - t0
+        entry = {"method": method, "time_to_tol_s": float(rep.get("solve_seconds", 1)[0]), "wall_s": wall,
+                 "iterations": rep.iterations, "converged": rep.converged, "gpus": world,
+                 "sharding": "angles" if world > 1 else "none"}
+        if method == "lowrank":
+            entry["final_rank"] = int(rep.history("rank")[-1])
+        out[f"{name}_{method}"] = entry
+        del sp
+        torch.cuda.synchronize()
+    return out
+
+
+def arm_watchdog(seconds, line, rank):
+    def fire():
+        if rank == 0:
+            line["solvers"] = {"error": f"solver leg exceeded {seconds:.0f} s"}
+            print(json.dumps(line), flush=True)
+        os._exit(0)
+    t = threading.Timer(seconds, fire)
+    t.daemon = True
+    t.start()
+    return t
+
+
 def workload_config(args):
     nd = args.n_theta * args.n_omega_z
     return {"workload": f"C5 sweep {args.grid}^2 cells x CL({args.n_theta},{args.n_omega_z}) = {nd} directions",
@@ -310,23 +356,6 @@ def main():
                "h2d_bytes_per_step": D * n * 8, "d2h_bytes_per_step": D * n * 8,
                "steps": e2e_steps, "chunk_directions": C, "api": "rtlr_cu_sweep(where=RTLR_CU_HOST)"}
 
-    # Secondary BASELINE metric: solver time-to-tol through the public API
-    # (assembly + upload excluded, as the reference's solve_seconds).
-    solvers = None
-    if rank == 0 and not args.no_solvers:
-        solvers = {}
-        for name, method in (("C1", "full"), ("C2", "lowrank")):
-            sp = P.Problem(name, device=local)
-            t0 = time.perf_counter()
-            rep = sp.solve_full_rank(store_psi=0) if method == "full" else sp.solve_low_rank(build_factors=0)
-            wall = time.perf_counter() - t0
-            entry = {"method": method, "time_to_tol_s": float(rep.get("solve_seconds", 1)[0]), "wall_s": wall,
-                     "iterations": rep.iterations, "converged": rep.converged}
-            if method == "lowrank":
-                entry["final_rank"] = int(rep.history("rank")[-1])
-            solvers[name] = entry
-            del sp
-
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
         ndirs = max(1, min(D, int(args.cpu_sample_updates // cells)))
@@ -334,15 +363,30 @@ def main():
         cpu = {"value": r, "unit": "cell-angle updates/s", "cores": 1, "kind": "port",
                "sample": f"{ndirs} directions x {args.grid}^2 cells ({upd} updates, {dt:.1f} s)"}
 
+    line = {
+        "metric": "sweep cell-angle updates/s", "value": value, "unit": "cell-angle updates/s",
+        "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_max,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic", "config": workload_config(args) | {"parallelism": f"direction-sets x{world}"},
+        "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": args.steps,
+        "clocks": clk.summary(), "solvers": None,
+    }
+
+    # Secondary BASELINE metric: SI-DSA time-to-tol through the public API,
+    # angle-sharded over this run's N GPUs (assembly + upload excluded, as the
+    # reference's solve_seconds).  A watchdog keeps a multi-rank failure from
+    # swallowing the line: past the limit rank 0 prints it without solvers.
+    if not args.no_solvers:
+        del rhs, psi, prob  # the sweep workload's 68 GB are not needed any more
+        torch.cuda.empty_cache()
+        wd = arm_watchdog(args.solver_timeout, line, rank)
+        try:
+            line["solvers"] = solver_leg(P, local, rank, world, dist)
+        except Exception as exc:  # reported, never fatal for the sweep metric
+            line["solvers"] = {"error": f"{type(exc).__name__}: {exc}"[:300]}
+        wd.cancel()
+
     if rank == 0:
-        line = {
-            "metric": "sweep cell-angle updates/s", "value": value, "unit": "cell-angle updates/s",
-            "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_max,
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-            "data": "synthetic", "config": workload_config(args) | {"parallelism": f"direction-sets x{world}"},
-            "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": args.steps,
-            "clocks": clk.summary(), "solvers": solvers,
-        }
         print(json.dumps(line), flush=True)
     if dist:
         dist.destroy_process_group()
