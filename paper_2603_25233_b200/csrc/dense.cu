@@ -710,11 +710,11 @@ __global__ void __launch_bounds__(256) jacobi_round(long long m, int n, int npad
 // ------------------------------------------------------------ blocked batched LU
 // Right-looking LU with partial pivoting (first maximum, as Eigen's
 // PartialPivLU) of the augmented systems [A_j | b_j] (r x (r+1), column-
-// major, ld r) in panels of kNb columns: panel factorisation (one CTA per
-// system), row swaps + unit-lower TRSM of the panel rows, a tiled GEMM
-// trailing update over many CTAs, then back substitution.  Forward
-// substitution on b happens through the augmented column.
-constexpr int kNb = 16;
+// major, ld r) in panels of up to 32 columns: panel factorisation in shared
+// memory (one CTA per system), then per 64-column tile of the trailing
+// columns the panel's row swaps, the unit-lower TRSM and the GEMM update
+// (many CTAs), then back substitution.  Forward substitution on b happens
+// through the augmented column.
 
 __global__ void __launch_bounds__(256) lu_assemble(int r, const int* __restrict__ angles, const double* __restrict__ dirs,
                                                    const double* __restrict__ proj, long long ldp, long long pstride,
@@ -736,158 +736,197 @@ __global__ void __launch_bounds__(256) lu_assemble(int r, const int* __restrict_
   }
 }
 
-__global__ void __launch_bounds__(256) lu_panel(int r, int k0, int jb, double* __restrict__ M, int* __restrict__ piv) {
-  __shared__ double shv[33];
-  __shared__ int shi[33];
+constexpr int kNbMax = 32;
+constexpr int kPanelSmemBytes = 200 * 1024;
+
+// Panel width for the panel starting at k0: 32, halved while the panel's
+// rows do not fit the shared-memory budget.
+__host__ __device__ inline int lu_panel_width(int r, int k0) {
+  int jb = kNbMax;
+  while (jb > 1 && static_cast<long long>(r - k0) * jb * 8 > kPanelSmemBytes) jb >>= 1;
+  return jb < r - k0 ? jb : r - k0;
+}
+
+// Partial-pivot LU of the panel columns k0..k0+jb-1 (rows k0..r-1) in shared
+// memory; pivots to piv; one CTA of NT threads per system.  Two barriers per
+// column: the pivot candidates of column j+1 are reduced by the same pass
+// that applies column j's rank-1 update (each thread owns whole rows).
+__device__ __forceinline__ void argmax_merge(double& best, int& bi, double ov, int oi) {
+  if (ov > best || (ov == best && oi < bi)) {
+    best = ov;
+    bi = oi;
+  }
+}
+
+template <int NT>
+__global__ void __launch_bounds__(NT) lu_panel_smem(int r, int k0, int jb, double* __restrict__ M,
+                                                    int* __restrict__ piv) {
+  constexpr int NW = NT / 32;
+  extern __shared__ double P[];  // (r - k0) x jb, column-major, ld = rows
+  __shared__ double shv[2][NW];
+  __shared__ int shi[2][NW];
   double* A = M + static_cast<size_t>(blockIdx.x) * r * (r + 1);
   int* pv = piv + static_cast<size_t>(blockIdx.x) * r;
-  const int tid = threadIdx.x, nt = blockDim.x;
-  for (int j = k0; j < k0 + jb; ++j) {
-    double best = -1.0;
-    int bi = r;
-    for (int i = j + tid; i < r; i += nt) {
-      const double v = fabs(A[i + static_cast<size_t>(j) * r]);
-      if (v > best) {
-        best = v;
-        bi = i;
-      }
-    }
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-      const double ov = __shfl_xor_sync(0xffffffffu, best, o);
-      const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
-      if (ov > best || (ov == best && oi < bi)) {
-        best = ov;
-        bi = oi;
-      }
-    }
-    if ((tid & 31) == 0) {
-      shv[tid >> 5] = best;
-      shi[tid >> 5] = bi;
-    }
-    __syncthreads();
-    if (tid == 0) {
-      double bv = shv[0];
-      int bix = shi[0];
-      for (int w = 1; w < (nt >> 5); ++w)
-        if (shv[w] > bv || (shv[w] == bv && shi[w] < bix)) {
-          bv = shv[w];
-          bix = shi[w];
-        }
-      shi[32] = bv > 0.0 ? bix : j;  // all-zero column: no swap (first zero pivot)
-      shv[32] = bv;
-      pv[j] = shi[32];
-    }
-    __syncthreads();
-    const int p = shi[32];
-    const bool nonzero = shv[32] > 0.0;
-    if (p != j)
-      for (int c = k0 + tid; c < k0 + jb; c += nt) {
-        const double t = A[j + static_cast<size_t>(c) * r];
-        A[j + static_cast<size_t>(c) * r] = A[p + static_cast<size_t>(c) * r];
-        A[p + static_cast<size_t>(c) * r] = t;
-      }
-    __syncthreads();
-    if (nonzero) {
-      const double d = A[j + static_cast<size_t>(j) * r];
-      for (int i = j + 1 + tid; i < r; i += nt) A[i + static_cast<size_t>(j) * r] /= d;
-    }
-    __syncthreads();
-    const int rows = r - j - 1, cols = k0 + jb - j - 1;
-    for (int e = tid; e < rows * cols; e += nt) {
-      const int i = j + 1 + e % rows, c = j + 1 + e / rows;
-      A[i + static_cast<size_t>(c) * r] -= A[i + static_cast<size_t>(j) * r] * A[j + static_cast<size_t>(c) * r];
-    }
-    __syncthreads();
-  }
-}
-
-// row swaps of the panel applied to the trailing columns, then U12 = L11^-1 A12
-__global__ void __launch_bounds__(256) lu_swap_trsm(int r, int k0, int jb, double* __restrict__ M,
-                                                    const int* __restrict__ piv) {
-  double* A = M + static_cast<size_t>(blockIdx.y) * r * (r + 1);
-  const int* pv = piv + static_cast<size_t>(blockIdx.y) * r;
-  const int c = k0 + jb + blockIdx.x * blockDim.x + threadIdx.x;
-  if (c > r) return;  // columns k0+jb .. r (r is the augmented rhs)
-  double* col = A + static_cast<size_t>(c) * r;
-  for (int j = k0; j < k0 + jb; ++j) {
-    const int p = pv[j];
-    if (p != j) {
-      const double t = col[j];
-      col[j] = col[p];
-      col[p] = t;
-    }
-  }
-  double u[kNb];
-#pragma unroll
-  for (int i = 0; i < kNb; ++i) {
-    if (i >= jb) break;
-    double s = col[k0 + i];
-    for (int l = 0; l < i; ++l) s -= A[k0 + i + static_cast<size_t>(k0 + l) * r] * u[l];
-    u[i] = s;
-    col[k0 + i] = s;
-  }
-}
-
-// A22 -= L21 U12 over rows k0+jb..r-1, columns k0+jb..r; grid (tilesM, tilesN, m)
-__global__ void __launch_bounds__(256) lu_update(int r, int k0, int jb, double* __restrict__ M) {
-  __shared__ double Ls[kNb][BM + 1];
-  __shared__ double Us[kNb][BN + 1];
-  double* A = M + static_cast<size_t>(blockIdx.z) * r * (r + 1);
-  const int row0 = k0 + jb + blockIdx.x * BM, col0 = k0 + jb + blockIdx.y * BN;
-  const int tid = threadIdx.x, tm = tid % 16, tn = tid / 16;
-  for (int e = tid; e < kNb * BM; e += 256) {
-    const int kk = e / BM, mm = e % BM;
-    const int i = row0 + mm;
-    Ls[kk][mm] = (kk < jb && i < r) ? A[i + static_cast<size_t>(k0 + kk) * r] : 0.0;
-    const int nn = e % BN, kk2 = e / BN;
-    const int c = col0 + nn;
-    Us[kk2][nn] = (kk2 < jb && c <= r) ? A[k0 + kk2 + static_cast<size_t>(c) * r] : 0.0;
+  const int rows = r - k0, tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  for (int e = tid; e < rows * jb; e += NT) {
+    const int i = e % rows, c = e / rows;
+    P[e] = A[k0 + i + static_cast<size_t>(k0 + c) * r];
   }
   __syncthreads();
-  double acc[4][4] = {};
+  auto publish = [&](int buf, double best, int bi) {
 #pragma unroll
-  for (int kk = 0; kk < kNb; ++kk) {
-    double a[4], b[4];
+    for (int o = 16; o > 0; o >>= 1)
+      argmax_merge(best, bi, __shfl_xor_sync(0xffffffffu, best, o), __shfl_xor_sync(0xffffffffu, bi, o));
+    if (lane == 0) {
+      shv[buf][wid] = best;
+      shi[buf][wid] = bi;
+    }
+  };
+  {  // pivot candidates of column 0
+    double best = -1.0;
+    int bi = rows;
+    for (int i = tid; i < rows; i += NT) argmax_merge(best, bi, fabs(P[i]), i);
+    publish(0, best, bi);
+  }
+  __syncthreads();
+  for (int j = 0; j < jb; ++j) {
+    const int buf = j & 1;
+    double bv = shv[buf][0];
+    int bix = shi[buf][0];
 #pragma unroll
-    for (int i = 0; i < 4; ++i) a[i] = Ls[kk][tm + 16 * i];
+    for (int w = 1; w < NW; ++w) argmax_merge(bv, bix, shv[buf][w], shi[buf][w]);
+    const int p = bv > 0.0 ? bix : j;  // all-zero column: no swap (first zero pivot)
+    if (tid == 0) pv[k0 + j] = k0 + p;
+    if (p != j && tid < jb) {
+      double* c = P + static_cast<size_t>(tid) * rows;
+      const double t = c[j];
+      c[j] = c[p];
+      c[p] = t;
+    }
+    __syncthreads();
+    const double* colj = P + static_cast<size_t>(j) * rows;
+    const double d = colj[j];
+    double best = -1.0;
+    int bi = rows;
+    for (int i = j + 1 + tid; i < rows; i += NT) {
+      const double l = d != 0.0 ? P[i + static_cast<size_t>(j) * rows] / d : P[i + static_cast<size_t>(j) * rows];
+      P[i + static_cast<size_t>(j) * rows] = l;
+      for (int c = j + 1; c < jb; ++c) P[i + static_cast<size_t>(c) * rows] -= l * P[j + static_cast<size_t>(c) * rows];
+      if (j + 1 < jb) argmax_merge(best, bi, fabs(P[i + static_cast<size_t>(j + 1) * rows]), i);
+    }
+    publish(buf ^ 1, best, bi);
+    __syncthreads();
+  }
+  for (int e = tid; e < rows * jb; e += NT) {
+    const int i = e % rows, c = e / rows;
+    A[k0 + i + static_cast<size_t>(k0 + c) * r] = P[e];
+  }
+}
+
+// For one 64-column tile of the trailing columns (k0+jb .. r, the last one
+// the augmented rhs): the panel's row swaps, U12 = L11^-1 A12, then
+// A22 -= L21 U12 row tile by row tile.  grid (column tiles, systems).
+__global__ void __launch_bounds__(256) lu_trail(int r, int k0, int jb, double* __restrict__ M,
+                                                const int* __restrict__ piv) {
+  __shared__ double Us[kNbMax][BN + 1];
+  __shared__ double Ls[kNbMax][BM + 1];
+  __shared__ double L11[kNbMax][kNbMax + 1];
+  double* A = M + static_cast<size_t>(blockIdx.y) * r * (r + 1);
+  const int* pv = piv + static_cast<size_t>(blockIdx.y) * r;
+  const int col0 = k0 + jb + blockIdx.x * BN;
+  const int tid = threadIdx.x;
+  // swaps, one thread per column of the tile
+  if (tid < BN) {
+    const int c = col0 + tid;
+    if (c <= r) {
+      double* col = A + static_cast<size_t>(c) * r;
+      for (int j = k0; j < k0 + jb; ++j) {
+        const int p = pv[j];
+        if (p != j) {
+          const double t = col[j];
+          col[j] = col[p];
+          col[p] = t;
+        }
+      }
+    }
+  }
+  for (int e = tid; e < jb * jb; e += 256) {
+    const int i = e % jb, l = e / jb;
+    L11[i][l] = A[k0 + i + static_cast<size_t>(k0 + l) * r];
+  }
+  __syncthreads();
+  // U12 tile: forward substitution with unit-lower L11, one thread per column
+  if (tid < BN) {
+    const int c = col0 + tid;
+    double* col = A + static_cast<size_t>(c) * r;
+    for (int i = 0; i < jb; ++i) {
+      double s = c <= r ? col[k0 + i] : 0.0;
+      for (int l = 0; l < i; ++l) s -= L11[i][l] * Us[l][tid];
+      Us[i][tid] = s;
+      if (c <= r) col[k0 + i] = s;
+    }
+    for (int i = jb; i < kNbMax; ++i) Us[i][tid] = 0.0;
+  }
+  __syncthreads();
+  const int tm = tid % 16, tn = tid / 16;
+  for (int row0 = k0 + jb; row0 < r; row0 += BM) {
+    for (int e = tid; e < kNbMax * BM; e += 256) {
+      const int mm = e % BM, kk = e / BM;
+      const int i = row0 + mm;
+      Ls[kk][mm] = (kk < jb && i < r) ? A[i + static_cast<size_t>(k0 + kk) * r] : 0.0;
+    }
+    __syncthreads();
+    double acc[4][4] = {};
+#pragma unroll 8
+    for (int kk = 0; kk < kNbMax; ++kk) {
+      double a[4], b[4];
 #pragma unroll
-    for (int j = 0; j < 4; ++j) b[j] = Us[kk][tn + 16 * j];
+      for (int i = 0; i < 4; ++i) a[i] = Ls[kk][tm + 16 * i];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) b[j] = Us[kk][tn + 16 * j];
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) acc[i][j] += a[i] * b[j];
+    }
 #pragma unroll
     for (int i = 0; i < 4; ++i)
 #pragma unroll
-      for (int j = 0; j < 4; ++j) acc[i][j] += a[i] * b[j];
+      for (int j = 0; j < 4; ++j) {
+        const int row = row0 + tm + 16 * i, c = col0 + tn + 16 * j;
+        if (row < r && c <= r) A[row + static_cast<size_t>(c) * r] -= acc[i][j];
+      }
+    __syncthreads();
   }
-#pragma unroll
-  for (int i = 0; i < 4; ++i)
-#pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      const int row = row0 + tm + 16 * i, c = col0 + tn + 16 * j;
-      if (row < r && c <= r) A[row + static_cast<size_t>(c) * r] -= acc[i][j];
-    }
 }
 
-// back substitution with U (column oriented, as Eigen), solution to sol
-__global__ void __launch_bounds__(256) lu_backsolve(int r, const double* __restrict__ M, double* __restrict__ sol,
-                                                    long long ldsol, int* __restrict__ flags) {
-  extern __shared__ double xs[];
-  const double* A = M + static_cast<size_t>(blockIdx.x) * r * (r + 1);
-  for (int i = threadIdx.x; i < r; i += blockDim.x) xs[i] = A[i + static_cast<size_t>(r) * r];
-  __syncthreads();
+// Back substitution with U (column oriented, as Eigen): one warp per system.
+__global__ void __launch_bounds__(256) lu_backsolve_warp(int r, int m, const double* __restrict__ M,
+                                                         double* __restrict__ sol, long long ldsol,
+                                                         int* __restrict__ flags) {
+  extern __shared__ double xsall[];
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int sys = blockIdx.x * (blockDim.x >> 5) + w;
+  if (sys >= m) return;
+  double* xs = xsall + static_cast<size_t>(w) * r;
+  const double* A = M + static_cast<size_t>(sys) * r * (r + 1);
+  for (int i = lane; i < r; i += 32) xs[i] = A[i + static_cast<size_t>(r) * r];
+  __syncwarp();
   for (int i = r - 1; i >= 0; --i) {
-    if (threadIdx.x == 0) xs[i] = xs[i] / A[i + static_cast<size_t>(i) * r];
-    __syncthreads();
-    const double xi = xs[i];
-    for (int j = threadIdx.x; j < i; j += blockDim.x) xs[j] -= xi * A[j + static_cast<size_t>(i) * r];
-    __syncthreads();
+    const double xi = xs[i] / A[i + static_cast<size_t>(i) * r];
+    __syncwarp();
+    if (lane == 0) xs[i] = xi;
+    const double* ui = A + static_cast<size_t>(i) * r;
+    for (int j = lane; j < i; j += 32) xs[j] -= xi * ui[j];
+    __syncwarp();
   }
   int bad = 0;
-  for (int i = threadIdx.x; i < r; i += blockDim.x) {
-    sol[i + blockIdx.x * ldsol] = xs[i];
+  for (int i = lane; i < r; i += 32) {
+    sol[i + static_cast<long long>(sys) * ldsol] = xs[i];
     if (!isfinite(xs[i])) bad = 1;
   }
-  bad = __syncthreads_or(bad);
-  if (threadIdx.x == 0) flags[blockIdx.x] = bad;
+  bad = __any_sync(0xffffffffu, bad);
+  if (lane == 0) flags[sys] = bad;
 }
 
 }  // namespace
@@ -994,18 +1033,23 @@ void galerkin_batch(int r, int m, const int* angles, const double* dirs, const d
     int* piv = reinterpret_cast<int*>(work + static_cast<size_t>(m) * r * (r + 1));
     lu_assemble<<<dim3(std::max(1, std::min(64, (r * (r + 1) + 255) / 256)), m), 256, 0, s>>>(
         r, angles, dirs, proj, ldp, proj_stride, prhs, extra, ldsol, M);
-    for (int k0 = 0; k0 < r; k0 += kNb) {
-      const int jb = std::min(kNb, r - k0);
-      lu_panel<<<m, 256, 0, s>>>(r, k0, jb, M, piv);
+    constexpr int kPanelThreads = 256;
+    RTLR_CUDA(cudaFuncSetAttribute(lu_panel_smem<kPanelThreads>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   kPanelSmemBytes));
+    for (int k0 = 0; k0 < r;) {
+      const int jb = lu_panel_width(r, k0);
+      lu_panel_smem<kPanelThreads><<<m, kPanelThreads, static_cast<size_t>(r - k0) * jb * sizeof(double), s>>>(
+          r, k0, jb, M, piv);
       const int ntrail = r + 1 - (k0 + jb);
-      if (ntrail > 0) {
-        lu_swap_trsm<<<dim3((ntrail + 127) / 128, m), 128, 0, s>>>(r, k0, jb, M, piv);
-        const int rows = r - (k0 + jb);
-        if (rows > 0)
-          lu_update<<<dim3((rows + BM - 1) / BM, (ntrail + BN - 1) / BN, m), 256, 0, s>>>(r, k0, jb, M);
-      }
+      if (ntrail > 0) lu_trail<<<dim3((ntrail + BN - 1) / BN, m), 256, 0, s>>>(r, k0, jb, M, piv);
+      k0 += jb;
     }
-    lu_backsolve<<<m, 256, static_cast<size_t>(r) * sizeof(double), s>>>(r, M, sol, ldsol, flags);
+    const int per = 8;  // systems (warps) per CTA
+    const size_t smem = static_cast<size_t>(per) * r * sizeof(double);
+    if (smem > 48 * 1024)
+      RTLR_CUDA(cudaFuncSetAttribute(lu_backsolve_warp, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     static_cast<int>(smem)));
+    lu_backsolve_warp<<<(m + per - 1) / per, 32 * per, smem, s>>>(r, m, M, sol, ldsol, flags);
     RTLR_CUDA(cudaGetLastError());
     return;
   }
