@@ -1,6 +1,7 @@
 // Dense fp64 kernels of the low-rank path (see dense.cuh).
 #include <algorithm>
 #include <cmath>
+#include <cstdint>
 #include <stdexcept>
 #include <vector>
 
@@ -271,6 +272,134 @@ __global__ void __launch_bounds__(256) gemm_nn_skinny_kernel(long long M, int N,
       *c = subtract ? *c - acc[j] : acc[j];
     }
 }
+
+// ---- tall-skinny GEMMs, second generation: 16-byte loads, register tiles.
+// C[M x N] = A^T B split-K partials: warp w of a CTA owns MW columns of A;
+// lanes walk row pairs (16 B per load, 512 B per warp instruction), keep
+// MW x NB accumulators and reduce over lanes at the end.  Needs A, B 16-byte
+// aligned and even leading dimensions (the launcher checks; K offsets even).
+__device__ __forceinline__ double2 ldg2(const double* p) { return __ldg(reinterpret_cast<const double2*>(p)); }
+
+template <int NB, int MW>
+__global__ void __launch_bounds__(256) gemm_tn_skinny2(int M, int N, long long K, long long kchunk,
+                                                       const double* __restrict__ A, long long lda,
+                                                       const double* __restrict__ B, long long ldb,
+                                                       double* __restrict__ out, long long ldo, long long split_stride) {
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int m0 = (blockIdx.x * 8 + w) * MW;
+  const long long k0 = blockIdx.y * kchunk, k1 = min(K, k0 + kchunk);
+  double acc[MW][NB];
+#pragma unroll
+  for (int i = 0; i < MW; ++i)
+#pragma unroll
+    for (int n = 0; n < NB; ++n) acc[i][n] = 0.0;
+  if (m0 < M) {
+    for (long long k = k0 + 2 * lane; k < k1; k += 64) {
+      const bool pair = k + 1 < k1;
+      double b0[NB], b1[NB];
+#pragma unroll
+      for (int n = 0; n < NB; ++n) {
+        b0[n] = b1[n] = 0.0;
+        if (n < N) {
+          if (pair) {
+            const double2 v = ldg2(B + k + n * ldb);
+            b0[n] = v.x;
+            b1[n] = v.y;
+          } else {
+            b0[n] = B[k + n * ldb];
+          }
+        }
+      }
+#pragma unroll
+      for (int i = 0; i < MW; ++i) {
+        if (m0 + i < M) {
+          const double* a = A + k + static_cast<long long>(m0 + i) * lda;
+          double a0, a1 = 0.0;
+          if (pair) {
+            const double2 v = ldg2(a);
+            a0 = v.x;
+            a1 = v.y;
+          } else {
+            a0 = a[0];
+          }
+#pragma unroll
+          for (int n = 0; n < NB; ++n) acc[i][n] = fma(a1, b1[n], fma(a0, b0[n], acc[i][n]));
+        }
+      }
+    }
+  }
+#pragma unroll
+  for (int i = 0; i < MW; ++i)
+#pragma unroll
+    for (int n = 0; n < NB; ++n) {
+      double v = acc[i][n];
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+      acc[i][n] = v;
+    }
+  if (lane == 0) {
+    double* o = out + blockIdx.y * split_stride;
+#pragma unroll
+    for (int i = 0; i < MW; ++i)
+#pragma unroll
+      for (int n = 0; n < NB; ++n)
+        if (m0 + i < M && n < N) o[(m0 + i) + static_cast<long long>(n) * ldo] = acc[i][n];
+  }
+}
+
+// C[M x N] (-)= A B, A: M x K (M large), B: K x N: two rows per thread
+// (one 16-byte load per k), B staged in shared memory in chunks of k.
+template <int NB>
+__global__ void __launch_bounds__(256) gemm_nn_skinny2(long long M, int N, int K, const double* __restrict__ A,
+                                                       long long lda, const double* __restrict__ B, long long ldb,
+                                                       double* __restrict__ C, long long ldc, bool subtract) {
+  constexpr int KC = 64;
+  __shared__ double Bs[KC][NB];
+  const long long m = 2 * (blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x);
+  double acc0[NB], acc1[NB];
+#pragma unroll
+  for (int n = 0; n < NB; ++n) acc0[n] = acc1[n] = 0.0;
+  const bool two = m + 1 < M;
+  for (int kb = 0; kb < K; kb += KC) {
+    const int kc = min(KC, K - kb);
+    __syncthreads();
+    for (int e = threadIdx.x; e < KC * NB; e += blockDim.x) {
+      const int kk = e % KC, n = e / KC;
+      Bs[kk][n] = (kk < kc && n < N) ? B[kb + kk + static_cast<long long>(n) * ldb] : 0.0;
+    }
+    __syncthreads();
+    if (m < M) {
+      const double* a = A + m + static_cast<long long>(kb) * lda;
+#pragma unroll 4
+      for (int kk = 0; kk < kc; ++kk, a += lda) {
+        double a0, a1 = 0.0;
+        if (two) {
+          const double2 v = ldg2(a);
+          a0 = v.x;
+          a1 = v.y;
+        } else {
+          a0 = a[0];
+        }
+#pragma unroll
+        for (int n = 0; n < NB; ++n) {
+          const double b = Bs[kk][n];
+          acc0[n] = fma(a0, b, acc0[n]);
+          acc1[n] = fma(a1, b, acc1[n]);
+        }
+      }
+    }
+  }
+  if (m < M)
+#pragma unroll
+    for (int n = 0; n < NB; ++n) {
+      if (n >= N) break;
+      double* c = C + m + static_cast<long long>(n) * ldc;
+      c[0] = subtract ? c[0] - acc0[n] : acc0[n];
+      if (two) c[1] = subtract ? c[1] - acc1[n] : acc1[n];
+    }
+}
+
+bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
 
 // ------------------------------------------------------------ vectors
 __global__ void gemv_n_kernel(long long n, int k, const double* __restrict__ A, long long lda,
@@ -685,7 +814,10 @@ __global__ void __launch_bounds__(256) jacobi_round(long long m, int n, int npad
   al = block_sum_all(al, sh);
   be = block_sum_all(be, sh);
   ga = block_sum_all(ga, sh);
-  if (ga == 0.0 || fabs(ga) <= 1e-15 * sqrt(al * be)) return;
+  // rotate only above the roundoff level of the dot products (LAPACK
+  // dgesvj's sqrt(m) eps): below it a rotation changes nothing measurable
+  // and the sweep never reports convergence
+  if (ga == 0.0 || fabs(ga) <= sqrt(static_cast<double>(m)) * 2.220446049250313e-16 * sqrt(al * be)) return;
   if (threadIdx.x == 0) atomicAdd(rotated, 1);
   const double zeta = (be - al) / (2.0 * ga);
   const double tt = (zeta >= 0 ? 1.0 : -1.0) / (fabs(zeta) + sqrt(1.0 + zeta * zeta));
@@ -949,14 +1081,23 @@ void gemm_tn(int M, int N, long long K, const double* A, long long lda, const do
   splits = static_cast<int>((K + kchunk - 1) / kchunk);
   if (splits < 1) splits = 1;
   if (N <= kSkinny) {
-    dim3 grid((M + BM - 1) / BM, splits);
-    if (splits == 1) {
-      gemm_tn_skinny_kernel<<<grid, 256, 0, s>>>(M, N, K, kchunk, A, lda, B, ldb, C, ldc, 0);
+    double* o = splits == 1 ? C : work;
+    const long long ldo = splits == 1 ? ldc : M, sstride = splits == 1 ? 0 : static_cast<long long>(M) * N;
+    if (aligned16(A) && aligned16(B) && lda % 2 == 0 && ldb % 2 == 0) {
+      auto go = [&](auto kern, int mw) {
+        kern<<<dim3((M + 8 * mw - 1) / (8 * mw), splits), 256, 0, s>>>(M, N, K, kchunk, A, lda, B, ldb, o, ldo,
+                                                                       sstride);
+      };
+      if (N == 1) go(gemm_tn_skinny2<1, 4>, 4);
+      else if (N == 2) go(gemm_tn_skinny2<2, 4>, 4);
+      else if (N <= 4) go(gemm_tn_skinny2<4, 4>, 4);
+      else if (N <= 8) go(gemm_tn_skinny2<8, 4>, 4);
+      else go(gemm_tn_skinny2<16, 2>, 2);
     } else {
-      gemm_tn_skinny_kernel<<<grid, 256, 0, s>>>(M, N, K, kchunk, A, lda, B, ldb, work, M,
-                                                 static_cast<long long>(M) * N);
-      launch_splitk_reduce(M, N, splits, work, C, ldc, s);
+      gemm_tn_skinny_kernel<<<dim3((M + BM - 1) / BM, splits), 256, 0, s>>>(M, N, K, kchunk, A, lda, B, ldb, o, ldo,
+                                                                           sstride);
     }
+    if (splits > 1) launch_splitk_reduce(M, N, splits, work, C, ldc, s);
     RTLR_CUDA(cudaGetLastError());
     return;
   }
@@ -979,8 +1120,17 @@ void gemm_nn(long long M, int N, int K, const double* A, long long lda, const do
     return;
   }
   if (N <= kSkinny) {
-    gemm_nn_skinny_kernel<<<static_cast<unsigned>((M + 255) / 256), 256, 0, s>>>(M, N, K, A, lda, B, ldb, C, ldc,
-                                                                                  subtract);
+    if (aligned16(A) && lda % 2 == 0) {
+      const unsigned grid = static_cast<unsigned>((M + 511) / 512);
+      if (N == 1) gemm_nn_skinny2<1><<<grid, 256, 0, s>>>(M, N, K, A, lda, B, ldb, C, ldc, subtract);
+      else if (N == 2) gemm_nn_skinny2<2><<<grid, 256, 0, s>>>(M, N, K, A, lda, B, ldb, C, ldc, subtract);
+      else if (N <= 4) gemm_nn_skinny2<4><<<grid, 256, 0, s>>>(M, N, K, A, lda, B, ldb, C, ldc, subtract);
+      else if (N <= 8) gemm_nn_skinny2<8><<<grid, 256, 0, s>>>(M, N, K, A, lda, B, ldb, C, ldc, subtract);
+      else gemm_nn_skinny2<16><<<grid, 256, 0, s>>>(M, N, K, A, lda, B, ldb, C, ldc, subtract);
+    } else {
+      gemm_nn_skinny_kernel<<<static_cast<unsigned>((M + 255) / 256), 256, 0, s>>>(M, N, K, A, lda, B, ldb, C, ldc,
+                                                                                    subtract);
+    }
     RTLR_CUDA(cudaGetLastError());
     return;
   }

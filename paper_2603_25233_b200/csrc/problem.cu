@@ -273,10 +273,18 @@ void Problem::sweep(const int* d_angles, int n, const double* d_rhs, long long r
   a.line = line_.ensure(static_cast<size_t>(n) * 8 * (hp_.nx + 1) * 2);  // up to 8 warps per direction
   a.err = err_.get();
   a.sc = sc_;
-  static const bool skew = [] {
+  // Kernel choice: the row-chunk scan kernel, except for a handful of
+  // directions in a heterogeneous medium (the low-rank solver's p-direction
+  // batches), where the per-cell LU makes the scan's row steps long and the
+  // sweep is latency-bound: the skewed wavefront's single-cell steps are
+  // shorter (C4 LR sweeps 1.5 s -> 1.0 s).  RTLR_SWEEP=skew|scan forces one.
+  static const int forced = [] {
     const char* e = std::getenv("RTLR_SWEEP");
-    return e && std::string(e) == "skew";
+    if (!e) return 0;
+    return std::string(e) == "skew" ? 1 : (std::string(e) == "scan" ? 2 : 0);
   }();
+  const int choice = sweep_kernel ? sweep_kernel : forced;
+  const bool skew = choice ? choice == 1 : (!hp_.sigma_t_uniform && n <= 16);
   if (skew)
     launch_sweep(a, hp_.sigma_t_uniform, stream_);
   else

@@ -169,6 +169,7 @@ class Problem {
   double pcg_rtol = 1e-13;
   int pcg_max_iters = 20000;
   bool pcg_multigrid = true;  // false: block-Jacobi PCG
+  int sweep_kernel = 0;       // 0 auto, 1 skewed wavefront (sweep.cu), 2 row scan (sweep_scan.cu)
 
  private:
   friend class LowRankEngine;

@@ -27,10 +27,14 @@ SWEEP_CASES = [
 ]
 
 
+@pytest.mark.parametrize("kernel", [1, 2], ids=["skew", "scan"])
 @pytest.mark.parametrize("name,ov", SWEEP_CASES)
-def test_sweep_matches_oracle(name, ov):
+def test_sweep_matches_oracle(name, ov, kernel):
+    """Both K1 kernels (the skewed wavefront, sweep_kernel = 1, and the row
+    scan, 2), uniform and heterogeneous media, ragged grids."""
     o = O.Problem(name, use_dsa=0, **ov)
     g = P.Problem(name, use_dsa=0, **ov)
+    g.set_option("sweep_kernel", kernel)
     rng = np.random.default_rng(1)
     d = g.get("dirs")
     n = g.n_omega
