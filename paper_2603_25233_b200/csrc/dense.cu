@@ -34,57 +34,6 @@ __device__ __forceinline__ double block_sum_all(double v, double* sh) {
 }
 
 // ------------------------------------------------------------ GEMM A^T B
-// grid (tilesM, tilesN, splits); each CTA accumulates a 64x64 tile over its
-// K range into part[split] (M x N col-major) or directly into C.
-__global__ void __launch_bounds__(256) gemm_tn_kernel(int M, int N, long long K, long long kchunk,
-                                                      const double* __restrict__ A, long long lda,
-                                                      const double* __restrict__ B, long long ldb,
-                                                      double* __restrict__ out, long long ldo, long long split_stride) {
-  __shared__ double As[BK][BM + 1];
-  __shared__ double Bs[BK][BN + 1];
-  const int tid = threadIdx.x;
-  const int tm = tid % 16, tn = tid / 16;  // 16 x 16 threads, 4 x 4 outputs each
-  const int m0 = blockIdx.x * BM, n0 = blockIdx.y * BN;
-  const long long k0 = blockIdx.z * kchunk;
-  const long long k1 = min(K, k0 + kchunk);
-  double acc[4][4] = {};
-  for (long long kb = k0; kb < k1; kb += BK) {
-    // load A[kb:kb+16, m0:m0+64] -> As[k][m]; 1024 elements, 4 per thread
-#pragma unroll
-    for (int e = 0; e < 4; ++e) {
-      const int idx = tid + e * 256;
-      const int kk = idx % BK, mm = idx / BK;
-      const long long k = kb + kk;
-      const int m = m0 + mm;
-      As[kk][mm] = (k < k1 && m < M) ? A[k + m * lda] : 0.0;
-      const int n = n0 + mm;
-      Bs[kk][mm] = (k < k1 && n < N) ? B[k + n * ldb] : 0.0;
-    }
-    __syncthreads();
-#pragma unroll
-    for (int kk = 0; kk < BK; ++kk) {
-      double a[4], b[4];
-#pragma unroll
-      for (int i = 0; i < 4; ++i) a[i] = As[kk][tm + 16 * i];
-#pragma unroll
-      for (int j = 0; j < 4; ++j) b[j] = Bs[kk][tn + 16 * j];
-#pragma unroll
-      for (int i = 0; i < 4; ++i)
-#pragma unroll
-        for (int j = 0; j < 4; ++j) acc[i][j] += a[i] * b[j];
-    }
-    __syncthreads();
-  }
-  double* o = out + blockIdx.z * split_stride;
-#pragma unroll
-  for (int i = 0; i < 4; ++i)
-#pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      const int m = m0 + tm + 16 * i, n = n0 + tn + 16 * j;
-      if (m < M && n < N) o[m + n * ldo] = acc[i][j];
-    }
-}
-
 // C = sum over the split-K partials.  Few outputs with many splits (the
 // CGS GEMVs): one warp per output, lanes stride the splits, fixed shuffle
 // tree; many outputs: one thread per output, splits in order.  Both orders
@@ -134,59 +83,6 @@ int tn_splits(int M, int N, long long K) {
   s = std::min<long long>(s, std::max<long long>(1, K / 256));
   s = std::min<long long>(s, 1024);
   return static_cast<int>(std::max<long long>(1, s));
-}
-
-// ------------------------------------------------------------ GEMM A B
-__global__ void __launch_bounds__(256) gemm_nn_kernel(long long M, int N, int K, const double* __restrict__ A,
-                                                      long long lda, const double* __restrict__ B, long long ldb,
-                                                      double* __restrict__ C, long long ldc, bool subtract) {
-  __shared__ double As[BK][BM + 1];
-  __shared__ double Bs[BK][BN + 1];
-  const int tid = threadIdx.x;
-  const int tm = tid % 16, tn = tid / 16;
-  const long long m0 = blockIdx.x * static_cast<long long>(BM);
-  const int n0 = blockIdx.y * BN;
-  double acc[4][4] = {};
-  for (int kb = 0; kb < K; kb += BK) {
-#pragma unroll
-    for (int e = 0; e < 4; ++e) {
-      const int idx = tid + e * 256;
-      const int mm = idx % BM, kk = idx / BM;  // A is M-contiguous
-      const long long m = m0 + mm;
-      const int k = kb + kk;
-      As[kk][mm] = (k < K && m < M) ? A[m + k * lda] : 0.0;
-      const int kk2 = idx % BK, nn = idx / BK;  // B is K-contiguous
-      const int k2 = kb + kk2, n = n0 + nn;
-      Bs[kk2][nn] = (k2 < K && n < N) ? B[k2 + n * ldb] : 0.0;
-    }
-    __syncthreads();
-#pragma unroll
-    for (int kk = 0; kk < BK; ++kk) {
-      double a[4], b[4];
-#pragma unroll
-      for (int i = 0; i < 4; ++i) a[i] = As[kk][tm + 16 * i];
-#pragma unroll
-      for (int j = 0; j < 4; ++j) b[j] = Bs[kk][tn + 16 * j];
-#pragma unroll
-      for (int i = 0; i < 4; ++i)
-#pragma unroll
-        for (int j = 0; j < 4; ++j) acc[i][j] += a[i] * b[j];
-    }
-    __syncthreads();
-  }
-#pragma unroll
-  for (int i = 0; i < 4; ++i)
-#pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      const long long m = m0 + tm + 16 * i;
-      const int n = n0 + tn + 16 * j;
-      if (m < M && n < N) {
-        if (subtract)
-          C[m + n * ldc] -= acc[i][j];
-        else
-          C[m + n * ldc] = acc[i][j];
-      }
-    }
 }
 
 // ------------------------------------------------------------ skinny GEMMs
@@ -400,6 +296,94 @@ __global__ void __launch_bounds__(256) gemm_nn_skinny2(long long M, int N, int K
 }
 
 bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
+
+// ---- fp64 tensor-core (DMMA) tiles for the wide contractions: K6 X^T [W]
+// (projections), the QR trailing updates and K8 X C.  mma.sync m8n8k4 f64:
+// A fragment (8 x 4, row): lane holds A[lane/4][lane%4]; B (4 x 8, col):
+// B[lane%4][lane/4]; C (8 x 8): C[lane/4][2(lane%4) + {0,1}].  CTA tile
+// 64 x 64, k step 16 staged in shared memory as [k][m] / [k][n]; 8 warps in
+// a 2 x 4 grid, 32 x 16 per warp (4 x 2 mma tiles).
+__device__ __forceinline__ void dmma884(double& c0, double& c1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%0, %1};"
+               : "+d"(c0), "+d"(c1)
+               : "d"(a), "d"(b));
+}
+
+constexpr int kMmaPad = 8;  // row stride 72 doubles: the 4 k-rows x 8 lanes of a fragment hit distinct banks
+
+// TRANS_A: op(A)[m][k] = A[k + m lda] (A^T B, split-K partials into out);
+// else op(A)[m][k] = A[m + k lda] (A B; out = C, or C -= when subtract).
+template <bool TRANS_A>
+__global__ void __launch_bounds__(256) gemm_dmma_kernel(long long M, int N, long long K, long long kchunk,
+                                                        const double* __restrict__ A, long long lda,
+                                                        const double* __restrict__ B, long long ldb,
+                                                        double* __restrict__ out, long long ldo, long long split_stride,
+                                                        bool subtract) {
+  __shared__ double As[BK][BM + kMmaPad];
+  __shared__ double Bs[BK][BN + kMmaPad];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int wm = (warp & 1) * 32, wn = (warp >> 1) * 16;  // warp tile origin in the CTA tile
+  const long long m0 = static_cast<long long>(blockIdx.x) * BM;
+  const int n0 = blockIdx.y * BN;
+  const long long k0 = TRANS_A ? blockIdx.z * kchunk : 0;
+  const long long k1 = TRANS_A ? min(K, k0 + kchunk) : K;
+  double acc[4][2][2];
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 2; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+  const int fr = lane >> 2, fc = lane & 3;
+  for (long long kb = k0; kb < k1; kb += BK) {
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      const int idx = tid + e * 256;
+      if (TRANS_A) {  // A[k + m lda], k fastest
+        const int kk = idx % BK, mm = idx / BK;
+        const long long k = kb + kk, m = m0 + mm;
+        As[kk][mm] = (k < k1 && m < M) ? A[k + m * lda] : 0.0;
+      } else {  // A[m + k lda], m fastest
+        const int mm = idx % BM, kk = idx / BM;
+        const long long k = kb + kk, m = m0 + mm;
+        As[kk][mm] = (k < k1 && m < M) ? A[m + k * lda] : 0.0;
+      }
+      const int kk = idx % BK, nn = idx / BK;
+      const long long k = kb + kk;
+      const int n = n0 + nn;
+      Bs[kk][nn] = (k < k1 && n < N) ? B[k + static_cast<long long>(n) * ldb] : 0.0;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int ks = 0; ks < BK; ks += 4) {
+      double a[4], b[2];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) a[i] = As[ks + fc][wm + 8 * i + fr];
+#pragma unroll
+      for (int j = 0; j < 2; ++j) b[j] = Bs[ks + fc][wn + 8 * j + fr];
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 2; ++j) dmma884(acc[i][j][0], acc[i][j][1], a[i], b[j]);
+    }
+    __syncthreads();
+  }
+  double* o = out + (TRANS_A ? blockIdx.z * split_stride : 0);
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 2; ++j)
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const long long m = m0 + wm + 8 * i + fr;
+        const int n = n0 + wn + 8 * j + 2 * fc + h;
+        if (m < M && n < N) {
+          double* c = o + m + static_cast<long long>(n) * ldo;
+          if (TRANS_A || !subtract)
+            *c = acc[i][j][h];
+          else
+            *c -= acc[i][j][h];
+        }
+      }
+}
 
 // ------------------------------------------------------------ vectors
 __global__ void gemv_n_kernel(long long n, int k, const double* __restrict__ A, long long lda,
@@ -1102,12 +1086,10 @@ void gemm_tn(int M, int N, long long K, const double* A, long long lda, const do
     return;
   }
   dim3 grid((M + BM - 1) / BM, (N + BN - 1) / BN, splits);
-  if (splits == 1) {
-    gemm_tn_kernel<<<grid, 256, 0, s>>>(M, N, K, kchunk, A, lda, B, ldb, C, ldc, 0);
-  } else {
-    gemm_tn_kernel<<<grid, 256, 0, s>>>(M, N, K, kchunk, A, lda, B, ldb, work, M, static_cast<long long>(M) * N);
-    launch_splitk_reduce(M, N, splits, work, C, ldc, s);
-  }
+  double* o = splits == 1 ? C : work;
+  const long long ldo = splits == 1 ? ldc : M, sstride = splits == 1 ? 0 : static_cast<long long>(M) * N;
+  gemm_dmma_kernel<true><<<grid, 256, 0, s>>>(M, N, K, kchunk, A, lda, B, ldb, o, ldo, sstride, false);
+  if (splits > 1) launch_splitk_reduce(M, N, splits, work, C, ldc, s);
   RTLR_CUDA(cudaGetLastError());
 }
 
@@ -1135,7 +1117,7 @@ void gemm_nn(long long M, int N, int K, const double* A, long long lda, const do
     return;
   }
   dim3 grid(static_cast<unsigned>((M + BM - 1) / BM), (N + BN - 1) / BN);
-  gemm_nn_kernel<<<grid, 256, 0, s>>>(M, N, K, A, lda, B, ldb, C, ldc, subtract);
+  gemm_dmma_kernel<false><<<grid, 256, 0, s>>>(M, N, K, 0, A, lda, B, ldb, C, ldc, 0, subtract);
   RTLR_CUDA(cudaGetLastError());
 }
 
