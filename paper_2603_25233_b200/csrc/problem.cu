@@ -270,7 +270,8 @@ void Problem::sweep(const int* d_angles, int n, const double* d_rhs, long long r
   a.psi = d_psi;
   a.psi_stride = psi_stride;
   a.sigma_t = sigma_t_.get();
-  a.line = line_.ensure(static_cast<size_t>(n) * 8 * (hp_.nx + 1) * 2);  // up to 8 warps per direction
+  // trace lines (up to 8 warps per direction) or the column-split boundary carries
+  a.line = line_.ensure(static_cast<size_t>(n) * 8 * (std::max(hp_.nx, hp_.ny) + 1) * 2);
   a.err = err_.get();
   a.sc = sc_;
   // Kernel choice: the row-chunk scan kernel, except for a handful of

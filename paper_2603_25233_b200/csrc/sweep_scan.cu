@@ -228,6 +228,13 @@ __device__ __forceinline__ void mat2_vec(const double* G, double x0, double x1, 
   y1 = G[1] * x0 + G[3] * x1;
 }
 
+// Warps per direction: kOne (one warp), kRows (warp w owns rows w, w+W, ...;
+// reads warp w-1's trace line behind its progress counter) or kSplit (warp
+// s owns column segment s of every row; its trace line covers only its
+// segment, and the x-carry at the segment boundary comes from warp s-1
+// through a per-row slot in global memory behind warp s-1's row counter).
+enum SweepMode { kOne = 0, kRows = 1, kSplit = 2 };
+
 // One warp's share of one direction.
 struct Dir {
   const double* rhs;
@@ -238,31 +245,39 @@ struct Dir {
   int* prod;          // shared memory, W progress counters
   double* my_line;
   const double* in_line;
+  double* carry;      // kSplit: (W-1) x ny x 2 boundary carries
   int* err;
   int nx, ny, W, w, pw, nchunk, nrows, pitch;
+  int rw, rW;         // row interleave: rows rw, rw + rW, ... (kRows: w, W; else 0, 1)
+  int kbeg, kend;     // this warp's chunk range within a row
   bool yu, smem_lines;
 };
 
-template <bool UNIFORM, bool MULTI, bool HAS_BC, bool XU>
+template <bool UNIFORM, int MODE, bool HAS_BC, bool XU>
 __device__ __forceinline__ void sweep_dir(const Dir& d) {
+  constexpr bool MULTI = MODE == kRows, SPLIT = MODE == kSplit;
   constexpr int kDx = XU ? 1 : -1;  // cell index step along the sweep
   const int lane = threadIdx.x & 31;
-  const int nx = d.nx, nchunk = d.nchunk, nrows = d.nrows;
+  const int nx = d.nx, nrows = d.nrows, kbeg = d.kbeg, kend = d.kend;
+  const int nchunk = kend - kbeg;  // chunks per row of this warp
+  const int colbase = kbeg * kChunk;  // first sweep column of this warp's segment
   const int c0 = kCpl * lane;  // this lane's first sweep column within a chunk
   const double kx0 = d.cst[kKT], kx1 = d.cst[kKT + 1], tx0 = d.cst[kKT + 2], tx1 = d.cst[kKT + 3];
   const double ky0 = d.cst[kKT + 4], ky1 = d.cst[kKT + 5], ty0 = d.cst[kKT + 6], ty1 = d.cst[kKT + 7];
   const double2* c2 = reinterpret_cast<const double2*>(d.cst);
 
   auto row0_of = [&](int rowk) -> long long {
-    const int r = d.w + rowk * d.W;
+    const int r = d.rw + rowk * d.rW;
     return static_cast<long long>(d.yu ? r : d.ny - 1 - r) * nx;
   };
-  // this lane's first cell in row ordinal rowk
-  auto first_cell = [&](int rowk) -> long long { return row0_of(rowk) + (XU ? c0 : nx - 1 - c0); };
+  // this lane's first cell of the warp's segment in row ordinal rowk
+  auto first_cell = [&](int rowk) -> long long {
+    return row0_of(rowk) + (XU ? colbase + c0 : nx - 1 - colbase - c0);
+  };
 
   // L2 prefetch, one chunk per step kAheadChunks ahead, issued by lane 0;
   // (prow, pk) walks the chunks in sweep order.
-  int prow = 0, pk = 0;
+  int prow = 0, pk = kbeg;
   long long prow0 = row0_of(0);
   auto prefetch_next = [&]() {
     if (prow >= nrows) return;
@@ -270,8 +285,8 @@ __device__ __forceinline__ void sweep_dir(const Dir& d) {
     const long long first = prow0 + (XU ? lo : nx - lo - cnt);
     prefetch_l2(d.rhs + 4 * first, static_cast<unsigned>(cnt) * 32u);
     if (HAS_BC) prefetch_l2(d.bc + 4 * first, static_cast<unsigned>(cnt) * 32u);
-    if (++pk == nchunk) {
-      pk = 0;
+    if (++pk == kend) {
+      pk = kbeg;
       if (++prow < nrows) prow0 = row0_of(prow);
     }
   };
@@ -281,26 +296,37 @@ __device__ __forceinline__ void sweep_dir(const Dir& d) {
   const int nsteps = nrows * nchunk;
   long long cell = first_cell(0);  // this lane's first cell of the current step
   long long next_row = nrows > 1 ? first_cell(1) : 0;
-  int rowk = 0, k = 0;
+  int rowk = 0, k = kbeg;
   double tc0 = 0.0, tc1 = 0.0;  // x-trace carry into the chunk (lane 0)
 
   double ra0[4], ra1[4], rb0[4], rb1[4];  // two register sets of sources
-  if (c0 < nx) ld_cell256(d.rhs + 4 * cell, ra0);
-  if (c0 + 1 < nx) ld_cell256(d.rhs + 4 * (cell + kDx), ra1);
+  if (colbase + c0 < nx) ld_cell256(d.rhs + 4 * cell, ra0);
+  if (colbase + c0 + 1 < nx) ld_cell256(d.rhs + 4 * (cell + kDx), ra1);
 
   auto step = [&](int t, double (&v0)[4], double (&v1)[4], double (&n0)[4], double (&n1)[4]) {
     const int col = k * kChunk + c0;
     const bool act0 = col < nx, act1 = col + 1 < nx;
     // next step's sources into the other register set
-    const bool last = k + 1 == nchunk;
+    const bool last = k + 1 == kend;
     const long long ncell = last ? next_row : cell + kDx * kChunk;
-    const int ncol = last ? c0 : col + kChunk;
+    const int ncol = last ? colbase + c0 : col + kChunk;
     if (t + 1 < nsteps) {
       if (ncol < nx) ld_cell256(d.rhs + 4 * ncell, n0);
       if (ncol + 1 < nx) ld_cell256(d.rhs + 4 * (ncell + kDx), n1);
     }
     if (lane == 0) prefetch_next();
-    if (k == 0) tc0 = tc1 = 0.0;  // vacuum x-inflow at the row start
+    if (k == kbeg) {  // x-inflow of the row (segment): vacuum, or warp s-1's boundary carry
+      tc0 = tc1 = 0.0;
+      if (SPLIT && d.w > 0) {
+        if (lane == 0) {
+          wait_progress(d.prod + d.w - 1, rowk + 1);
+          const double2 cin = __ldcg(reinterpret_cast<const double2*>(d.carry) + (d.w - 1) * d.ny + rowk);
+          tc0 = cin.x;
+          tc1 = cin.y;
+        }
+        __syncwarp();  // reconverge after lane 0's spin, or every shuffle takes the divergent path
+      }
+    }
     if (HAS_BC) {
       double g0[4], g1[4];
       if (act0) ld_cell256(d.bc + 4 * cell, g0);
@@ -313,14 +339,14 @@ __device__ __forceinline__ void sweep_dir(const Dir& d) {
     }
     // y-upwind traces (per x-mode) of these columns from the previous row
     double y00 = 0.0, y01 = 0.0, y10 = 0.0, y11 = 0.0;  // y{cell}{x-mode}
-    if (d.w + rowk * d.W > 0) {
+    if (d.rw + rowk * d.rW > 0) {
       if (MULTI) {
         if (lane == 0) wait_progress(d.prod + d.pw, (d.w == 0 ? rowk - 1 : rowk) * nchunk + k + 1);
         __syncwarp();
       }
       if (act0) {
-        const double2 p0 = ld_line(d.in_line + col, d.smem_lines);
-        const double2 p1 = ld_line(d.in_line + d.pitch + col, d.smem_lines);
+        const double2 p0 = ld_line(d.in_line + (col - colbase), d.smem_lines);
+        const double2 p1 = ld_line(d.in_line + d.pitch + (col - colbase), d.smem_lines);
         y00 = p0.x;
         y01 = p1.x;
         y10 = act1 ? p0.y : 0.0;  // the padding column of an odd row is never written
@@ -483,16 +509,25 @@ __device__ __forceinline__ void sweep_dir(const Dir& d) {
       st_cell256(p, ps0);
       if (act1) st_cell256(p + 4 * kDx, ps1);
       // y-outflow traces (per x-mode) for the next row
-      st_line(d.my_line + col, ty0 * ps0[0] + ty1 * ps0[2], ty0 * ps1[0] + ty1 * ps1[2], d.smem_lines);
-      st_line(d.my_line + d.pitch + col, ty0 * ps0[1] + ty1 * ps0[3], ty0 * ps1[1] + ty1 * ps1[3],
+      st_line(d.my_line + (col - colbase), ty0 * ps0[0] + ty1 * ps0[2], ty0 * ps1[0] + ty1 * ps1[2],
+              d.smem_lines);
+      st_line(d.my_line + d.pitch + (col - colbase), ty0 * ps0[1] + ty1 * ps0[3], ty0 * ps1[1] + ty1 * ps1[3],
               d.smem_lines);
     }
     __syncwarp();  // (own line: the next row reads what this row wrote)
     if (MULTI && lane == 0) publish_progress(d.prod + d.w, t + 1);
+    if (SPLIT && last && d.w + 1 < d.W) {
+      // the carry out of this segment's last (full) chunk: lane 0 holds it after the rotation
+      if (lane == 0) {
+        __stcg(reinterpret_cast<double2*>(d.carry) + d.w * d.ny + rowk, make_double2(tc0, tc1));
+        publish_progress(d.prod + d.w, rowk + 1);
+      }
+      __syncwarp();
+    }
     // advance
     cell = ncell;
     if (last) {
-      k = 0;
+      k = kbeg;
       ++rowk;
       next_row = rowk + 1 < nrows ? first_cell(rowk + 1) : 0;
     } else {
@@ -506,8 +541,9 @@ __device__ __forceinline__ void sweep_dir(const Dir& d) {
   }
 }
 
-template <bool UNIFORM, bool MULTI, bool HAS_BC>
-__global__ void __launch_bounds__(256, 2) sweep_scan_kernel(const SweepArgs a, int W, bool smem_lines) {
+// nck: chunks per segment (kSplit); the trace lines then span one segment.
+template <bool UNIFORM, int MODE, bool HAS_BC>
+__global__ void __launch_bounds__(256, 2) sweep_scan_kernel(const SweepArgs a, int W, bool smem_lines, int nck) {
   extern __shared__ double smem[];
   const int lane = threadIdx.x & 31;
   const int wib = threadIdx.x >> 5;
@@ -516,8 +552,9 @@ __global__ void __launch_bounds__(256, 2) sweep_scan_kernel(const SweepArgs a, i
   const int slot = blockIdx.x * groups + g;
   if (slot >= a.n) return;  // a whole direction group exits together
   const int nx = a.nx, ny = a.ny;
-  const int pitch = line_pitch(nx);
-  double* base = smem + static_cast<size_t>(g) * group_doubles(W, nx, smem_lines);
+  const int linew = MODE == kSplit ? nck * kChunk : nx;  // columns per trace line
+  const int pitch = line_pitch(linew);
+  double* base = smem + static_cast<size_t>(g) * group_doubles(W, linew, smem_lines);
   double* cst = base;
   int* prod = reinterpret_cast<int*>(base + kConsts);
   double* lines = smem_lines ? base + kConsts + 2 * ((W + 3) / 4) : a.line + static_cast<size_t>(slot) * W * 2 * pitch;
@@ -593,21 +630,37 @@ __global__ void __launch_bounds__(256, 2) sweep_scan_kernel(const SweepArgs a, i
   d.prod = prod;
   d.pw = (w + W - 1) % W;
   d.my_line = lines + static_cast<size_t>(w) * 2 * pitch;
-  d.in_line = lines + static_cast<size_t>(d.pw) * 2 * pitch;
+  // kRows reads warp w-1's line (the previous row); otherwise a warp's own
+  // line holds its columns of the previous row
+  d.in_line = lines + static_cast<size_t>(MODE == kRows ? d.pw : w) * 2 * pitch;
   d.err = a.err;
   d.nx = nx;
   d.ny = ny;
   d.W = W;
   d.w = w;
   d.nchunk = (nx + kChunk - 1) / kChunk;
-  d.nrows = (ny - w + W - 1) / W;  // rows w, w+W, ... of this warp
+  if (MODE == kSplit) {  // segment w of every row; boundary carries in the (unused) global line buffer
+    d.rw = 0;
+    d.rW = 1;
+    d.nrows = ny;
+    d.kbeg = w * nck;
+    d.kend = min(d.nchunk, (w + 1) * nck);
+    d.carry = a.line + static_cast<size_t>(slot) * (W - 1) * ny * 2;
+  } else {
+    d.rw = w;
+    d.rW = W;
+    d.nrows = (ny - w + W - 1) / W;  // rows w, w+W, ... of this warp
+    d.kbeg = 0;
+    d.kend = d.nchunk;
+    d.carry = nullptr;
+  }
   d.pitch = pitch;
   d.yu = yu;
   d.smem_lines = smem_lines;
   if (xu)
-    sweep_dir<UNIFORM, MULTI, HAS_BC, true>(d);
+    sweep_dir<UNIFORM, MODE, HAS_BC, true>(d);
   else
-    sweep_dir<UNIFORM, MULTI, HAS_BC, false>(d);
+    sweep_dir<UNIFORM, MODE, HAS_BC, false>(d);
 }
 
 int sm_count() {
@@ -623,43 +676,70 @@ int sm_count() {
 
 void launch_sweep_scan(const SweepArgs& a, bool uniform, cudaStream_t s) {
   if (a.n <= 0) return;
-  const bool smem_lines =
-      static_cast<size_t>(kWarps) * 2 * line_pitch(a.nx) * sizeof(double) <= kLineSmemBudget;
-  // Warps per direction: the W in {1, 2, 4, 8} (at most one per 2 rows) whose
-  // last wave of warps is fullest — the resident warp slots are
-  // SMs x blocks/SM x kWarps; ties keep the smaller W.
-  int W = 1;
-  double best = -1.0;
-  for (int c = 1; c <= kWarps && (c == 1 || 2 * c <= a.ny); c *= 2) {
-    const size_t smem = static_cast<size_t>(kWarps / c) * group_doubles(c, a.nx, smem_lines) * sizeof(double);
+  const int nchunk = (a.nx + kChunk - 1) / kChunk;
+  auto lines_fit = [](int linew) {
+    return static_cast<size_t>(kWarps) * 2 * line_pitch(linew) * sizeof(double) <= kLineSmemBudget;
+  };
+  // Last-wave fill of n*c warps over the resident warp slots (SMs x blocks/SM x kWarps).
+  auto wave_eff = [&](int c, int linew, bool smem_lines) {
+    const size_t smem = static_cast<size_t>(kWarps / c) * group_doubles(c, linew, smem_lines) * sizeof(double);
     const int per_sm = std::max(1, std::min(2, static_cast<int>((227u * 1024u) / (smem + 1024u))));
     const double slots = static_cast<double>(sm_count()) * per_sm * kWarps;
     const double waves = static_cast<double>(a.n) * c / slots;
-    const double eff = waves <= 1.0 ? waves : waves / std::ceil(waves);
-    if (eff > best + 1e-3) {
-      best = eff;
-      W = c;
+    return waves <= 1.0 ? waves : waves / std::ceil(waves);
+  };
+  // Warps per direction W in {1, 2, 4, 8}, best last-wave fill, ties keep the
+  // smaller W.  Rows whose full-width trace lines fit shared memory (nx <=
+  // 768): row interleave (at most one warp per 2 rows).  Wider rows: column
+  // segments (every segment non-empty, lines of one segment in shared
+  // memory); only if no split fits do the lines go to L2.
+  int mode = kOne, W = 1, nck = nchunk, linew = a.nx;
+  bool smem_lines = lines_fit(a.nx);
+  double best = -1.0;
+  if (smem_lines) {
+    for (int c = 1; c <= kWarps && (c == 1 || 2 * c <= a.ny); c *= 2) {
+      const double eff = wave_eff(c, a.nx, true);
+      if (eff > best + 1e-3) best = eff, W = c;
+    }
+    mode = W > 1 ? kRows : kOne;
+  } else {
+    for (int c = 2; c <= kWarps; c *= 2) {
+      const int k = (nchunk + c - 1) / c;
+      if ((c - 1) * k >= nchunk || !lines_fit(k * kChunk)) continue;
+      const double eff = wave_eff(c, k * kChunk, true);
+      if (eff > best + 1e-3) best = eff, W = c, nck = k;
+    }
+    if (W > 1) {
+      mode = kSplit;
+      smem_lines = true;
+      linew = nck * kChunk;
+    } else {  // rows in L2
+      for (int c = 1; c <= kWarps && (c == 1 || 2 * c <= a.ny); c *= 2) {
+        const double eff = wave_eff(c, a.nx, false);
+        if (eff > best + 1e-3) best = eff, W = c;
+      }
+      mode = W > 1 ? kRows : kOne;
     }
   }
   const int groups = kWarps / W;
   const int blocks = (a.n + groups - 1) / groups;
-  const size_t smem = static_cast<size_t>(groups) * group_doubles(W, a.nx, smem_lines) * sizeof(double);
+  const size_t smem = static_cast<size_t>(groups) * group_doubles(W, linew, smem_lines) * sizeof(double);
   auto go = [&](auto kern) {
     RTLR_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
-    kern<<<blocks, kWarps * 32, smem, s>>>(a, W, smem_lines);
+    kern<<<blocks, kWarps * 32, smem, s>>>(a, W, smem_lines, nck);
   };
   const bool bc = a.bc != nullptr;
+#define RTLR_SCAN_GO(U, M) (bc ? go(sweep_scan_kernel<U, M, true>) : go(sweep_scan_kernel<U, M, false>))
   if (uniform) {
-    if (W > 1)
-      bc ? go(sweep_scan_kernel<true, true, true>) : go(sweep_scan_kernel<true, true, false>);
-    else
-      bc ? go(sweep_scan_kernel<true, false, true>) : go(sweep_scan_kernel<true, false, false>);
+    if (mode == kSplit) RTLR_SCAN_GO(true, kSplit);
+    else if (mode == kRows) RTLR_SCAN_GO(true, kRows);
+    else RTLR_SCAN_GO(true, kOne);
   } else {
-    if (W > 1)
-      bc ? go(sweep_scan_kernel<false, true, true>) : go(sweep_scan_kernel<false, true, false>);
-    else
-      bc ? go(sweep_scan_kernel<false, false, true>) : go(sweep_scan_kernel<false, false, false>);
+    if (mode == kSplit) RTLR_SCAN_GO(false, kSplit);
+    else if (mode == kRows) RTLR_SCAN_GO(false, kRows);
+    else RTLR_SCAN_GO(false, kOne);
   }
+#undef RTLR_SCAN_GO
   RTLR_CUDA(cudaGetLastError());
 }
 

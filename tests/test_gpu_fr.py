@@ -24,6 +24,9 @@ SWEEP_CASES = [
     ("homogeneous(1,1)", {"nx": 33, "ny": 65}),   # ragged bands
     ("C3", {"nx": 70, "ny": 40, "n_theta": 8, "n_omega_z": 4}),
     ("C4", {"nx": 64, "ny": 96, "n_theta": 8, "n_omega_z": 4}),
+    # rows wider than 768 cells: the scan kernel splits rows into column segments
+    ("homogeneous(1,1)", {"nx": 1000, "ny": 24, "n_theta": 8, "n_omega_z": 2}),
+    ("C4", {"nx": 1030, "ny": 12, "n_theta": 4, "n_omega_z": 4}),
 ]
 
 
