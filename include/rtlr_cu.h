@@ -160,6 +160,13 @@ int rtlr_cu_partition_angles(int n_theta, int n_omega_z, int nranks, int rank, i
  * *bsz = ceil(m / nranks) items, gathered back in order with one in-place
  * all-gather.  Pure host logic (no GPU needed). */
 int rtlr_cu_shard_block(int m, int nranks, int rank, int* begin, int* end, int* bsz);
+/* psi_difference (report.cpp:47-58): ||psi_full - X diag(S) V^T||_F with
+ * psi_full N_x x N_Omega, X N_x x rank, S rank, V N_Omega x rank (all
+ * column-major, e.g. a full-rank report's "psi" and a low-rank report's
+ * "X", "S", "V"); the reconstruction is formed 128 angles at a time. */
+int rtlr_cu_psi_difference(rtlr_cu_problem* p, const double* psi_full, const double* X, const double* S,
+                           const double* V, int rank, double* out, int where);
+
 /* ---- dense kernels of the truncation path, host buffers in and out (for
  * tests and tools): the blocked Householder QR of the low-rank basis rebuild
  * (low_rank.cpp:112-130): a (m x n, m >= n, column-major) = q r, q m x n with

@@ -38,7 +38,7 @@ EXPORTS = [
     "rtlr_cu_report_get", "rtlr_cu_report_sampled", "rtlr_cu_report_destroy",
     "rtlr_cu_partition_angles", "rtlr_cu_problem_fr_options", "rtlr_cu_problem_lr_options",
     "rtlr_cu_sweep_async", "rtlr_cu_check", "rtlr_cu_nccl_unique_id", "rtlr_cu_problem_set_comm",
-    "rtlr_cu_shard_block", "rtlr_cu_dense_qr",
+    "rtlr_cu_shard_block", "rtlr_cu_dense_qr", "rtlr_cu_psi_difference",
 ]
 
 
@@ -108,6 +108,7 @@ def load_library(path: str = LIB_PATH):
     L.rtlr_cu_si_step.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p,
                                   ctypes.c_int]
     L.rtlr_cu_dsa_solve.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int, _I]
+    L.rtlr_cu_psi_difference.argtypes = [ctypes.c_void_p] + [ctypes.c_void_p] * 4 + [ctypes.c_int, _D, ctypes.c_int]
     L.rtlr_cu_dsa_correct.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p,
                                       ctypes.c_int]
     L.rtlr_cu_c5_fill.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int64, ctypes.c_int64,
@@ -181,6 +182,26 @@ def dense_qr(a: np.ndarray, device: int = 0):
     r = np.zeros((n, n), dtype=np.float64, order="F")
     _check(load_library().rtlr_cu_dense_qr(device, m, n, _dp(a), _dp(q), _dp(r)))
     return q, r
+
+
+def compare_runs(full, low, problem=None) -> dict:
+    """compare_runs (report.cpp:60-74): speedup, compression ratio, ||phi_LR -
+    phi_FR||_2 and, when the full-rank report holds psi and the low-rank one
+    its factors, ||psi_FR - X S V^T||_F (computed on the problem's GPU)."""
+    if full.phi.size != low.phi.size:
+        raise RtlrError("compare_runs: reports come from different discretizations")
+    fs, ls = float(full.get("solve_seconds", 1)[0]), float(low.get("solve_seconds", 1)[0])
+    n_x = full.phi.size
+    n_omega = problem.n_omega if problem is not None else None
+    out = {"speedup": fs / ls if ls > 0 else 0.0,
+           "compression_ratio": low.psi_dofs / (n_x * n_omega) if n_omega else None,
+           "phi_diff_two_norm": float(np.linalg.norm(low.phi - full.phi)), "has_psi_diff": False}
+    if problem is not None and full.has_psi and low.factor_rank > 0:
+        r = low.factor_rank
+        out["psi_diff_two_norm"] = problem.psi_difference(
+            full.get("psi", n_x * n_omega), low.get("X", n_x * r), low.get("S", r), low.get("V", n_omega * r))
+        out["has_psi_diff"] = True
+    return out
 
 
 class Report:
@@ -364,6 +385,18 @@ class Problem:
         out = np.zeros(self.n)
         _check(load_library().rtlr_cu_dsa_correct(self.h, _dp(a), _dp(b), _dp(out), HOST))
         return out
+
+    def psi_difference(self, psi_full: np.ndarray, X: np.ndarray, S: np.ndarray, V: np.ndarray) -> float:
+        """psi_difference (report.cpp:47-58): ||psi_full - X diag(S) V^T||_F on the GPU."""
+        r = int(np.asarray(S).size)
+        ps = np.asfortranarray(np.reshape(psi_full, (self.n, self.n_omega), order="F"), dtype=np.float64)
+        x = np.asfortranarray(np.reshape(X, (self.n, r), order="F"), dtype=np.float64)
+        v = np.asfortranarray(np.reshape(V, (self.n_omega, r), order="F"), dtype=np.float64)
+        sv = np.ascontiguousarray(S, dtype=np.float64)
+        out = ctypes.c_double(0.0)
+        _check(load_library().rtlr_cu_psi_difference(self.h, _dp(ps), _dp(x), _dp(sv), _dp(v), r,
+                                                      ctypes.byref(out), HOST))
+        return out.value
 
     # ---- drivers ----
     def solve_full_rank(self, **opts) -> Report:

@@ -551,6 +551,18 @@ int rtlr_cu_partition_angles(int n_theta, int n_omega_z, int nranks, int rank, i
   });
 }
 
+int rtlr_cu_psi_difference(rtlr_cu_problem* p, const double* psi_full, const double* X, const double* S,
+                           const double* V, int rank, double* out, int where) {
+  return guard([&] {
+    need(p && psi_full && out && rank >= 0 && (rank == 0 || (X && S && V)), "psi_difference: bad argument");
+    Problem& P = gpu(p);
+    const size_t n = P.host().ndof, nom = P.host().n_omega;
+    In ps(psi_full, n * nom, where, P.stream()), x(X, n * rank, where, P.stream()), sv(S, rank, where, P.stream()),
+        v(V, nom * rank, where, P.stream());
+    *out = P.psi_difference(ps.d, x.d, sv.d, v.d, rank);
+  });
+}
+
 int rtlr_cu_dense_qr(int device, int64_t m, int n, const double* a, double* q, double* r) {
   return guard([&] {
     need(m >= n && n >= 1 && a && q && r, "dense_qr: need m >= n >= 1 and host buffers");

@@ -112,6 +112,29 @@ __global__ void add_vec(int n, double* __restrict__ a, const double* __restrict_
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) a[i] += b[i];
 }
 
+__global__ void sqdiff_partials(long long rows, int cols, const double* __restrict__ a, long long lda,
+                                const double* __restrict__ b, long long ldb, double* __restrict__ part) {
+  // part[blockIdx.x] = sum over this block's fixed share of (a - b)^2
+  __shared__ double sh[32];
+  const long long total = rows * cols;
+  double s = 0.0;
+  for (long long e = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; e < total;
+       e += static_cast<long long>(gridDim.x) * blockDim.x) {
+    const long long i = e % rows, j = e / rows;
+    const double d = a[i + j * lda] - b[i + j * ldb];
+    s += d * d;
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+  if ((threadIdx.x & 31) == 0) sh[threadIdx.x >> 5] = s;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double t = 0.0;
+    for (int k = 0; k < (blockDim.x >> 5); ++k) t += sh[k];
+    part[blockIdx.x] = t;
+  }
+}
+
 int g1(long long n) {
   long long g = (n + 255) / 256;
   return static_cast<int>(std::max<long long>(1, std::min<long long>(g, 148 * 16)));
@@ -761,6 +784,40 @@ std::vector<double> LowRankEngine::svd(bool vectors, int keep, std::vector<doubl
     *Vout = std::move(V);
   }
   return s;
+}
+
+// report.cpp:47-58: the reconstruction X diag(S) V^T is formed 128 angles at
+// a time (as the reference's block loop), never whole.
+double Problem::psi_difference(const double* d_psi, const double* d_X, const double* d_S, const double* d_V,
+                               int r) {
+  const long long n = hp_.ndof;
+  const int nom = hp_.n_omega, block = 128, parts = 296;
+  if (r < 0) throw std::invalid_argument("psi_difference: negative rank");
+  // SV^T = diag(S) V^T (r x N_Omega), on the host from the device factors
+  std::vector<double> S(r), V(static_cast<size_t>(nom) * r), svt(static_cast<size_t>(r) * nom);
+  if (r > 0) {
+    RTLR_CUDA(cudaMemcpyAsync(S.data(), d_S, r * sizeof(double), cudaMemcpyDeviceToHost, stream_));
+    RTLR_CUDA(cudaMemcpyAsync(V.data(), d_V, V.size() * sizeof(double), cudaMemcpyDeviceToHost, stream_));
+    RTLR_CUDA(cudaStreamSynchronize(stream_));
+  }
+  for (int j = 0; j < nom; ++j)
+    for (int k = 0; k < r; ++k) svt[k + static_cast<size_t>(j) * r] = S[k] * V[j + static_cast<size_t>(k) * nom];
+  DBuf<double> dsvt, rec, part;
+  dsvt.upload(svt.data(), svt.size(), stream_);
+  double* Y = rec.ensure(static_cast<size_t>(n) * block);
+  double* pp = part.ensure(parts);
+  std::vector<double> hp(parts);
+  double acc = 0.0;
+  for (int j0 = 0; j0 < nom; j0 += block) {
+    const int nb = std::min(block, nom - j0);
+    gemm_nn(n, nb, r, d_X, n, dsvt.get() + static_cast<size_t>(j0) * r, r, Y, n, stream_);
+    sqdiff_partials<<<parts, 256, 0, stream_>>>(n, nb, d_psi + static_cast<size_t>(j0) * n, n, Y, n, pp);
+    RTLR_CUDA(cudaGetLastError());
+    RTLR_CUDA(cudaMemcpyAsync(hp.data(), pp, parts * sizeof(double), cudaMemcpyDeviceToHost, stream_));
+    RTLR_CUDA(cudaStreamSynchronize(stream_));
+    for (double v : hp) acc += v;  // fixed order
+  }
+  return std::sqrt(acc);
 }
 
 // proj/src/low_rank.cpp:436-492

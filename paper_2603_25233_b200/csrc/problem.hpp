@@ -142,6 +142,10 @@ class Problem {
 
   SolveReport solve_full_rank(const FullRankOptions& o);
   SolveReport solve_low_rank(const LowRankOptions& o);
+  // psi_difference (report.cpp:47-58): || Psi_full - X diag(S) V^T ||_F,
+  // device pointers; angles in blocks of 128 (a DMMA GEMM per block plus a
+  // fixed-order squared-difference reduction).
+  double psi_difference(const double* d_psi, const double* d_X, const double* d_S, const double* d_V, int rank);
 
   void check_error();  // throws runtime_error("sweep: singular local block")
 

@@ -141,3 +141,21 @@ def test_blocked_householder_qr(m, n):
     assert np.linalg.norm(q.T @ q - np.eye(n)) <= 1e-13
     r_ref = np.linalg.qr(a, mode="r")
     assert np.allclose(np.abs(np.diag(r)), np.abs(np.diag(r_ref)), rtol=1e-8, atol=1e-12)
+
+
+def test_psi_difference_matches_oracle():
+    """psi_difference (report.cpp:47-58) on the GPU, fed the oracle's own
+    full-rank psi and low-rank factors, against the oracle's value."""
+    name, ov = "pin_cell", {}
+    o = O.Problem(name, **ov)
+    full, low = o.solve("full"), o.solve("lowrank")
+    n, nom, r = o.n, o.n_theta * o.n_omega_z, low.factor_rank
+    psi, X, S, V = full.get("psi", n * nom), low.get("X", n * r), low.get("S", r), low.get("V", nom * r)
+    ref = O.lib().oracle_psi_difference(full.h, low.h)
+    g = P.Problem(name, **ov)
+    got = g.psi_difference(psi, X, S, V)
+    assert abs(got - ref) <= 1e-12 * max(1.0, abs(ref)) + 1e-15, (got, ref)
+    # and the GPU's own runs, compared the reference's way (compare_runs)
+    cmp = P.compare_runs(g.solve_full_rank(), g.solve_low_rank(), problem=g)
+    assert cmp["has_psi_diff"] and cmp["psi_diff_two_norm"] <= 1e-5
+    assert cmp["phi_diff_two_norm"] <= 1e-6 and 0 < cmp["compression_ratio"] < 1
