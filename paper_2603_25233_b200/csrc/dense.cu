@@ -313,6 +313,95 @@ constexpr int kMmaPad = 8;  // row stride 72 doubles: the 4 k-rows x 8 lanes of 
 
 // TRANS_A: op(A)[m][k] = A[k + m lda] (A^T B, split-K partials into out);
 // else op(A)[m][k] = A[m + k lda] (A B; out = C, or C -= when subtract).
+// A^T B split-K on DMMA with a two-stage cp.async pipeline: both operands
+// are K-contiguous, so a 64 x 32 tile of each is 64 runs of 256 B staged as
+// [m][k] / [n][k] (row stride 36 doubles: fragment loads hit distinct banks)
+// while the tensor cores work on the other stage.  Needs A, B 16-byte
+// aligned with even leading dimensions and K even (the launcher checks).
+constexpr int kTnBk = 32, kTnLd = kTnBk + 4;
+
+__device__ __forceinline__ void cp_async16(double* smem_dst, const double* src, bool valid) {
+  const unsigned d = static_cast<unsigned>(__cvta_generic_to_shared(smem_dst));
+  const int n = valid ? 16 : 0;  // zero-fill outside the matrix
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(d), "l"(src), "r"(n) : "memory");
+}
+
+__global__ void __launch_bounds__(256) gemm_tn_dmma_pipe(int M, int N, long long K, long long kchunk,
+                                                         const double* __restrict__ A, long long lda,
+                                                         const double* __restrict__ B, long long ldb,
+                                                         double* __restrict__ out, long long ldo,
+                                                         long long split_stride) {
+  extern __shared__ double sm[];
+  double* As = sm;                           // [2][BM][kTnLd]
+  double* Bs = sm + 2 * BM * kTnLd;          // [2][BN][kTnLd]
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int wm = (warp & 1) * 32, wn = (warp >> 1) * 16;
+  const int m0 = blockIdx.x * BM, n0 = blockIdx.y * BN;
+  const long long k0 = blockIdx.z * kchunk, k1 = min(K, k0 + kchunk);
+  const int fr = lane >> 2, fc = lane & 3;
+  const int nt = min(2, max(0, (N - (n0 + wn) + 7) / 8));  // this warp's live 8-column tiles
+  auto stage = [&](int buf, long long kb) {
+    // 64 rows x 32 k per operand = 64 x 16 chunks of 16 B; 4 + 4 per thread
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      const int idx = tid + e * 256, row = idx >> 4, kq = (idx & 15) * 2;
+      const long long k = kb + kq;
+      const int m = m0 + row, n = n0 + row;
+      const bool ka = k < k1;
+      cp_async16(As + (buf * BM + row) * kTnLd + kq, A + (ka && m < M ? k + static_cast<long long>(m) * lda : 0),
+                 ka && m < M);
+      cp_async16(Bs + (buf * BN + row) * kTnLd + kq, B + (ka && n < N ? k + static_cast<long long>(n) * ldb : 0),
+                 ka && n < N);
+    }
+    asm volatile("cp.async.commit_group;" ::: "memory");
+  };
+  double acc[4][2][2];
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 2; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+  int buf = 0;
+  if (k0 < k1) stage(0, k0);
+  for (long long kb = k0; kb < k1; kb += kTnBk, buf ^= 1) {
+    if (kb + kTnBk < k1) {
+      stage(buf ^ 1, kb + kTnBk);
+      asm volatile("cp.async.wait_group 1;" ::: "memory");
+    } else {
+      asm volatile("cp.async.wait_group 0;" ::: "memory");
+    }
+    __syncthreads();
+    const double* as = As + buf * BM * kTnLd;
+    const double* bs = Bs + buf * BN * kTnLd;
+    if (nt > 0) {  // warps whose 16 columns all lie past N (skinny products) skip the tensor work
+#pragma unroll
+      for (int ks = 0; ks < kTnBk; ks += 4) {
+        double a[4], b[2];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) a[i] = as[(wm + 8 * i + fr) * kTnLd + ks + fc];
+#pragma unroll
+        for (int j = 0; j < 2; ++j) b[j] = bs[(wn + 8 * j + fr) * kTnLd + ks + fc];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          dmma884(acc[i][0][0], acc[i][0][1], a[i], b[0]);
+          if (nt > 1) dmma884(acc[i][1][0], acc[i][1][1], a[i], b[1]);
+        }
+      }
+    }
+    __syncthreads();  // the stage is refilled next iteration
+  }
+  double* o = out + blockIdx.z * split_stride;
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 2; ++j)
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int m = m0 + wm + 8 * i + fr;
+        const int n = n0 + wn + 8 * j + 2 * fc + h;
+        if (m < M && n < N) o[m + static_cast<long long>(n) * ldo] = acc[i][j][h];
+      }
+}
+
 template <bool TRANS_A>
 __global__ void __launch_bounds__(256) gemm_dmma_kernel(long long M, int N, long long K, long long kchunk,
                                                         const double* __restrict__ A, long long lda,
@@ -1064,7 +1153,9 @@ void gemm_tn(int M, int N, long long K, const double* A, long long lda, const do
   kchunk = ((kchunk + 31) / 32) * 32;
   splits = static_cast<int>((K + kchunk - 1) / kchunk);
   if (splits < 1) splits = 1;
-  if (N <= kSkinny) {
+  const bool pipe_ok = aligned16(A) && aligned16(B) && lda % 2 == 0 && ldb % 2 == 0 && K % 2 == 0 &&
+                       kchunk % kTnBk == 0;
+  if (N <= kSkinny && !pipe_ok) {
     double* o = splits == 1 ? C : work;
     const long long ldo = splits == 1 ? ldc : M, sstride = splits == 1 ? 0 : static_cast<long long>(M) * N;
     if (aligned16(A) && aligned16(B) && lda % 2 == 0 && ldb % 2 == 0) {
@@ -1088,7 +1179,13 @@ void gemm_tn(int M, int N, long long K, const double* A, long long lda, const do
   dim3 grid((M + BM - 1) / BM, (N + BN - 1) / BN, splits);
   double* o = splits == 1 ? C : work;
   const long long ldo = splits == 1 ? ldc : M, sstride = splits == 1 ? 0 : static_cast<long long>(M) * N;
-  gemm_dmma_kernel<true><<<grid, 256, 0, s>>>(M, N, K, kchunk, A, lda, B, ldb, o, ldo, sstride, false);
+  if (pipe_ok) {
+    const int smem = 2 * (BM + BN) * kTnLd * static_cast<int>(sizeof(double));
+    RTLR_CUDA(cudaFuncSetAttribute(gemm_tn_dmma_pipe, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    gemm_tn_dmma_pipe<<<grid, 256, smem, s>>>(M, N, K, kchunk, A, lda, B, ldb, o, ldo, sstride);
+  } else {
+    gemm_dmma_kernel<true><<<grid, 256, 0, s>>>(M, N, K, kchunk, A, lda, B, ldb, o, ldo, sstride, false);
+  }
   if (splits > 1) launch_splitk_reduce(M, N, splits, work, C, ldc, s);
   RTLR_CUDA(cudaGetLastError());
 }
