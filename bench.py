@@ -184,7 +184,8 @@ def run_reference(args, rank, world):
     print(json.dumps(line), flush=True)
 
 
-SOLVER_JOBS = (("C2", "lowrank"), ("C4", "full"), ("C4", "lowrank"))
+SOLVER_JOBS = (("C1", "full"), ("C1", "lowrank"), ("C2", "lowrank"), ("C4", "full"), ("C4", "lowrank"))
+CPU_REFERENCE_JOBS = (("C1", "full"), ("C1", "lowrank"))  # the oracle finishes these in seconds
 
 
 def solver_leg(P, local, rank, world, dist):
@@ -211,10 +212,29 @@ def solver_leg(P, local, rank, world, dist):
                  "sharding": "angles" if world > 1 else "none"}
         if method == "lowrank":
             entry["final_rank"] = int(rep.history("rank")[-1])
+        if world == 1 and (name, method) in CPU_REFERENCE_JOBS:
+            entry["cpu_reference"] = cpu_solver_reference(name, method, rep)
         out[f"{name}_{method}"] = entry
         del sp
         torch.cuda.synchronize()
     return out
+
+
+def cpu_solver_reference(name, method, gpu_rep):
+    """The reference's CPU solver (the oracle restatement; R itself cannot be
+    built) on the same config, 1 host core, timed in the same run; and the
+    GPU run's parity against it."""
+    import numpy as np
+    sys.path.insert(0, os.path.join(ROOT, "tests"))
+    import _oracle as O
+    o = O.Problem(name)
+    t0 = time.perf_counter()
+    r = o.solve(method)
+    dt = time.perf_counter() - t0
+    phi = r.get("phi", o.n)
+    return {"seconds": dt, "cores": 1, "kind": "port", "iterations": r.iterations,
+            "phi_rel_l2_gpu_vs_cpu": float(np.linalg.norm(gpu_rep.phi - phi) / np.linalg.norm(phi)),
+            "final_rank": int(r.history("rank")[-1]) if method == "lowrank" else None}
 
 
 def arm_watchdog(seconds, line, rank):
