@@ -402,6 +402,95 @@ __global__ void __launch_bounds__(256) gemm_tn_dmma_pipe(int M, int N, long long
       }
 }
 
+// C (-)= A B on DMMA with the same two-stage cp.async pipeline: A (M x K,
+// M-contiguous, M huge) is staged [k][m] in 16-byte pieces, B (K x N, any
+// ld) [n][k] in 8-byte pieces.  Needs A 16-byte aligned, lda and M even.
+constexpr int kNnLdA = BM + 8;
+__device__ __forceinline__ void cp_async8(double* smem_dst, const double* src, bool valid) {
+  const unsigned d = static_cast<unsigned>(__cvta_generic_to_shared(smem_dst));
+  const int n = valid ? 8 : 0;
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;" ::"r"(d), "l"(src), "r"(n) : "memory");
+}
+
+__global__ void __launch_bounds__(256) gemm_nn_dmma_pipe(long long M, int N, int K, const double* __restrict__ A,
+                                                         long long lda, const double* __restrict__ B, long long ldb,
+                                                         double* __restrict__ C, long long ldc, bool subtract) {
+  extern __shared__ double sm[];
+  double* As = sm;                          // [2][kTnBk][kNnLdA]
+  double* Bs = sm + 2 * kTnBk * kNnLdA;     // [2][BN][kTnLd]
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int wm = (warp & 1) * 32, wn = (warp >> 1) * 16;
+  const long long m0 = static_cast<long long>(blockIdx.x) * BM;
+  const int n0 = blockIdx.y * BN;
+  const int fr = lane >> 2, fc = lane & 3;
+  const int nt = min(2, max(0, (N - (n0 + wn) + 7) / 8));
+  auto stage = [&](int buf, int kb) {
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {  // A: 32 k x 32 pairs of m
+      const int idx = tid + e * 256, kk = idx >> 5, mq = (idx & 31) * 2;
+      const int k = kb + kk;
+      const long long m = m0 + mq;
+      const bool v = k < K && m < M;
+      cp_async16(As + (buf * kTnBk + kk) * kNnLdA + mq, A + (v ? m + static_cast<long long>(k) * lda : 0), v);
+    }
+#pragma unroll
+    for (int e = 0; e < 8; ++e) {  // B: 64 n x 32 k, one double each
+      const int idx = tid + e * 256, row = idx >> 5, kk = idx & 31;
+      const int k = kb + kk, n = n0 + row;
+      const bool v = k < K && n < N;
+      cp_async8(Bs + (buf * BN + row) * kTnLd + kk, B + (v ? k + static_cast<long long>(n) * ldb : 0), v);
+    }
+    asm volatile("cp.async.commit_group;" ::: "memory");
+  };
+  double acc[4][2][2];
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 2; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+  int buf = 0;
+  stage(0, 0);
+  for (int kb = 0; kb < K; kb += kTnBk, buf ^= 1) {
+    if (kb + kTnBk < K) {
+      stage(buf ^ 1, kb + kTnBk);
+      asm volatile("cp.async.wait_group 1;" ::: "memory");
+    } else {
+      asm volatile("cp.async.wait_group 0;" ::: "memory");
+    }
+    __syncthreads();
+    const double* as = As + buf * kTnBk * kNnLdA;
+    const double* bs = Bs + buf * BN * kTnLd;
+    if (nt > 0) {
+#pragma unroll
+      for (int ks = 0; ks < kTnBk; ks += 4) {
+        double a[4], b[2];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) a[i] = as[(ks + fc) * kNnLdA + wm + 8 * i + fr];
+#pragma unroll
+        for (int j = 0; j < 2; ++j) b[j] = bs[(wn + 8 * j + fr) * kTnLd + ks + fc];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          dmma884(acc[i][0][0], acc[i][0][1], a[i], b[0]);
+          if (nt > 1) dmma884(acc[i][1][0], acc[i][1][1], a[i], b[1]);
+        }
+      }
+    }
+    __syncthreads();
+  }
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 2; ++j)
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const long long m = m0 + wm + 8 * i + fr;
+        const int n = n0 + wn + 8 * j + 2 * fc + h;
+        if (m < M && n < N) {
+          double* c = C + m + static_cast<long long>(n) * ldc;
+          *c = subtract ? *c - acc[i][j][h] : acc[i][j][h];
+        }
+      }
+}
+
 template <bool TRANS_A>
 __global__ void __launch_bounds__(256) gemm_dmma_kernel(long long M, int N, long long K, long long kchunk,
                                                         const double* __restrict__ A, long long lda,
@@ -1198,7 +1287,8 @@ void gemm_nn(long long M, int N, int K, const double* A, long long lda, const do
       for (int j = 0; j < N; ++j) RTLR_CUDA(cudaMemsetAsync(C + j * ldc, 0, M * sizeof(double), s));
     return;
   }
-  if (N <= kSkinny) {
+  const bool pipe_ok = aligned16(A) && lda % 2 == 0 && M % 2 == 0;
+  if (N <= 8 || (N <= kSkinny && !pipe_ok)) {
     if (aligned16(A) && lda % 2 == 0) {
       const unsigned grid = static_cast<unsigned>((M + 511) / 512);
       if (N == 1) gemm_nn_skinny2<1><<<grid, 256, 0, s>>>(M, N, K, A, lda, B, ldb, C, ldc, subtract);
@@ -1214,7 +1304,13 @@ void gemm_nn(long long M, int N, int K, const double* A, long long lda, const do
     return;
   }
   dim3 grid(static_cast<unsigned>((M + BM - 1) / BM), (N + BN - 1) / BN);
-  gemm_dmma_kernel<false><<<grid, 256, 0, s>>>(M, N, K, 0, A, lda, B, ldb, C, ldc, 0, subtract);
+  if (pipe_ok) {
+    const int smem = 2 * (kTnBk * kNnLdA + BN * kTnLd) * static_cast<int>(sizeof(double));
+    RTLR_CUDA(cudaFuncSetAttribute(gemm_nn_dmma_pipe, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    gemm_nn_dmma_pipe<<<grid, 256, smem, s>>>(M, N, K, A, lda, B, ldb, C, ldc, subtract);
+  } else {
+    gemm_dmma_kernel<false><<<grid, 256, 0, s>>>(M, N, K, 0, A, lda, B, ldb, C, ldc, 0, subtract);
+  }
   RTLR_CUDA(cudaGetLastError());
 }
 

@@ -223,6 +223,14 @@ class LowRankEngine {
   PhaseTimer pt_;
   int reorth_count_ = 0;        // Householder rebuilds (all inner loops)
   double reorth_seconds_ = 0.0;  // their wall time (meaningful with RTLR_PROFILE=1)
+  double cgs_split_[3] = {0, 0, 0};  // RTLR_PROFILE: block GEMMs / per-snapshot loop / overlap check
+  void lap(int slot, std::chrono::steady_clock::time_point& t) {
+    if (!pt_.on) return;
+    RTLR_CUDA(cudaStreamSynchronize(s_));
+    const auto now = std::chrono::steady_clock::now();
+    cgs_split_[slot] += std::chrono::duration<double>(now - t).count();
+    t = now;
+  }
 
   InnerResult inner(const double* d_phi_prev, SubsampleRng& rng);
   int rank() const { return rank_; }
@@ -316,6 +324,8 @@ bool LowRankEngine::mgs_ro_update(const double* snaps, const std::vector<int>& a
   // kept.  X_old is read 4 times per batch instead of up to 4 times per
   // snapshot.
   const int r_old = rank_;
+  if (pt_.on) RTLR_CUDA(cudaStreamSynchronize(s_));
+  auto tlap = std::chrono::steady_clock::now();
   double* Rm = rem_.ensure(static_cast<size_t>(n_) * p_in);
   RTLR_CUDA(cudaMemcpyAsync(Rm, snaps, static_cast<size_t>(n_) * p_in * sizeof(double), cudaMemcpyDeviceToDevice, s_));
   double* nr = nrm_.ensure(std::max(p_in, 128));
@@ -338,6 +348,7 @@ bool LowRankEngine::mgs_ro_update(const double* snaps, const std::vector<int>& a
   } else {
     RTLR_CUDA(cudaStreamSynchronize(s_));
   }
+  lap(0, tlap);
   double* cnew = vec_.get();
   double* corr = vec_.get() + rmax_;
   std::vector<double> hc(p_in), hc2(p_in);
@@ -373,6 +384,7 @@ bool LowRankEngine::mgs_ro_update(const double* snaps, const std::vector<int>& a
     sampled_.push_back(angles[i]);
     ++n_snap_;
   }
+  lap(1, tlap);
   bool reorth = false;
   if (rank_ > prev_rank_ && rank_ >= 2) {
     const double overlap = std::abs(host_dot(X_.col(0), X_.col(rank_ - 1), n_));
@@ -878,7 +890,8 @@ SolveReport Problem::solve_low_rank(const LowRankOptions& o) {
   if (eng.pt_.on) {
     std::fprintf(stderr, "[rtlr profile] low-rank phases (s):");
     for (auto& e : eng.pt_.acc) std::fprintf(stderr, " %s=%.4f", e.first.c_str(), e.second);
-    std::fprintf(stderr, " | reorth: %d rebuilds, %.4f s (inside cgs)\n", eng.reorth_count_, eng.reorth_seconds_);
+    std::fprintf(stderr, " | reorth: %d rebuilds, %.4f s (inside cgs) | cgs: block %.4f, per-snapshot %.4f\n",
+                 eng.reorth_count_, eng.reorth_seconds_, eng.cgs_split_[0], eng.cgs_split_[1]);
   }
   rep.phi.resize(n);
   RTLR_CUDA(cudaMemcpyAsync(rep.phi.data(), phi, n * sizeof(double), cudaMemcpyDeviceToHost, stream_));
