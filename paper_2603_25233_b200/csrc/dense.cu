@@ -574,7 +574,7 @@ __global__ void gemv_n_kernel(long long n, int k, const double* __restrict__ A, 
   }
 }
 
-constexpr int kDotParts = 296;
+constexpr int kDotParts = kDotWork;
 
 __global__ void dot_partials(long long n, const double* __restrict__ a, const double* __restrict__ b,
                              double* __restrict__ part) {

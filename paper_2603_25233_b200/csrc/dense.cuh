@@ -23,7 +23,9 @@ size_t gemm_tn_work(int M, int N, long long K);
 void gemv_n(long long n, int k, const double* A, long long lda, const double* x, double alpha, double* y,
             cudaStream_t s);
 
-// Deterministic dot products / norms: out = sum a*b (partials then fixed-order sum)
+// Deterministic dot products / norms: out = sum a*b (partials then fixed-order sum);
+// work >= kDotWork doubles
+constexpr int kDotWork = 296;
 void dot(long long n, const double* a, const double* b, double* work, double* out, cudaStream_t s);
 void scale_copy(long long n, const double* x, const double* h, double* y, cudaStream_t s);  // y = x / *h
 void axpy_dev(long long n, const double* alpha, double sign, const double* x, double* y, cudaStream_t s);

@@ -135,6 +135,118 @@ __global__ void sqdiff_partials(long long rows, int cols, const double* __restri
   }
 }
 
+// ---- the within-batch CGS of mgs_ro_update on the device, no host syncs:
+// the accepted count k, the second-pass flag, h and the accept/position
+// flags live in device memory and gate the kernels; the host reads the
+// batch's outcome once (low_rank.cpp:74-105).
+constexpr int kCgsMax = 16;     // snapshots per batch handled on the device
+constexpr int kCgsParts = 296;  // fixed row partition of the dot products
+
+struct CgsState {
+  int k;                  // vectors accepted so far in this batch
+  int do2;                // second pass for the current snapshot
+  int acc[kCgsMax], pos[kCgsMax];
+  double rn2, h2;         // |rem|^2 after pass 1 / after all passes
+  double h[kCgsMax];
+  double coef[kCgsMax][kCgsMax];  // coef[i][j] = x_{r_old+j}^T rem_i (both passes)
+  double c[kCgsMax];      // the current pass's coefficients
+};
+
+// partial dots of X[:, j] (j < min(m, st.k)) with v; part[j * gridDim.x + block]
+__global__ void __launch_bounds__(256) cgs_dots(long long n, int m, const double* __restrict__ X, long long ldx,
+                                                const double* __restrict__ v, const CgsState* st, bool second,
+                                                double* __restrict__ part) {
+  __shared__ double sh[8][kCgsMax];
+  if (second && !st->do2) return;
+  const int k = min(m, st->k);
+  if (k == 0) return;
+  double acc[kCgsMax];
+#pragma unroll
+  for (int j = 0; j < kCgsMax; ++j) acc[j] = 0.0;
+  for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<long long>(gridDim.x) * blockDim.x) {
+    const double vi = v[i];
+#pragma unroll
+    for (int j = 0; j < kCgsMax; ++j)
+      if (j < k) acc[j] += X[i + j * ldx] * vi;
+  }
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+#pragma unroll
+  for (int j = 0; j < kCgsMax; ++j) {
+    double t = acc[j];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
+    if (lane == 0) sh[w][j] = t;
+  }
+  __syncthreads();
+  if (threadIdx.x < k) {
+    double t = 0.0;
+    for (int ww = 0; ww < (blockDim.x >> 5); ++ww) t += sh[ww][threadIdx.x];
+    part[threadIdx.x * gridDim.x + blockIdx.x] = t;
+  }
+}
+
+// c[j] = sum of the partials in block order; coef[i][j] += c[j]; one warp per j
+__global__ void cgs_finish(int m, int parts, const double* __restrict__ part, CgsState* st, int i, bool second) {
+  if (second && !st->do2) return;
+  const int k = min(m, st->k);
+  const int j = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (j >= k) return;
+  double t = 0.0;
+  for (int z = lane; z < parts; z += 32) t += part[j * parts + z];
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
+  if (lane == 0) {
+    st->c[j] = t;
+    st->coef[i][j] += t;
+  }
+}
+
+// v -= X[:, 0:k] c
+__global__ void cgs_axpy(long long n, int m, const double* __restrict__ X, long long ldx, const CgsState* st,
+                         bool second, double* __restrict__ v) {
+  if (second && !st->do2) return;
+  const int k = min(m, st->k);
+  if (k == 0) return;
+  double c[kCgsMax];
+#pragma unroll
+  for (int j = 0; j < kCgsMax; ++j) c[j] = j < k ? st->c[j] : 0.0;
+  for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<long long>(gridDim.x) * blockDim.x) {
+    double s = 0.0;
+#pragma unroll
+    for (int j = 0; j < kCgsMax; ++j)
+      if (j < k) s += X[i + j * ldx] * c[j];
+    v[i] -= s;
+  }
+}
+
+// the reference's conditional second pass: |rem| < 0.5 |snapshot| after pass 1
+__global__ void cgs_gate(CgsState* st, double norm0) {
+  st->do2 = st->k > 0 && sqrt(st->rn2) < 0.5 * norm0;
+}
+
+// drop test h > 1e-12 |snapshot| (low_rank.hpp:61-62): accepted vectors take
+// the next column
+__global__ void cgs_accept(CgsState* st, int i, double norm0) {
+  const double h = sqrt(st->h2);
+  st->h[i] = h;
+  const int acc = norm0 > 0.0 && h > 1e-12 * norm0;
+  st->acc[i] = acc;
+  st->pos[i] = st->k;
+  if (acc) ++st->k;
+}
+
+__global__ void cgs_store(long long n, const double* __restrict__ v, const CgsState* st, int i,
+                          double* __restrict__ X0, long long ldx) {
+  if (!st->acc[i]) return;
+  double* col = X0 + static_cast<long long>(st->pos[i]) * ldx;
+  const double h = st->h[i];
+  for (long long e = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; e < n;
+       e += static_cast<long long>(gridDim.x) * blockDim.x)
+    col[e] = v[e] / h;
+}
+
 int g1(long long n) {
   long long g = (n + 255) / 256;
   return static_cast<int>(std::max<long long>(1, std::min<long long>(g, 148 * 16)));
@@ -275,7 +387,7 @@ class LowRankEngine {
   const double* dirs_;
   DMat X_;
   DBuf<double> proj_, prhs_, rhs_core_, phi_, phi_old_, rem_, vec_, C_, work_, snaps_, wbuf_, gbuf_, sol_, cand_,
-      ybuf_, nrm_, qa_, qq_, qr_, tau_, hrec_, luw_, gsol_;
+      ybuf_, nrm_, qa_, qq_, qr_, tau_, hrec_, luw_, gsol_, cgs_;
   DBuf<int> ang_, ang2_, flags_, pos_;
   double* hbuf_ = nullptr;
   int rank_ = 0, n_snap_ = 0, prev_rank_ = 0;
@@ -349,40 +461,87 @@ bool LowRankEngine::mgs_ro_update(const double* snaps, const std::vector<int>& a
     RTLR_CUDA(cudaStreamSynchronize(s_));
   }
   lap(0, tlap);
-  double* cnew = vec_.get();
-  double* corr = vec_.get() + rmax_;
-  std::vector<double> hc(p_in), hc2(p_in);
-  for (int i = 0; i < p_in; ++i) {
-    double* rem = Rm + static_cast<size_t>(i) * n_;
-    const int k_new = rank_ - r_old;
-    std::vector<double> reccol(rank_ + 1, 0.0);
-    for (int k = 0; k < r_old; ++k) reccol[k] = cold[k + static_cast<size_t>(i) * r_old];
-    if (k_new > 0) {
-      tn(k_new, 1, X_.col(r_old), X_.ld, rem, n_, cnew, k_new);
-      gemv_n(n_, k_new, X_.col(r_old), X_.ld, cnew, -1.0, rem, s_);
-      RTLR_CUDA(cudaMemcpyAsync(hc.data(), cnew, k_new * sizeof(double), cudaMemcpyDeviceToHost, s_));
-      const double rn = std::sqrt(host_dot(rem, rem, n_));
-      if (rn < 0.5 * norm0[i]) {
-        tn(k_new, 1, X_.col(r_old), X_.ld, rem, n_, corr, k_new);
-        gemv_n(n_, k_new, X_.col(r_old), X_.ld, corr, -1.0, rem, s_);
-        RTLR_CUDA(cudaMemcpyAsync(hc2.data(), corr, k_new * sizeof(double), cudaMemcpyDeviceToHost, s_));
-        RTLR_CUDA(cudaStreamSynchronize(s_));
-        for (int k = 0; k < k_new; ++k) hc[k] += hc2[k];
+  // Within-batch CGS against the vectors this batch accepts.  Up to
+  // kCgsMax snapshots (every regular batch): on the device, gated by device
+  // flags, one host read per batch.  Larger batches (verification offenders)
+  // take the host-driven loop.
+  if (p_in <= kCgsMax) {
+    double* part = work(static_cast<size_t>(kCgsMax) * kCgsParts + kDotWork + 8);
+    double* dwork = part + static_cast<size_t>(kCgsMax) * kCgsParts;
+    CgsState* st = reinterpret_cast<CgsState*>(cgs_.ensure((sizeof(CgsState) + 7) / 8));
+    RTLR_CUDA(cudaMemsetAsync(st, 0, sizeof(CgsState), s_));
+    double* Xb = X_.col(r_old);
+    for (int i = 0; i < p_in; ++i) {
+      double* rem = Rm + static_cast<size_t>(i) * n_;
+      if (i > 0) {
+        cgs_dots<<<kCgsParts, 256, 0, s_>>>(n_, i, Xb, X_.ld, rem, st, false, part);
+        cgs_finish<<<1, 32 * kCgsMax, 0, s_>>>(i, kCgsParts, part, st, i, false);
+        cgs_axpy<<<g1(n_), 256, 0, s_>>>(n_, i, Xb, X_.ld, st, false, rem);
+        dot(n_, rem, rem, dwork, &st->rn2, s_);
+        cgs_gate<<<1, 1, 0, s_>>>(st, norm0[i]);
+        cgs_dots<<<kCgsParts, 256, 0, s_>>>(n_, i, Xb, X_.ld, rem, st, true, part);
+        cgs_finish<<<1, 32 * kCgsMax, 0, s_>>>(i, kCgsParts, part, st, i, true);
+        cgs_axpy<<<g1(n_), 256, 0, s_>>>(n_, i, Xb, X_.ld, st, true, rem);
       }
-      for (int k = 0; k < k_new; ++k) reccol[r_old + k] = hc[k];
+      dot(n_, rem, rem, dwork, &st->h2, s_);
+      cgs_accept<<<1, 1, 0, s_>>>(st, i, norm0[i]);
+      cgs_store<<<g1(n_), 256, 0, s_>>>(n_, rem, st, i, Xb, X_.ld);
     }
-    const double h = std::sqrt(host_dot(rem, rem, n_));
-    if (norm0[i] > 0.0 && h > 1e-12 * norm0[i]) {  // drop_tol (low_rank.hpp:61-62)
-      scale_val_kernel<<<g1(n_), 256, 0, s_>>>(n_, rem, h, X_.col(rank_));
-      reccol[rank_] = h;
-      accepted.push_back(i);
-      ++rank_;
-    } else {
-      reccol.resize(rank_);
+    RTLR_CUDA(cudaGetLastError());
+    CgsState h;
+    RTLR_CUDA(cudaMemcpyAsync(&h, st, sizeof(CgsState), cudaMemcpyDeviceToHost, s_));
+    RTLR_CUDA(cudaStreamSynchronize(s_));
+    for (int i = 0; i < p_in; ++i) {
+      // record column: old-basis coefficients, this batch's coefficients, h if accepted
+      const int k_before = h.pos[i];
+      std::vector<double> reccol(r_old + k_before + (h.acc[i] ? 1 : 0), 0.0);
+      for (int k = 0; k < r_old; ++k) reccol[k] = cold[k + static_cast<size_t>(i) * r_old];
+      for (int j = 0; j < k_before; ++j) reccol[r_old + j] = h.coef[i][j];
+      if (h.acc[i]) {
+        reccol[r_old + k_before] = h.h[i];
+        accepted.push_back(i);
+      }
+      rec_.push_back(std::move(reccol));
+      sampled_.push_back(angles[i]);
+      ++n_snap_;
     }
-    rec_.push_back(std::move(reccol));
-    sampled_.push_back(angles[i]);
-    ++n_snap_;
+    rank_ = r_old + h.k;
+  } else {
+    double* cnew = vec_.get();
+    double* corr = vec_.get() + rmax_;
+    std::vector<double> hc(p_in), hc2(p_in);
+    for (int i = 0; i < p_in; ++i) {
+      double* rem = Rm + static_cast<size_t>(i) * n_;
+      const int k_new = rank_ - r_old;
+      std::vector<double> reccol(rank_ + 1, 0.0);
+      for (int k = 0; k < r_old; ++k) reccol[k] = cold[k + static_cast<size_t>(i) * r_old];
+      if (k_new > 0) {
+        tn(k_new, 1, X_.col(r_old), X_.ld, rem, n_, cnew, k_new);
+        gemv_n(n_, k_new, X_.col(r_old), X_.ld, cnew, -1.0, rem, s_);
+        RTLR_CUDA(cudaMemcpyAsync(hc.data(), cnew, k_new * sizeof(double), cudaMemcpyDeviceToHost, s_));
+        const double rn = std::sqrt(host_dot(rem, rem, n_));
+        if (rn < 0.5 * norm0[i]) {
+          tn(k_new, 1, X_.col(r_old), X_.ld, rem, n_, corr, k_new);
+          gemv_n(n_, k_new, X_.col(r_old), X_.ld, corr, -1.0, rem, s_);
+          RTLR_CUDA(cudaMemcpyAsync(hc2.data(), corr, k_new * sizeof(double), cudaMemcpyDeviceToHost, s_));
+          RTLR_CUDA(cudaStreamSynchronize(s_));
+          for (int k = 0; k < k_new; ++k) hc[k] += hc2[k];
+        }
+        for (int k = 0; k < k_new; ++k) reccol[r_old + k] = hc[k];
+      }
+      const double h = std::sqrt(host_dot(rem, rem, n_));
+      if (norm0[i] > 0.0 && h > 1e-12 * norm0[i]) {  // drop_tol (low_rank.hpp:61-62)
+        scale_val_kernel<<<g1(n_), 256, 0, s_>>>(n_, rem, h, X_.col(rank_));
+        reccol[rank_] = h;
+        accepted.push_back(i);
+        ++rank_;
+      } else {
+        reccol.resize(rank_);
+      }
+      rec_.push_back(std::move(reccol));
+      sampled_.push_back(angles[i]);
+      ++n_snap_;
+    }
   }
   lap(1, tlap);
   bool reorth = false;
