@@ -1198,22 +1198,41 @@ __global__ void __launch_bounds__(256) lu_trail(int r, int k0, int jb, double* _
 __global__ void __launch_bounds__(256) lu_backsolve_warp(int r, int m, const double* __restrict__ M,
                                                          double* __restrict__ sol, long long ldsol,
                                                          int* __restrict__ flags) {
+  // Blocked by 32 from the bottom: the 32 x 32 diagonal block of U sits in
+  // shared memory and is solved with the unknowns in lanes (shuffle
+  // broadcasts, no global load on the dependency chain); the rows above
+  // then take one GEMV with the block's 32 solved unknowns.
   extern __shared__ double xsall[];
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int sys = blockIdx.x * (blockDim.x >> 5) + w;
   if (sys >= m) return;
-  double* xs = xsall + static_cast<size_t>(w) * r;
+  double* xs = xsall + static_cast<size_t>(w) * (r + 32 * 33);
+  double* ub = xs + r;  // 32 x 33 diagonal block, ub[j * 33 + i] = U[i0 + j][i0 + i]
   const double* A = M + static_cast<size_t>(sys) * r * (r + 1);
   for (int i = lane; i < r; i += 32) xs[i] = A[i + static_cast<size_t>(r) * r];
-  __syncwarp();
-  for (int i = r - 1; i >= 0; --i) {
-    const double xi = xs[i] / A[i + static_cast<size_t>(i) * r];
+  for (int i0 = ((r - 1) / 32) * 32; i0 >= 0; i0 -= 32) {
+    const int bs = min(32, r - i0);
     __syncwarp();
-    if (lane == 0) xs[i] = xi;
-    const double* ui = A + static_cast<size_t>(i) * r;
-    for (int j = lane; j < i; j += 32) xs[j] -= xi * ui[j];
+    for (int e = lane; e < bs * bs; e += 32) {
+      const int j = e % bs, i = e / bs;  // row j, column i of the block
+      ub[j * 33 + i] = A[i0 + j + static_cast<size_t>(i0 + i) * r];
+    }
     __syncwarp();
+    double x = lane < bs ? xs[i0 + lane] : 0.0;
+    for (int i = bs - 1; i >= 0; --i) {
+      const double xi = __shfl_sync(0xffffffffu, x, i) / ub[i * 33 + i];
+      if (lane == i) x = xi;
+      if (lane < i) x -= xi * ub[lane * 33 + i];
+    }
+    if (lane < bs) xs[i0 + lane] = x;
+    // rows above: xs[row] -= sum_l U[row][i0 + l] x_l
+    for (int row = lane; row < i0; row += 32) {
+      double acc = 0.0;
+      for (int l = 0; l < bs; ++l) acc += A[row + static_cast<size_t>(i0 + l) * r] * __shfl_sync(0xffffffffu, x, l);
+      xs[row] -= acc;
+    }
   }
+  __syncwarp();
   int bad = 0;
   for (int i = lane; i < r; i += 32) {
     sol[i + static_cast<long long>(sys) * ldsol] = xs[i];
@@ -1370,7 +1389,7 @@ void galerkin_batch(int r, int m, const int* angles, const double* dirs, const d
       k0 += jb;
     }
     const int per = 8;  // systems (warps) per CTA
-    const size_t smem = static_cast<size_t>(per) * r * sizeof(double);
+    const size_t smem = static_cast<size_t>(per) * (r + 32 * 33) * sizeof(double);
     if (smem > 48 * 1024)
       RTLR_CUDA(cudaFuncSetAttribute(lu_backsolve_warp, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      static_cast<int>(smem)));
