@@ -326,6 +326,65 @@ __device__ __forceinline__ void cp_async16(double* smem_dst, const double* src, 
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(d), "l"(src), "r"(n) : "memory");
 }
 
+// A^T B for N <= 8 (the CGS block products): one 8 x 8 DMMA tile per warp,
+// 64 columns of A per CTA, a four-stage cp.async pipeline of 64 x 32 A tiles
+// (16 KB) and 8 x 32 B tiles, so enough bytes are in flight to run at HBM
+// bandwidth.  Same alignment contract and split-K partials as the wide kernel.
+constexpr int kSkStages = 4;
+__global__ void __launch_bounds__(256) gemm_tn_skinny_pipe(int M, int N, long long K, long long kchunk,
+                                                           const double* __restrict__ A, long long lda,
+                                                           const double* __restrict__ B, long long ldb,
+                                                           double* __restrict__ out, long long ldo,
+                                                           long long split_stride) {
+  extern __shared__ double sm[];
+  double* As = sm;                               // [stages][64][kTnLd]
+  double* Bs = sm + kSkStages * 64 * kTnLd;      // [stages][8][kTnLd]
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int m0 = blockIdx.x * 64;
+  const long long k0 = blockIdx.y * kchunk, k1 = min(K, k0 + kchunk);
+  const int fr = lane >> 2, fc = lane & 3;
+  auto stage = [&](int buf, long long kb) {
+    if (kb < k1) {
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {  // A: 64 rows x 16 pieces
+        const int idx = tid + e * 256, row = idx >> 4, kq = (idx & 15) * 2;
+        const long long k = kb + kq;
+        const int m = m0 + row;
+        const bool v = k < k1 && m < M;
+        cp_async16(As + (buf * 64 + row) * kTnLd + kq, A + (v ? k + static_cast<long long>(m) * lda : 0), v);
+      }
+      if (tid < 128) {  // B: 8 rows x 16 pieces
+        const int row = tid >> 4, kq = (tid & 15) * 2;
+        const long long k = kb + kq;
+        const bool v = k < k1 && row < N;
+        cp_async16(Bs + (buf * 8 + row) * kTnLd + kq, B + (v ? k + static_cast<long long>(row) * ldb : 0), v);
+      }
+    }
+    asm volatile("cp.async.commit_group;" ::: "memory");  // (possibly empty) group keeps the count uniform
+  };
+  double c0 = 0.0, c1 = 0.0;
+#pragma unroll
+  for (int p = 0; p < kSkStages - 1; ++p) stage(p, k0 + p * kTnBk);
+  int buf = 0;
+  for (long long kb = k0; kb < k1; kb += kTnBk) {
+    stage((buf + kSkStages - 1) % kSkStages, kb + (kSkStages - 1) * kTnBk);
+    asm volatile("cp.async.wait_group %0;" ::"n"(kSkStages - 1) : "memory");
+    __syncthreads();
+    const double* as = As + (buf * 64 + warp * 8 + fr) * kTnLd;
+    const double* bs = Bs + (buf * 8 + fr) * kTnLd;
+#pragma unroll
+    for (int ks = 0; ks < kTnBk; ks += 4) dmma884(c0, c1, as[ks + fc], bs[ks + fc]);
+    __syncthreads();
+    buf = (buf + 1) % kSkStages;
+  }
+  const int m = m0 + warp * 8 + fr, n = 2 * fc;
+  double* o = out + blockIdx.y * split_stride;
+  if (m < M) {
+    if (n < N) o[m + static_cast<long long>(n) * ldo] = c0;
+    if (n + 1 < N) o[m + static_cast<long long>(n + 1) * ldo] = c1;
+  }
+}
+
 __global__ void __launch_bounds__(256) gemm_tn_dmma_pipe(int M, int N, long long K, long long kchunk,
                                                          const double* __restrict__ A, long long lda,
                                                          const double* __restrict__ B, long long ldb,
@@ -1287,7 +1346,12 @@ void gemm_tn(int M, int N, long long K, const double* A, long long lda, const do
   dim3 grid((M + BM - 1) / BM, (N + BN - 1) / BN, splits);
   double* o = splits == 1 ? C : work;
   const long long ldo = splits == 1 ? ldc : M, sstride = splits == 1 ? 0 : static_cast<long long>(M) * N;
-  if (pipe_ok) {
+  if (pipe_ok && N <= 8) {
+    const int smem = kSkStages * (64 + 8) * kTnLd * static_cast<int>(sizeof(double));
+    RTLR_CUDA(cudaFuncSetAttribute(gemm_tn_skinny_pipe, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    gemm_tn_skinny_pipe<<<dim3((M + 63) / 64, splits), 256, smem, s>>>(M, N, K, kchunk, A, lda, B, ldb, o, ldo,
+                                                                       sstride);
+  } else if (pipe_ok) {
     const int smem = 2 * (BM + BN) * kTnLd * static_cast<int>(sizeof(double));
     RTLR_CUDA(cudaFuncSetAttribute(gemm_tn_dmma_pipe, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
     gemm_tn_dmma_pipe<<<grid, 256, smem, s>>>(M, N, K, kchunk, A, lda, B, ldb, o, ldo, sstride);
