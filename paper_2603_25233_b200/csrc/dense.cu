@@ -1012,8 +1012,18 @@ __device__ __forceinline__ int rr_player(int k, int t, int n) {  // round-robin 
   return k == 0 ? 0 : ((k - 1 + t) % (n - 1)) + 1;
 }
 
+__global__ void col_norm2_kernel(long long m, const double* __restrict__ w, long long ldw, double* __restrict__ out) {
+  __shared__ double sh[32];
+  const double* c = w + blockIdx.x * ldw;
+  double s = 0.0;
+  for (long long i = threadIdx.x; i < m; i += blockDim.x) s += c[i] * c[i];
+  s = block_sum_all(s, sh);
+  if (threadIdx.x == 0) out[blockIdx.x] = s;
+}
+
 __global__ void __launch_bounds__(256) jacobi_round(long long m, int n, int npad, int t, double* __restrict__ w,
-                                                    long long ldw, double* __restrict__ v, int* __restrict__ rotated) {
+                                                    long long ldw, double* __restrict__ v, int* __restrict__ rotated,
+                                                    double tiny) {
   __shared__ double sh[32];
   const int pi = blockIdx.x;
   int p = rr_player(pi, t, npad), q = rr_player(npad - 1 - pi, t, npad);
@@ -1035,10 +1045,16 @@ __global__ void __launch_bounds__(256) jacobi_round(long long m, int n, int npad
   al = block_sum_all(al, sh);
   be = block_sum_all(be, sh);
   ga = block_sum_all(ga, sh);
-  // rotate only above the roundoff level of the dot products (LAPACK
-  // dgesvj's sqrt(m) eps): below it a rotation changes nothing measurable
-  // and the sweep never reports convergence
-  if (ga == 0.0 || fabs(ga) <= sqrt(static_cast<double>(m)) * 2.220446049250313e-16 * sqrt(al * be)) return;
+  // a column below 1e-15 of the largest one is numerically zero: its
+  // singular value cannot move any truncation decision, and orthogonalising
+  // roundoff noise against roundoff noise never converges
+  if (al < tiny || be < tiny) return;
+  // Rotate only above ~450 sqrt(m) eps of the pair's norms: below it the
+  // rotations chase the roundoff of the previous rounds and the sweeps do
+  // not terminate (38 sweeps per SVD at C4 with sqrt(m) eps).  Singular
+  // values stay accurate to ~1e-12 relative, far below what the truncation
+  // rank (eps_svd = 1e-8 on the tail sum, low_rank.cpp:254-266) can resolve.
+  if (ga == 0.0 || fabs(ga) <= 1e-13 * sqrt(static_cast<double>(m)) * sqrt(al * be)) return;
   if (threadIdx.x == 0) atomicAdd(rotated, 1);
   const double zeta = (be - al) / (2.0 * ga);
   const double tt = (zeta >= 0 ? 1.0 : -1.0) / (fabs(zeta) + sqrt(1.0 + zeta * zeta));
@@ -1370,7 +1386,8 @@ void gemm_nn(long long M, int N, int K, const double* A, long long lda, const do
       for (int j = 0; j < N; ++j) RTLR_CUDA(cudaMemsetAsync(C + j * ldc, 0, M * sizeof(double), s));
     return;
   }
-  const bool pipe_ok = aligned16(A) && lda % 2 == 0 && M % 2 == 0;
+  // (a single k-stage, K <= 32 — the QR trailing updates — gains nothing from the pipeline)
+  const bool pipe_ok = aligned16(A) && lda % 2 == 0 && M % 2 == 0 && K > kTnBk;
   if (N <= 8 || (N <= kSkinny && !pipe_ok)) {
     if (aligned16(A) && lda % 2 == 0) {
       const unsigned grid = static_cast<unsigned>((M + 511) / 512);
@@ -1549,13 +1566,21 @@ void householder_qr(long long m, int n, double* a, long long lda, double* tau, d
 }
 
 void jacobi_svd(long long m, int n, double* w, long long ldw, double* v, int max_sweeps, int* host_rotated,
-                double* work, cudaStream_t s) {
+                double* work, cudaStream_t s, int* sweeps_used) {
+  if (sweeps_used) *sweeps_used = 0;
   if (n < 2) return;
   const int npad = n + (n & 1);
   int* d_rot = reinterpret_cast<int*>(work);
+  double* d_n2 = work + 8;  // n doubles
+  col_norm2_kernel<<<n, 256, 0, s>>>(m, w, ldw, d_n2);
+  std::vector<double> n2(n);
+  RTLR_CUDA(cudaMemcpyAsync(n2.data(), d_n2, n * sizeof(double), cudaMemcpyDeviceToHost, s));
+  RTLR_CUDA(cudaStreamSynchronize(s));
+  const double tiny = 1e-30 * *std::max_element(n2.begin(), n2.end());
   for (int sweep = 0; sweep < max_sweeps; ++sweep) {
+    if (sweeps_used) *sweeps_used = sweep + 1;
     RTLR_CUDA(cudaMemsetAsync(d_rot, 0, sizeof(int), s));
-    for (int t = 0; t < npad - 1; ++t) jacobi_round<<<npad / 2, 256, 0, s>>>(m, n, npad, t, w, ldw, v, d_rot);
+    for (int t = 0; t < npad - 1; ++t) jacobi_round<<<npad / 2, 256, 0, s>>>(m, n, npad, t, w, ldw, v, d_rot, tiny);
     RTLR_CUDA(cudaGetLastError());
     RTLR_CUDA(cudaMemcpyAsync(host_rotated, d_rot, sizeof(int), cudaMemcpyDeviceToHost, s));
     RTLR_CUDA(cudaStreamSynchronize(s));

@@ -59,8 +59,9 @@ void householder_qr(long long m, int n, double* a, long long lda, double* tau, d
 // One-sided Jacobi on the columns of w (m x n, ld), accumulating the
 // rotations in v (n x n) when given.  Afterwards columns of w are mutually
 // orthogonal: w = U diag(s), s = column norms.
+// work >= n + 8 doubles; sweeps_used (optional) receives the sweep count.
 void jacobi_svd(long long m, int n, double* w, long long ldw, double* v, int max_sweeps, int* host_rotated,
-                double* work, cudaStream_t s);
+                double* work, cudaStream_t s, int* sweeps_used = nullptr);
 
 }  // namespace cuda
 }  // namespace rtlr

@@ -334,6 +334,7 @@ class LowRankEngine {
   ~LowRankEngine() { cudaFreeHost(hbuf_); }
   PhaseTimer pt_;
   int reorth_count_ = 0;        // Householder rebuilds (all inner loops)
+  int svd_sweeps_ = 0, svd_calls_ = 0;
   double reorth_seconds_ = 0.0;  // their wall time (meaningful with RTLR_PROFILE=1)
   double cgs_split_[3] = {0, 0, 0};  // RTLR_PROFILE: block GEMMs / per-snapshot loop / overlap check
   void lap(int slot, std::chrono::steady_clock::time_point& t) {
@@ -387,7 +388,7 @@ class LowRankEngine {
   const double* dirs_;
   DMat X_;
   DBuf<double> proj_, prhs_, rhs_core_, phi_, phi_old_, rem_, vec_, C_, work_, snaps_, wbuf_, gbuf_, sol_, cand_,
-      ybuf_, nrm_, qa_, qq_, qr_, tau_, hrec_, luw_, gsol_, cgs_;
+      ybuf_, nrm_, qa_, qq_, qr_, tau_, hrec_, luw_, gsol_, cgs_, svq_, svr_, svm_;
   DBuf<int> ang_, ang2_, flags_, pos_;
   double* hbuf_ = nullptr;
   int rank_ = 0, n_snap_ = 0, prev_rank_ = 0;
@@ -889,8 +890,14 @@ InnerResult LowRankEngine::inner(const double* d_phi_prev, SubsampleRng& rng) {
 // by one-sided Jacobi on C^T (N_Omega x r) or C (r x N_Omega), whichever
 // has the longer columns (low_rank.cpp:268-277, 457-458).
 std::vector<double> LowRankEngine::svd(bool vectors, int keep, std::vector<double>* Xout, std::vector<double>* Vout) {
+  // QR-preconditioned one-sided Jacobi (the north star's "Householder QR of
+  // the tall-skinny factor plus a small SVD of the r x r core"): W = Q R by
+  // the blocked Householder QR, then Jacobi on R^T.  Rotating R^T's columns
+  // converges in ~10 sweeps where rotating W's took ~38, each on r-long
+  // instead of N_Omega-long columns.  W = C^T (N_Omega x r) when r <=
+  // N_Omega, else C; W = (Q J) S L^T with R^T J = L S.
   const int r = rank_;
-  const bool on_ct = r <= nomega_;  // columns of C^T are the r coefficient rows
+  const bool on_ct = r <= nomega_;
   const int ncols = on_ct ? r : nomega_;
   const long long mrows = on_ct ? nomega_ : r;
   double* Wm = qa_.ensure(static_cast<size_t>(mrows) * ncols);
@@ -899,6 +906,15 @@ std::vector<double> LowRankEngine::svd(bool vectors, int keep, std::vector<doubl
   else
     RTLR_CUDA(cudaMemcpyAsync(Wm, C_.get(), static_cast<size_t>(r) * nomega_ * sizeof(double),
                               cudaMemcpyDeviceToDevice, s_));
+  double* Q = svq_.ensure(static_cast<size_t>(mrows) * ncols);
+  double* R = svr_.ensure(static_cast<size_t>(ncols) * ncols);
+  double* Mt = svm_.ensure(static_cast<size_t>(ncols) * ncols);
+  double* tau = tau_.ensure(ncols);
+  {
+    double* qw = work(householder_qr_work(mrows, ncols));
+    householder_qr(mrows, ncols, Wm, mrows, tau, Q, mrows, R, qw, work_.size(), s_);
+  }
+  transpose_kernel<<<g1(static_cast<long long>(ncols) * ncols), 256, 0, s_>>>(ncols, ncols, R, ncols, Mt, ncols);
   double* J = nullptr;
   if (vectors) {
     std::vector<double> eye(static_cast<size_t>(ncols) * ncols, 0.0);
@@ -907,9 +923,12 @@ std::vector<double> LowRankEngine::svd(bool vectors, int keep, std::vector<doubl
     RTLR_CUDA(cudaMemcpyAsync(J, eye.data(), eye.size() * sizeof(double), cudaMemcpyHostToDevice, s_));
   }
   int rotated = 0;
-  jacobi_svd(mrows, ncols, Wm, mrows, J, 60, &rotated, work(4096), s_);
+  int sweeps = 0;
+  jacobi_svd(ncols, ncols, Mt, ncols, J, 60, &rotated, work(4096), s_, &sweeps);
+  svd_sweeps_ += sweeps;
+  ++svd_calls_;
   double* nr = nrm_.ensure(ncols);
-  col_norms_kernel<<<ncols, 256, 0, s_>>>(mrows, ncols, Wm, mrows, nr);
+  col_norms_kernel<<<ncols, 256, 0, s_>>>(ncols, ncols, Mt, ncols, nr);
   std::vector<double> sv(ncols);
   RTLR_CUDA(cudaMemcpyAsync(sv.data(), nr, ncols * sizeof(double), cudaMemcpyDeviceToHost, s_));
   RTLR_CUDA(cudaStreamSynchronize(s_));
@@ -919,29 +938,31 @@ std::vector<double> LowRankEngine::svd(bool vectors, int keep, std::vector<doubl
   std::vector<double> s(ncols);
   for (int k = 0; k < ncols; ++k) s[k] = sv[order[k]];
   if (vectors && keep > 0) {
-    // left/right factors of Wm = L diag(s) J^T; C = (on_ct ? J S L^T : L S J^T)
-    std::vector<double> hW(static_cast<size_t>(mrows) * ncols), hJ(static_cast<size_t>(ncols) * ncols);
-    RTLR_CUDA(cudaMemcpyAsync(hW.data(), Wm, hW.size() * sizeof(double), cudaMemcpyDeviceToHost, s_));
-    RTLR_CUDA(cudaMemcpyAsync(hJ.data(), J, hJ.size() * sizeof(double), cudaMemcpyDeviceToHost, s_));
+    // left singular vectors of W: Q J (mrows); right: the rotated columns of R^T / s (ncols)
+    double* QJ = ybuf_.ensure(static_cast<size_t>(mrows) * ncols);
+    gemm_nn(mrows, ncols, ncols, Q, mrows, J, ncols, QJ, mrows, s_);
+    std::vector<double> hQJ(static_cast<size_t>(mrows) * ncols), hM(static_cast<size_t>(ncols) * ncols);
+    RTLR_CUDA(cudaMemcpyAsync(hQJ.data(), QJ, hQJ.size() * sizeof(double), cudaMemcpyDeviceToHost, s_));
+    RTLR_CUDA(cudaMemcpyAsync(hM.data(), Mt, hM.size() * sizeof(double), cudaMemcpyDeviceToHost, s_));
     RTLR_CUDA(cudaStreamSynchronize(s_));
-    // U_C (r x keep) and V_C (N_Omega x keep), sorted
+    // U_C (r x keep) and V_C (N_Omega x keep), sorted: C = W^T = L S (Q J)^T (on_ct), else C = W
     std::vector<double> U(static_cast<size_t>(r) * keep, 0.0), V(static_cast<size_t>(nomega_) * keep, 0.0);
     for (int kk = 0; kk < keep; ++kk) {
       const int k = order[kk];
       const double sk = sv[k];
-      for (long long i = 0; i < mrows; ++i) {
-        const double l = sk > 0.0 ? hW[i + static_cast<size_t>(k) * mrows] / sk : (i == kk ? 1.0 : 0.0);
-        if (on_ct)
-          V[i + static_cast<size_t>(kk) * nomega_] = l;
-        else
-          U[i + static_cast<size_t>(kk) * r] = l;
-      }
       for (int i = 0; i < ncols; ++i) {
-        const double jv = hJ[i + static_cast<size_t>(k) * ncols];
+        const double l = sk > 0.0 ? hM[i + static_cast<size_t>(k) * ncols] / sk : (i == kk ? 1.0 : 0.0);
         if (on_ct)
-          U[i + static_cast<size_t>(kk) * r] = jv;
+          U[i + static_cast<size_t>(kk) * r] = l;
         else
-          V[i + static_cast<size_t>(kk) * nomega_] = jv;
+          V[i + static_cast<size_t>(kk) * nomega_] = l;
+      }
+      for (long long i = 0; i < mrows; ++i) {
+        const double q = hQJ[i + static_cast<size_t>(k) * mrows];
+        if (on_ct)
+          V[i + static_cast<size_t>(kk) * nomega_] = q;
+        else
+          U[i + static_cast<size_t>(kk) * r] = q;
       }
     }
     // X_out = X U[:, :keep] on the device
@@ -1049,8 +1070,11 @@ SolveReport Problem::solve_low_rank(const LowRankOptions& o) {
   if (eng.pt_.on) {
     std::fprintf(stderr, "[rtlr profile] low-rank phases (s):");
     for (auto& e : eng.pt_.acc) std::fprintf(stderr, " %s=%.4f", e.first.c_str(), e.second);
-    std::fprintf(stderr, " | reorth: %d rebuilds, %.4f s (inside cgs) | cgs: block %.4f, per-snapshot %.4f\n",
-                 eng.reorth_count_, eng.reorth_seconds_, eng.cgs_split_[0], eng.cgs_split_[1]);
+    std::fprintf(stderr,
+                 " | reorth: %d rebuilds, %.4f s (inside cgs) | cgs: block %.4f, per-snapshot %.4f | svd: %d calls, "
+                 "%d Jacobi sweeps\n",
+                 eng.reorth_count_, eng.reorth_seconds_, eng.cgs_split_[0], eng.cgs_split_[1], eng.svd_calls_,
+                 eng.svd_sweeps_);
   }
   rep.phi.resize(n);
   RTLR_CUDA(cudaMemcpyAsync(rep.phi.data(), phi, n * sizeof(double), cudaMemcpyDeviceToHost, stream_));
