@@ -1197,8 +1197,10 @@ __global__ void __launch_bounds__(NT) lu_panel_smem(int r, int k0, int jb, doubl
 // A22 -= L21 U12 row tile by row tile.  grid (column tiles, systems).
 __global__ void __launch_bounds__(256) lu_trail(int r, int k0, int jb, double* __restrict__ M,
                                                 const int* __restrict__ piv) {
-  __shared__ double Us[kNbMax][BN + 1];
-  __shared__ double Ls[kNbMax][BM + 1];
+  // row stride 72 (= 8 mod 16 doubles): the 4 k-rows x 8 lanes of a DMMA
+  // fragment load land in distinct banks
+  __shared__ double Us[kNbMax][BN + 8];
+  __shared__ double Ls[kNbMax][BM + 8];
   __shared__ double L11[kNbMax][kNbMax + 1];
   double* A = M + static_cast<size_t>(blockIdx.y) * r * (r + 1);
   const int* pv = piv + static_cast<size_t>(blockIdx.y) * r;
@@ -1237,7 +1239,10 @@ __global__ void __launch_bounds__(256) lu_trail(int r, int k0, int jb, double* _
     for (int i = jb; i < kNbMax; ++i) Us[i][tid] = 0.0;
   }
   __syncthreads();
-  const int tm = tid % 16, tn = tid / 16;
+  // A22 -= L21 U12 on DMMA: 8 warps as 2 x 4, 32 x 16 of the 64 x 64 tile each
+  const int lane = tid & 31, warp = tid >> 5, fr = lane >> 2, fc = lane & 3;
+  const int wm = (warp & 1) * 32, wn = (warp >> 1) * 16;
+  const int ks_end = (jb + 3) & ~3;  // k past jb is zero-padded
   for (int row0 = k0 + jb; row0 < r; row0 += BM) {
     for (int e = tid; e < kNbMax * BM; e += 256) {
       const int mm = e % BM, kk = e / BM;
@@ -1245,26 +1250,31 @@ __global__ void __launch_bounds__(256) lu_trail(int r, int k0, int jb, double* _
       Ls[kk][mm] = (kk < jb && i < r) ? A[i + static_cast<size_t>(k0 + kk) * r] : 0.0;
     }
     __syncthreads();
-    double acc[4][4] = {};
-#pragma unroll 8
-    for (int kk = 0; kk < kNbMax; ++kk) {
-      double a[4], b[4];
+    double acc[4][2][2];
 #pragma unroll
-      for (int i = 0; i < 4; ++i) a[i] = Ls[kk][tm + 16 * i];
+    for (int i = 0; i < 4; ++i)
 #pragma unroll
-      for (int j = 0; j < 4; ++j) b[j] = Us[kk][tn + 16 * j];
+      for (int j = 0; j < 2; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+    for (int ks = 0; ks < ks_end; ks += 4) {
+      double a[4], b[2];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) a[i] = Ls[ks + fc][wm + 8 * i + fr];
+#pragma unroll
+      for (int j = 0; j < 2; ++j) b[j] = Us[ks + fc][wn + 8 * j + fr];
 #pragma unroll
       for (int i = 0; i < 4; ++i)
 #pragma unroll
-        for (int j = 0; j < 4; ++j) acc[i][j] += a[i] * b[j];
+        for (int j = 0; j < 2; ++j) dmma884(acc[i][j][0], acc[i][j][1], a[i], b[j]);
     }
 #pragma unroll
     for (int i = 0; i < 4; ++i)
 #pragma unroll
-      for (int j = 0; j < 4; ++j) {
-        const int row = row0 + tm + 16 * i, c = col0 + tn + 16 * j;
-        if (row < r && c <= r) A[row + static_cast<size_t>(c) * r] -= acc[i][j];
-      }
+      for (int j = 0; j < 2; ++j)
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const int row = row0 + wm + 8 * i + fr, c = col0 + wn + 8 * j + 2 * fc + h;
+          if (row < r && c <= r) A[row + static_cast<size_t>(c) * r] -= acc[i][j][h];
+        }
     __syncthreads();
   }
 }

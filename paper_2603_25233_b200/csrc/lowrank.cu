@@ -335,6 +335,7 @@ class LowRankEngine {
   PhaseTimer pt_;
   int reorth_count_ = 0;        // Householder rebuilds (all inner loops)
   int svd_sweeps_ = 0, svd_calls_ = 0;
+  long long gal_calls_ = 0, gal_systems_ = 0;
   double reorth_seconds_ = 0.0;  // their wall time (meaningful with RTLR_PROFILE=1)
   double cgs_split_[3] = {0, 0, 0};  // RTLR_PROFILE: block GEMMs / per-snapshot loop / overlap check
   void lap(int slot, std::chrono::steady_clock::time_point& t) {
@@ -651,6 +652,8 @@ void LowRankEngine::galerkin(const std::vector<int>& angles, double* d_sol, long
 // assembles every column on every rank (d_sol holds padded(m) columns).
 void LowRankEngine::galerkin_solve(const std::vector<int>& angles, double* d_sol, long long ldsol) {
   const int m = static_cast<int>(angles.size());
+  ++gal_calls_;
+  gal_systems_ += m;
   const ShardBlock sb = blk(m);
   const long long rr = static_cast<long long>(rank_) * rank_;
   const int chunk = rank_ > kSmemLuMax ? static_cast<int>(std::max<long long>(1, (128LL << 20) / rr)) : 4096;
@@ -1072,9 +1075,9 @@ SolveReport Problem::solve_low_rank(const LowRankOptions& o) {
     for (auto& e : eng.pt_.acc) std::fprintf(stderr, " %s=%.4f", e.first.c_str(), e.second);
     std::fprintf(stderr,
                  " | reorth: %d rebuilds, %.4f s (inside cgs) | cgs: block %.4f, per-snapshot %.4f | svd: %d calls, "
-                 "%d Jacobi sweeps\n",
+                 "%d Jacobi sweeps | galerkin: %lld batches, %lld systems\n",
                  eng.reorth_count_, eng.reorth_seconds_, eng.cgs_split_[0], eng.cgs_split_[1], eng.svd_calls_,
-                 eng.svd_sweeps_);
+                 eng.svd_sweeps_, eng.gal_calls_, eng.gal_systems_);
   }
   rep.phi.resize(n);
   RTLR_CUDA(cudaMemcpyAsync(rep.phi.data(), phi, n * sizeof(double), cudaMemcpyDeviceToHost, stream_));
