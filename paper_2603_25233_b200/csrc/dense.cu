@@ -1310,10 +1310,22 @@ __global__ void __launch_bounds__(256) lu_backsolve_warp(int r, int m, const dou
       if (lane < i) x -= xi * ub[lane * 33 + i];
     }
     if (lane < bs) xs[i0 + lane] = x;
-    // rows above: xs[row] -= sum_l U[row][i0 + l] x_l
+    __syncwarp();
+    // rows above: xs[row] -= sum_l U[row][i0 + l] x_l; the 32 loads of a row
+    // are issued together (a dependent load per l left the loop latency-bound)
+    const double* xb = xs + i0;
     for (int row = lane; row < i0; row += 32) {
+      const double* ar = A + row + static_cast<size_t>(i0) * r;
       double acc = 0.0;
-      for (int l = 0; l < bs; ++l) acc += A[row + static_cast<size_t>(i0 + l) * r] * __shfl_sync(0xffffffffu, x, l);
+      if (bs == 32) {
+        double v[32];
+#pragma unroll
+        for (int l = 0; l < 32; ++l) v[l] = ar[static_cast<size_t>(l) * r];
+#pragma unroll
+        for (int l = 0; l < 32; ++l) acc += v[l] * xb[l];
+      } else {
+        for (int l = 0; l < bs; ++l) acc += ar[static_cast<size_t>(l) * r] * xb[l];
+      }
       xs[row] -= acc;
     }
   }
