@@ -1599,15 +1599,26 @@ void jacobi_svd(long long m, int n, double* w, long long ldw, double* v, int max
   RTLR_CUDA(cudaMemcpyAsync(n2.data(), d_n2, n * sizeof(double), cudaMemcpyDeviceToHost, s));
   RTLR_CUDA(cudaStreamSynchronize(s));
   const double tiny = 1e-30 * *std::max_element(n2.begin(), n2.end());
+  // One sweep (npad - 1 dependent rounds, each a small launch) is captured
+  // once as a CUDA graph and replayed per sweep: the rounds are
+  // launch-latency bound, and a graph launch of the whole sweep costs about
+  // one kernel launch.
+  cudaGraph_t graph = nullptr;
+  cudaGraphExec_t exec = nullptr;
+  RTLR_CUDA(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
+  cudaMemsetAsync(d_rot, 0, sizeof(int), s);
+  for (int t = 0; t < npad - 1; ++t) jacobi_round<<<npad / 2, 256, 0, s>>>(m, n, npad, t, w, ldw, v, d_rot, tiny);
+  RTLR_CUDA(cudaStreamEndCapture(s, &graph));
+  RTLR_CUDA(cudaGraphInstantiate(&exec, graph, 0));
   for (int sweep = 0; sweep < max_sweeps; ++sweep) {
     if (sweeps_used) *sweeps_used = sweep + 1;
-    RTLR_CUDA(cudaMemsetAsync(d_rot, 0, sizeof(int), s));
-    for (int t = 0; t < npad - 1; ++t) jacobi_round<<<npad / 2, 256, 0, s>>>(m, n, npad, t, w, ldw, v, d_rot, tiny);
-    RTLR_CUDA(cudaGetLastError());
+    RTLR_CUDA(cudaGraphLaunch(exec, s));
     RTLR_CUDA(cudaMemcpyAsync(host_rotated, d_rot, sizeof(int), cudaMemcpyDeviceToHost, s));
     RTLR_CUDA(cudaStreamSynchronize(s));
     if (*host_rotated == 0) break;
   }
+  cudaGraphExecDestroy(exec);
+  cudaGraphDestroy(graph);
 }
 
 }  // namespace cuda
