@@ -63,7 +63,20 @@ struct SweepArgs {
   double* line;             // n x nx x 2 inter-band trace buffers
   int* err;                 // set to 1 on a singular local block
   StreamDev sc;
+  // Optional (general media, row-scan kernel): per-direction per-cell block
+  // data factored ahead of the sweep, n x kPrefDoubles x pref_stride
+  // (structure of arrays; see launch_sweep_prefactor).
+  const double* pref = nullptr;
+  long long pref_stride = 0;
 };
+
+// Per (direction, cell): M^-1 (16, column-major), Qc = -M^-1 K_x (8), G = T_x Qc (4)
+// for M = Omega_x A_x + Omega_y A_y + Sigma_t(cell), factored with the
+// reference's partial-pivot LU and singular test.  Off the sweep's critical
+// path, so latency-bound sweeps (a few directions, heterogeneous media) step
+// faster.  table: n x kPrefDoubles x stride doubles; stride >= ncell, even.
+constexpr int kPrefDoubles = 28;
+void launch_sweep_prefactor(const SweepArgs& a, double* table, long long stride, cudaStream_t s);
 
 // Skewed lane-per-row wavefront (sweep.cu) and row-chunk affine-scan
 // (sweep_scan.cu) formulations of K1; Problem::sweep picks the scan kernel

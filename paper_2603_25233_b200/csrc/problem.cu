@@ -274,22 +274,34 @@ void Problem::sweep(const int* d_angles, int n, const double* d_rhs, long long r
   a.line = line_.ensure(static_cast<size_t>(n) * 8 * (std::max(hp_.nx, hp_.ny) + 1) * 2);
   a.err = err_.get();
   a.sc = sc_;
-  // Kernel choice: the row-chunk scan kernel, except for a handful of
-  // directions in a heterogeneous medium (the low-rank solver's p-direction
-  // batches), where the per-cell LU makes the scan's row steps long and the
-  // sweep is latency-bound: the skewed wavefront's single-cell steps are
-  // shorter (C4 LR sweeps 1.5 s -> 1.0 s).  RTLR_SWEEP=skew|scan forces one.
+  // Kernel choice (option sweep_kernel / RTLR_SWEEP=skew|scan|pref): the
+  // row-chunk scan kernel; for a handful of directions in a heterogeneous
+  // medium (the low-rank solver's p-direction batches, latency-bound) the
+  // cell blocks are factored ahead of the sweep (launch_sweep_prefactor), so
+  // the scan's row steps carry no LU on their critical path.
   static const int forced = [] {
     const char* e = std::getenv("RTLR_SWEEP");
     if (!e) return 0;
-    return std::string(e) == "skew" ? 1 : (std::string(e) == "scan" ? 2 : 0);
+    const std::string v(e);
+    return v == "skew" ? 1 : (v == "scan" ? 2 : (v == "pref" ? 3 : 0));
   }();
-  const int choice = sweep_kernel ? sweep_kernel : forced;
-  const bool skew = choice ? choice == 1 : (!hp_.sigma_t_uniform && n <= 16);
-  if (skew)
+  int choice = sweep_kernel ? sweep_kernel : forced;
+  if (choice == 0) choice = (!hp_.sigma_t_uniform && n <= 16 && hp_.nx % 2 == 0) ? 3 : 2;
+  if (choice == 3 && (hp_.sigma_t_uniform || hp_.nx % 2 != 0)) choice = 2;  // nothing to factor / pairs unaligned
+  if (choice == 1) {
     launch_sweep(a, hp_.sigma_t_uniform, stream_);
-  else
-    launch_sweep_scan(a, hp_.sigma_t_uniform, stream_);
+    return;
+  }
+  if (choice == 3) {
+    // SoA table, two cells of padding on each side (a lane's cell pair may
+    // reach one cell past the row ends; those lanes' values are never used)
+    const long long stride = (static_cast<long long>(hp_.ncell) + 5) & ~1LL;
+    double* t = pref_.ensure(static_cast<size_t>(n) * kPrefDoubles * stride + 4);
+    launch_sweep_prefactor(a, t + 2, stride, stream_);
+    a.pref = t + 2;
+    a.pref_stride = stride;
+  }
+  launch_sweep_scan(a, hp_.sigma_t_uniform, stream_);
 }
 
 void Problem::sweep_host(const int* h_angles, int n, const double* h_rhs, long long rhs_stride, double* h_psi,

@@ -173,7 +173,7 @@ class Problem {
   double pcg_rtol = 1e-13;
   int pcg_max_iters = 20000;
   bool pcg_multigrid = true;  // false: block-Jacobi PCG
-  int sweep_kernel = 0;       // 0 auto, 1 skewed wavefront (sweep.cu), 2 row scan (sweep_scan.cu)
+  int sweep_kernel = 0;  // 0 auto, 1 skewed wavefront (sweep.cu), 2 row scan, 3 row scan on prefactored blocks
 
  private:
   friend class LowRankEngine;
@@ -188,7 +188,7 @@ class Problem {
   StreamDev sc_{};
   DBuf<double> dirs_, weights_, sigma_t_, sigma_s_, source_, bc_, sip_, jac_;
   DBuf<int> err_, angle_idx_;
-  DBuf<double> line_, norm_work_, pcg_vec_, pcg_part_, uniq_w_, scratch_, hin_[2], hout_[2];
+  DBuf<double> line_, norm_work_, pcg_vec_, pcg_part_, uniq_w_, scratch_, hin_[2], hout_[2], pref_;
   DBuf<int> hang_;
   cudaStream_t copy_in_ = nullptr, copy_out_ = nullptr;
   DBuf<PcgState> pcg_state_;

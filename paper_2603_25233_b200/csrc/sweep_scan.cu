@@ -246,6 +246,8 @@ struct Dir {
   double* my_line;
   const double* in_line;
   double* carry;      // kSplit: (W-1) x ny x 2 boundary carries
+  const double* pref;  // general media: this direction's prefactored block data (or nullptr)
+  long long pref_stride;
   int* err;
   int nx, ny, W, w, pw, nchunk, nrows, pitch;
   int rw, rW;         // row interleave: rows rw, rw + rW, ... (kRows: w, W; else 0, 1)
@@ -279,18 +281,25 @@ __device__ __forceinline__ void sweep_dir(const Dir& d) {
   // (prow, pk) walks the chunks in sweep order.
   int prow = 0, pk = kbeg;
   long long prow0 = row0_of(0);
+  // (general media with prefactored blocks: lanes 1..28 prefetch the 28
+  // structure-of-arrays planes of the same chunk; every lane then walks.)
+  const bool pf_lane = UNIFORM ? lane == 0 : (lane == 0 || (d.pref && lane <= kPrefDoubles));
   auto prefetch_next = [&]() {
     if (prow >= nrows) return;
     const int lo = pk * kChunk, cnt = min(kChunk, nx - lo);
     const long long first = prow0 + (XU ? lo : nx - lo - cnt);
-    prefetch_l2(d.rhs + 4 * first, static_cast<unsigned>(cnt) * 32u);
-    if (HAS_BC) prefetch_l2(d.bc + 4 * first, static_cast<unsigned>(cnt) * 32u);
+    if (lane == 0) {
+      prefetch_l2(d.rhs + 4 * first, static_cast<unsigned>(cnt) * 32u);
+      if (HAS_BC) prefetch_l2(d.bc + 4 * first, static_cast<unsigned>(cnt) * 32u);
+    } else if (!UNIFORM) {
+      prefetch_l2(d.pref + (lane - 1) * d.pref_stride + first, static_cast<unsigned>(cnt) * 8u);
+    }
     if (++pk == kend) {
       pk = kbeg;
       if (++prow < nrows) prow0 = row0_of(prow);
     }
   };
-  if (lane == 0)
+  if (pf_lane)
     for (int u = 0; u < kAheadChunks; ++u) prefetch_next();
 
   const int nsteps = nrows * nchunk;
@@ -314,7 +323,7 @@ __device__ __forceinline__ void sweep_dir(const Dir& d) {
       if (ncol < nx) ld_cell256(d.rhs + 4 * ncell, n0);
       if (ncol + 1 < nx) ld_cell256(d.rhs + 4 * (ncell + kDx), n1);
     }
-    if (lane == 0) prefetch_next();
+    if (pf_lane) prefetch_next();
     if (k == kbeg) {  // x-inflow of the row (segment): vacuum, or warp s-1's boundary carry
       tc0 = tc1 = 0.0;
       if (SPLIT && d.w > 0) {
@@ -416,7 +425,37 @@ __device__ __forceinline__ void sweep_dir(const Dir& d) {
       }
     } else {
       // per cell: [u | Qc] = M_a^-1 [local | -K_x], G_a = T_x Qc, f_a = T_x u
-      double Qc0[8], Qc1[8];
+      double Qc0[8], Qc1[8], G0[4], G1[4];
+      if (d.pref) {
+        // prefactored (launch_sweep_prefactor): M^-1, Qc and G of the lane's cell
+        // pair, structure of arrays, the pair's lower cell first
+        const long long lo = act0 ? (XU ? cell : cell + kDx) : 0;
+        const double* tb = d.pref + lo;
+        auto pair = [&](int k) { return __ldg(reinterpret_cast<const double2*>(tb + k * d.pref_stride)); };
+        double u0[4] = {0.0, 0.0, 0.0, 0.0}, u1[4] = {0.0, 0.0, 0.0, 0.0};
+#pragma unroll
+        for (int c = 0; c < 4; ++c)
+#pragma unroll
+          for (int i = 0; i < 4; ++i) {
+            const double2 m = pair(c * 4 + i);
+            u0[i] = fma(XU ? m.x : m.y, v0[c], u0[i]);
+            u1[i] = fma(XU ? m.y : m.x, v1[c], u1[i]);
+          }
+#pragma unroll
+        for (int i = 0; i < 4; ++i) v0[i] = u0[i], v1[i] = u1[i];
+#pragma unroll
+        for (int e = 0; e < 8; ++e) {
+          const double2 q = pair(16 + e);
+          Qc0[e] = XU ? q.x : q.y;
+          Qc1[e] = XU ? q.y : q.x;
+        }
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          const double2 g = pair(24 + e);
+          G0[e] = XU ? g.x : g.y;
+          G1[e] = XU ? g.y : g.x;
+        }
+      } else {
       bool ok0, ok1;
       {
         double A[16];
@@ -447,13 +486,13 @@ __device__ __forceinline__ void sweep_dir(const Dir& d) {
         for (int i = 0; i < 4; ++i) Qc1[i] = b1[i], Qc1[4 + i] = b2[i];
       }
       if ((!ok0 && act0) || (!ok1 && act1)) atomicExch(d.err, 1);
-      double G0[4], G1[4];
 #pragma unroll
       for (int c = 0; c < 2; ++c) {
         G0[c * 2 + 0] = tx0 * Qc0[c * 4 + 0] + tx1 * Qc0[c * 4 + 1];
         G0[c * 2 + 1] = tx0 * Qc0[c * 4 + 2] + tx1 * Qc0[c * 4 + 3];
         G1[c * 2 + 0] = tx0 * Qc1[c * 4 + 0] + tx1 * Qc1[c * 4 + 1];
         G1[c * 2 + 1] = tx0 * Qc1[c * 4 + 2] + tx1 * Qc1[c * 4 + 3];
+      }
       }
       const double f00 = tx0 * v0[0] + tx1 * v0[1], f01 = tx0 * v0[2] + tx1 * v0[3];
       const double f10 = tx0 * v1[0] + tx1 * v1[1], f11 = tx0 * v1[2] + tx1 * v1[3];
@@ -634,6 +673,8 @@ __global__ void __launch_bounds__(256, 2) sweep_scan_kernel(const SweepArgs a, i
   // line holds its columns of the previous row
   d.in_line = lines + static_cast<size_t>(MODE == kRows ? d.pw : w) * 2 * pitch;
   d.err = a.err;
+  d.pref = a.pref ? a.pref + static_cast<long long>(slot) * kPrefDoubles * a.pref_stride : nullptr;
+  d.pref_stride = a.pref_stride;
   d.nx = nx;
   d.ny = ny;
   d.W = W;
@@ -663,6 +704,62 @@ __global__ void __launch_bounds__(256, 2) sweep_scan_kernel(const SweepArgs a, i
     sweep_dir<UNIFORM, MODE, HAS_BC, false>(d);
 }
 
+// Per (direction slot, cell): the block M = Omega_x A_x + Omega_y A_y +
+// Sigma_t(cell) in the sweep's own arithmetic, factored with the reference's
+// partial-pivot LU (singular test as sweep.cpp:49-52), and written as M^-1,
+// Qc = -M^-1 K_x and G = T_x Qc, structure of arrays.
+__global__ void __launch_bounds__(256) sweep_prefactor_kernel(const SweepArgs a, double* __restrict__ table,
+                                                              long long stride) {
+  const int slot = blockIdx.y;
+  const long long c = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x;
+  const long long ncell = static_cast<long long>(a.nx) * a.ny;
+  if (c >= ncell) return;
+  const int ang = a.angles ? a.angles[slot] : slot;
+  const double omx = a.dirs[3 * ang], omy = a.dirs[3 * ang + 1];
+  const bool xu = omx >= 0.0, yu = omy >= 0.0;
+  const double* ax = xu ? a.sc.ax_minus : a.sc.ax_plus;
+  const double* ay = yu ? a.sc.ay_minus : a.sc.ay_plus;
+  double M[16];
+#pragma unroll
+  for (int k = 0; k < 16; ++k) M[k] = (omx * ax[k] + omy * ay[k]) + a.sigma_t[16 * c + k];
+  double Mi[16];
+  bool ok = true;
+#pragma unroll
+  for (int c0 = 0; c0 < 4; c0 += 3) {
+    double A[16], e0[4] = {0, 0, 0, 0}, e1[4] = {0, 0, 0, 0}, e2[4] = {0, 0, 0, 0};
+#pragma unroll
+    for (int k = 0; k < 16; ++k) A[k] = M[k];
+    e0[c0] = 1.0;
+    if (c0 + 1 < 4) e1[c0 + 1] = 1.0;
+    if (c0 + 2 < 4) e2[c0 + 2] = 1.0;
+    ok = lu_solve4x3(A, e0, e1, e2) && ok;
+#pragma unroll
+    for (int r = 0; r < 4; ++r) {
+      Mi[c0 * 4 + r] = e0[r];
+      if (c0 + 1 < 4) Mi[(c0 + 1) * 4 + r] = e1[r];
+      if (c0 + 2 < 4) Mi[(c0 + 2) * 4 + r] = e2[r];
+    }
+  }
+  if (!ok) atomicExch(a.err, 1);
+  const double kx0 = omx * (xu ? -a.sc.trx_l[0] : a.sc.trx_r[0]), kx1 = omx * (xu ? -a.sc.trx_l[1] : a.sc.trx_r[1]);
+  const double tx0 = xu ? a.sc.trx_r[0] : a.sc.trx_l[0], tx1 = xu ? a.sc.trx_r[1] : a.sc.trx_l[1];
+  double* t = table + static_cast<long long>(slot) * kPrefDoubles * stride + c;
+#pragma unroll
+  for (int k = 0; k < 16; ++k) t[k * stride] = Mi[k];
+  double Q[8];
+#pragma unroll
+  for (int my = 0; my < 2; ++my)
+#pragma unroll
+    for (int r = 0; r < 4; ++r) {
+      Q[my * 4 + r] = -(Mi[(my * 2 + 0) * 4 + r] * kx0 + Mi[(my * 2 + 1) * 4 + r] * kx1);
+      t[(16 + my * 4 + r) * stride] = Q[my * 4 + r];
+    }
+#pragma unroll
+  for (int col = 0; col < 2; ++col)
+#pragma unroll
+    for (int m = 0; m < 2; ++m) t[(24 + col * 2 + m) * stride] = tx0 * Q[col * 4 + m * 2] + tx1 * Q[col * 4 + m * 2 + 1];
+}
+
 int sm_count() {
   static const int n = [] {
     int dev = 0, v = 148;
@@ -673,6 +770,13 @@ int sm_count() {
 }
 
 }  // namespace
+
+void launch_sweep_prefactor(const SweepArgs& a, double* table, long long stride, cudaStream_t s) {
+  if (a.n <= 0) return;
+  const long long ncell = static_cast<long long>(a.nx) * a.ny;
+  sweep_prefactor_kernel<<<dim3(static_cast<unsigned>((ncell + 255) / 256), a.n), 256, 0, s>>>(a, table, stride);
+  RTLR_CUDA(cudaGetLastError());
+}
 
 void launch_sweep_scan(const SweepArgs& a, bool uniform, cudaStream_t s) {
   if (a.n <= 0) return;

@@ -30,11 +30,12 @@ SWEEP_CASES = [
 ]
 
 
-@pytest.mark.parametrize("kernel", [1, 2], ids=["skew", "scan"])
+@pytest.mark.parametrize("kernel", [1, 2, 3], ids=["skew", "scan", "scan-prefactored"])
 @pytest.mark.parametrize("name,ov", SWEEP_CASES)
 def test_sweep_matches_oracle(name, ov, kernel):
-    """Both K1 kernels (the skewed wavefront, sweep_kernel = 1, and the row
-    scan, 2), uniform and heterogeneous media, ragged grids."""
+    """Every K1 path (the skewed wavefront, sweep_kernel = 1; the row scan, 2;
+    the row scan on prefactored cell blocks, 3 — heterogeneous media with an
+    even nx, else it runs 2), uniform and heterogeneous media, ragged grids."""
     o = O.Problem(name, use_dsa=0, **ov)
     g = P.Problem(name, use_dsa=0, **ov)
     g.set_option("sweep_kernel", kernel)
