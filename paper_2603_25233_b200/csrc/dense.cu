@@ -1112,7 +1112,7 @@ constexpr int kPanelSmemBytes = 200 * 1024;
 // rows do not fit the shared-memory budget.
 __host__ __device__ inline int lu_panel_width(int r, int k0) {
   int jb = kNbMax;
-  while (jb > 1 && static_cast<long long>(r - k0) * jb * 8 > kPanelSmemBytes) jb >>= 1;
+  while (jb > 1 && static_cast<long long>(r - k0) * (jb * 8 + 4) > kPanelSmemBytes) jb >>= 1;
   return jb < r - k0 ? jb : r - k0;
 }
 
@@ -1127,9 +1127,11 @@ __device__ __forceinline__ void argmax_merge(double& best, int& bi, double ov, i
   }
 }
 
+constexpr int kPermInts = 1 + 4 * 32;  // count, then up to 2 kNbMax dst rows and 2 kNbMax src rows
+
 template <int NT>
 __global__ void __launch_bounds__(NT) lu_panel_smem(int r, int k0, int jb, double* __restrict__ M,
-                                                    int* __restrict__ piv) {
+                                                    int* __restrict__ piv, int* __restrict__ perm) {
   constexpr int NW = NT / 32;
   extern __shared__ double P[];  // (r - k0) x jb, column-major, ld = rows
   __shared__ double shv[2][NW];
@@ -1190,35 +1192,72 @@ __global__ void __launch_bounds__(NT) lu_panel_smem(int r, int k0, int jb, doubl
     const int i = e % rows, c = e / rows;
     A[k0 + i + static_cast<size_t>(k0 + c) * r] = P[e];
   }
+  // The panel's row swaps as one permutation of at most 2 jb rows, so the
+  // trailing columns apply them with independent loads (lu_trail): after
+  // the swaps, row dst[k] holds what row src[k] held.  slot[] maps a panel
+  // row to its entry (shared memory after the panel, O(1) lookups).
+  int* slot = reinterpret_cast<int*>(P + static_cast<size_t>(rows) * jb);
+  __shared__ int rowp[2 * kNbMax], cont[2 * kNbMax];
+  for (int i = tid; i < rows; i += NT) slot[i] = -1;
+  __syncthreads();
+  if (tid == 0) {
+    int np = 0;
+    auto pos_of = [&](int row) {
+      int q = slot[row - k0];
+      if (q < 0) {
+        q = np++;
+        slot[row - k0] = q;
+        rowp[q] = row;
+        cont[q] = row;
+      }
+      return q;
+    };
+    for (int j = 0; j < jb; ++j) {
+      const int a = k0 + j, b = pv[k0 + j];
+      if (a == b) continue;
+      const int pa = pos_of(a), pb = pos_of(b);
+      const int t = cont[pa];
+      cont[pa] = cont[pb];
+      cont[pb] = t;
+    }
+    int* pm = perm + static_cast<size_t>(blockIdx.x) * kPermInts;
+    int cnt = 0;
+    for (int q = 0; q < np; ++q)
+      if (cont[q] != rowp[q]) {
+        pm[1 + cnt] = rowp[q];
+        pm[1 + 2 * kNbMax + cnt] = cont[q];
+        ++cnt;
+      }
+    pm[0] = cnt;
+  }
 }
 
 // For one 64-column tile of the trailing columns (k0+jb .. r, the last one
 // the augmented rhs): the panel's row swaps, U12 = L11^-1 A12, then
 // A22 -= L21 U12 row tile by row tile.  grid (column tiles, systems).
 __global__ void __launch_bounds__(256) lu_trail(int r, int k0, int jb, double* __restrict__ M,
-                                                const int* __restrict__ piv) {
+                                                const int* __restrict__ perm) {
   // row stride 72 (= 8 mod 16 doubles): the 4 k-rows x 8 lanes of a DMMA
-  // fragment load land in distinct banks
-  __shared__ double Us[kNbMax][BN + 8];
-  __shared__ double Ls[kNbMax][BM + 8];
+  // fragment load land in distinct banks.  The permutation staging at the
+  // start reuses the same buffer.
+  __shared__ double shbuf[2 * kNbMax * (BM + 8)];
   __shared__ double L11[kNbMax][kNbMax + 1];
+  double (*Us)[BN + 8] = reinterpret_cast<double (*)[BN + 8]>(shbuf);
+  double (*Ls)[BM + 8] = reinterpret_cast<double (*)[BM + 8]>(shbuf + kNbMax * (BN + 8));
   double* A = M + static_cast<size_t>(blockIdx.y) * r * (r + 1);
-  const int* pv = piv + static_cast<size_t>(blockIdx.y) * r;
+  const int* pm = perm + static_cast<size_t>(blockIdx.y) * kPermInts;
   const int col0 = k0 + jb + blockIdx.x * BN;
   const int tid = threadIdx.x;
-  // swaps, one thread per column of the tile
+  const int cnt = pm[0];
+  // the panel's swaps on this tile's columns: every source value loaded
+  // (independently) before any destination is written; one thread per column
   if (tid < BN) {
     const int c = col0 + tid;
     if (c <= r) {
       double* col = A + static_cast<size_t>(c) * r;
-      for (int j = k0; j < k0 + jb; ++j) {
-        const int p = pv[j];
-        if (p != j) {
-          const double t = col[j];
-          col[j] = col[p];
-          col[p] = t;
-        }
-      }
+      double* st = shbuf + tid;  // staging, stride BN + 1
+      for (int k = 0; k < cnt; ++k) st[k * (BN + 1)] = col[pm[1 + 2 * kNbMax + k]];
+      for (int k = 0; k < cnt; ++k) col[pm[1 + k]] = st[k * (BN + 1)];
     }
   }
   for (int e = tid; e < jb * jb; e += 256) {
@@ -1226,16 +1265,19 @@ __global__ void __launch_bounds__(256) lu_trail(int r, int k0, int jb, double* _
     L11[i][l] = A[k0 + i + static_cast<size_t>(k0 + l) * r];
   }
   __syncthreads();
-  // U12 tile: forward substitution with unit-lower L11, one thread per column
+  // U12 tile: forward substitution with unit-lower L11, one thread per
+  // column, its jb values loaded up front
   if (tid < BN) {
     const int c = col0 + tid;
     double* col = A + static_cast<size_t>(c) * r;
+    for (int i = 0; i < jb; ++i) Us[i][tid] = c <= r ? col[k0 + i] : 0.0;
     for (int i = 0; i < jb; ++i) {
-      double s = c <= r ? col[k0 + i] : 0.0;
+      double s = Us[i][tid];
       for (int l = 0; l < i; ++l) s -= L11[i][l] * Us[l][tid];
       Us[i][tid] = s;
-      if (c <= r) col[k0 + i] = s;
     }
+    if (c <= r)
+      for (int i = 0; i < jb; ++i) col[k0 + i] = Us[i][tid];
     for (int i = jb; i < kNbMax; ++i) Us[i][tid] = 0.0;
   }
   __syncthreads();
@@ -1468,7 +1510,7 @@ void stream_products(const StencilArgs& a, int p, const double* P, long long ldp
 
 size_t galerkin_work_doubles(int r, int m) {
   if (r <= kSmemLuMax) return 0;
-  return static_cast<size_t>(m) * (static_cast<size_t>(r) * (r + 1) + r);
+  return static_cast<size_t>(m) * (static_cast<size_t>(r) * (r + 1) + r + (kPermInts + 1) / 2 + 1);
 }
 
 void galerkin_batch(int r, int m, const int* angles, const double* dirs, const double* proj, long long ldp,
@@ -1478,6 +1520,7 @@ void galerkin_batch(int r, int m, const int* angles, const double* dirs, const d
   if (r > kSmemLuMax) {
     double* M = work;
     int* piv = reinterpret_cast<int*>(work + static_cast<size_t>(m) * r * (r + 1));
+    int* perm = reinterpret_cast<int*>(work + static_cast<size_t>(m) * (r * static_cast<size_t>(r + 1) + r));
     lu_assemble<<<dim3(std::max(1, std::min(64, (r * (r + 1) + 255) / 256)), m), 256, 0, s>>>(
         r, angles, dirs, proj, ldp, proj_stride, prhs, extra, ldsol, M);
     constexpr int kPanelThreads = 256;
@@ -1485,10 +1528,10 @@ void galerkin_batch(int r, int m, const int* angles, const double* dirs, const d
                                    kPanelSmemBytes));
     for (int k0 = 0; k0 < r;) {
       const int jb = lu_panel_width(r, k0);
-      lu_panel_smem<kPanelThreads><<<m, kPanelThreads, static_cast<size_t>(r - k0) * jb * sizeof(double), s>>>(
-          r, k0, jb, M, piv);
+      lu_panel_smem<kPanelThreads><<<m, kPanelThreads, static_cast<size_t>(r - k0) * (jb * sizeof(double) + 4), s>>>(
+          r, k0, jb, M, piv, perm);
       const int ntrail = r + 1 - (k0 + jb);
-      if (ntrail > 0) lu_trail<<<dim3((ntrail + BN - 1) / BN, m), 256, 0, s>>>(r, k0, jb, M, piv);
+      if (ntrail > 0) lu_trail<<<dim3((ntrail + BN - 1) / BN, m), 256, 0, s>>>(r, k0, jb, M, perm);
       k0 += jb;
     }
     const int per = 8;  // systems (warps) per CTA
