@@ -375,6 +375,27 @@ def main():
         e2e = {"value": world * D * cells / float(et.item()), "unit": "cell-angle updates/s",
                "h2d_bytes_per_step": D * n * 8, "d2h_bytes_per_step": D * n * 8,
                "steps": e2e_steps, "chunk_directions": C, "api": "rtlr_cu_sweep(where=RTLR_CU_HOST)"}
+        # The e2e bound: 64 B of PCIe traffic per update, H2D and D2H at once.
+        # Measured here with the same pinned buffers (torch copies on two streams).
+        d_a = torch.empty(C * n, dtype=torch.float64, device="cuda")
+        d_b = torch.empty(C * n, dtype=torch.float64, device="cuda")
+        s_in, s_out = torch.cuda.Stream(), torch.cuda.Stream()
+        for _ in range(2):
+            with torch.cuda.stream(s_in):
+                d_a.copy_(h_rhs, non_blocking=True)
+            with torch.cuda.stream(s_out):
+                h_psi.copy_(d_b, non_blocking=True)
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        with torch.cuda.stream(s_in):
+            d_a.copy_(h_rhs, non_blocking=True)
+        with torch.cuda.stream(s_out):
+            h_psi.copy_(d_b, non_blocking=True)
+        torch.cuda.synchronize()
+        pcie = 2 * C * n * 8 / (time.perf_counter() - t0) / 1e9
+        e2e["pcie_gbs_h2d_plus_d2h"] = pcie
+        e2e["frac_of_pcie"] = e2e["value"] / world * BYTES_PER_UPDATE / 1e9 / pcie
+        del d_a, d_b
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:

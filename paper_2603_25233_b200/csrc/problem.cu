@@ -306,20 +306,25 @@ void Problem::sweep(const int* d_angles, int n, const double* d_rhs, long long r
 
 void Problem::sweep_host(const int* h_angles, int n, const double* h_rhs, long long rhs_stride, double* h_psi,
                          long long psi_stride) {
+  // H2D / sweep / D2H pipelined over direction chunks on three streams with
+  // kHostBufs rotating device buffers.  Chunks of ~64 MB keep PCIe at full
+  // rate in both directions while the fill and drain of the pipeline stay a
+  // small fraction of a call (the sweep of a chunk hides under its copies).
   if (n <= 0) return;
+  constexpr int kHostBufs = 3;
   const size_t nd = hp_.ndof;
   if (!copy_in_) RTLR_CUDA(cudaStreamCreateWithFlags(&copy_in_, cudaStreamNonBlocking));
   if (!copy_out_) RTLR_CUDA(cudaStreamCreateWithFlags(&copy_out_, cudaStreamNonBlocking));
-  const int chunk = static_cast<int>(std::max<size_t>(1, std::min<size_t>(n, (size_t{256} << 20) / (nd * 8))));
+  const int chunk = static_cast<int>(std::max<size_t>(1, std::min<size_t>(n, (size_t{64} << 20) / (nd * 8))));
   int* d_ang = hang_.ensure(n);
   RTLR_CUDA(cudaMemcpyAsync(d_ang, h_angles, n * sizeof(int), cudaMemcpyHostToDevice, stream_));
   const bool shared = rhs_stride == 0;
-  for (int b = 0; b < 2; ++b) {
+  for (int b = 0; b < kHostBufs; ++b) {
     hin_[b].ensure(shared ? nd : nd * chunk);
     hout_[b].ensure(nd * chunk);
   }
-  cudaEvent_t in_done[2], comp_done[2], out_done[2];
-  for (int b = 0; b < 2; ++b) {
+  cudaEvent_t in_done[kHostBufs], comp_done[kHostBufs], out_done[kHostBufs];
+  for (int b = 0; b < kHostBufs; ++b) {
     RTLR_CUDA(cudaEventCreateWithFlags(&in_done[b], cudaEventDisableTiming));
     RTLR_CUDA(cudaEventCreateWithFlags(&comp_done[b], cudaEventDisableTiming));
     RTLR_CUDA(cudaEventCreateWithFlags(&out_done[b], cudaEventDisableTiming));
@@ -328,15 +333,15 @@ void Problem::sweep_host(const int* h_angles, int n, const double* h_rhs, long l
   if (shared) RTLR_CUDA(cudaMemcpyAsync(hin_[0].get(), h_rhs, nd * 8, cudaMemcpyHostToDevice, copy_in_));
   int k = 0;
   for (int c0 = 0; c0 < n; c0 += chunk, ++k) {
-    const int b = k & 1, c = std::min(chunk, n - c0);
+    const int b = k % kHostBufs, c = std::min(chunk, n - c0);
     if (!shared) {
-      if (k >= 2) RTLR_CUDA(cudaStreamWaitEvent(copy_in_, comp_done[b], 0));  // buffer b consumed
+      if (k >= kHostBufs) RTLR_CUDA(cudaStreamWaitEvent(copy_in_, comp_done[b], 0));  // buffer b consumed
       RTLR_CUDA(cudaMemcpy2DAsync(hin_[b].get(), nd * 8, h_rhs + static_cast<size_t>(c0) * rhs_stride,
                                   static_cast<size_t>(rhs_stride) * 8, nd * 8, c, cudaMemcpyHostToDevice, copy_in_));
     }
     RTLR_CUDA(cudaEventRecord(in_done[b], copy_in_));
     RTLR_CUDA(cudaStreamWaitEvent(stream_, in_done[b], 0));
-    if (k >= 2) RTLR_CUDA(cudaStreamWaitEvent(stream_, out_done[b], 0));  // output buffer drained
+    if (k >= kHostBufs) RTLR_CUDA(cudaStreamWaitEvent(stream_, out_done[b], 0));  // output buffer drained
     sweep(d_ang + c0, c, shared ? hin_[0].get() : hin_[b].get(), shared ? 0 : static_cast<long long>(nd),
           hout_[b].get(), static_cast<long long>(nd));
     RTLR_CUDA(cudaEventRecord(comp_done[b], stream_));
@@ -347,7 +352,7 @@ void Problem::sweep_host(const int* h_angles, int n, const double* h_rhs, long l
   }
   RTLR_CUDA(cudaStreamSynchronize(copy_out_));
   RTLR_CUDA(cudaStreamSynchronize(stream_));
-  for (int b = 0; b < 2; ++b) {
+  for (int b = 0; b < kHostBufs; ++b) {
     cudaEventDestroy(in_done[b]);
     cudaEventDestroy(comp_done[b]);
     cudaEventDestroy(out_done[b]);

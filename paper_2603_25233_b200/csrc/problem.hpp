@@ -188,7 +188,7 @@ class Problem {
   StreamDev sc_{};
   DBuf<double> dirs_, weights_, sigma_t_, sigma_s_, source_, bc_, sip_, jac_;
   DBuf<int> err_, angle_idx_;
-  DBuf<double> line_, norm_work_, pcg_vec_, pcg_part_, uniq_w_, scratch_, hin_[2], hout_[2], pref_;
+  DBuf<double> line_, norm_work_, pcg_vec_, pcg_part_, uniq_w_, scratch_, hin_[3], hout_[3], pref_;
   DBuf<int> hang_;
   cudaStream_t copy_in_ = nullptr, copy_out_ = nullptr;
   DBuf<PcgState> pcg_state_;
