@@ -6,6 +6,7 @@
 // Every reduction is deterministic: a fixed grid writes one partial per
 // block and consumers sum the partials in a fixed order, so reruns are
 // bitwise identical (proj/tests/test_low_rank.cpp:441-470 contract).
+#include <cstdlib>
 #include "linalg.cuh"
 #include "mg.cuh"
 
@@ -200,6 +201,7 @@ __global__ void pcg_init(const PcgArgs a) {
     a.state->done = 0;
     a.state->iters = 0;
     a.state->failed = 0;
+    a.state->it_base = 0;
   }
 }
 
@@ -230,8 +232,9 @@ __global__ void pcg_spmv(const PcgArgs a) {
 }
 
 // alpha = rz/pq; x += alpha p; r -= alpha q; z = M^-1 r; partials r.r, r.z
-__global__ void pcg_update(const PcgArgs a, int it) {
+__global__ void pcg_update(const PcgArgs a, int local) {
   if (a.state->done) return;
+  const int it = a.state->it_base + local;
   __shared__ double sh[40];
   const double rz = sum_partials(a.part_rz + (it & 1) * a.nparts, a.nparts, sh);
   const double pq = sum_partials(a.part_pq, a.nparts, sh);
@@ -273,8 +276,9 @@ __global__ void pcg_update(const PcgArgs a, int it) {
 }
 
 // convergence test; beta = rz_new/rz_old; p = z + beta p
-__global__ void pcg_direction(const PcgArgs a, int it) {
+__global__ void pcg_direction(const PcgArgs a, int local) {
   if (a.state->done) return;
+  const int it = a.state->it_base + local;
   __shared__ double sh[40];
   const double rr = sum_partials(a.part_rr, a.nparts, sh);
   const double bb = a.state->bb;
@@ -322,11 +326,14 @@ __global__ void pcg_init_mg(const PcgArgs a) {
     a.state->done = 0;
     a.state->iters = 0;
     a.state->failed = 0;
+    a.state->it_base = 0;
   }
 }
-// p = z (init) ; partials of r.z into part_rz[slot]
-__global__ void pcg_rz(const PcgArgs a, int slot, bool copy_p) {
+// p = z (init) ; partials of r.z into part_rz[slot], slot = (it_base + local + 1) & 1
+// (init: local = -1)
+__global__ void pcg_rz(const PcgArgs a, int local, bool copy_p) {
   if (a.state->done) return;
+  const int slot = (a.state->it_base + local + 1) & 1;
   __shared__ double sh[40];
   double rz = 0.0;
   for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < a.ncell; c += gridDim.x * blockDim.x) {
@@ -341,8 +348,9 @@ __global__ void pcg_rz(const PcgArgs a, int slot, bool copy_p) {
   if (threadIdx.x == 0) a.part_rz[slot * a.nparts + blockIdx.x] = rz;
 }
 // alpha = rz/pq; x += alpha p; r -= alpha q; partials r.r
-__global__ void pcg_update_mg(const PcgArgs a, int it) {
+__global__ void pcg_update_mg(const PcgArgs a, int local) {
   if (a.state->done) return;
+  const int it = a.state->it_base + local;
   __shared__ double sh[40];
   const double rz = sum_partials(a.part_rz + (it & 1) * a.nparts, a.nparts, sh);
   const double pq = sum_partials(a.part_pq, a.nparts, sh);
@@ -420,32 +428,79 @@ void bsr_apply(const PcgArgs& a, const double* x, double* y, cudaStream_t s) {
   RTLR_CUDA(cudaGetLastError());
 }
 
-int pcg_solve(const PcgArgs& a, PcgState* host_state, cudaStream_t s) {
+namespace {
+
+__global__ void pcg_advance(PcgState* st, int chunk) { st->it_base += chunk; }
+
+bool same_loop(const PcgArgs& u, const PcgArgs& v) {  // everything the loop kernels read (not b)
+  return u.nx == v.nx && u.ny == v.ny && u.ncell == v.ncell && u.nparts == v.nparts && u.max_iters == v.max_iters &&
+         u.rtol2 == v.rtol2 && u.sip == v.sip && u.jac == v.jac && u.x == v.x && u.r == v.r && u.z == v.z &&
+         u.p == v.p && u.q == v.q && u.part_rz == v.part_rz && u.part_pq == v.part_pq && u.part_rr == v.part_rr &&
+         u.part_bb == v.part_bb && u.state == v.state && u.mg == v.mg && u.tmp4 == v.tmp4;
+}
+
+// One chunk of PCG iterations (every kernel returns at once after state->done).
+void pcg_chunk(const PcgArgs& a, int chunk, cudaStream_t s) {
+  const int g = a.nparts;
+  for (int i = 0; i < chunk; ++i) {
+    pcg_spmv<<<g, kThreads, 0, s>>>(a);
+    if (a.mg) {
+      pcg_update_mg<<<g, kThreads, 0, s>>>(a, i);
+      mg_vcycle(a, *a.mg, a.r, a.z, a.tmp4, s);
+      pcg_rz<<<g, kThreads, 0, s>>>(a, i, false);
+    } else {
+      pcg_update<<<g, kThreads, 0, s>>>(a, i);
+    }
+    pcg_direction<<<g, kThreads, 0, s>>>(a, i);
+  }
+  pcg_advance<<<1, 1, 0, s>>>(a.state, chunk);
+  RTLR_CUDA(cudaGetLastError());
+}
+
+}  // namespace
+
+PcgGraph::~PcgGraph() { reset(); }
+void PcgGraph::reset() {
+  if (exec) cudaGraphExecDestroy(exec);
+  exec = nullptr;
+}
+
+int pcg_solve(const PcgArgs& a, PcgState* host_state, cudaStream_t s, PcgGraph* graph) {
   const int g = a.nparts;
   if (a.mg) {
     pcg_init_mg<<<g, kThreads, 0, s>>>(a);
     pcg_check_zero<<<1, kThreads, 0, s>>>(a);
     mg_vcycle(a, *a.mg, a.r, a.z, a.tmp4, s);
-    pcg_rz<<<g, kThreads, 0, s>>>(a, 0, true);
+    pcg_rz<<<g, kThreads, 0, s>>>(a, -1, true);
   } else {
     pcg_init<<<g, kThreads, 0, s>>>(a);
     pcg_check_zero<<<1, kThreads, 0, s>>>(a);
   }
   RTLR_CUDA(cudaGetLastError());
   const int chunk = a.mg ? 8 : 32;
+  // The loop body is the same launch sequence every chunk: captured once per
+  // buffer set as a CUDA graph (the legacy default stream cannot capture).
+  static const bool graphs_off = [] {
+    const char* e = std::getenv("RTLR_PCG_GRAPH");
+    return e != nullptr && e[0] == '0';
+  }();
+  const bool use_graph = graph != nullptr && s != nullptr && !graphs_off;
+  if (use_graph && (graph->exec == nullptr || graph->chunk != chunk || !same_loop(graph->key, a))) {
+    graph->reset();
+    cudaGraph_t gr = nullptr;
+    RTLR_CUDA(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
+    pcg_chunk(a, chunk, s);
+    RTLR_CUDA(cudaStreamEndCapture(s, &gr));
+    RTLR_CUDA(cudaGraphInstantiate(&graph->exec, gr, 0));
+    cudaGraphDestroy(gr);
+    graph->key = a;
+    graph->chunk = chunk;
+  }
   for (int it0 = 0; it0 < a.max_iters; it0 += chunk) {
-    for (int it = it0; it < it0 + chunk && it < a.max_iters; ++it) {
-      pcg_spmv<<<g, kThreads, 0, s>>>(a);
-      if (a.mg) {
-        pcg_update_mg<<<g, kThreads, 0, s>>>(a, it);
-        mg_vcycle(a, *a.mg, a.r, a.z, a.tmp4, s);
-        pcg_rz<<<g, kThreads, 0, s>>>(a, (it + 1) & 1, false);
-      } else {
-        pcg_update<<<g, kThreads, 0, s>>>(a, it);
-      }
-      pcg_direction<<<g, kThreads, 0, s>>>(a, it);
-    }
-    RTLR_CUDA(cudaGetLastError());
+    if (use_graph)
+      RTLR_CUDA(cudaGraphLaunch(graph->exec, s));
+    else
+      pcg_chunk(a, chunk, s);
     RTLR_CUDA(cudaMemcpyAsync(host_state, a.state, sizeof(PcgState), cudaMemcpyDeviceToHost, s));
     RTLR_CUDA(cudaStreamSynchronize(s));
     if (host_state->done) break;

@@ -10,7 +10,7 @@ constexpr int kNormParts = 296;  // 2 x 148 SMs
 
 struct PcgState {
   double bb, rr;
-  int done, iters, failed, pad;
+  int done, iters, failed, it_base;  // it_base: first iteration of the running chunk
 };
 
 struct PcgArgs {
@@ -35,7 +35,19 @@ void phi_accumulate(int ndof, int nu, const double* psi, long long ld, const dou
 void diff_norms(int n, const double* a, const double* b, double* work, double* out2, cudaStream_t s);
 void vadd(int n, const double* a, const double* b, double* out, cudaStream_t s);
 void bsr_apply(const PcgArgs& a, const double* x, double* y, cudaStream_t s);
-int pcg_solve(const PcgArgs& a, PcgState* host_state, cudaStream_t s);
+// Cached CUDA graph of one chunk of PCG iterations (pcg_solve); rebuilt when
+// the loop's buffers change.
+struct PcgGraph {
+  cudaGraphExec_t exec = nullptr;
+  PcgArgs key{};
+  int chunk = 0;
+  PcgGraph() = default;
+  PcgGraph(const PcgGraph&) = delete;
+  PcgGraph& operator=(const PcgGraph&) = delete;
+  ~PcgGraph();
+  void reset();
+};
+int pcg_solve(const PcgArgs& a, PcgState* host_state, cudaStream_t s, PcgGraph* graph = nullptr);
 
 }  // namespace cuda
 }  // namespace rtlr

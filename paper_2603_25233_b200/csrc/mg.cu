@@ -1,6 +1,7 @@
 // Multigrid V-cycle preconditioner for the SIP-DG DSA system (see mg.cuh).
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <stdexcept>
 
 #include "linalg.cuh"
@@ -164,23 +165,67 @@ __global__ void dense_apply(const int* done, int n, const double* __restrict__ i
   }
 }
 
-void vcycle5(const int* done, const MgDevice& mg, int l, cudaStream_t s) {
+// Cycle shape.  Defaults were chosen by measuring PCG iterations and DSA
+// time on C1-C4 (K12); the environment overrides exist for that
+// tuning only.
+struct MgKnobs {
+  int nu5 = 2;        // damped-Jacobi steps before and after the coarse correction, 5-point levels
+  int nu_dg = 1;      // block-Jacobi steps before and after, DG level
+  int w_levels = 0;   // the first w_levels 5-point levels recurse twice (W-cycle)
+  // Aggregated operators scaled by 1/alpha.  The Galerkin product of 2x2
+  // piecewise-constant aggregation doubles every face coupling relative to a
+  // re-discretisation on the coarse grid, so the plain coarse correction
+  // under-corrects smooth error; alpha ~2 restores it (C4: 344 -> 78 PCG
+  // iterations per DSA solve).  Still an SPD preconditioner: symmetric
+  // cycle, A-convergent smoothers, SPD coarse operators.
+  double alpha = 2.2;
+};
+const MgKnobs& knobs() {
+  static const MgKnobs k = [] {
+    MgKnobs v;
+    if (const char* e = std::getenv("RTLR_MG_NU5")) v.nu5 = std::max(1, std::atoi(e));
+    if (const char* e = std::getenv("RTLR_MG_NUDG")) v.nu_dg = std::max(1, std::atoi(e));
+    if (const char* e = std::getenv("RTLR_MG_WLEVELS")) v.w_levels = std::max(0, std::atoi(e));
+    if (const char* e = std::getenv("RTLR_MG_ALPHA")) v.alpha = std::atof(e);
+    if (!(v.alpha > 0.0)) v.alpha = 2.2;
+    return v;
+  }();
+  return k;
+}
+
+// x[l] <- one cycle for A_l x = b[l], from x = 0 (zero) or from the x[l] held.
+void cycle5(const int* done, const MgDevice& mg, int l, bool zero, cudaStream_t s) {
   if (l == mg.nlev - 1) {
+    if (!zero) throw std::logic_error("multigrid: second visit of the coarsest level");
     dense_apply<<<1, 256, 0, s>>>(done, mg.ncoarse, mg.cinv, mg.b[l], mg.x[l]);
     return;
   }
+  const MgKnobs& k = knobs();
   const L5 L{mg.nx[l], mg.ny[l], mg.nx[l] * mg.ny[l], mg.st[l]};
   const int g = grid_for(L.n);
-  l5_first<<<g, 256, 0, s>>>(done, L, mg.b[l], mg.x[l]);
-  l5_smooth<<<g, 256, 0, s>>>(done, L, mg.b[l], mg.x[l], mg.t[l]);
+  double* cur = mg.x[l];
+  double* oth = mg.t[l];
+  int i = 0;
+  if (zero) {
+    l5_first<<<g, 256, 0, s>>>(done, L, mg.b[l], cur);
+    i = 1;
+  }
+  for (; i < k.nu5; ++i) {
+    l5_smooth<<<g, 256, 0, s>>>(done, L, mg.b[l], cur, oth);
+    std::swap(cur, oth);
+  }
   const int cnx = mg.nx[l + 1], cny = mg.ny[l + 1];
-  l5_restrict<<<grid_for(static_cast<long long>(cnx) * cny), 256, 0, s>>>(done, L, mg.b[l], mg.t[l], cnx, cny,
+  l5_restrict<<<grid_for(static_cast<long long>(cnx) * cny), 256, 0, s>>>(done, L, mg.b[l], cur, cnx, cny,
                                                                           mg.b[l + 1]);
-  vcycle5(done, mg, l + 1, s);
-  l5_prolong<<<g, 256, 0, s>>>(done, L, mg.t[l], mg.x[l + 1], cnx);
-  l5_smooth<<<g, 256, 0, s>>>(done, L, mg.b[l], mg.t[l], mg.x[l]);
-  l5_smooth<<<g, 256, 0, s>>>(done, L, mg.b[l], mg.x[l], mg.t[l]);
-  RTLR_CUDA(cudaMemcpyAsync(mg.x[l], mg.t[l], L.n * sizeof(double), cudaMemcpyDeviceToDevice, s));
+  cycle5(done, mg, l + 1, true, s);
+  if (l < k.w_levels && l + 1 < mg.nlev - 1) cycle5(done, mg, l + 1, false, s);
+  l5_prolong<<<g, 256, 0, s>>>(done, L, cur, mg.x[l + 1], cnx);
+  for (i = 0; i < k.nu5; ++i) {
+    l5_smooth<<<g, 256, 0, s>>>(done, L, mg.b[l], cur, oth);
+    std::swap(cur, oth);
+  }
+  if (cur != mg.x[l])
+    RTLR_CUDA(cudaMemcpyAsync(mg.x[l], cur, L.n * sizeof(double), cudaMemcpyDeviceToDevice, s));
 }
 
 void invert_dense(int n, std::vector<double>& a) {  // Gauss-Jordan, partial pivoting, column-major
@@ -247,6 +292,8 @@ std::vector<MgLevelHost> build_mg_hierarchy(int nx, int ny, const std::vector<do
             c.st[(d + 1) * nc + C] += v;  // same direction between aggregates
         }
       }
+    if (knobs().alpha != 1.0)
+      for (double& v : c.st) v /= knobs().alpha;
     lv.push_back(std::move(c));
   }
   // dense inverse of the coarsest level
@@ -270,15 +317,26 @@ std::vector<MgLevelHost> build_mg_hierarchy(int nx, int ny, const std::vector<do
 void mg_vcycle(const PcgArgs& a, const MgDevice& mg, const double* r, double* z, double* tmp4, cudaStream_t s) {
   const int g = grid_for(a.ncell);
   const int* done = &a.state->done;
-  // pre-smooth from zero: z = omega J^-1 r
-  dg_first<<<g, 256, 0, s>>>(a, r, z);
+  const MgKnobs& k = knobs();
+  const size_t bytes = 4 * static_cast<size_t>(a.ncell) * sizeof(double);
+  // pre-smooth from zero: z = omega J^-1 r, then nu_dg - 1 more steps
+  double* cur = z;
+  double* oth = tmp4;
+  dg_first<<<g, 256, 0, s>>>(a, r, cur);
+  for (int i = 1; i < k.nu_dg; ++i) {
+    dg_smooth<<<g, 256, 0, s>>>(a, r, cur, oth);
+    std::swap(cur, oth);
+  }
   // coarse correction through the cell-average level
-  dg_restrict<<<g, 256, 0, s>>>(a, r, z, mg.b[0]);
-  vcycle5(done, mg, 0, s);
-  dg_prolong<<<g, 256, 0, s>>>(a, z, mg.x[0]);
+  dg_restrict<<<g, 256, 0, s>>>(a, r, cur, mg.b[0]);
+  cycle5(done, mg, 0, true, s);
+  dg_prolong<<<g, 256, 0, s>>>(a, cur, mg.x[0]);
   // post-smooth (same damped block Jacobi)
-  dg_smooth<<<g, 256, 0, s>>>(a, r, z, tmp4);
-  RTLR_CUDA(cudaMemcpyAsync(z, tmp4, 4 * static_cast<size_t>(a.ncell) * sizeof(double), cudaMemcpyDeviceToDevice, s));
+  for (int i = 0; i < k.nu_dg; ++i) {
+    dg_smooth<<<g, 256, 0, s>>>(a, r, cur, oth);
+    std::swap(cur, oth);
+  }
+  if (cur != z) RTLR_CUDA(cudaMemcpyAsync(z, cur, bytes, cudaMemcpyDeviceToDevice, s));
   RTLR_CUDA(cudaGetLastError());
 }
 

@@ -2,8 +2,8 @@
 // SURVEY.md §8(f)1): block-Jacobi smoothing on the DG level, a cell-average
 // (P0) level whose operator is the Galerkin product P0^T A P0 (entry (0,0)
 // of every 4x4 BSR block: a 5-point stencil), then 2x2 aggregation levels
-// with Galerkin coarse operators (again 5-point) down to a small grid
-// solved by a dense inverse.  Symmetric (equal pre/post damped Jacobi), so
+// with scaled Galerkin coarse operators (again 5-point; see MgKnobs::alpha)
+// down to a small grid solved by a dense inverse.  Symmetric (equal pre/post damped Jacobi), so
 // it is a valid CG preconditioner.  Deterministic: no atomics.
 #pragma once
 

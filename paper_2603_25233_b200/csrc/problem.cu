@@ -168,10 +168,11 @@ void Problem::upload() {
     }
     sip_.upload(soa.data(), soa.size(), s);
     jac_.upload(jac.data(), jac.size(), s);
-    pcg_vec_.ensure(6 * static_cast<size_t>(h.ndof));
+    pcg_vec_.ensure(7 * static_cast<size_t>(h.ndof));  // r z p q rhs tmp4 x
     // multigrid hierarchy for the preconditioner (mg.cuh)
     std::vector<double> cinv;
     const std::vector<MgLevelHost> lv = build_mg_hierarchy(h.nx, h.ny, h.sip, 64, cinv);
+    pcg_graph_.reset();
     mg_bufs_.clear();
     mg_ = MgDevice{};
     mg_.nlev = static_cast<int>(lv.size());
@@ -380,9 +381,9 @@ PcgArgs Problem::pcg_args(const double* b, double* x) {
   a.sip = sip_.get();
   a.jac = jac_.get();
   a.b = b;
-  a.x = x;
   double* v = pcg_vec_.get();
   const size_t n = hp_.ndof;
+  a.x = x ? x : v + 6 * n;
   a.r = v;
   a.z = v + n;
   a.p = v + 2 * n;
@@ -402,8 +403,12 @@ PcgArgs Problem::pcg_args(const double* b, double* x) {
 
 int Problem::dsa_solve(const double* d_rhs, double* d_x) {
   if (sip_.get() == nullptr) throw std::invalid_argument("dsa: problem assembled without a diffusion system");
-  PcgArgs a = pcg_args(d_rhs, d_x);
-  return pcg_solve(a, h_state_, stream_);
+  // the iteration runs on resident vectors (so its captured graph is reused
+  // across calls); the solution is copied out
+  PcgArgs a = pcg_args(d_rhs, nullptr);
+  const int it = pcg_solve(a, h_state_, stream_, &pcg_graph_);
+  RTLR_CUDA(cudaMemcpyAsync(d_x, a.x, hp_.ndof * sizeof(double), cudaMemcpyDeviceToDevice, stream_));
+  return it;
 }
 
 int Problem::dsa_correct(const double* d_phi_star, const double* d_phi_prev, double* d_delta) {

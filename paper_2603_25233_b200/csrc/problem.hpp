@@ -194,6 +194,7 @@ class Problem {
   DBuf<PcgState> pcg_state_;
   std::vector<std::unique_ptr<DBuf<double>>> mg_bufs_;
   MgDevice mg_;
+  PcgGraph pcg_graph_;  // after the buffers it references
   PcgState* h_state_ = nullptr;
   double* h_pin_ = nullptr;  // small pinned host scratch
   std::vector<int> uniq_rep_, uniq_of_;
