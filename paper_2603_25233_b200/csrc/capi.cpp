@@ -270,8 +270,9 @@ int rtlr_cu_problem_set_option(rtlr_cu_problem* p, const char* key, double v) {
     else if (k == "pcg_max_iters") p->p->pcg_max_iters = static_cast<int>(v);
     else if (k == "pcg_multigrid") p->p->pcg_multigrid = v != 0.0;
     else if (k == "sweep_kernel") {
-      need(v == 0.0 || v == 1.0 || v == 2.0 || v == 3.0,
-           "sweep_kernel: 0 (auto), 1 (skewed wavefront), 2 (row scan), 3 (row scan, prefactored blocks)");
+      need(v == 0.0 || v == 1.0 || v == 2.0 || v == 3.0 || v == 4.0,
+           "sweep_kernel: 0 (auto), 1 (skewed wavefront), 2 (row scan), 3 (row scan, prefactored blocks), "
+           "4 (cluster wavefront)");
       p->p->sweep_kernel = static_cast<int>(v);
     } else throw std::invalid_argument("unknown option '" + k + "'");
   });

@@ -76,13 +76,24 @@ struct SweepArgs {
 // path, so latency-bound sweeps (a few directions, heterogeneous media) step
 // faster.  table: n x kPrefDoubles x stride doubles; stride >= ncell, even.
 constexpr int kPrefDoubles = 28;
-void launch_sweep_prefactor(const SweepArgs& a, double* table, long long stride, cudaStream_t s);
+constexpr int kPrefMinvDoubles = 16;  // M^-1 only (the wavefront kernel's table)
+void launch_sweep_prefactor(const SweepArgs& a, double* table, long long stride, cudaStream_t s,
+                            int planes = kPrefDoubles);
 
 // Skewed lane-per-row wavefront (sweep.cu) and row-chunk affine-scan
 // (sweep_scan.cu) formulations of K1; Problem::sweep picks the scan kernel
 // unless RTLR_SWEEP=skew.
 void launch_sweep(const SweepArgs& a, bool uniform_sigma_t, cudaStream_t s);
 void launch_sweep_scan(const SweepArgs& a, bool uniform_sigma_t, cudaStream_t s);
+// Few-direction wavefront sweep: one thread-block cluster (cluster CTAs x 8
+// warps) per direction, rows interleaved over the cluster's warps, traces
+// handed on through distributed shared memory.  General media need a.pref
+// (kPrefMinvDoubles planes).  cluster 0: sweep_wave_cluster's choice.
+void launch_sweep_wave(const SweepArgs& a, bool uniform_sigma_t, int cluster, cudaStream_t s);
+// Cluster size for the wavefront kernel on this launch (all n clusters
+// co-resident), or 0 when it does not apply (too many directions, rows too
+// wide for the shared-memory trace lines).
+int sweep_wave_cluster(const SweepArgs& a, bool uniform_sigma_t);
 
 // Generates C5 sources: rhs[k][dof] = U[0,1)(seed, (dir0+k)*ndof + dof).
 void launch_c5_fill(double* rhs, long long n_dirs, long long dir0, long long ndof,

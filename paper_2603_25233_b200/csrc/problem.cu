@@ -275,32 +275,50 @@ void Problem::sweep(const int* d_angles, int n, const double* d_rhs, long long r
   a.line = line_.ensure(static_cast<size_t>(n) * 8 * (std::max(hp_.nx, hp_.ny) + 1) * 2);
   a.err = err_.get();
   a.sc = sc_;
-  // Kernel choice (option sweep_kernel / RTLR_SWEEP=skew|scan|pref): the
-  // row-chunk scan kernel; for a handful of directions in a heterogeneous
-  // medium (the low-rank solver's p-direction batches, latency-bound) the
-  // cell blocks are factored ahead of the sweep (launch_sweep_prefactor), so
-  // the scan's row steps carry no LU on their critical path.
+  // Kernel choice (option sweep_kernel / RTLR_SWEEP=skew|scan|pref|wave):
+  // for a handful of directions (the low-rank solver's p-direction batches,
+  // latency-bound) the cluster wavefront, one thread-block cluster per
+  // direction, with the cell blocks of a heterogeneous medium inverted ahead
+  // of it (launch_sweep_prefactor); otherwise the row-chunk scan kernel, one
+  // SM's warps per direction.
   static const int forced = [] {
     const char* e = std::getenv("RTLR_SWEEP");
     if (!e) return 0;
     const std::string v(e);
-    return v == "skew" ? 1 : (v == "scan" ? 2 : (v == "pref" ? 3 : 0));
+    return v == "skew" ? 1 : (v == "scan" ? 2 : (v == "pref" ? 3 : (v == "wave" ? 4 : 0)));
+  }();
+  static const int wave_cluster = [] {  // RTLR_WAVE_CS: fixed cluster size (tuning)
+    const char* e = std::getenv("RTLR_WAVE_CS");
+    return e ? std::max(1, std::min(16, std::atoi(e))) : 0;
   }();
   int choice = sweep_kernel ? sweep_kernel : forced;
+  int cluster = wave_cluster;
+  if (choice == 0 || choice == 4) {
+    // a few directions: the cluster wavefront whenever every cluster fits at once
+    const int cs = sweep_wave_cluster(a, hp_.sigma_t_uniform);
+    if (choice == 0 && cs > 0) choice = 4;
+    if (choice == 4 && cluster == 0) cluster = cs > 0 ? cs : 2;
+  }
   if (choice == 0) choice = (!hp_.sigma_t_uniform && n <= 16 && hp_.nx % 2 == 0) ? 3 : 2;
   if (choice == 3 && (hp_.sigma_t_uniform || hp_.nx % 2 != 0)) choice = 2;  // nothing to factor / pairs unaligned
+  if (choice == 4 && (hp_.nx * 16 * 8 + 8 * 1024 > 220 * 1024)) choice = 2;  // trace lines must fit shared memory
   if (choice == 1) {
     launch_sweep(a, hp_.sigma_t_uniform, stream_);
     return;
   }
-  if (choice == 3) {
+  if (choice == 3 || (choice == 4 && !hp_.sigma_t_uniform)) {
     // SoA table, two cells of padding on each side (a lane's cell pair may
     // reach one cell past the row ends; those lanes' values are never used)
+    const int planes = choice == 4 ? kPrefMinvDoubles : kPrefDoubles;
     const long long stride = (static_cast<long long>(hp_.ncell) + 5) & ~1LL;
-    double* t = pref_.ensure(static_cast<size_t>(n) * kPrefDoubles * stride + 4);
-    launch_sweep_prefactor(a, t + 2, stride, stream_);
+    double* t = pref_.ensure(static_cast<size_t>(n) * planes * stride + 4);
+    launch_sweep_prefactor(a, t + 2, stride, stream_, planes);
     a.pref = t + 2;
     a.pref_stride = stride;
+  }
+  if (choice == 4) {
+    launch_sweep_wave(a, hp_.sigma_t_uniform, cluster, stream_);
+    return;
   }
   launch_sweep_scan(a, hp_.sigma_t_uniform, stream_);
 }

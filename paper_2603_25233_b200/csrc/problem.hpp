@@ -173,7 +173,8 @@ class Problem {
   double pcg_rtol = 1e-13;
   int pcg_max_iters = 20000;
   bool pcg_multigrid = true;  // false: block-Jacobi PCG
-  int sweep_kernel = 0;  // 0 auto, 1 skewed wavefront (sweep.cu), 2 row scan, 3 row scan on prefactored blocks
+  int sweep_kernel = 0;  // 0 auto, 1 skewed wavefront (sweep.cu), 2 row scan, 3 row scan on prefactored blocks,
+                         // 4 cluster wavefront (few directions)
 
  private:
   friend class LowRankEngine;

@@ -35,6 +35,8 @@
 // full affine maps.
 #include <algorithm>
 #include <cmath>
+#include <stdexcept>
+#include <vector>
 
 #include "device.cuh"
 
@@ -580,6 +582,67 @@ __device__ __forceinline__ void sweep_dir(const Dir& d) {
   }
 }
 
+// Per-direction constants (kConsts layout above), written by one warp.
+template <bool UNIFORM>
+__device__ __forceinline__ void dir_consts(const SweepArgs& a, double omx, double omy, bool xu, bool yu, double* cst,
+                                           int lane) {
+  const double* ax = xu ? a.sc.ax_minus : a.sc.ax_plus;
+  const double* ay = yu ? a.sc.ay_minus : a.sc.ay_plus;
+  if (lane < 16) {
+    const double dv = omx * ax[lane] + omy * ay[lane];
+    cst[lane] = UNIFORM ? dv + a.sigma_t[lane] : dv;
+  }
+  if (lane < 2) {
+    // (B psi_up)[my,mx] = c[mx] (t . psi_up[my,:]), (c,t) = (-t_L,t_R) minus / (t_R,t_L) plus
+    cst[kKT + lane] = omx * (xu ? -a.sc.trx_l[lane] : a.sc.trx_r[lane]);
+    cst[kKT + 2 + lane] = xu ? a.sc.trx_r[lane] : a.sc.trx_l[lane];
+    cst[kKT + 4 + lane] = omy * (yu ? -a.sc.try_l[lane] : a.sc.try_r[lane]);
+    cst[kKT + 6 + lane] = yu ? a.sc.try_r[lane] : a.sc.try_l[lane];
+  }
+  __syncwarp();
+  if (UNIFORM && lane == 0) {
+    // M^-1 columns via the reference LU; Q = -M^-1 K_x; G = T_x Q; (G^2)^(l+1)
+    double Mi[16];
+    for (int c = 0; c < 4; c += 3) {
+      double A[16], e0[4] = {0, 0, 0, 0}, e1[4] = {0, 0, 0, 0}, e2[4] = {0, 0, 0, 0};
+      for (int k = 0; k < 16; ++k) A[k] = cst[k];
+      e0[c] = 1.0;
+      if (c + 1 < 4) e1[c + 1] = 1.0;
+      if (c + 2 < 4) e2[c + 2] = 1.0;
+      if (!lu_solve4x3(A, e0, e1, e2)) atomicExch(a.err, 1);
+      for (int r = 0; r < 4; ++r) {
+        Mi[c * 4 + r] = e0[r];
+        if (c + 1 < 4) Mi[(c + 1) * 4 + r] = e1[r];
+        if (c + 2 < 4) Mi[(c + 2) * 4 + r] = e2[r];
+      }
+    }
+    const double kx0 = cst[kKT], kx1 = cst[kKT + 1], tx0 = cst[kKT + 2], tx1 = cst[kKT + 3];
+    // K_x (4 x 2): column my has kx[mx] at rows (my, mx)
+    double Q[8];
+    for (int my = 0; my < 2; ++my)
+      for (int r = 0; r < 4; ++r)
+        Q[my * 4 + r] = -(Mi[(my * 2 + 0) * 4 + r] * kx0 + Mi[(my * 2 + 1) * 4 + r] * kx1);
+    // G = T_x Q (2 x 2): row m = tx . Q[(m,0..1), :]
+    double Gm[4];
+    for (int col = 0; col < 2; ++col)
+      for (int m = 0; m < 2; ++m) Gm[col * 2 + m] = tx0 * Q[col * 4 + m * 2] + tx1 * Q[col * 4 + m * 2 + 1];
+    for (int k = 0; k < 16; ++k) cst[k] = Mi[k];
+    for (int k = 0; k < 8; ++k) cst[kQ + k] = Q[k];
+    for (int e = 0; e < 4; ++e) cst[kG + e] = Gm[e];
+    double G2[4];
+    for (int col = 0; col < 2; ++col)
+      for (int m = 0; m < 2; ++m) G2[col * 2 + m] = Gm[m] * Gm[col * 2] + Gm[2 + m] * Gm[col * 2 + 1];
+    double P[4] = {G2[0], G2[1], G2[2], G2[3]};
+    for (int k = 0; k < 32; ++k) {
+      for (int e = 0; e < 4; ++e) cst[kGP + 4 * k + e] = P[e];
+      double N[4];
+      for (int col = 0; col < 2; ++col)
+        for (int m = 0; m < 2; ++m) N[col * 2 + m] = G2[m] * P[col * 2] + G2[2 + m] * P[col * 2 + 1];
+      for (int e = 0; e < 4; ++e) P[e] = N[e];
+    }
+  }
+}
+
 // nck: chunks per segment (kSplit); the trace lines then span one segment.
 template <bool UNIFORM, int MODE, bool HAS_BC>
 __global__ void __launch_bounds__(256, 2) sweep_scan_kernel(const SweepArgs a, int W, bool smem_lines, int nck) {
@@ -601,61 +664,7 @@ __global__ void __launch_bounds__(256, 2) sweep_scan_kernel(const SweepArgs a, i
   const double omx = a.dirs[3 * ang], omy = a.dirs[3 * ang + 1];
   const bool xu = omx >= 0.0, yu = omy >= 0.0;  // sweep.cpp:37-38
   if (w == 0) {
-    const double* ax = xu ? a.sc.ax_minus : a.sc.ax_plus;
-    const double* ay = yu ? a.sc.ay_minus : a.sc.ay_plus;
-    if (lane < 16) {
-      const double dv = omx * ax[lane] + omy * ay[lane];
-      cst[lane] = UNIFORM ? dv + a.sigma_t[lane] : dv;
-    }
-    if (lane < 2) {
-      // (B psi_up)[my,mx] = c[mx] (t . psi_up[my,:]), (c,t) = (-t_L,t_R) minus / (t_R,t_L) plus
-      cst[kKT + lane] = omx * (xu ? -a.sc.trx_l[lane] : a.sc.trx_r[lane]);
-      cst[kKT + 2 + lane] = xu ? a.sc.trx_r[lane] : a.sc.trx_l[lane];
-      cst[kKT + 4 + lane] = omy * (yu ? -a.sc.try_l[lane] : a.sc.try_r[lane]);
-      cst[kKT + 6 + lane] = yu ? a.sc.try_r[lane] : a.sc.try_l[lane];
-    }
-    __syncwarp();
-    if (UNIFORM && lane == 0) {
-      // M^-1 columns via the reference LU; Q = -M^-1 K_x; G = T_x Q; (G^2)^(l+1)
-      double Mi[16];
-      for (int c = 0; c < 4; c += 3) {
-        double A[16], e0[4] = {0, 0, 0, 0}, e1[4] = {0, 0, 0, 0}, e2[4] = {0, 0, 0, 0};
-        for (int k = 0; k < 16; ++k) A[k] = cst[k];
-        e0[c] = 1.0;
-        if (c + 1 < 4) e1[c + 1] = 1.0;
-        if (c + 2 < 4) e2[c + 2] = 1.0;
-        if (!lu_solve4x3(A, e0, e1, e2)) atomicExch(a.err, 1);
-        for (int r = 0; r < 4; ++r) {
-          Mi[c * 4 + r] = e0[r];
-          if (c + 1 < 4) Mi[(c + 1) * 4 + r] = e1[r];
-          if (c + 2 < 4) Mi[(c + 2) * 4 + r] = e2[r];
-        }
-      }
-      const double kx0 = cst[kKT], kx1 = cst[kKT + 1], tx0 = cst[kKT + 2], tx1 = cst[kKT + 3];
-      // K_x (4 x 2): column my has kx[mx] at rows (my, mx)
-      double Q[8];
-      for (int my = 0; my < 2; ++my)
-        for (int r = 0; r < 4; ++r)
-          Q[my * 4 + r] = -(Mi[(my * 2 + 0) * 4 + r] * kx0 + Mi[(my * 2 + 1) * 4 + r] * kx1);
-      // G = T_x Q (2 x 2): row m = tx . Q[(m,0..1), :]
-      double Gm[4];
-      for (int col = 0; col < 2; ++col)
-        for (int m = 0; m < 2; ++m) Gm[col * 2 + m] = tx0 * Q[col * 4 + m * 2] + tx1 * Q[col * 4 + m * 2 + 1];
-      for (int k = 0; k < 16; ++k) cst[k] = Mi[k];
-      for (int k = 0; k < 8; ++k) cst[kQ + k] = Q[k];
-      for (int e = 0; e < 4; ++e) cst[kG + e] = Gm[e];
-      double G2[4];
-      for (int col = 0; col < 2; ++col)
-        for (int m = 0; m < 2; ++m) G2[col * 2 + m] = Gm[m] * Gm[col * 2] + Gm[2 + m] * Gm[col * 2 + 1];
-      double P[4] = {G2[0], G2[1], G2[2], G2[3]};
-      for (int k = 0; k < 32; ++k) {
-        for (int e = 0; e < 4; ++e) cst[kGP + 4 * k + e] = P[e];
-        double N[4];
-        for (int col = 0; col < 2; ++col)
-          for (int m = 0; m < 2; ++m) N[col * 2 + m] = G2[m] * P[col * 2] + G2[2 + m] * P[col * 2 + 1];
-        for (int e = 0; e < 4; ++e) P[e] = N[e];
-      }
-    }
+    dir_consts<UNIFORM>(a, omx, omy, xu, yu, cst, lane);
     if (lane < W) prod[lane] = 0;
   }
   asm volatile("bar.sync %0, %1;" ::"r"(g + 1), "r"(W * 32) : "memory");
@@ -709,7 +718,7 @@ __global__ void __launch_bounds__(256, 2) sweep_scan_kernel(const SweepArgs a, i
 // partial-pivot LU (singular test as sweep.cpp:49-52), and written as M^-1,
 // Qc = -M^-1 K_x and G = T_x Qc, structure of arrays.
 __global__ void __launch_bounds__(256) sweep_prefactor_kernel(const SweepArgs a, double* __restrict__ table,
-                                                              long long stride) {
+                                                              long long stride, int planes) {
   const int slot = blockIdx.y;
   const long long c = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x;
   const long long ncell = static_cast<long long>(a.nx) * a.ny;
@@ -743,9 +752,10 @@ __global__ void __launch_bounds__(256) sweep_prefactor_kernel(const SweepArgs a,
   if (!ok) atomicExch(a.err, 1);
   const double kx0 = omx * (xu ? -a.sc.trx_l[0] : a.sc.trx_r[0]), kx1 = omx * (xu ? -a.sc.trx_l[1] : a.sc.trx_r[1]);
   const double tx0 = xu ? a.sc.trx_r[0] : a.sc.trx_l[0], tx1 = xu ? a.sc.trx_r[1] : a.sc.trx_l[1];
-  double* t = table + static_cast<long long>(slot) * kPrefDoubles * stride + c;
+  double* t = table + static_cast<long long>(slot) * planes * stride + c;
 #pragma unroll
   for (int k = 0; k < 16; ++k) t[k * stride] = Mi[k];
+  if (planes == kPrefMinvDoubles) return;  // the wavefront kernel forms Qc and G itself
   double Q[8];
 #pragma unroll
   for (int my = 0; my < 2; ++my)
@@ -760,6 +770,279 @@ __global__ void __launch_bounds__(256) sweep_prefactor_kernel(const SweepArgs a,
     for (int m = 0; m < 2; ++m) t[(24 + col * 2 + m) * stride] = tx0 * Q[col * 4 + m * 2] + tx1 * Q[col * 4 + m * 2 + 1];
 }
 
+// ---------------------------------------------------------------- wavefront mode
+// A few directions (the low-rank inner loop's p sampled directions) leave
+// the row-chunk kernel latency-bound: one SM per direction, every chunk step
+// (loads, LU-free block algebra, the scan) on the sweep DAG's critical path.
+// Here one direction runs on a thread-block cluster of CS CTAs x 8 warps;
+// global warp g (= rank*8 + warp) owns rows g, g + 8 CS, ...  Each 32-cell
+// chunk step is split: everything independent of the upwind row (the source
+// and block loads, u = M^-1 rhs, the y-coupling Qy = -M^-1 K_y, the scan's
+// transfer-matrix products level by level) runs before the wait; after the
+// previous row's traces arrive only the 2-vector scan, the carry and psi
+// remain.  The y-outflow traces go straight into the next row's warp's
+// shared memory (st.async into distributed shared memory, possibly another
+// CTA of the cluster), completing bytes on that warp's per-chunk mbarrier.
+constexpr int kWaveWarps = 8;
+constexpr size_t kWaveSmemMax = 220 * 1024;
+
+__device__ __forceinline__ unsigned cluster_ctarank() {
+  unsigned r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ unsigned map_cluster(unsigned saddr, unsigned rank) {
+  unsigned r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(saddr), "r"(rank));
+  return r;
+}
+__device__ __forceinline__ void cluster_barrier() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+// Row hand-off: the producer lanes push their y-outflow traces into the
+// consumer warp's shared memory with st.async, each completing 16 bytes of
+// transaction count on the consumer's per-chunk mbarrier; the consumer arms
+// the barrier with the chunk's byte count and waits on its phase parity.  No
+// fences on either side, and the wait is a hardware barrier test rather
+// than a polled flag.
+__device__ __forceinline__ void st_async_v2(unsigned addr, double x, double y, unsigned mbar) {
+  asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.v2.f64 [%0], {%1, %2}, [%3];" ::"r"(addr),
+               "d"(x), "d"(y), "r"(mbar)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_init(unsigned bar, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect(unsigned bar, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(unsigned bar, unsigned parity) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\tWAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+      "@!p bra WAIT_%=;\n\t}" ::"r"(bar),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void prefetch_line_l2(const double* p) {
+  asm volatile("prefetch.global.L2 [%0];" ::"l"(p));
+}
+__device__ __forceinline__ double shfl_i(double x, int src) { return shfl_idx_f64(x, src); }
+// 2 x 2 column-major products
+__device__ __forceinline__ void mm2(const double* A, const double* B, double* C) {
+  C[0] = A[0] * B[0] + A[2] * B[1];
+  C[1] = A[1] * B[0] + A[3] * B[1];
+  C[2] = A[0] * B[2] + A[2] * B[3];
+  C[3] = A[1] * B[2] + A[3] * B[3];
+}
+
+template <bool UNIFORM, bool HAS_BC>
+__global__ void __launch_bounds__(256, 1) sweep_wave_kernel(const SweepArgs a, int CS) {
+  extern __shared__ double smem[];
+  const int lane = threadIdx.x & 31;
+  const int wib = threadIdx.x >> 5;
+  const unsigned crank = cluster_ctarank();
+  const int slot = blockIdx.x / CS;
+  const int nx = a.nx, ny = a.ny;
+  const int nchunk = (nx + 31) / 32;
+  double* cst = smem;
+  unsigned long long* bars = reinterpret_cast<unsigned long long*>(smem + kConsts);  // kWaveWarps x nchunk
+  double* lines = smem + kConsts + kWaveWarps * nchunk;  // kWaveWarps x nx x (mode 0, mode 1)
+  const int ang = a.angles ? a.angles[slot] : slot;
+  const double omx = a.dirs[3 * ang], omy = a.dirs[3 * ang + 1];
+  const bool xu = omx >= 0.0, yu = omy >= 0.0;  // sweep.cpp:37-38
+  if (wib == 0) dir_consts<UNIFORM>(a, omx, omy, xu, yu, cst, lane);
+  for (int i = threadIdx.x; i < kWaveWarps * nchunk; i += blockDim.x) mbar_init(smem_u32(bars + i), 1);
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  cluster_barrier();  // constants and initialised barriers before any remote store
+
+  const int WT = CS * kWaveWarps;
+  const int g = static_cast<int>(crank) * kWaveWarps + wib;
+  const int gc = (g + 1) % WT;  // the warp owning the next row
+  const unsigned out_line = map_cluster(smem_u32(lines + static_cast<size_t>(gc % kWaveWarps) * 2 * nx),
+                                        static_cast<unsigned>(gc / kWaveWarps));
+  const unsigned out_bar = map_cluster(smem_u32(bars + static_cast<size_t>(gc % kWaveWarps) * nchunk),
+                                       static_cast<unsigned>(gc / kWaveWarps));
+  const unsigned my_bar = smem_u32(bars + static_cast<size_t>(wib) * nchunk);
+  const double* in_line = lines + static_cast<size_t>(wib) * 2 * nx;
+  const double* rhs = a.rhs + static_cast<long long>(slot) * a.rhs_stride;
+  const double* bc = HAS_BC ? a.bc + static_cast<long long>(ang) * a.bc_stride : nullptr;
+  double* psi = a.psi + static_cast<long long>(slot) * a.psi_stride;
+  const double* tb = UNIFORM ? nullptr : a.pref + static_cast<long long>(slot) * kPrefMinvDoubles * a.pref_stride;
+  const long long ps = a.pref_stride;
+  const double kx0 = cst[kKT], kx1 = cst[kKT + 1];
+  const double tx0 = cst[kKT + 2], tx1 = cst[kKT + 3];
+  const double ky0 = cst[kKT + 4], ky1 = cst[kKT + 5], ty0 = cst[kKT + 6], ty1 = cst[kKT + 7];
+  auto cell_of = [&](int r, int col) -> long long {
+    return static_cast<long long>(yu ? r : ny - 1 - r) * nx + (xu ? col : nx - 1 - col);
+  };
+  // L2 prefetch of the next chunk step's sources and block planes: 8 + 56
+  // lines of 128 B, two per lane (per-lane prefetches: no uniform-address loop)
+  auto prefetch = [&](int r, int k) {
+    if (r >= ny) return;
+    const int lo = k * 32, cnt = min(32, nx - lo);
+    const long long first = static_cast<long long>(yu ? r : ny - 1 - r) * nx + (xu ? lo : nx - lo - cnt);
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int i = lane + 32 * h;
+      if (i < 8) {
+        if (16 * i < 4 * cnt) prefetch_line_l2(rhs + 4 * first + 16 * i);
+      } else if (!UNIFORM && i < 8 + 2 * kPrefMinvDoubles) {
+        const int pl = (i - 8) >> 1, half = (i - 8) & 1;
+        if (16 * half < cnt) prefetch_line_l2(tb + pl * ps + first + 16 * half);
+      }
+    }
+    if (HAS_BC && lane < 8 && 16 * lane < 4 * cnt) prefetch_line_l2(bc + 4 * first + 16 * lane);
+  };
+
+  // Node q = (row ordinal j, chunk k) of this warp, row r = g + j WT.  The
+  // sources and block planes of node q + 1 load into registers before node
+  // q waits on its upwind row, so their latency hides behind the wait.
+  const int nrow_w = g < ny ? (ny - g + WT - 1) / WT : 0;
+  const int nodes = nrow_w * nchunk;
+  auto node_cell = [&](int q) -> long long {
+    const int col = (q % nchunk) * 32 + lane;
+    return cell_of(g + (q / nchunk) * WT, col < nx ? col : nx - 1);
+  };
+  double dv[4], dt[UNIFORM ? 1 : kPrefMinvDoubles];
+  auto load = [&](int q) {
+    const long long c = node_cell(q);
+    ld_cell256(rhs + 4 * c, dv);
+    if (HAS_BC) {
+      double gb[4];
+      ld_cell256(bc + 4 * c, gb);
+#pragma unroll
+      for (int i = 0; i < 4; ++i) dv[i] += gb[i];
+    }
+    if (!UNIFORM) {
+#pragma unroll
+      for (int e = 0; e < kPrefMinvDoubles; ++e) dt[e] = __ldg(tb + c + e * ps);
+    }
+  };
+  if (nodes > 0) load(0);
+  double tc0 = 0.0, tc1 = 0.0;  // x-inflow of the chunk (every lane holds it)
+  for (int q = 0; q < nodes; ++q) {
+    const int j = q / nchunk, k = q - j * nchunk, r = g + j * WT;
+    if (k == 0) tc0 = tc1 = 0.0;
+    const unsigned parity = static_cast<unsigned>(g == 0 ? j - 1 : j) & 1u;  // this row's phase of the barriers
+    {
+      const unsigned bytes = 16u * static_cast<unsigned>(min(32, nx - 32 * k));
+      if (r > 0 && lane == 0) mbar_expect(my_bar + 8u * k, bytes);
+      if (q + 2 < nodes) {
+        const int q2 = q + 2, j2 = q2 / nchunk;
+        prefetch(g + j2 * WT, q2 - j2 * nchunk);
+      }
+      const int col = k * 32 + lane;
+      const bool act = col < nx;
+      const long long cell = cell_of(r, act ? col : nx - 1);
+      // ---- independent of the upwind row
+      double v[4] = {dv[0], dv[1], dv[2], dv[3]};
+      double Mi[16], Qc[8], G[4];
+      if (UNIFORM) {
+#pragma unroll
+        for (int e = 0; e < 16; ++e) Mi[e] = cst[e];
+#pragma unroll
+        for (int e = 0; e < 8; ++e) Qc[e] = cst[kQ + e];
+#pragma unroll
+        for (int e = 0; e < 4; ++e) G[e] = cst[kG + e];
+      } else {
+#pragma unroll
+        for (int e = 0; e < 16; ++e) Mi[e] = dt[e];
+        // Qc = -M^-1 K_x, G = T_x Qc (as sweep_prefactor_kernel)
+#pragma unroll
+        for (int my = 0; my < 2; ++my)
+#pragma unroll
+          for (int i = 0; i < 4; ++i) Qc[my * 4 + i] = -(Mi[(my * 2 + 0) * 4 + i] * kx0 + Mi[(my * 2 + 1) * 4 + i] * kx1);
+#pragma unroll
+        for (int c = 0; c < 2; ++c)
+#pragma unroll
+          for (int m = 0; m < 2; ++m) G[c * 2 + m] = tx0 * Qc[c * 4 + m * 2] + tx1 * Qc[c * 4 + m * 2 + 1];
+      }
+      // u = M^-1 rhs; Qy = -M^-1 K_y (K_y: column mx has ky[my] at rows (my, mx))
+      double u[4], Qy[8];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        u[i] = Mi[i] * v[0] + Mi[4 + i] * v[1] + Mi[8 + i] * v[2] + Mi[12 + i] * v[3];
+        Qy[i] = -(ky0 * Mi[i] + ky1 * Mi[8 + i]);
+        Qy[4 + i] = -(ky0 * Mi[4 + i] + ky1 * Mi[12 + i]);
+      }
+      // f = T_x u + Gy y, Gy = T_x Qy (rows: y-mode)
+      double f0 = tx0 * u[0] + tx1 * u[1], f1 = tx0 * u[2] + tx1 * u[3];
+      double Gy[4] = {tx0 * Qy[0] + tx1 * Qy[1], tx0 * Qy[2] + tx1 * Qy[3], tx0 * Qy[4] + tx1 * Qy[5],
+                      tx0 * Qy[6] + tx1 * Qy[7]};
+      if (q + 1 < nodes) load(q + 1);  // (v and the planes are consumed)
+      if (!act) {  // past the row end (last in sweep order): the zero map
+        f0 = f1 = 0.0;
+#pragma unroll
+        for (int e = 0; e < 4; ++e) G[e] = Gy[e] = 0.0;
+      }
+      // transfer-matrix scan: A_l before each level, the lane's prefix map after
+      double Al[5][4], A[4] = {G[0], G[1], G[2], G[3]};
+#pragma unroll
+      for (int l = 0; l < 5; ++l) {
+        const int dd = 1 << l;
+        const bool in = lane >= dd;
+#pragma unroll
+        for (int e = 0; e < 4; ++e) Al[l][e] = A[e];
+        double P[4];
+#pragma unroll
+        for (int e = 0; e < 4; ++e) P[e] = shfl_up_f64(A[e], dd);
+        if (!in) P[0] = 1.0, P[1] = 0.0, P[2] = 0.0, P[3] = 1.0;
+        double N[4];
+        mm2(A, P, N);
+#pragma unroll
+        for (int e = 0; e < 4; ++e) A[e] = N[e];
+      }
+      const int src = (lane + 31) & 31;
+      double rA[4], A31[4];
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        rA[e] = shfl_i(A[e], src);
+        A31[e] = shfl_i(A[e], 31);
+      }
+      if (lane == 0) rA[0] = 1.0, rA[1] = 0.0, rA[2] = 0.0, rA[3] = 1.0;
+      // ---- the previous row's traces
+      double y0 = 0.0, y1 = 0.0;
+      if (r > 0) {
+        mbar_wait(my_bar + 8u * k, parity);
+        if (act) {
+          const double2 t2 = ld_line(in_line + 2 * col, true);
+          y0 = t2.x;
+          y1 = t2.y;
+        }
+      }
+      // ---- dependent part
+      double s0 = f0 + Gy[0] * y0 + Gy[2] * y1, s1 = f1 + Gy[1] * y0 + Gy[3] * y1;
+#pragma unroll
+      for (int l = 0; l < 5; ++l) {
+        const int dd = 1 << l;
+        double o0 = shfl_up_f64(s0, dd), o1 = shfl_up_f64(s1, dd);
+        o0 = lane >= dd ? o0 : 0.0;
+        o1 = lane >= dd ? o1 : 0.0;
+        s0 += Al[l][0] * o0 + Al[l][2] * o1;
+        s1 += Al[l][1] * o0 + Al[l][3] * o1;
+      }
+      double rs0 = shfl_i(s0, src), rs1 = shfl_i(s1, src);
+      const double e0 = shfl_i(s0, 31), e1 = shfl_i(s1, 31);
+      if (lane == 0) rs0 = rs1 = 0.0;
+      const double ti0 = rs0 + rA[0] * tc0 + rA[2] * tc1, ti1 = rs1 + rA[1] * tc0 + rA[3] * tc1;
+      const double n0 = e0 + A31[0] * tc0 + A31[2] * tc1, n1 = e1 + A31[1] * tc0 + A31[3] * tc1;
+      tc0 = n0;
+      tc1 = n1;
+      double p[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) p[i] = u[i] + Qy[i] * y0 + Qy[4 + i] * y1 + Qc[i] * ti0 + Qc[4 + i] * ti1;
+      if (act) {
+        st_cell256(psi + 4 * cell, p);
+        if (r + 1 < ny)
+          st_async_v2(out_line + 16u * static_cast<unsigned>(col), ty0 * p[0] + ty1 * p[2], ty0 * p[1] + ty1 * p[3],
+                      out_bar + 8u * k);
+      }
+    }
+  }
+  cluster_barrier();  // (every hand-off was consumed; the CTAs leave together)
+}
+
 int sm_count() {
   static const int n = [] {
     int dev = 0, v = 148;
@@ -771,10 +1054,12 @@ int sm_count() {
 
 }  // namespace
 
-void launch_sweep_prefactor(const SweepArgs& a, double* table, long long stride, cudaStream_t s) {
+void launch_sweep_prefactor(const SweepArgs& a, double* table, long long stride, cudaStream_t s, int planes) {
   if (a.n <= 0) return;
+  if (planes != kPrefDoubles && planes != kPrefMinvDoubles) throw std::invalid_argument("sweep_prefactor: planes");
   const long long ncell = static_cast<long long>(a.nx) * a.ny;
-  sweep_prefactor_kernel<<<dim3(static_cast<unsigned>((ncell + 255) / 256), a.n), 256, 0, s>>>(a, table, stride);
+  sweep_prefactor_kernel<<<dim3(static_cast<unsigned>((ncell + 255) / 256), a.n), 256, 0, s>>>(a, table, stride,
+                                                                                               planes);
   RTLR_CUDA(cudaGetLastError());
 }
 
@@ -844,6 +1129,83 @@ void launch_sweep_scan(const SweepArgs& a, bool uniform, cudaStream_t s) {
     else RTLR_SCAN_GO(false, kOne);
   }
 #undef RTLR_SCAN_GO
+  RTLR_CUDA(cudaGetLastError());
+}
+
+
+namespace {
+
+size_t wave_smem(int nx) {
+  const int nchunk = (nx + 31) / 32;
+  return (kConsts + static_cast<size_t>(kWaveWarps) * nchunk + static_cast<size_t>(kWaveWarps) * 2 * nx) *
+         sizeof(double);
+}
+
+template <class F>
+void wave_dispatch(bool uniform, bool bc, F&& go) {
+  if (uniform)
+    bc ? go(sweep_wave_kernel<true, true>) : go(sweep_wave_kernel<true, false>);
+  else
+    bc ? go(sweep_wave_kernel<false, true>) : go(sweep_wave_kernel<false, false>);
+}
+
+template <class K>
+cudaLaunchConfig_t wave_config(K kern, int cluster, int nclusters, size_t smem, cudaStream_t s,
+                               cudaLaunchAttribute* at) {
+  RTLR_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+  if (cluster > 8) RTLR_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(static_cast<unsigned>(nclusters) * cluster);
+  cfg.blockDim = dim3(kWaveWarps * 32);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = cluster;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  return cfg;
+}
+
+}  // namespace
+
+int sweep_wave_cluster(const SweepArgs& a, bool uniform) {
+  if (a.n <= 0 || wave_smem(a.nx) > kWaveSmemMax) return 0;
+  // Largest cluster (8, 4, 2 CTAs) of which all n fit on the GPU at once
+  // (the query accounts for GPC placement); cached per kernel and row width.
+  static std::vector<std::pair<long long, int>> cache;  // key -> max active clusters
+  const bool bc = a.bc != nullptr;
+  for (int cs = 8; cs >= 2; cs /= 2) {
+    const long long key = ((static_cast<long long>(a.nx) * 4 + (uniform ? 2 : 0) + (bc ? 1 : 0)) << 5) | cs;
+    int fit = -1;
+    for (auto& e : cache)
+      if (e.first == key) fit = e.second;
+    if (fit < 0) {
+      wave_dispatch(uniform, bc, [&](auto kern) {
+        cudaLaunchAttribute at[1];
+        const cudaLaunchConfig_t cfg = wave_config(kern, cs, 1, wave_smem(a.nx), nullptr, at);
+        RTLR_CUDA(cudaOccupancyMaxActiveClusters(&fit, kern, &cfg));
+      });
+      cache.push_back({key, fit});
+    }
+    if (fit >= a.n) return cs;
+  }
+  return 0;
+}
+
+void launch_sweep_wave(const SweepArgs& a, bool uniform, int cluster, cudaStream_t s) {
+  if (a.n <= 0) return;
+  if (!uniform && a.pref == nullptr) throw std::logic_error("sweep_wave: general media need the M^-1 table");
+  if (cluster == 0) cluster = sweep_wave_cluster(a, uniform);
+  if (cluster < 1 || cluster > 16) throw std::invalid_argument("sweep_wave: cluster size must be 1..16");
+  const size_t smem = wave_smem(a.nx);
+  if (smem > kWaveSmemMax) throw std::invalid_argument("sweep_wave: rows too wide for the shared-memory trace lines");
+  wave_dispatch(uniform, a.bc != nullptr, [&](auto kern) {
+    cudaLaunchAttribute at[1];
+    const cudaLaunchConfig_t cfg = wave_config(kern, cluster, a.n, smem, s, at);
+    RTLR_CUDA(cudaLaunchKernelEx(&cfg, kern, a, cluster));
+  });
   RTLR_CUDA(cudaGetLastError());
 }
 

@@ -30,12 +30,13 @@ SWEEP_CASES = [
 ]
 
 
-@pytest.mark.parametrize("kernel", [1, 2, 3], ids=["skew", "scan", "scan-prefactored"])
+@pytest.mark.parametrize("kernel", [1, 2, 3, 4], ids=["skew", "scan", "scan-prefactored", "cluster-wave"])
 @pytest.mark.parametrize("name,ov", SWEEP_CASES)
 def test_sweep_matches_oracle(name, ov, kernel):
     """Every K1 path (the skewed wavefront, sweep_kernel = 1; the row scan, 2;
     the row scan on prefactored cell blocks, 3 — heterogeneous media with an
-    even nx, else it runs 2), uniform and heterogeneous media, ragged grids."""
+    even nx, else it runs 2; the cluster wavefront, 4), uniform and
+    heterogeneous media, ragged grids."""
     o = O.Problem(name, use_dsa=0, **ov)
     g = P.Problem(name, use_dsa=0, **ov)
     g.set_option("sweep_kernel", kernel)
@@ -52,6 +53,28 @@ def test_sweep_matches_oracle(name, ov, kernel):
     psi2 = g.sweep(np.arange(n), src)
     for j in range(0, n, max(1, n // 8)):
         assert rel(psi2[:, j], o.sweep(d[j, 0], d[j, 1], src)) <= 1e-12
+
+
+@pytest.mark.parametrize("kernel", [1, 2, 3, 4], ids=["skew", "scan", "scan-prefactored", "cluster-wave"])
+@pytest.mark.parametrize("name,ov", [
+    ("homogeneous(1,1)", {"nx": 33, "ny": 20, "n_theta": 4, "n_omega_z": 2, "boundary_const": 1.0}),
+    ("C4", {"nx": 64, "ny": 70, "n_theta": 4, "n_omega_z": 2, "boundary_const": 0.5}),
+])
+def test_sweep_inflow_matches_oracle(name, ov, kernel):
+    """Inflow boundary data enters every K1 path as a per-angle source
+    (sweep.cpp's rhs + g_j): GPU sweep of rhs against the oracle's sweep of
+    rhs + boundary_vector."""
+    o = O.Problem(name, use_dsa=0, **ov)
+    g = P.Problem(name, use_dsa=0, **ov)
+    g.set_option("sweep_kernel", kernel)
+    rng = np.random.default_rng(5)
+    d = g.get("dirs")
+    n = g.n_omega
+    rhs = rng.standard_normal((g.n, n))
+    psi = g.sweep(np.arange(n), rhs)
+    for j in range(n):
+        ref = o.sweep(d[j, 0], d[j, 1], rhs[:, j] + o.boundary_vector(d[j, 0], d[j, 1]))
+        assert rel(psi[:, j], ref) <= 1e-12, (j, rel(psi[:, j], ref))
 
 
 def test_sweep_zero_rhs_exact_zero():  # test_sweep.cpp:34-42
