@@ -34,9 +34,14 @@
 // (first maximum, singular test min|U_ii| <= 1e-14 max|block|) and scan the
 // full affine maps.
 #include <algorithm>
+#include <cstdint>
+#include <cstdlib>
+#include <cstring>
 #include <cmath>
 #include <stdexcept>
 #include <vector>
+
+#include <cuda.h>  // CUtensorMap (the encoder is fetched through the runtime)
 
 #include "device.cuh"
 
@@ -205,11 +210,45 @@ __device__ __forceinline__ void fma2(double& s0, double& s1, double2 p01, double
   s1 = fma(p23.y, o1, fma(p01.y, o0, s1));
 }
 
+// mbarrier and TMA primitives (shared-memory addresses as 32-bit offsets).
+__device__ __forceinline__ void mbar_init(unsigned bar, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect(unsigned bar, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(unsigned bar, unsigned parity) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\tWAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+      "@!p bra WAIT_%=;\n\t}" ::"r"(bar),
+      "r"(parity)
+      : "memory");
+}
+// One 2-D tile (16 rows of 128 B) of the source tensor into shared memory,
+// completing its bytes on bar.
+__device__ __forceinline__ void tma_load_tile(unsigned dst, const CUtensorMap* map, unsigned bar, int row) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4}], [%2];" ::"r"(dst),
+      "l"(map), "r"(bar), "r"(0), "r"(row)
+      : "memory");
+}
+__device__ __forceinline__ void ld_shared_v2(unsigned addr, double& x, double& y) {
+  asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];" : "=d"(x), "=d"(y) : "r"(addr) : "memory");
+}
+
 constexpr int kLineSmemBudget = 96 * 1024;  // bytes of trace lines per block kept in smem
 constexpr int kWarps = 8;                   // warps per block
 constexpr int kCpl = 2;                     // adjacent cells per lane
 constexpr int kChunk = 32 * kCpl;           // cells per warp step
 constexpr int kAheadChunks = 4;             // minimum L2 prefetch distance (chunks)
+// Wide uniform kernel (sweep_dir_wide): four adjacent cells per lane, 128-cell
+// chunks, sources through a per-warp TMA ring of 4 KB tiles (32 rows of
+// 128 B, 128-byte swizzle: the lanes' 16-byte reads are bank-conflict free).
+constexpr int kWCpl = 4;
+constexpr int kWChunk = 32 * kWCpl;
+constexpr int kWTileBytes = kWChunk * 32;
+constexpr int kMaxStages = 6;
 
 // Per-direction constants (shared memory, written by warp 0 of the group):
 //   [0..16)   M^-1 (uniform) or Omega_x Ax + Omega_y Ay (general), column-major
@@ -221,8 +260,10 @@ constexpr int kKT = 16, kQ = 24, kG = 32, kGP = 36, kConsts = 164;
 
 // Doubles per trace plane (even, so both planes stay 16-byte aligned).
 __host__ __device__ constexpr int line_pitch(int nx) { return (nx + 1) & ~1; }
-__host__ __device__ constexpr int group_doubles(int W, int nx, bool smem_lines) {
-  return kConsts + 2 * ((W + 3) / 4) + (smem_lines ? W * 2 * line_pitch(nx) : 0);
+// (the wide kernel reads and writes four columns at a time: multiple of 4)
+__host__ __device__ constexpr int line_pitch_w(int nx, bool wide) { return wide ? (nx + 3) & ~3 : line_pitch(nx); }
+__host__ __device__ constexpr int group_doubles(int W, int nx, bool smem_lines, bool wide = false) {
+  return kConsts + 2 * ((W + 3) / 4) + (smem_lines ? W * 2 * line_pitch_w(nx, wide) : 0);
 }
 
 __device__ __forceinline__ void mat2_vec(const double* G, double x0, double x1, double& y0, double& y1) {
@@ -251,6 +292,10 @@ struct Dir {
   const double* pref;  // general media: this direction's prefactored block data (or nullptr)
   long long pref_stride;
   int* err;
+  const CUtensorMap* tmap;  // wide: the source tensor (rows of 128 B)
+  unsigned ring, bars;      // wide: this warp's ring tiles and mbarriers (shared memory)
+  long long src_row0;       // wide: first tensor row of this direction's sources
+  int stages;               // wide: ring depth
   int nx, ny, W, w, pw, nchunk, nrows, pitch;
   int rw, rW;         // row interleave: rows rw, rw + rW, ... (kRows: w, W; else 0, 1)
   int kbeg, kend;     // this warp's chunk range within a row
@@ -310,6 +355,16 @@ __device__ __forceinline__ void sweep_dir(const Dir& d) {
   int rowk = 0, k = kbeg;
   double tc0 = 0.0, tc1 = 0.0;  // x-trace carry into the chunk (lane 0)
 
+  // Uniform media: the per-direction constants live in registers for the
+  // whole sweep (the kernel runs one block per SM for this).  Read from
+  // shared memory every step they were ~half of the L1 data-pipe wavefronts,
+  // the limiter once the power cap pulls the SM clock down.
+  double2 creg[UNIFORM ? kConsts / 2 : 1];
+  if (UNIFORM) {
+#pragma unroll
+    for (int i = 0; i < (UNIFORM ? kConsts / 2 : 1); ++i) creg[i] = c2[i];
+  }
+  auto C2 = [&](int i) -> double2 { return UNIFORM ? creg[UNIFORM ? i : 0] : c2[i]; };
   double ra0[4], ra1[4], rb0[4], rb1[4];  // two register sets of sources
   if (colbase + c0 < nx) ld_cell256(d.rhs + 4 * cell, ra0);
   if (colbase + c0 + 1 < nx) ld_cell256(d.rhs + 4 * (cell + kDx), ra1);
@@ -379,7 +434,7 @@ __device__ __forceinline__ void sweep_dir(const Dir& d) {
       double u0[4], u1[4];
 #pragma unroll
       for (int c = 0; c < 4; ++c) {  // u = M^-1 v, column by column
-        const double2 lo = c2[2 * c], hi = c2[2 * c + 1];
+        const double2 lo = C2(2 * c), hi = C2(2 * c + 1);
         if (c == 0) {
           u0[0] = lo.x * v0[0], u0[1] = lo.y * v0[0], u0[2] = hi.x * v0[0], u0[3] = hi.y * v0[0];
           u1[0] = lo.x * v1[0], u1[1] = lo.y * v1[0], u1[2] = hi.x * v1[0], u1[3] = hi.y * v1[0];
@@ -392,10 +447,10 @@ __device__ __forceinline__ void sweep_dir(const Dir& d) {
       // lane 0 also applies its map to the chunk's carry.
       const double f00 = tx0 * u0[0] + tx1 * u0[1], f01 = tx0 * u0[2] + tx1 * u0[3];
       const double f10 = tx0 * u1[0] + tx1 * u1[1], f11 = tx0 * u1[2] + tx1 * u1[3];
-      const double2 g01 = c2[kG / 2], g23 = c2[kG / 2 + 1];
+      const double2 g01 = C2(kG / 2), g23 = C2(kG / 2 + 1);
       double s0 = f10 + g01.x * f00 + g23.x * f01;
       double s1 = f11 + g01.y * f00 + g23.y * f01;
-      fma2(s0, s1, c2[kGP / 2], c2[kGP / 2 + 1], tc0, tc1);  // tc = 0 off lane 0
+      fma2(s0, s1, C2(kGP / 2), C2(kGP / 2 + 1), tc0, tc1);  // tc = 0 off lane 0
       // inclusive scan over the lanes: s_l <- s_l + G^(2d) s_{l-d}
 #pragma unroll
       for (int l = 0; l < 5; ++l) {
@@ -404,7 +459,7 @@ __device__ __forceinline__ void sweep_dir(const Dir& d) {
         double o1 = shfl_up_f64(s1, dd);
         o0 = lane >= dd ? o0 : 0.0;
         o1 = lane >= dd ? o1 : 0.0;
-        fma2(s0, s1, c2[(kGP + 4 * (dd - 1)) / 2], c2[(kGP + 4 * (dd - 1)) / 2 + 1], o0, o1);
+        fma2(s0, s1, C2((kGP + 4 * (dd - 1)) / 2), C2((kGP + 4 * (dd - 1)) / 2 + 1), o0, o1);
       }
       // One rotation: lane l > 0 receives tau_in from lane l-1; lane 0
       // receives lane 31's tau, the next chunk's carry (only lane 0 keeps one).
@@ -419,7 +474,7 @@ __device__ __forceinline__ void sweep_dir(const Dir& d) {
       const double m0 = f00 + g01.x * ti0 + g23.x * ti1, m1 = f01 + g01.y * ti0 + g23.y * ti1;
 #pragma unroll
       for (int h = 0; h < 2; ++h) {
-        const double2 qa = c2[kQ / 2 + h], qb = c2[kQ / 2 + 2 + h];  // Q[2h..2h+1], Q[4+2h..]
+        const double2 qa = C2(kQ / 2 + h), qb = C2(kQ / 2 + 2 + h);  // Q[2h..2h+1], Q[4+2h..]
         ps0[2 * h] = u0[2 * h] + qa.x * ti0 + qb.x * ti1;
         ps0[2 * h + 1] = u0[2 * h + 1] + qa.y * ti0 + qb.y * ti1;
         ps1[2 * h] = u1[2 * h] + qa.x * m0 + qb.x * m1;
@@ -582,6 +637,239 @@ __device__ __forceinline__ void sweep_dir(const Dir& d) {
   }
 }
 
+// The uniform-medium sweep with four adjacent cells per lane (128-cell
+// chunks): the per-direction constants live in registers, the sources
+// arrive through a TMA ring (lane 0 keeps `stages` tiles in flight), and a
+// lane composes its four cells' maps by Horner (tau -> G^4 tau + s), so the
+// 5-level shuffle scan and the carry rotation are paid once per 128 cells.
+// Trace lines are always in shared memory.  Same DAG, progress counters and
+// column-split carries as sweep_dir.
+template <int MODE, bool HAS_BC, bool XU>
+__device__ __forceinline__ void sweep_dir_wide(const Dir& d) {
+  constexpr bool MULTI = MODE == kRows, SPLIT = MODE == kSplit;
+  constexpr int kDx = XU ? 1 : -1;
+  constexpr int C = kWCpl;
+  const int lane = threadIdx.x & 31;
+  const int nx = d.nx, nrows = d.nrows, kbeg = d.kbeg, kend = d.kend;
+  const int nchunk = kend - kbeg;
+  const int colbase = kbeg * kWChunk;
+  const int c0 = C * lane;
+  const double* cs = d.cst;
+  double Mi[16], Q[8], G[4], L[5][4];
+#pragma unroll
+  for (int k = 0; k < 16; ++k) Mi[k] = cs[k];
+#pragma unroll
+  for (int k = 0; k < 8; ++k) Q[k] = cs[kQ + k];
+#pragma unroll
+  for (int k = 0; k < 4; ++k) G[k] = cs[kG + k];
+#pragma unroll
+  for (int l = 0; l < 5; ++l)  // G^(4 d), d = 2^l: entry 2d - 1 of the G^(2(i+1)) table
+#pragma unroll
+    for (int k = 0; k < 4; ++k) L[l][k] = cs[kGP + 4 * ((2 << l) - 1) + k];
+  const double tx0 = cs[kKT + 2], tx1 = cs[kKT + 3];
+  const double ky0 = cs[kKT + 4], ky1 = cs[kKT + 5], ty0 = cs[kKT + 6], ty1 = cs[kKT + 7];
+
+  auto row0_of = [&](int rowk) -> long long {
+    const int r = d.rw + rowk * d.rW;
+    return static_cast<long long>(d.yu ? r : d.ny - 1 - r) * nx;
+  };
+  auto first_cell = [&](int rowk) -> long long {
+    return row0_of(rowk) + (XU ? colbase + c0 : nx - 1 - colbase - c0);
+  };
+  const int nsteps = nrows * nchunk;
+  const int S = d.stages;
+
+  // TMA producer (lane 0): (trow, tk) walks the chunks in sweep order; a
+  // tile starts at its chunk's first cell in memory order (the box may run
+  // past the row; rows past the tensor are zero-filled).  With inflow data
+  // the chunk's bc cells are prefetched into L2 alongside.
+  int tissued = 0, trow = 0, tk = kbeg, ist = 0;
+  long long trow0 = row0_of(0);
+  auto tma_issue = [&]() {
+    if (tissued >= nsteps) return;
+    const int lo = tk * kWChunk;
+    const long long first = trow0 + (XU ? lo : nx - lo - kWChunk);  // multiple of 4 cells
+    const unsigned bar = d.bars + 8u * ist;
+    mbar_expect(bar, kWTileBytes);
+    tma_load_tile(d.ring + ist * kWTileBytes, d.tmap, bar, static_cast<int>(d.src_row0 + first / 4));
+    if (HAS_BC) {
+      const int cnt = min(kWChunk, nx - lo);
+      prefetch_l2(d.bc + 4 * (trow0 + (XU ? lo : nx - lo - cnt)), static_cast<unsigned>(cnt) * 32u);
+    }
+    if (++ist == S) ist = 0;
+    ++tissued;
+    if (++tk == kend) {
+      tk = kbeg;
+      if (++trow < nrows) trow0 = row0_of(trow);
+    }
+  };
+  if (lane == 0)
+    for (int u = 0; u < S; ++u) tma_issue();
+  // this lane's cells in a tile: memory index m -> 128-B row m / 4 (the same
+  // row for all four: XU ? lane : 31 - lane), 16-B unit 2 (m % 4) + h,
+  // swizzled by the row (CU_TENSOR_MAP_SWIZZLE_128B)
+  const int trw = XU ? lane : 31 - lane;
+  const unsigned tbase = static_cast<unsigned>(trw * 128), tsw = static_cast<unsigned>(trw & 7);
+  auto unit = [&](int c, int h) -> unsigned {
+    const unsigned u = static_cast<unsigned>(2 * (XU ? c : 3 - c) + h);
+    return tbase + ((u ^ tsw) << 4);
+  };
+
+  long long cell = first_cell(0);
+  long long next_row = nrows > 1 ? first_cell(1) : 0;
+  int rowk = 0, k = kbeg, st = 0;
+  unsigned ph = 0;
+  double tc0 = 0.0, tc1 = 0.0;  // x-trace carry into the chunk (lane 0)
+
+  for (int t = 0; t < nsteps; ++t) {
+    const int col = k * kWChunk + c0;
+    bool act[C];
+#pragma unroll
+    for (int c = 0; c < C; ++c) act[c] = col + c < nx;
+    const bool last = k + 1 == kend;
+    double v[C][4];
+    {
+      mbar_wait(d.bars + 8u * st, ph);
+      const unsigned tile = d.ring + st * kWTileBytes;
+#pragma unroll
+      for (int c = 0; c < C; ++c) {
+        ld_shared_v2(tile + unit(c, 0), v[c][0], v[c][1]);
+        ld_shared_v2(tile + unit(c, 1), v[c][2], v[c][3]);
+      }
+    }
+    if (k == kbeg) {  // x-inflow of the row (segment): vacuum, or warp s-1's boundary carry
+      tc0 = tc1 = 0.0;
+      if (SPLIT && d.w > 0) {
+        if (lane == 0) {
+          wait_progress(d.prod + d.w - 1, rowk + 1);
+          const double2 cin = __ldcg(reinterpret_cast<const double2*>(d.carry) + (d.w - 1) * d.ny + rowk);
+          tc0 = cin.x;
+          tc1 = cin.y;
+        }
+        __syncwarp();
+      }
+    }
+    if (HAS_BC) {
+#pragma unroll
+      for (int c = 0; c < C; ++c) {
+        double g[4];
+        if (act[c]) {
+          ld_cell256(d.bc + 4 * (cell + kDx * c), g);
+#pragma unroll
+          for (int i = 0; i < 4; ++i) v[c][i] += g[i];
+        }
+      }
+    }
+    // y-upwind traces (per x-mode) of these columns from the previous row
+    double y[C][2];
+#pragma unroll
+    for (int c = 0; c < C; ++c) y[c][0] = y[c][1] = 0.0;
+    if (d.rw + rowk * d.rW > 0) {
+      if (MULTI) {
+        if (lane == 0) wait_progress(d.prod + d.pw, (d.w == 0 ? rowk - 1 : rowk) * nchunk + k + 1);
+        __syncwarp();
+      }
+      if (act[0]) {
+        const double* p0 = d.in_line + (col - colbase);
+#pragma unroll
+        for (int pl = 0; pl < 2; ++pl) {
+          const unsigned a0 = smem_u32(p0 + pl * d.pitch);
+          ld_shared_v2(a0, y[0][pl], y[1][pl]);
+          ld_shared_v2(a0 + 16u, y[2][pl], y[3][pl]);
+        }
+#pragma unroll
+        for (int c = 1; c < C; ++c)  // columns past the row end hold stale values
+          if (!act[c]) y[c][0] = y[c][1] = 0.0;
+      }
+    }
+    // u = M^-1 (rhs - Omega_y By psi_y); f = T_x u (per y-mode)
+    double u[C][4], f[C][2];
+#pragma unroll
+    for (int c = 0; c < C; ++c) {
+      const double w0 = v[c][0] - ky0 * y[c][0], w1 = v[c][1] - ky0 * y[c][1];
+      const double w2 = v[c][2] - ky1 * y[c][0], w3 = v[c][3] - ky1 * y[c][1];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) u[c][i] = Mi[i] * w0 + Mi[4 + i] * w1 + Mi[8 + i] * w2 + Mi[12 + i] * w3;
+      f[c][0] = tx0 * u[c][0] + tx1 * u[c][1];
+      f[c][1] = tx0 * u[c][2] + tx1 * u[c][3];
+    }
+    // lane map tau -> G^4 tau + s (Horner over the four cells); lane 0 also
+    // applies it to the chunk's carry
+    double s0 = f[0][0], s1 = f[0][1];
+#pragma unroll
+    for (int c = 1; c < C; ++c) {
+      const double n0 = f[c][0] + G[0] * s0 + G[2] * s1;
+      const double n1 = f[c][1] + G[1] * s0 + G[3] * s1;
+      s0 = n0;
+      s1 = n1;
+    }
+    fma2(s0, s1, make_double2(L[0][0], L[0][1]), make_double2(L[0][2], L[0][3]), tc0, tc1);  // tc = 0 off lane 0
+#pragma unroll
+    for (int l = 0; l < 5; ++l) {
+      const int dd = 1 << l;
+      double o0 = shfl_up_f64(s0, dd);
+      double o1 = shfl_up_f64(s1, dd);
+      o0 = lane >= dd ? o0 : 0.0;
+      o1 = lane >= dd ? o1 : 0.0;
+      fma2(s0, s1, make_double2(L[l][0], L[l][1]), make_double2(L[l][2], L[l][3]), o0, o1);
+    }
+    double ti0 = shfl_idx_f64(s0, (lane + 31) & 31);
+    double ti1 = shfl_idx_f64(s1, (lane + 31) & 31);
+    if (lane == 0) {
+      const double n0 = ti0, n1 = ti1;
+      ti0 = tc0, ti1 = tc1;
+      tc0 = n0, tc1 = n1;
+    }
+    // psi_c = u_c + Q tau, tau <- G tau + f_c, cell by cell
+    double ps[C][4];
+#pragma unroll
+    for (int c = 0; c < C; ++c) {
+#pragma unroll
+      for (int i = 0; i < 4; ++i) ps[c][i] = u[c][i] + Q[i] * ti0 + Q[4 + i] * ti1;
+      if (c + 1 < C) {
+        const double n0 = f[c][0] + G[0] * ti0 + G[2] * ti1;
+        const double n1 = f[c][1] + G[1] * ti0 + G[3] * ti1;
+        ti0 = n0;
+        ti1 = n1;
+      }
+    }
+#pragma unroll
+    for (int c = 0; c < C; ++c)
+      if (act[c]) st_cell256(d.psi + 4 * (cell + kDx * c), ps[c]);
+    if (act[0]) {  // y-outflow traces (per x-mode) for the next row
+      double* q0 = d.my_line + (col - colbase);
+#pragma unroll
+      for (int pl = 0; pl < 2; ++pl) {
+        double o[C];
+#pragma unroll
+        for (int c = 0; c < C; ++c) o[c] = ty0 * ps[c][pl] + ty1 * ps[c][2 + pl];
+        st_line(q0 + pl * d.pitch, o[0], o[1], true);
+        st_line(q0 + pl * d.pitch + 2, o[2], o[3], true);
+      }
+    }
+    __syncwarp();  // (own line: the next row reads what this row wrote; the tile is consumed)
+    if (lane == 0) tma_issue();  // refill the stage this step consumed
+    if (++st == S) st = 0, ph ^= 1u;
+    if (MULTI && lane == 0) publish_progress(d.prod + d.w, t + 1);
+    if (SPLIT && last && d.w + 1 < d.W) {
+      if (lane == 0) {
+        __stcg(reinterpret_cast<double2*>(d.carry) + d.w * d.ny + rowk, make_double2(tc0, tc1));
+        publish_progress(d.prod + d.w, rowk + 1);
+      }
+      __syncwarp();
+    }
+    if (last) {
+      cell = next_row;
+      k = kbeg;
+      ++rowk;
+      next_row = rowk + 1 < nrows ? first_cell(rowk + 1) : 0;
+    } else {
+      cell += kDx * kWChunk;
+      ++k;
+    }
+  }
+}
+
 // Per-direction constants (kConsts layout above), written by one warp.
 template <bool UNIFORM>
 __device__ __forceinline__ void dir_consts(const SweepArgs& a, double omx, double omy, bool xu, bool yu, double* cst,
@@ -644,9 +932,21 @@ __device__ __forceinline__ void dir_consts(const SweepArgs& a, double omx, doubl
 }
 
 // nck: chunks per segment (kSplit); the trace lines then span one segment.
-template <bool UNIFORM, int MODE, bool HAS_BC>
-__global__ void __launch_bounds__(256, 2) sweep_scan_kernel(const SweepArgs a, int W, bool smem_lines, int nck) {
-  extern __shared__ double smem[];
+// WIDE (uniform media only): sweep_dir_wide with the TMA source ring of
+// `stages` 4 KB tiles per warp at the front of dynamic shared memory.
+template <bool UNIFORM, int MODE, bool HAS_BC, bool WIDE>
+__global__ void __launch_bounds__(256, UNIFORM ? 1 : 2)
+    sweep_scan_kernel(const SweepArgs a, int W, bool smem_lines, int nck, int stages,
+                      const __grid_constant__ CUtensorMap tmap) {
+  static_assert(!WIDE || UNIFORM, "the wide kernel is for uniform media");
+  extern __shared__ __align__(1024) unsigned char smem_raw[];
+  __shared__ __align__(8) unsigned long long tma_bars[WIDE ? kWarps * kMaxStages : 1];
+  // ring tiles first (1024-byte aligned for the swizzle), then the groups
+  const unsigned raw = smem_u32(smem_raw);
+  const unsigned ring = (raw + 1023u) & ~1023u;
+  double* smem =
+      reinterpret_cast<double*>(smem_raw + (WIDE ? ring - raw + static_cast<unsigned>(kWarps * stages * kWTileBytes) : 0));
+  constexpr int kCh = WIDE ? kWChunk : kChunk;
   const int lane = threadIdx.x & 31;
   const int wib = threadIdx.x >> 5;
   const int groups = kWarps / W;
@@ -654,9 +954,9 @@ __global__ void __launch_bounds__(256, 2) sweep_scan_kernel(const SweepArgs a, i
   const int slot = blockIdx.x * groups + g;
   if (slot >= a.n) return;  // a whole direction group exits together
   const int nx = a.nx, ny = a.ny;
-  const int linew = MODE == kSplit ? nck * kChunk : nx;  // columns per trace line
-  const int pitch = line_pitch(linew);
-  double* base = smem + static_cast<size_t>(g) * group_doubles(W, linew, smem_lines);
+  const int linew = MODE == kSplit ? nck * kCh : nx;  // columns per trace line
+  const int pitch = line_pitch_w(linew, WIDE);
+  double* base = smem + static_cast<size_t>(g) * group_doubles(W, linew, smem_lines, WIDE);
   double* cst = base;
   int* prod = reinterpret_cast<int*>(base + kConsts);
   double* lines = smem_lines ? base + kConsts + 2 * ((W + 3) / 4) : a.line + static_cast<size_t>(slot) * W * 2 * pitch;
@@ -682,13 +982,25 @@ __global__ void __launch_bounds__(256, 2) sweep_scan_kernel(const SweepArgs a, i
   // line holds its columns of the previous row
   d.in_line = lines + static_cast<size_t>(MODE == kRows ? d.pw : w) * 2 * pitch;
   d.err = a.err;
+  d.tmap = &tmap;
+  d.ring = ring + static_cast<unsigned>(wib * stages * kWTileBytes);
+  d.bars = smem_u32(tma_bars) + (WIDE ? 8u * kMaxStages * wib : 0u);
+  d.src_row0 = static_cast<long long>(slot) * a.rhs_stride / 16;
+  d.stages = stages;
+  if (WIDE) {
+    if (lane == 0) {
+      for (int u = 0; u < stages; ++u) mbar_init(d.bars + 8u * u, 1);
+      asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncwarp();
+  }
   d.pref = a.pref ? a.pref + static_cast<long long>(slot) * kPrefDoubles * a.pref_stride : nullptr;
   d.pref_stride = a.pref_stride;
   d.nx = nx;
   d.ny = ny;
   d.W = W;
   d.w = w;
-  d.nchunk = (nx + kChunk - 1) / kChunk;
+  d.nchunk = (nx + kCh - 1) / kCh;
   if (MODE == kSplit) {  // segment w of every row; boundary carries in the (unused) global line buffer
     d.rw = 0;
     d.rW = 1;
@@ -707,10 +1019,17 @@ __global__ void __launch_bounds__(256, 2) sweep_scan_kernel(const SweepArgs a, i
   d.pitch = pitch;
   d.yu = yu;
   d.smem_lines = smem_lines;
-  if (xu)
-    sweep_dir<UNIFORM, MODE, HAS_BC, true>(d);
-  else
-    sweep_dir<UNIFORM, MODE, HAS_BC, false>(d);
+  if constexpr (WIDE) {
+    if (xu)
+      sweep_dir_wide<MODE, HAS_BC, true>(d);
+    else
+      sweep_dir_wide<MODE, HAS_BC, false>(d);
+  } else {
+    if (xu)
+      sweep_dir<UNIFORM, MODE, HAS_BC, true>(d);
+    else
+      sweep_dir<UNIFORM, MODE, HAS_BC, false>(d);
+  }
 }
 
 // Per (direction slot, cell): the block M = Omega_x A_x + Omega_y A_y +
@@ -809,20 +1128,6 @@ __device__ __forceinline__ void st_async_v2(unsigned addr, double x, double y, u
   asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.v2.f64 [%0], {%1, %2}, [%3];" ::"r"(addr),
                "d"(x), "d"(y), "r"(mbar)
                : "memory");
-}
-__device__ __forceinline__ void mbar_init(unsigned bar, unsigned count) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(count) : "memory");
-}
-__device__ __forceinline__ void mbar_expect(unsigned bar, unsigned bytes) {
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
-}
-__device__ __forceinline__ void mbar_wait(unsigned bar, unsigned parity) {
-  asm volatile(
-      "{\n\t.reg .pred p;\n\tWAIT_%=:\n\t"
-      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
-      "@!p bra WAIT_%=;\n\t}" ::"r"(bar),
-      "r"(parity)
-      : "memory");
 }
 __device__ __forceinline__ void prefetch_line_l2(const double* p) {
   asm volatile("prefetch.global.L2 [%0];" ::"l"(p));
@@ -1063,62 +1368,149 @@ void launch_sweep_prefactor(const SweepArgs& a, double* table, long long stride,
   RTLR_CUDA(cudaGetLastError());
 }
 
+namespace {
+
+constexpr size_t kScanSmemMax = 220 * 1024;  // dynamic shared memory per block (<= 227 KB with the static part)
+
+using EncodeTiled = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                 const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                 CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+EncodeTiled encode_tiled() {
+  static const EncodeTiled fn = [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+      p = nullptr;
+    return reinterpret_cast<EncodeTiled>(p);
+  }();
+  return fn;
+}
+
+// The sources of all n directions as a 2-D tensor of 128-byte rows (16
+// doubles = 4 cells); a chunk is a 16 x 32 box (128 cells), 128-byte swizzle.
+bool make_source_map(const SweepArgs& a, CUtensorMap* m) {
+  const EncodeTiled enc = encode_tiled();
+  if (!enc) return false;
+  const unsigned long long total = static_cast<unsigned long long>(a.n - 1) * a.rhs_stride +
+                                   4ull * static_cast<unsigned long long>(a.nx) * a.ny;
+  const cuuint64_t dims[2] = {16, (total + 15) / 16};
+  const cuuint64_t strides[1] = {128};
+  const cuuint32_t box[2] = {16, static_cast<cuuint32_t>(kWChunk / 4)};
+  const cuuint32_t estr[2] = {1, 1};
+  return enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, const_cast<double*>(a.rhs), dims, strides, box, estr,
+             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+}  // namespace
+
 void launch_sweep_scan(const SweepArgs& a, bool uniform, cudaStream_t s) {
   if (a.n <= 0) return;
-  const int nchunk = (a.nx + kChunk - 1) / kChunk;
-  auto lines_fit = [](int linew) {
-    return static_cast<size_t>(kWarps) * 2 * line_pitch(linew) * sizeof(double) <= kLineSmemBudget;
+  // Launch plan for a chunk width (64 cells, or 128 for the wide kernel).
+  struct Plan {
+    int mode = kOne, W = 1, nck = 1, linew = 0;
+    bool smem_lines = true;
+    size_t smem = 0;  // groups' dynamic shared memory
   };
-  // Last-wave fill of n*c warps over the resident warp slots (SMs x blocks/SM x kWarps).
-  auto wave_eff = [&](int c, int linew, bool smem_lines) {
-    const size_t smem = static_cast<size_t>(kWarps / c) * group_doubles(c, linew, smem_lines) * sizeof(double);
-    const int per_sm = std::max(1, std::min(2, static_cast<int>((227u * 1024u) / (smem + 1024u))));
-    const double slots = static_cast<double>(sm_count()) * per_sm * kWarps;
-    const double waves = static_cast<double>(a.n) * c / slots;
-    return waves <= 1.0 ? waves : waves / std::ceil(waves);
-  };
-  // Warps per direction W in {1, 2, 4, 8}, best last-wave fill, ties keep the
-  // smaller W.  Rows whose full-width trace lines fit shared memory (nx <=
-  // 768): row interleave (at most one warp per 2 rows).  Wider rows: column
-  // segments (every segment non-empty, lines of one segment in shared
-  // memory); only if no split fits do the lines go to L2.
-  int mode = kOne, W = 1, nck = nchunk, linew = a.nx;
-  bool smem_lines = lines_fit(a.nx);
-  double best = -1.0;
-  if (smem_lines) {
-    for (int c = 1; c <= kWarps && (c == 1 || 2 * c <= a.ny); c *= 2) {
-      const double eff = wave_eff(c, a.nx, true);
-      if (eff > best + 1e-3) best = eff, W = c;
-    }
-    mode = W > 1 ? kRows : kOne;
-  } else {
-    for (int c = 2; c <= kWarps; c *= 2) {
-      const int k = (nchunk + c - 1) / c;
-      if ((c - 1) * k >= nchunk || !lines_fit(k * kChunk)) continue;
-      const double eff = wave_eff(c, k * kChunk, true);
-      if (eff > best + 1e-3) best = eff, W = c, nck = k;
-    }
-    if (W > 1) {
-      mode = kSplit;
-      smem_lines = true;
-      linew = nck * kChunk;
-    } else {  // rows in L2
-      for (int c = 1; c <= kWarps && (c == 1 || 2 * c <= a.ny); c *= 2) {
-        const double eff = wave_eff(c, a.nx, false);
-        if (eff > best + 1e-3) best = eff, W = c;
+  auto plan_for = [&](bool wide) {
+    const int ch = wide ? kWChunk : kChunk;
+    const int nchunk = (a.nx + ch - 1) / ch;
+    auto lines_fit = [&](int linew) {
+      return static_cast<size_t>(kWarps) * 2 * line_pitch_w(linew, wide) * sizeof(double) <= kLineSmemBudget;
+    };
+    // Last-wave fill of n*c warps over the resident warp slots (SMs x blocks/SM x kWarps).
+    auto wave_eff = [&](int c, int linew, bool smem_lines) {
+      const size_t smem = static_cast<size_t>(kWarps / c) * group_doubles(c, linew, smem_lines, wide) * sizeof(double);
+      const int per_sm = std::max(1, std::min(uniform ? 1 : 2, static_cast<int>((227u * 1024u) / (smem + 1024u))));
+      const double slots = static_cast<double>(sm_count()) * per_sm * kWarps;
+      const double waves = static_cast<double>(a.n) * c / slots;
+      return waves <= 1.0 ? waves : waves / std::ceil(waves);
+    };
+    // Warps per direction W in {1, 2, 4, 8}, best last-wave fill, ties keep
+    // the smaller W.  Rows whose full-width trace lines fit shared memory
+    // (nx <= 768): row interleave (at most one warp per 2 rows).  Wider
+    // rows: column segments (every segment non-empty, lines of one segment
+    // in shared memory); only if no split fits do the lines go to L2.
+    Plan p;
+    p.nck = nchunk;
+    p.linew = a.nx;
+    p.smem_lines = lines_fit(a.nx);
+    double best = -1.0;
+    if (p.smem_lines) {
+      // (c <= nchunk: the row chain of ny + nchunk - 1 dependent steps stays
+      // shorter than a warp's own ny / c rows x nchunk steps)
+      for (int c = 1; c <= kWarps && (c == 1 || (2 * c <= a.ny && c <= nchunk)); c *= 2) {
+        const double eff = wave_eff(c, a.nx, true);
+        if (eff > best + 1e-3) best = eff, p.W = c;
       }
-      mode = W > 1 ? kRows : kOne;
+      p.mode = p.W > 1 ? kRows : kOne;
+    } else {
+      for (int c = 2; c <= kWarps; c *= 2) {
+        const int k = (nchunk + c - 1) / c;
+        if ((c - 1) * k >= nchunk || !lines_fit(k * ch)) continue;
+        const double eff = wave_eff(c, k * ch, true);
+        if (eff > best + 1e-3) best = eff, p.W = c, p.nck = k;
+      }
+      if (p.W > 1) {
+        p.mode = kSplit;
+        p.smem_lines = true;
+        p.linew = p.nck * ch;
+      } else {  // rows in L2
+        for (int c = 1; c <= kWarps && (c == 1 || 2 * c <= a.ny); c *= 2) {
+          const double eff = wave_eff(c, a.nx, false);
+          if (eff > best + 1e-3) best = eff, p.W = c;
+        }
+        p.mode = p.W > 1 ? kRows : kOne;
+      }
     }
+    p.smem = static_cast<size_t>(kWarps / p.W) * group_doubles(p.W, p.linew, p.smem_lines, wide) * sizeof(double);
+    return p;
+  };
+  // Uniform media take the wide kernel when the rows of the source tensor
+  // (128 B = 4 cells) line up with the chunks, rows are at least one chunk
+  // wide, the trace lines sit in shared memory and a ring of >= 2 tiles fits.
+  CUtensorMap tmap;
+  std::memset(&tmap, 0, sizeof(tmap));
+  const char* te = std::getenv("RTLR_SWEEP_TMA");
+  bool wide = uniform && !(te && te[0] == '0') && a.nx >= kWChunk && a.nx % 4 == 0 && a.rhs_stride % 16 == 0 &&
+              reinterpret_cast<uintptr_t>(a.rhs) % 16 == 0;
+  Plan pl;
+  int stages = 0;
+  if (wide) {
+    pl = plan_for(true);
+    const size_t room = kScanSmemMax > pl.smem + 1024 ? kScanSmemMax - pl.smem - 1024 : 0;
+    stages = static_cast<int>(std::min<size_t>(kMaxStages, room / (static_cast<size_t>(kWarps) * kWTileBytes)));
+    // Wide steps are longer: only when the directions (nearly) fill the
+    // resident warp slots, i.e. the sweep is bandwidth-bound; a latency-bound
+    // sweep of a few directions keeps the 64-cell steps (C5 256^2 x 256:
+    // 0.25 ms narrow vs 0.46 ms wide; 512^2 x 1024, 86% of the slots: 3.22 ms
+    // wide vs 3.28 ms narrow).  RTLR_SWEEP_TMA=1 forces the wide kernel
+    // wherever it applies, =0 disables it.
+    const bool fills = (te && te[0] == '1') ||
+                       4LL * a.n * pl.W >= 3LL * sm_count() * kWarps;
+    wide = fills && pl.smem_lines && stages >= 2 && make_source_map(a, &tmap);
   }
+  size_t smem;
+  if (wide) {
+    smem = pl.smem + 1024 + static_cast<size_t>(kWarps) * stages * kWTileBytes;
+  } else {
+    pl = plan_for(false);
+    smem = pl.smem;
+  }
+  const int W = pl.W, mode = pl.mode, nck = pl.nck;
+  const bool smem_lines = pl.smem_lines;
   const int groups = kWarps / W;
   const int blocks = (a.n + groups - 1) / groups;
-  const size_t smem = static_cast<size_t>(groups) * group_doubles(W, linew, smem_lines) * sizeof(double);
   auto go = [&](auto kern) {
-    RTLR_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
-    kern<<<blocks, kWarps * 32, smem, s>>>(a, W, smem_lines, nck);
+    RTLR_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kScanSmemMax)));
+    kern<<<blocks, kWarps * 32, smem, s>>>(a, W, smem_lines, nck, stages, tmap);
   };
   const bool bc = a.bc != nullptr;
-#define RTLR_SCAN_GO(U, M) (bc ? go(sweep_scan_kernel<U, M, true>) : go(sweep_scan_kernel<U, M, false>))
+#define RTLR_SCAN_GO(U, M)                                                                        \
+  (wide ? (bc ? go(sweep_scan_kernel<U, M, true, U>) : go(sweep_scan_kernel<U, M, false, U>))   \
+        : (bc ? go(sweep_scan_kernel<U, M, true, false>) : go(sweep_scan_kernel<U, M, false, false>)))
   if (uniform) {
     if (mode == kSplit) RTLR_SCAN_GO(true, kSplit);
     else if (mode == kRows) RTLR_SCAN_GO(true, kRows);

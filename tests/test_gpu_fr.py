@@ -27,6 +27,11 @@ SWEEP_CASES = [
     # rows wider than 768 cells: the scan kernel splits rows into column segments
     ("homogeneous(1,1)", {"nx": 1000, "ny": 24, "n_theta": 8, "n_omega_z": 2}),
     ("C4", {"nx": 1030, "ny": 12, "n_theta": 4, "n_omega_z": 4}),
+    # uniform, nx >= 128 with nx % 4 == 0 but not a multiple of the 128-cell
+    # chunk: the wide kernel's TMA boxes run past the row ends (both x
+    # directions); C2's 128 x 128 is exactly one chunk per row
+    ("homogeneous(1,1)", {"nx": 196, "ny": 30, "n_theta": 8, "n_omega_z": 2}),
+    ("C2", {"n_theta": 8, "n_omega_z": 4}),
 ]
 
 
@@ -59,6 +64,7 @@ def test_sweep_matches_oracle(name, ov, kernel):
 @pytest.mark.parametrize("name,ov", [
     ("homogeneous(1,1)", {"nx": 33, "ny": 20, "n_theta": 4, "n_omega_z": 2, "boundary_const": 1.0}),
     ("C4", {"nx": 64, "ny": 70, "n_theta": 4, "n_omega_z": 2, "boundary_const": 0.5}),
+    ("homogeneous(1,1)", {"nx": 132, "ny": 20, "n_theta": 4, "n_omega_z": 2, "boundary_const": 1.0}),
 ])
 def test_sweep_inflow_matches_oracle(name, ov, kernel):
     """Inflow boundary data enters every K1 path as a per-angle source
@@ -75,6 +81,37 @@ def test_sweep_inflow_matches_oracle(name, ov, kernel):
     for j in range(n):
         ref = o.sweep(d[j, 0], d[j, 1], rhs[:, j] + o.boundary_vector(d[j, 0], d[j, 1]))
         assert rel(psi[:, j], ref) <= 1e-12, (j, rel(psi[:, j], ref))
+
+
+@pytest.mark.parametrize("name,ov", [
+    ("C2", {"n_theta": 8, "n_omega_z": 4}),
+    ("homogeneous(1,1)", {"nx": 196, "ny": 30, "n_theta": 8, "n_omega_z": 2}),
+    ("homogeneous(1,1)", {"nx": 1000, "ny": 24, "n_theta": 8, "n_omega_z": 2}),
+    ("homogeneous(1,1)", {"nx": 132, "ny": 20, "n_theta": 4, "n_omega_z": 2, "boundary_const": 1.0}),
+])
+def test_sweep_wide_kernel_matches_narrow(name, ov, monkeypatch):
+    """Uniform media with rows >= 128 cells: the wide kernel (four cells per
+    lane, TMA source ring; RTLR_SWEEP_TMA=1 forces it) and the
+    two-cells-per-lane kernel (RTLR_SWEEP_TMA=0) against each other and the oracle, per-direction and
+    shared right-hand sides.  They associate the row scan differently, so
+    the bar is the sweep tolerance, not bitwise equality."""
+    o = O.Problem(name, use_dsa=0, **ov)
+    g = P.Problem(name, use_dsa=0, **ov)
+    g.set_option("sweep_kernel", 2)
+    rng = np.random.default_rng(7)
+    d = g.get("dirs")
+    n = g.n_omega
+    rhs = rng.standard_normal((g.n, n))
+    src = g.get("source")
+    monkeypatch.setenv("RTLR_SWEEP_TMA", "1")  # (a few directions would pick the narrow kernel)
+    a, a2 = g.sweep(np.arange(n), rhs), g.sweep(np.arange(n), src)
+    monkeypatch.setenv("RTLR_SWEEP_TMA", "0")
+    b, b2 = g.sweep(np.arange(n), rhs), g.sweep(np.arange(n), src)
+    for j in range(n):
+        assert rel(a[:, j], b[:, j]) <= 1e-13 and rel(a2[:, j], b2[:, j]) <= 1e-13
+    for j in range(0, n, max(1, n // 4)):
+        bcv = o.boundary_vector(d[j, 0], d[j, 1]) if "boundary_const" in ov else 0.0
+        assert rel(a[:, j], o.sweep(d[j, 0], d[j, 1], rhs[:, j] + bcv)) <= 1e-12
 
 
 def test_sweep_zero_rhs_exact_zero():  # test_sweep.cpp:34-42
