@@ -260,8 +260,14 @@ constexpr int kKT = 16, kQ = 24, kG = 32, kGP = 36, kConsts = 164;
 
 // Doubles per trace plane (even, so both planes stay 16-byte aligned).
 __host__ __device__ constexpr int line_pitch(int nx) { return (nx + 1) & ~1; }
-// (the wide kernel reads and writes four columns at a time: multiple of 4)
-__host__ __device__ constexpr int line_pitch_w(int nx, bool wide) { return wide ? (nx + 3) & ~3 : line_pitch(nx); }
+// The wide kernel reads and writes four columns (32 B) per lane: its lines
+// carry two doubles of padding after every 16 columns, so the 8 lanes of a
+// 16-byte shared-memory phase hit distinct banks (unpadded, lanes l and l+4
+// collide).
+__host__ __device__ constexpr int wide_line_idx(int c) { return c + 2 * (c >> 4); }
+__host__ __device__ constexpr int line_pitch_w(int nx, bool wide) {
+  return wide ? (wide_line_idx((nx + 3) & ~3) + 3) & ~3 : line_pitch(nx);
+}
 __host__ __device__ constexpr int group_doubles(int W, int nx, bool smem_lines, bool wide = false) {
   return kConsts + 2 * ((W + 3) / 4) + (smem_lines ? W * 2 * line_pitch_w(nx, wide) : 0);
 }
@@ -770,7 +776,7 @@ __device__ __forceinline__ void sweep_dir_wide(const Dir& d) {
         __syncwarp();
       }
       if (act[0]) {
-        const double* p0 = d.in_line + (col - colbase);
+        const double* p0 = d.in_line + wide_line_idx(col - colbase);
 #pragma unroll
         for (int pl = 0; pl < 2; ++pl) {
           const unsigned a0 = smem_u32(p0 + pl * d.pitch);
@@ -837,7 +843,7 @@ __device__ __forceinline__ void sweep_dir_wide(const Dir& d) {
     for (int c = 0; c < C; ++c)
       if (act[c]) st_cell256(d.psi + 4 * (cell + kDx * c), ps[c]);
     if (act[0]) {  // y-outflow traces (per x-mode) for the next row
-      double* q0 = d.my_line + (col - colbase);
+      double* q0 = d.my_line + wide_line_idx(col - colbase);
 #pragma unroll
       for (int pl = 0; pl < 2; ++pl) {
         double o[C];
