@@ -1381,6 +1381,65 @@ __global__ void __launch_bounds__(256) lu_backsolve_warp(int r, int m, const dou
   if (lane == 0) flags[sys] = bad;
 }
 
+// The same back substitution with one CTA per system: warp 0 solves each
+// 32 x 32 diagonal block from shared memory, then all 8 warps share the
+// update of the rows above (one row per thread, the 32 loads of a row issued
+// together).  Per element the same operations in the same order as
+// lu_backsolve_warp, so the solutions are bitwise identical; a few systems
+// (the q greedy candidates) no longer leave the GPU with one warp each.
+__global__ void __launch_bounds__(256) lu_backsolve_cta(int r, const double* __restrict__ M,
+                                                        double* __restrict__ sol, long long ldsol,
+                                                        int* __restrict__ flags) {
+  extern __shared__ double xs[];
+  double* ub = xs + r;  // 32 x 33 diagonal block, ub[j * 33 + i] = U[i0 + j][i0 + i]
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int sys = blockIdx.x;
+  const double* A = M + static_cast<size_t>(sys) * r * (r + 1);
+  for (int i = tid; i < r; i += blockDim.x) xs[i] = A[i + static_cast<size_t>(r) * r];
+  for (int i0 = ((r - 1) / 32) * 32; i0 >= 0; i0 -= 32) {
+    const int bs = min(32, r - i0);
+    __syncthreads();
+    for (int e = tid; e < bs * bs; e += blockDim.x) {
+      const int j = e % bs, i = e / bs;  // row j, column i of the block
+      ub[j * 33 + i] = A[i0 + j + static_cast<size_t>(i0 + i) * r];
+    }
+    __syncthreads();
+    if (warp == 0) {
+      double x = lane < bs ? xs[i0 + lane] : 0.0;
+      for (int i = bs - 1; i >= 0; --i) {
+        const double xi = __shfl_sync(0xffffffffu, x, i) / ub[i * 33 + i];
+        if (lane == i) x = xi;
+        if (lane < i) x -= xi * ub[lane * 33 + i];
+      }
+      if (lane < bs) xs[i0 + lane] = x;
+    }
+    __syncthreads();
+    const double* xb = xs + i0;
+    for (int row = tid; row < i0; row += blockDim.x) {
+      const double* ar = A + row + static_cast<size_t>(i0) * r;
+      double acc = 0.0;
+      if (bs == 32) {
+        double v[32];
+#pragma unroll
+        for (int l = 0; l < 32; ++l) v[l] = ar[static_cast<size_t>(l) * r];
+#pragma unroll
+        for (int l = 0; l < 32; ++l) acc += v[l] * xb[l];
+      } else {
+        for (int l = 0; l < bs; ++l) acc += ar[static_cast<size_t>(l) * r] * xb[l];
+      }
+      xs[row] -= acc;
+    }
+  }
+  __syncthreads();
+  int bad = 0;
+  for (int i = tid; i < r; i += blockDim.x) {
+    sol[i + static_cast<long long>(sys) * ldsol] = xs[i];
+    if (!isfinite(xs[i])) bad = 1;
+  }
+  bad = __syncthreads_or(bad);
+  if (tid == 0) flags[sys] = bad;
+}
+
 }  // namespace
 
 size_t gemm_tn_work(int M, int N, long long K) {
@@ -1534,12 +1593,22 @@ void galerkin_batch(int r, int m, const int* angles, const double* dirs, const d
       if (ntrail > 0) lu_trail<<<dim3((ntrail + BN - 1) / BN, m), 256, 0, s>>>(r, k0, jb, M, perm);
       k0 += jb;
     }
-    const int per = 8;  // systems (warps) per CTA
-    const size_t smem = static_cast<size_t>(per) * (r + 32 * 33) * sizeof(double);
-    if (smem > 48 * 1024)
-      RTLR_CUDA(cudaFuncSetAttribute(lu_backsolve_warp, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     static_cast<int>(smem)));
-    lu_backsolve_warp<<<(m + per - 1) / per, 32 * per, smem, s>>>(r, m, M, sol, ldsol, flags);
+    // One CTA per system while the systems do not fill the GPU with warps;
+    // beyond that one warp per system (8 per CTA) has the parallelism.
+    if (m < 8 * 148) {
+      const size_t smem = (static_cast<size_t>(r) + 32 * 33) * sizeof(double);
+      if (smem > 48 * 1024)
+        RTLR_CUDA(cudaFuncSetAttribute(lu_backsolve_cta, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       static_cast<int>(smem)));
+      lu_backsolve_cta<<<m, 256, smem, s>>>(r, M, sol, ldsol, flags);
+    } else {
+      const int per = 8;  // systems (warps) per CTA
+      const size_t smem = static_cast<size_t>(per) * (r + 32 * 33) * sizeof(double);
+      if (smem > 48 * 1024)
+        RTLR_CUDA(cudaFuncSetAttribute(lu_backsolve_warp, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       static_cast<int>(smem)));
+      lu_backsolve_warp<<<(m + per - 1) / per, 32 * per, smem, s>>>(r, m, M, sol, ldsol, flags);
+    }
     RTLR_CUDA(cudaGetLastError());
     return;
   }

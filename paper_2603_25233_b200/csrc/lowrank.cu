@@ -327,6 +327,14 @@ class LowRankEngine {
     dirs_ = P.dirs_.get();
     sa_ = StencilArgs{hp_.nx, hp_.ny, hp_.ncell, P.sigma_t_.get(), P.sc_};
     RTLR_CUDA(cudaMallocHost(&hbuf_, 64 * sizeof(double)));
+    // The basis grows every inner iteration; reserving it for the largest
+    // possible rank up front (when that takes at most a quarter of the free
+    // device memory: 17 GB at C4) keeps multi-GB cudaMalloc/cudaFree pairs,
+    // which synchronise the device, out of the first outer iteration.
+    size_t free_b = 0, total_b = 0;
+    if (cudaMemGetInfo(&free_b, &total_b) == cudaSuccess &&
+        static_cast<double>(n_) * rmax_ * sizeof(double) <= 0.25 * static_cast<double>(free_b))
+      X_.reserve(n_, rmax_, s_);
     const char* e = std::getenv("RTLR_PROFILE");
     pt_.on = e && e[0] == '1';
     pt_.s = s_;

@@ -1,0 +1,96 @@
+// Batched Galerkin LU timing (K7, dense.cu galerkin_batch) on synthetic
+// systems: A_j = omx Px + omy Py + Pt with a dominant Pt, r x r, m angles.
+// Build:  nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++17 \
+//           -I paper_2603_25233_b200/csrc -I include tools/lu_bench.cu \
+//           -o tools/lu_bench -Lpaper_2603_25233_b200/lib -lrtlr_cu \
+//           -Xlinker -rpath=$PWD/paper_2603_25233_b200/lib
+// Run:    tools/lu_bench r m [reps]   (prints ms per batch, GFLOP/s, max residual)
+#include <cmath>
+#include <cstdio>
+#include <cstdlib>
+#include <random>
+#include <vector>
+
+#include "dense.cuh"
+
+#define CK(x)                                                                              \
+  do {                                                                                     \
+    cudaError_t e_ = (x);                                                                  \
+    if (e_ != cudaSuccess) {                                                               \
+      std::fprintf(stderr, "%s:%d %s\n", __FILE__, __LINE__, cudaGetErrorString(e_));      \
+      std::exit(1);                                                                        \
+    }                                                                                      \
+  } while (0)
+
+int main(int argc, char** argv) {
+  const int r = argc > 1 ? std::atoi(argv[1]) : 600;
+  const int m = argc > 2 ? std::atoi(argv[2]) : 16;
+  const int reps = argc > 3 ? std::atoi(argv[3]) : 5;
+  std::mt19937_64 g(12345);
+  std::uniform_real_distribution<double> u(-1.0, 1.0);
+  const size_t rr = static_cast<size_t>(r) * r;
+  std::vector<double> proj(5 * rr), prhs(r), dirs(3 * m);
+  for (int k = 0; k < 5; ++k)
+    for (size_t e = 0; e < rr; ++e) proj[k * rr + e] = 0.3 * u(g) / std::sqrt(static_cast<double>(r));
+  for (int i = 0; i < r; ++i) proj[4 * rr + i + static_cast<size_t>(i) * r] += 2.0 + u(g);
+  for (int i = 0; i < r; ++i) prhs[i] = u(g);
+  std::vector<int> ang(m);
+  for (int j = 0; j < m; ++j) {
+    dirs[3 * j] = u(g);
+    dirs[3 * j + 1] = u(g);
+    dirs[3 * j + 2] = 0.0;
+    ang[j] = j;
+  }
+  double *dproj, *dprhs, *ddirs, *dsol, *dwork;
+  int *dang, *dflags;
+  const size_t wd = rtlr::cuda::galerkin_work_doubles(r, m);
+  CK(cudaMalloc(&dproj, proj.size() * 8));
+  CK(cudaMalloc(&dprhs, r * 8));
+  CK(cudaMalloc(&ddirs, dirs.size() * 8));
+  CK(cudaMalloc(&dsol, static_cast<size_t>(r) * m * 8));
+  CK(cudaMalloc(&dwork, std::max<size_t>(wd, 1) * 8));
+  CK(cudaMalloc(&dang, m * 4));
+  CK(cudaMalloc(&dflags, m * 4));
+  CK(cudaMemcpy(dproj, proj.data(), proj.size() * 8, cudaMemcpyHostToDevice));
+  CK(cudaMemcpy(dprhs, prhs.data(), r * 8, cudaMemcpyHostToDevice));
+  CK(cudaMemcpy(ddirs, dirs.data(), dirs.size() * 8, cudaMemcpyHostToDevice));
+  CK(cudaMemcpy(dang, ang.data(), m * 4, cudaMemcpyHostToDevice));
+  cudaStream_t s;
+  CK(cudaStreamCreate(&s));
+  auto run = [&] {
+    rtlr::cuda::galerkin_batch(r, m, dang, ddirs, dproj, r, rr, dprhs, nullptr, dsol, r, dflags, dwork, s);
+  };
+  run();
+  CK(cudaStreamSynchronize(s));
+  cudaEvent_t a, b;
+  CK(cudaEventCreate(&a));
+  CK(cudaEventCreate(&b));
+  CK(cudaEventRecord(a, s));
+  for (int i = 0; i < reps; ++i) run();
+  CK(cudaEventRecord(b, s));
+  CK(cudaEventSynchronize(b));
+  float ms = 0.f;
+  CK(cudaEventElapsedTime(&ms, a, b));
+  ms /= reps;
+  std::vector<double> sol(static_cast<size_t>(r) * m);
+  CK(cudaMemcpy(sol.data(), dsol, sol.size() * 8, cudaMemcpyDeviceToHost));
+  double worst = 0.0;
+  for (int j = 0; j < m; j += std::max(1, m / 8)) {  // relative residual of a few systems
+    double num = 0.0, den = 0.0;
+    const size_t px = (dirs[3 * j] >= 0.0 ? 0 : 1) * rr, py = (dirs[3 * j + 1] >= 0.0 ? 2 : 3) * rr;
+    for (int i = 0; i < r; ++i) {
+      double acc = 0.0;
+      for (int k = 0; k < r; ++k) {
+        const size_t e = i + static_cast<size_t>(k) * r;
+        acc += (dirs[3 * j] * proj[px + e] + dirs[3 * j + 1] * proj[py + e] + proj[4 * rr + e]) * sol[k + static_cast<size_t>(j) * r];
+      }
+      num += (acc - prhs[i]) * (acc - prhs[i]);
+      den += prhs[i] * prhs[i];
+    }
+    worst = std::max(worst, std::sqrt(num / den));
+  }
+  const double gf = m * (2.0 / 3.0) * r * static_cast<double>(r) * r * 1e-9;
+  std::printf("r %d m %d: %.3f ms per batch, %.1f GFLOP/s (2/3 r^3 per system), max rel residual %.2e\n", r, m, ms,
+              gf / (ms * 1e-3), worst);
+  return worst < 1e-10 ? 0 : 1;
+}
