@@ -85,6 +85,13 @@ int tn_splits(int M, int N, long long K) {
   return static_cast<int>(std::max<long long>(1, s));
 }
 
+// Split count of gemm_tn_dmma_nt (128-row tiles, ~4 CTAs per SM).
+long long nt_splits(int M, long long K) {
+  const long long tiles = (M + 127) / 128;
+  long long sp = std::min<long long>((2 * 148 * 2 + tiles - 1) / tiles, std::max<long long>(1, K / 256));
+  return std::max<long long>(1, std::min<long long>(sp, 1024));
+}
+
 // ------------------------------------------------------------ skinny GEMMs
 // N <= 16 columns (CGS batches, candidate blocks): the 64-wide tiles above
 // would waste up to 8x the flops.
@@ -457,6 +464,84 @@ __global__ void __launch_bounds__(256) gemm_tn_dmma_pipe(int M, int N, long long
       for (int h = 0; h < 2; ++h) {
         const int m = m0 + wm + 8 * i + fr;
         const int n = n0 + wn + 8 * j + 2 * fc + h;
+        if (m < M && n < N) o[m + static_cast<long long>(n) * ldo] = acc[i][j][h];
+      }
+}
+
+// A^T B for 8 < N <= 48 (the border-extension products X^T [5p stencil
+// images]: N = 40 at p = 8, 20 at p = 4): 128 columns of A per CTA, every
+// warp owns 16 of them against all ceil(N/8) column tiles of B, so no warp
+// idles on padding columns and B is re-read once per 128 (not 64) columns
+// of A.  Three-stage cp.async pipeline of 128 x 32 A and 48 x 32 B tiles.
+// Same alignment contract and split-K partials as gemm_tn_dmma_pipe.
+constexpr int kNtBm = 128, kNtStages = 3, kNtMaxN = 48;
+template <int NT>
+__global__ void __launch_bounds__(256) gemm_tn_dmma_nt(int M, int N, long long K, long long kchunk,
+                                                       const double* __restrict__ A, long long lda,
+                                                       const double* __restrict__ B, long long ldb,
+                                                       double* __restrict__ out, long long ldo,
+                                                       long long split_stride) {
+  extern __shared__ double sm[];
+  double* As = sm;                                  // [stages][128][kTnLd]
+  double* Bs = sm + kNtStages * kNtBm * kTnLd;      // [stages][8 NT][kTnLd]
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int m0 = blockIdx.x * kNtBm, wm = warp * 16;
+  const long long k0 = blockIdx.y * kchunk, k1 = min(K, k0 + kchunk);
+  const int fr = lane >> 2, fc = lane & 3;
+  auto stage = [&](int buf, long long kb) {
+    if (kb < k1) {
+#pragma unroll
+      for (int e = 0; e < 8; ++e) {  // A: 128 rows x 16 pieces of 16 B
+        const int idx = tid + e * 256, row = idx >> 4, kq = (idx & 15) * 2;
+        const long long k = kb + kq;
+        const int m = m0 + row;
+        const bool v = k < k1 && m < M;
+        cp_async16(As + (buf * kNtBm + row) * kTnLd + kq, A + (v ? k + static_cast<long long>(m) * lda : 0), v);
+      }
+      for (int idx = tid; idx < 8 * NT * 16; idx += 256) {  // B: 8 NT rows x 16 pieces
+        const int row = idx >> 4, kq = (idx & 15) * 2;
+        const long long k = kb + kq;
+        const bool v = k < k1 && row < N;
+        cp_async16(Bs + (buf * 8 * NT + row) * kTnLd + kq, B + (v ? k + static_cast<long long>(row) * ldb : 0), v);
+      }
+    }
+    asm volatile("cp.async.commit_group;" ::: "memory");
+  };
+  double acc[2][NT][2];
+#pragma unroll
+  for (int i = 0; i < 2; ++i)
+#pragma unroll
+    for (int j = 0; j < NT; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+#pragma unroll
+  for (int p = 0; p < kNtStages - 1; ++p) stage(p, k0 + p * kTnBk);
+  int buf = 0;
+  for (long long kb = k0; kb < k1; kb += kTnBk) {
+    stage((buf + kNtStages - 1) % kNtStages, kb + (kNtStages - 1) * kTnBk);
+    asm volatile("cp.async.wait_group %0;" ::"n"(kNtStages - 1) : "memory");
+    __syncthreads();
+    const double* as = As + (buf * kNtBm + wm + fr) * kTnLd;
+    const double* bs = Bs + (buf * 8 * NT + fr) * kTnLd;
+#pragma unroll
+    for (int ks = 0; ks < kTnBk; ks += 4) {
+      const double a0 = as[ks + fc], a1 = as[8 * kTnLd + ks + fc];
+#pragma unroll
+      for (int j = 0; j < NT; ++j) {
+        const double b = bs[8 * j * kTnLd + ks + fc];
+        dmma884(acc[0][j][0], acc[0][j][1], a0, b);
+        dmma884(acc[1][j][0], acc[1][j][1], a1, b);
+      }
+    }
+    __syncthreads();
+    buf = (buf + 1) % kNtStages;
+  }
+  double* o = out + blockIdx.y * split_stride;
+#pragma unroll
+  for (int i = 0; i < 2; ++i)
+#pragma unroll
+    for (int j = 0; j < NT; ++j)
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int m = m0 + wm + 8 * i + fr, n = 8 * j + 2 * fc + h;
         if (m < M && n < N) o[m + static_cast<long long>(n) * ldo] = acc[i][j][h];
       }
 }
@@ -1443,7 +1528,10 @@ __global__ void __launch_bounds__(256) lu_backsolve_cta(int r, const double* __r
 }  // namespace
 
 size_t gemm_tn_work(int M, int N, long long K) {
-  return static_cast<size_t>(tn_splits(M, N, K)) * M * N;
+  const long long sp = N > 8 && N <= kNtMaxN && static_cast<double>(M) * N * K >= 1e9
+                           ? std::max<long long>(nt_splits(M, K), tn_splits(M, N, K))
+                                              : tn_splits(M, N, K);
+  return static_cast<size_t>(sp) * M * N;
 }
 
 void gemm_tn(int M, int N, long long K, const double* A, long long lda, const double* B, long long ldb, double* C,
@@ -1479,6 +1567,39 @@ void gemm_tn(int M, int N, long long K, const double* A, long long lda, const do
                                                                            sstride);
     }
     if (splits > 1) launch_splitk_reduce(M, N, splits, work, C, ldc, s);
+    RTLR_CUDA(cudaGetLastError());
+    return;
+  }
+  static const bool nt_off = [] {  // RTLR_TN_NT=0: the 64 x 64 tile kernel for these shapes too (A/B timing)
+    const char* e = std::getenv("RTLR_TN_NT");
+    return e && e[0] == '0';
+  }();
+  // (small products, e.g. C2's 178 x 20 x 65536, stay on the 64 x 64 tiles: 46 vs 54 us)
+  if (pipe_ok && N > 8 && N <= kNtMaxN && !nt_off && static_cast<double>(M) * N * K >= 1e9) {
+    // (own split count: 128-row tiles, ~4 CTAs per SM; still a function of the shape only)
+    const long long tiles = (M + kNtBm - 1) / kNtBm;
+    long long sp = nt_splits(M, K);
+    long long kc = ((K + sp - 1) / sp + kTnBk - 1) / kTnBk * kTnBk;
+    sp = (K + kc - 1) / kc;
+    if (static_cast<size_t>(sp) * M * N > work_doubles && sp > 1)
+      throw std::invalid_argument("gemm_tn: work buffer smaller than gemm_tn_work(M, N, K)");
+    double* o2 = sp == 1 ? C : work;
+    const long long ldo2 = sp == 1 ? ldc : M, ss2 = sp == 1 ? 0 : static_cast<long long>(M) * N;
+    const int nt = (N + 7) / 8;
+    const int smem = kNtStages * (kNtBm + 8 * nt) * kTnLd * static_cast<int>(sizeof(double));
+    auto go = [&](auto kern) {
+      RTLR_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+      kern<<<dim3(static_cast<unsigned>(tiles), static_cast<unsigned>(sp)), 256, smem, s>>>(M, N, K, kc, A, lda, B,
+                                                                                          ldb, o2, ldo2, ss2);
+    };
+    switch (nt) {
+      case 2: go(gemm_tn_dmma_nt<2>); break;
+      case 3: go(gemm_tn_dmma_nt<3>); break;
+      case 4: go(gemm_tn_dmma_nt<4>); break;
+      case 5: go(gemm_tn_dmma_nt<5>); break;
+      default: go(gemm_tn_dmma_nt<6>); break;
+    }
+    if (sp > 1) launch_splitk_reduce(M, N, static_cast<int>(sp), work, C, ldc, s);
     RTLR_CUDA(cudaGetLastError());
     return;
   }
