@@ -556,6 +556,85 @@ __device__ __forceinline__ void cp_async8(double* smem_dst, const double* src, b
   asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;" ::"r"(d), "l"(src), "r"(n) : "memory");
 }
 
+// C (-)= A B for N > 8 with 128-row tiles: every warp owns 16 rows against
+// all NT column tiles of its CTA's column group (8 NT columns; column groups
+// of the same rows are adjacent in launch order, so A is re-read from L2),
+// three-stage cp.async pipeline.  A staged [k][m] with row stride 132
+// doubles (the fragment loads' half-warps hit distinct banks).  Same
+// contract as gemm_nn_dmma_pipe.
+constexpr int kNnNtLdA = kNtBm + 4;
+template <int NT>
+__global__ void __launch_bounds__(256) gemm_nn_dmma_nt(long long M, int N, int K, const double* __restrict__ A,
+                                                       long long lda, const double* __restrict__ B, long long ldb,
+                                                       double* __restrict__ C, long long ldc, bool subtract) {
+  extern __shared__ double sm[];
+  double* As = sm;                                    // [stages][32][kNnNtLdA]
+  double* Bs = sm + kNtStages * kTnBk * kNnNtLdA;     // [stages][8 NT][kTnLd]
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const long long m0 = static_cast<long long>(blockIdx.y) * kNtBm;
+  const int n0 = blockIdx.x * 8 * NT, wm = warp * 16;
+  const int fr = lane >> 2, fc = lane & 3;
+  auto stage = [&](int buf, int kb) {
+    if (kb < K) {
+#pragma unroll
+      for (int e = 0; e < 8; ++e) {  // A: 32 k x 64 pairs of m
+        const int idx = tid + e * 256, kk = idx >> 6, mq = (idx & 63) * 2;
+        const int k = kb + kk;
+        const long long m = m0 + mq;
+        const bool v = k < K && m < M;
+        cp_async16(As + (buf * kTnBk + kk) * kNnNtLdA + mq, A + (v ? m + static_cast<long long>(k) * lda : 0), v);
+      }
+      for (int idx = tid; idx < 8 * NT * kTnBk; idx += 256) {  // B: 8 NT n x 32 k, one double each
+        const int row = idx >> 5, kk = idx & 31;
+        const int k = kb + kk, n = n0 + row;
+        const bool v = k < K && n < N;
+        cp_async8(Bs + (buf * 8 * NT + row) * kTnLd + kk, B + (v ? k + static_cast<long long>(n) * ldb : 0), v);
+      }
+    }
+    asm volatile("cp.async.commit_group;" ::: "memory");
+  };
+  double acc[2][NT][2];
+#pragma unroll
+  for (int i = 0; i < 2; ++i)
+#pragma unroll
+    for (int j = 0; j < NT; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+#pragma unroll
+  for (int p = 0; p < kNtStages - 1; ++p) stage(p, p * kTnBk);
+  int buf = 0;
+  for (int kb = 0; kb < K; kb += kTnBk) {
+    stage((buf + kNtStages - 1) % kNtStages, kb + (kNtStages - 1) * kTnBk);
+    asm volatile("cp.async.wait_group %0;" ::"n"(kNtStages - 1) : "memory");
+    __syncthreads();
+    const double* as = As + buf * kTnBk * kNnNtLdA + wm + fr;
+    const double* bs = Bs + (buf * 8 * NT + fr) * kTnLd;
+#pragma unroll
+    for (int ks = 0; ks < kTnBk; ks += 4) {
+      const double a0 = as[(ks + fc) * kNnNtLdA], a1 = as[(ks + fc) * kNnNtLdA + 8];
+#pragma unroll
+      for (int j = 0; j < NT; ++j) {
+        const double b = bs[8 * j * kTnLd + ks + fc];
+        dmma884(acc[0][j][0], acc[0][j][1], a0, b);
+        dmma884(acc[1][j][0], acc[1][j][1], a1, b);
+      }
+    }
+    __syncthreads();
+    buf = (buf + 1) % kNtStages;
+  }
+#pragma unroll
+  for (int i = 0; i < 2; ++i)
+#pragma unroll
+    for (int j = 0; j < NT; ++j)
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const long long m = m0 + wm + 8 * i + fr;
+        const int n = n0 + 8 * j + 2 * fc + h;
+        if (m < M && n < N) {
+          double* c = C + m + static_cast<long long>(n) * ldc;
+          *c = subtract ? *c - acc[i][j][h] : acc[i][j][h];
+        }
+      }
+}
+
 __global__ void __launch_bounds__(256) gemm_nn_dmma_pipe(long long M, int N, int K, const double* __restrict__ A,
                                                          long long lda, const double* __restrict__ B, long long ldb,
                                                          double* __restrict__ C, long long ldc, bool subtract) {
@@ -1643,6 +1722,30 @@ void gemm_nn(long long M, int N, int K, const double* A, long long lda, const do
     } else {
       gemm_nn_skinny_kernel<<<static_cast<unsigned>((M + 255) / 256), 256, 0, s>>>(M, N, K, A, lda, B, ldb, C, ldc,
                                                                                     subtract);
+    }
+    RTLR_CUDA(cudaGetLastError());
+    return;
+  }
+  static const bool nt_off = [] {  // RTLR_NN_NT=0: the 64 x 64 tile kernel (A/B timing)
+    const char* e = std::getenv("RTLR_NN_NT");
+    return e && e[0] == '0';
+  }();
+  // (N <= 32, e.g. the q = 16 candidate columns: 1.27 -> 0.89 ms at 1M x 16 x 600; wider
+  // products, e.g. the 128-angle verification blocks, run at ~80% of the fp64 tensor peak
+  // on the 64 x 64 tiles: 5.5 vs 6.2 ms at 1M x 128 x 600)
+  if (pipe_ok && !nt_off && N <= 32) {
+    const int nt = std::min(4, (N + 7) / 8);
+    const unsigned groups = static_cast<unsigned>((N + 8 * nt - 1) / (8 * nt));
+    const int smem = kNtStages * (kTnBk * kNnNtLdA + 8 * nt * kTnLd) * static_cast<int>(sizeof(double));
+    auto go = [&](auto kern) {
+      RTLR_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+      kern<<<dim3(groups, static_cast<unsigned>((M + kNtBm - 1) / kNtBm)), 256, smem, s>>>(M, N, K, A, lda, B, ldb,
+                                                                                            C, ldc, subtract);
+    };
+    switch (nt) {
+      case 2: go(gemm_nn_dmma_nt<2>); break;
+      case 3: go(gemm_nn_dmma_nt<3>); break;
+      default: go(gemm_nn_dmma_nt<4>); break;
     }
     RTLR_CUDA(cudaGetLastError());
     return;
