@@ -1711,7 +1711,12 @@ void gemm_nn(long long M, int N, int K, const double* A, long long lda, const do
   }
   // (a single k-stage, K <= 32 — the QR trailing updates — gains nothing from the pipeline)
   const bool pipe_ok = aligned16(A) && lda % 2 == 0 && M % 2 == 0 && K > kTnBk;
-  if (N <= 8 || (N <= kSkinny && !pipe_ok)) {
+  static const bool nt_off = [] {  // RTLR_NN_NT=0: the 64 x 64 tile / FFMA skinny kernels (A/B timing)
+    const char* e = std::getenv("RTLR_NN_NT");
+    return e && e[0] == '0';
+  }();
+  // (N = 8 with the pipeline's alignment — the CGS block updates — takes the DMMA tiles below)
+  if ((N <= 8 && !(pipe_ok && !nt_off && N == 8)) || (N <= kSkinny && !pipe_ok)) {
     if (aligned16(A) && lda % 2 == 0) {
       const unsigned grid = static_cast<unsigned>((M + 511) / 512);
       if (N == 1) gemm_nn_skinny2<1><<<grid, 256, 0, s>>>(M, N, K, A, lda, B, ldb, C, ldc, subtract);
@@ -1726,15 +1731,11 @@ void gemm_nn(long long M, int N, int K, const double* A, long long lda, const do
     RTLR_CUDA(cudaGetLastError());
     return;
   }
-  static const bool nt_off = [] {  // RTLR_NN_NT=0: the 64 x 64 tile kernel (A/B timing)
-    const char* e = std::getenv("RTLR_NN_NT");
-    return e && e[0] == '0';
-  }();
   // (N <= 32, e.g. the q = 16 candidate columns: 1.27 -> 0.89 ms at 1M x 16 x 600; wider
   // products, e.g. the 128-angle verification blocks, run at ~80% of the fp64 tensor peak
   // on the 64 x 64 tiles: 5.5 vs 6.2 ms at 1M x 128 x 600)
   if (pipe_ok && !nt_off && N <= 32) {
-    const int nt = std::min(4, (N + 7) / 8);
+    const int nt = std::min(4, (N + 7) / 8);  // (N = 8: the CGS block updates, 1 column tile)
     const unsigned groups = static_cast<unsigned>((N + 8 * nt - 1) / (8 * nt));
     const int smem = kNtStages * (kTnBk * kNnNtLdA + 8 * nt * kTnLd) * static_cast<int>(sizeof(double));
     auto go = [&](auto kern) {
@@ -1743,6 +1744,7 @@ void gemm_nn(long long M, int N, int K, const double* A, long long lda, const do
                                                                                             C, ldc, subtract);
     };
     switch (nt) {
+      case 1: go(gemm_nn_dmma_nt<1>); break;
       case 2: go(gemm_nn_dmma_nt<2>); break;
       case 3: go(gemm_nn_dmma_nt<3>); break;
       default: go(gemm_nn_dmma_nt<4>); break;
