@@ -18,6 +18,8 @@
 #include <cstdio>
 #include <string>
 
+#include <cooperative_groups.h>
+
 #include "dense.cuh"
 #include "problem.hpp"
 
@@ -245,6 +247,162 @@ __global__ void cgs_store(long long n, const double* __restrict__ v, const CgsSt
   for (long long e = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; e < n;
        e += static_cast<long long>(gridDim.x) * blockDim.x)
     col[e] = v[e] / h;
+}
+
+// The whole within-batch CGS of one batch in one cooperative launch
+// (kCgsParts CTAs x 256 threads, grid-wide barriers between dependent
+// steps) instead of ~13 launches per snapshot.  Every CTA reduces the
+// partials itself, in the order cgs_finish / dot_finish use, and the
+// per-thread index sets are those of cgs_dots / dot_partials, so the
+// results (and the CgsState the host reads) are bitwise those of the
+// launch-per-step sequence above.
+struct CgsNorms {
+  double v[kCgsMax];
+};
+
+__device__ __forceinline__ double cgs_warp_sum(double t) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
+  return t;
+}
+
+__global__ void __launch_bounds__(256, 2) cgs_batch_kernel(long long n, int p_in, CgsNorms norm0, double* __restrict__ R,
+                                                           double* __restrict__ X, long long ldx, CgsState* st,
+                                                           double* __restrict__ part, double* __restrict__ part2) {
+  namespace cg = cooperative_groups;
+  cg::grid_group grid = cg::this_grid();
+  __shared__ double sh[8][kCgsMax];
+  __shared__ double csh[kCgsMax];
+  __shared__ double red[8];
+  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+  const long long stride = static_cast<long long>(gridDim.x) * blockDim.x;
+  const long long i0 = blockIdx.x * static_cast<long long>(blockDim.x) + tid;
+  const bool lead = blockIdx.x == 0;
+  // sum over the kCgsParts partials part2[] as dot_finish does (one block of 256)
+  auto finish_dot = [&]() -> double {
+    double v = 0.0;
+    for (int z = tid; z < static_cast<int>(gridDim.x); z += blockDim.x) v += part2[z];
+    v = cgs_warp_sum(v);
+    __syncthreads();
+    if (lane == 0) red[w] = v;
+    __syncthreads();
+    double t = 0.0;
+    for (int ww = 0; ww < 8; ++ww) t += red[ww];
+    __syncthreads();
+    return t;
+  };
+  // this CTA's partial of sum v^2 (block_sum_all order) into part2[block]
+  auto store_norm_partial = [&](double sv) {
+    sv = cgs_warp_sum(sv);
+    __syncthreads();
+    if (lane == 0) red[w] = sv;
+    __syncthreads();
+    if (tid == 0) {
+      double t = 0.0;
+      for (int ww = 0; ww < 8; ++ww) t += red[ww];
+      part2[blockIdx.x] = t;
+    }
+    __syncthreads();
+  };
+  // one projection pass of v against X[:, 0:k]: dots, reduction, v -= X c
+  // fused with the partial of |v|^2; coef[i][:] += c
+  auto pass = [&](double* v, int k, int i) {
+    double acc[kCgsMax];
+#pragma unroll
+    for (int j = 0; j < kCgsMax; ++j) acc[j] = 0.0;
+    for (long long e = i0; e < n; e += stride) {
+      const double vi = v[e];
+#pragma unroll
+      for (int j = 0; j < kCgsMax; ++j)
+        if (j < k) acc[j] += X[e + j * ldx] * vi;
+    }
+#pragma unroll
+    for (int j = 0; j < kCgsMax; ++j) {
+      const double t = cgs_warp_sum(acc[j]);
+      if (lane == 0) sh[w][j] = t;
+    }
+    __syncthreads();
+    if (tid < k) {
+      double t = 0.0;
+      for (int ww = 0; ww < 8; ++ww) t += sh[ww][tid];
+      part[tid * gridDim.x + blockIdx.x] = t;
+    }
+    grid.sync();
+    for (int j = w; j < k; j += 8) {  // cgs_finish's order: lanes stride the partials, xor tree
+      double t = 0.0;
+      for (int z = lane; z < static_cast<int>(gridDim.x); z += 32) t += part[j * gridDim.x + z];
+      t = cgs_warp_sum(t);
+      if (lane == 0) csh[j] = t;
+    }
+    __syncthreads();
+    if (lead && tid < k) {
+      st->c[tid] = csh[tid];
+      st->coef[i][tid] += csh[tid];
+    }
+    double c[kCgsMax];
+#pragma unroll
+    for (int j = 0; j < kCgsMax; ++j) c[j] = j < k ? csh[j] : 0.0;
+    double sv = 0.0;
+    for (long long e = i0; e < n; e += stride) {
+      double s = 0.0;
+#pragma unroll
+      for (int j = 0; j < kCgsMax; ++j)
+        if (j < k) s += X[e + j * ldx] * c[j];
+      const double nv = v[e] - s;
+      v[e] = nv;
+      sv += nv * nv;
+    }
+    store_norm_partial(sv);
+    grid.sync();
+  };
+  auto norm_only = [&](const double* v) {
+    double sv = 0.0;
+    for (long long e = i0; e < n; e += stride) sv += v[e] * v[e];
+    store_norm_partial(sv);
+    grid.sync();
+  };
+  int k = 0;
+  for (int i = 0; i < p_in; ++i) {
+    double* rem = R + static_cast<long long>(i) * n;
+    double h2;
+    if (i > 0) {
+      if (k > 0)
+        pass(rem, k, i);
+      else
+        norm_only(rem);
+      const double rn2 = finish_dot();
+      const int do2 = k > 0 && sqrt(rn2) < 0.5 * norm0.v[i];
+      if (lead && tid == 0) {
+        st->rn2 = rn2;
+        st->do2 = do2;
+      }
+      if (do2) {
+        pass(rem, k, i);
+        h2 = finish_dot();
+      } else {
+        h2 = rn2;  // (dot(rem, rem) of the unchanged rem: the same partials, the same sum)
+      }
+    } else {
+      norm_only(rem);
+      h2 = finish_dot();
+    }
+    const double h = sqrt(h2);
+    const int acc = norm0.v[i] > 0.0 && h > 1e-12 * norm0.v[i];
+    const int pos = k;
+    if (lead && tid == 0) {
+      st->h2 = h2;
+      st->h[i] = h;
+      st->acc[i] = acc;
+      st->pos[i] = pos;
+      st->k = k + acc;
+    }
+    if (acc) {
+      double* col = X + static_cast<long long>(pos) * ldx;
+      for (long long e = i0; e < n; e += stride) col[e] = rem[e] / h;
+    }
+    k += acc;
+    grid.sync();  // the next snapshot projects against this column
+  }
 }
 
 int g1(long long n) {
@@ -481,7 +639,24 @@ bool LowRankEngine::mgs_ro_update(const double* snaps, const std::vector<int>& a
     CgsState* st = reinterpret_cast<CgsState*>(cgs_.ensure((sizeof(CgsState) + 7) / 8));
     RTLR_CUDA(cudaMemsetAsync(st, 0, sizeof(CgsState), s_));
     double* Xb = X_.col(r_old);
-    for (int i = 0; i < p_in; ++i) {
+    static const bool coop = [] {
+      int dev = 0, ok = 0;
+      cudaGetDevice(&dev);
+      cudaDeviceGetAttribute(&ok, cudaDevAttrCooperativeLaunch, dev);
+      const char* e = std::getenv("RTLR_CGS_COOP");
+      return ok != 0 && !(e && e[0] == '0');
+    }();
+    if (coop) {
+      CgsNorms nv{};
+      for (int i = 0; i < p_in; ++i) nv.v[i] = norm0[i];
+      long long nn = n_;
+      long long ldx = X_.ld;
+      double* part2 = dwork;
+      void* args[] = {&nn, const_cast<int*>(&p_in), &nv, &Rm, &Xb, &ldx, &st, &part, &part2};
+      RTLR_CUDA(cudaLaunchCooperativeKernel(reinterpret_cast<void*>(cgs_batch_kernel), dim3(kCgsParts), dim3(256), args,
+                                            0, s_));
+    }
+    for (int i = 0; i < p_in && !coop; ++i) {
       double* rem = Rm + static_cast<size_t>(i) * n_;
       if (i > 0) {
         cgs_dots<<<kCgsParts, 256, 0, s_>>>(n_, i, Xb, X_.ld, rem, st, false, part);
