@@ -5,6 +5,8 @@
 #include <stdexcept>
 #include <vector>
 
+#include <cooperative_groups.h>
+
 #include "dense.cuh"
 
 namespace rtlr {
@@ -1185,11 +1187,11 @@ __global__ void col_norm2_kernel(long long m, const double* __restrict__ w, long
   if (threadIdx.x == 0) out[blockIdx.x] = s;
 }
 
-__global__ void __launch_bounds__(256) jacobi_round(long long m, int n, int npad, int t, double* __restrict__ w,
-                                                    long long ldw, double* __restrict__ v, int* __restrict__ rotated,
-                                                    double tiny) {
-  __shared__ double sh[32];
-  const int pi = blockIdx.x;
+// One pair (p, q) of round t of the round-robin schedule; the pair index pi
+// runs over npad / 2 pairs.  Uniform within the CTA (block_sum_all).
+__device__ __forceinline__ void jacobi_pair(long long m, int n, int npad, int t, int pi, double* __restrict__ w,
+                                            long long ldw, double* __restrict__ v, int* __restrict__ rotated,
+                                            double tiny, double* sh) {
   int p = rr_player(pi, t, npad), q = rr_player(npad - 1 - pi, t, npad);
   if (p > q) {
     const int tmp = p;
@@ -1236,6 +1238,45 @@ __global__ void __launch_bounds__(256) jacobi_round(long long m, int n, int npad
       vp[i] = c * x - s * y;
       vq[i] = s * x + c * y;
     }
+  }
+}
+
+__global__ void __launch_bounds__(256) jacobi_round(long long m, int n, int npad, int t, double* __restrict__ w,
+                                                    long long ldw, double* __restrict__ v, int* __restrict__ rotated,
+                                                    double tiny) {
+  __shared__ double sh[32];
+  jacobi_pair(m, n, npad, t, blockIdx.x, w, ldw, v, rotated, tiny, sh);
+}
+
+// Every sweep of one SVD in one cooperative launch: the CTAs loop over the
+// pairs of a round, a grid-wide barrier separates the rounds, and after each
+// sweep every CTA reads the sweep's rotation count (three counters in turn,
+// so the one being reset was last read two sweeps ago).  Same pairs, same
+// arithmetic, same stopping rule as the per-round launches.
+// ctl: [0..2] rotation counters (ctl[0] zero at launch), [3] sweeps used,
+// [4] rotations in the last sweep.
+__global__ void __launch_bounds__(256) jacobi_sweeps_coop(long long m, int n, int npad, double* __restrict__ w,
+                                                          long long ldw, double* __restrict__ v, int* ctl, double tiny,
+                                                          int max_sweeps) {
+  namespace cg = cooperative_groups;
+  cg::grid_group grid = cg::this_grid();
+  __shared__ double sh[32];
+  int sweep = 0, last = 0;
+  while (sweep < max_sweeps) {
+    int* rot = ctl + sweep % 3;
+    if (blockIdx.x == 0 && threadIdx.x == 0) ctl[(sweep + 1) % 3] = 0;
+    for (int t = 0; t < npad - 1; ++t) {
+      for (int pi = blockIdx.x; pi < npad / 2; pi += gridDim.x)
+        jacobi_pair(m, n, npad, t, pi, w, ldw, v, rot, tiny, sh);
+      grid.sync();
+    }
+    last = *reinterpret_cast<volatile int*>(rot);
+    ++sweep;
+    if (last == 0) break;
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    ctl[3] = sweep;
+    ctl[4] = last;
   }
 }
 
@@ -1937,6 +1978,29 @@ void jacobi_svd(long long m, int n, double* w, long long ldw, double* v, int max
   RTLR_CUDA(cudaMemcpyAsync(n2.data(), d_n2, n * sizeof(double), cudaMemcpyDeviceToHost, s));
   RTLR_CUDA(cudaStreamSynchronize(s));
   const double tiny = 1e-30 * *std::max_element(n2.begin(), n2.end());
+  static const int coop_grid = [] {  // co-resident CTAs of the cooperative sweep kernel (0: unsupported)
+    int dev = 0, ok = 0, per = 0, sms = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&ok, cudaDevAttrCooperativeLaunch, dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, jacobi_sweeps_coop, 256, 0);
+    const char* e = std::getenv("RTLR_JACOBI_COOP");
+    return (ok && !(e && e[0] == '0')) ? per * sms : 0;
+  }();
+  if (coop_grid > 0) {
+    int* ctl = d_rot;  // 5 ints (work holds >= 8 doubles before d_n2)
+    RTLR_CUDA(cudaMemsetAsync(ctl, 0, 5 * sizeof(int), s));
+    int grid = std::min(npad / 2, coop_grid);
+    void* args[] = {&m, &n, const_cast<int*>(&npad), &w, &ldw, &v, &ctl, const_cast<double*>(&tiny), &max_sweeps};
+    RTLR_CUDA(cudaLaunchCooperativeKernel(reinterpret_cast<void*>(jacobi_sweeps_coop), dim3(grid), dim3(256), args, 0,
+                                          s));
+    int hc[5];
+    RTLR_CUDA(cudaMemcpyAsync(hc, ctl, sizeof(hc), cudaMemcpyDeviceToHost, s));
+    RTLR_CUDA(cudaStreamSynchronize(s));
+    if (sweeps_used) *sweeps_used = hc[3];
+    *host_rotated = hc[4];
+    return;
+  }
   // One sweep (npad - 1 dependent rounds, each a small launch) is captured
   // once as a CUDA graph and replayed per sweep: the rounds are
   // launch-latency bound, and a graph launch of the whole sweep costs about
