@@ -159,3 +159,38 @@ def test_psi_difference_matches_oracle():
     cmp = P.compare_runs(g.solve_full_rank(), g.solve_low_rank(), problem=g)
     assert cmp["has_psi_diff"] and cmp["psi_diff_two_norm"] <= 1e-5
     assert cmp["phi_diff_two_norm"] <= 1e-6 and 0 < cmp["compression_ratio"] < 1
+
+
+_SWITCH_RUN = r'''
+import sys, numpy as np
+sys.path.insert(0, sys.argv[1])
+sys.path.insert(0, sys.argv[1] + "/tests")
+import paper_2603_25233_b200 as P
+g = P.Problem("C2", nx=64, ny=64, n_theta=16, n_omega_z=8)
+r = g.solve_low_rank(build_factors=1)
+np.save(sys.argv[2], np.asarray(r.phi))
+'''
+
+
+@pytest.mark.parametrize("switch", ["RTLR_CGS_COOP", "RTLR_JACOBI_COOP", "RTLR_NN_NT", "RTLR_TN_NT", "RTLR_SWEEP_TMA"])
+def test_device_path_switches_keep_the_solve(switch, tmp_path):
+    """The fused / cooperative device paths against the launch-per-step and
+    64 x 64-tile paths they replaced (each switch is read once per process,
+    so each setting runs in its own process).  The cooperative CGS and
+    Jacobi kernels reduce in the same order: bitwise equal.  The GEMM tile
+    and sweep kernel choices change summation orders: within the LR
+    tolerance."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    out = {}
+    for v in ("1", "0"):
+        f = str(tmp_path / f"phi_{v}.npy")
+        env = dict(os.environ, **{switch: v})
+        subprocess.run([sys.executable, "-c", _SWITCH_RUN, root, f], env=env, check=True, timeout=600)
+        out[v] = np.load(f)
+    if switch in ("RTLR_CGS_COOP", "RTLR_JACOBI_COOP"):
+        assert np.array_equal(out["1"], out["0"])
+    else:
+        assert rel(out["1"], out["0"]) <= 1e-8
