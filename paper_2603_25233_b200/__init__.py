@@ -245,7 +245,10 @@ class Report:
 
     def __del__(self):
         if getattr(self, "h", None):
-            load_library().rtlr_cu_report_destroy(self.h)
+            try:
+                load_library().rtlr_cu_report_destroy(self.h)
+            except TypeError:  # interpreter shutdown: module globals already cleared
+                pass
             self.h = None
 
 
@@ -419,5 +422,8 @@ class Problem:
 
     def __del__(self):
         if getattr(self, "h", None):
-            load_library().rtlr_cu_problem_destroy(self.h)
+            try:
+                load_library().rtlr_cu_problem_destroy(self.h)
+            except TypeError:  # interpreter shutdown: module globals already cleared
+                pass
             self.h = None

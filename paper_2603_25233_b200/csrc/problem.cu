@@ -279,8 +279,8 @@ void Problem::sweep(const int* d_angles, int n, const double* d_rhs, long long r
   // for a handful of directions (the low-rank solver's p-direction batches,
   // latency-bound) the cluster wavefront, one thread-block cluster per
   // direction, with the cell blocks of a heterogeneous medium inverted ahead
-  // of it (launch_sweep_prefactor); otherwise the row-chunk scan kernel, one
-  // SM's warps per direction.
+  // of it (launch_sweep_prefactor); otherwise the row-chunk scan kernel in
+  // uniform media and the skewed wavefront in heterogeneous ones.
   static const int forced = [] {
     const char* e = std::getenv("RTLR_SWEEP");
     if (!e) return 0;
@@ -299,7 +299,11 @@ void Problem::sweep(const int* d_angles, int n, const double* d_rhs, long long r
     if (choice == 0 && cs > 0) choice = 4;
     if (choice == 4 && cluster == 0) cluster = cs > 0 ? cs : 2;
   }
-  if (choice == 0) choice = (!hp_.sigma_t_uniform && n <= 16 && hp_.nx % 2 == 0) ? 3 : 2;
+  // Heterogeneous media beyond what the clusters hold at once: the skewed
+  // wavefront's single-cell steps beat the row scan's per-cell LU inside the
+  // scan (C4: 1024 directions 13.7 vs 22.1 ms, 128: 2.8 vs 4.2 ms; C3: 576
+  // directions 2.35 vs 3.1 ms); up to 16 directions the prefactored scan.
+  if (choice == 0) choice = hp_.sigma_t_uniform ? 2 : (n <= 16 && hp_.nx % 2 == 0 ? 3 : 1);
   if (choice == 3 && (hp_.sigma_t_uniform || hp_.nx % 2 != 0)) choice = 2;  // nothing to factor / pairs unaligned
   if (choice == 4 && (hp_.nx * 16 * 8 + 8 * 1024 > 220 * 1024)) choice = 2;  // trace lines must fit shared memory
   if (choice == 1) {
