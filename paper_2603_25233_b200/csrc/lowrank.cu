@@ -525,7 +525,8 @@ class LowRankEngine {
   void update_projections(bool reorth);
   void galerkin(const std::vector<int>& angles, double* d_sol, long long ldsol);
   void galerkin_solve(const std::vector<int>& angles, double* d_sol, long long ldsol);
-  std::vector<double> residual_norms(const std::vector<int>& angles, const double* coeffs, long long ldc);
+  std::vector<double> residual_norms(const std::vector<int>& angles, const double* coeffs, long long ldc,
+                                     bool mirror_equal = false);
   void build_full_coefficients(const std::vector<int>* cand, const double* cand_sol);
   void phi_from_C();
   double host_dot(const double* a, const double* b, long long n);
@@ -555,8 +556,8 @@ class LowRankEngine {
   const double* dirs_;
   DMat X_;
   DBuf<double> proj_, prhs_, rhs_core_, phi_, phi_old_, rem_, vec_, C_, work_, snaps_, wbuf_, gbuf_, sol_, cand_,
-      ybuf_, nrm_, qa_, qq_, qr_, tau_, hrec_, luw_, gsol_, cgs_, svq_, svr_, svm_;
-  DBuf<int> ang_, ang2_, flags_, pos_;
+      ybuf_, nrm_, qa_, qq_, qr_, tau_, hrec_, luw_, gsol_, cgs_, svq_, svr_, svm_, rcoef_;
+  DBuf<int> ang_, ang2_, flags_, pos_, rfrom_;
   double* hbuf_ = nullptr;
   int rank_ = 0, n_snap_ = 0, prev_rank_ = 0;
   std::vector<std::vector<double>> rec_;
@@ -882,7 +883,34 @@ void LowRankEngine::galerkin_solve(const std::vector<int>& angles, double* d_sol
 // ||rhs_j - (D_j + Sigma_t) X c_j|| for the listed angles, expanded block-
 // wise (low_rank.cpp:283-307); coefficient column k belongs to angles[k].
 std::vector<double> LowRankEngine::residual_norms(const std::vector<int>& angles, const double* coeffs,
-                                                  long long ldc) {
+                                                  long long ldc, bool mirror_equal) {
+  // Mirror directions with equal coefficient columns (Galerkin solutions,
+  // copied per distinct system) have bitwise equal residuals: each distinct
+  // one is evaluated once (the GEMM and the per-angle reduction do not
+  // depend on a column's position in the block) and the norm copied.
+  if (mirror_equal && !hp_.bc_any && !angles.empty()) {
+    std::vector<int> reps, from, pos(angles.size()), seen(P_.uniq_rep_.size(), -1);
+    for (size_t k = 0; k < angles.size(); ++k) {
+      const int u = P_.uniq_of_[angles[k]];
+      if (seen[u] < 0) {
+        seen[u] = static_cast<int>(reps.size());
+        reps.push_back(angles[k]);
+        from.push_back(static_cast<int>(k));
+      }
+      pos[k] = seen[u];
+    }
+    if (reps.size() < angles.size()) {
+      const int nr = static_cast<int>(reps.size());
+      double* rc = rcoef_.ensure(static_cast<size_t>(rank_) * padded(nr));
+      int* df = upload_ints(rfrom_, from);
+      gather_cols<<<g1(static_cast<long long>(rank_) * nr), 256, 0, s_>>>(rank_, nr, df, coeffs, ldc, rc, rank_);
+      RTLR_CUDA(cudaGetLastError());
+      const std::vector<double> rn = residual_norms(reps, rc, rank_, false);
+      std::vector<double> out(angles.size());
+      for (size_t k = 0; k < angles.size(); ++k) out[k] = rn[pos[k]];
+      return out;
+    }
+  }
   // Sharded: this rank evaluates its block of the angles; the norms are
   // all-gathered (every rank then takes the same greedy decisions).
   const int m = static_cast<int>(angles.size());
@@ -1018,7 +1046,7 @@ InnerResult LowRankEngine::inner(const double* d_phi_prev, SubsampleRng& rng) {
     galerkin(cands, csol, rank_);
     pt_.stop();
     pt_.start("residual_q");
-    std::vector<double> norms = residual_norms(cands, csol, rank_);
+    std::vector<double> norms = residual_norms(cands, csol, rank_, /*mirror_equal=*/true);
     pt_.stop();
     std::vector<int> order(m);
     std::iota(order.begin(), order.end(), 0);
@@ -1050,7 +1078,7 @@ InnerResult LowRankEngine::inner(const double* d_phi_prev, SubsampleRng& rng) {
         gather_cols<<<g1(static_cast<long long>(rank_) * unsampled.size()), 256, 0, s_>>>(
             rank_, static_cast<int>(unsampled.size()), du, C_.get(), rank_, Cu, rank_);
         pt_.start("verify");
-        std::vector<double> vn = residual_norms(unsampled, Cu, rank_);
+        std::vector<double> vn = residual_norms(unsampled, Cu, rank_, /*mirror_equal=*/true);
         pt_.stop();
         std::vector<std::pair<double, int>> outstanding;
         for (size_t i = 0; i < unsampled.size(); ++i)
