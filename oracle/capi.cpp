@@ -211,7 +211,8 @@ long long oracle_problem_nnz(void* h, const char* which) {
 
 int oracle_problem_csr(void* h, const char* which, int* rowptr, int* colidx, double* val) {
   return guard([&] {
-    const Csr& m = pick_csr(static_cast<Problem*>(h), which);
+    const std::string w(which);
+    const Csr& m = pick_csr(static_cast<Problem*>(h), w);
     std::memcpy(rowptr, m.rowptr.data(), sizeof(int) * m.rowptr.size());
     std::memcpy(colidx, m.colidx.data(), sizeof(int) * m.colidx.size());
     std::memcpy(val, m.val.data(), sizeof(double) * m.val.size());
