@@ -1440,15 +1440,18 @@ __global__ void __launch_bounds__(NT) lu_panel_smem(int r, int k0, int jb, doubl
 // For one 64-column tile of the trailing columns (k0+jb .. r, the last one
 // the augmented rhs): the panel's row swaps, U12 = L11^-1 A12, then
 // A22 -= L21 U12 row tile by row tile.  grid (column tiles, systems).
-__global__ void __launch_bounds__(256) lu_trail(int r, int k0, int jb, double* __restrict__ M,
+constexpr int kTrailSmem = (3 * kNbMax * (BN + 8) + kNbMax * (kNbMax + 1)) * static_cast<int>(sizeof(double));
+__global__ void __launch_bounds__(256, 2) lu_trail(int r, int k0, int jb, double* __restrict__ M,
                                                 const int* __restrict__ perm) {
-  // row stride 72 (= 8 mod 16 doubles): the 4 k-rows x 8 lanes of a DMMA
-  // fragment load land in distinct banks.  The permutation staging at the
-  // start reuses the same buffer.
-  __shared__ double shbuf[2 * kNbMax * (BM + 8)];
-  __shared__ double L11[kNbMax][kNbMax + 1];
-  double (*Us)[BN + 8] = reinterpret_cast<double (*)[BN + 8]>(shbuf);
-  double (*Ls)[BM + 8] = reinterpret_cast<double (*)[BM + 8]>(shbuf + kNbMax * (BN + 8));
+  // dynamic shared memory (kTrailSmem): U12 [32][72], two L21 buffers
+  // [32][72] (the permutation staging at the start reuses them), L11
+  // [32][33].  Row stride 72 (= 8 mod 16 doubles): the 4 k-rows x 8 lanes of
+  // a DMMA fragment load land in distinct banks.
+  extern __shared__ double trail_sm[];
+  double* shbuf = trail_sm + kNbMax * (BN + 8);  // = the L21 buffers
+  double* lsbuf = shbuf;
+  double (*L11)[kNbMax + 1] = reinterpret_cast<double (*)[kNbMax + 1]>(trail_sm + 3 * kNbMax * (BN + 8));
+  double (*Us)[BN + 8] = reinterpret_cast<double (*)[BN + 8]>(trail_sm);
   double* A = M + static_cast<size_t>(blockIdx.y) * r * (r + 1);
   const int* pm = perm + static_cast<size_t>(blockIdx.y) * kPermInts;
   const int col0 = k0 + jb + blockIdx.x * BN;
@@ -1486,16 +1489,44 @@ __global__ void __launch_bounds__(256) lu_trail(int r, int k0, int jb, double* _
     for (int i = jb; i < kNbMax; ++i) Us[i][tid] = 0.0;
   }
   __syncthreads();
-  // A22 -= L21 U12 on DMMA: 8 warps as 2 x 4, 32 x 16 of the 64 x 64 tile each
+  // A22 -= L21 U12 on DMMA: 8 warps as 2 x 4, 32 x 16 of the 64 x 64 tile each.
+  // Software-pipelined over the row tiles: the next tile's L21 block streams
+  // into the other shared buffer (cp.async, 8-byte pieces: columns of an odd
+  // r are only 8-byte aligned) and this tile's 16 C values per thread are
+  // loaded before the tensor work, so neither latency sits on the chain.
   const int lane = tid & 31, warp = tid >> 5, fr = lane >> 2, fc = lane & 3;
   const int wm = (warp & 1) * 32, wn = (warp >> 1) * 16;
   const int ks_end = (jb + 3) & ~3;  // k past jb is zero-padded
-  for (int row0 = k0 + jb; row0 < r; row0 += BM) {
+  double (*Lb)[kNbMax][BM + 8] = reinterpret_cast<double (*)[kNbMax][BM + 8]>(lsbuf);
+  auto stage_l = [&](int buf, int row0) {
     for (int e = tid; e < kNbMax * BM; e += 256) {
       const int mm = e % BM, kk = e / BM;
       const int i = row0 + mm;
-      Ls[kk][mm] = (kk < jb && i < r) ? A[i + static_cast<size_t>(k0 + kk) * r] : 0.0;
+      const bool v = kk < jb && i < r;
+      cp_async8(&Lb[buf][kk][mm], A + (v ? i + static_cast<size_t>(k0 + kk) * r : 0), v);
     }
+    asm volatile("cp.async.commit_group;" ::: "memory");
+  };
+  const int rbeg = k0 + jb;
+  if (rbeg < r) stage_l(0, rbeg);
+  int buf = 0;
+  for (int row0 = rbeg; row0 < r; row0 += BM, buf ^= 1) {
+    const bool more = row0 + BM < r;
+    if (more) stage_l(buf ^ 1, row0 + BM);
+    double cin[4][2][2];
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+      for (int j = 0; j < 2; ++j)
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const int row = row0 + wm + 8 * i + fr, c = col0 + wn + 8 * j + 2 * fc + h;
+          cin[i][j][h] = (row < r && c <= r) ? A[row + static_cast<size_t>(c) * r] : 0.0;
+        }
+    if (more)
+      asm volatile("cp.async.wait_group 1;" ::: "memory");
+    else
+      asm volatile("cp.async.wait_group 0;" ::: "memory");
     __syncthreads();
     double acc[4][2][2];
 #pragma unroll
@@ -1505,7 +1536,7 @@ __global__ void __launch_bounds__(256) lu_trail(int r, int k0, int jb, double* _
     for (int ks = 0; ks < ks_end; ks += 4) {
       double a[4], b[2];
 #pragma unroll
-      for (int i = 0; i < 4; ++i) a[i] = Ls[ks + fc][wm + 8 * i + fr];
+      for (int i = 0; i < 4; ++i) a[i] = Lb[buf][ks + fc][wm + 8 * i + fr];
 #pragma unroll
       for (int j = 0; j < 2; ++j) b[j] = Us[ks + fc][wn + 8 * j + fr];
 #pragma unroll
@@ -1520,9 +1551,9 @@ __global__ void __launch_bounds__(256) lu_trail(int r, int k0, int jb, double* _
 #pragma unroll
         for (int h = 0; h < 2; ++h) {
           const int row = row0 + wm + 8 * i + fr, c = col0 + wn + 8 * j + 2 * fc + h;
-          if (row < r && c <= r) A[row + static_cast<size_t>(c) * r] -= acc[i][j][h];
+          if (row < r && c <= r) A[row + static_cast<size_t>(c) * r] = cin[i][j][h] - acc[i][j][h];
         }
-    __syncthreads();
+    __syncthreads();  // the buffer is refilled two tiles on
   }
 }
 
@@ -1852,12 +1883,13 @@ void galerkin_batch(int r, int m, const int* angles, const double* dirs, const d
     constexpr int kPanelThreads = 256;
     RTLR_CUDA(cudaFuncSetAttribute(lu_panel_smem<kPanelThreads>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                    kPanelSmemBytes));
+    RTLR_CUDA(cudaFuncSetAttribute(lu_trail, cudaFuncAttributeMaxDynamicSharedMemorySize, kTrailSmem));
     for (int k0 = 0; k0 < r;) {
       const int jb = lu_panel_width(r, k0);
       lu_panel_smem<kPanelThreads><<<m, kPanelThreads, static_cast<size_t>(r - k0) * (jb * sizeof(double) + 4), s>>>(
           r, k0, jb, M, piv, perm);
       const int ntrail = r + 1 - (k0 + jb);
-      if (ntrail > 0) lu_trail<<<dim3((ntrail + BN - 1) / BN, m), 256, 0, s>>>(r, k0, jb, M, perm);
+      if (ntrail > 0) lu_trail<<<dim3((ntrail + BN - 1) / BN, m), 256, kTrailSmem, s>>>(r, k0, jb, M, perm);
       k0 += jb;
     }
     // One CTA per system while the systems do not fill the GPU with warps;
