@@ -1471,6 +1471,15 @@ void launch_sweep_scan(const SweepArgs& a, bool uniform, cudaStream_t s) {
         p.mode = p.W > 1 ? kRows : kOne;
       }
     }
+    static const int forced_w = [] {  // RTLR_SCAN_W: warps per direction for row-interleaved plans (tuning)
+      const char* e = std::getenv("RTLR_SCAN_W");
+      const int v = e ? std::atoi(e) : 0;
+      return (v == 1 || v == 2 || v == 4 || v == 8) ? v : 0;
+    }();
+    if (forced_w && p.mode != kSplit && (forced_w == 1 || 2 * forced_w <= a.ny)) {
+      p.W = forced_w;
+      p.mode = forced_w > 1 ? kRows : kOne;
+    }
     p.smem = static_cast<size_t>(kWarps / p.W) * group_doubles(p.W, p.linew, p.smem_lines, wide) * sizeof(double);
     return p;
   };
@@ -1487,7 +1496,12 @@ void launch_sweep_scan(const SweepArgs& a, bool uniform, cudaStream_t s) {
   if (wide) {
     pl = plan_for(true);
     const size_t room = kScanSmemMax > pl.smem + 1024 ? kScanSmemMax - pl.smem - 1024 : 0;
-    stages = static_cast<int>(std::min<size_t>(kMaxStages, room / (static_cast<size_t>(kWarps) * kWTileBytes)));
+    static const int max_stages = [] {  // RTLR_SCAN_STAGES: cap on the TMA ring depth (tuning)
+      const char* e = std::getenv("RTLR_SCAN_STAGES");
+      const int v = e ? std::atoi(e) : 0;
+      return v >= 2 && v <= kMaxStages ? v : kMaxStages;
+    }();
+    stages = static_cast<int>(std::min<size_t>(max_stages, room / (static_cast<size_t>(kWarps) * kWTileBytes)));
     // Wide steps are longer: only when the directions (nearly) fill the
     // resident warp slots, i.e. the sweep is bandwidth-bound; a latency-bound
     // sweep of a few directions keeps the 64-cell steps (C5 256^2 x 256:
