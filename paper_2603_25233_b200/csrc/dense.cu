@@ -1676,6 +1676,60 @@ __global__ void __launch_bounds__(256) lu_backsolve_cta(int r, const double* __r
   if (tid == 0) flags[sys] = bad;
 }
 
+// R of a Householder QR (Eigen's makeHouseholder conventions, as hh_make)
+// in one cooperative launch, for the truncation SVD's W = C^T (N_Omega x r)
+// whose Q is not needed: column k's reflector is applied to every column
+// right of it by one warp per column (its own dot product, no cross-CTA
+// reduction); every warp derives beta / tau from its own identical
+// reduction of the column, so a step needs one grid-wide barrier.  Column
+// k is only read during step k, so nothing is written back to it; R (n x n,
+// upper) goes straight to r.
+__global__ void __launch_bounds__(256) qr_r_coop(long long m, int n, double* __restrict__ a, long long lda,
+                                                 double* __restrict__ r) {
+  namespace cg = cooperative_groups;
+  cg::grid_group grid = cg::this_grid();
+  const int lane = threadIdx.x & 31;
+  const int gw = static_cast<int>((blockIdx.x * blockDim.x + threadIdx.x) >> 5);
+  const int nw = static_cast<int>((gridDim.x * blockDim.x) >> 5);
+  const int kmax = static_cast<int>(min(static_cast<long long>(n), m));
+  for (int i = threadIdx.x + blockIdx.x * blockDim.x; i < n * n; i += gridDim.x * blockDim.x) r[i] = 0.0;
+  grid.sync();
+  for (int k = 0; k < kmax; ++k) {
+    const double* x = a + static_cast<long long>(k) * lda;
+    double sq = 0.0;
+    for (long long i = k + 1 + lane; i < m; i += 32) sq += x[i] * x[i];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) sq += __shfl_xor_sync(0xffffffffu, sq, o);
+    const double c0 = x[k];
+    double beta, tau, denom;
+    if (sq <= 2.2250738585072014e-308) {
+      tau = 0.0;
+      beta = c0;
+      denom = 0.0;
+    } else {
+      beta = sqrt(c0 * c0 + sq);
+      if (c0 >= 0.0) beta = -beta;
+      denom = c0 - beta;
+      tau = (beta - c0) / beta;
+    }
+    if (gw == 0 && lane == 0) r[k + static_cast<long long>(k) * n] = beta;
+    for (int j = k + 1 + gw; j < n; j += nw) {
+      double* col = a + static_cast<long long>(j) * lda;
+      double d = 0.0;
+      for (long long i = k + 1 + lane; i < m; i += 32) d += (denom == 0.0 ? 0.0 : x[i] / denom) * col[i];
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) d += __shfl_xor_sync(0xffffffffu, d, o);
+      const double w = tau * (col[k] + d);
+      for (long long i = k + 1 + lane; i < m; i += 32) col[i] -= w * (denom == 0.0 ? 0.0 : x[i] / denom);
+      if (lane == 0) {
+        col[k] -= w;
+        r[k + static_cast<long long>(j) * n] = col[k];
+      }
+    }
+    grid.sync();
+  }
+}
+
 }  // namespace
 
 size_t gemm_tn_work(int M, int N, long long K) {
@@ -1996,6 +2050,24 @@ void householder_qr(long long m, int n, double* a, long long lda, double* tau, d
     gemm_nn(rows, nq, jb, V, rows, W, jb, Qb, ldq, s, /*subtract=*/true);
   }
   RTLR_CUDA(cudaGetLastError());
+}
+
+bool householder_r_coop(long long m, int n, double* a, long long lda, double* r, cudaStream_t s) {
+  static const int grid = [] {  // co-resident CTAs (0: cooperative launch unsupported or disabled)
+    int dev = 0, ok = 0, per = 0, sms = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&ok, cudaDevAttrCooperativeLaunch, dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, qr_r_coop, 256, 0);
+    const char* e = std::getenv("RTLR_QR_COOP");
+    return (ok && !(e && e[0] == '0')) ? std::min(per, 2) * sms : 0;
+  }();
+  if (grid <= 0 || n <= 0) return false;
+  // one warp per column right of the current one; 8 warps per CTA
+  const int g = std::max(1, std::min(grid, (n + 7) / 8));
+  void* args[] = {&m, &n, &a, &lda, &r};
+  RTLR_CUDA(cudaLaunchCooperativeKernel(reinterpret_cast<void*>(qr_r_coop), dim3(g), dim3(256), args, 0, s));
+  return true;
 }
 
 void jacobi_svd(long long m, int n, double* w, long long ldw, double* v, int max_sweeps, int* host_rotated,

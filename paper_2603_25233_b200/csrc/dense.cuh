@@ -56,6 +56,11 @@ size_t householder_qr_work(long long m, int n);
 void householder_qr(long long m, int n, double* a, long long lda, double* tau, double* q, long long ldq,
                     double* r, double* work, size_t work_doubles, cudaStream_t s);
 
+// R only (n x n upper, into r) of the Householder QR of a (m x n, ld lda,
+// overwritten), in one cooperative launch; false if cooperative launches
+// are unavailable (or RTLR_QR_COOP=0) and nothing was done.
+bool householder_r_coop(long long m, int n, double* a, long long lda, double* r, cudaStream_t s);
+
 // One-sided Jacobi on the columns of w (m x n, ld), accumulating the
 // rotations in v (n x n) when given.  Afterwards columns of w are mutually
 // orthogonal: w = U diag(s), s = column norms.

@@ -1124,7 +1124,9 @@ std::vector<double> LowRankEngine::svd(bool vectors, int keep, std::vector<doubl
   double* R = svr_.ensure(static_cast<size_t>(ncols) * ncols);
   double* Mt = svm_.ensure(static_cast<size_t>(ncols) * ncols);
   double* tau = tau_.ensure(ncols);
-  {
+  // Singular values only (every outer iteration): R from the cooperative
+  // QR; with vectors (the last iteration) the blocked QR forms Q too.
+  if (vectors || !householder_r_coop(mrows, ncols, Wm, mrows, R, s_)) {
     double* qw = work(householder_qr_work(mrows, ncols));
     householder_qr(mrows, ncols, Wm, mrows, tau, Q, mrows, R, qw, work_.size(), s_);
   }
