@@ -172,7 +172,8 @@ np.save(sys.argv[2], np.asarray(r.phi))
 '''
 
 
-@pytest.mark.parametrize("switch", ["RTLR_CGS_COOP", "RTLR_JACOBI_COOP", "RTLR_NN_NT", "RTLR_TN_NT", "RTLR_SWEEP_TMA"])
+@pytest.mark.parametrize("switch", ["RTLR_CGS_COOP", "RTLR_JACOBI_COOP", "RTLR_QR_COOP", "RTLR_NN_NT", "RTLR_TN_NT",
+                                    "RTLR_SWEEP_TMA"])
 def test_device_path_switches_keep_the_solve(switch, tmp_path):
     """The fused / cooperative device paths against the launch-per-step and
     64 x 64-tile paths they replaced (each switch is read once per process,
