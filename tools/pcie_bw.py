@@ -1,3 +1,5 @@
+"""Pinned-host PCIe bandwidth on this box: H2D alone, D2H alone and both at
+once on two streams (2 GB each way) -- the bound of bench.py's e2e leg."""
 import torch, time
 n = 256 << 20  # 2 GB of doubles
 h1 = torch.empty(n, dtype=torch.float64, pin_memory=True); h2 = torch.empty(n, dtype=torch.float64, pin_memory=True)
