@@ -62,6 +62,26 @@ int rtlr_cu_config_set(rtlr_cu_config* cfg, const char* key, double value);
 /* which: "sigma_s" | "sigma_a" | "source" | "boundary" */
 int rtlr_cu_config_set_field(rtlr_cu_config* cfg, const char* which, rtlr_cu_field_fn fn, void* user);
 void rtlr_cu_config_destroy(rtlr_cu_config* cfg);
+/* parse_config_text / load_config_file (problem.cpp:329-459): "key = value"
+ * lines, '#' comments, "preset = name" resets the fields it covers (solver
+ * parameters and run.mode kept), FieldSpec keys "<field>.kind | value |
+ * outside | x0 | x1 | y0 | y1 | decay | center_x | center_y" for the
+ * reference presets; CONFIG_ERROR with the reference's messages. */
+int rtlr_cu_config_parse(const char* text, rtlr_cu_config** out);
+int rtlr_cu_config_load(const char* path, rtlr_cu_config** out);
+/* run.mode: "full" | "lowrank" | "both" (default both) */
+int rtlr_cu_config_set_mode(rtlr_cu_config* cfg, const char* mode);
+
+/* ---- run / run_assembled + write_outputs (report.cpp:60-195), the
+ * rtlr_bench driver (tools/rtlr_bench.cpp): assemble once on `device`, solve
+ * FR and/or LR per run.mode for the config's seed (nseeds = 0) or for each
+ * of `seeds`, compare FR and LR when both ran (psi difference on the GPU),
+ * write metrics.csv, history.csv and flux_{fr,lr}[_log][_<run_id>].txt into
+ * out_dir (skipped when out_dir is NULL or ""), and the printable summary
+ * into summary (NUL-terminated, truncated to summary_cap).  *all_converged
+ * = 0 when a driver hit its iteration cap (rtlr_bench exit code 2). */
+int rtlr_cu_run(const rtlr_cu_config* cfg, int device, const int64_t* seeds, int nseeds, const char* out_dir,
+                int log_flux, char* summary, size_t summary_cap, int* all_converged);
 
 /* ---- assemble_problem (problem.hpp:108, problem.cpp:461-483) + upload.
  * device < 0 assembles on the host only (inputs can be inspected with

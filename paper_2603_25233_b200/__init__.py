@@ -39,6 +39,7 @@ EXPORTS = [
     "rtlr_cu_partition_angles", "rtlr_cu_problem_fr_options", "rtlr_cu_problem_lr_options",
     "rtlr_cu_sweep_async", "rtlr_cu_check", "rtlr_cu_nccl_unique_id", "rtlr_cu_problem_set_comm",
     "rtlr_cu_shard_block", "rtlr_cu_dense_qr", "rtlr_cu_psi_difference",
+    "rtlr_cu_config_parse", "rtlr_cu_config_load", "rtlr_cu_config_set_mode", "rtlr_cu_run",
 ]
 
 
@@ -86,6 +87,11 @@ def load_library(path: str = LIB_PATH):
     L.rtlr_cu_config_create.argtypes = [ctypes.c_char_p, ctypes.POINTER(ctypes.c_void_p)]
     L.rtlr_cu_config_set.argtypes = [ctypes.c_void_p, ctypes.c_char_p, ctypes.c_double]
     L.rtlr_cu_config_destroy.argtypes = [ctypes.c_void_p]
+    L.rtlr_cu_config_parse.argtypes = [ctypes.c_char_p, ctypes.POINTER(ctypes.c_void_p)]
+    L.rtlr_cu_config_load.argtypes = [ctypes.c_char_p, ctypes.POINTER(ctypes.c_void_p)]
+    L.rtlr_cu_config_set_mode.argtypes = [ctypes.c_void_p, ctypes.c_char_p]
+    L.rtlr_cu_run.argtypes = [ctypes.c_void_p, ctypes.c_int, _I64, ctypes.c_int, ctypes.c_char_p, ctypes.c_int,
+                              ctypes.c_char_p, ctypes.c_size_t, ctypes.POINTER(ctypes.c_int)]
     L.rtlr_cu_problem_create.argtypes = [ctypes.c_void_p, ctypes.c_int, ctypes.POINTER(ctypes.c_void_p)]
     L.rtlr_cu_problem_destroy.argtypes = [ctypes.c_void_p]
     L.rtlr_cu_problem_info.argtypes = [ctypes.c_void_p, _I64]
@@ -252,6 +258,42 @@ class Report:
             self.h = None
 
 
+def _make_config(L, name, config_text=None, config_path=None):
+    cfg = ctypes.c_void_p()
+    if config_text is not None:
+        _check(L.rtlr_cu_config_parse(config_text.encode(), ctypes.byref(cfg)))
+    elif config_path is not None:
+        _check(L.rtlr_cu_config_load(os.fsencode(config_path), ctypes.byref(cfg)))
+    else:
+        _check(L.rtlr_cu_config_create(name.encode(), ctypes.byref(cfg)))
+    return cfg
+
+
+def run(preset: str = None, config_text: str = None, config_path: str = None, mode: str = None, seeds=None,
+        out_dir: str = None, device: int = 0, log_flux: bool = False, **overrides):
+    """The reference's run / rtlr_bench driver (report.cpp:60-195,
+    tools/rtlr_bench.cpp): FR and/or LR per run mode (the config's run.mode,
+    or `mode`), compared when both ran, for the config's seed or each of
+    `seeds`; writes metrics.csv, history.csv and the flux grids into out_dir
+    when given.  Returns (summary text, all drivers converged)."""
+    L = load_library()
+    cfg = _make_config(L, preset, config_text, config_path)
+    try:
+        for k, v in overrides.items():
+            _check(L.rtlr_cu_config_set(cfg, k.encode(), float(v)))
+        if mode is not None:
+            _check(L.rtlr_cu_config_set_mode(cfg, mode.encode()))
+        sd = np.ascontiguousarray(seeds if seeds is not None else [], dtype=np.int64)
+        buf = ctypes.create_string_buffer(1 << 16)
+        ok = ctypes.c_int(0)
+        _check(L.rtlr_cu_run(cfg, device, sd.ctypes.data_as(_I64) if len(sd) else None, len(sd),
+                             os.fsencode(out_dir) if out_dir else None, int(log_flux), buf, len(buf),
+                             ctypes.byref(ok)))
+    finally:
+        L.rtlr_cu_config_destroy(cfg)
+    return buf.value.decode(), bool(ok.value)
+
+
 class Problem:
     """An assembled problem resident on one GPU (AssembledProblem,
     proj/include/rtlr/problem.hpp:98-106).  `name` is a reference preset
@@ -259,10 +301,11 @@ class Problem:
     keyword overrides use the reference's config keys.  device < 0 assembles
     on the host only (inputs inspectable, no GPU calls)."""
 
-    def __init__(self, name: str, device: int = 0, **overrides):
+    def __init__(self, name: str = None, device: int = 0, config_text: str = None, **overrides):
+        """config_text: a reference config file's contents (key = value lines,
+        parse_config_text) instead of a preset name."""
         L = load_library()
-        cfg = ctypes.c_void_p()
-        _check(L.rtlr_cu_config_create(name.encode(), ctypes.byref(cfg)))
+        cfg = _make_config(L, name, config_text)
         try:
             for k, v in overrides.items():
                 _check(L.rtlr_cu_config_set(cfg, k.encode(), float(v)))

@@ -78,7 +78,24 @@ def build(verbose: bool = False) -> str:
         r = subprocess.run(cmd, capture_output=True, text=True)
         if r.returncode != 0:
             raise RuntimeError(f"link failed:\n{r.stdout}\n{r.stderr}")
+    _build_cli()
     return LIB
+
+
+CLI_SRC = os.path.join(PKG, "cli", "rtlr_cu_bench.cpp")
+CLI = os.path.join(LIB_DIR, "rtlr_cu_bench")
+
+
+def _build_cli():
+    """The rtlr_bench driver (C ABI only) next to the library it links."""
+    if os.path.exists(CLI) and os.path.getmtime(CLI) >= max(os.path.getmtime(CLI_SRC), os.path.getmtime(LIB)):
+        return
+    nccl = [a for a in _nccl_link() if a.startswith("-L")]
+    cmd = ["g++", "-O2", "-std=c++17", "-I", os.path.join(os.path.dirname(PKG), "include"), CLI_SRC, "-o", CLI,
+           "-L" + LIB_DIR, "-lrtlr_cu", "-Wl,-rpath,$ORIGIN"] + ["-Wl,-rpath-link," + a[2:] for a in nccl]
+    r = subprocess.run(cmd, capture_output=True, text=True)
+    if r.returncode != 0:
+        raise RuntimeError(f"cli build failed:\n{r.stdout}\n{r.stderr}")
 
 
 if __name__ == "__main__":

@@ -7,12 +7,14 @@
 
 #include "../../include/rtlr_cu.h"
 #include "dense.cuh"
+#include "harness.hpp"
 #include "problem.hpp"
 
 using namespace rtlr::cuda;
 
 struct rtlr_cu_config {
   ProblemConfig cfg;
+  RunMode mode = RunMode::Both;  // run.mode (problem.hpp:83)
 };
 struct rtlr_cu_problem {
   std::unique_ptr<Problem> p;
@@ -179,6 +181,70 @@ int rtlr_cu_config_set_field(rtlr_cu_config* cfg, const char* which, rtlr_cu_fie
 }
 
 void rtlr_cu_config_destroy(rtlr_cu_config* cfg) { delete cfg; }
+
+int rtlr_cu_config_parse(const char* text, rtlr_cu_config** out) {
+  return guard([&] {
+    need(text && out, "config: null argument");
+    RunConfig rc = parse_config_text(text);
+    auto c = std::make_unique<rtlr_cu_config>();
+    c->cfg = std::move(rc.cfg);
+    c->mode = rc.mode;
+    *out = c.release();
+  });
+}
+
+int rtlr_cu_config_load(const char* path, rtlr_cu_config** out) {
+  return guard([&] {
+    need(path && out, "config: null argument");
+    RunConfig rc = load_config_file(path);
+    auto c = std::make_unique<rtlr_cu_config>();
+    c->cfg = std::move(rc.cfg);
+    c->mode = rc.mode;
+    *out = c.release();
+  });
+}
+
+int rtlr_cu_config_set_mode(rtlr_cu_config* cfg, const char* mode) {
+  return guard([&] {
+    need(cfg && mode, "config: null argument");
+    cfg->mode = run_mode_from_name(mode);
+  });
+}
+
+int rtlr_cu_run(const rtlr_cu_config* cfg, int device, const int64_t* seeds, int nseeds, const char* out_dir,
+                int log_flux, char* summary, size_t summary_cap, int* all_conv) {
+  return guard([&] {
+    need(cfg != nullptr && (nseeds == 0 || seeds != nullptr) && nseeds >= 0, "run: bad argument");
+    validate_config(cfg->cfg);
+    RunConfig rc{cfg->cfg, cfg->mode};
+    std::vector<RunResult> results;
+    std::string text;
+    {
+      Problem P(rc.cfg, device);  // assembled once for every seed (rtlr_bench batch)
+      if (nseeds == 0) {
+        results.push_back(run_assembled(rc, P));
+        text += run_summary(results.back());
+      } else {
+        for (int i = 0; i < nseeds; ++i) {
+          RunConfig c = rc;
+          c.cfg.solver.seed = static_cast<std::uint64_t>(seeds[i]);
+          results.push_back(run_assembled(c, P));
+          text += run_summary(results.back());
+        }
+        text += batch_summary(results);
+      }
+    }
+    if (out_dir && *out_dir) write_outputs(results, out_dir, log_flux != 0);
+    bool ok = true;
+    for (const RunResult& r : results) ok = ok && all_converged(r);
+    if (all_conv) *all_conv = ok ? 1 : 0;
+    if (summary && summary_cap > 0) {
+      const size_t n = std::min(summary_cap - 1, text.size());
+      std::memcpy(summary, text.data(), n);
+      summary[n] = 0;
+    }
+  });
+}
 
 int rtlr_cu_problem_create(const rtlr_cu_config* cfg, int device, rtlr_cu_problem** out) {
   return guard([&] {
