@@ -476,7 +476,7 @@ __global__ void __launch_bounds__(256) gemm_tn_dmma_pipe(int M, int N, long long
 // idles on padding columns and B is re-read once per 128 (not 64) columns
 // of A.  Three-stage cp.async pipeline of 128 x 32 A and 48 x 32 B tiles.
 // Same alignment contract and split-K partials as gemm_tn_dmma_pipe.
-constexpr int kNtBm = 128, kNtStages = 3, kNtMaxN = 48;
+constexpr int kNtBm = 128, kNtStages = 2, kNtMaxN = 48;
 template <int NT>
 __global__ void __launch_bounds__(256) gemm_tn_dmma_nt(int M, int N, long long K, long long kchunk,
                                                        const double* __restrict__ A, long long lda,
