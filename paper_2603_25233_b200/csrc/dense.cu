@@ -470,11 +470,13 @@ __global__ void __launch_bounds__(256) gemm_tn_dmma_pipe(int M, int N, long long
       }
 }
 
-// A^T B for 8 < N <= 48 (the border-extension products X^T [5p stencil
+// A^T B for 4 <= N <= 48 (the border-extension products X^T [5p stencil
 // images]: N = 40 at p = 8, 20 at p = 4): 128 columns of A per CTA, every
 // warp owns 16 of them against all ceil(N/8) column tiles of B, so no warp
 // idles on padding columns and B is re-read once per 128 (not 64) columns
-// of A.  Three-stage cp.async pipeline of 128 x 32 A and 48 x 32 B tiles.
+// of A.  Two-stage cp.async pipeline of 128 x 32 A and up to 48 x 32 B tiles (two CTAs
+// per SM; three stages with one CTA were 17% slower).  Also the CGS projections
+// with 4-8 columns (one padded column tile).
 // Same alignment contract and split-K partials as gemm_tn_dmma_pipe.
 constexpr int kNtBm = 128, kNtStages = 2, kNtMaxN = 48;
 template <int NT>
@@ -561,7 +563,7 @@ __device__ __forceinline__ void cp_async8(double* smem_dst, const double* src, b
 // C (-)= A B for N > 8 with 128-row tiles: every warp owns 16 rows against
 // all NT column tiles of its CTA's column group (8 NT columns; column groups
 // of the same rows are adjacent in launch order, so A is re-read from L2),
-// three-stage cp.async pipeline.  A staged [k][m] with row stride 132
+// two-stage cp.async pipeline.  A staged [k][m] with row stride 132
 // doubles (the fragment loads' half-warps hit distinct banks).  Same
 // contract as gemm_nn_dmma_pipe.
 constexpr int kNnNtLdA = kNtBm + 4;
@@ -1733,7 +1735,7 @@ __global__ void __launch_bounds__(256) qr_r_coop(long long m, int n, double* __r
 }  // namespace
 
 size_t gemm_tn_work(int M, int N, long long K) {
-  const long long sp = N > 8 && N <= kNtMaxN && static_cast<double>(M) * N * K >= 1e9
+  const long long sp = N >= 4 && N <= kNtMaxN && static_cast<double>(M) * N * K >= 1e9
                            ? std::max<long long>(nt_splits(M, K), tn_splits(M, N, K))
                                               : tn_splits(M, N, K);
   return static_cast<size_t>(sp) * M * N;
@@ -1780,7 +1782,7 @@ void gemm_tn(int M, int N, long long K, const double* A, long long lda, const do
     return e && e[0] == '0';
   }();
   // (small products, e.g. C2's 178 x 20 x 65536, stay on the 64 x 64 tiles: 46 vs 54 us)
-  if (pipe_ok && N > 8 && N <= kNtMaxN && !nt_off && static_cast<double>(M) * N * K >= 1e9) {
+  if (pipe_ok && N >= 4 && N <= kNtMaxN && !nt_off && static_cast<double>(M) * N * K >= 1e9) {
     // (own split count: 128-row tiles, ~4 CTAs per SM; still a function of the shape only)
     const long long tiles = (M + kNtBm - 1) / kNtBm;
     long long sp = nt_splits(M, K);
@@ -1798,6 +1800,7 @@ void gemm_tn(int M, int N, long long K, const double* A, long long lda, const do
                                                                                           ldb, o2, ldo2, ss2);
     };
     switch (nt) {
+      case 1: go(gemm_tn_dmma_nt<1>); break;
       case 2: go(gemm_tn_dmma_nt<2>); break;
       case 3: go(gemm_tn_dmma_nt<3>); break;
       case 4: go(gemm_tn_dmma_nt<4>); break;
