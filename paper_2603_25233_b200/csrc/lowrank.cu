@@ -640,12 +640,14 @@ bool LowRankEngine::mgs_ro_update(const double* snaps, const std::vector<int>& a
     CgsState* st = reinterpret_cast<CgsState*>(cgs_.ensure((sizeof(CgsState) + 7) / 8));
     RTLR_CUDA(cudaMemsetAsync(st, 0, sizeof(CgsState), s_));
     double* Xb = X_.col(r_old);
-    static const bool coop = [] {
-      int dev = 0, ok = 0;
+    static const bool coop = [] {  // (all kCgsParts CTAs must be co-resident)
+      int dev = 0, ok = 0, per = 0, sms = 0;
       cudaGetDevice(&dev);
       cudaDeviceGetAttribute(&ok, cudaDevAttrCooperativeLaunch, dev);
+      cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, cgs_batch_kernel, 256, 0);
       const char* e = std::getenv("RTLR_CGS_COOP");
-      return ok != 0 && !(e && e[0] == '0');
+      return ok != 0 && per * sms >= kCgsParts && !(e && e[0] == '0');
     }();
     if (coop) {
       CgsNorms nv{};
