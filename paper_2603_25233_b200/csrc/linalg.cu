@@ -214,18 +214,64 @@ __global__ void pcg_check_zero(const PcgArgs a) {
   }
 }
 
-// q = A p; partials of p.q
+// Two adjacent cells of bsr_row at once: the SoA matrix entries of the pair
+// as one 16-byte load (ncell even), each cell's neighbours as bsr_row has
+// them; per cell the same products in the same order.
+__device__ __forceinline__ void bsr_row_pair(const PcgArgs& a, int c, const double* x, double y0[4], double y1[4]) {
+  const int ax = c % a.nx, by = c / a.nx;
+  const int c1 = c + 1, ax1 = c1 % a.nx, by1 = c1 / a.nx;
+  const int nb0[5] = {c, ax > 0 ? c - 1 : -1, ax + 1 < a.nx ? c + 1 : -1, by > 0 ? c - a.nx : -1,
+                      by + 1 < a.ny ? c + a.nx : -1};
+  const int nb1[5] = {c1, ax1 > 0 ? c1 - 1 : -1, ax1 + 1 < a.nx ? c1 + 1 : -1, by1 > 0 ? c1 - a.nx : -1,
+                      by1 + 1 < a.ny ? c1 + a.nx : -1};
+#pragma unroll
+  for (int i = 0; i < 4; ++i) y0[i] = y1[i] = 0.0;
+#pragma unroll
+  for (int s = 0; s < 5; ++s) {
+    double v0[4] = {0, 0, 0, 0}, v1[4] = {0, 0, 0, 0};
+    if (nb0[s] >= 0) ld4(x + 4 * static_cast<size_t>(nb0[s]), v0);
+    if (nb1[s] >= 0) ld4(x + 4 * static_cast<size_t>(nb1[s]), v1);
+#pragma unroll
+    for (int j = 0; j < 4; ++j)
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const double2 m = __ldg(reinterpret_cast<const double2*>(a.sip + static_cast<size_t>(s * 16 + j * 4 + i) * a.ncell + c));
+        if (nb0[s] >= 0) y0[i] += m.x * v0[j];
+        if (nb1[s] >= 0) y1[i] += m.y * v1[j];
+      }
+  }
+}
+
+// q = A p; partials of p.q.  Two cells per thread when ncell is even (16-byte
+// matrix loads, twice the bytes in flight per thread).
 __global__ void pcg_spmv(const PcgArgs a) {
   if (a.state->done) return;
   __shared__ double sh[40];
   double pq = 0.0;
-  for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < a.ncell; c += gridDim.x * blockDim.x) {
-    double y[4], p[4];
-    bsr_row(a, c, a.p, y);
-    st4(a.q + 4 * static_cast<size_t>(c), y);
-    ld4(a.p + 4 * static_cast<size_t>(c), p);
+  if ((a.ncell & 1) == 0) {
+    const int npair = a.ncell / 2;
+    for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < npair; t += gridDim.x * blockDim.x) {
+      const int c = 2 * t;
+      double y0[4], y1[4], p0[4], p1[4];
+      bsr_row_pair(a, c, a.p, y0, y1);
+      st4(a.q + 4 * static_cast<size_t>(c), y0);
+      st4(a.q + 4 * static_cast<size_t>(c + 1), y1);
+      ld4(a.p + 4 * static_cast<size_t>(c), p0);
+      ld4(a.p + 4 * static_cast<size_t>(c + 1), p1);
 #pragma unroll
-    for (int i = 0; i < 4; ++i) pq += p[i] * y[i];
+      for (int i = 0; i < 4; ++i) pq += p0[i] * y0[i];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) pq += p1[i] * y1[i];
+    }
+  } else {
+    for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < a.ncell; c += gridDim.x * blockDim.x) {
+      double y[4], p[4];
+      bsr_row(a, c, a.p, y);
+      st4(a.q + 4 * static_cast<size_t>(c), y);
+      ld4(a.p + 4 * static_cast<size_t>(c), p);
+#pragma unroll
+      for (int i = 0; i < 4; ++i) pq += p[i] * y[i];
+    }
   }
   pq = block_sum(pq, sh);
   if (threadIdx.x == 0) a.part_pq[blockIdx.x] = pq;
