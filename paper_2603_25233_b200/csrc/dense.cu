@@ -851,34 +851,59 @@ __device__ __forceinline__ double col_mv(const double* B, int i, const double* v
   return B[4 * i] * v[0] + B[4 * i + 1] * v[1] + B[4 * i + 2] * v[2] + B[4 * i + 3] * v[3];
 }
 
+// One thread per (cell, column): the cell's four DOFs of all five products,
+// its own and neighbour coefficients as 16-byte loads, 2-D grid (cells x
+// columns, no 64-bit index division).  Per output the same row_mv / col_mv
+// arithmetic as before.
 __global__ void stream_products_kernel(const StencilArgs A, int p, const double* __restrict__ P, long long ldp,
                                        double* __restrict__ W, long long ldw) {
-  const long long ndof = 4LL * A.ncell;
-  const long long total = ndof * p;
-  for (long long e = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; e < total;
-       e += static_cast<long long>(gridDim.x) * blockDim.x) {
-    const int j = static_cast<int>(e / ndof);
-    const long long r = e % ndof;
-    const int c = static_cast<int>(r >> 2), i = static_cast<int>(r & 3);
-    const int a = c % A.nx, b = c / A.nx;
-    const double* pc = P + j * ldp + 4LL * c;
-    const long long up = 4LL * A.nx;
-    double dxm = row_mv(A.sc.ax_minus, i, pc);
-    if (a > 0) dxm += row_mv(A.sc.bx_minus, i, pc - 4);
-    double dxmt = col_mv(A.sc.ax_minus, i, pc);
-    if (a + 1 < A.nx) dxmt += col_mv(A.sc.bx_minus, i, pc + 4);
-    double dym = row_mv(A.sc.ay_minus, i, pc);
-    if (b > 0) dym += row_mv(A.sc.by_minus, i, pc - up);
-    double dymt = col_mv(A.sc.ay_minus, i, pc);
-    if (b + 1 < A.ny) dymt += col_mv(A.sc.by_minus, i, pc + up);
-    const double st = row_mv(A.sigma_t + 16LL * c, i, pc);
-    const long long o = r + j * ldw;
-    const long long blk = p * ldw;
-    W[o] = dxm;
-    W[o + blk] = dxmt;
-    W[o + 2 * blk] = dym;
-    W[o + 3 * blk] = dymt;
-    W[o + 4 * blk] = st;
+  const int c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= A.ncell) return;
+  const int j = blockIdx.y;
+  const int a = c % A.nx, b = c / A.nx;
+  const double* pc = P + j * ldp + 4LL * c;
+  const long long up = 4LL * A.nx;
+  auto ld4v = [](const double* q, double v[4]) {
+    const double2 x = __ldg(reinterpret_cast<const double2*>(q)), y = __ldg(reinterpret_cast<const double2*>(q) + 1);
+    v[0] = x.x, v[1] = x.y, v[2] = y.x, v[3] = y.y;
+  };
+  double v[4], w[4] = {0, 0, 0, 0}, e[4] = {0, 0, 0, 0}, s[4] = {0, 0, 0, 0}, n[4] = {0, 0, 0, 0}, st[16];
+  ld4v(pc, v);
+  if (a > 0) ld4v(pc - 4, w);
+  if (a + 1 < A.nx) ld4v(pc + 4, e);
+  if (b > 0) ld4v(pc - up, s);
+  if (b + 1 < A.ny) ld4v(pc + up, n);
+  const double2* sb = reinterpret_cast<const double2*>(A.sigma_t + 16LL * c);
+#pragma unroll
+  for (int k = 0; k < 8; ++k) {
+    const double2 t = __ldg(sb + k);
+    st[2 * k] = t.x;
+    st[2 * k + 1] = t.y;
+  }
+  double out[5][4];
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    double dxm = row_mv(A.sc.ax_minus, i, v);
+    if (a > 0) dxm += row_mv(A.sc.bx_minus, i, w);
+    double dxmt = col_mv(A.sc.ax_minus, i, v);
+    if (a + 1 < A.nx) dxmt += col_mv(A.sc.bx_minus, i, e);
+    double dym = row_mv(A.sc.ay_minus, i, v);
+    if (b > 0) dym += row_mv(A.sc.by_minus, i, s);
+    double dymt = col_mv(A.sc.ay_minus, i, v);
+    if (b + 1 < A.ny) dymt += col_mv(A.sc.by_minus, i, n);
+    out[0][i] = dxm;
+    out[1][i] = dxmt;
+    out[2][i] = dym;
+    out[3][i] = dymt;
+    out[4][i] = row_mv(st, i, v);
+  }
+  const long long blk = p * ldw;
+  double* o = W + 4LL * c + j * ldw;
+#pragma unroll
+  for (int k = 0; k < 5; ++k) {
+    double2* q = reinterpret_cast<double2*>(o + k * blk);
+    q[0] = make_double2(out[k][0], out[k][1]);
+    q[1] = make_double2(out[k][2], out[k][3]);
   }
 }
 
@@ -1918,7 +1943,10 @@ void axpy_dev(long long n, const double* alpha, double sign, const double* x, do
 void stream_products(const StencilArgs& a, int p, const double* P, long long ldp, double* W, long long ldw,
                      cudaStream_t s) {
   if (p <= 0) return;
-  stream_products_kernel<<<grid1d(4LL * a.ncell * p), 256, 0, s>>>(a, p, P, ldp, W, ldw);
+  if ((ldp & 1) || (ldw & 1) || !aligned16(P) || !aligned16(W))
+    throw std::invalid_argument("stream_products: P, W and their leading dimensions must be 16-byte aligned");
+  stream_products_kernel<<<dim3(static_cast<unsigned>((a.ncell + 255) / 256), static_cast<unsigned>(p)), 256, 0, s>>>(
+      a, p, P, ldp, W, ldw);
   RTLR_CUDA(cudaGetLastError());
 }
 
