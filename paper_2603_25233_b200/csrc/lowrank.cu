@@ -503,7 +503,7 @@ class LowRankEngine {
   int svd_sweeps_ = 0, svd_calls_ = 0;
   long long gal_calls_ = 0, gal_systems_ = 0;
   double reorth_seconds_ = 0.0;  // their wall time (meaningful with RTLR_PROFILE=1)
-  double cgs_split_[3] = {0, 0, 0};  // RTLR_PROFILE: block GEMMs / per-snapshot loop / overlap check
+  double cgs_split_[4] = {0, 0, 0, 0};  // RTLR_PROFILE: block GEMMs + host / per-snapshot loop / overlap / GEMMs only
   void lap(int slot, std::chrono::steady_clock::time_point& t) {
     if (!pt_.on) return;
     RTLR_CUDA(cudaStreamSynchronize(s_));
@@ -616,10 +616,17 @@ bool LowRankEngine::mgs_ro_update(const double* snaps, const std::vector<int>& a
   if (r_old > 0) {
     double* C1 = gbuf_.ensure(static_cast<size_t>(2) * r_old * p_in);
     double* C2 = C1 + static_cast<size_t>(r_old) * p_in;
+    auto tg = std::chrono::steady_clock::now();
+    if (pt_.on) RTLR_CUDA(cudaStreamSynchronize(s_));
+    tg = std::chrono::steady_clock::now();
+    // (the second pass is unconditional: with the reference's test
+    // |rem| < 0.5 |psi| some snapshot of the batch needs it in 97-100% of
+    // the batches at C2-C4, and the test itself cost more than it saved)
     tn(r_old, p_in, X_.col(0), X_.ld, snaps, n_, C1, r_old);
     gemm_nn(n_, p_in, r_old, X_.col(0), X_.ld, C1, r_old, Rm, n_, s_, /*subtract=*/true);
     tn(r_old, p_in, X_.col(0), X_.ld, Rm, n_, C2, r_old);
     gemm_nn(n_, p_in, r_old, X_.col(0), X_.ld, C2, r_old, Rm, n_, s_, /*subtract=*/true);
+    lap(3, tg);
     std::vector<double> h1(static_cast<size_t>(r_old) * p_in), h2(h1.size());
     RTLR_CUDA(cudaMemcpyAsync(h1.data(), C1, h1.size() * sizeof(double), cudaMemcpyDeviceToHost, s_));
     RTLR_CUDA(cudaMemcpyAsync(h2.data(), C2, h2.size() * sizeof(double), cudaMemcpyDeviceToHost, s_));
@@ -1289,9 +1296,9 @@ SolveReport Problem::solve_low_rank(const LowRankOptions& o) {
     std::fprintf(stderr, "[rtlr profile] low-rank phases (s):");
     for (auto& e : eng.pt_.acc) std::fprintf(stderr, " %s=%.4f", e.first.c_str(), e.second);
     std::fprintf(stderr,
-                 " | reorth: %d rebuilds, %.4f s (inside cgs) | cgs: block %.4f, per-snapshot %.4f | svd: %d calls, "
+                 " | reorth: %d rebuilds, %.4f s (inside cgs) | cgs: block %.4f (GEMMs %.4f), per-snapshot %.4f | svd: %d calls, "
                  "%d Jacobi sweeps | galerkin: %lld batches, %lld systems\n",
-                 eng.reorth_count_, eng.reorth_seconds_, eng.cgs_split_[0], eng.cgs_split_[1], eng.svd_calls_,
+                 eng.reorth_count_, eng.reorth_seconds_, eng.cgs_split_[0], eng.cgs_split_[3], eng.cgs_split_[1], eng.svd_calls_,
                  eng.svd_sweeps_, eng.gal_calls_, eng.gal_systems_);
   }
   rep.phi.resize(n);
