@@ -1371,6 +1371,8 @@ __global__ void __launch_bounds__(NT) lu_panel_smem(int r, int k0, int jb, doubl
   double* A = M + static_cast<size_t>(blockIdx.x) * r * (r + 1);
   int* pv = piv + static_cast<size_t>(blockIdx.x) * r;
   const int rows = r - k0, tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  constexpr int kHalf = kNbMax / 2;
+  const bool split = jb > kHalf && rows > kHalf;
   for (int e = tid; e < rows * jb; e += NT) {
     const int i = e % rows, c = e / rows;
     P[e] = A[k0 + i + static_cast<size_t>(k0 + c) * r];
@@ -1411,14 +1413,50 @@ __global__ void __launch_bounds__(NT) lu_panel_smem(int r, int k0, int jb, doubl
     const double d = colj[j];
     double best = -1.0;
     int bi = rows;
+    // Two halves of kHalf columns: the first half's rank-1 updates stop at
+    // its own last column; its effect on the second half is applied once,
+    // as a TRSM on the half's rows and a register-accumulated update of the
+    // rows below (the same subtractions in the same order per element, on
+    // the rows as the swaps left them: bitwise the unblocked factors).
+    const int cend = (split && j < kHalf) ? kHalf : jb;
     for (int i = j + 1 + tid; i < rows; i += NT) {
       const double l = d != 0.0 ? P[i + static_cast<size_t>(j) * rows] / d : P[i + static_cast<size_t>(j) * rows];
       P[i + static_cast<size_t>(j) * rows] = l;
-      for (int c = j + 1; c < jb; ++c) P[i + static_cast<size_t>(c) * rows] -= l * P[j + static_cast<size_t>(c) * rows];
-      if (j + 1 < jb) argmax_merge(best, bi, fabs(P[i + static_cast<size_t>(j + 1) * rows]), i);
+      for (int c = j + 1; c < cend; ++c) P[i + static_cast<size_t>(c) * rows] -= l * P[j + static_cast<size_t>(c) * rows];
+      if (j + 1 < cend) argmax_merge(best, bi, fabs(P[i + static_cast<size_t>(j + 1) * rows]), i);
     }
     publish(buf ^ 1, best, bi);
     __syncthreads();
+    if (split && j == kHalf - 1) {
+      // U12: rows 1..kHalf-1 of the second half, forward substitution (one thread per column)
+      if (tid < jb - kHalf) {
+        double* pc = P + static_cast<size_t>(kHalf + tid) * rows;
+        for (int i = 1; i < kHalf; ++i) {
+          double a = pc[i];
+          for (int l2 = 0; l2 < i; ++l2) a -= P[i + static_cast<size_t>(l2) * rows] * pc[l2];
+          pc[i] = a;
+        }
+      }
+      __syncthreads();
+      // rows kHalf.. of the second half: A22 -= L21 U12, l in order; pivot candidates of column kHalf
+      best = -1.0;
+      bi = rows;
+      for (int i = kHalf + tid; i < rows; i += NT) {
+        double lrow[kHalf];
+#pragma unroll
+        for (int l2 = 0; l2 < kHalf; ++l2) lrow[l2] = P[i + static_cast<size_t>(l2) * rows];
+        for (int c = kHalf; c < jb; ++c) {
+          double* pc = P + static_cast<size_t>(c) * rows;
+          double a = pc[i];
+#pragma unroll
+          for (int l2 = 0; l2 < kHalf; ++l2) a -= lrow[l2] * pc[l2];
+          pc[i] = a;
+          if (c == kHalf) argmax_merge(best, bi, fabs(a), i);
+        }
+      }
+      publish(buf ^ 1, best, bi);
+      __syncthreads();
+    }
   }
   for (int e = tid; e < rows * jb; e += NT) {
     const int i = e % rows, c = e / rows;
