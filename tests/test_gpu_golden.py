@@ -21,7 +21,7 @@ def load(tag):
 
 
 @pytest.mark.parametrize("name,method", [("C1", "full"), ("C2", "full"), ("C2", "lowrank"),
-                                         ("C3", "full"), ("C3", "lowrank")])
+                                         ("C3", "full"), ("C3", "lowrank"), ("C4", "full")])
 def test_baseline_config_matches_oracle(name, method):
     g = load(f"{name}_{method}")
     p = P.Problem(name)
@@ -37,3 +37,20 @@ def test_baseline_config_matches_oracle(name, method):
         ranks, ref_ranks = r.history("rank"), g["rank"]
         print(f"  ranks GPU {list(map(int, ranks))} oracle {list(map(int, ref_ranks))}")
         assert abs(int(ranks[-1]) - int(ref_ranks[-1])) <= 2
+
+
+def test_c4_low_rank_against_oracle_full_rank():
+    """C4's low-rank oracle run takes days on one core, so the GPU low-rank
+    solve is held to the oracle's full-rank flux: the low-rank iteration
+    converges to the same SI-DSA fixed point (the reference's LR-vs-FR bar is
+    1e-6 absolute, proj/tests/test_low_rank.cpp:472-498); asserted here at the
+    low-rank parity bar, 1e-8 relative, and iterations +-1."""
+    g = load("C4_full")
+    p = P.Problem("C4")
+    r = p.solve_low_rank(build_factors=0)
+    ref = g["phi"]
+    err = np.linalg.norm(r.phi - ref) / np.linalg.norm(ref)
+    print(f"C4 lowrank vs oracle full: it {r.iterations} vs {int(g['iterations'])}, rel {err:.2e}, "
+          f"abs {np.linalg.norm(r.phi - ref):.2e}, rank {int(r.history('rank')[-1])}")
+    assert r.converged and abs(r.iterations - int(g["iterations"])) <= 1
+    assert np.linalg.norm(r.phi - ref) <= 1e-6 and err <= 1e-8
