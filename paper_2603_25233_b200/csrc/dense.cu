@@ -1902,7 +1902,7 @@ void gemm_nn(long long M, int N, int K, const double* A, long long lda, const do
     return;
   }
   // (a single k-stage, K <= 32 — the QR trailing updates — gains nothing from the pipeline)
-  const bool pipe_ok = aligned16(A) && lda % 2 == 0 && M % 2 == 0 && K > kTnBk;
+  const bool pipe_ok = aligned16(A) && lda % 2 == 0 && M % 2 == 0 && K >= 8;
   static const bool nt_off = [] {  // RTLR_NN_NT=0: the 64 x 64 tile / FFMA skinny kernels (A/B timing)
     const char* e = std::getenv("RTLR_NN_NT");
     return e && e[0] == '0';
