@@ -17,6 +17,7 @@
 #include <cstdlib>
 #include <cstdio>
 #include <string>
+#include <thread>
 
 #include <cooperative_groups.h>
 
@@ -793,13 +794,26 @@ bool LowRankEngine::mgs_ro_update(const double* snaps, const std::vector<int>& a
       for (int i = 0; i < prev_rank_ && i < static_cast<int>(rec_[j].size()); ++i) old[j][i] = rec_[j][i];
     rank_ = r_new;
     for (int j = 0; j < n_snap_; ++j) rec_[j].assign(rank_, 0.0);
-    if (m0 > 0 && prev_rank_ > 0)
-      for (int j = 0; j < m0; ++j)
-        for (int i = 0; i < rank_; ++i) {
-          double acc = 0.0;
-          for (int k = 0; k < prev_rank_; ++k) acc += hR[i + static_cast<size_t>(k) * r_new] * old[j][k];
-          rec_[j][i] = acc;
+    if (m0 > 0 && prev_rank_ > 0) {
+      // rec_j = R[:, :prev] old_j: k outer so R's columns stream contiguously
+      // (every element still sums k = 0, 1, ... in order: bitwise the same),
+      // records split over host threads (m0 x r x prev ~ 3e8 products at C4)
+      auto rows = [&](int j0, int j1) {
+        for (int j = j0; j < j1; ++j) {
+          std::vector<double>& out = rec_[j];
+          for (int k = 0; k < prev_rank_; ++k) {
+            const double o = old[j][k];
+            const double* rk = hR.data() + static_cast<size_t>(k) * r_new;
+            for (int i = 0; i < rank_; ++i) out[i] += rk[i] * o;
+          }
         }
+      };
+      const int nt = std::max(1, std::min<int>(16, static_cast<int>(std::thread::hardware_concurrency())));
+      std::vector<std::thread> pool;
+      const int per = (m0 + nt - 1) / nt;
+      for (int t = 0; t < nt && t * per < m0; ++t) pool.emplace_back(rows, t * per, std::min(m0, (t + 1) * per));
+      for (auto& th : pool) th.join();
+    }
     for (int j = 0; j < p_in; ++j)
       for (int i = 0; i < rank_; ++i) rec_[m0 + j][i] = hB[i + static_cast<size_t>(j) * r_new];
     reorth_seconds_ += std::chrono::duration<double>(std::chrono::steady_clock::now() - tq0).count();
