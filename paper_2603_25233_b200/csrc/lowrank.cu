@@ -498,10 +498,7 @@ class LowRankEngine {
     pt_.on = e && e[0] == '1';
     pt_.s = s_;
   }
-  ~LowRankEngine() {
-    for (void* p : uploads_) cudaFreeAsync(p, s_);
-    cudaFreeHost(hbuf_);
-  }
+  ~LowRankEngine() { cudaFreeHost(hbuf_); }
   PhaseTimer pt_;
   int reorth_count_ = 0;        // Householder rebuilds (all inner loops)
   int svd_sweeps_ = 0, svd_calls_ = 0;
@@ -535,8 +532,6 @@ class LowRankEngine {
   void phi_from_C();
   double host_dot(const double* a, const double* b, long long n);
   int* upload_ints(DBuf<int>& buf, const std::vector<int>& a);
-  void release_uploads();
-  std::vector<void*> uploads_;
   double* work(size_t need) { return work_.ensure(std::max<size_t>(need, 4096)); }
   // C = A^T B (K = N_x) with its split-K workspace
   void tn(int M, int N, const double* A, long long lda, const double* B, long long ldb, double* C, long long ldc) {
@@ -578,22 +573,14 @@ double LowRankEngine::host_dot(const double* a, const double* b, long long n) {
   return hbuf_[0];
 }
 
-// Index lists go to their own stream-ordered allocations (the device's
-// memory pool), released once the inner iteration's kernels are queued, so
-// an upload never waits for the kernels still reading an earlier list (the
-// former reuse of one buffer per call site synchronised the stream first).
-int* LowRankEngine::upload_ints(DBuf<int>& /*call site*/, const std::vector<int>& a) {
-  void* d = nullptr;
-  const size_t bytes = std::max<size_t>(a.size(), 1) * sizeof(int);
-  RTLR_CUDA(cudaMallocAsync(&d, bytes, s_));
+int* LowRankEngine::upload_ints(DBuf<int>& buf, const std::vector<int>& a) {
+  // (synchronous reuse of one buffer per call site: stream-ordered pool
+  // allocations per upload were tried and made the C4 solve 15-30% slower
+  // and erratic)
+  RTLR_CUDA(cudaStreamSynchronize(s_));  // the buffer may still feed a queued kernel
+  int* d = buf.ensure(std::max<size_t>(a.size(), 1));
   if (!a.empty()) RTLR_CUDA(cudaMemcpyAsync(d, a.data(), a.size() * sizeof(int), cudaMemcpyHostToDevice, s_));
-  uploads_.push_back(d);
-  return static_cast<int*>(d);
-}
-
-void LowRankEngine::release_uploads() {
-  for (void* p : uploads_) RTLR_CUDA(cudaFreeAsync(p, s_));
-  uploads_.clear();
+  return d;
 }
 
 void LowRankEngine::reset(const double* d_phi_prev) {
@@ -1040,7 +1027,6 @@ InnerResult LowRankEngine::inner(const double* d_phi_prev, SubsampleRng& rng) {
   std::iota(all.begin(), all.end(), 0);
   std::vector<int> next = rng.sample_without_replacement(all, std::min(prm_.p, nomega_));
   while (true) {
-    release_uploads();  // (the previous iteration's index lists; stream-ordered frees)
     ++out.iterations;
     const int p_now = static_cast<int>(next.size());
     double* S = snaps_.ensure(static_cast<size_t>(n_) * padded(p_now));
@@ -1135,7 +1121,6 @@ InnerResult LowRankEngine::inner(const double* d_phi_prev, SubsampleRng& rng) {
       RTLR_CUDA(cudaMemcpyAsync(phi_old_.get(), phi_.get(), n_ * sizeof(double), cudaMemcpyDeviceToDevice, s_));
     }
   }
-  release_uploads();
   out.rank = rank_;
   out.sampled_count = n_snap_;
   return out;
