@@ -194,7 +194,120 @@ const MgKnobs& knobs() {
 }
 
 // x[l] <- one cycle for A_l x = b[l], from x = 0 (zero) or from the x[l] held.
+// The coarse end of the V-cycle (every 5-point level from l0 down, and the
+// dense coarsest solve) in one CTA: the same smooth / restrict / prolong /
+// dense steps as the per-level launches, in the same order and with the
+// same arithmetic per element, separated by block barriers instead of
+// kernel boundaries.  On the small levels the launches were pure latency.
+constexpr int kMaxLev = 24;
+constexpr int kFuseCells = 64 * 64;  // levels at or below this size run fused
+struct CoarseView {
+  int l0, nlev, nu5, ncoarse;
+  int nx[kMaxLev], ny[kMaxLev];
+  const double* st[kMaxLev];
+  double *x[kMaxLev], *b[kMaxLev], *t[kMaxLev];
+  const double* cinv;
+};
+
+__global__ void __launch_bounds__(1024) coarse_cycle(const int* done, const CoarseView v) {
+  if (*done) return;
+  const int tid = threadIdx.x, nt = blockDim.x;
+  double* cur[kMaxLev];
+  double* oth[kMaxLev];
+  // descent: pre-smoothing from zero, restriction
+  for (int l = v.l0; l < v.nlev - 1; ++l) {
+    const L5 L{v.nx[l], v.ny[l], v.nx[l] * v.ny[l], v.st[l]};
+    double* c = v.x[l];
+    double* o = v.t[l];
+    for (int i = tid; i < L.n; i += nt) c[i] = kOmega5 * v.b[l][i] / L.st[i];
+    __syncthreads();
+    for (int it = 1; it < v.nu5; ++it) {
+      for (int i = tid; i < L.n; i += nt) o[i] = c[i] + kOmega5 * (v.b[l][i] - ax5(L, i, c)) / L.st[i];
+      __syncthreads();
+      double* tt = c;
+      c = o;
+      o = tt;
+    }
+    const int cnx = v.nx[l + 1], cny = v.ny[l + 1];
+    for (int C = tid; C < cnx * cny; C += nt) {
+      const int A = C % cnx, B = C / cnx;
+      double sum = 0.0;
+      for (int db = 0; db < 2; ++db)
+        for (int da = 0; da < 2; ++da) {
+          const int a = 2 * A + da, bb = 2 * B + db;
+          if (a < L.nx && bb < L.ny) {
+            const int f = bb * L.nx + a;
+            sum += v.b[l][f] - ax5(L, f, c);
+          }
+        }
+      v.b[l + 1][C] = sum;
+    }
+    __syncthreads();
+    cur[l] = c;
+    oth[l] = o;
+  }
+  // coarsest: x = inv b
+  {
+    const int l = v.nlev - 1, n = v.ncoarse;
+    for (int i = tid; i < n; i += nt) {
+      double sum = 0.0;
+      for (int j = 0; j < n; ++j) sum += v.cinv[i + j * n] * v.b[l][j];
+      v.x[l][i] = sum;
+    }
+    __syncthreads();
+  }
+  // ascent: prolongation, post-smoothing, result into x[l]
+  for (int l = v.nlev - 2; l >= v.l0; --l) {
+    const L5 L{v.nx[l], v.ny[l], v.nx[l] * v.ny[l], v.st[l]};
+    double* c = cur[l];
+    double* o = oth[l];
+    const int cnx = v.nx[l + 1];
+    for (int f = tid; f < L.n; f += nt) {
+      const int a = f % L.nx, bb = f / L.nx;
+      c[f] += v.x[l + 1][(bb / 2) * cnx + a / 2];
+    }
+    __syncthreads();
+    for (int it = 0; it < v.nu5; ++it) {
+      for (int i = tid; i < L.n; i += nt) o[i] = c[i] + kOmega5 * (v.b[l][i] - ax5(L, i, c)) / L.st[i];
+      __syncthreads();
+      double* tt = c;
+      c = o;
+      o = tt;
+    }
+    if (c != v.x[l]) {
+      for (int i = tid; i < L.n; i += nt) v.x[l][i] = c[i];
+      __syncthreads();
+    }
+  }
+}
+
 void cycle5(const int* done, const MgDevice& mg, int l, bool zero, cudaStream_t s) {
+  {
+    const MgKnobs& kk = knobs();
+    static const bool fuse_off = [] {  // RTLR_MG_FUSE=0: one launch per step on every level
+      const char* e = std::getenv("RTLR_MG_FUSE");
+      return e && e[0] == '0';
+    }();
+    if (!fuse_off && zero && l < mg.nlev - 1 && static_cast<long long>(mg.nx[l]) * mg.ny[l] <= kFuseCells &&
+        l >= kk.w_levels && mg.nlev <= kMaxLev) {
+      CoarseView v{};
+      v.l0 = l;
+      v.nlev = mg.nlev;
+      v.nu5 = kk.nu5;
+      v.ncoarse = mg.ncoarse;
+      v.cinv = mg.cinv;
+      for (int q = 0; q < mg.nlev; ++q) {
+        v.nx[q] = mg.nx[q];
+        v.ny[q] = mg.ny[q];
+        v.st[q] = mg.st[q];
+        v.x[q] = mg.x[q];
+        v.b[q] = mg.b[q];
+        v.t[q] = mg.t[q];
+      }
+      coarse_cycle<<<1, 1024, 0, s>>>(done, v);
+      return;
+    }
+  }
   if (l == mg.nlev - 1) {
     if (!zero) throw std::logic_error("multigrid: second visit of the coarsest level");
     dense_apply<<<1, 256, 0, s>>>(done, mg.ncoarse, mg.cinv, mg.b[l], mg.x[l]);

@@ -172,8 +172,8 @@ np.save(sys.argv[2], np.asarray(r.phi))
 '''
 
 
-@pytest.mark.parametrize("switch", ["RTLR_CGS_COOP", "RTLR_JACOBI_COOP", "RTLR_QR_COOP", "RTLR_NN_NT", "RTLR_TN_NT",
-                                    "RTLR_SWEEP_TMA"])
+@pytest.mark.parametrize("switch", ["RTLR_CGS_COOP", "RTLR_JACOBI_COOP", "RTLR_QR_COOP", "RTLR_MG_FUSE", "RTLR_NN_NT",
+                                    "RTLR_TN_NT", "RTLR_SWEEP_TMA"])
 def test_device_path_switches_keep_the_solve(switch, tmp_path):
     """The fused / cooperative device paths against the launch-per-step and
     64 x 64-tile paths they replaced (each switch is read once per process,
@@ -191,7 +191,7 @@ def test_device_path_switches_keep_the_solve(switch, tmp_path):
         env = dict(os.environ, **{switch: v})
         subprocess.run([sys.executable, "-c", _SWITCH_RUN, root, f], env=env, check=True, timeout=600)
         out[v] = np.load(f)
-    if switch in ("RTLR_CGS_COOP", "RTLR_JACOBI_COOP"):
+    if switch in ("RTLR_CGS_COOP", "RTLR_JACOBI_COOP", "RTLR_MG_FUSE"):
         assert np.array_equal(out["1"], out["0"])
     else:
         assert rel(out["1"], out["0"]) <= 1e-8
