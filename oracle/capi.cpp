@@ -156,6 +156,26 @@ int oracle_problem_set(void* h, const char* key, double v) {
   });
 }
 
+// A ScalarField (dg_space.hpp:10) as a C callback, for "sigma_s" | "sigma_a"
+// | "source" | "boundary" (the same callable the product's
+// rtlr_cu_config_set_field takes).
+int oracle_problem_set_field(void* h, const char* which, double (*fn)(void*, double, double), void* user) {
+  return guard([&] {
+    ProblemSpec& s = static_cast<Problem*>(h)->spec;
+    if (!fn) throw std::invalid_argument("null field");
+    Field f = [fn, user](double x, double y) { return fn(user, x, y); };
+    std::string w = which;
+    if (w == "sigma_s") s.sigma_s = f;
+    else if (w == "sigma_a") s.sigma_a = f;
+    else if (w == "source") s.source = f;
+    else if (w == "boundary") {
+      s.boundary = f;
+      s.boundary_zero = false;
+    } else
+      throw std::invalid_argument("unknown field " + w);
+  });
+}
+
 int oracle_problem_assemble(void* h) {
   return guard([&] {
     Problem* p = static_cast<Problem*>(h);

@@ -23,6 +23,8 @@ HOST, DEVICE = 0, 1
 _D = ctypes.POINTER(ctypes.c_double)
 _I = ctypes.POINTER(ctypes.c_int)
 _I64 = ctypes.POINTER(ctypes.c_int64)
+# rtlr_cu_field_fn: double f(void* user, double x, double y) (ScalarField, dg_space.hpp:10)
+FIELD_FN = ctypes.CFUNCTYPE(ctypes.c_double, ctypes.c_void_p, ctypes.c_double, ctypes.c_double)
 _lib = None
 
 # Every symbol include/rtlr_cu.h declares.
@@ -87,6 +89,7 @@ def load_library(path: str = LIB_PATH):
     L.rtlr_cu_config_create.argtypes = [ctypes.c_char_p, ctypes.POINTER(ctypes.c_void_p)]
     L.rtlr_cu_config_set.argtypes = [ctypes.c_void_p, ctypes.c_char_p, ctypes.c_double]
     L.rtlr_cu_config_destroy.argtypes = [ctypes.c_void_p]
+    L.rtlr_cu_config_set_field.argtypes = [ctypes.c_void_p, ctypes.c_char_p, FIELD_FN, ctypes.c_void_p]
     L.rtlr_cu_config_parse.argtypes = [ctypes.c_char_p, ctypes.POINTER(ctypes.c_void_p)]
     L.rtlr_cu_config_load.argtypes = [ctypes.c_char_p, ctypes.POINTER(ctypes.c_void_p)]
     L.rtlr_cu_config_set_mode.argtypes = [ctypes.c_void_p, ctypes.c_char_p]
@@ -301,14 +304,21 @@ class Problem:
     keyword overrides use the reference's config keys.  device < 0 assembles
     on the host only (inputs inspectable, no GPU calls)."""
 
-    def __init__(self, name: str = None, device: int = 0, config_text: str = None, **overrides):
+    def __init__(self, name: str = None, device: int = 0, config_text: str = None, fields=None, **overrides):
         """config_text: a reference config file's contents (key = value lines,
-        parse_config_text) instead of a preset name."""
+        parse_config_text) instead of a preset name.  fields: {"sigma_s" |
+        "sigma_a" | "source" | "boundary": f(x, y)} — arbitrary ScalarField
+        callables (rtlr_cu_config_set_field), evaluated during assembly."""
         L = load_library()
         cfg = _make_config(L, name, config_text)
+        self._fields = []
         try:
             for k, v in overrides.items():
                 _check(L.rtlr_cu_config_set(cfg, k.encode(), float(v)))
+            for which, f in (fields or {}).items():
+                cb = FIELD_FN(lambda _u, x, y, f=f: float(f(x, y)))
+                self._fields.append(cb)
+                _check(L.rtlr_cu_config_set_field(cfg, which.encode(), cb, None))
             h = ctypes.c_void_p()
             _check(L.rtlr_cu_problem_create(cfg, device, ctypes.byref(h)))
             self.h = h

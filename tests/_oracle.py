@@ -20,6 +20,8 @@ _lib = None
 _D = ctypes.POINTER(ctypes.c_double)
 _I = ctypes.POINTER(ctypes.c_int)
 _LL = ctypes.POINTER(ctypes.c_longlong)
+# ScalarField callback: double f(void* user, double x, double y)
+FIELD_FN = ctypes.CFUNCTYPE(ctypes.c_double, ctypes.c_void_p, ctypes.c_double, ctypes.c_double)
 
 
 def build() -> None:
@@ -38,6 +40,7 @@ def lib():
         L.oracle_problem_free.argtypes = [ctypes.c_void_p]
         L.oracle_problem_set.argtypes = [ctypes.c_void_p, ctypes.c_char_p, ctypes.c_double]
         L.oracle_problem_assemble.argtypes = [ctypes.c_void_p]
+        L.oracle_problem_set_field.argtypes = [ctypes.c_void_p, ctypes.c_char_p, FIELD_FN, ctypes.c_void_p]
         L.oracle_problem_info.argtypes = [ctypes.c_void_p, _LL]
         L.oracle_problem_get.argtypes = [ctypes.c_void_p, ctypes.c_char_p, _D]
         L.oracle_problem_nnz.restype = ctypes.c_longlong
@@ -162,12 +165,19 @@ class Result:
 class Problem:
     """An assembled oracle problem (preset name or C1..C5 plus overrides)."""
 
-    def __init__(self, name: str, assemble: bool = True, **overrides):
+    def __init__(self, name: str, assemble: bool = True, fields=None, **overrides):
+        """fields: {"sigma_s" | "sigma_a" | "source" | "boundary": f(x, y)}
+        (arbitrary ScalarField callables, as the reference's assembly takes)."""
         self.h = lib().oracle_problem_new(name.encode())
         if not self.h:
             raise OracleError(lib().oracle_last_error().decode())
         for k, v in overrides.items():
             _check(lib().oracle_problem_set(self.h, k.encode(), float(v)))
+        self._fields = []
+        for which, f in (fields or {}).items():
+            cb = FIELD_FN(lambda _u, x, y, f=f: float(f(x, y)))
+            self._fields.append(cb)
+            _check(lib().oracle_problem_set_field(self.h, which.encode(), cb, None))
         if assemble:
             self.assemble()
 
