@@ -14,15 +14,19 @@ the reference's sweep, proj/src/sweep.cpp:9-57) timed on a bounded sample.
 --impl reference times that CPU implementation on all host threads instead
 (the reference itself cannot be built: Eigen is absent).
 
-Multi-GPU: one process per GPU (torchrun); every rank sweeps its own copy of
-the direction set with rank-specific sources (weak scaling, no collective on
-the data path); the step time is the max over ranks.
+Multi-GPU: one process per GPU (torchrun; `--gpus N` without a torchrun
+environment re-launches itself under torch.distributed.run).  The workload's
+direction set is partitioned over the ranks (rtlr_cu_partition_angles:
+mirror-pair units dealt round-robin, every rank spans all quadrants) — strong
+scaling of one fixed job, no collective on the data path (the sweeps are
+independent per direction); the step time is the max over ranks.
 """
 from __future__ import annotations
 
 import argparse
 import json
 import os
+import socket
 import statistics
 import subprocess
 import sys
@@ -53,6 +57,49 @@ def parse():
     ap.add_argument("--cpu-sample-updates", type=float, default=8e7,
                     help="CPU baseline sample size in cell-angle updates (~10 s of one core)")
     return ap.parse_args()
+
+
+def cpu_model():
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+def host_mem_available():
+    try:
+        with open("/proc/meminfo") as f:
+            for line in f:
+                if line.startswith("MemAvailable:"):
+                    return int(line.split()[1]) * 1024
+    except OSError:
+        pass
+    return 0
+
+
+def free_port():
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def maybe_spawn(args):
+    """`--gpus N` outside torchrun: re-launch under torch.distributed.run
+    (one process per GPU, 127.0.0.1 rendezvous).  Inside torchrun the world
+    size must equal --gpus."""
+    world = os.environ.get("WORLD_SIZE")
+    if world is None:
+        if args.gpus > 1 and args.impl == "ours":
+            cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+                   "--master-addr=127.0.0.1", f"--master-port={free_port()}", os.path.abspath(__file__)] + sys.argv[1:]
+            sys.exit(subprocess.call(cmd))
+        return
+    if int(world) != args.gpus:
+        raise SystemExit(f"bench.py: --gpus {args.gpus} but the launcher started WORLD_SIZE={world} ranks")
 
 
 def load_peaks():
@@ -173,18 +220,19 @@ def run_reference(args, rank, world):
     line = {
         "impl": "reference", "metric": "sweep cell-angle updates/s", "value": value,
         "unit": "cell-angle updates/s", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": 1e3 * statistics.mean(times), "higher_is_better": True, "scaling": "weak",
+        "ms_per_step": 1e3 * statistics.mean(times), "higher_is_better": True, "scaling": "strong",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": workload_config(args),
         "cpu_baseline": {"value": value, "unit": "cell-angle updates/s", "cores": threads, "kind": "port",
-                         "sample": sample},
+                         "sample": sample, "cpu_model": cpu_model()},
         "e2e": {"value": value, "unit": "cell-angle updates/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
 
 
-SOLVER_JOBS = (("C1", "full"), ("C1", "lowrank"), ("C2", "lowrank"), ("C4", "full"), ("C4", "lowrank"))
+SOLVER_JOBS = (("C1", "full"), ("C1", "lowrank"), ("C2", "full"), ("C2", "lowrank"), ("C3", "full"),
+               ("C3", "lowrank"), ("C4", "full"), ("C4", "lowrank"))
 CPU_REFERENCE_JOBS = (("C1", "full"), ("C1", "lowrank"))  # the oracle finishes these in seconds
 SOLVER_REPEATS = 2
 
@@ -263,11 +311,13 @@ def workload_config(args):
     return {"workload": f"C5 sweep {args.grid}^2 cells x CL({args.n_theta},{args.n_omega_z}) = {nd} directions",
             "grid": args.grid, "directions": nd, "quadrature": f"CL({args.n_theta},{args.n_omega_z})",
             "sigma_t": 1.0, "source": "U[0,1) per (cell, direction), counter-based, seed 12345",
-            "l2": "inputs larger than L2 (no flush needed)", "parallelism": f"direction sets x{args.gpus}"}
+            "l2": "inputs larger than L2 (no flush needed)",
+            "parallelism": f"direction partition x{args.gpus}"}
 
 
 def main():
     args = parse()
+    maybe_spawn(args)
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
@@ -292,12 +342,23 @@ def main():
     stream = torch.cuda.Stream()
     torch.cuda.set_stream(stream)
     prob.set_stream(stream.cuda_stream)
-    D, n = prob.n_omega, prob.n
+    D_all, n = prob.n_omega, prob.n
     cells = n // 4
+    # This rank's share of the directions (all of them at N = 1); the source
+    # of direction j is c5_fill's stream for j whatever rank sweeps it.
+    mine = np.arange(D_all, dtype=np.int32) if world == 1 else \
+        P.partition_angles(args.n_theta, args.n_omega_z, world, rank).astype(np.int32)
+    D = len(mine)
     rhs = torch.empty(D * n, dtype=torch.float64, device="cuda")
     psi = torch.empty(D * n, dtype=torch.float64, device="cuda")
-    angles = torch.arange(D, dtype=torch.int32, device="cuda")
-    prob.c5_fill(rhs.data_ptr(), D, rank * D, SEED)
+    angles = torch.from_numpy(mine).to("cuda")
+    torch.cuda.synchronize()
+    if world == 1:
+        prob.c5_fill(rhs.data_ptr(), D, 0, SEED)
+    else:
+        for k, j in enumerate(mine.tolist()):
+            prob.c5_fill(rhs.data_ptr() + 8 * k * n, 1, j, SEED)
+    prob.synchronize()
 
     def step():
         prob.sweep_async(angles.data_ptr(), D, rhs.data_ptr(), n, psi.data_ptr(), n)
@@ -331,7 +392,7 @@ def main():
     if dist:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     ms_max = float(t.item())
-    value = world * D * cells / (ms_max * 1e-3)
+    value = D_all * cells / (ms_max * 1e-3)  # the whole job's updates over the slowest rank's time
 
     # A single launch after an idle gap: the board's power cap lowers the SM
     # clock under sustained load, so this is the kernel's unthrottled speed.
@@ -354,14 +415,22 @@ def main():
                 "kernel_ms_min": min(launch_ms), "kernel_ms_isolated": isolated_ms,
                 "frac_isolated": BYTES_PER_UPDATE * D * cells / (isolated_ms * 1e-3) / 1e9 / peak}
 
-    # End to end through the C ABI with pinned host buffers.
+    # End to end through the C ABI with pinned host buffers: this rank's
+    # sources start in host memory and its angular fluxes end there, every
+    # byte crossing PCIe inside the timed region.  When the host has the RAM,
+    # the buffers hold the whole workload (the real c5 sources of every
+    # direction, one rtlr_cu_sweep call per step that pipelines H2D / sweep /
+    # D2H internally); otherwise `e2e_chunk` directions at a time through one
+    # pinned buffer pair (same copy volume, the first chunk's sources re-sent).
     e2e = None
     if not args.no_e2e:
-        C = min(args.e2e_chunk, D)
+        full_bytes = 2 * D * n * 8
+        whole = host_mem_available() > 1.5 * full_bytes + (16 << 30)
+        C = D if whole else min(args.e2e_chunk, D)
         h_rhs = torch.empty(C * n, dtype=torch.float64, pin_memory=True)
         h_psi = torch.empty(C * n, dtype=torch.float64, pin_memory=True)
         h_rhs.copy_(rhs[:C * n])
-        chunks = [np.arange(c0, min(D, c0 + C), dtype=np.int32) for c0 in range(0, D, C)]
+        chunks = [mine[c0:c0 + C] for c0 in range(0, D, C)]
 
         def e2e_step():
             for ang in chunks:
@@ -381,11 +450,18 @@ def main():
         et = torch.tensor([wall], dtype=torch.float64, device="cuda")
         if dist:
             dist.all_reduce(et, op=dist.ReduceOp.MAX)
-        e2e = {"value": world * D * cells / float(et.item()), "unit": "cell-angle updates/s",
+        e2e = {"value": D_all * cells / float(et.item()), "unit": "cell-angle updates/s",
                "h2d_bytes_per_step": D * n * 8, "d2h_bytes_per_step": D * n * 8,
-               "steps": e2e_steps, "chunk_directions": C, "api": "rtlr_cu_sweep(where=RTLR_CU_HOST)"}
+               "steps": e2e_steps, "chunk_directions": C, "api": "rtlr_cu_sweep(where=RTLR_CU_HOST)",
+               "inputs": ("every direction's own c5 sources in pinned host memory" if whole else
+                          f"{C}-direction pinned buffers, the first chunk's sources re-sent for every chunk")}
+        if whole:  # parity of the e2e output on a few directions against the device run
+            for k in (0, D // 2, D - 1):
+                assert torch.equal(h_psi[k * n:(k + 1) * n], psi[k * n:(k + 1) * n].cpu()), "e2e psi differs"
+        C = min(args.e2e_chunk, D)
         # The e2e bound: 64 B of PCIe traffic per update, H2D and D2H at once.
         # Measured here with the same pinned buffers (torch copies on two streams).
+        h_rhs, h_psi = h_rhs[:C * n], h_psi[:C * n]
         d_a = torch.empty(C * n, dtype=torch.float64, device="cuda")
         d_b = torch.empty(C * n, dtype=torch.float64, device="cuda")
         s_in, s_out = torch.cuda.Stream(), torch.cuda.Stream()
@@ -404,20 +480,21 @@ def main():
         pcie = 2 * C * n * 8 / (time.perf_counter() - t0) / 1e9
         e2e["pcie_gbs_h2d_plus_d2h"] = pcie
         e2e["frac_of_pcie"] = e2e["value"] / world * BYTES_PER_UPDATE / 1e9 / pcie
-        del d_a, d_b
+        del d_a, d_b, h_rhs, h_psi
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
         ndirs = max(1, min(D, int(args.cpu_sample_updates // cells)))
         r, upd, dt = cpu_sweep_rate(args.grid, args.n_theta, args.n_omega_z, ndirs, 1)
         cpu = {"value": r, "unit": "cell-angle updates/s", "cores": 1, "kind": "port",
-               "sample": f"{ndirs} directions x {args.grid}^2 cells ({upd} updates, {dt:.1f} s)"}
+               "sample": f"{ndirs} directions x {args.grid}^2 cells ({upd} updates, {dt:.1f} s)",
+               "cpu_model": cpu_model(), "host_threads": os.cpu_count()}
 
     line = {
         "metric": "sweep cell-angle updates/s", "value": value, "unit": "cell-angle updates/s",
         "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_max,
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-        "data": "synthetic", "config": workload_config(args) | {"parallelism": f"direction-sets x{world}"},
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic", "config": workload_config(args),
         "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": args.steps,
         "clocks": clk.summary(), "solvers": None,
     }

@@ -866,14 +866,21 @@ void LowRankEngine::galerkin_solve(const std::vector<int>& angles, double* d_sol
   gal_systems_ += m;
   const ShardBlock sb = blk(m);
   const long long rr = static_cast<long long>(rank_) * rank_;
-  // Systems per LU batch for r > kSmemLuMax: a 1 GB workspace (372 systems at
-  // r = 600; the all-angle solves of C4 are ~1000 systems, their batches run
-  // 13% faster than at 128 MB).  Results do not depend on the batching.
-  static const long long chunk_bytes = [] {
+  // Systems per LU batch for r > kSmemLuMax: up to a 4 GiB LU workspace
+  // (galerkin_work_doubles per system: the r x (r+1) augmented matrix, the
+  // pivots and the permutation; 2.9 MB at r = 600, so 1,480 systems — C4's
+  // all-angle solves, ~1,000 distinct systems per call, run as one batch:
+  // 33.8 -> 29.4 ms per call against 372-system batches).  The grid's y
+  // dimension carries the systems, so a batch is capped at 65,535.  Results
+  // do not depend on the batching.
+  static const long long budget_bytes = [] {
     const char* e = std::getenv("RTLR_GAL_CHUNK_MB");
-    return (e && std::atoll(e) > 0 ? std::atoll(e) : 1024LL) << 20;
+    return (e && std::atoll(e) > 0 ? std::atoll(e) : 4096LL) << 20;
   }();
-  const int chunk = rank_ > kSmemLuMax ? static_cast<int>(std::max<long long>(1, chunk_bytes / rr)) : 4096;
+  const long long per_system = static_cast<long long>(galerkin_work_doubles(rank_, 1)) * sizeof(double);
+  const int chunk = rank_ > kSmemLuMax
+                        ? static_cast<int>(std::min<long long>(65535, std::max<long long>(1, budget_bytes / per_system)))
+                        : 4096;
   int bad = 0;
   for (int j0 = sb.begin; j0 < sb.end; j0 += chunk) {
     const int mc = std::min(chunk, sb.end - j0);
@@ -881,12 +888,20 @@ void LowRankEngine::galerkin_solve(const std::vector<int>& angles, double* d_sol
     int* d_ang = upload_ints(ang_, sub);
     double* out = d_sol + static_cast<long long>(j0) * ldsol;
     const double* extra = nullptr;
-    if (hp_.bc_any) {  // reduced_rhs: + X^T g_j (low_rank.cpp:185-190)
-      double* Gb = ybuf_.ensure(static_cast<size_t>(n_) * mc);
-      for (int j = 0; j < mc; ++j)
-        RTLR_CUDA(cudaMemcpyAsync(Gb + static_cast<size_t>(j) * n_, P_.bc_.get() + static_cast<size_t>(sub[j]) * n_,
-                                  n_ * sizeof(double), cudaMemcpyDeviceToDevice, s_));
-      tn(rank_, mc, X_.col(0), X_.ld, Gb, n_, out, ldsol);
+    if (hp_.bc_any) {
+      // reduced_rhs: + X^T g_j (low_rank.cpp:185-190), formed in sub-blocks
+      // of kBcCols boundary vectors so the staging buffer stays n x kBcCols
+      // whatever the batch size
+      constexpr int kBcCols = 64;
+      double* Gb = ybuf_.ensure(static_cast<size_t>(n_) * std::min(mc, kBcCols));
+      for (int b0 = 0; b0 < mc; b0 += kBcCols) {
+        const int nb = std::min(kBcCols, mc - b0);
+        for (int j = 0; j < nb; ++j)
+          RTLR_CUDA(cudaMemcpyAsync(Gb + static_cast<size_t>(j) * n_,
+                                    P_.bc_.get() + static_cast<size_t>(sub[b0 + j]) * n_, n_ * sizeof(double),
+                                    cudaMemcpyDeviceToDevice, s_));
+        tn(rank_, nb, X_.col(0), X_.ld, Gb, n_, out + static_cast<long long>(b0) * ldsol, ldsol);
+      }
       extra = out;
     }
     int* flags = flags_.ensure(mc);
