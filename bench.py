@@ -455,9 +455,14 @@ def main():
                "steps": e2e_steps, "chunk_directions": C, "api": "rtlr_cu_sweep(where=RTLR_CU_HOST)",
                "inputs": ("every direction's own c5 sources in pinned host memory" if whole else
                           f"{C}-direction pinned buffers, the first chunk's sources re-sent for every chunk")}
-        if whole:  # parity of the e2e output on a few directions against the device run
+        if whole:  # the e2e output against the device run on a few directions (the host path's
+            # ~64 MB chunks take the few-direction kernels: same sweep, other rounding)
+            worst = 0.0
             for k in (0, D // 2, D - 1):
-                assert torch.equal(h_psi[k * n:(k + 1) * n], psi[k * n:(k + 1) * n].cpu()), "e2e psi differs"
+                a, b = h_psi[k * n:(k + 1) * n], psi[k * n:(k + 1) * n].cpu()
+                worst = max(worst, float((a - b).norm() / b.norm()))
+            assert worst <= 1e-12, f"e2e psi differs from the device run: rel {worst:.2e}"
+            e2e["psi_rel_vs_device"] = worst
         C = min(args.e2e_chunk, D)
         # The e2e bound: 64 B of PCIe traffic per update, H2D and D2H at once.
         # Measured here with the same pinned buffers (torch copies on two streams).

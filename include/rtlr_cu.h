@@ -194,6 +194,108 @@ int rtlr_cu_psi_difference(rtlr_cu_problem* p, const double* psi_full, const dou
  * orthonormal columns, r n x n upper triangular (Eigen sign conventions). */
 int rtlr_cu_dense_qr(int device, int64_t m, int n, const double* a, double* q, double* r);
 
+/* ---- caller-assembled problems.  The reference's solvers take assembled
+ * objects, not a config: solve_full_rank(ops, quad, bc, source, dsa, opts)
+ * (full_rank.hpp:41-43), solve_low_rank(...) (low_rank.hpp:156-158),
+ * si_step (full_rank.hpp:28-30), sweep (sweep.hpp:14-15), with ops a
+ * DiscreteOperators (operators.hpp:17-32), quad an AngularQuadrature
+ * (quadrature.hpp:12-20), bc a BoundaryData (full_rank.hpp:11-20) and dsa a
+ * DiffusionSystem (diffusion.hpp:16-39).  rtlr_cu_problem_upload takes the
+ * same data as plain arrays; every rtlr_cu_problem entry point above then
+ * works on it.  K = 1 (4 DOFs per cell, DOF = (b*nx + a)*4 + my*2 + mx); the
+ * streaming blocks are those of the mesh (operators.cpp:47-112). */
+typedef struct {
+  int nx, ny;                      /* SpatialMesh (dg_space.hpp:15-30) */
+  double x_min, x_max, y_min, y_max;
+  int n_theta, n_omega_z;          /* CL shape of dirs (sharding keeps mirror pairs together); 0, 0: any set */
+  int n_omega;
+  const double* dirs;              /* n_omega x 3 row-major (Omega_x, Omega_y, Omega_z), quad.dirs */
+  const double* weights;           /* n_omega, quad.weights */
+  const double* sigma_t_blocks;    /* ncell x 16 (4x4 column-major per cell), ops.sigma_t_blocks */
+  const double* sigma_s_blocks;    /* ncell x 16, the blocks of ops.sigma_s */
+  const double* sigma_a_blocks;    /* ncell x 16 or NULL (= sigma_t - sigma_s), the blocks of ops.sigma_a */
+  const double* source;            /* N_x, the projected source G */
+  const double* boundary;          /* n_omega x N_x (bc.per_angle) or NULL: vacuum */
+  const double* sip_bsr;           /* ncell x 5 x 16 (self, west, east, south, north) or NULL: built from the blocks */
+  int use_dsa;                     /* 0: no diffusion system (dsa == nullptr) */
+} rtlr_cu_problem_desc;
+int rtlr_cu_problem_upload(const rtlr_cu_problem_desc* desc, int device, rtlr_cu_problem** out);
+
+/* ---- low-rank primitives (low_rank.hpp:18-144), device-resident. */
+typedef struct rtlr_cu_rng rtlr_cu_rng;           /* SubsampleRng (low_rank.hpp:18-27) */
+typedef struct rtlr_cu_lr_basis rtlr_cu_lr_basis; /* LowRankBasis (low_rank.hpp:42-102) */
+typedef struct rtlr_cu_inner rtlr_cu_inner;       /* InnerLoopResult (low_rank.hpp:125-136) */
+typedef struct { /* LowRankParams (low_rank.hpp:29-36) */
+  int p, q;
+  double eps_res, eps_diff, eps_svd, eps_mgs;
+} rtlr_cu_lr_params;
+void rtlr_cu_lr_params_default(rtlr_cu_lr_params* o);
+
+/* SubsampleRng: mt19937_64(seed), masked-rejection draw_below (low_rank.cpp:15-27)
+ * and the partial Fisher-Yates sample_without_replacement (:29-37);
+ * *n_out = min(count, n). */
+int rtlr_cu_rng_create(uint64_t seed, rtlr_cu_rng** out);
+void rtlr_cu_rng_destroy(rtlr_cu_rng* r);
+int rtlr_cu_rng_draw_below(rtlr_cu_rng* r, uint64_t n, uint64_t* out);
+int rtlr_cu_rng_sample(rtlr_cu_rng* r, const int* pool, int n, int count, int* out, int* n_out);
+
+/* LowRankBasis(ops, quad, bc, rhs_core) (low_rank.cpp:39-44): an empty
+ * basis for this rhs_core (N_x); params carries eps_mgs for
+ * mgs_ro_update's overlap trigger and p, q for greedy_subsample. */
+int rtlr_cu_lr_basis_create(rtlr_cu_problem* p, const rtlr_cu_lr_params* params, const double* rhs_core, int where,
+                            rtlr_cu_lr_basis** out);
+void rtlr_cu_lr_basis_destroy(rtlr_cu_lr_basis* b);
+/* info: rank, snapshot_count, n_dofs, n_omega */
+int rtlr_cu_lr_basis_info(const rtlr_cu_lr_basis* b, int64_t info[4]);
+/* "basis" (N_x x rank), "record" (coefficient_record, rank x snapshot_count),
+ * "dx_minus" | "dx_plus" | "dy_minus" | "dy_plus" | "sigma_t" (projected_*,
+ * rank x rank), "prhs" (X^T rhs_core, rank), "rhs_core" (N_x), all
+ * column-major. */
+int rtlr_cu_lr_basis_get(const rtlr_cu_lr_basis* b, const char* what, double* out, int where);
+int rtlr_cu_lr_basis_sampled(const rtlr_cu_lr_basis* b, int* out); /* sampled_angles(), snapshot_count entries */
+/* mgs_ro_update(snapshots, angles, eps_mgs, drop_tol) (low_rank.cpp:66-132);
+ * snapshots N_x x n column-major; *reorthogonalized = 1 when the overlap
+ * test forced the rebuild. */
+int rtlr_cu_lr_mgs_ro_update(rtlr_cu_lr_basis* b, const double* snapshots, const int* angles, int n, double eps_mgs,
+                             double drop_tol, int where, int* reorthogonalized);
+int rtlr_cu_lr_update_projections(rtlr_cu_lr_basis* b, int reorthogonalized); /* low_rank.cpp:136-174 */
+/* galerkin_solve(angle) for m angles (low_rank.cpp:176-200): sol rank x m */
+int rtlr_cu_lr_galerkin_solve(rtlr_cu_lr_basis* b, const int* angles, int m, double* sol, int where);
+/* residual_norm(angle, c) for m angles (low_rank.cpp:202-215): coeffs rank x m */
+int rtlr_cu_lr_residual_norms(rtlr_cu_lr_basis* b, const int* angles, int m, const double* coeffs, double* norms,
+                              int where);
+/* greedy_subsample(basis, sampled_mask, p, q, rng) (low_rank.cpp:217-252):
+ * sampled_mask N_Omega bytes; selected (>= p entries), candidates (>= q),
+ * candidate_solutions (rank x q, may be NULL), residual_norms (q, may be
+ * NULL); counts in *n_selected, *n_candidates. */
+int rtlr_cu_lr_greedy_subsample(rtlr_cu_lr_basis* b, const unsigned char* sampled_mask, int p, int q, rtlr_cu_rng* rng,
+                                int* selected, int* n_selected, double* max_residual, int* candidates,
+                                int* n_candidates, double* candidate_solutions, double* residual_norms, int where);
+/* build_full_coefficients (low_rank.cpp:311-336): C (rank x N_Omega) from the
+ * record (sampled angles), m candidate solutions (rank x m, may be m = 0),
+ * Galerkin solves for the rest; phi = X (C w) (low_rank.cpp:385). */
+int rtlr_cu_lr_build_coefficients(rtlr_cu_lr_basis* b, const int* candidates, int m, const double* candidate_solutions,
+                                  double* C, double* phi, int where);
+/* truncation_rank (low_rank.cpp:254-266), host arrays */
+int rtlr_cu_truncation_rank(const double* s, int n, double eps_svd, int* out);
+/* truncate_factors(C, X, eps_svd) (low_rank.cpp:268-277): C rank x N_Omega,
+ * X N_x x rank; out X_out (N_x x r'), S_out (r'), V_out (N_Omega x r') with
+ * room for r' <= rank; *rank_out = r'.  S_out alone (X_out = V_out = NULL)
+ * gives all rank singular values of C (the per-outer-iteration SVD,
+ * low_rank.cpp:457). */
+int rtlr_cu_truncate_factors(rtlr_cu_problem* p, const double* C, const double* X, int rank, double eps_svd, int where,
+                             int* rank_out, double* X_out, double* S_out, double* V_out);
+/* low_rank_si(ops, quad, bc, source, phi_prev, params, rng) (low_rank.cpp:340-434) */
+int rtlr_cu_low_rank_si(rtlr_cu_problem* p, const double* phi_prev, const rtlr_cu_lr_params* params, rtlr_cu_rng* rng,
+                        int where, rtlr_cu_inner** out);
+/* info: iterations, rank, sampled_count, reorthogonalizations,
+ * verification_rejections, exhausted_all_angles, n_dofs, n_omega */
+int rtlr_cu_inner_info(const rtlr_cu_inner* r, int64_t info[8]);
+/* "phi_star" (N_x), "coefficients" (rank x N_Omega), "basis" (N_x x rank) */
+int rtlr_cu_inner_get(const rtlr_cu_inner* r, const char* what, double* out, int where);
+int rtlr_cu_inner_sampled(const rtlr_cu_inner* r, int* out); /* sampled_order, sampled_count entries */
+void rtlr_cu_inner_destroy(rtlr_cu_inner* r);
+
 /* NCCL (over NVLink / NVSwitch) for the sharded drivers: rank 0 creates the
  * 128-byte id, the launcher broadcasts it, every rank attaches its problem.
  * solve_full_rank then sweeps this rank's directions and sums the scalar-

@@ -42,6 +42,13 @@ EXPORTS = [
     "rtlr_cu_sweep_async", "rtlr_cu_check", "rtlr_cu_nccl_unique_id", "rtlr_cu_problem_set_comm",
     "rtlr_cu_shard_block", "rtlr_cu_dense_qr", "rtlr_cu_psi_difference",
     "rtlr_cu_config_parse", "rtlr_cu_config_load", "rtlr_cu_config_set_mode", "rtlr_cu_run",
+    "rtlr_cu_problem_upload", "rtlr_cu_lr_params_default", "rtlr_cu_rng_create", "rtlr_cu_rng_destroy",
+    "rtlr_cu_rng_draw_below", "rtlr_cu_rng_sample", "rtlr_cu_lr_basis_create", "rtlr_cu_lr_basis_destroy",
+    "rtlr_cu_lr_basis_info", "rtlr_cu_lr_basis_get", "rtlr_cu_lr_basis_sampled", "rtlr_cu_lr_mgs_ro_update",
+    "rtlr_cu_lr_update_projections", "rtlr_cu_lr_galerkin_solve", "rtlr_cu_lr_residual_norms",
+    "rtlr_cu_lr_greedy_subsample", "rtlr_cu_lr_build_coefficients", "rtlr_cu_truncation_rank",
+    "rtlr_cu_truncate_factors", "rtlr_cu_low_rank_si", "rtlr_cu_inner_info", "rtlr_cu_inner_get",
+    "rtlr_cu_inner_sampled", "rtlr_cu_inner_destroy",
 ]
 
 
@@ -56,6 +63,23 @@ class LrOptions(ctypes.Structure):
                 ("eps_mgs", ctypes.c_double), ("eps_si_sa", ctypes.c_double),
                 ("max_iterations", ctypes.c_int), ("use_dsa", ctypes.c_int),
                 ("seed", ctypes.c_uint64), ("build_factors", ctypes.c_int)]
+
+
+class LrParams(ctypes.Structure):
+    """LowRankParams (low_rank.hpp:29-36)."""
+    _fields_ = [("p", ctypes.c_int), ("q", ctypes.c_int), ("eps_res", ctypes.c_double),
+                ("eps_diff", ctypes.c_double), ("eps_svd", ctypes.c_double), ("eps_mgs", ctypes.c_double)]
+
+
+class ProblemDesc(ctypes.Structure):
+    """rtlr_cu_problem_desc: a caller-assembled problem."""
+    _fields_ = [("nx", ctypes.c_int), ("ny", ctypes.c_int), ("x_min", ctypes.c_double),
+                ("x_max", ctypes.c_double), ("y_min", ctypes.c_double), ("y_max", ctypes.c_double),
+                ("n_theta", ctypes.c_int), ("n_omega_z", ctypes.c_int), ("n_omega", ctypes.c_int),
+                ("dirs", ctypes.c_void_p), ("weights", ctypes.c_void_p), ("sigma_t_blocks", ctypes.c_void_p),
+                ("sigma_s_blocks", ctypes.c_void_p), ("sigma_a_blocks", ctypes.c_void_p),
+                ("source", ctypes.c_void_p), ("boundary", ctypes.c_void_p), ("sip_bsr", ctypes.c_void_p),
+                ("use_dsa", ctypes.c_int)]
 
 
 class RtlrError(RuntimeError):
@@ -139,6 +163,37 @@ def load_library(path: str = LIB_PATH):
     L.rtlr_cu_shard_block.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.c_int, _ip, _ip, _ip]
     L.rtlr_cu_dense_qr.argtypes = [ctypes.c_int, ctypes.c_int64, ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p,
                                    ctypes.c_void_p]
+    V, Vp, Dp = ctypes.c_void_p, ctypes.POINTER(ctypes.c_void_p), _D
+    L.rtlr_cu_problem_upload.argtypes = [ctypes.POINTER(ProblemDesc), ctypes.c_int, Vp]
+    L.rtlr_cu_lr_params_default.argtypes = [ctypes.POINTER(LrParams)]
+    L.rtlr_cu_lr_params_default.restype = None
+    L.rtlr_cu_rng_create.argtypes = [ctypes.c_uint64, Vp]
+    L.rtlr_cu_rng_destroy.argtypes = [V]
+    L.rtlr_cu_rng_destroy.restype = None
+    L.rtlr_cu_rng_draw_below.argtypes = [V, ctypes.c_uint64, ctypes.POINTER(ctypes.c_uint64)]
+    L.rtlr_cu_rng_sample.argtypes = [V, _ip, ctypes.c_int, ctypes.c_int, _ip, _ip]
+    L.rtlr_cu_lr_basis_create.argtypes = [V, ctypes.POINTER(LrParams), V, ctypes.c_int, Vp]
+    L.rtlr_cu_lr_basis_destroy.argtypes = [V]
+    L.rtlr_cu_lr_basis_destroy.restype = None
+    L.rtlr_cu_lr_basis_info.argtypes = [V, _I64]
+    L.rtlr_cu_lr_basis_get.argtypes = [V, ctypes.c_char_p, V, ctypes.c_int]
+    L.rtlr_cu_lr_basis_sampled.argtypes = [V, _ip]
+    L.rtlr_cu_lr_mgs_ro_update.argtypes = [V, V, _ip, ctypes.c_int, ctypes.c_double, ctypes.c_double, ctypes.c_int,
+                                           _ip]
+    L.rtlr_cu_lr_update_projections.argtypes = [V, ctypes.c_int]
+    L.rtlr_cu_lr_galerkin_solve.argtypes = [V, _ip, ctypes.c_int, V, ctypes.c_int]
+    L.rtlr_cu_lr_residual_norms.argtypes = [V, _ip, ctypes.c_int, V, V, ctypes.c_int]
+    L.rtlr_cu_lr_greedy_subsample.argtypes = [V, ctypes.c_char_p, ctypes.c_int, ctypes.c_int, V, _ip, _ip, Dp, _ip,
+                                              _ip, V, V, ctypes.c_int]
+    L.rtlr_cu_lr_build_coefficients.argtypes = [V, _ip, ctypes.c_int, V, V, V, ctypes.c_int]
+    L.rtlr_cu_truncation_rank.argtypes = [Dp, ctypes.c_int, ctypes.c_double, _ip]
+    L.rtlr_cu_truncate_factors.argtypes = [V, V, V, ctypes.c_int, ctypes.c_double, ctypes.c_int, _ip, V, V, V]
+    L.rtlr_cu_low_rank_si.argtypes = [V, V, ctypes.POINTER(LrParams), V, ctypes.c_int, Vp]
+    L.rtlr_cu_inner_info.argtypes = [V, _I64]
+    L.rtlr_cu_inner_get.argtypes = [V, ctypes.c_char_p, V, ctypes.c_int]
+    L.rtlr_cu_inner_sampled.argtypes = [V, _ip]
+    L.rtlr_cu_inner_destroy.argtypes = [V]
+    L.rtlr_cu_inner_destroy.restype = None
     _lib = L
     return L
 
@@ -480,3 +535,316 @@ class Problem:
             except TypeError:  # interpreter shutdown: module globals already cleared
                 pass
             self.h = None
+
+
+# ---------------------------------------------------------------- caller-assembled problems
+def upload_problem(nx: int, ny: int, dirs, weights, sigma_t_blocks, sigma_s_blocks, source,
+                   domain=(0.0, 1.0, 0.0, 1.0), n_theta: int = 0, n_omega_z: int = 0, sigma_a_blocks=None,
+                   boundary=None, sip_bsr=None, use_dsa: bool = True, device: int = 0) -> "Problem":
+    """rtlr_cu_problem_upload: a Problem from the arrays the reference's
+    solvers take (solve_full_rank(ops, quad, bc, source, dsa, opts),
+    full_rank.hpp:41-43).  Blocks are (ncell, 4, 4) arrays (row, column);
+    dirs (n_omega, 3); boundary (n_omega, N_x) per-angle inflow vectors;
+    sip_bsr (ncell, 5, 4, 4) in the order self, west, east, south, north."""
+    def blocks(b):  # (ncell, 4, 4) -> ncell x 16 column-major blocks
+        b = np.asarray(b, dtype=np.float64)
+        return np.ascontiguousarray(b.reshape(-1, 4, 4).transpose(0, 2, 1)).ravel()
+
+    keep = []
+
+    def ptr(a):
+        if a is None:
+            return None
+        a = np.ascontiguousarray(a, dtype=np.float64)
+        keep.append(a)
+        return a.ctypes.data
+
+    dirs = np.asarray(dirs, dtype=np.float64).reshape(-1, 3)
+    d = ProblemDesc()
+    d.nx, d.ny = nx, ny
+    d.x_min, d.x_max, d.y_min, d.y_max = domain
+    d.n_theta, d.n_omega_z, d.n_omega = n_theta, n_omega_z, dirs.shape[0]
+    d.dirs, d.weights = ptr(dirs), ptr(weights)
+    d.sigma_t_blocks, d.sigma_s_blocks = ptr(blocks(sigma_t_blocks)), ptr(blocks(sigma_s_blocks))
+    d.sigma_a_blocks = ptr(None if sigma_a_blocks is None else blocks(sigma_a_blocks))
+    d.source = ptr(source)
+    d.boundary = ptr(boundary)
+    if sip_bsr is not None:
+        sip_bsr = np.ascontiguousarray(np.asarray(sip_bsr, dtype=np.float64).reshape(-1, 5, 4, 4)
+                                       .transpose(0, 1, 3, 2)).ravel()
+    d.sip_bsr = ptr(sip_bsr)
+    d.use_dsa = int(bool(use_dsa))
+    h = ctypes.c_void_p()
+    _check(load_library().rtlr_cu_problem_upload(ctypes.byref(d), device, ctypes.byref(h)))
+    return Problem._from_handle(h)
+
+
+def _problem_from_handle(cls, h):
+    self = cls.__new__(cls)
+    self.h = h
+    self._fields = []
+    info = np.zeros(8, dtype=np.int64)
+    _check(load_library().rtlr_cu_problem_info(self.h, info.ctypes.data_as(_I64)))
+    self.nx, self.ny, self.n_theta, self.n_omega_z, self.n, self.n_omega = (int(v) for v in info[:6])
+    self.n_unique = int(info[6])
+    self.sigma_t_uniform = bool(info[7])
+    self.ncell = self.n // 4
+    return self
+
+
+Problem._from_handle = classmethod(_problem_from_handle)
+
+
+# ---------------------------------------------------------------- low-rank primitives
+def lr_params(**kw) -> LrParams:
+    """LowRankParams with the reference's defaults (low_rank.hpp:29-36)."""
+    o = LrParams()
+    load_library().rtlr_cu_lr_params_default(ctypes.byref(o))
+    for k, v in kw.items():
+        setattr(o, k, v)
+    return o
+
+
+def _ints(a):
+    return np.ascontiguousarray(np.atleast_1d(np.asarray(a, dtype=np.int32)))
+
+
+class SubsampleRng:
+    """SubsampleRng (low_rank.hpp:18-27): mt19937_64, masked rejection."""
+
+    def __init__(self, seed: int):
+        h = ctypes.c_void_p()
+        _check(load_library().rtlr_cu_rng_create(seed, ctypes.byref(h)))
+        self.h = h
+
+    def draw_below(self, n: int) -> int:
+        out = ctypes.c_uint64(0)
+        _check(load_library().rtlr_cu_rng_draw_below(self.h, n, ctypes.byref(out)))
+        return out.value
+
+    def sample_without_replacement(self, pool, count: int) -> list:
+        pool = _ints(pool) if len(pool) else np.zeros(0, dtype=np.int32)
+        out = np.zeros(max(1, min(count, len(pool))), dtype=np.int32)
+        n = ctypes.c_int(0)
+        _check(load_library().rtlr_cu_rng_sample(self.h, pool.ctypes.data_as(_I), len(pool), count,
+                                                 out.ctypes.data_as(_I), ctypes.byref(n)))
+        return [int(v) for v in out[:n.value]]
+
+    def __del__(self):
+        if getattr(self, "h", None):
+            try:
+                load_library().rtlr_cu_rng_destroy(self.h)
+            except TypeError:
+                pass
+            self.h = None
+
+
+class LowRankBasis:
+    """LowRankBasis(ops, quad, bc, rhs_core) (low_rank.hpp:42-102) on the
+    problem's GPU: mgs_ro_update, update_projections, galerkin_solve,
+    residual norms and the projected operators, host numpy in and out."""
+
+    def __init__(self, problem: "Problem", rhs_core, params: LrParams = None):
+        self.problem = problem
+        rhs = np.ascontiguousarray(rhs_core, dtype=np.float64)
+        self.params = params or lr_params()
+        h = ctypes.c_void_p()
+        _check(load_library().rtlr_cu_lr_basis_create(problem.h, ctypes.byref(self.params), rhs.ctypes.data, HOST,
+                                                      ctypes.byref(h)))
+        self.h = h
+
+    def _info(self):
+        info = np.zeros(4, dtype=np.int64)
+        _check(load_library().rtlr_cu_lr_basis_info(self.h, info.ctypes.data_as(_I64)))
+        return [int(v) for v in info]
+
+    def rank(self) -> int:
+        return self._info()[0]
+
+    def snapshot_count(self) -> int:
+        return self._info()[1]
+
+    def _get(self, what, shape):
+        out = np.zeros(int(np.prod(shape)) or 1)
+        _check(load_library().rtlr_cu_lr_basis_get(self.h, what.encode(), out.ctypes.data, HOST))
+        return out[:int(np.prod(shape))].reshape(shape, order="F")
+
+    def basis(self) -> np.ndarray:
+        r, _, n, _ = self._info()
+        return self._get("basis", (n, r))
+
+    def coefficient_record(self) -> np.ndarray:
+        r, m, _, _ = self._info()
+        return self._get("record", (r, m))
+
+    def projected(self, which: str) -> np.ndarray:
+        """which: dx_minus | dx_plus | dy_minus | dy_plus | sigma_t"""
+        r = self.rank()
+        return self._get(which, (r, r))
+
+    def prhs(self) -> np.ndarray:
+        return self._get("prhs", (self.rank(),))
+
+    def sampled_angles(self) -> list:
+        m = self.snapshot_count()
+        out = np.zeros(max(1, m), dtype=np.int32)
+        _check(load_library().rtlr_cu_lr_basis_sampled(self.h, out.ctypes.data_as(_I)))
+        return [int(v) for v in out[:m]]
+
+    def mgs_ro_update(self, snapshots, angles, eps_mgs: float = 1e-10, drop_tol: float = 1e-12) -> bool:
+        snaps = np.asfortranarray(np.reshape(snapshots, (self.problem.n, -1), order="F"), dtype=np.float64)
+        ang = _ints(angles)
+        ro = ctypes.c_int(0)
+        _check(load_library().rtlr_cu_lr_mgs_ro_update(self.h, snaps.ctypes.data, ang.ctypes.data_as(_I), len(ang),
+                                                       eps_mgs, drop_tol, HOST, ctypes.byref(ro)))
+        return bool(ro.value)
+
+    def update_projections(self, reorthogonalized: bool):
+        _check(load_library().rtlr_cu_lr_update_projections(self.h, int(bool(reorthogonalized))))
+
+    def galerkin_solve(self, angles) -> np.ndarray:
+        """Reduced solutions, one column per angle (rank x m)."""
+        ang = _ints(angles)
+        r = self.rank()
+        out = np.zeros((r, len(ang)), order="F")
+        _check(load_library().rtlr_cu_lr_galerkin_solve(self.h, ang.ctypes.data_as(_I), len(ang), out.ctypes.data,
+                                                        HOST))
+        return out
+
+    def residual_norms(self, angles, coeffs) -> np.ndarray:
+        ang = _ints(angles)
+        c = np.asfortranarray(np.reshape(coeffs, (self.rank(), len(ang)), order="F"), dtype=np.float64)
+        out = np.zeros(len(ang))
+        _check(load_library().rtlr_cu_lr_residual_norms(self.h, ang.ctypes.data_as(_I), len(ang), c.ctypes.data,
+                                                        out.ctypes.data, HOST))
+        return out
+
+    def build_full_coefficients(self, candidates=(), candidate_solutions=None):
+        """(C, phi): C rank x N_Omega (record / candidates / Galerkin solves), phi = X (C w)."""
+        cand = _ints(candidates) if len(candidates) else np.zeros(0, dtype=np.int32)
+        r = self.rank()
+        cs = None
+        if len(cand):
+            cs = np.asfortranarray(np.reshape(candidate_solutions, (r, len(cand)), order="F"), dtype=np.float64)
+        C = np.zeros((r, self.problem.n_omega), order="F")
+        phi = np.zeros(self.problem.n)
+        _check(load_library().rtlr_cu_lr_build_coefficients(
+            self.h, cand.ctypes.data_as(_I), len(cand), None if cs is None else cs.ctypes.data, C.ctypes.data,
+            phi.ctypes.data, HOST))
+        return C, phi
+
+    def __del__(self):
+        if getattr(self, "h", None):
+            try:
+                load_library().rtlr_cu_lr_basis_destroy(self.h)
+            except TypeError:
+                pass
+            self.h = None
+
+
+def greedy_subsample(basis: LowRankBasis, sampled_mask, p: int, q: int, rng: SubsampleRng) -> dict:
+    """greedy_subsample (low_rank.hpp:114-116) -> SubsampleOutcome fields."""
+    mask = np.ascontiguousarray(np.asarray(sampled_mask, dtype=np.uint8))
+    r = basis.rank()
+    sel = np.zeros(max(1, p), dtype=np.int32)
+    cand = np.zeros(max(1, q), dtype=np.int32)
+    ns, nc = ctypes.c_int(0), ctypes.c_int(0)
+    mx = ctypes.c_double(0.0)
+    sols = np.zeros((r, q), order="F")
+    norms = np.zeros(q)
+    _check(load_library().rtlr_cu_lr_greedy_subsample(
+        basis.h, mask.tobytes(), p, q, rng.h, sel.ctypes.data_as(_I), ctypes.byref(ns), ctypes.byref(mx),
+        cand.ctypes.data_as(_I), ctypes.byref(nc), sols.ctypes.data, norms.ctypes.data, HOST))
+    m = nc.value
+    return {"selected": [int(v) for v in sel[:ns.value]], "max_residual": mx.value,
+            "candidates": [int(v) for v in cand[:m]], "candidate_solutions": sols[:, :m],
+            "residual_norms": norms[:m]}
+
+
+def truncation_rank(s, eps_svd: float) -> int:
+    """truncation_rank (low_rank.cpp:254-266)."""
+    s = np.ascontiguousarray(s, dtype=np.float64)
+    out = ctypes.c_int(0)
+    _check(load_library().rtlr_cu_truncation_rank(s.ctypes.data_as(_D), len(s), eps_svd, ctypes.byref(out)))
+    return out.value
+
+
+def truncate_factors(problem: "Problem", C, X, eps_svd: float):
+    """truncate_factors(C, X, eps_svd) (low_rank.cpp:268-277) on the GPU ->
+    (X_out, S, V) with X_out N_x x r', V N_Omega x r'."""
+    C = np.asfortranarray(C, dtype=np.float64)
+    X = np.asfortranarray(X, dtype=np.float64)
+    r = C.shape[0]
+    n, nom = X.shape[0], C.shape[1]
+    Xo = np.zeros((n, r), order="F")
+    S = np.zeros(r)
+    Vo = np.zeros((nom, r), order="F")
+    ro = ctypes.c_int(0)
+    _check(load_library().rtlr_cu_truncate_factors(problem.h, C.ctypes.data, X.ctypes.data, r, eps_svd, HOST,
+                                                   ctypes.byref(ro), Xo.ctypes.data, S.ctypes.data, Vo.ctypes.data))
+    k = ro.value
+    return Xo[:, :k].copy(order="F"), S[:k].copy(), Vo[:, :k].copy(order="F")
+
+
+def svd_values(problem: "Problem", C, X) -> np.ndarray:
+    """The per-outer-iteration singular values of C (low_rank.cpp:457)."""
+    C = np.asfortranarray(C, dtype=np.float64)
+    X = np.asfortranarray(X, dtype=np.float64)
+    r = C.shape[0]
+    S = np.zeros(r)
+    ro = ctypes.c_int(0)
+    _check(load_library().rtlr_cu_truncate_factors(problem.h, C.ctypes.data, X.ctypes.data, r, 0.0, HOST,
+                                                   ctypes.byref(ro), None, S.ctypes.data, None))
+    return S[:ro.value]
+
+
+class InnerLoopResult:
+    """InnerLoopResult (low_rank.hpp:125-136) of low_rank_si."""
+
+    def __init__(self, h):
+        self.h = h
+        info = np.zeros(8, dtype=np.int64)
+        _check(load_library().rtlr_cu_inner_info(h, info.ctypes.data_as(_I64)))
+        (self.iterations, self.rank, self.sampled_count, self.reorthogonalizations, self.verification_rejections,
+         ex, self.n, self.n_omega) = (int(v) for v in info)
+        self.exhausted_all_angles = bool(ex)
+
+    def _get(self, what, shape):
+        out = np.zeros(int(np.prod(shape)) or 1)
+        _check(load_library().rtlr_cu_inner_get(self.h, what.encode(), out.ctypes.data, HOST))
+        return out[:int(np.prod(shape))].reshape(shape, order="F")
+
+    @property
+    def phi_star(self):
+        return self._get("phi_star", (self.n,))
+
+    @property
+    def coefficients(self):
+        return self._get("coefficients", (self.rank, self.n_omega))
+
+    @property
+    def basis(self):
+        return self._get("basis", (self.n, self.rank))
+
+    @property
+    def sampled_order(self):
+        out = np.zeros(max(1, self.sampled_count), dtype=np.int32)
+        _check(load_library().rtlr_cu_inner_sampled(self.h, out.ctypes.data_as(_I)))
+        return [int(v) for v in out[:self.sampled_count]]
+
+    def __del__(self):
+        if getattr(self, "h", None):
+            try:
+                load_library().rtlr_cu_inner_destroy(self.h)
+            except TypeError:
+                pass
+            self.h = None
+
+
+def low_rank_si(problem: "Problem", phi_prev, params: LrParams, rng: SubsampleRng) -> InnerLoopResult:
+    """low_rank_si(ops, quad, bc, source, phi_prev, params, rng) (low_rank.hpp:141-144)."""
+    phi = np.ascontiguousarray(phi_prev, dtype=np.float64)
+    h = ctypes.c_void_p()
+    _check(load_library().rtlr_cu_low_rank_si(problem.h, phi.ctypes.data, ctypes.byref(params), rng.h, HOST,
+                                              ctypes.byref(h)))
+    return InnerLoopResult(h)

@@ -6,98 +6,16 @@
 #include <string>
 
 #include "../../include/rtlr_cu.h"
+#include "capi_internal.hpp"
 #include "dense.cuh"
 #include "harness.hpp"
 #include "problem.hpp"
 
 using namespace rtlr::cuda;
 
-struct rtlr_cu_config {
-  ProblemConfig cfg;
-  RunMode mode = RunMode::Both;  // run.mode (problem.hpp:83)
-};
-struct rtlr_cu_problem {
-  std::unique_ptr<Problem> p;
-};
-struct rtlr_cu_report {
-  SolveReport r;
-};
-
 namespace {
 
-thread_local std::string g_err;
-
-template <class F>
-int guard(F&& f) {
-  try {
-    f();
-    return RTLR_CU_OK;
-  } catch (const ConfigError& e) {
-    g_err = e.what();
-    return RTLR_CU_CONFIG_ERROR;
-  } catch (const CudaError& e) {
-    g_err = e.what();
-    return RTLR_CU_CUDA_ERROR;
-  } catch (const std::invalid_argument& e) {
-    g_err = e.what();
-    return RTLR_CU_INVALID_ARGUMENT;
-  } catch (const std::exception& e) {
-    g_err = e.what();
-    return RTLR_CU_RUNTIME_ERROR;
-  }
-}
-
-void need(bool c, const char* msg) {
-  if (!c) throw std::invalid_argument(msg);
-}
-
-// GPU entry points on a host-only (device < 0) problem fail loudly.
-Problem& gpu(rtlr_cu_problem* p) {
-  need(p != nullptr, "problem: null argument");
-  if (p->p->device() < 0) throw std::invalid_argument("problem was assembled host-only (device < 0)");
-  return *p->p;
-}
-
-// Stages a host or device input vector on the device.
-struct In {
-  const double* d = nullptr;
-  double* owned = nullptr;
-  In(const double* src, size_t n, int where, cudaStream_t s) {
-    if (where == RTLR_CU_DEVICE || src == nullptr) {
-      d = src;
-      return;
-    }
-    RTLR_CUDA(cudaMallocAsync(&owned, n * sizeof(double), s));
-    RTLR_CUDA(cudaMemcpyAsync(owned, src, n * sizeof(double), cudaMemcpyHostToDevice, s));
-    d = owned;
-  }
-  ~In() {
-    if (owned) cudaFree(owned);
-  }
-};
-struct Out {
-  double* d = nullptr;
-  double* host = nullptr;
-  size_t n = 0;
-  cudaStream_t s;
-  Out(double* dst, size_t n_, int where, cudaStream_t s_) : n(n_), s(s_) {
-    if (where == RTLR_CU_DEVICE || dst == nullptr) {
-      d = dst;
-      return;
-    }
-    host = dst;
-    RTLR_CUDA(cudaMallocAsync(&d, n * sizeof(double), s));
-  }
-  void finish() {
-    if (host) {
-      RTLR_CUDA(cudaMemcpyAsync(host, d, n * sizeof(double), cudaMemcpyDeviceToHost, s));
-      RTLR_CUDA(cudaStreamSynchronize(s));
-    }
-  }
-  ~Out() {
-    if (host && d) cudaFree(d);
-  }
-};
+using namespace rtlr_capi;
 
 void set_key(ProblemConfig& c, std::string k, double v) {
   for (const char* pre : {"mesh.", "quadrature.", "solver.", "domain.", "space."})

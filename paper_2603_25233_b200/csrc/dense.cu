@@ -814,6 +814,25 @@ __global__ void dot_partials(long long n, const double* __restrict__ a, const do
   if (threadIdx.x == 0) part[blockIdx.x] = s;
 }
 
+// dot_partials against column *col of B (a column chosen on the device);
+// *col < 0: zero.  Same partition and order as dot_partials.
+__global__ void dot_partials_ind(long long n, const double* __restrict__ a, const double* __restrict__ B, long long ldb,
+                                 const int* __restrict__ col, double* __restrict__ part) {
+  __shared__ double sh[32];
+  const int c = *col;
+  if (c < 0) {
+    if (threadIdx.x == 0) part[blockIdx.x] = 0.0;
+    return;
+  }
+  const double* b = B + static_cast<long long>(c) * ldb;
+  double s = 0.0;
+  for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<long long>(gridDim.x) * blockDim.x)
+    s += a[i] * b[i];
+  s = block_sum_all(s, sh);
+  if (threadIdx.x == 0) part[blockIdx.x] = s;
+}
+
 __global__ void dot_finish(int parts, const double* __restrict__ part, double* __restrict__ out) {
   __shared__ double sh[32];
   double s = 0.0;
@@ -1964,6 +1983,13 @@ void gemv_n(long long n, int k, const double* A, long long lda, const double* x,
 
 void dot(long long n, const double* a, const double* b, double* work, double* out, cudaStream_t s) {
   dot_partials<<<kDotParts, 256, 0, s>>>(n, a, b, work);
+  dot_finish<<<1, 256, 0, s>>>(kDotParts, work, out);
+  RTLR_CUDA(cudaGetLastError());
+}
+
+void dot_indirect(long long n, const double* a, const double* B, long long ldb, const int* d_col, double* work,
+                  double* out, cudaStream_t s) {
+  dot_partials_ind<<<kDotParts, 256, 0, s>>>(n, a, B, ldb, d_col, work);
   dot_finish<<<1, 256, 0, s>>>(kDotParts, work, out);
   RTLR_CUDA(cudaGetLastError());
 }

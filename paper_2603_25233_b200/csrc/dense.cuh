@@ -27,6 +27,9 @@ void gemv_n(long long n, int k, const double* A, long long lda, const double* x,
 // work >= kDotWork doubles
 constexpr int kDotWork = 296;
 void dot(long long n, const double* a, const double* b, double* work, double* out, cudaStream_t s);
+// out = a . B[:, *d_col] (column picked on the device; *d_col < 0 gives 0)
+void dot_indirect(long long n, const double* a, const double* B, long long ldb, const int* d_col, double* work,
+                  double* out, cudaStream_t s);
 void scale_copy(long long n, const double* x, const double* h, double* y, cudaStream_t s);  // y = x / *h
 void axpy_dev(long long n, const double* alpha, double sign, const double* x, double* y, cudaStream_t s);
 

@@ -390,6 +390,145 @@ void add16(double* dst, const double* src) {
 
 }  // namespace
 
+// SIP-DG diffusion matrix + Sigma_a (diffusion.cpp:90-193) from the
+// assembled Sigma_t / Sigma_a blocks and the mesh.
+void build_sip(HostProblem& hp) {
+  const double dx = hp.dx, dy = hp.dy;
+  hp.sip.clear();
+  // SIP-DG diffusion matrix + Sigma_a (diffusion.cpp:90-193), in BSR.  The
+  // reference sums duplicate triplets in insertion order: volume, x faces
+  // (rows b outer, faces af inner), y faces (columns a outer, bf inner),
+  // then adds Sigma_a.  For the self block of cell (a,b) that order is
+  // volume, left x face, right x face, bottom y face, top y face.
+  const double pen = 4.0 * std::max(1 * (1 + 1), 1);
+  std::vector<double> d_cell(hp.ncell);
+  for (int c = 0; c < hp.ncell; ++c) {
+    const double sig = hp.sigma_t[16 * static_cast<size_t>(c)];  // (0,0) entry
+    if (!(sig > 0.0)) throw std::runtime_error("build_diffusion: sigma_t must be positive");
+    d_cell[c] = 1.0 / (3.0 * sig);
+  }
+  double stx[4], sty[4], vol[16], voly[16];
+  stiffness_1d(dx, stx);
+  stiffness_1d(dy, sty);
+  tensor_x4(stx, vol);
+  tensor_y4(sty, voly);
+  for (int i = 0; i < 16; ++i) vol[i] = vol[i] + voly[i];
+  double vxl[2], vxr[2], gxl[2], gxr[2], vyl[2], vyr[2], gyl[2], gyr[2];
+  edge_values(dx, false, vxl);
+  edge_values(dx, true, vxr);
+  edge_derivatives(dx, false, gxl);
+  edge_derivatives(dx, true, gxr);
+  edge_values(dy, false, vyl);
+  edge_values(dy, true, vyr);
+  edge_derivatives(dy, false, gyl);
+  edge_derivatives(dy, true, gyr);
+  hp.sip.assign(static_cast<size_t>(hp.ncell) * 80, 0.0);
+  auto blk = [&](int c, int slot) { return &hp.sip[(static_cast<size_t>(c) * 5 + slot) * 16]; };
+  for (int c = 0; c < hp.ncell; ++c)
+    for (int i = 0; i < 16; ++i) blk(c, 0)[i] = d_cell[c] * vol[i];
+  // x faces: self-block contributions must be added left face first, then
+  // right face; both happen in this (b, af ascending) loop order.
+  double e[4], t16[16];
+  for (int b = 0; b < hp.ny; ++b)
+    for (int af = 0; af <= hp.nx; ++af) {
+      const bool has_l = af > 0, has_r = af < hp.nx;
+      const int cl = has_l ? b * hp.nx + af - 1 : -1, cr = has_r ? b * hp.nx + af : -1;
+      if (has_l && has_r) {
+        const double dl = d_cell[cl], dr = d_cell[cr];
+        const double wsum = dl + dr, wl = dr / wsum, wr = dl / wsum;
+        const double dharm = 2.0 * dl * dr / wsum;
+        const double gamma = pen * dharm / dx;
+        double fl[2], fr[2];
+        scale2(wl * dl, gxr, fl);
+        scale2(wr * dr, gxl, fr);
+        sip_face(vxr, fl, 1, vxr, fl, 1, gamma, e);
+        tensor_x4(e, t16);
+        add16(blk(cl, 0), t16);
+        sip_face(vxr, fl, 1, vxl, fr, -1, gamma, e);
+        tensor_x4(e, t16);
+        add16(blk(cl, 2), t16);  // east neighbour of cl
+        sip_face(vxl, fr, -1, vxr, fl, 1, gamma, e);
+        tensor_x4(e, t16);
+        add16(blk(cr, 1), t16);  // west neighbour of cr
+        sip_face(vxl, fr, -1, vxl, fr, -1, gamma, e);
+        tensor_x4(e, t16);
+        add16(blk(cr, 0), t16);
+      } else {
+        const int c = has_l ? cl : cr;
+        const double* v = has_l ? vxr : vxl;
+        double g[2];
+        if (has_l)
+          scale2(d_cell[c], gxr, g);
+        else
+          scale2(-d_cell[c], gxl, g);
+        const double gamma = pen * d_cell[c] / dx;
+        sip_face(v, g, 1, v, g, 1, gamma, e);
+        tensor_x4(e, t16);
+        add16(blk(c, 0), t16);
+      }
+    }
+  for (int a = 0; a < hp.nx; ++a)
+    for (int bf = 0; bf <= hp.ny; ++bf) {
+      const bool has_b = bf > 0, has_t = bf < hp.ny;
+      const int cb = has_b ? (bf - 1) * hp.nx + a : -1, ct = has_t ? bf * hp.nx + a : -1;
+      if (has_b && has_t) {
+        const double db = d_cell[cb], dt = d_cell[ct];
+        const double wsum = db + dt, wb = dt / wsum, wt = db / wsum;
+        const double dharm = 2.0 * db * dt / wsum;
+        const double gamma = pen * dharm / dy;
+        double fb[2], ft[2];
+        scale2(wb * db, gyr, fb);
+        scale2(wt * dt, gyl, ft);
+        sip_face(vyr, fb, 1, vyr, fb, 1, gamma, e);
+        tensor_y4(e, t16);
+        add16(blk(cb, 0), t16);
+        sip_face(vyr, fb, 1, vyl, ft, -1, gamma, e);
+        tensor_y4(e, t16);
+        add16(blk(cb, 4), t16);  // north neighbour of cb
+        sip_face(vyl, ft, -1, vyr, fb, 1, gamma, e);
+        tensor_y4(e, t16);
+        add16(blk(ct, 3), t16);  // south neighbour of ct
+        sip_face(vyl, ft, -1, vyl, ft, -1, gamma, e);
+        tensor_y4(e, t16);
+        add16(blk(ct, 0), t16);
+      } else {
+        const int c = has_b ? cb : ct;
+        const double* v = has_b ? vyr : vyl;
+        double g[2];
+        if (has_b)
+          scale2(d_cell[c], gyr, g);
+        else
+          scale2(-d_cell[c], gyl, g);
+        const double gamma = pen * d_cell[c] / dy;
+        sip_face(v, g, 1, v, g, 1, gamma, e);
+        tensor_y4(e, t16);
+        add16(blk(c, 0), t16);
+      }
+    }
+  for (int c = 0; c < hp.ncell; ++c) add16(blk(c, 0), &hp.sigma_a[16 * static_cast<size_t>(c)]);
+}
+
+void build_stream_consts(HostProblem& hp) {  // operators.cpp:101-112
+  double amx[4], apx[4], bmx[4], bpx[4], amy[4], apy[4], bmy[4], bpy[4];
+  stream_consts(hp.dx, amx, apx, bmx, bpx, hp.sc.trx_r, hp.sc.trx_l);
+  stream_consts(hp.dy, amy, apy, bmy, bpy, hp.sc.try_r, hp.sc.try_l);
+  tensor_x4(amx, hp.sc.ax_minus);
+  tensor_x4(apx, hp.sc.ax_plus);
+  tensor_x4(bmx, hp.sc.bx_minus);
+  tensor_x4(bpx, hp.sc.bx_plus);
+  tensor_y4(amy, hp.sc.ay_minus);
+  tensor_y4(apy, hp.sc.ay_plus);
+  tensor_y4(bmy, hp.sc.by_minus);
+  tensor_y4(bpy, hp.sc.by_plus);
+}
+
+void detect_uniform(HostProblem& hp) {  // every Sigma_t block bitwise identical
+  hp.sigma_t_uniform = true;
+  for (int c = 1; c < hp.ncell && hp.sigma_t_uniform; ++c)
+    if (std::memcmp(&hp.sigma_t[16 * static_cast<size_t>(c)], &hp.sigma_t[0], 16 * sizeof(double)) != 0)
+      hp.sigma_t_uniform = false;
+}
+
 void assemble(const ProblemConfig& cfg, HostProblem& hp) {
   const auto t0 = std::chrono::steady_clock::now();
   validate_config(cfg);
@@ -408,20 +547,7 @@ void assemble(const ProblemConfig& cfg, HostProblem& hp) {
   auto x_center = [&](int a) { return cfg.x_min + (a + 0.5) * ((cfg.x_max - cfg.x_min) / cfg.nx); };
   auto y_center = [&](int b) { return cfg.y_min + (b + 0.5) * ((cfg.y_max - cfg.y_min) / cfg.ny); };
 
-  // Streaming blocks (operators.cpp:101-112).
-  {
-    double amx[4], apx[4], bmx[4], bpx[4], amy[4], apy[4], bmy[4], bpy[4];
-    stream_consts(dx, amx, apx, bmx, bpx, hp.sc.trx_r, hp.sc.trx_l);
-    stream_consts(dy, amy, apy, bmy, bpy, hp.sc.try_r, hp.sc.try_l);
-    tensor_x4(amx, hp.sc.ax_minus);
-    tensor_x4(apx, hp.sc.ax_plus);
-    tensor_x4(bmx, hp.sc.bx_minus);
-    tensor_x4(bpx, hp.sc.bx_plus);
-    tensor_y4(amy, hp.sc.ay_minus);
-    tensor_y4(apy, hp.sc.ay_plus);
-    tensor_y4(bmy, hp.sc.by_minus);
-    tensor_y4(bpy, hp.sc.by_plus);
-  }
+  build_stream_consts(hp);
 
   // Cross-section blocks by 3x3 Gauss points (operators.cpp:137-181).
   std::vector<double> gn, gw;
@@ -461,10 +587,7 @@ void assemble(const ProblemConfig& cfg, HostProblem& hp) {
       double* bt = &hp.sigma_t[16 * static_cast<size_t>(c)];
       for (int i = 0; i < 16; ++i) bt[i] = bs[i] + ba[i];
     }
-  hp.sigma_t_uniform = true;
-  for (int c = 1; c < hp.ncell && hp.sigma_t_uniform; ++c)
-    if (std::memcmp(&hp.sigma_t[16 * static_cast<size_t>(c)], &hp.sigma_t[0], 16 * sizeof(double)) != 0)
-      hp.sigma_t_uniform = false;
+  detect_uniform(hp);
 
   // Source projection (operators.cpp:191-225).
   hp.source.assign(hp.ndof, 0.0);
@@ -508,120 +631,76 @@ void assemble(const ProblemConfig& cfg, HostProblem& hp) {
     }
   }
 
-  // SIP-DG diffusion matrix + Sigma_a (diffusion.cpp:90-193), in BSR.  The
-  // reference sums duplicate triplets in insertion order: volume, x faces
-  // (rows b outer, faces af inner), y faces (columns a outer, bf inner),
-  // then adds Sigma_a.  For the self block of cell (a,b) that order is
-  // volume, left x face, right x face, bottom y face, top y face.
   hp.sip.clear();
-  if (cfg.solver.use_dsa) {
-    const double pen = 4.0 * std::max(1 * (1 + 1), 1);
-    std::vector<double> d_cell(hp.ncell);
-    for (int c = 0; c < hp.ncell; ++c) {
-      const double sig = hp.sigma_t[16 * static_cast<size_t>(c)];  // (0,0) entry
-      if (!(sig > 0.0)) throw std::runtime_error("build_diffusion: sigma_t must be positive");
-      d_cell[c] = 1.0 / (3.0 * sig);
-    }
-    double stx[4], sty[4], vol[16], voly[16];
-    stiffness_1d(dx, stx);
-    stiffness_1d(dy, sty);
-    tensor_x4(stx, vol);
-    tensor_y4(sty, voly);
-    for (int i = 0; i < 16; ++i) vol[i] = vol[i] + voly[i];
-    double vxl[2], vxr[2], gxl[2], gxr[2], vyl[2], vyr[2], gyl[2], gyr[2];
-    edge_values(dx, false, vxl);
-    edge_values(dx, true, vxr);
-    edge_derivatives(dx, false, gxl);
-    edge_derivatives(dx, true, gxr);
-    edge_values(dy, false, vyl);
-    edge_values(dy, true, vyr);
-    edge_derivatives(dy, false, gyl);
-    edge_derivatives(dy, true, gyr);
-    hp.sip.assign(static_cast<size_t>(hp.ncell) * 80, 0.0);
-    auto blk = [&](int c, int slot) { return &hp.sip[(static_cast<size_t>(c) * 5 + slot) * 16]; };
-    for (int c = 0; c < hp.ncell; ++c)
-      for (int i = 0; i < 16; ++i) blk(c, 0)[i] = d_cell[c] * vol[i];
-    // x faces: self-block contributions must be added left face first, then
-    // right face; both happen in this (b, af ascending) loop order.
-    double e[4], t16[16];
-    for (int b = 0; b < hp.ny; ++b)
-      for (int af = 0; af <= hp.nx; ++af) {
-        const bool has_l = af > 0, has_r = af < hp.nx;
-        const int cl = has_l ? b * hp.nx + af - 1 : -1, cr = has_r ? b * hp.nx + af : -1;
-        if (has_l && has_r) {
-          const double dl = d_cell[cl], dr = d_cell[cr];
-          const double wsum = dl + dr, wl = dr / wsum, wr = dl / wsum;
-          const double dharm = 2.0 * dl * dr / wsum;
-          const double gamma = pen * dharm / dx;
-          double fl[2], fr[2];
-          scale2(wl * dl, gxr, fl);
-          scale2(wr * dr, gxl, fr);
-          sip_face(vxr, fl, 1, vxr, fl, 1, gamma, e);
-          tensor_x4(e, t16);
-          add16(blk(cl, 0), t16);
-          sip_face(vxr, fl, 1, vxl, fr, -1, gamma, e);
-          tensor_x4(e, t16);
-          add16(blk(cl, 2), t16);  // east neighbour of cl
-          sip_face(vxl, fr, -1, vxr, fl, 1, gamma, e);
-          tensor_x4(e, t16);
-          add16(blk(cr, 1), t16);  // west neighbour of cr
-          sip_face(vxl, fr, -1, vxl, fr, -1, gamma, e);
-          tensor_x4(e, t16);
-          add16(blk(cr, 0), t16);
-        } else {
-          const int c = has_l ? cl : cr;
-          const double* v = has_l ? vxr : vxl;
-          double g[2];
-          if (has_l)
-            scale2(d_cell[c], gxr, g);
-          else
-            scale2(-d_cell[c], gxl, g);
-          const double gamma = pen * d_cell[c] / dx;
-          sip_face(v, g, 1, v, g, 1, gamma, e);
-          tensor_x4(e, t16);
-          add16(blk(c, 0), t16);
-        }
-      }
-    for (int a = 0; a < hp.nx; ++a)
-      for (int bf = 0; bf <= hp.ny; ++bf) {
-        const bool has_b = bf > 0, has_t = bf < hp.ny;
-        const int cb = has_b ? (bf - 1) * hp.nx + a : -1, ct = has_t ? bf * hp.nx + a : -1;
-        if (has_b && has_t) {
-          const double db = d_cell[cb], dt = d_cell[ct];
-          const double wsum = db + dt, wb = dt / wsum, wt = db / wsum;
-          const double dharm = 2.0 * db * dt / wsum;
-          const double gamma = pen * dharm / dy;
-          double fb[2], ft[2];
-          scale2(wb * db, gyr, fb);
-          scale2(wt * dt, gyl, ft);
-          sip_face(vyr, fb, 1, vyr, fb, 1, gamma, e);
-          tensor_y4(e, t16);
-          add16(blk(cb, 0), t16);
-          sip_face(vyr, fb, 1, vyl, ft, -1, gamma, e);
-          tensor_y4(e, t16);
-          add16(blk(cb, 4), t16);  // north neighbour of cb
-          sip_face(vyl, ft, -1, vyr, fb, 1, gamma, e);
-          tensor_y4(e, t16);
-          add16(blk(ct, 3), t16);  // south neighbour of ct
-          sip_face(vyl, ft, -1, vyl, ft, -1, gamma, e);
-          tensor_y4(e, t16);
-          add16(blk(ct, 0), t16);
-        } else {
-          const int c = has_b ? cb : ct;
-          const double* v = has_b ? vyr : vyl;
-          double g[2];
-          if (has_b)
-            scale2(d_cell[c], gyr, g);
-          else
-            scale2(-d_cell[c], gyl, g);
-          const double gamma = pen * d_cell[c] / dy;
-          sip_face(v, g, 1, v, g, 1, gamma, e);
-          tensor_y4(e, t16);
-          add16(blk(c, 0), t16);
-        }
-      }
-    for (int c = 0; c < hp.ncell; ++c) add16(blk(c, 0), &hp.sigma_a[16 * static_cast<size_t>(c)]);
+  if (cfg.solver.use_dsa) build_sip(hp);
+  hp.assembly_seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+}
+
+void assemble_arrays(const ProblemArrays& in, HostProblem& hp) {
+  const auto t0 = std::chrono::steady_clock::now();
+  if (in.nx < 1 || in.ny < 1) throw std::invalid_argument("problem_upload: mesh must have at least one cell");
+  if (!(in.x_max > in.x_min) || !(in.y_max > in.y_min)) throw std::invalid_argument("problem_upload: empty domain");
+  if (in.n_omega < 1) throw std::invalid_argument("problem_upload: need at least one direction");
+  if (in.n_theta < 0 || in.n_omega_z < 0 ||
+      ((in.n_theta > 0 || in.n_omega_z > 0) && in.n_theta * in.n_omega_z != in.n_omega))
+    throw std::invalid_argument("problem_upload: n_theta * n_omega_z must equal n_omega");
+  if (!in.dirs || !in.weights || !in.sigma_t || !in.sigma_s || !in.source)
+    throw std::invalid_argument("problem_upload: dirs, weights, sigma_t, sigma_s and source are required");
+  ProblemConfig& c = hp.cfg;
+  c = ProblemConfig{};
+  c.preset = "uploaded";
+  c.x_min = in.x_min;
+  c.x_max = in.x_max;
+  c.y_min = in.y_min;
+  c.y_max = in.y_max;
+  c.nx = in.nx;
+  c.ny = in.ny;
+  // an unstructured direction set is one azimuthal line (partition_angles
+  // then deals single directions)
+  c.n_theta = in.n_theta > 0 ? in.n_theta : in.n_omega;
+  c.n_omega_z = in.n_omega_z > 0 ? in.n_omega_z : 1;
+  c.solver = in.solver;
+  c.solver.use_dsa = in.use_dsa;
+  c.boundary_zero = in.boundary == nullptr;
+  hp.nx = in.nx;
+  hp.ny = in.ny;
+  hp.ncell = in.nx * in.ny;
+  hp.ndof = 4 * hp.ncell;
+  hp.dx = (in.x_max - in.x_min) / in.nx;
+  hp.dy = (in.y_max - in.y_min) / in.ny;
+  hp.n_omega = in.n_omega;
+  const size_t nb = 16 * static_cast<size_t>(hp.ncell);
+  hp.dirs.assign(in.dirs, in.dirs + 3 * static_cast<size_t>(in.n_omega));
+  hp.weights.assign(in.weights, in.weights + in.n_omega);
+  for (double v : hp.dirs)
+    if (!std::isfinite(v)) throw std::invalid_argument("problem_upload: non-finite direction");
+  build_stream_consts(hp);
+  hp.sigma_t.assign(in.sigma_t, in.sigma_t + nb);
+  hp.sigma_s.assign(in.sigma_s, in.sigma_s + nb);
+  if (in.sigma_a) {
+    hp.sigma_a.assign(in.sigma_a, in.sigma_a + nb);
+  } else {
+    hp.sigma_a.resize(nb);
+    for (size_t i = 0; i < nb; ++i) hp.sigma_a[i] = hp.sigma_t[i] - hp.sigma_s[i];
   }
+  detect_uniform(hp);
+  hp.source.assign(in.source, in.source + hp.ndof);
+  hp.bc_any = false;
+  hp.bc.clear();
+  if (in.boundary) {
+    const size_t nbc = static_cast<size_t>(hp.n_omega) * hp.ndof;
+    double max_abs = 0.0;
+    for (size_t i = 0; i < nbc; ++i) max_abs = std::max(max_abs, std::abs(in.boundary[i]));
+    if (max_abs != 0.0) {  // BoundaryData stays empty for a zero datum (full_rank.cpp:32)
+      hp.bc_any = true;
+      hp.bc.assign(in.boundary, in.boundary + nbc);
+    }
+  }
+  hp.sip.clear();
+  if (in.sip)
+    hp.sip.assign(in.sip, in.sip + 80 * static_cast<size_t>(hp.ncell));
+  else if (in.use_dsa)
+    build_sip(hp);
   hp.assembly_seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
 }
 

@@ -86,6 +86,33 @@ struct HostProblem {
 
 void assemble(const ProblemConfig& cfg, HostProblem& out);
 
+// A caller-assembled problem (the inputs of solve_full_rank(ops, quad, bc,
+// source, dsa, ...), full_rank.hpp:41-43, as plain arrays): the K = 1 mesh,
+// any direction set, per-cell 4x4 cross-section blocks (column-major),
+// the projected source, optional per-angle inflow vectors and optional SIP
+// matrix.  Pointers are borrowed for the call.
+struct ProblemArrays {
+  int nx = 0, ny = 0;
+  double x_min = 0, x_max = 1, y_min = 0, y_max = 1;
+  int n_theta = 0, n_omega_z = 0;  // CL shape (0, 0: unstructured; n_omega given)
+  int n_omega = 0;
+  const double* dirs = nullptr;      // n_omega x 3 row-major
+  const double* weights = nullptr;   // n_omega
+  const double* sigma_t = nullptr;   // ncell x 16
+  const double* sigma_s = nullptr;   // ncell x 16
+  const double* sigma_a = nullptr;   // ncell x 16 or null (= sigma_t - sigma_s)
+  const double* source = nullptr;    // N_x
+  const double* boundary = nullptr;  // n_omega x N_x or null (vacuum)
+  const double* sip = nullptr;       // ncell x 5 x 16 or null (built from the blocks when use_dsa)
+  bool use_dsa = true;
+  SolverParams solver;
+};
+void assemble_arrays(const ProblemArrays& in, HostProblem& out);
+// pieces of assemble(), shared with assemble_arrays()
+void build_stream_consts(HostProblem& hp);
+void build_sip(HostProblem& hp);
+void detect_uniform(HostProblem& hp);
+
 // Boundary vector of one direction (operators.cpp:227-281).
 void boundary_vector(const HostProblem& hp, const Field& g, int angle, double* out);
 

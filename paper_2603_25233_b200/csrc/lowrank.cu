@@ -17,11 +17,11 @@
 #include <cstdlib>
 #include <cstdio>
 #include <string>
-#include <thread>
 
 #include <cooperative_groups.h>
 
 #include "dense.cuh"
+#include "lowrank.hpp"
 #include "problem.hpp"
 
 namespace rtlr {
@@ -153,6 +153,8 @@ struct CgsState {
   double h[kCgsMax];
   double coef[kCgsMax][kCgsMax];  // coef[i][j] = x_{r_old+j}^T rem_i (both passes)
   double c[kCgsMax];      // the current pass's coefficients
+  int ocol;               // last accepted column when the overlap test applies, else -1
+  double overlap;         // x_0^T x_ocol (low_rank.cpp:107-111)
 };
 
 // partial dots of X[:, j] (j < min(m, st.k)) with v; part[j * gridDim.x + block]
@@ -225,16 +227,18 @@ __global__ void cgs_axpy(long long n, int m, const double* __restrict__ X, long 
 }
 
 // the reference's conditional second pass: |rem| < 0.5 |snapshot| after pass 1
-__global__ void cgs_gate(CgsState* st, double norm0) {
+__global__ void cgs_gate(CgsState* st, const double* norm0p) {
+  const double norm0 = *norm0p;
   st->do2 = st->k > 0 && sqrt(st->rn2) < 0.5 * norm0;
 }
 
 // drop test h > 1e-12 |snapshot| (low_rank.hpp:61-62): accepted vectors take
 // the next column
-__global__ void cgs_accept(CgsState* st, int i, double norm0) {
+__global__ void cgs_accept(CgsState* st, int i, const double* norm0p, double drop_tol) {
+  const double norm0 = *norm0p;
   const double h = sqrt(st->h2);
   st->h[i] = h;
-  const int acc = norm0 > 0.0 && h > 1e-12 * norm0;
+  const int acc = norm0 > 0.0 && h > drop_tol * norm0;
   st->acc[i] = acc;
   st->pos[i] = st->k;
   if (acc) ++st->k;
@@ -250,6 +254,30 @@ __global__ void cgs_store(long long n, const double* __restrict__ v, const CgsSt
     col[e] = v[e] / h;
 }
 
+// The batch's record columns (low_rank.cpp:96-104) straight into the device
+// record: old-basis coefficients (both block passes, summed as the host did),
+// this batch's within-batch coefficients, h when accepted.  Column i of the
+// batch at rec + i*ldr; rows beyond a column's length stay zero.
+__global__ void rec_batch_kernel(int r_old, int p_in, const double* __restrict__ C1, const double* __restrict__ C2,
+                                 const CgsState* __restrict__ st, double* __restrict__ rec, long long ldr) {
+  const int i = blockIdx.x;
+  if (i >= p_in) return;
+  double* col = rec + static_cast<long long>(i) * ldr;
+  const int kb = st->pos[i];
+  for (int k = threadIdx.x; k < r_old; k += blockDim.x)
+    col[k] = C1[k + static_cast<long long>(i) * r_old] + C2[k + static_cast<long long>(i) * r_old];
+  for (int j = threadIdx.x; j < kb; j += blockDim.x) col[r_old + j] = st->coef[i][j];
+  if (threadIdx.x == 0 && st->acc[i]) col[r_old + kb] = st->h[i];
+}
+
+// The overlap test's column (low_rank.cpp:107-111): only when this batch
+// added a column and the rank is >= 2.
+__global__ void overlap_col_kernel(CgsState* st, int r_old) {
+  const int r = r_old + st->k;
+  st->ocol = (st->k > 0 && r >= 2) ? r - 1 : -1;
+  st->overlap = 0.0;
+}
+
 // The whole within-batch CGS of one batch in one cooperative launch
 // (kCgsParts CTAs x 256 threads, grid-wide barriers between dependent
 // steps) instead of ~13 launches per snapshot.  Every CTA reduces the
@@ -257,17 +285,15 @@ __global__ void cgs_store(long long n, const double* __restrict__ v, const CgsSt
 // per-thread index sets are those of cgs_dots / dot_partials, so the
 // results (and the CgsState the host reads) are bitwise those of the
 // launch-per-step sequence above.
-struct CgsNorms {
-  double v[kCgsMax];
-};
-
 __device__ __forceinline__ double cgs_warp_sum(double t) {
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
   return t;
 }
 
-__global__ void __launch_bounds__(256, 2) cgs_batch_kernel(long long n, int p_in, CgsNorms norm0, double* __restrict__ R,
+__global__ void __launch_bounds__(256, 2) cgs_batch_kernel(long long n, int p_in, const double* __restrict__ norm0,
+                                                           double drop_tol,
+                                                           double* __restrict__ R,
                                                            double* __restrict__ X, long long ldx, CgsState* st,
                                                            double* __restrict__ part, double* __restrict__ part2) {
   namespace cg = cooperative_groups;
@@ -372,7 +398,7 @@ __global__ void __launch_bounds__(256, 2) cgs_batch_kernel(long long n, int p_in
       else
         norm_only(rem);
       const double rn2 = finish_dot();
-      const int do2 = k > 0 && sqrt(rn2) < 0.5 * norm0.v[i];
+      const int do2 = k > 0 && sqrt(rn2) < 0.5 * norm0[i];
       if (lead && tid == 0) {
         st->rn2 = rn2;
         st->do2 = do2;
@@ -388,7 +414,7 @@ __global__ void __launch_bounds__(256, 2) cgs_batch_kernel(long long n, int p_in
       h2 = finish_dot();
     }
     const double h = sqrt(h2);
-    const int acc = norm0.v[i] > 0.0 && h > 1e-12 * norm0.v[i];
+    const int acc = norm0[i] > 0.0 && h > drop_tol * norm0[i];
     const int pos = k;
     if (lead && tid == 0) {
       st->h2 = h2;
@@ -406,164 +432,62 @@ __global__ void __launch_bounds__(256, 2) cgs_batch_kernel(long long n, int p_in
   }
 }
 
+__global__ void or_flags_kernel(int m, const int* __restrict__ flags, int* __restrict__ bad) {
+  int v = 0;
+  for (int j = threadIdx.x; j < m; j += blockDim.x) v |= flags[j];
+  v = __reduce_or_sync(0xffffffffu, v);
+  if ((threadIdx.x & 31) == 0 && v) atomicOr(bad, v);
+}
+
 int g1(long long n) {
   long long g = (n + 255) / 256;
   return static_cast<int>(std::max<long long>(1, std::min<long long>(g, 148 * 16)));
 }
 
-// Device matrix with geometric growth of its column capacity.
-struct DMat {
-  DBuf<double> buf;
-  long long ld = 0;
-  int cap = 0;
-  void reserve(long long rows, int cols, cudaStream_t s) {
-    if (cols <= cap && rows == ld) return;
-    const int nc = std::max({cols, 2 * cap, 16});
-    DBuf<double> nb;
-    nb.ensure(static_cast<size_t>(rows) * nc);
-    if (cap > 0 && rows == ld)
-      RTLR_CUDA(cudaMemcpyAsync(nb.get(), buf.get(), static_cast<size_t>(ld) * cap * sizeof(double),
-                                cudaMemcpyDeviceToDevice, s));
-    RTLR_CUDA(cudaStreamSynchronize(s));
-    buf.swap(nb);
-    ld = rows;
-    cap = nc;
-  }
-  double* col(int j) const { return buf.get() + static_cast<size_t>(ld) * j; }
-};
-
-// Per-phase wall-clock accounting (RTLR_PROFILE=1): synchronizes the stream
-// at phase boundaries, so it is off by default.
-struct PhaseTimer {
-  bool on = false;
-  cudaStream_t s = nullptr;
-  std::vector<std::pair<std::string, double>> acc;
-  std::chrono::steady_clock::time_point t0;
-  std::string cur;
-  void start(const char* name) {
-    if (!on) return;
-    RTLR_CUDA(cudaStreamSynchronize(s));
-    t0 = std::chrono::steady_clock::now();
-    cur = name;
-  }
-  void stop() {
-    if (!on) return;
-    RTLR_CUDA(cudaStreamSynchronize(s));
-    const double dt = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
-    for (auto& e : acc)
-      if (e.first == cur) {
-        e.second += dt;
-        return;
-      }
-    acc.push_back({cur, dt});
-  }
-};
-
 }  // namespace
 
-struct InnerResult {
-  int iterations = 0, rank = 0, sampled_count = 0, reorthogonalizations = 0, verification_rejections = 0;
-  bool exhausted = false;
-  std::vector<int> sampled_order;
-};
+LowRankEngine::LowRankEngine(Problem& P, const LowRankParams& prm) : P_(P), prm_(prm), hp_(P.hp_) {
+  s_ = P.stream_;
+  n_ = hp_.ndof;
+  nomega_ = hp_.n_omega;
+  rmax_ = static_cast<int>(std::min<long long>(n_, nomega_));
+  ldp_ = rmax_;
+  proj_.ensure(5 * static_cast<size_t>(ldp_) * ldp_);
+  prhs_.ensure(ldp_);
+  rhs_core_.ensure(n_);
+  phi_.ensure(n_);
+  phi_old_.ensure(n_);
+  rem_.ensure(n_);
+  vec_.ensure(3 * static_cast<size_t>(rmax_) + 64);
+  dirs_ = P.dirs_.get();
+  sa_ = StencilArgs{hp_.nx, hp_.ny, hp_.ncell, P.sigma_t_.get(), P.sc_};
+  RTLR_CUDA(cudaMallocHost(&hbuf_, 64 * sizeof(double)));
+  RTLR_CUDA(cudaMallocHost(&hstate_, sizeof(CgsState)));
+  RTLR_CUDA(cudaMallocHost(&hflags_, 2 * sizeof(int)));
+  hflags_[0] = hflags_[1] = 0;
+  gal_bad_.ensure(1);
+  RTLR_CUDA(cudaMemsetAsync(gal_bad_.get(), 0, sizeof(int), s_));
+  ring_.init(s_);
+  ldr_ = rmax_;
+  // The basis grows every inner iteration; reserving it for the largest
+  // possible rank up front (when that takes at most a quarter of the free
+  // device memory: 17 GB at C4) keeps multi-GB cudaMalloc/cudaFree pairs,
+  // which synchronise the device, out of the first outer iteration.
+  size_t free_b = 0, total_b = 0;
+  if (cudaMemGetInfo(&free_b, &total_b) == cudaSuccess &&
+      static_cast<double>(n_) * rmax_ * sizeof(double) <= 0.25 * static_cast<double>(free_b))
+    X_.reserve(n_, rmax_, s_);
+  const char* e = std::getenv("RTLR_PROFILE");
+  pt_.on = e && e[0] == '1';
+  pt_.s = s_;
+}
 
-// The inner-loop machinery (LowRankBasis + low_rank_si) on one GPU.
-class LowRankEngine {
- public:
-  LowRankEngine(Problem& P, const LowRankParams& prm) : P_(P), prm_(prm), hp_(P.hp_) {
-    s_ = P.stream_;
-    n_ = hp_.ndof;
-    nomega_ = hp_.n_omega;
-    rmax_ = static_cast<int>(std::min<long long>(n_, nomega_));
-    ldp_ = rmax_;
-    proj_.ensure(5 * static_cast<size_t>(ldp_) * ldp_);
-    prhs_.ensure(ldp_);
-    rhs_core_.ensure(n_);
-    phi_.ensure(n_);
-    phi_old_.ensure(n_);
-    rem_.ensure(n_);
-    vec_.ensure(3 * static_cast<size_t>(rmax_) + 64);
-    dirs_ = P.dirs_.get();
-    sa_ = StencilArgs{hp_.nx, hp_.ny, hp_.ncell, P.sigma_t_.get(), P.sc_};
-    RTLR_CUDA(cudaMallocHost(&hbuf_, 64 * sizeof(double)));
-    // The basis grows every inner iteration; reserving it for the largest
-    // possible rank up front (when that takes at most a quarter of the free
-    // device memory: 17 GB at C4) keeps multi-GB cudaMalloc/cudaFree pairs,
-    // which synchronise the device, out of the first outer iteration.
-    size_t free_b = 0, total_b = 0;
-    if (cudaMemGetInfo(&free_b, &total_b) == cudaSuccess &&
-        static_cast<double>(n_) * rmax_ * sizeof(double) <= 0.25 * static_cast<double>(free_b))
-      X_.reserve(n_, rmax_, s_);
-    const char* e = std::getenv("RTLR_PROFILE");
-    pt_.on = e && e[0] == '1';
-    pt_.s = s_;
-  }
-  ~LowRankEngine() { cudaFreeHost(hbuf_); }
-  PhaseTimer pt_;
-  int reorth_count_ = 0;        // Householder rebuilds (all inner loops)
-  int svd_sweeps_ = 0, svd_calls_ = 0;
-  long long gal_calls_ = 0, gal_systems_ = 0;
-  double reorth_seconds_ = 0.0;  // their wall time (meaningful with RTLR_PROFILE=1)
-  double cgs_split_[4] = {0, 0, 0, 0};  // RTLR_PROFILE: block GEMMs + host / per-snapshot loop / overlap / GEMMs only
-  void lap(int slot, std::chrono::steady_clock::time_point& t) {
-    if (!pt_.on) return;
-    RTLR_CUDA(cudaStreamSynchronize(s_));
-    const auto now = std::chrono::steady_clock::now();
-    cgs_split_[slot] += std::chrono::duration<double>(now - t).count();
-    t = now;
-  }
-
-  InnerResult inner(const double* d_phi_prev, SubsampleRng& rng);
-  int rank() const { return rank_; }
-  double* phi() { return phi_.get(); }
-  // Thin SVD of C (r x N_Omega): singular values (non-increasing); with U,
-  // V the factors X_out = X U[:, :r'] and V[:, :r'] of truncate_factors.
-  std::vector<double> svd(bool vectors, int keep, std::vector<double>* Xout, std::vector<double>* Vout);
-
- private:
-  void reset(const double* d_phi_prev);
-  bool mgs_ro_update(const double* snaps, const std::vector<int>& angles);
-  void update_projections(bool reorth);
-  void galerkin(const std::vector<int>& angles, double* d_sol, long long ldsol);
-  void galerkin_solve(const std::vector<int>& angles, double* d_sol, long long ldsol);
-  std::vector<double> residual_norms(const std::vector<int>& angles, const double* coeffs, long long ldc,
-                                     bool mirror_equal = false);
-  void build_full_coefficients(const std::vector<int>* cand, const double* cand_sol);
-  void phi_from_C();
-  double host_dot(const double* a, const double* b, long long n);
-  int* upload_ints(DBuf<int>& buf, const std::vector<int>& a);
-  double* work(size_t need) { return work_.ensure(std::max<size_t>(need, 4096)); }
-  // C = A^T B (K = N_x) with its split-K workspace
-  void tn(int M, int N, const double* A, long long lda, const double* B, long long ldb, double* C, long long ldc) {
-    double* w = work(gemm_tn_work(M, N, n_));
-    gemm_tn(M, N, n_, A, lda, B, ldb, C, ldc, w, work_.size(), s_);
-  }
-  // Angle sharding of one phase's m items over the communicator's ranks
-  // (the whole list without one); padded(m) = items incl. the all-gather pad.
-  ShardBlock blk(int m) const {
-    if (!P_.sharded()) return ShardBlock{0, m, m};
-    return shard_block(m, P_.nranks(), P_.rank());
-  }
-  int padded(int m) const { return P_.sharded() ? blk(m).bsz * P_.nranks() : m; }
-
-  Problem& P_;
-  LowRankParams prm_;
-  const HostProblem& hp_;
-  cudaStream_t s_;
-  long long n_;
-  int nomega_, rmax_;
-  long long ldp_;
-  StencilArgs sa_;
-  const double* dirs_;
-  DMat X_;
-  DBuf<double> proj_, prhs_, rhs_core_, phi_, phi_old_, rem_, vec_, C_, work_, snaps_, wbuf_, gbuf_, sol_, cand_,
-      ybuf_, nrm_, qa_, qq_, qr_, tau_, hrec_, luw_, gsol_, cgs_, svq_, svr_, svm_, rcoef_;
-  DBuf<int> ang_, ang2_, flags_, pos_, rfrom_;
-  double* hbuf_ = nullptr;
-  int rank_ = 0, n_snap_ = 0, prev_rank_ = 0;
-  std::vector<std::vector<double>> rec_;
-  std::vector<int> sampled_;
-};
+LowRankEngine::~LowRankEngine() {
+  cudaStreamSynchronize(s_);
+  cudaFreeHost(hbuf_);
+  cudaFreeHost(hstate_);
+  cudaFreeHost(hflags_);
+}
 
 double LowRankEngine::host_dot(const double* a, const double* b, long long n) {
   double* out = vec_.get() + 3 * static_cast<size_t>(rmax_);
@@ -573,31 +497,99 @@ double LowRankEngine::host_dot(const double* a, const double* b, long long n) {
   return hbuf_[0];
 }
 
-int* LowRankEngine::upload_ints(DBuf<int>& buf, const std::vector<int>& a) {
-  // (synchronous reuse of one buffer per call site: stream-ordered pool
-  // allocations per upload were tried and made the C4 solve 15-30% slower
-  // and erratic)
-  RTLR_CUDA(cudaStreamSynchronize(s_));  // the buffer may still feed a queued kernel
-  int* d = buf.ensure(std::max<size_t>(a.size(), 1));
-  if (!a.empty()) RTLR_CUDA(cudaMemcpyAsync(d, a.data(), a.size() * sizeof(int), cudaMemcpyHostToDevice, s_));
-  return d;
+int* LowRankEngine::upload_ints(DBuf<int>&, const std::vector<int>& a) { return ring_.upload(a); }
+
+// Deferred error flags: the sweeps' singular-block flag and the Galerkin
+// solves' non-finite flag are read with the next state the host reads anyway
+// (enqueue before that synchronisation, check after it); the reference's
+// exception and message follow.
+void LowRankEngine::flags_enqueue() {
+  RTLR_CUDA(cudaMemcpyAsync(hflags_, gal_bad_.get(), sizeof(int), cudaMemcpyDeviceToHost, s_));
+  RTLR_CUDA(cudaMemcpyAsync(hflags_ + 1, P_.err_.get(), sizeof(int), cudaMemcpyDeviceToHost, s_));
+}
+
+void LowRankEngine::flags_check() {
+  if (hflags_[1]) {
+    hflags_[1] = 0;
+    RTLR_CUDA(cudaMemsetAsync(P_.err_.get(), 0, sizeof(int), s_));
+    throw std::runtime_error("sweep: singular local block");
+  }
+  if (hflags_[0]) {
+    hflags_[0] = 0;
+    RTLR_CUDA(cudaMemsetAsync(gal_bad_.get(), 0, sizeof(int), s_));
+    throw std::runtime_error("galerkin_solve: singular reduced system");
+  }
 }
 
 void LowRankEngine::reset(const double* d_phi_prev) {
   // rhs_core = Sigma_s phi_prev + G; fresh basis (low_rank.cpp:349-351)
   P_.rhs_core(d_phi_prev, rhs_core_.get());
   RTLR_CUDA(cudaMemcpyAsync(phi_old_.get(), d_phi_prev, n_ * sizeof(double), cudaMemcpyDeviceToDevice, s_));
+  reset_rhs(nullptr);
+}
+
+// LowRankBasis(ops, quad, bc, rhs_core) (low_rank.cpp:39-44): an empty basis;
+// d_rhs_core == nullptr keeps the one reset() just formed.
+void LowRankEngine::reset_rhs(const double* d_rhs_core) {
+  if (d_rhs_core)
+    RTLR_CUDA(cudaMemcpyAsync(rhs_core_.get(), d_rhs_core, n_ * sizeof(double), cudaMemcpyDeviceToDevice, s_));
   rank_ = n_snap_ = prev_rank_ = 0;
-  rec_.clear();
+  rec_cols_ = std::max(rec_cols_, nomega_);
+  rec_.ensure(static_cast<size_t>(ldr_) * rec_cols_);
+  RTLR_CUDA(cudaMemsetAsync(rec_.get(), 0, static_cast<size_t>(ldr_) * rec_cols_ * sizeof(double), s_));
   sampled_.clear();
   X_.reserve(n_, 16, s_);
 }
 
-// proj/src/low_rank.cpp:66-132
+// Room for rank_need basis columns and snaps_need record columns.  The
+// solvers never exceed min(N_x, N_Omega) columns (every snapshot is a
+// distinct angle); the primitives accept any snapshot stream (the
+// reference's record grows, low_rank.cpp:45-64), so the projections, the
+// record and the small vectors grow geometrically, contents kept.
+void LowRankEngine::grow(int rank_need, int snaps_need) {
+  if (rank_need > rmax_) {
+    const int nr = static_cast<int>(std::min<long long>(n_, std::max(rank_need, 2 * rmax_)));
+    DBuf<double> np, nrec, nprhs;
+    np.ensure(5 * static_cast<size_t>(nr) * nr);
+    for (int k = 0; k < 5; ++k)
+      RTLR_CUDA(cudaMemcpy2DAsync(np.get() + static_cast<size_t>(k) * nr * nr, nr * sizeof(double),
+                                  proj_.get() + static_cast<size_t>(k) * ldp_ * ldp_, ldp_ * sizeof(double),
+                                  ldp_ * sizeof(double), ldp_, cudaMemcpyDeviceToDevice, s_));
+    nprhs.ensure(nr);
+    RTLR_CUDA(cudaMemcpyAsync(nprhs.get(), prhs_.get(), ldp_ * sizeof(double), cudaMemcpyDeviceToDevice, s_));
+    nrec.ensure(static_cast<size_t>(nr) * rec_cols_);
+    RTLR_CUDA(cudaMemsetAsync(nrec.get(), 0, static_cast<size_t>(nr) * rec_cols_ * sizeof(double), s_));
+    RTLR_CUDA(cudaMemcpy2DAsync(nrec.get(), nr * sizeof(double), rec_.get(), ldr_ * sizeof(double),
+                                ldr_ * sizeof(double), rec_cols_, cudaMemcpyDeviceToDevice, s_));
+    RTLR_CUDA(cudaStreamSynchronize(s_));
+    proj_.swap(np);
+    prhs_.swap(nprhs);
+    rec_.swap(nrec);
+    rmax_ = nr;
+    ldp_ = ldr_ = nr;
+    vec_.ensure(3 * static_cast<size_t>(rmax_) + 64);
+  }
+  if (snaps_need > rec_cols_) {
+    const int nc = std::max(snaps_need, 2 * rec_cols_);
+    DBuf<double> nrec;
+    nrec.ensure(static_cast<size_t>(ldr_) * nc);
+    RTLR_CUDA(cudaMemsetAsync(nrec.get(), 0, static_cast<size_t>(ldr_) * nc * sizeof(double), s_));
+    RTLR_CUDA(cudaMemcpyAsync(nrec.get(), rec_.get(), static_cast<size_t>(ldr_) * rec_cols_ * sizeof(double),
+                              cudaMemcpyDeviceToDevice, s_));
+    RTLR_CUDA(cudaStreamSynchronize(s_));
+    rec_.swap(nrec);
+    rec_cols_ = nc;
+  }
+}
+
+// proj/src/low_rank.cpp:66-132.  The coefficient record (low_rank.hpp:93,
+// R's r x n_snap matrix, a column per snapshot) lives on the device in rec_
+// (rmax x N_Omega, ld ldr_, zero below each column's length).
 bool LowRankEngine::mgs_ro_update(const double* snaps, const std::vector<int>& angles) {
   const int p_in = static_cast<int>(angles.size());
   prev_rank_ = rank_;
   const int m0 = n_snap_;
+  grow(static_cast<int>(std::min<long long>(n_, rank_ + p_in)), n_snap_ + p_in);
   X_.reserve(n_, rank_ + p_in, s_);
   std::vector<int> accepted;
   // Block classical Gram-Schmidt, equivalent to the reference's per-snapshot
@@ -615,11 +607,10 @@ bool LowRankEngine::mgs_ro_update(const double* snaps, const std::vector<int>& a
   RTLR_CUDA(cudaMemcpyAsync(Rm, snaps, static_cast<size_t>(n_) * p_in * sizeof(double), cudaMemcpyDeviceToDevice, s_));
   double* nr = nrm_.ensure(std::max(p_in, 128));
   col_norms_kernel<<<p_in, 256, 0, s_>>>(n_, p_in, snaps, n_, nr);
-  std::vector<double> norm0(p_in), cold;
-  RTLR_CUDA(cudaMemcpyAsync(norm0.data(), nr, p_in * sizeof(double), cudaMemcpyDeviceToHost, s_));
+  double *C1 = nullptr, *C2 = nullptr;
   if (r_old > 0) {
-    double* C1 = gbuf_.ensure(static_cast<size_t>(2) * r_old * p_in);
-    double* C2 = C1 + static_cast<size_t>(r_old) * p_in;
+    C1 = gbuf_.ensure(static_cast<size_t>(2) * r_old * p_in);
+    C2 = C1 + static_cast<size_t>(r_old) * p_in;
     auto tg = std::chrono::steady_clock::now();
     if (pt_.on) RTLR_CUDA(cudaStreamSynchronize(s_));
     tg = std::chrono::steady_clock::now();
@@ -631,20 +622,16 @@ bool LowRankEngine::mgs_ro_update(const double* snaps, const std::vector<int>& a
     tn(r_old, p_in, X_.col(0), X_.ld, Rm, n_, C2, r_old);
     gemm_nn(n_, p_in, r_old, X_.col(0), X_.ld, C2, r_old, Rm, n_, s_, /*subtract=*/true);
     lap(3, tg);
-    std::vector<double> h1(static_cast<size_t>(r_old) * p_in), h2(h1.size());
-    RTLR_CUDA(cudaMemcpyAsync(h1.data(), C1, h1.size() * sizeof(double), cudaMemcpyDeviceToHost, s_));
-    RTLR_CUDA(cudaMemcpyAsync(h2.data(), C2, h2.size() * sizeof(double), cudaMemcpyDeviceToHost, s_));
-    RTLR_CUDA(cudaStreamSynchronize(s_));
-    cold.resize(h1.size());
-    for (size_t k = 0; k < h1.size(); ++k) cold[k] = h1[k] + h2[k];
-  } else {
-    RTLR_CUDA(cudaStreamSynchronize(s_));
   }
   lap(0, tlap);
+  bool have_overlap = false;
+  double overlap = 0.0;
   // Within-batch CGS against the vectors this batch accepts.  Up to
   // kCgsMax snapshots (every regular batch): on the device, gated by device
-  // flags, one host read per batch.  Larger batches (verification offenders)
-  // take the host-driven loop.
+  // flags; the batch's record columns and the overlap test's dot product are
+  // formed there too, so the host reads one small state per batch (its only
+  // synchronisation).  Larger batches (verification offenders) take the
+  // host-driven loop.
   if (p_in <= kCgsMax) {
     double* part = work(static_cast<size_t>(kCgsMax) * kCgsParts + kDotWork + 8);
     double* dwork = part + static_cast<size_t>(kCgsMax) * kCgsParts;
@@ -661,12 +648,12 @@ bool LowRankEngine::mgs_ro_update(const double* snaps, const std::vector<int>& a
       return ok != 0 && per * sms >= kCgsParts && !(e && e[0] == '0');
     }();
     if (coop) {
-      CgsNorms nv{};
-      for (int i = 0; i < p_in; ++i) nv.v[i] = norm0[i];
       long long nn = n_;
       long long ldx = X_.ld;
       double* part2 = dwork;
-      void* args[] = {&nn, const_cast<int*>(&p_in), &nv, &Rm, &Xb, &ldx, &st, &part, &part2};
+      const double* nrc = nr;
+      double dtol = drop_tol_;
+      void* args[] = {&nn, const_cast<int*>(&p_in), &nrc, &dtol, &Rm, &Xb, &ldx, &st, &part, &part2};
       RTLR_CUDA(cudaLaunchCooperativeKernel(reinterpret_cast<void*>(cgs_batch_kernel), dim3(kCgsParts), dim3(256), args,
                                             0, s_));
     }
@@ -677,35 +664,44 @@ bool LowRankEngine::mgs_ro_update(const double* snaps, const std::vector<int>& a
         cgs_finish<<<1, 32 * kCgsMax, 0, s_>>>(i, kCgsParts, part, st, i, false);
         cgs_axpy<<<g1(n_), 256, 0, s_>>>(n_, i, Xb, X_.ld, st, false, rem);
         dot(n_, rem, rem, dwork, &st->rn2, s_);
-        cgs_gate<<<1, 1, 0, s_>>>(st, norm0[i]);
+        cgs_gate<<<1, 1, 0, s_>>>(st, nr + i);
         cgs_dots<<<kCgsParts, 256, 0, s_>>>(n_, i, Xb, X_.ld, rem, st, true, part);
         cgs_finish<<<1, 32 * kCgsMax, 0, s_>>>(i, kCgsParts, part, st, i, true);
         cgs_axpy<<<g1(n_), 256, 0, s_>>>(n_, i, Xb, X_.ld, st, true, rem);
       }
       dot(n_, rem, rem, dwork, &st->h2, s_);
-      cgs_accept<<<1, 1, 0, s_>>>(st, i, norm0[i]);
+      cgs_accept<<<1, 1, 0, s_>>>(st, i, nr + i, drop_tol_);
       cgs_store<<<g1(n_), 256, 0, s_>>>(n_, rem, st, i, Xb, X_.ld);
     }
+    rec_batch_kernel<<<p_in, 256, 0, s_>>>(r_old, p_in, C1, C2, st, rec_col(m0), ldr_);
+    overlap_col_kernel<<<1, 1, 0, s_>>>(st, r_old);
+    dot_indirect(n_, X_.col(0), X_.col(0), X_.ld, &st->ocol, dwork, &st->overlap, s_);
     RTLR_CUDA(cudaGetLastError());
-    CgsState h;
-    RTLR_CUDA(cudaMemcpyAsync(&h, st, sizeof(CgsState), cudaMemcpyDeviceToHost, s_));
+    CgsState* h = reinterpret_cast<CgsState*>(hstate_);
+    RTLR_CUDA(cudaMemcpyAsync(h, st, sizeof(CgsState), cudaMemcpyDeviceToHost, s_));
+    flags_enqueue();
     RTLR_CUDA(cudaStreamSynchronize(s_));
+    flags_check();
     for (int i = 0; i < p_in; ++i) {
-      // record column: old-basis coefficients, this batch's coefficients, h if accepted
-      const int k_before = h.pos[i];
-      std::vector<double> reccol(r_old + k_before + (h.acc[i] ? 1 : 0), 0.0);
-      for (int k = 0; k < r_old; ++k) reccol[k] = cold[k + static_cast<size_t>(i) * r_old];
-      for (int j = 0; j < k_before; ++j) reccol[r_old + j] = h.coef[i][j];
-      if (h.acc[i]) {
-        reccol[r_old + k_before] = h.h[i];
-        accepted.push_back(i);
-      }
-      rec_.push_back(std::move(reccol));
+      if (h->acc[i]) accepted.push_back(i);
       sampled_.push_back(angles[i]);
       ++n_snap_;
     }
-    rank_ = r_old + h.k;
+    rank_ = r_old + h->k;
+    have_overlap = h->ocol >= 0;
+    overlap = std::abs(h->overlap);
   } else {
+    std::vector<double> norm0(p_in), cold;
+    RTLR_CUDA(cudaMemcpyAsync(norm0.data(), nr, p_in * sizeof(double), cudaMemcpyDeviceToHost, s_));
+    if (r_old > 0) {
+      std::vector<double> h1(static_cast<size_t>(r_old) * p_in), h2(h1.size());
+      RTLR_CUDA(cudaMemcpyAsync(h1.data(), C1, h1.size() * sizeof(double), cudaMemcpyDeviceToHost, s_));
+      RTLR_CUDA(cudaMemcpyAsync(h2.data(), C2, h2.size() * sizeof(double), cudaMemcpyDeviceToHost, s_));
+      RTLR_CUDA(cudaStreamSynchronize(s_));
+      cold.resize(h1.size());
+      for (size_t k = 0; k < h1.size(); ++k) cold[k] = h1[k] + h2[k];
+    }
+    RTLR_CUDA(cudaStreamSynchronize(s_));
     double* cnew = vec_.get();
     double* corr = vec_.get() + rmax_;
     std::vector<double> hc(p_in), hc2(p_in);
@@ -729,7 +725,7 @@ bool LowRankEngine::mgs_ro_update(const double* snaps, const std::vector<int>& a
         for (int k = 0; k < k_new; ++k) reccol[r_old + k] = hc[k];
       }
       const double h = std::sqrt(host_dot(rem, rem, n_));
-      if (norm0[i] > 0.0 && h > 1e-12 * norm0[i]) {  // drop_tol (low_rank.hpp:61-62)
+      if (norm0[i] > 0.0 && h > drop_tol_ * norm0[i]) {  // drop_tol (low_rank.hpp:61-62)
         scale_val_kernel<<<g1(n_), 256, 0, s_>>>(n_, rem, h, X_.col(rank_));
         reccol[rank_] = h;
         accepted.push_back(i);
@@ -737,17 +733,19 @@ bool LowRankEngine::mgs_ro_update(const double* snaps, const std::vector<int>& a
       } else {
         reccol.resize(rank_);
       }
-      rec_.push_back(std::move(reccol));
+      // (pageable source: the copy is staged before the call returns)
+      RTLR_CUDA(cudaMemcpyAsync(rec_col(n_snap_), reccol.data(), reccol.size() * sizeof(double),
+                                cudaMemcpyHostToDevice, s_));
       sampled_.push_back(angles[i]);
       ++n_snap_;
     }
+    if (rank_ > prev_rank_ && rank_ >= 2) {
+      have_overlap = true;
+      overlap = std::abs(host_dot(X_.col(0), X_.col(rank_ - 1), n_));
+    }
   }
   lap(1, tlap);
-  bool reorth = false;
-  if (rank_ > prev_rank_ && rank_ >= 2) {
-    const double overlap = std::abs(host_dot(X_.col(0), X_.col(rank_ - 1), n_));
-    reorth = overlap > prm_.eps_mgs;
-  }
+  const bool reorth = have_overlap && overlap > prm_.eps_mgs;
   if (reorth) {
     ++reorth_count_;
     if (pt_.on) RTLR_CUDA(cudaStreamSynchronize(s_));
@@ -767,42 +765,23 @@ bool LowRankEngine::mgs_ro_update(const double* snaps, const std::vector<int>& a
     double* tau = tau_.ensure(r_new);
     double* qw = work(householder_qr_work(n_, r_new));
     householder_qr(n_, r_new, M, n_, tau, Q, n_, R, qw, work_.size(), s_);
-    std::vector<double> hR(static_cast<size_t>(r_new) * r_new);
-    RTLR_CUDA(cudaMemcpyAsync(hR.data(), R, hR.size() * sizeof(double), cudaMemcpyDeviceToHost, s_));
+    // batch columns: Q^T snapshots (low_rank.cpp:126-129)
     double* B = gbuf_.ensure(static_cast<size_t>(r_new) * p_in);
     tn(r_new, p_in, Q, n_, snaps, n_, B, r_new);
-    std::vector<double> hB(static_cast<size_t>(r_new) * p_in);
-    RTLR_CUDA(cudaMemcpyAsync(hB.data(), B, hB.size() * sizeof(double), cudaMemcpyDeviceToHost, s_));
     RTLR_CUDA(cudaMemcpyAsync(X_.col(0), Q, static_cast<size_t>(n_) * r_new * sizeof(double),
                               cudaMemcpyDeviceToDevice, s_));
-    RTLR_CUDA(cudaStreamSynchronize(s_));
-    std::vector<std::vector<double>> old(m0, std::vector<double>(prev_rank_, 0.0));
-    for (int j = 0; j < m0; ++j)
-      for (int i = 0; i < prev_rank_ && i < static_cast<int>(rec_[j].size()); ++i) old[j][i] = rec_[j][i];
     rank_ = r_new;
-    for (int j = 0; j < n_snap_; ++j) rec_[j].assign(rank_, 0.0);
     if (m0 > 0 && prev_rank_ > 0) {
-      // rec_j = R[:, :prev] old_j: k outer so R's columns stream contiguously
-      // (every element still sums k = 0, 1, ... in order: bitwise the same),
-      // records split over host threads (m0 x r x prev ~ 3e8 products at C4)
-      auto rows = [&](int j0, int j1) {
-        for (int j = j0; j < j1; ++j) {
-          std::vector<double>& out = rec_[j];
-          for (int k = 0; k < prev_rank_; ++k) {
-            const double o = old[j][k];
-            const double* rk = hR.data() + static_cast<size_t>(k) * r_new;
-            for (int i = 0; i < rank_; ++i) out[i] += rk[i] * o;
-          }
-        }
-      };
-      const int nt = std::max(1, std::min<int>(16, static_cast<int>(std::thread::hardware_concurrency())));
-      std::vector<std::thread> pool;
-      const int per = (m0 + nt - 1) / nt;
-      for (int t = 0; t < nt && t * per < m0; ++t) pool.emplace_back(rows, t * per, std::min(m0, (t + 1) * per));
-      for (auto& th : pool) th.join();
+      // old record columns: R[:, :prev] old_j (low_rank.cpp:121-125), one
+      // r_new x m0 x prev product on the DMMA tiles
+      double* T = hrec_.ensure(static_cast<size_t>(r_new) * m0);
+      gemm_nn(r_new, m0, prev_rank_, R, r_new, rec_.get(), ldr_, T, r_new, s_);
+      RTLR_CUDA(cudaMemcpy2DAsync(rec_.get(), ldr_ * sizeof(double), T, r_new * sizeof(double), r_new * sizeof(double),
+                                  m0, cudaMemcpyDeviceToDevice, s_));
     }
-    for (int j = 0; j < p_in; ++j)
-      for (int i = 0; i < rank_; ++i) rec_[m0 + j][i] = hB[i + static_cast<size_t>(j) * r_new];
+    RTLR_CUDA(cudaMemcpy2DAsync(rec_col(m0), ldr_ * sizeof(double), B, r_new * sizeof(double), r_new * sizeof(double),
+                                p_in, cudaMemcpyDeviceToDevice, s_));
+    if (pt_.on) RTLR_CUDA(cudaStreamSynchronize(s_));
     reorth_seconds_ += std::chrono::duration<double>(std::chrono::steady_clock::now() - tq0).count();
   }
   return reorth;
@@ -881,7 +860,6 @@ void LowRankEngine::galerkin_solve(const std::vector<int>& angles, double* d_sol
   const int chunk = rank_ > kSmemLuMax
                         ? static_cast<int>(std::min<long long>(65535, std::max<long long>(1, budget_bytes / per_system)))
                         : 4096;
-  int bad = 0;
   for (int j0 = sb.begin; j0 < sb.end; j0 += chunk) {
     const int mc = std::min(chunk, sb.end - j0);
     std::vector<int> sub(angles.begin() + j0, angles.begin() + j0 + mc);
@@ -908,24 +886,16 @@ void LowRankEngine::galerkin_solve(const std::vector<int>& angles, double* d_sol
     double* lw = rank_ > kSmemLuMax ? luw_.ensure(galerkin_work_doubles(rank_, mc)) : nullptr;
     galerkin_batch(rank_, mc, d_ang, dirs_, proj_.get(), ldp_, ldp_ * ldp_, prhs_.get(), extra, out, ldsol, flags, lw,
                    s_);
-    std::vector<int> hf(mc);
-    RTLR_CUDA(cudaMemcpyAsync(hf.data(), flags, mc * sizeof(int), cudaMemcpyDeviceToHost, s_));
-    RTLR_CUDA(cudaStreamSynchronize(s_));
-    for (int v : hf) bad |= v;
+    or_flags_kernel<<<1, 256, 0, s_>>>(mc, flags, gal_bad_.get());
+    RTLR_CUDA(cudaGetLastError());
   }
   if (P_.sharded()) {
-    // every rank learns of a singular system before anyone throws
-    int* d = flags_.ensure(1);
-    RTLR_CUDA(cudaMemcpyAsync(d, &bad, sizeof(int), cudaMemcpyHostToDevice, s_));
-    P_.allreduce_max(d, 1);
-    RTLR_CUDA(cudaMemcpyAsync(&bad, d, sizeof(int), cudaMemcpyDeviceToHost, s_));
-    RTLR_CUDA(cudaStreamSynchronize(s_));
-    if (!bad) {
-      if (ldsol != rank_) throw std::logic_error("galerkin: sharded solutions must be packed (ldsol == rank)");
-      P_.allgather_inplace(d_sol, static_cast<size_t>(sb.bsz) * ldsol);
-    }
+    // every rank holds the same flag (checked with the next host read, so all
+    // ranks throw together) and every column
+    P_.allreduce_max(gal_bad_.get(), 1);
+    if (ldsol != rank_) throw std::logic_error("galerkin: sharded solutions must be packed (ldsol == rank)");
+    P_.allgather_inplace(d_sol, static_cast<size_t>(sb.bsz) * ldsol);
   }
-  if (bad) throw std::runtime_error("galerkin_solve: singular reduced system");
 }
 
 // ||rhs_j - (D_j + Sigma_t) X c_j|| for the listed angles, expanded block-
@@ -978,7 +948,9 @@ std::vector<double> LowRankEngine::residual_norms(const std::vector<int>& angles
   }
   P_.allgather_inplace(nr_all, sb.bsz);
   RTLR_CUDA(cudaMemcpyAsync(out.data(), nr_all, m * sizeof(double), cudaMemcpyDeviceToHost, s_));
+  flags_enqueue();
   RTLR_CUDA(cudaStreamSynchronize(s_));
+  flags_check();
   return out;
 }
 
@@ -988,17 +960,13 @@ void LowRankEngine::build_full_coefficients(const std::vector<int>* cand, const 
   const int r = rank_;
   double* C = C_.ensure(static_cast<size_t>(r) * nomega_);
   std::vector<char> done(nomega_, 0);
-  std::vector<double> hrec(static_cast<size_t>(r) * n_snap_, 0.0);
   std::vector<int> idx(n_snap_);
   for (int i = 0; i < n_snap_; ++i) {
-    for (int k = 0; k < r && k < static_cast<int>(rec_[i].size()); ++k) hrec[k + static_cast<size_t>(i) * r] = rec_[i][k];
     idx[i] = sampled_[i];
     done[sampled_[i]] = 1;
   }
-  double* d = hrec_.ensure(std::max<size_t>(hrec.size(), 1));
-  RTLR_CUDA(cudaMemcpyAsync(d, hrec.data(), hrec.size() * sizeof(double), cudaMemcpyHostToDevice, s_));
   int* di = upload_ints(ang2_, idx);
-  scatter_cols<<<g1(static_cast<long long>(r) * n_snap_), 256, 0, s_>>>(r, n_snap_, di, d, r, C, r);
+  scatter_cols<<<g1(static_cast<long long>(r) * n_snap_), 256, 0, s_>>>(r, n_snap_, di, rec_.get(), ldr_, C, r);
   if (cand) {
     std::vector<int> to, from;
     for (size_t i = 0; i < cand->size(); ++i)
@@ -1039,6 +1007,49 @@ void LowRankEngine::phi_from_C() {
   gemv_n(n_, rank_, X_.col(0), X_.ld, cw, 1.0, phi_.get(), s_);
 }
 
+// proj/src/low_rank.cpp:217-252: q random unsampled candidates (the RNG's
+// partial Fisher-Yates over the ascending pool), their Galerkin solutions
+// (kept in cand_), full-space residual norms, the p largest (ties by angle).
+GreedyOutcome LowRankEngine::greedy_subsample(const std::vector<char>& sampled, int p, int q, SubsampleRng& rng) {
+  GreedyOutcome g;
+  std::vector<int> pool;
+  for (int j = 0; j < nomega_; ++j)
+    if (!sampled[j]) pool.push_back(j);
+  g.candidates = rng.sample_without_replacement(std::move(pool), q);
+  const std::vector<int>& cands = g.candidates;
+  const int m = static_cast<int>(cands.size());
+  if (m == 0) return g;
+  double* csol = cand_.ensure(static_cast<size_t>(rank_) * padded(m));
+  pt_.start("galerkin_q");
+  galerkin(cands, csol, rank_);
+  pt_.stop();
+  pt_.start("residual_q");
+  g.residual_norms = residual_norms(cands, csol, rank_, /*mirror_equal=*/true);
+  pt_.stop();
+  const std::vector<double>& norms = g.residual_norms;
+  std::vector<int> order(m);
+  std::iota(order.begin(), order.end(), 0);
+  std::sort(order.begin(), order.end(), [&](int a, int b) {
+    if (norms[a] != norms[b]) return norms[a] > norms[b];
+    return cands[a] < cands[b];
+  });
+  g.max_residual = norms[order.front()];
+  for (int i = 0; i < std::min(p, m); ++i) g.selected.push_back(cands[order[i]]);
+  return g;
+}
+
+// Loads caller factors for svd() (truncate_factors on external C and X).
+void LowRankEngine::load_factors(const double* d_C, const double* d_X, int r) {
+  if (r < 1 || r > n_) throw std::invalid_argument("truncate_factors: rank out of range");
+  grow(r, 0);
+  X_.reserve(n_, r, s_);
+  RTLR_CUDA(cudaMemcpy2DAsync(X_.col(0), X_.ld * sizeof(double), d_X, n_ * sizeof(double), n_ * sizeof(double), r,
+                              cudaMemcpyDeviceToDevice, s_));
+  double* C = C_.ensure(static_cast<size_t>(r) * nomega_);
+  RTLR_CUDA(cudaMemcpyAsync(C, d_C, static_cast<size_t>(r) * nomega_ * sizeof(double), cudaMemcpyDeviceToDevice, s_));
+  rank_ = r;
+}
+
 // proj/src/low_rank.cpp:340-434
 InnerResult LowRankEngine::inner(const double* d_phi_prev, SubsampleRng& rng) {
   if (prm_.p < 1 || prm_.q < prm_.p) throw std::invalid_argument("low_rank_si: need 1 <= p <= q");
@@ -1057,11 +1068,11 @@ InnerResult LowRankEngine::inner(const double* d_phi_prev, SubsampleRng& rng) {
     {  // sharded: this rank's block of the sampled sweeps, then one all-gather
       const ShardBlock sb = blk(p_now);
       P_.sweep(d_next + sb.begin, sb.end - sb.begin, rhs_core_.get(), 0, S + static_cast<size_t>(sb.begin) * n_, n_);
+      // (the singular-block flag is read with the CGS state; sharded, it is
+      // max-reduced first so every rank throws together)
       if (P_.sharded()) {
-        P_.check_error_all();
+        P_.allreduce_max(P_.err_.get(), 1);
         P_.allgather_inplace(S, static_cast<size_t>(sb.bsz) * n_);
-      } else {
-        P_.check_error();
       }
     }
     pt_.stop();
@@ -1083,28 +1094,11 @@ InnerResult LowRankEngine::inner(const double* d_phi_prev, SubsampleRng& rng) {
       phi_from_C();
       break;
     }
-    // greedy_subsample (low_rank.cpp:217-252)
-    std::vector<int> pool;
-    for (int j = 0; j < nomega_; ++j)
-      if (!sampled[j]) pool.push_back(j);
-    std::vector<int> cands = rng.sample_without_replacement(std::move(pool), prm_.q);
-    const int m = static_cast<int>(cands.size());
-    double* csol = cand_.ensure(static_cast<size_t>(rank_) * padded(m));
-    pt_.start("galerkin_q");
-    galerkin(cands, csol, rank_);
-    pt_.stop();
-    pt_.start("residual_q");
-    std::vector<double> norms = residual_norms(cands, csol, rank_, /*mirror_equal=*/true);
-    pt_.stop();
-    std::vector<int> order(m);
-    std::iota(order.begin(), order.end(), 0);
-    std::sort(order.begin(), order.end(), [&](int a, int b) {
-      if (norms[a] != norms[b]) return norms[a] > norms[b];
-      return cands[a] < cands[b];
-    });
-    const double max_residual = norms[order.front()];
-    next.clear();
-    for (int i = 0; i < std::min(prm_.p, m); ++i) next.push_back(cands[order[i]]);
+    const GreedyOutcome g = greedy_subsample(sampled, prm_.p, prm_.q, rng);
+    const std::vector<int>& cands = g.candidates;
+    const double* csol = cand_.get();
+    const double max_residual = g.max_residual;
+    next = g.selected;
 
     if (max_residual < prm_.eps_res) {
       pt_.start("build_C");
@@ -1115,7 +1109,9 @@ InnerResult LowRankEngine::inner(const double* d_phi_prev, SubsampleRng& rng) {
       double* w = work(2 * kNormParts + 8);
       diff_norms(static_cast<int>(n_), phi_.get(), phi_old_.get(), w, w + 2 * kNormParts, s_);
       RTLR_CUDA(cudaMemcpyAsync(hbuf_, w + 2 * kNormParts, 2 * sizeof(double), cudaMemcpyDeviceToHost, s_));
+      flags_enqueue();
       RTLR_CUDA(cudaStreamSynchronize(s_));
+      flags_check();
       if (hbuf_[0] <= prm_.eps_diff) {
         // verify every unsampled angle before accepting (low_rank.cpp:396-424)
         std::vector<int> unsampled;
@@ -1143,6 +1139,9 @@ InnerResult LowRankEngine::inner(const double* d_phi_prev, SubsampleRng& rng) {
       RTLR_CUDA(cudaMemcpyAsync(phi_old_.get(), phi_.get(), n_ * sizeof(double), cudaMemcpyDeviceToDevice, s_));
     }
   }
+  flags_enqueue();
+  RTLR_CUDA(cudaStreamSynchronize(s_));
+  flags_check();
   out.rank = rank_;
   out.sampled_count = n_snap_;
   return out;

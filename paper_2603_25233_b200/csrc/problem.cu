@@ -53,7 +53,9 @@ void Problem::set_comm(int nranks, int rank, const void* id) {
   std::vector<double> w;
   for (int a : mine) {
     const int u = uniq_of_[a];
-    if (seen[u]) continue;
+    // each distinct operator is swept by the rank owning its representative
+    // (CL mirror pairs never split; an arbitrary direction set may)
+    if (seen[u] || uniq_rep_[u] != a) continue;
     seen[u] = 1;
     reps.push_back(uniq_rep_[u]);
     w.push_back(uniq_w_host_[u]);
@@ -98,6 +100,17 @@ void invert4_host(const double* m, double* inv) {
 
 Problem::Problem(const ProblemConfig& cfg, int device) : device_(device) {
   assemble(cfg, hp_);
+  init();
+}
+
+// A caller-assembled problem (rtlr_cu_problem_upload): the host arrays are
+// taken as given (assemble_arrays validates and completes them).
+Problem::Problem(HostProblem&& hp, int device) : device_(device) {
+  hp_ = std::move(hp);
+  init();
+}
+
+void Problem::init() {
   dedupe_directions();
   if (device_ < 0) return;  // host-only assembly (inspection without a GPU)
   RTLR_CUDA(cudaSetDevice(device_));

@@ -112,6 +112,7 @@ void nccl_unique_id(unsigned char* out);
 class Problem {
  public:
   Problem(const ProblemConfig& cfg, int device);
+  Problem(HostProblem&& hp, int device);  // caller-assembled (assemble_arrays)
   ~Problem();
   Problem(const Problem&) = delete;
   Problem& operator=(const Problem&) = delete;
@@ -178,6 +179,7 @@ class Problem {
 
  private:
   friend class LowRankEngine;
+  void init();
   void upload();
   void dedupe_directions();
   PcgArgs pcg_args(const double* b, double* x);

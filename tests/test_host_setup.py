@@ -136,3 +136,55 @@ def test_c5_uniform_matches_oracle():
     vals = [O.c5_uniform(12345, c) for c in (0, 1, 2, 10**9, 2**40 + 7)]
     assert all(0.0 <= v < 1.0 for v in vals)
     assert len(set(vals)) == len(vals)
+
+
+@pytest.mark.parametrize("name,ov", [("pin_cell", {"nx": 12, "ny": 10}), ("C4", {"nx": 32, "ny": 32, "n_theta": 8,
+                                                                                "n_omega_z": 4})])
+def test_uploaded_arrays_assemble_like_the_preset(name, ov):
+    """rtlr_cu_problem_upload on the host (device < 0) with a preset's own
+    arrays: the completed problem (SIP matrix built from the blocks, streaming
+    blocks from the mesh) is bitwise the preset's."""
+    a = P.Problem(name, device=-1, **ov)
+    dom = {"pin_cell": (-1.0, 1.0, -1.0, 1.0), "C4": (0.0, 1.0, 0.0, 1.0)}[name]
+    u = P.upload_problem(a.nx, a.ny, a.get("dirs"), a.get("weights"), a.get("sigma_t_blocks"),
+                         a.get("sigma_s_blocks"), a.get("source"), domain=dom, n_theta=a.n_theta,
+                         n_omega_z=a.n_omega_z, sigma_a_blocks=a.get("sigma_a_blocks"), device=-1)
+    for what in ("dirs", "weights", "source", "sigma_t_blocks", "sigma_s_blocks", "sigma_a_blocks", "sip_bsr",
+                 "stream_blocks"):
+        assert np.array_equal(u.get(what), a.get(what)), what
+    assert (u.n_unique, u.sigma_t_uniform) == (a.n_unique, a.sigma_t_uniform)
+
+
+def test_upload_rejects_bad_descriptions():
+    a = P.Problem("homogeneous(1,1)", device=-1, nx=4, ny=4)
+    args = (a.nx, a.ny, a.get("dirs"), a.get("weights"), a.get("sigma_t_blocks"), a.get("sigma_s_blocks"),
+            a.get("source"))
+    with pytest.raises(P.InvalidArgument):
+        P.upload_problem(*args, n_theta=3, n_omega_z=3, device=-1)  # 9 != 32 directions
+    with pytest.raises(P.InvalidArgument):
+        P.upload_problem(0, 4, *args[2:], device=-1)
+    bad = a.get("sigma_t_blocks").copy()
+    bad[0, 0, 0] = 0.0
+    with pytest.raises(P.RtlrError, match="sigma_t must be positive"):
+        P.upload_problem(a.nx, a.ny, a.get("dirs"), a.get("weights"), bad, a.get("sigma_s_blocks"), a.get("source"),
+                         device=-1)
+
+
+def test_host_low_rank_helpers():
+    """SubsampleRng / truncation_rank through the ABI (host logic, no GPU):
+    the reference's known answers (test_low_rank.cpp:57-82, 330-336)."""
+    a, b = P.SubsampleRng(1234), P.SubsampleRng(1234)
+    for _ in range(50):
+        sa, sb = a.sample_without_replacement(list(range(128)), 3), b.sample_without_replacement(list(range(128)), 3)
+        assert sa == sb and len(set(sa)) == 3
+    c = P.SubsampleRng(99)
+    for _ in range(2000):
+        s = c.sample_without_replacement(list(range(10)), 3)
+        assert len(set(s)) == 3 and all(0 <= v < 10 for v in s)
+    assert sorted(P.SubsampleRng(5).sample_without_replacement(list(range(10)), 64)) == list(range(10))
+    assert P.truncation_rank([1.0, 1e-4, 1e-12], 1e-8) == 2
+    assert P.truncation_rank([1.0, 1e-4, 1e-12], 1e-2) == 1
+    assert P.truncation_rank([1.0, 1e-4, 1e-12], 1e-18) == 3
+    assert P.truncation_rank([0.0, 0.0, 0.0, 0.0], 1e-8) == 1
+    p = P.lr_params()
+    assert (p.p, p.q, p.eps_res, p.eps_diff, p.eps_svd, p.eps_mgs) == (1, 8, 1e-7, 1e-7, 1e-8, 1e-10)
