@@ -221,7 +221,10 @@ typedef struct {
 } rtlr_cu_problem_desc;
 int rtlr_cu_problem_upload(const rtlr_cu_problem_desc* desc, int device, rtlr_cu_problem** out);
 
-/* ---- low-rank primitives (low_rank.hpp:18-144), device-resident. */
+/* ---- low-rank primitives (low_rank.hpp:18-144), device-resident.  A basis
+ * or inner-loop result borrows its problem (as the reference's LowRankBasis
+ * borrows ops / quad / bc, low_rank.hpp:89-91): destroy it before the
+ * problem. */
 typedef struct rtlr_cu_rng rtlr_cu_rng;           /* SubsampleRng (low_rank.hpp:18-27) */
 typedef struct rtlr_cu_lr_basis rtlr_cu_lr_basis; /* LowRankBasis (low_rank.hpp:42-102) */
 typedef struct rtlr_cu_inner rtlr_cu_inner;       /* InnerLoopResult (low_rank.hpp:125-136) */

@@ -801,8 +801,9 @@ def svd_values(problem: "Problem", C, X) -> np.ndarray:
 class InnerLoopResult:
     """InnerLoopResult (low_rank.hpp:125-136) of low_rank_si."""
 
-    def __init__(self, h):
+    def __init__(self, h, problem):
         self.h = h
+        self.problem = problem  # the engine borrows the problem: keep it alive
         info = np.zeros(8, dtype=np.int64)
         _check(load_library().rtlr_cu_inner_info(h, info.ctypes.data_as(_I64)))
         (self.iterations, self.rank, self.sampled_count, self.reorthogonalizations, self.verification_rejections,
@@ -847,4 +848,4 @@ def low_rank_si(problem: "Problem", phi_prev, params: LrParams, rng: SubsampleRn
     h = ctypes.c_void_p()
     _check(load_library().rtlr_cu_low_rank_si(problem.h, phi.ctypes.data, ctypes.byref(params), rng.h, HOST,
                                               ctypes.byref(h)))
-    return InnerLoopResult(h)
+    return InnerLoopResult(h, problem)

@@ -79,6 +79,7 @@ def build(verbose: bool = False) -> str:
         if r.returncode != 0:
             raise RuntimeError(f"link failed:\n{r.stdout}\n{r.stderr}")
     _build_cli()
+    _build_facade_test()
     return LIB
 
 
@@ -96,6 +97,26 @@ def _build_cli():
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:
         raise RuntimeError(f"cli build failed:\n{r.stdout}\n{r.stderr}")
+
+
+FACADE_SRC = os.path.join(os.path.dirname(PKG), "tests", "cpp", "facade_test.cpp")
+FACADE = os.path.join(LIB_DIR, "rtlr_cu_facade_test")
+
+
+def _build_facade_test():
+    """The C++ consumer of include/rtlr_cu.hpp (the rtlr::cuda façade), built
+    against the header and the library only (tests/cpp/facade_test.cpp)."""
+    hdrs = [os.path.join(os.path.dirname(PKG), "include", f) for f in ("rtlr_cu.h", "rtlr_cu.hpp")]
+    if os.path.exists(FACADE) and os.path.getmtime(FACADE) >= max(os.path.getmtime(p) for p in
+                                                                  [FACADE_SRC, LIB] + hdrs):
+        return
+    nccl = [a for a in _nccl_link() if a.startswith("-L")]
+    cmd = ["g++", "-O2", "-std=c++17", "-Wall", "-Wextra", "-I", os.path.join(os.path.dirname(PKG), "include"),
+           FACADE_SRC, "-o", FACADE, "-L" + LIB_DIR, "-lrtlr_cu", "-Wl,-rpath,$ORIGIN"] + \
+          ["-Wl,-rpath-link," + a[2:] for a in nccl]
+    r = subprocess.run(cmd, capture_output=True, text=True)
+    if r.returncode != 0:
+        raise RuntimeError(f"facade test build failed:\n{r.stdout}\n{r.stderr}")
 
 
 if __name__ == "__main__":

@@ -334,3 +334,14 @@ def test_uploaded_problem_matches_preset_solves():
     assert np.array_equal(fa.phi, fu.phi) and fa.iterations == fu.iterations
     la, lu = a.solve_low_rank(seed=3), u.solve_low_rank(seed=3)
     assert np.array_equal(la.phi, lu.phi) and la.sampled_log() == lu.sampled_log()
+
+
+def test_cpp_facade_consumer_on_gpu():
+    """The C++ façade consumer (tests/cpp/facade_test.cpp) with its GPU checks:
+    solve_full_rank / solve_low_rank / LowRankBasis / greedy_subsample /
+    low_rank_si / DiffusionSystem through include/rtlr_cu.hpp."""
+    import subprocess
+    from paper_2603_25233_b200 import build as B
+    r = subprocess.run([B.FACADE], capture_output=True, text=True, timeout=600)
+    print(r.stdout, r.stderr)
+    assert r.returncode == 0, r.stdout + r.stderr

@@ -188,3 +188,14 @@ def test_host_low_rank_helpers():
     assert P.truncation_rank([0.0, 0.0, 0.0, 0.0], 1e-8) == 1
     p = P.lr_params()
     assert (p.p, p.q, p.eps_res, p.eps_diff, p.eps_svd, p.eps_mgs) == (1, 8, 1e-7, 1e-7, 1e-8, 1e-10)
+
+
+def test_cpp_facade_consumer_builds_and_runs_host_only():
+    """include/rtlr_cu.hpp (the rtlr::cuda façade of INTEGRATION.md §1) compiled
+    into a C++ consumer (tests/cpp/facade_test.cpp) that links only the
+    library; its host-only checks run without a GPU."""
+    import subprocess
+    from paper_2603_25233_b200 import build as B
+    B._build_facade_test()
+    r = subprocess.run([B.FACADE, "--no-gpu"], capture_output=True, text=True, timeout=120)
+    assert r.returncode == 0, r.stdout + r.stderr
