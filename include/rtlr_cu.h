@@ -99,7 +99,8 @@ int rtlr_cu_problem_get(const rtlr_cu_problem* p, const char* what, double* out)
 int rtlr_cu_problem_set_stream(rtlr_cu_problem* p, void* cuda_stream);
 /* "pcg_rtol", "pcg_max_iters", "pcg_multigrid" (0: block-Jacobi PCG), "sweep_kernel"
  * (0 auto, 1 skewed wavefront, 2 row scan, 3 row scan on prefactored cell blocks,
- * 4 cluster wavefront for a few directions) */
+ * 4 cluster wavefront for a few directions, 5 direction groups with a fused
+ * scalar-flux epilogue: heterogeneous media, one shared right-hand side) */
 int rtlr_cu_problem_set_option(rtlr_cu_problem* p, const char* key, double value);
 int rtlr_cu_synchronize(rtlr_cu_problem* p);
 

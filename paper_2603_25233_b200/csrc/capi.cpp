@@ -254,9 +254,9 @@ int rtlr_cu_problem_set_option(rtlr_cu_problem* p, const char* key, double v) {
     else if (k == "pcg_max_iters") p->p->pcg_max_iters = static_cast<int>(v);
     else if (k == "pcg_multigrid") p->p->pcg_multigrid = v != 0.0;
     else if (k == "sweep_kernel") {
-      need(v == 0.0 || v == 1.0 || v == 2.0 || v == 3.0 || v == 4.0,
+      need(v == 0.0 || v == 1.0 || v == 2.0 || v == 3.0 || v == 4.0 || v == 5.0,
            "sweep_kernel: 0 (auto), 1 (skewed wavefront), 2 (row scan), 3 (row scan, prefactored blocks), "
-           "4 (cluster wavefront)");
+           "4 (cluster wavefront), 5 (direction groups, heterogeneous media, shared right-hand side)");
       p->p->sweep_kernel = static_cast<int>(v);
     } else throw std::invalid_argument("unknown option '" + k + "'");
   });
@@ -291,7 +291,9 @@ int rtlr_cu_sweep(rtlr_cu_problem* p, const int* angles, int n, const double* rh
     const size_t rhs_n = rhs_stride == 0 ? h.ndof : static_cast<size_t>(rhs_stride) * (n - 1) + h.ndof;
     In r(rhs, rhs_n, where, s);
     Out o(psi, static_cast<size_t>(psi_stride) * (n - 1) + h.ndof, where, s);
-    P.sweep(d_ang, n, r.d, rhs_stride, o.d, psi_stride);
+    // one shared right-hand side in a heterogeneous medium: direction groups
+    if (!(rhs_stride == 0 && P.sweep_het(ang, nullptr, r.d, o.d, psi_stride, nullptr)))
+      P.sweep(d_ang, n, r.d, rhs_stride, o.d, psi_stride);
     o.finish();
     cudaFreeAsync(d_ang, s);
     P.check_error();

@@ -61,6 +61,8 @@ void Problem::set_comm(int nranks, int rank, const void* id) {
     w.push_back(uniq_w_host_[u]);
   }
   my_n_ = static_cast<int>(reps.size());
+  my_rep_host_ = reps;
+  my_w_host_ = w;
   my_idx_.upload(reps.data(), reps.size(), stream_);
   my_w_.upload(w.data(), w.size(), stream_);
   RTLR_CUDA(cudaStreamSynchronize(stream_));
@@ -340,6 +342,89 @@ void Problem::sweep(const int* d_angles, int n, const double* d_rhs, long long r
   launch_sweep_scan(a, hp_.sigma_t_uniform, stream_);
 }
 
+bool Problem::het_applies(int n) const {
+  if (sweep_kernel == 5) return !hp_.sigma_t_uniform && n > 0;
+  if (sweep_kernel != 0) return false;
+  static const bool off = [] {
+    const char* e = std::getenv("RTLR_SWEEP");
+    return e != nullptr && std::string(e) != "het";
+  }();
+  return !off && !hp_.sigma_t_uniform && n >= 4 * kHetD;
+}
+
+bool Problem::sweep_het(const std::vector<int>& angles, const std::vector<double>* weights, const double* d_rhs,
+                        double* d_psi, long long psi_stride, double* d_phi, bool use_bc) {
+  const int n = static_cast<int>(angles.size());
+  if (!het_applies(n)) return false;
+  const int nx = hp_.nx, ny = hp_.ny;
+  if (!sig_skew_.get()) {  // once per problem: the four skewed copies of Sigma_t
+    sig_skew_.ensure(skew_layout_doubles(nx, ny, 8));
+    build_skew_layout(nx, ny, sigma_t_.get(), 8, sig_skew_.get(), stream_);
+  }
+  build_skew_layout(nx, ny, d_rhs, 2, rhs_skew_.ensure(skew_layout_doubles(nx, ny, 2)), stream_);
+  // slot tables (cached: the full-rank iteration sweeps the same list every time)
+  const bool same = het_key_ == angles && (weights ? het_wkey_ == *weights : het_wkey_.empty());
+  if (!same) {
+    std::vector<int> orient, slot_angle, slot_pos;
+    std::vector<double> slot_w;
+    for (int o = 0; o < 4; ++o) {
+      std::vector<int> ks;
+      for (int k = 0; k < n; ++k) {
+        const int j = angles[k];
+        const int oj = (hp_.dirs[3 * j] >= 0.0 ? 0 : 1) + (hp_.dirs[3 * j + 1] >= 0.0 ? 0 : 2);  // sweep.cpp:37-38
+        if (oj == o) ks.push_back(k);
+      }
+      for (size_t g0 = 0; g0 < ks.size(); g0 += kHetD) {
+        orient.push_back(o);
+        for (int d = 0; d < kHetD; ++d) {
+          const bool real = g0 + d < ks.size();
+          const int k = real ? ks[g0 + d] : -1;
+          slot_angle.push_back(real ? angles[k] : -1);
+          slot_pos.push_back(k);
+          slot_w.push_back(real && weights ? (*weights)[k] : 0.0);
+        }
+      }
+    }
+    het_groups_ = static_cast<int>(orient.size());
+    std::vector<int> pack(orient);
+    pack.insert(pack.end(), slot_angle.begin(), slot_angle.end());
+    pack.insert(pack.end(), slot_pos.begin(), slot_pos.end());
+    het_i_.ensure(pack.size());
+    RTLR_CUDA(cudaMemcpyAsync(het_i_.get(), pack.data(), pack.size() * sizeof(int), cudaMemcpyHostToDevice, stream_));
+    het_w_.ensure(slot_w.size());
+    RTLR_CUDA(cudaMemcpyAsync(het_w_.get(), slot_w.data(), slot_w.size() * sizeof(double), cudaMemcpyHostToDevice,
+                              stream_));
+    RTLR_CUDA(cudaStreamSynchronize(stream_));  // the host tables may go
+    het_key_ = angles;
+    het_wkey_ = weights ? *weights : std::vector<double>();
+  }
+  const int G = het_groups_;
+  SweepHetArgs a{};
+  a.nx = nx;
+  a.ny = ny;
+  a.ngroups = G;
+  a.W = sweep_het_warps(nx, ny, G);
+  a.ndof = hp_.ndof;
+  a.dirs = dirs_.get();
+  a.group_orient = het_i_.get();
+  a.slot_angle = het_i_.get() + G;
+  a.slot_pos = het_i_.get() + G + static_cast<size_t>(G) * kHetD;
+  a.slot_weight = d_phi ? het_w_.get() : nullptr;
+  a.sig_skew = sig_skew_.get();
+  a.rhs_skew = rhs_skew_.get();
+  a.bc = (use_bc && hp_.bc_any) ? bc_.get() : nullptr;
+  a.bc_stride = hp_.ndof;
+  a.psi = d_psi;
+  a.psi_stride = psi_stride;
+  a.phi_part = d_phi ? het_part_.ensure(static_cast<size_t>(G) * hp_.ndof) : nullptr;
+  a.line = het_line_.ensure(static_cast<size_t>(G) * a.W * kHetD * nx * 2);
+  a.err = err_.get();
+  a.sc = sc_;
+  launch_sweep_het(a, stream_);
+  if (d_phi) reduce_phi_parts(hp_.ndof, G, a.phi_part, d_phi, stream_);
+  return true;
+}
+
 void Problem::sweep_host(const int* h_angles, int n, const double* h_rhs, long long rhs_stride, double* h_psi,
                          long long psi_stride) {
   // H2D / sweep / D2H pipelined over direction chunks on three streams with
@@ -459,8 +544,10 @@ void Problem::si_step(const double* d_phi_prev, double* d_phi_star, double* d_ps
   double* rc = scratch_.ensure(n + n * static_cast<size_t>(nu));
   double* psi_u = rc + n;
   rhs_core(d_phi_prev, rc);
-  sweep(angle_idx_.get(), nu, rc, 0, psi_u, static_cast<long long>(n));
-  phi_accumulate(static_cast<int>(n), nu, psi_u, static_cast<long long>(n), uniq_w_.get(), d_phi_star, stream_);
+  if (!sweep_het(uniq_rep_, &uniq_w_host_, rc, psi_u, static_cast<long long>(n), d_phi_star)) {
+    sweep(angle_idx_.get(), nu, rc, 0, psi_u, static_cast<long long>(n));
+    phi_accumulate(static_cast<int>(n), nu, psi_u, static_cast<long long>(n), uniq_w_.get(), d_phi_star, stream_);
+  }
   if (d_psi_or_null)
     for (int j = 0; j < hp_.n_omega; ++j)
       RTLR_CUDA(cudaMemcpyAsync(d_psi_or_null + j * n, psi_u + uniq_of_[j] * n, n * sizeof(double),
@@ -491,10 +578,21 @@ SolveReport Problem::solve_full_rank(const FullRankOptions& o) {
   const int nsweep = sharded ? my_n_ : nu;
   const int* sweep_idx = sharded ? my_idx_.get() : angle_idx_.get();
   const double* sweep_w = sharded ? my_w_.get() : uniq_w_.get();
+  const std::vector<int>& h_idx = sharded ? my_rep_host_ : uniq_rep_;
+  const std::vector<double>& h_w = sharded ? my_w_host_ : uniq_w_host_;
+  // Heterogeneous media: the direction-group sweep forms phi* in its
+  // epilogue and psi is never written (streaming path, full_rank.cpp:90-97);
+  // with store_psi the converged iteration's sweep is repeated once with psi
+  // output (bitwise the psi phi* came from).
+  const bool het = het_applies(nsweep);
   for (int it = 1; it <= o.max_iterations; ++it) {
     rhs_core(phi, rc);
-    sweep(sweep_idx, nsweep, rc, 0, psi_u, static_cast<long long>(n));
-    phi_accumulate(static_cast<int>(n), nsweep, psi_u, static_cast<long long>(n), sweep_w, phi_star, stream_);
+    if (het) {
+      sweep_het(h_idx, &h_w, rc, nullptr, 0, phi_star);
+    } else {
+      sweep(sweep_idx, nsweep, rc, 0, psi_u, static_cast<long long>(n));
+      phi_accumulate(static_cast<int>(n), nsweep, psi_u, static_cast<long long>(n), sweep_w, phi_star, stream_);
+    }
     if (sharded)
       RTLR_NCCL(ncclAllReduce(phi_star, phi_star, n, ncclDouble, ncclSum, static_cast<ncclComm_t>(comm_), stream_));
     diff_norms(static_cast<int>(n), phi_star, phi, norm_work_.get(), norm_work_.get() + 2 * kNormParts, stream_);
@@ -524,6 +622,10 @@ SolveReport Problem::solve_full_rank(const FullRankOptions& o) {
   }
   if (!rep.converged)
     RTLR_CUDA(cudaMemcpyAsync(phi, phi_star, n * sizeof(double), cudaMemcpyDeviceToDevice, stream_));
+  if (het && o.store_psi && !sharded) {  // psi of the last sweep: its right-hand side is still in rc
+    sweep_het(h_idx, &h_w, rc, psi_u, static_cast<long long>(n), nullptr);
+    check_error();
+  }
   rep.phi.resize(n);
   RTLR_CUDA(cudaMemcpyAsync(rep.phi.data(), phi, n * sizeof(double), cudaMemcpyDeviceToHost, stream_));
   RTLR_CUDA(cudaStreamSynchronize(stream_));

@@ -12,6 +12,7 @@
 #include "host.hpp"
 #include "linalg.cuh"
 #include "mg.cuh"
+#include "sweep_het.cuh"
 
 namespace rtlr {
 namespace cuda {
@@ -131,6 +132,15 @@ class Problem {
   // streams.  h_angles on the host.
   void sweep_host(const int* h_angles, int n, const double* h_rhs, long long rhs_stride, double* h_psi,
                   long long psi_stride);
+  // Heterogeneous medium, many directions, one shared right-hand side
+  // (the full-rank SI sweeps): the direction-group kernel (sweep_het.cu).
+  // weights (per listed angle) and d_phi: the scalar flux sum_k w_k psi_k is
+  // formed in the sweep's epilogue (no psi traffic); d_psi (optional) gets
+  // column k of angle k (psi_stride).  false when the kernel does not apply
+  // (uniform medium, too few directions): nothing was done.
+  bool sweep_het(const std::vector<int>& angles, const std::vector<double>* weights, const double* d_rhs,
+                 double* d_psi, long long psi_stride, double* d_phi, bool use_bc = true);
+  bool het_applies(int n) const;
   // StreamingOperator::apply (operators.cpp:283-288): out = (Sigma_t + Ox Dx + Oy Dy) v
   void apply(double omx, double omy, const double* d_v, double* d_out);
   // DiffusionSystem::solve / correct (diffusion.cpp:203-213); returns PCG iterations
@@ -175,7 +185,7 @@ class Problem {
   int pcg_max_iters = 20000;
   bool pcg_multigrid = true;  // false: block-Jacobi PCG
   int sweep_kernel = 0;  // 0 auto, 1 skewed wavefront (sweep.cu), 2 row scan, 3 row scan on prefactored blocks,
-                         // 4 cluster wavefront (few directions)
+                         // 4 cluster wavefront (few directions), 5 direction-group kernel (sweep_het.cu)
 
  private:
   friend class LowRankEngine;
@@ -204,8 +214,17 @@ class Problem {
   std::vector<double> uniq_w_host_;
   int nranks_ = 1, rank_ = 0;
   void* comm_ = nullptr;  // ncclComm_t
+  // direction-group sweep (sweep_het.cu): skewed Sigma_t (built once), the
+  // skewed source, trace lines, scalar-flux partials, the cached slot tables
+  DBuf<double> sig_skew_, rhs_skew_, het_line_, het_part_, het_w_;
+  DBuf<int> het_i_;
+  std::vector<int> het_key_;
+  std::vector<double> het_wkey_;
+  int het_groups_ = 0;
   DBuf<int> my_idx_;      // this rank's unique-direction representatives
   DBuf<double> my_w_;
+  std::vector<int> my_rep_host_;
+  std::vector<double> my_w_host_;
   int my_n_ = 0;
 };
 

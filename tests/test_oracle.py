@@ -310,3 +310,26 @@ def test_dsa_accelerates_si():  # acceptance.cpp criterion 7 (6 vs >= 200)
     plain = p.solve("full")
     assert dsa.converged and dsa.iterations == 6
     assert 5 * dsa.iterations <= plain.iterations
+
+
+def test_criterion5_fixture_reproduces_the_reference():
+    """The one-off oracle fixture tests/golden/criterion5.npz (make_criterion5.py)
+    against the reference's own reference-resolution results,
+    proj/test_output.txt:31 (acceptance.cpp:244-313): homogeneous(100,2) seed 1
+    rank 52, iterations 6/6; variable_scattering:full seed 1 rank 317, C-R
+    40.86 %, iterations 9/9; pin_cell:full FR 17 iterations, mean LR rank
+    220.00 over seeds 1..8.  The oracle reproduces every number exactly."""
+    import os
+    f = np.load(os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden", "criterion5.npz"))
+    assert int(f["homogeneous_100_2__lowrank__s1.factor_rank"]) == 52
+    assert int(f["homogeneous_100_2__full__s1.iterations"]) == 6
+    assert int(f["homogeneous_100_2__lowrank__s1.iterations"]) == 6
+    r = int(f["variable_scattering_full__lowrank__s1.factor_rank"])
+    assert r == 317
+    nx, nom = int(f["variable_scattering_full__lowrank__s1.n_dofs"]), int(f["variable_scattering_full__lowrank__s1.n_omega"])
+    assert round(100 * r * (nx + nom) / (nx * nom), 2) == 40.86
+    assert int(f["variable_scattering_full__full__s1.iterations"]) == 9
+    assert int(f["variable_scattering_full__lowrank__s1.iterations"]) == 9
+    assert int(f["pin_cell_full__full__s1.iterations"]) == 17
+    ranks = [int(f[f"pin_cell_full__lowrank__s{s}.factor_rank"]) for s in range(1, 9)]
+    assert np.mean(ranks) == 220.0
