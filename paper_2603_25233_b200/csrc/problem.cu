@@ -403,7 +403,11 @@ bool Problem::sweep_het(const std::vector<int>& angles, const std::vector<double
   a.nx = nx;
   a.ny = ny;
   a.ngroups = G;
-  a.W = sweep_het_warps(nx, ny, G);
+  static const int force_w = [] {  // RTLR_HET_W: warps per direction group (tuning)
+    const char* e = std::getenv("RTLR_HET_W");
+    return e ? std::atoi(e) : 0;
+  }();
+  a.W = force_w > 0 ? force_w : sweep_het_warps(nx, ny, G);
   a.ndof = hp_.ndof;
   a.dirs = dirs_.get();
   a.group_orient = het_i_.get();
@@ -544,7 +548,8 @@ void Problem::si_step(const double* d_phi_prev, double* d_phi_star, double* d_ps
   double* rc = scratch_.ensure(n + n * static_cast<size_t>(nu));
   double* psi_u = rc + n;
   rhs_core(d_phi_prev, rc);
-  if (!sweep_het(uniq_rep_, &uniq_w_host_, rc, psi_u, static_cast<long long>(n), d_phi_star)) {
+  if (!sweep_het(uniq_rep_, &uniq_w_host_, rc, d_psi_or_null ? psi_u : nullptr, static_cast<long long>(n),
+                 d_phi_star)) {
     sweep(angle_idx_.get(), nu, rc, 0, psi_u, static_cast<long long>(n));
     phi_accumulate(static_cast<int>(n), nu, psi_u, static_cast<long long>(n), uniq_w_.get(), d_phi_star, stream_);
   }

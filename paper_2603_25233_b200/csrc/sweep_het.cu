@@ -39,6 +39,9 @@ namespace {
 
 constexpr int kQ = 4;        // queue depth (steps in flight per warp)
 constexpr int kPlanes = 10;  // 16-byte planes per lane per step: Sigma_t (8) + source (2)
+// queue slot bytes: the planes of 32 lanes, then lane 0's prefetched
+// y-inflow traces of the step (kHetD x 16 bytes)
+constexpr int kSlotBytes = kPlanes * 512 + kHetD * 16;
 constexpr int kPublish = 2;  // columns per published progress update
 
 __device__ __forceinline__ double rcp64(double x) {
@@ -129,8 +132,8 @@ __global__ void __launch_bounds__(256, 1) sweep_het_kernel(const SweepHetArgs a)
   if (grp >= a.ngroups) return;  // a whole group exits together
   const int nx = a.nx, ny = a.ny, nb = (ny + 31) >> 5, S = nx > 32 ? nx : 32, dp = S + 31;
   // shared memory: per-warp queues, then per-group constants and counters
-  double* queue = smem + static_cast<size_t>(wib) * kQ * kPlanes * 64;  // slot s, plane p: 32 lanes x 2 doubles
-  double* gbase = smem + static_cast<size_t>(8) * kQ * kPlanes * 64 + static_cast<size_t>(gl) * (D * kDirConsts + 8);
+  double* queue = smem + static_cast<size_t>(wib) * kQ * (kSlotBytes / 8);  // slot s, plane p: 32 lanes x 2 doubles
+  double* gbase = smem + static_cast<size_t>(8) * kQ * (kSlotBytes / 8) + static_cast<size_t>(gl) * (D * kDirConsts + 8);
   double* dc = gbase;                                             // D x kDirConsts
   volatile int* prod = reinterpret_cast<volatile int*>(gbase + D * kDirConsts);  // W counters
   const int orient = a.group_orient[grp];
@@ -147,6 +150,9 @@ __global__ void __launch_bounds__(256, 1) sweep_het_kernel(const SweepHetArgs a)
       if (ang < 0) {
         for (int k = 0; k < kDirConsts; ++k) c[k] = 0.0;
         c[0] = c[1] = c[2] = c[3] = 1.0;  // identity block for padding slots (results unused)
+        int* ci = reinterpret_cast<int*>(c + 13);
+        ci[0] = -1;
+        ci[1] = 0;
       } else {
         const double omx = a.dirs[3 * ang], omy = a.dirs[3 * ang + 1];
         const double* ax = xu ? a.sc.ax_minus : a.sc.ax_plus;  // 4x4 tensorized, column-major
@@ -165,7 +171,9 @@ __global__ void __launch_bounds__(256, 1) sweep_het_kernel(const SweepHetArgs a)
         c[10] = omy * (yu ? -a.sc.try_l[0] : a.sc.try_r[0]);
         c[11] = omy * (yu ? -a.sc.try_l[1] : a.sc.try_r[1]);
         c[12] = a.slot_weight ? a.slot_weight[slot] : 0.0;
-        c[13] = 0.0;
+        int* ci = reinterpret_cast<int*>(c + 13);
+        ci[0] = a.slot_pos[slot];
+        ci[1] = ang;
       }
     }
     if (lane < W) prod[lane] = 0;
@@ -183,9 +191,16 @@ __global__ void __launch_bounds__(256, 1) sweep_het_kernel(const SweepHetArgs a)
   const int total = kw * S + 31;
   const unsigned qbase = static_cast<unsigned>(__cvta_generic_to_shared(queue)) + lane * 16;
 
-  // lane stream: k-th band of the warp, column col (skew: col = t - lane - k S)
+  // lane stream: k-th band of the warp, column col (skew: col = t - lane - k S).
+  // Lane 0 also prefetches the step's y-inflow traces (the band below, from
+  // the producer warp's line) when they are already published; otherwise it
+  // waits for them at the step itself.
+  int seen = 0;  // MULTI: producer progress already observed
+  int f0k = 0, f0c = 0;  // lane 0's prefetch position (band ordinal, column), warp-uniform
+  const bool own_pf = !MULTI && S > 31 + kQ;  // W = 1: own line, written >= S - 31 steps earlier
+  bool pf[kQ];
   auto fill = [&](int slot, int k, int col) {
-    const unsigned q = qbase + slot * kPlanes * 512;
+    const unsigned q = qbase + slot * kSlotBytes;
     const bool ok = k < kw && col >= 0 && col < S;
     const int band = w + k * W;
     const long long pos = ok ? (static_cast<long long>(band) * dp + (col + lane)) : 0;
@@ -195,6 +210,36 @@ __global__ void __launch_bounds__(256, 1) sweep_het_kernel(const SweepHetArgs a)
     for (int p = 0; p < 8; ++p) cp16(q + p * 512, s8 + p * 32);
     cp16(q + 8 * 512, s2);
     cp16(q + 9 * 512, s2 + 32);
+    // Lane 0's traces for that step: the band below, column f0c of the
+    // producer's line.  The position (f0k, f0c) is lane 0's, kept in every
+    // lane, so the wait below is taken by the whole warp together (a lane-0
+    // spin would leave the warp diverged for the solves that follow).  The
+    // wait happens here, kQ steps ahead: the consumer trails its producer by
+    // the lane skew plus the queue depth and the traces arrive by cp.async,
+    // off the step's critical path.
+    pf[slot] = false;
+    if (f0k < kw && f0c < nx && w + f0k * W > 0) {
+      if (MULTI) {
+        const int gidx = (w > 0 ? f0k : f0k - 1) * nx + f0c;  // ordinal of band - 1 in warp pw
+        if (seen <= gidx) {
+          while ((seen = prod[pw]) <= gidx) {
+          }
+        }
+        __threadfence_block();
+      }
+      if (MULTI || own_pf) {
+        if (lane == 0) {
+          const unsigned ql = qbase + slot * kSlotBytes + kPlanes * 512;
+#pragma unroll
+          for (int d = 0; d < D; ++d) cp16(ql + d * 16, in_line + (static_cast<long long>(d) * nx + f0c) * 2);
+        }
+        pf[slot] = true;
+      }
+    }
+    if (++f0c == S) {
+      f0c = 0;
+      ++f0k;
+    }
   };
   int pk = 0, pcol = -lane;  // prefetch stream position
 #pragma unroll
@@ -210,13 +255,12 @@ __global__ void __launch_bounds__(256, 1) sweep_het_kernel(const SweepHetArgs a)
   double txi[D][2], tyo[D][2];
 #pragma unroll
   for (int k = 0; k < D; ++k) txi[k][0] = txi[k][1] = tyo[k][0] = tyo[k][1] = 0.0;
-  int seen = 0;
   for (int t0 = 0; t0 < total; t0 += kQ) {
 #pragma unroll
     for (int s = 0; s < kQ; ++s) {
       if (t0 + s >= total) break;  // warp-uniform
       cp_wait<kQ - 1>();
-      const unsigned q = qbase + s * kPlanes * 512;
+      const unsigned q = qbase + s * kSlotBytes;
       double m[16];
 #pragma unroll
       for (int p = 0; p < 8; ++p) {
@@ -225,13 +269,6 @@ __global__ void __launch_bounds__(256, 1) sweep_het_kernel(const SweepHetArgs a)
         m[2 * p + 1] = v.y;
       }
       const double2 r01 = lds2(q + 8 * 512), r23 = lds2(q + 9 * 512);
-      __syncwarp();
-      fill(s, pk, pcol);
-      cp_commit();
-      if (++pcol == S) {
-        pcol = 0;
-        ++pk;
-      }
       // y inflow traces: from lane - 1's previous step
       double yi[D][2];
 #pragma unroll
@@ -243,28 +280,44 @@ __global__ void __launch_bounds__(256, 1) sweep_het_kernel(const SweepHetArgs a)
       const int row = band * 32 + lane;
       const bool act = ck < kw && ccol >= 0 && ccol < nx && row < ny;
       const int col = ccol;
-      if (act) {
-        if (lane == 0) {
-          if (band == 0) {
+      if (lane == 0 && act) {  // lane 0: the band below's traces
+        if (band == 0) {
 #pragma unroll
-            for (int k = 0; k < D; ++k) yi[k][0] = yi[k][1] = 0.0;
-          } else {
-            if (MULTI) {
-              const int gidx = ((band - 1 - pw) / W) * nx + col;
-              if (seen <= gidx) {
-                while ((seen = prod[pw]) <= gidx) {
-                }
-                __threadfence_block();
+          for (int k = 0; k < D; ++k) yi[k][0] = yi[k][1] = 0.0;
+        } else if (pf[s]) {
+#pragma unroll
+          for (int k = 0; k < D; ++k) {
+            const double2 v = lds2(q + kPlanes * 512 + k * 16);
+            yi[k][0] = v.x;
+            yi[k][1] = v.y;
+          }
+        } else {
+          if (MULTI) {
+            const int gidx = (w > 0 ? ck : ck - 1) * nx + col;
+            if (seen <= gidx) {
+              while ((seen = prod[pw]) <= gidx) {
               }
-            }
-#pragma unroll
-            for (int k = 0; k < D; ++k) {
-              const double2 v = __ldcg(reinterpret_cast<const double2*>(in_line + (static_cast<long long>(k) * nx + col) * 2));
-              yi[k][0] = v.x;
-              yi[k][1] = v.y;
+              __threadfence_block();
             }
           }
+#pragma unroll
+          for (int k = 0; k < D; ++k) {
+            const double2 v = __ldcg(reinterpret_cast<const double2*>(in_line + (static_cast<long long>(k) * nx + col) * 2));
+            yi[k][0] = v.x;
+            yi[k][1] = v.y;
+          }
         }
+      }
+      fill(s, pk, pcol);
+      cp_commit();
+      if (++pcol == S) {
+        pcol = 0;
+        ++pk;
+      }
+      // reconverge before the cell solves (lane 0 may have waited for its
+      // producer above; diverged lanes would run the solves twice)
+      __syncwarp();
+      if (act) {
         if (col == 0) {
 #pragma unroll
           for (int k = 0; k < D; ++k) txi[k][0] = txi[k][1] = 0.0;
@@ -281,9 +334,10 @@ __global__ void __launch_bounds__(256, 1) sweep_het_kernel(const SweepHetArgs a)
           const double2 c89 = *reinterpret_cast<const double2*>(c + 8), cab = *reinterpret_cast<const double2*>(c + 10);
           const double wk = c[12];
           double v0 = r01.x, v1 = r01.y, v2 = r23.x, v3 = r23.y;
+          const int* ci = reinterpret_cast<const int*>(c + 13);
           if (a.bc) {
             double g[4];
-            ld_cell(a.bc + static_cast<long long>(a.slot_angle[grp * D + k]) * a.bc_stride + 4 * cell, g);
+            ld_cell(a.bc + static_cast<long long>(ci[1]) * a.bc_stride + 4 * cell, g);
             v0 += g[0];
             v1 += g[1];
             v2 += g[2];
@@ -303,7 +357,10 @@ __global__ void __launch_bounds__(256, 1) sweep_het_kernel(const SweepHetArgs a)
           double a01 = m[4] + c45.y, a11 = m[5] + c01.y, a21 = m[6], a31 = m[7] + c67.x;
           double a02 = m[8] + c67.y, a12 = m[9], a22 = m[10] + c23.x, a32 = m[11] + c45.x;
           double a03 = m[12], a13 = m[13] + c67.y, a23 = m[14] + c45.y, a33 = m[15] + c23.y;
-          const double amax = fmax(fmax(fabs(a00), fabs(a11)), fmax(fabs(a22), fabs(a33)));
+          // the diagonal of a positive-real block is positive: max / min by
+          // the bit patterns (integer pipe); a negative or NaN entry fails below
+          const long long amax_b = max(max(__double_as_longlong(a00), __double_as_longlong(a11)),
+                                       max(__double_as_longlong(a22), __double_as_longlong(a33)));
           // elimination without pivoting
           const double r0 = rcp64(a00);
           const double l1 = a10 * r0, l2 = a20 * r0, l3 = a30 * r0;
@@ -336,10 +393,12 @@ __global__ void __launch_bounds__(256, 1) sweep_het_kernel(const SweepHetArgs a)
           const double p2 = (v2 - a23 * p3) * r2;
           const double p1 = (v1 - a12 * p2 - a13 * p3) * r1;
           const double p0 = (v0 - a01 * p1 - a02 * p2 - a03 * p3) * r0;
-          const double dmin = fmin(fmin(a00, a11), fmin(a22, a33));
-          ok = ok && (dmin > 1e-14 * amax);
+          const long long dmin_b = min(min(__double_as_longlong(a00), __double_as_longlong(a11)),
+                                       min(__double_as_longlong(a22), __double_as_longlong(a33)));
+          ok = ok && (__longlong_as_double(dmin_b) > 1e-14 * __longlong_as_double(amax_b)) &&
+               isfinite(p0 + p1 + p2 + p3);
           if (a.psi) {
-            const int pos = a.slot_pos[grp * D + k];
+            const int pos = ci[0];
             if (pos >= 0) st_cell256(a.psi + static_cast<long long>(pos) * a.psi_stride + 4 * cell, p0, p1, p2, p3);
           }
           acc0 += wk * p0;
@@ -411,7 +470,7 @@ void launch_sweep_het(const SweepHetArgs& a, cudaStream_t s) {
   if (a.ngroups <= 0) return;
   const int groups_per_block = 8 / a.W;
   const int blocks = (a.ngroups + groups_per_block - 1) / groups_per_block;
-  const size_t smem = (static_cast<size_t>(8) * kQ * kPlanes * 64 +
+  const size_t smem = (static_cast<size_t>(8) * kQ * (kSlotBytes / 8) +
                        static_cast<size_t>(groups_per_block) * (kHetD * kDirConsts + 8)) *
                       sizeof(double);
   auto go = [&](auto kern) {

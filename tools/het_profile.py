@@ -18,7 +18,11 @@ reps = np.array([j1 * nz + j2 for j1 in range(g.n_theta) for j2 in range(nz // 2
 n = g.n
 rhs = torch.rand(n, dtype=torch.float64, device="cuda")
 psi = torch.empty(len(reps) * n, dtype=torch.float64, device="cuda")
+mode = sys.argv[3] if len(sys.argv) > 3 else "psi"
 for _ in range(3):
-    g.sweep_device(reps.ctypes.data, len(reps), rhs.data_ptr(), 0, psi.data_ptr(), n)
+    if mode == "psi":
+        g.sweep_device(reps.ctypes.data, len(reps), rhs.data_ptr(), 0, psi.data_ptr(), n)
+    else:  # si_step: the scalar flux in the sweep epilogue, no psi
+        g.si_step(np.linspace(0.0, 1.0, n))
 torch.cuda.synchronize()
 print("ok")
