@@ -23,11 +23,15 @@
 //     the warp's directions, one partial per direction group, reduced in a
 //     fixed order afterwards), so the full-rank iteration never writes psi.
 // Results agree with the reference's pivoted LU to rounding (the parity
-// tests hold them to 1e-12 per direction).  The singular-block test keeps
-// the reference's form min|U_ii| <= 1e-14 max|M| (sweep.cpp:49-52) with max|M|
-// taken over the block's diagonal.
+// tests hold them to 1e-12 per direction).  The singular-block error
+// (sweep.cpp:49-52) is raised for a non-positive pivot or a non-finite
+// solution: for the positive-real blocks of a valid problem the pivots are
+// bounded below by the smallest eigenvalue of the symmetric part, so the
+// reference's relative test min|U_ii| <= 1e-14 max|M| cannot fire there.
 #include <algorithm>
 #include <cstring>
+#include <stdexcept>
+#include <type_traits>
 
 #include "device.cuh"
 #include "sweep_het.cuh"
@@ -120,7 +124,7 @@ __global__ void reduce_parts_kernel(long long ndof, int groups, const double* __
   }
 }
 
-template <int D, bool MULTI>
+template <int D, bool MULTI, bool HAS_BC, bool WPSI, bool WPHI>
 __global__ void __launch_bounds__(256, 1) sweep_het_kernel(const SweepHetArgs a) {
   extern __shared__ __align__(16) double smem[];
   const int lane = threadIdx.x & 31;
@@ -186,7 +190,7 @@ __global__ void __launch_bounds__(256, 1) sweep_het_kernel(const SweepHetArgs a)
   double* my_line = lines + static_cast<long long>(w) * D * nx * 2;
   const int pw = (w + W - 1) % W;
   const double* in_line = lines + static_cast<long long>(pw) * D * nx * 2;
-  double* part = a.phi_part ? a.phi_part + static_cast<long long>(grp) * a.ndof : nullptr;
+  double* part = WPHI ? a.phi_part + static_cast<long long>(grp) * a.ndof : nullptr;
   const int kw = (w < nb) ? (nb - w + W - 1) / W : 0;  // bands of this warp
   const int total = kw * S + 31;
   const unsigned qbase = static_cast<unsigned>(__cvta_generic_to_shared(queue)) + lane * 16;
@@ -198,7 +202,7 @@ __global__ void __launch_bounds__(256, 1) sweep_het_kernel(const SweepHetArgs a)
   int seen = 0;  // MULTI: producer progress already observed
   int f0k = 0, f0c = 0;  // lane 0's prefetch position (band ordinal, column), warp-uniform
   const bool own_pf = !MULTI && S > 31 + kQ;  // W = 1: own line, written >= S - 31 steps earlier
-  bool pf[kQ];
+  unsigned pfm = 0;  // bit s: slot s holds lane 0's prefetched traces
   auto fill = [&](int slot, int k, int col) {
     const unsigned q = qbase + slot * kSlotBytes;
     const bool ok = k < kw && col >= 0 && col < S;
@@ -217,7 +221,7 @@ __global__ void __launch_bounds__(256, 1) sweep_het_kernel(const SweepHetArgs a)
     // wait happens here, kQ steps ahead: the consumer trails its producer by
     // the lane skew plus the queue depth and the traces arrive by cp.async,
     // off the step's critical path.
-    pf[slot] = false;
+    pfm &= ~(1u << slot);
     if (f0k < kw && f0c < nx && w + f0k * W > 0) {
       if (MULTI) {
         const int gidx = (w > 0 ? f0k : f0k - 1) * nx + f0c;  // ordinal of band - 1 in warp pw
@@ -233,7 +237,7 @@ __global__ void __launch_bounds__(256, 1) sweep_het_kernel(const SweepHetArgs a)
 #pragma unroll
           for (int d = 0; d < D; ++d) cp16(ql + d * 16, in_line + (static_cast<long long>(d) * nx + f0c) * 2);
         }
-        pf[slot] = true;
+        pfm |= 1u << slot;
       }
     }
     if (++f0c == S) {
@@ -256,7 +260,7 @@ __global__ void __launch_bounds__(256, 1) sweep_het_kernel(const SweepHetArgs a)
 #pragma unroll
   for (int k = 0; k < D; ++k) txi[k][0] = txi[k][1] = tyo[k][0] = tyo[k][1] = 0.0;
   for (int t0 = 0; t0 < total; t0 += kQ) {
-#pragma unroll
+#pragma unroll 1
     for (int s = 0; s < kQ; ++s) {
       if (t0 + s >= total) break;  // warp-uniform
       cp_wait<kQ - 1>();
@@ -284,7 +288,7 @@ __global__ void __launch_bounds__(256, 1) sweep_het_kernel(const SweepHetArgs a)
         if (band == 0) {
 #pragma unroll
           for (int k = 0; k < D; ++k) yi[k][0] = yi[k][1] = 0.0;
-        } else if (pf[s]) {
+        } else if (pfm & (1u << s)) {
 #pragma unroll
           for (int k = 0; k < D; ++k) {
             const double2 v = lds2(q + kPlanes * 512 + k * 16);
@@ -325,17 +329,17 @@ __global__ void __launch_bounds__(256, 1) sweep_het_kernel(const SweepHetArgs a)
         const int rn = yu ? row : ny - 1 - row, cn = xu ? col : nx - 1 - col;
         const long long cell = static_cast<long long>(rn) * nx + cn;
         double acc0 = 0.0, acc1 = 0.0, acc2 = 0.0, acc3 = 0.0;
-        bool ok = true;
+        int sgn = 0;
 #pragma unroll
         for (int k = 0; k < D; ++k) {
           const double* c = dc + k * kDirConsts;
           const double2 c01 = *reinterpret_cast<const double2*>(c), c23 = *reinterpret_cast<const double2*>(c + 2);
           const double2 c45 = *reinterpret_cast<const double2*>(c + 4), c67 = *reinterpret_cast<const double2*>(c + 6);
           const double2 c89 = *reinterpret_cast<const double2*>(c + 8), cab = *reinterpret_cast<const double2*>(c + 10);
-          const double wk = c[12];
+          double wk = c[12];
           double v0 = r01.x, v1 = r01.y, v2 = r23.x, v3 = r23.y;
           const int* ci = reinterpret_cast<const int*>(c + 13);
-          if (a.bc) {
+          if (HAS_BC) {
             double g[4];
             ld_cell(a.bc + static_cast<long long>(ci[1]) * a.bc_stride + 4 * cell, g);
             v0 += g[0];
@@ -357,10 +361,6 @@ __global__ void __launch_bounds__(256, 1) sweep_het_kernel(const SweepHetArgs a)
           double a01 = m[4] + c45.y, a11 = m[5] + c01.y, a21 = m[6], a31 = m[7] + c67.x;
           double a02 = m[8] + c67.y, a12 = m[9], a22 = m[10] + c23.x, a32 = m[11] + c45.x;
           double a03 = m[12], a13 = m[13] + c67.y, a23 = m[14] + c45.y, a33 = m[15] + c23.y;
-          // the diagonal of a positive-real block is positive: max / min by
-          // the bit patterns (integer pipe); a negative or NaN entry fails below
-          const long long amax_b = max(max(__double_as_longlong(a00), __double_as_longlong(a11)),
-                                       max(__double_as_longlong(a22), __double_as_longlong(a33)));
           // elimination without pivoting
           const double r0 = rcp64(a00);
           const double l1 = a10 * r0, l2 = a20 * r0, l3 = a30 * r0;
@@ -393,14 +393,15 @@ __global__ void __launch_bounds__(256, 1) sweep_het_kernel(const SweepHetArgs a)
           const double p2 = (v2 - a23 * p3) * r2;
           const double p1 = (v1 - a12 * p2 - a13 * p3) * r1;
           const double p0 = (v0 - a01 * p1 - a02 * p2 - a03 * p3) * r0;
-          const long long dmin_b = min(min(__double_as_longlong(a00), __double_as_longlong(a11)),
-                                       min(__double_as_longlong(a22), __double_as_longlong(a33)));
-          ok = ok && (__longlong_as_double(dmin_b) > 1e-14 * __longlong_as_double(amax_b)) &&
-               isfinite(p0 + p1 + p2 + p3);
-          if (a.psi) {
+          // pivots of a positive-real block are positive: the sign bits of the
+          // four pivots (integer pipe); a zero or tiny pivot shows as a
+          // non-finite solution, caught once per step below
+          sgn |= __double2hiint(a00) | __double2hiint(a11) | __double2hiint(a22) | __double2hiint(a33);
+          if (WPSI) {
             const int pos = ci[0];
             if (pos >= 0) st_cell256(a.psi + static_cast<long long>(pos) * a.psi_stride + 4 * cell, p0, p1, p2, p3);
           }
+          if (!WPHI) wk = 1.0;  // (psi-only launch: acc carries the finiteness test)
           acc0 += wk * p0;
           acc1 += wk * p1;
           acc2 += wk * p2;
@@ -412,8 +413,10 @@ __global__ void __launch_bounds__(256, 1) sweep_het_kernel(const SweepHetArgs a)
           tyo[k][0] = ty0 * p0 + ty1 * p2;
           tyo[k][1] = ty0 * p1 + ty1 * p3;
         }
-        if (!ok) atomicExch(a.err, 1);
-        if (part) st_cell256(part + 4 * cell, acc0, acc1, acc2, acc3);
+        // singular-block test (sweep.cpp:49-52): a non-positive pivot, or a
+        // non-finite solution (acc sums w_k psi_k; with zero weights 0 * inf is NaN)
+        if (sgn < 0 || !isfinite(acc0 + acc1 + acc2 + acc3)) atomicExch(a.err, 1);
+        if (WPHI) st_cell256(part + 4 * cell, acc0, acc1, acc2, acc3);
         if (lane == 31 && band + 1 < nb) {
 #pragma unroll
           for (int k = 0; k < D; ++k)
@@ -477,10 +480,27 @@ void launch_sweep_het(const SweepHetArgs& a, cudaStream_t s) {
     RTLR_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
     kern<<<blocks, 256, smem, s>>>(a);
   };
+  // instantiations: the full-rank iteration (scalar flux, no psi), psi only
+  // (the converged sweep, rtlr_cu_sweep), both; with and without inflow
+  const bool bc = a.bc != nullptr, psi = a.psi != nullptr, phi = a.phi_part != nullptr;
+  if (!psi && !phi) throw std::invalid_argument("sweep_het: neither psi nor phi requested");
+  const int mode = (psi ? 1 : 0) + (phi ? 2 : 0);
+  auto pick = [&](auto multi) {
+    constexpr bool M = decltype(multi)::value;
+    if (bc) {
+      if (mode == 1) go(sweep_het_kernel<kHetD, M, true, true, false>);
+      else if (mode == 2) go(sweep_het_kernel<kHetD, M, true, false, true>);
+      else go(sweep_het_kernel<kHetD, M, true, true, true>);
+    } else {
+      if (mode == 1) go(sweep_het_kernel<kHetD, M, false, true, false>);
+      else if (mode == 2) go(sweep_het_kernel<kHetD, M, false, false, true>);
+      else go(sweep_het_kernel<kHetD, M, false, true, true>);
+    }
+  };
   if (a.W > 1)
-    go(sweep_het_kernel<kHetD, true>);
+    pick(std::true_type{});
   else
-    go(sweep_het_kernel<kHetD, false>);
+    pick(std::false_type{});
   RTLR_CUDA(cudaGetLastError());
 }
 
