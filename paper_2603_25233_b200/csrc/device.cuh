@@ -42,8 +42,8 @@ void launch_stream_apply(const StencilArgs& a, double omx, double omy, const dou
                          cudaStream_t s);
 // norms[k] = || rhs (+ bc_k) - A_k y_k ||_2 for a batch of m angles, y_k =
 // Y + k*ldy.  Deterministic: fixed per-angle reduction tree independent of
-// the batch position.  work >= m * kResidParts doubles.
-constexpr int kResidParts = 64;
+// the batch position.  work >= m * residual_parts(ncell) doubles.
+int residual_parts(int ncell);
 void launch_residual_norms(const StencilArgs& a, int m, const int* d_angles, const double* d_dirs,
                            const double* Y, long long ldy, const double* rhs, const double* bc,
                            long long bc_stride, double* work, double* norms, cudaStream_t s);

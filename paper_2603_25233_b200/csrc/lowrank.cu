@@ -944,7 +944,7 @@ std::vector<double> LowRankEngine::residual_norms(const std::vector<int>& angles
     gemm_nn(n_, nb, rank_, X_.col(0), X_.ld, coeffs + static_cast<long long>(i0) * ldc, ldc, Y, n_, s_);
     int* d_ang = upload_ints(ang_, sub);
     launch_residual_norms(sa_, nb, d_ang, dirs_, Y, n_, rhs_core_.get(), hp_.bc_any ? P_.bc_.get() : nullptr, n_,
-                          work(static_cast<size_t>(block) * kResidParts), nr_all + i0, s_);
+                          work(static_cast<size_t>(block) * residual_parts(hp_.ncell)), nr_all + i0, s_);
   }
   P_.allgather_inplace(nr_all, sb.bsz);
   RTLR_CUDA(cudaMemcpyAsync(out.data(), nr_all, m * sizeof(double), cudaMemcpyDeviceToHost, s_));
@@ -1122,6 +1122,8 @@ InnerResult LowRankEngine::inner(const double* d_phi_prev, SubsampleRng& rng) {
         gather_cols<<<g1(static_cast<long long>(rank_) * unsampled.size()), 256, 0, s_>>>(
             rank_, static_cast<int>(unsampled.size()), du, C_.get(), rank_, Cu, rank_);
         pt_.start("verify");
+        ++verify_calls_;
+        verify_angles_ += static_cast<long long>(unsampled.size());
         std::vector<double> vn = residual_norms(unsampled, Cu, rank_, /*mirror_equal=*/true);
         pt_.stop();
         std::vector<std::pair<double, int>> outstanding;
@@ -1335,9 +1337,9 @@ SolveReport Problem::solve_low_rank(const LowRankOptions& o) {
     for (auto& e : eng.pt_.acc) std::fprintf(stderr, " %s=%.4f", e.first.c_str(), e.second);
     std::fprintf(stderr,
                  " | reorth: %d rebuilds, %.4f s (inside cgs) | cgs: block %.4f (GEMMs %.4f), per-snapshot %.4f | svd: %d calls, "
-                 "%d Jacobi sweeps | galerkin: %lld batches, %lld systems\n",
+                 "%d Jacobi sweeps | galerkin: %lld batches, %lld systems | verify: %lld passes, %lld angles\n",
                  eng.reorth_count_, eng.reorth_seconds_, eng.cgs_split_[0], eng.cgs_split_[3], eng.cgs_split_[1], eng.svd_calls_,
-                 eng.svd_sweeps_, eng.gal_calls_, eng.gal_systems_);
+                 eng.svd_sweeps_, eng.gal_calls_, eng.gal_systems_, eng.verify_calls_, eng.verify_angles_);
   }
   rep.phi.resize(n);
   RTLR_CUDA(cudaMemcpyAsync(rep.phi.data(), phi, n * sizeof(double), cudaMemcpyDeviceToHost, stream_));

@@ -144,6 +144,7 @@ class LowRankEngine {
   int reorth_count_ = 0;        // Householder rebuilds (all inner loops)
   int svd_sweeps_ = 0, svd_calls_ = 0;
   long long gal_calls_ = 0, gal_systems_ = 0;
+  long long verify_calls_ = 0, verify_angles_ = 0;
   double reorth_seconds_ = 0.0;  // their wall time (meaningful with RTLR_PROFILE=1)
   double cgs_split_[4] = {0, 0, 0, 0};  // RTLR_PROFILE: block GEMMs + host / per-snapshot loop / overlap / GEMMs only
   void lap(int slot, std::chrono::steady_clock::time_point& t) {

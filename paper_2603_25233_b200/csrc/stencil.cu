@@ -6,6 +6,8 @@
 // Per DOF row the sum runs over the stored CSR entries in column order
 // (upwind neighbour block before or after the diagonal block, exact zeros
 // skipped) without FMA contraction, so apply() is bitwise the reference's.
+#include <algorithm>
+
 #include "device.cuh"
 
 namespace rtlr {
@@ -63,46 +65,135 @@ __global__ void stream_apply_kernel(const StencilArgs A, double omx, double omy,
   }
 }
 
-// grid = (kResidParts, m): block (p, k) sums squares of the residual of
-// angle k over the rows p, p + P*256, ... in a fixed pattern.
-__global__ void residual_partials(const StencilArgs A, const int* __restrict__ angles,
-                                  const double* __restrict__ dirs, const double* __restrict__ Y,
-                                  long long ldy, const double* __restrict__ rhs,
-                                  const double* __restrict__ bc, long long bc_stride,
-                                  double* __restrict__ work) {
-  __shared__ double sh[32];
-  const int k = blockIdx.y;
-  const int ang = angles ? angles[k] : k;
-  const double omx = dirs[3 * ang], omy = dirs[3 * ang + 1];
-  const double* y = Y + k * ldy;
-  const double* g = bc ? bc + ang * bc_stride : nullptr;
-  const int ndof = 4 * A.ncell;
-  double acc = 0.0;
-  for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < ndof; r += gridDim.x * blockDim.x) {
-    const int c = r >> 2;
-    double res = rhs[r] - apply_row(A, c % A.nx, c / A.nx, r & 3, omx, omy, y);
-    if (g) res += g[r];
-    acc += res * res;
+// Residual norms, one thread per cell and a group of RG angles per block row
+// (blockIdx.y): the cell's Sigma_t block and source are loaded once (two
+// 256-bit loads each... 16 + 4 doubles) and reused for the group's angles;
+// each angle's expanded solution y_k is read as 32-byte cells (the upwind
+// neighbours mostly from L1).  Row arithmetic is apply_row's (Sigma_t row,
+// then the streaming terms in the CSR column order, no FMA contraction).
+// Block (p, g) writes one partial per angle of the group; the per-angle sum
+// over partials runs in a fixed order, independent of the angle's position
+// in the batch, so equal columns give bitwise equal norms.
+constexpr int kResidGroup = 4;
+constexpr int kResidThreads = 256;
+
+__device__ __forceinline__ void ld4(const double* p, double v[4]) {
+  asm volatile("ld.global.nc.v4.f64 {%0, %1, %2, %3}, [%4];"
+               : "=d"(v[0]), "=d"(v[1]), "=d"(v[2]), "=d"(v[3])
+               : "l"(p));
+}
+
+// out[i] (+)= sum_j B[j*4+i] v[j] over the nonzeros of a streaming block
+__device__ __forceinline__ void blk_add(const double* B, const double v[4], double t[4]) {
+#pragma unroll
+  for (int i = 0; i < 4; ++i) t[i] = blk_row(B, i, v, t[i]);
+}
+
+__global__ void __launch_bounds__(kResidThreads) residual_cells(const StencilArgs A, int m, const int* __restrict__ angles,
+                                                                const double* __restrict__ dirs, const double* __restrict__ Y,
+                                                                long long ldy, const double* __restrict__ rhs,
+                                                                const double* __restrict__ bc, long long bc_stride,
+                                                                double* __restrict__ work) {
+  __shared__ double sh[kResidGroup][kResidThreads / 32];
+  const int c = blockIdx.x * kResidThreads + threadIdx.x;
+  const int k0 = blockIdx.y * kResidGroup;
+  double acc[kResidGroup];
+#pragma unroll
+  for (int j = 0; j < kResidGroup; ++j) acc[j] = 0.0;
+  if (c < A.ncell) {
+    const int a = c % A.nx, b = c / A.nx;
+    double S[16], r[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) ld4(A.sigma_t + 16 * static_cast<size_t>(c) + 4 * q, S + 4 * q);
+    ld4(rhs + 4 * static_cast<size_t>(c), r);
+    const size_t up = 4 * static_cast<size_t>(A.nx);
+#pragma unroll
+    for (int j = 0; j < kResidGroup; ++j) {
+      const int k = k0 + j;
+      if (k >= m) break;
+      const int ang = angles ? angles[k] : k;
+      const double omx = dirs[3 * ang], omy = dirs[3 * ang + 1];
+      const double* y = Y + k * ldy + 4 * static_cast<size_t>(c);
+      double v[4];
+      ld4(y, v);
+      double out[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) out[i] = blk_row(S, i, v, 0.0);
+      if (omx != 0.0) {
+        double t[4] = {0.0, 0.0, 0.0, 0.0}, w[4];
+        if (omx >= 0.0) {  // D_x^-: west neighbour columns precede the diagonal
+          if (a > 0) {
+            ld4(y - 4, w);
+            blk_add(A.sc.bx_minus, w, t);
+          }
+          blk_add(A.sc.ax_minus, v, t);
+        } else {  // D_x^+: diagonal, then east neighbour
+          blk_add(A.sc.ax_plus, v, t);
+          if (a + 1 < A.nx) {
+            ld4(y + 4, w);
+            blk_add(A.sc.bx_plus, w, t);
+          }
+        }
+#pragma unroll
+        for (int i = 0; i < 4; ++i) out[i] = __dadd_rn(out[i], __dmul_rn(omx, t[i]));
+      }
+      if (omy != 0.0) {
+        double t[4] = {0.0, 0.0, 0.0, 0.0}, w[4];
+        if (omy >= 0.0) {
+          if (b > 0) {
+            ld4(y - up, w);
+            blk_add(A.sc.by_minus, w, t);
+          }
+          blk_add(A.sc.ay_minus, v, t);
+        } else {
+          blk_add(A.sc.ay_plus, v, t);
+          if (b + 1 < A.ny) {
+            ld4(y + up, w);
+            blk_add(A.sc.by_plus, w, t);
+          }
+        }
+#pragma unroll
+        for (int i = 0; i < 4; ++i) out[i] = __dadd_rn(out[i], __dmul_rn(omy, t[i]));
+      }
+      double g[4] = {0.0, 0.0, 0.0, 0.0};
+      if (bc) ld4(bc + static_cast<long long>(ang) * bc_stride + 4 * static_cast<size_t>(c), g);
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        double res = __dsub_rn(r[i], out[i]);
+        if (bc) res = __dadd_rn(res, g[i]);
+        acc[j] = __fma_rn(res, res, acc[j]);
+      }
+    }
   }
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
 #pragma unroll
-  for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
-  if ((threadIdx.x & 31) == 0) sh[threadIdx.x >> 5] = acc;
+  for (int j = 0; j < kResidGroup; ++j) {
+    double v = acc[j];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    if (lane == 0) sh[j][wid] = v;
+  }
   __syncthreads();
-  if (threadIdx.x < 32) {
-    double s = threadIdx.x < (blockDim.x >> 5) ? sh[threadIdx.x] : 0.0;
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
-    if (threadIdx.x == 0) work[static_cast<size_t>(k) * gridDim.x + blockIdx.x] = s;
+  if (threadIdx.x < kResidGroup) {
+    const int k = k0 + threadIdx.x;
+    if (k < m) {
+      double s = 0.0;
+      for (int w = 0; w < kResidThreads / 32; ++w) s += sh[threadIdx.x][w];
+      work[static_cast<size_t>(k) * gridDim.x + blockIdx.x] = s;
+    }
   }
 }
 
 __global__ void residual_finish(int m, int parts, const double* __restrict__ work,
                                 double* __restrict__ norms) {
-  const int k = blockIdx.x * blockDim.x + threadIdx.x;
+  // one warp per angle: lanes stride the partials, fixed shuffle tree
+  const int k = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
   if (k >= m) return;
   double s = 0.0;
-  for (int p = 0; p < parts; ++p) s += work[static_cast<size_t>(k) * parts + p];
-  norms[k] = sqrt(s);
+  for (int p = lane; p < parts; p += 32) s += work[static_cast<size_t>(k) * parts + p];
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+  if (lane == 0) norms[k] = sqrt(s);
 }
 
 }  // namespace
@@ -120,16 +211,19 @@ void launch_residual_norms(const StencilArgs& a, int m, const int* d_angles, con
                            const double* Y, long long ldy, const double* rhs, const double* bc,
                            long long bc_stride, double* work, double* norms, cudaStream_t s) {
   if (m <= 0) return;
-  for (int k0 = 0; k0 < m; k0 += 65535) {
-    const int mk = (m - k0 < 65535) ? m - k0 : 65535;
-    residual_partials<<<dim3(kResidParts, mk), 256, 0, s>>>(
-        a, d_angles ? d_angles + k0 : nullptr, d_dirs, Y + k0 * ldy, ldy, rhs, bc, bc_stride,
-        work + static_cast<size_t>(k0) * kResidParts);
+  const int parts = residual_parts(a.ncell);
+  for (int k0 = 0; k0 < m; k0 += 65535 * kResidGroup) {
+    const int mk = std::min(m - k0, 65535 * kResidGroup);
+    residual_cells<<<dim3(parts, (mk + kResidGroup - 1) / kResidGroup), kResidThreads, 0, s>>>(
+        a, mk, d_angles ? d_angles + k0 : nullptr, d_dirs, Y + k0 * ldy, ldy, rhs, bc, bc_stride,
+        work + static_cast<size_t>(k0) * parts);
     RTLR_CUDA(cudaGetLastError());
   }
-  residual_finish<<<(m + 127) / 128, 128, 0, s>>>(m, kResidParts, work, norms);
+  residual_finish<<<(m * 32 + 255) / 256, 256, 0, s>>>(m, parts, work, norms);
   RTLR_CUDA(cudaGetLastError());
 }
+
+int residual_parts(int ncell) { return (ncell + kResidThreads - 1) / kResidThreads; }
 
 }  // namespace cuda
 }  // namespace rtlr
