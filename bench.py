@@ -53,6 +53,11 @@ def parse():
     ap.add_argument("--no-solvers", action="store_true", help="skip the solver time-to-tol leg")
     ap.add_argument("--solver-timeout", type=float, default=420.0, help="watchdog for the solver leg (s)")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--matrix", action="store_true",
+                    help="BASELINE config C5's whole matrix: grids 256^2..2048^2 x CL(32,8), CL(64,16), CL(128,32), "
+                         "direction batches streamed through device buffers where a point exceeds HBM; one line per point")
+    ap.add_argument("--matrix-budget-gb", type=float, default=64.0,
+                    help="device bytes for the streamed source / psi batch buffers")
     ap.add_argument("--no-cpu", action="store_true", help="skip the CPU baseline sample")
     ap.add_argument("--cpu-sample-updates", type=float, default=8e7,
                     help="CPU baseline sample size in cell-angle updates (~10 s of one core)")
@@ -315,6 +320,96 @@ def workload_config(args):
             "parallelism": f"direction partition x{args.gpus}"}
 
 
+C5_GRIDS = (256, 512, 1024, 2048)
+C5_QUADS = ((32, 8), (64, 16), (128, 32))  # CL(n_theta, n_omega_z): 256, 1024, 4096 directions (Appendix A)
+
+
+def run_matrix(args, P, rank, world, dist, local):
+    """C5 (BASELINE configs[4]): every grid x direction-count point, one JSON
+    line each.  A point's directions are this rank's partition_angles share;
+    they are swept in batches that fit --matrix-budget-gb (two buffers: the
+    batch's c5 sources, generated on the device per batch, and its psi), so
+    the three points larger than HBM (1024^2 x 4096, 2048^2 x 1024, 2048^2 x
+    4096: 0.27-1.1 TB of sources + psi) stream through the same memory.
+    `value` counts the sweep launches only (CUDA events around each); the
+    source generation is reported beside it."""
+    import numpy as np
+    import torch
+    peak, peak_kind = load_peaks()
+    for grid in C5_GRIDS:
+        for nt, nz in C5_QUADS:
+            prob = P.Problem("C5", device=local, nx=grid, ny=grid, n_theta=nt, n_omega_z=nz, use_dsa=0)
+            stream = torch.cuda.Stream()
+            torch.cuda.set_stream(stream)
+            prob.set_stream(stream.cuda_stream)
+            D_all, n = prob.n_omega, prob.n
+            cells = n // 4
+            mine = np.arange(D_all, dtype=np.int32) if world == 1 else \
+                P.partition_angles(nt, nz, world, rank).astype(np.int32)
+            D = len(mine)
+            B = int(max(1, min(D, args.matrix_budget_gb * 2**30 // (2 * n * 8))))
+            rhs = torch.empty(B * n, dtype=torch.float64, device="cuda")
+            psi = torch.empty(B * n, dtype=torch.float64, device="cuda")
+            angles = torch.from_numpy(mine).to("cuda")
+            contiguous = world == 1  # this rank's directions are 0..D-1
+
+            def fill(b0, nb):
+                if contiguous:
+                    prob.c5_fill(rhs.data_ptr(), nb, b0, SEED)
+                else:
+                    for k in range(nb):
+                        prob.c5_fill(rhs.data_ptr() + 8 * k * n, 1, int(mine[b0 + k]), SEED)
+
+            batches = [(b0, min(B, D - b0)) for b0 in range(0, D, B)]
+            fill(*batches[0])
+            for _ in range(max(1, args.warmup)):
+                prob.sweep_async(angles.data_ptr(), batches[0][1], rhs.data_ptr(), n, psi.data_ptr(), n)
+            prob.check()
+            if dist:
+                dist.barrier()
+            torch.cuda.synchronize()
+            steps = max(1, min(args.steps, 3)) if len(batches) == 1 else 1
+            ev = []
+            f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            f0.record(stream)
+            for _ in range(steps):
+                for b0, nb in batches:
+                    if len(batches) > 1:
+                        fill(b0, nb)
+                    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                    e0.record(stream)
+                    prob.sweep_async(angles.data_ptr() + 4 * b0, nb, rhs.data_ptr(), n, psi.data_ptr(), n)
+                    e1.record(stream)
+                    ev.append((e0, e1))
+            f1.record(stream)
+            torch.cuda.synchronize()
+            prob.check()
+            sweep_ms = sum(a.elapsed_time(b) for a, b in ev) / steps
+            wall_ms = f0.elapsed_time(f1) / steps
+            t = torch.tensor([sweep_ms, wall_ms], dtype=torch.float64, device="cuda")
+            if dist:
+                dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            sweep_ms, wall_ms = float(t[0]), float(t[1])
+            upd = D_all * cells
+            achieved = BYTES_PER_UPDATE * upd / (sweep_ms * 1e-3) / 1e9
+            if rank == 0:
+                print(json.dumps({
+                    "metric": "sweep cell-angle updates/s", "value": upd / (sweep_ms * 1e-3),
+                    "unit": "cell-angle updates/s", "n_gpus": world, "higher_is_better": True, "scaling": "strong",
+                    "dtype": "f64", "data": "synthetic",
+                    "config": {"workload": f"C5 sweep {grid}^2 cells x CL({nt},{nz}) = {D_all} directions",
+                               "grid": grid, "directions": D_all, "quadrature": f"CL({nt},{nz})",
+                               "parallelism": f"direction partition x{world}",
+                               "streamed": len(batches) > 1, "batch_directions": B, "batches": len(batches),
+                               "bytes_algorithmic": BYTES_PER_UPDATE * upd},
+                    "ms_sweeps": sweep_ms, "ms_with_source_generation": wall_ms,
+                    "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                                 "frac": achieved / peak, "peak_kind": peak_kind,
+                                 "bytes_per_update": BYTES_PER_UPDATE}}), flush=True)
+            del rhs, psi, prob
+            torch.cuda.empty_cache()
+
+
 def main():
     args = parse()
     maybe_spawn(args)
@@ -334,6 +429,11 @@ def main():
     if world > 1:
         import torch.distributed as dist
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    if args.matrix:
+        run_matrix(args, P, rank, world, dist, local)
+        if dist:
+            dist.destroy_process_group()
+        return
 
     prob = P.Problem("C5", device=local, nx=args.grid, ny=args.grid, n_theta=args.n_theta,
                      n_omega_z=args.n_omega_z, use_dsa=0)
