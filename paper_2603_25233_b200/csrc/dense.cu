@@ -875,9 +875,9 @@ __device__ __forceinline__ double col_mv(const double* B, int i, const double* v
 // columns, no 64-bit index division).  Per output the same row_mv / col_mv
 // arithmetic as before.
 __global__ void stream_products_kernel(const StencilArgs A, int p, const double* __restrict__ P, long long ldp,
-                                       double* __restrict__ W, long long ldw) {
-  const int c = blockIdx.x * blockDim.x + threadIdx.x;
-  if (c >= A.ncell) return;
+                                       double* __restrict__ W, long long ldw, int c0, int c1) {
+  const int c = c0 + blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= c1) return;
   const int j = blockIdx.y;
   const int a = c % A.nx, b = c / A.nx;
   const double* pc = P + j * ldp + 4LL * c;
@@ -2005,12 +2005,14 @@ void axpy_dev(long long n, const double* alpha, double sign, const double* x, do
 }
 
 void stream_products(const StencilArgs& a, int p, const double* P, long long ldp, double* W, long long ldw,
-                     cudaStream_t s) {
+                     cudaStream_t s, int c0, int c1) {
   if (p <= 0) return;
+  if (c1 < 0) c1 = a.ncell;
+  if (c1 <= c0) return;
   if ((ldp & 1) || (ldw & 1) || !aligned16(P) || !aligned16(W))
     throw std::invalid_argument("stream_products: P, W and their leading dimensions must be 16-byte aligned");
-  stream_products_kernel<<<dim3(static_cast<unsigned>((a.ncell + 255) / 256), static_cast<unsigned>(p)), 256, 0, s>>>(
-      a, p, P, ldp, W, ldw);
+  stream_products_kernel<<<dim3(static_cast<unsigned>((c1 - c0 + 255) / 256), static_cast<unsigned>(p)), 256, 0, s>>>(
+      a, p, P, ldp, W, ldw, c0, c1);
   RTLR_CUDA(cudaGetLastError());
 }
 

@@ -37,7 +37,7 @@ void axpy_dev(long long n, const double* alpha, double sign, const double* x, do
 // W = [Dx^- P, (Dx^-)^T P, Dy^- P, (Dy^-)^T P, Sigma_t P], each N_x x p,
 // written at W + k*p*ldw.
 void stream_products(const StencilArgs& a, int p, const double* P, long long ldp, double* W, long long ldw,
-                     cudaStream_t s);
+                     cudaStream_t s, int c0 = 0, int c1 = -1);  // cells [c0, c1) only (c1 < 0: all)
 
 // Batched Galerkin solves (low_rank.cpp:176-200): for each of m angles,
 // A_j = omx Px + omy Py + Pt (r x r, from the 5 projections with leading

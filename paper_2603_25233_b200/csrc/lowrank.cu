@@ -432,6 +432,31 @@ __global__ void __launch_bounds__(256, 2) cgs_batch_kernel(long long n, int p_in
   }
 }
 
+__global__ void add_2d_kernel(int M, int N, const double* __restrict__ T, long long ldt, double* __restrict__ C,
+                              long long ldc) {
+  const long long total = static_cast<long long>(M) * N;
+  for (long long e = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; e < total;
+       e += static_cast<long long>(gridDim.x) * blockDim.x) {
+    const int i = static_cast<int>(e % M), j = static_cast<int>(e / M);
+    C[i + j * ldc] += T[i + j * ldt];
+  }
+}
+
+// rows [r0, r0 + rows) of S (p columns, ld lds) <-> a packed rows x p block
+__global__ void pack_rows_kernel(long long rows, int p, const double* __restrict__ S, long long lds, double* __restrict__ B,
+                                 bool unpack, double* __restrict__ Sout) {
+  const long long total = rows * p;
+  for (long long e = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; e < total;
+       e += static_cast<long long>(gridDim.x) * blockDim.x) {
+    const long long i = e % rows;
+    const int j = static_cast<int>(e / rows);
+    if (unpack)
+      Sout[i + j * lds] = B[e];
+    else
+      B[e] = S[i + j * lds];
+  }
+}
+
 __global__ void or_flags_kernel(int m, const int* __restrict__ flags, int* __restrict__ bad) {
   int v = 0;
   for (int j = threadIdx.x; j < m; j += blockDim.x) v |= flags[j];
@@ -480,6 +505,77 @@ LowRankEngine::LowRankEngine(Problem& P, const LowRankParams& prm) : P_(P), prm_
   const char* e = std::getenv("RTLR_PROFILE");
   pt_.on = e && e[0] == '1';
   pt_.s = s_;
+  // row slices of the tall contractions
+  const char* rs = std::getenv("RTLR_LR_ROWSLICE");
+  const char* vs = std::getenv("RTLR_ROWSLICE_VIRTUAL");
+  if (P.sharded() && P.nranks() > 1 && !(rs && rs[0] == '0')) {
+    nslice_ = P.nranks();
+    my_slice_ = P.rank();
+  } else if (!P.sharded() && vs && std::atoi(vs) > 1) {
+    nslice_ = std::atoi(vs);
+    vslice_ = true;
+  }
+  slice_c_.resize(nslice_ + 1);
+  for (int k = 0; k <= nslice_; ++k)
+    slice_c_[k] = static_cast<int>(static_cast<long long>(k) * hp_.ncell / nslice_);
+}
+
+void LowRankEngine::tn_rows(int M, int N, const double* A, long long lda, const double* B, long long ldb, double* C,
+                            long long ldc) {
+  if (M <= 0 || N <= 0) return;
+  if (nslice_ == 1) {
+    tn(M, N, A, lda, B, ldb, C, ldc);
+    return;
+  }
+  double* T = tpart_.ensure(static_cast<size_t>(M) * N);
+  auto part = [&](int k, double* out, long long ldo) {
+    const long long r0 = slice_row(k), rows = slice_row(k + 1) - r0;
+    double* w = work(gemm_tn_work(M, N, rows));
+    gemm_tn(M, N, rows, A + r0, lda, B + r0, ldb, out, ldo, w, work_.size(), s_);
+  };
+  if (!vslice_) {
+    part(my_slice_, T, M);
+    P_.allreduce_sum(T, static_cast<size_t>(M) * N);
+    RTLR_CUDA(cudaMemcpy2DAsync(C, ldc * sizeof(double), T, M * sizeof(double), M * sizeof(double), N,
+                                cudaMemcpyDeviceToDevice, s_));
+    return;
+  }
+  part(0, C, ldc);
+  for (int k = 1; k < nslice_; ++k) {
+    part(k, T, M);
+    add_2d_kernel<<<g1(static_cast<long long>(M) * N), 256, 0, s_>>>(M, N, T, M, C, ldc);
+  }
+  RTLR_CUDA(cudaGetLastError());
+}
+
+void LowRankEngine::nn_rows_sub(int p, int r, const double* Xm, long long ldx, const double* Cc, long long ldc,
+                                double* S, long long lds, bool share) {
+  if (nslice_ == 1) {
+    gemm_nn(n_, p, r, Xm, ldx, Cc, ldc, S, lds, s_, /*subtract=*/true);
+    return;
+  }
+  const int first = vslice_ ? 0 : my_slice_, last = vslice_ ? nslice_ : my_slice_ + 1;
+  for (int k = first; k < last; ++k) {
+    const long long r0 = slice_row(k), rows = slice_row(k + 1) - r0;
+    gemm_nn(rows, p, r, Xm + r0, ldx, Cc, ldc, S + r0, lds, s_, /*subtract=*/true);
+  }
+  if (!share) return;
+  // every slice's rows to every rank: pack, all-gather, unpack
+  long long maxrows = 0;
+  for (int k = 0; k < nslice_; ++k) maxrows = std::max(maxrows, slice_row(k + 1) - slice_row(k));
+  const size_t chunk = static_cast<size_t>(maxrows) * p;
+  double* G = gath_.ensure(chunk * nslice_);
+  for (int k = first; k < last; ++k) {
+    const long long r0 = slice_row(k), rows = slice_row(k + 1) - r0;
+    pack_rows_kernel<<<g1(rows * p), 256, 0, s_>>>(rows, p, S + r0, lds, G + k * chunk, false, nullptr);
+  }
+  if (!vslice_) P_.allgather_inplace(G, chunk);
+  for (int k = 0; k < nslice_; ++k) {
+    if (!vslice_ && k == my_slice_) continue;
+    const long long r0 = slice_row(k), rows = slice_row(k + 1) - r0;
+    pack_rows_kernel<<<g1(rows * p), 256, 0, s_>>>(rows, p, nullptr, lds, G + k * chunk, true, S + r0);
+  }
+  RTLR_CUDA(cudaGetLastError());
 }
 
 LowRankEngine::~LowRankEngine() {
@@ -617,10 +713,12 @@ bool LowRankEngine::mgs_ro_update(const double* snaps, const std::vector<int>& a
     // (the second pass is unconditional: with the reference's test
     // |rem| < 0.5 |psi| some snapshot of the batch needs it in 97-100% of
     // the batches at C2-C4, and the test itself cost more than it saved)
-    tn(r_old, p_in, X_.col(0), X_.ld, snaps, n_, C1, r_old);
-    gemm_nn(n_, p_in, r_old, X_.col(0), X_.ld, C1, r_old, Rm, n_, s_, /*subtract=*/true);
-    tn(r_old, p_in, X_.col(0), X_.ld, Rm, n_, C2, r_old);
-    gemm_nn(n_, p_in, r_old, X_.col(0), X_.ld, C2, r_old, Rm, n_, s_, /*subtract=*/true);
+    // (row-sliced over ranks: each rank projects and updates its rows, the
+    // r_old x p blocks are allreduced, the remainders' rows all-gathered once)
+    tn_rows(r_old, p_in, X_.col(0), X_.ld, snaps, n_, C1, r_old);
+    nn_rows_sub(p_in, r_old, X_.col(0), X_.ld, C1, r_old, Rm, n_, /*share=*/false);
+    tn_rows(r_old, p_in, X_.col(0), X_.ld, Rm, n_, C2, r_old);
+    nn_rows_sub(p_in, r_old, X_.col(0), X_.ld, C2, r_old, Rm, n_, /*share=*/true);
     lap(3, tg);
   }
   lap(0, tlap);
@@ -798,14 +896,19 @@ void LowRankEngine::update_projections(bool reorth) {
   for (int c0 = 0; c0 < pn; c0 += chunk) {
     const int pc = std::min(chunk, pn - c0);
     double* W = wbuf_.ensure(static_cast<size_t>(n_) * 5 * chunk);
-    stream_products(sa_, pc, X_.col(r0 + c0), X_.ld, W, n_, s_);
+    // (row-sliced over ranks: the stencil images of this rank's cells, X^T W
+    // over its rows, one allreduce of the rank x 5pc block)
+    if (nslice_ > 1 && !vslice_)
+      stream_products(sa_, pc, X_.col(r0 + c0), X_.ld, W, n_, s_, slice_c_[my_slice_], slice_c_[my_slice_ + 1]);
+    else
+      stream_products(sa_, pc, X_.col(r0 + c0), X_.ld, W, n_, s_);
     double* G = gbuf_.ensure(static_cast<size_t>(rank_) * 5 * chunk);
-    tn(rank_, 5 * pc, X_.col(0), X_.ld, W, n_, G, rank_);
+    tn_rows(rank_, 5 * pc, X_.col(0), X_.ld, W, n_, G, rank_);
     proj_border_kernel<<<g1(static_cast<long long>(rank_) * pc), 256, 0, s_>>>(r0, pn, c0, pc, G, rank_, proj_.get(),
                                                                              ldp_, ldp_ * ldp_, rank_);
     RTLR_CUDA(cudaGetLastError());
   }
-  tn(pn, 1, X_.col(r0), X_.ld, rhs_core_.get(), n_, prhs_.get() + r0, pn);
+  tn_rows(pn, 1, X_.col(r0), X_.ld, rhs_core_.get(), n_, prhs_.get() + r0, pn);
 }
 
 // galerkin_solve for a list of angles (low_rank.cpp:192-200), batched.

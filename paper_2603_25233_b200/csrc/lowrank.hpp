@@ -218,6 +218,20 @@ class LowRankEngine {
  private:
   void galerkin_solve(const std::vector<int>& angles, double* d_sol, long long ldsol);
   void grow(int rank_need, int snaps_need);
+  // Row slicing of the tall contractions: with a
+  // communicator each rank forms X^T B over its cell range and one
+  // allreduce sums the M x N block (the CGS projections and the border
+  // extension's X^T W); S -= X C runs on the rank's rows and the rows are
+  // all-gathered.  RTLR_ROWSLICE_VIRTUAL=R on one GPU runs the same slices
+  // one after another and sums them in slice order (the slicing arithmetic
+  // without the collective, for tests).
+  void tn_rows(int M, int N, const double* A, long long lda, const double* B, long long ldb, double* C, long long ldc);
+  void nn_rows_sub(int p, int r, const double* Xm, long long ldx, const double* Cc, long long ldc, double* S,
+                   long long lds, bool share);
+  long long slice_row(int k) const { return 4LL * slice_c_[k]; }
+  int nslice_ = 1, my_slice_ = 0;
+  bool vslice_ = false;
+  std::vector<int> slice_c_;
   double host_dot(const double* a, const double* b, long long n);
   int* upload_ints(DBuf<int>& buf, const std::vector<int>& a);
   void flags_enqueue();
@@ -250,6 +264,7 @@ class LowRankEngine {
   DBuf<double> proj_, prhs_, rhs_core_, phi_, phi_old_, rem_, vec_, C_, work_, snaps_, wbuf_, gbuf_, sol_, cand_,
       ybuf_, nrm_, qa_, qq_, qr_, tau_, hrec_, luw_, gsol_, cgs_, svq_, svr_, svm_, rcoef_;
   DBuf<int> ang_, ang2_, flags_, pos_, rfrom_;
+  DBuf<double> tpart_, gath_;
   double* hbuf_ = nullptr;
   void* hstate_ = nullptr;  // pinned CgsState read back once per CGS batch
   int* hflags_ = nullptr;   // pinned: [0] Galerkin non-finite, [1] sweep singular block

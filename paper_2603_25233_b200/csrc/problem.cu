@@ -265,6 +265,11 @@ void Problem::allgather_inplace(double* buf, size_t count_per_rank) {
                           static_cast<ncclComm_t>(comm_), stream_));
 }
 
+void Problem::allreduce_sum(double* d_buf, size_t n) {
+  if (!comm_ || n == 0) return;
+  RTLR_NCCL(ncclAllReduce(d_buf, d_buf, n, ncclDouble, ncclSum, static_cast<ncclComm_t>(comm_), stream_));
+}
+
 void Problem::allreduce_max(int* d_buf, int n) {
   if (!comm_ || n <= 0) return;
   RTLR_NCCL(ncclAllReduce(d_buf, d_buf, n, ncclInt, ncclMax, static_cast<ncclComm_t>(comm_), stream_));

@@ -171,6 +171,7 @@ class Problem {
   // Collectives on the problem stream (no-ops without a communicator):
   // in-place all-gather of count_per_rank doubles per rank; max over ranks.
   void allgather_inplace(double* buf, size_t count_per_rank);
+  void allreduce_sum(double* d_buf, size_t n);
   void allreduce_max(int* d_buf, int n);
   // check_error() with the singular-block flag max-reduced over the ranks
   // first, so every rank throws together (no rank left in a collective).

@@ -195,3 +195,42 @@ def test_device_path_switches_keep_the_solve(switch, tmp_path):
         assert np.array_equal(out["1"], out["0"])
     else:
         assert rel(out["1"], out["0"]) <= 1e-8
+
+
+_ROWSLICE_SCRIPT = r"""
+import sys, numpy as np
+sys.path.insert(0, sys.argv[1])
+import paper_2603_25233_b200 as P
+p = P.Problem(sys.argv[2], seed=7, **eval(sys.argv[3]))
+r = p.solve_low_rank()
+np.save(sys.argv[4], np.concatenate([[r.iterations, r.history("rank")[-1]], r.phi]))
+"""
+
+
+@pytest.mark.parametrize("name,ov", [("pin_cell", {"nx": 24, "ny": 24}), ("C4", {"nx": 48, "ny": 40, "n_theta": 16,
+                                                                                "n_omega_z": 8, "p": 4, "q": 8})])
+def test_row_sliced_contractions_match_the_unsliced_solve(name, ov, tmp_path):
+    """The multi-GPU row slicing of the tall contractions (CGS projections,
+    border extension X^T W, the remainder update with its row all-gather;
+    SURVEY.md §8(e)) run as 3 virtual slices on one GPU
+    (RTLR_ROWSLICE_VIRTUAL=3: every slice's partial product and the
+    pack / unpack of the gathered rows, summed in slice order): the low-rank
+    solve agrees with the unsliced one (rounding of the split sums only) and
+    with the oracle."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    out = {}
+    for tag, env in (("plain", {}), ("sliced", {"RTLR_ROWSLICE_VIRTUAL": "3"})):
+        f = str(tmp_path / f"{tag}.npy")
+        e = dict(os.environ, **env)
+        subprocess.run([sys.executable, "-c", _ROWSLICE_SCRIPT, root, name, repr(ov), f], check=True, env=e,
+                       timeout=600)
+        out[tag] = np.load(f)
+    a, b = out["plain"], out["sliced"]
+    assert a[0] == b[0] and abs(a[1] - b[1]) <= 2  # iterations, final rank
+    assert rel(b[2:], a[2:]) <= 1e-10, rel(b[2:], a[2:])
+    o = O.Problem(name, seed=7, **ov)
+    ref = o.solve("lowrank").get("phi", o.n)
+    assert rel(b[2:], ref) <= 1e-8
