@@ -2,6 +2,8 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdint>
+#include <cstdlib>
+#include <string>
 #include <stdexcept>
 #include <vector>
 
@@ -1380,6 +1382,46 @@ __device__ __forceinline__ void argmax_merge(double& best, int& bi, double ov, i
 
 constexpr int kPermInts = 1 + 4 * 32;  // count, then up to 2 kNbMax dst rows and 2 kNbMax src rows
 
+// The panel's row swaps as one permutation of at most 2 jb rows, so the
+// trailing columns apply them with independent loads (lu_trail): after
+// the swaps, row dst[k] holds what row src[k] held.  slot[] (rows ints of
+// shared memory) maps a panel row to its entry (O(1) lookups).
+__device__ void lu_panel_perm(int rows, int k0, int jb, const int* pv, int* slot, int* pm) {
+  __shared__ int rowp[2 * kNbMax], cont[2 * kNbMax];
+  const int tid = threadIdx.x;
+  for (int i = tid; i < rows; i += blockDim.x) slot[i] = -1;
+  __syncthreads();
+  if (tid == 0) {
+    int np = 0;
+    auto pos_of = [&](int row) {
+      int q = slot[row - k0];
+      if (q < 0) {
+        q = np++;
+        slot[row - k0] = q;
+        rowp[q] = row;
+        cont[q] = row;
+      }
+      return q;
+    };
+    for (int j = 0; j < jb; ++j) {
+      const int a = k0 + j, b = pv[k0 + j];
+      if (a == b) continue;
+      const int pa = pos_of(a), pb = pos_of(b);
+      const int t = cont[pa];
+      cont[pa] = cont[pb];
+      cont[pb] = t;
+    }
+    int cnt = 0;
+    for (int q = 0; q < np; ++q)
+      if (cont[q] != rowp[q]) {
+        pm[1 + cnt] = rowp[q];
+        pm[1 + 2 * kNbMax + cnt] = cont[q];
+        ++cnt;
+      }
+    pm[0] = cnt;
+  }
+}
+
 template <int NT>
 __global__ void __launch_bounds__(NT) lu_panel_smem(int r, int k0, int jb, double* __restrict__ M,
                                                     int* __restrict__ piv, int* __restrict__ perm) {
@@ -1481,44 +1523,165 @@ __global__ void __launch_bounds__(NT) lu_panel_smem(int r, int k0, int jb, doubl
     const int i = e % rows, c = e / rows;
     A[k0 + i + static_cast<size_t>(k0 + c) * r] = P[e];
   }
-  // The panel's row swaps as one permutation of at most 2 jb rows, so the
-  // trailing columns apply them with independent loads (lu_trail): after
-  // the swaps, row dst[k] holds what row src[k] held.  slot[] maps a panel
-  // row to its entry (shared memory after the panel, O(1) lookups).
-  int* slot = reinterpret_cast<int*>(P + static_cast<size_t>(rows) * jb);
-  __shared__ int rowp[2 * kNbMax], cont[2 * kNbMax];
-  for (int i = tid; i < rows; i += NT) slot[i] = -1;
-  __syncthreads();
-  if (tid == 0) {
-    int np = 0;
-    auto pos_of = [&](int row) {
-      int q = slot[row - k0];
-      if (q < 0) {
-        q = np++;
-        slot[row - k0] = q;
-        rowp[q] = row;
-        cont[q] = row;
-      }
-      return q;
-    };
-    for (int j = 0; j < jb; ++j) {
-      const int a = k0 + j, b = pv[k0 + j];
-      if (a == b) continue;
-      const int pa = pos_of(a), pb = pos_of(b);
-      const int t = cont[pa];
-      cont[pa] = cont[pb];
-      cont[pb] = t;
+  lu_panel_perm(rows, k0, jb, pv, reinterpret_cast<int*>(P + static_cast<size_t>(rows) * jb),
+                perm + static_cast<size_t>(blockIdx.x) * kPermInts);
+}
+
+// Register-resident panel for panels of up to 256 RPT rows (RPT <= 2; the greedy
+// candidates' 16-system batches are latency-bound on the panel: the shared-
+// memory panel above spends ~2 us per column on shared-memory traffic and
+// two barriers).  Thread t owns panel rows t, t + 256, ... and keeps each
+// row's active part (columns j..) in registers, shifted left one column per
+// step, so every register index is compile-time inside a small loop body
+// (a fully unrolled 32-column body stalls on instruction fetch).  Finished
+// entries (the L column of each step, the pivot row's U part) go to a
+// shared-memory copy of the panel, where row swaps of the L parts happen.
+// One barrier per column: before it every warp publishes its argmax
+// candidate for column j with that row's active part, and the owner of row
+// j publishes row j (double-buffered by column parity), so after it every
+// thread knows the pivot row.  The per-element operations (l = a / d,
+// a -= l u in column order) are those of the unblocked factorisation, as in
+// lu_panel_smem: bitwise the same factors.
+template <int RPT>
+__global__ void __launch_bounds__(256, 1) lu_panel_reg(int r, int k0, int jb, double* __restrict__ M,
+                                                       int* __restrict__ piv, int* __restrict__ perm) {
+  constexpr int NT = 256, NW = NT / 32;
+  extern __shared__ double P[];  // rows x kNbMax finished entries (ld rows), then rows ints
+  __shared__ __align__(16) double cand[2][NW][kNbMax];
+  __shared__ __align__(16) double rowj[2][kNbMax];
+  __shared__ double shv[2][NW];
+  __shared__ int shi[2][NW];
+  double* A = M + static_cast<size_t>(blockIdx.x) * r * (r + 1);
+  int* pv = piv + static_cast<size_t>(blockIdx.x) * r;
+  const int rows = r - k0, tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  // active parts; columns >= jb are zero and stay zero (the pivot row's are)
+  double a[RPT][kNbMax];
+#pragma unroll
+  for (int c = 0; c < kNbMax; ++c)
+#pragma unroll
+    for (int q = 0; q < RPT; ++q) {
+      const int i = tid + NT * q;
+      a[q][c] = (i < rows && c < jb) ? A[k0 + i + static_cast<size_t>(k0 + c) * r] : 0.0;
     }
-    int* pm = perm + static_cast<size_t>(blockIdx.x) * kPermInts;
-    int cnt = 0;
-    for (int q = 0; q < np; ++q)
-      if (cont[q] != rowp[q]) {
-        pm[1 + cnt] = rowp[q];
-        pm[1 + 2 * kNbMax + cnt] = cont[q];
-        ++cnt;
+  // column j (active index 0): argmax candidate over rows >= j with its active part, and row j
+  auto publish = [&](int j) {
+    const int buf = j & 1;
+    double best = -1.0;
+    int bi = rows, bq = -1;
+#pragma unroll
+    for (int q = 0; q < RPT; ++q) {
+      const int i = tid + NT * q;
+      if (i >= j && i < rows) {
+        const double v = fabs(a[q][0]);
+        if (v > best) {  // q ascending: rows ascending, first maximum kept
+          best = v;
+          bi = i;
+          bq = q;
+        }
       }
-    pm[0] = cnt;
+    }
+    double wb = best;
+    int wi = bi;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1)
+      argmax_merge(wb, wi, __shfl_xor_sync(0xffffffffu, wb, o), __shfl_xor_sync(0xffffffffu, wi, o));
+    if (lane == 0) {
+      shv[buf][wid] = wb;
+      shi[buf][wid] = wi;
+    }
+#pragma unroll
+    for (int q = 0; q < RPT; ++q) {
+      const int i = tid + NT * q;
+      if (bq == q && wi == bi) {
+        double2* dst = reinterpret_cast<double2*>(cand[buf][wid]);
+#pragma unroll
+        for (int c = 0; c < kNbMax; c += 2) dst[c / 2] = make_double2(a[q][c], a[q][c + 1]);
+      }
+      if (i == j) {
+        double2* dst = reinterpret_cast<double2*>(rowj[buf]);
+#pragma unroll
+        for (int c = 0; c < kNbMax; c += 2) dst[c / 2] = make_double2(a[q][c], a[q][c + 1]);
+      }
+    }
+  };
+  publish(0);
+  __syncthreads();
+#pragma unroll 1
+  for (int j = 0; j < jb; ++j) {
+    const int buf = j & 1;
+    double bv = shv[buf][0];
+    int bix = shi[buf][0], bw = 0;
+#pragma unroll
+    for (int w = 1; w < NW; ++w) {
+      const double ov = shv[buf][w];
+      const int oi = shi[buf][w];
+      if (ov > bv || (ov == bv && oi < bix)) {
+        bv = ov;
+        bix = oi;
+        bw = w;
+      }
+    }
+    const int p = bv > 0.0 ? bix : j;  // all-zero column: no swap (first zero pivot)
+    if (tid == 0) pv[k0 + j] = k0 + p;
+    const double2* U2 = reinterpret_cast<const double2*>(p == j ? rowj[buf] : cand[buf][bw]);
+    const double2* R2 = reinterpret_cast<const double2*>(rowj[buf]);
+#pragma unroll
+    for (int q = 0; q < RPT; ++q) {
+      const int i = tid + NT * q;
+      if (p != j && i == j) {  // row j <- row p
+#pragma unroll
+        for (int c = 0; c < kNbMax; c += 2) {
+          const double2 v = U2[c / 2];
+          a[q][c] = v.x;
+          a[q][c + 1] = v.y;
+        }
+      } else if (p != j && i == p) {  // row p <- row j, with the L parts swapped in P
+#pragma unroll
+        for (int c = 0; c < kNbMax; c += 2) {
+          const double2 v = R2[c / 2];
+          a[q][c] = v.x;
+          a[q][c + 1] = v.y;
+        }
+        for (int c = 0; c < j; ++c) {
+          const double t = P[j + c * rows];
+          P[j + c * rows] = P[p + c * rows];
+          P[p + c * rows] = t;
+        }
+      }
+      if (i == j)  // the pivot row's U part is final
+#pragma unroll
+        for (int c = 0; c < kNbMax; ++c)
+          if (c < jb - j) P[j + (j + c) * rows] = a[q][c];
+    }
+    const double d = U2[0].x;
+    // rank-1 update of the rows below j (column order), then shift left
+#pragma unroll
+    for (int q = 0; q < RPT; ++q) {
+      const int i = tid + NT * q;
+      if (i > j && i < rows) {
+        const double l = d != 0.0 ? a[q][0] / d : a[q][0];
+        P[i + j * rows] = l;
+#pragma unroll
+        for (int c = 2; c < kNbMax; c += 2) {
+          const double2 u = U2[c / 2];
+          a[q][c] -= l * u.x;
+          a[q][c + 1] -= l * u.y;
+        }
+        a[q][1] -= l * U2[0].y;
+      }
+#pragma unroll
+      for (int c = 0; c + 1 < kNbMax; ++c) a[q][c] = a[q][c + 1];
+      a[q][kNbMax - 1] = 0.0;
+    }
+    if (j + 1 < jb) publish(j + 1);
+    __syncthreads();
   }
+  for (int e = tid; e < rows * jb; e += NT) {
+    const int i = e % rows, c = e / rows;
+    A[k0 + i + static_cast<size_t>(k0 + c) * r] = P[e];
+  }
+  lu_panel_perm(rows, k0, jb, pv, reinterpret_cast<int*>(P + static_cast<size_t>(rows) * kNbMax),
+                perm + static_cast<size_t>(blockIdx.x) * kPermInts);
 }
 
 // For one 64-column tile of the trailing columns (k0+jb .. r, the last one
@@ -2035,10 +2198,29 @@ void galerkin_batch(int r, int m, const int* angles, const double* dirs, const d
     RTLR_CUDA(cudaFuncSetAttribute(lu_panel_smem<kPanelThreads>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                    kPanelSmemBytes));
     RTLR_CUDA(cudaFuncSetAttribute(lu_trail, cudaFuncAttributeMaxDynamicSharedMemorySize, kTrailSmem));
+    static const int reg_panel = [] {  // RTLR_LU_PANEL=smem: the shared-memory panel only
+      const char* e = std::getenv("RTLR_LU_PANEL");
+      if (e && std::string(e) == "smem") return 0;
+      const int bytes = 512 * static_cast<int>(kNbMax * sizeof(double) + sizeof(int));
+      RTLR_CUDA(cudaFuncSetAttribute(lu_panel_reg<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
+      RTLR_CUDA(cudaFuncSetAttribute(lu_panel_reg<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
+      return 1;
+    }();
     for (int k0 = 0; k0 < r;) {
       const int jb = lu_panel_width(r, k0);
-      lu_panel_smem<kPanelThreads><<<m, kPanelThreads, static_cast<size_t>(r - k0) * (jb * sizeof(double) + 4), s>>>(
-          r, k0, jb, M, piv, perm);
+      const int rows = r - k0;
+      const size_t slot_bytes = static_cast<size_t>(rows) * (kNbMax * sizeof(double) + sizeof(int));
+      // (small batches only: at one CTA per SM the register panel loses to
+      // the shared-memory one once the batch fills the GPU; 3 rows per
+      // thread spill)
+      const bool small = reg_panel && m <= 64 && jb == kNbMax;
+      if (small && rows <= 256)
+        lu_panel_reg<1><<<m, 256, slot_bytes, s>>>(r, k0, jb, M, piv, perm);
+      else if (small && rows <= 512)
+        lu_panel_reg<2><<<m, 256, slot_bytes, s>>>(r, k0, jb, M, piv, perm);
+      else
+        lu_panel_smem<kPanelThreads><<<m, kPanelThreads, static_cast<size_t>(rows) * (jb * sizeof(double) + 4), s>>>(
+            r, k0, jb, M, piv, perm);
       const int ntrail = r + 1 - (k0 + jb);
       if (ntrail > 0) lu_trail<<<dim3((ntrail + BN - 1) / BN, m), 256, kTrailSmem, s>>>(r, k0, jb, M, perm);
       k0 += jb;

@@ -105,6 +105,67 @@ __global__ void col_norms_kernel(long long m, int n, const double* __restrict__ 
   }
 }
 
+// The CGS batch's remainder copy Rm = S and the snapshots' norms in one
+// pass over S: grid (kSnapParts, columns), each CTA a contiguous row chunk
+// (fixed-order partials, 16-byte loads), then one warp per column sums the
+// partials in a fixed order.  (The column-per-CTA kernel above used only p
+// CTAs: 600 us per C4 batch for 64 MB.)
+constexpr int kSnapParts = 128;
+__global__ void __launch_bounds__(256) copy_norm_parts(long long m, const double* __restrict__ w, long long ldw,
+                                                       double* __restrict__ dst, long long ldd,
+                                                       double* __restrict__ part) {
+  __shared__ double sh[8];
+  const int j = blockIdx.y;
+  const long long pairs = m >> 1;
+  const long long per = (pairs + kSnapParts - 1) / kSnapParts;
+  const long long q0 = blockIdx.x * per, q1 = min(pairs, q0 + per);
+  const double* c = w + j * ldw;
+  double* d = dst ? dst + j * ldd : nullptr;
+  const bool vec = ((ldw | ldd) & 1) == 0 && (reinterpret_cast<uintptr_t>(w) & 15) == 0 &&
+                   (!dst || (reinterpret_cast<uintptr_t>(dst) & 15) == 0);
+  double s = 0.0;
+  for (long long q = q0 + threadIdx.x; q < q1; q += blockDim.x) {
+    double2 v;
+    if (vec) {
+      v = reinterpret_cast<const double2*>(c)[q];
+      if (d) reinterpret_cast<double2*>(d)[q] = v;
+    } else {
+      v.x = c[2 * q];
+      v.y = c[2 * q + 1];
+      if (d) {
+        d[2 * q] = v.x;
+        d[2 * q + 1] = v.y;
+      }
+    }
+    s += v.x * v.x;
+    s += v.y * v.y;
+  }
+  if (blockIdx.x == kSnapParts - 1 && (m & 1) && threadIdx.x == 0) {
+    const double v = c[m - 1];
+    if (d) d[m - 1] = v;
+    s += v * v;
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+  if ((threadIdx.x & 31) == 0) sh[threadIdx.x >> 5] = s;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double t = 0.0;
+    for (int k = 0; k < 8; ++k) t += sh[k];
+    part[static_cast<size_t>(j) * kSnapParts + blockIdx.x] = t;
+  }
+}
+
+__global__ void norm_parts_finish(int n, const double* __restrict__ part, double* __restrict__ out) {
+  const int j = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5), lane = threadIdx.x & 31;
+  if (j >= n) return;
+  double s = 0.0;
+  for (int k = lane; k < kSnapParts; k += 32) s += part[static_cast<size_t>(j) * kSnapParts + k];
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+  if (lane == 0) out[j] = sqrt(s);
+}
+
 __global__ void scale_val_kernel(long long n, const double* __restrict__ x, double h, double* __restrict__ y) {
   for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < n;
        i += static_cast<long long>(gridDim.x) * blockDim.x)
@@ -700,9 +761,13 @@ bool LowRankEngine::mgs_ro_update(const double* snaps, const std::vector<int>& a
   if (pt_.on) RTLR_CUDA(cudaStreamSynchronize(s_));
   auto tlap = std::chrono::steady_clock::now();
   double* Rm = rem_.ensure(static_cast<size_t>(n_) * p_in);
-  RTLR_CUDA(cudaMemcpyAsync(Rm, snaps, static_cast<size_t>(n_) * p_in * sizeof(double), cudaMemcpyDeviceToDevice, s_));
   double* nr = nrm_.ensure(std::max(p_in, 128));
-  col_norms_kernel<<<p_in, 256, 0, s_>>>(n_, p_in, snaps, n_, nr);
+  {
+    double* parts = npart_.ensure(static_cast<size_t>(kSnapParts) * p_in);
+    copy_norm_parts<<<dim3(kSnapParts, p_in), 256, 0, s_>>>(n_, snaps, n_, Rm, n_, parts);
+    norm_parts_finish<<<(p_in + 7) / 8, 256, 0, s_>>>(p_in, parts, nr);
+    RTLR_CUDA(cudaGetLastError());
+  }
   double *C1 = nullptr, *C2 = nullptr;
   if (r_old > 0) {
     C1 = gbuf_.ensure(static_cast<size_t>(2) * r_old * p_in);

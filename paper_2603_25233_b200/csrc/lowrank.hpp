@@ -264,7 +264,7 @@ class LowRankEngine {
   DBuf<double> proj_, prhs_, rhs_core_, phi_, phi_old_, rem_, vec_, C_, work_, snaps_, wbuf_, gbuf_, sol_, cand_,
       ybuf_, nrm_, qa_, qq_, qr_, tau_, hrec_, luw_, gsol_, cgs_, svq_, svr_, svm_, rcoef_;
   DBuf<int> ang_, ang2_, flags_, pos_, rfrom_;
-  DBuf<double> tpart_, gath_;
+  DBuf<double> tpart_, gath_, npart_;
   double* hbuf_ = nullptr;
   void* hstate_ = nullptr;  // pinned CgsState read back once per CGS batch
   int* hflags_ = nullptr;   // pinned: [0] Galerkin non-finite, [1] sweep singular block

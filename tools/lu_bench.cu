@@ -6,6 +6,7 @@
 //           -Xlinker -rpath=$PWD/paper_2603_25233_b200/lib
 // Run:    tools/lu_bench r m [reps]   (prints ms per batch, GFLOP/s, max residual)
 #include <cmath>
+#include <cstring>
 #include <cstdio>
 #include <cstdlib>
 #include <random>
@@ -90,7 +91,14 @@ int main(int argc, char** argv) {
     worst = std::max(worst, std::sqrt(num / den));
   }
   const double gf = m * (2.0 / 3.0) * r * static_cast<double>(r) * r * 1e-9;
-  std::printf("r %d m %d: %.3f ms per batch, %.1f GFLOP/s (2/3 r^3 per system), max rel residual %.2e\n", r, m, ms,
-              gf / (ms * 1e-3), worst);
+  // bit checksum of every solution (compares kernel variants bitwise)
+  unsigned long long h = 1469598103934665603ull;
+  for (double v : sol) {
+    unsigned long long b;
+    std::memcpy(&b, &v, 8);
+    h = (h ^ b) * 1099511628211ull;
+  }
+  std::printf("r %d m %d: %.3f ms per batch, %.1f GFLOP/s (2/3 r^3 per system), max rel residual %.2e, bits %016llx\n",
+              r, m, ms, gf / (ms * 1e-3), worst, h);
   return worst < 1e-10 ? 0 : 1;
 }
