@@ -90,17 +90,25 @@ int rtlr_cu_problem_create(const rtlr_cu_config* cfg, int device, rtlr_cu_proble
 void rtlr_cu_problem_destroy(rtlr_cu_problem* p);
 /* info: nx, ny, n_theta, n_omega_z, n_dofs, n_omega, n_unique_dirs, sigma_t_uniform */
 int rtlr_cu_problem_info(const rtlr_cu_problem* p, int64_t info[8]);
+/* DG degree K of the problem (DGSpace::degree, dg_space.hpp:38) and its DOFs
+ * per cell s = (K+1)^2 (dofs_per_cell, :43).  K != 1 (0, 2..4) problems run
+ * rtlr_cu_sweep / rtlr_cu_sweep_async / rtlr_cu_sweep_dirs / rtlr_cu_apply
+ * (sweep.cpp:10-57, operators.cpp:283-288 for any K; test_sweep.cpp:142-155);
+ * the solvers, rhs_core and the DSA are K = 1 and return INVALID_ARGUMENT. */
+int rtlr_cu_problem_degree(const rtlr_cu_problem* p, int* degree, int* dofs_per_cell);
 /* Host copies of the assembled inputs: "dirs" (N_Omega x 3), "weights",
  * "source", "sigma_t_blocks" / "sigma_s_blocks" / "sigma_a_blocks"
- * (ncell x 16, column-major blocks), "sip_bsr" (ncell x 5 x 16: self, west,
- * east, south, north), "stream_blocks" (ax-,ax+,ay-,ay+,bx-,bx+,by-,by+). */
+ * (ncell x s^2, column-major blocks), "sip_bsr" (ncell x 5 x 16: self, west,
+ * east, south, north; K = 1), "stream_blocks" (ax-,ax+,ay-,ay+,bx-,bx+,by-,by+,
+ * s x s each). */
 int rtlr_cu_problem_get(const rtlr_cu_problem* p, const char* what, double* out);
 /* Launch work on an external cudaStream_t (NULL: the problem's own stream). */
 int rtlr_cu_problem_set_stream(rtlr_cu_problem* p, void* cuda_stream);
 /* "pcg_rtol", "pcg_max_iters", "pcg_multigrid" (0: block-Jacobi PCG), "sweep_kernel"
  * (0 auto, 1 skewed wavefront, 2 row scan, 3 row scan on prefactored cell blocks,
  * 4 cluster wavefront for a few directions, 5 direction groups with a fused
- * scalar-flux epilogue: heterogeneous media, one shared right-hand side) */
+ * scalar-flux epilogue: heterogeneous media, one shared right-hand side,
+ * 6 the general-degree diagonal wavefront, any K) */
 int rtlr_cu_problem_set_option(rtlr_cu_problem* p, const char* key, double value);
 int rtlr_cu_synchronize(rtlr_cu_problem* p);
 

@@ -32,7 +32,7 @@ EXPORTS = [
     "rtlr_cu_last_error", "rtlr_cu_version", "rtlr_cu_device_count", "rtlr_cu_config_create",
     "rtlr_cu_config_set", "rtlr_cu_config_set_field", "rtlr_cu_config_destroy",
     "rtlr_cu_problem_create", "rtlr_cu_problem_destroy", "rtlr_cu_problem_info",
-    "rtlr_cu_problem_get", "rtlr_cu_problem_set_stream", "rtlr_cu_problem_set_option",
+    "rtlr_cu_problem_get", "rtlr_cu_problem_degree", "rtlr_cu_problem_set_stream", "rtlr_cu_problem_set_option",
     "rtlr_cu_synchronize", "rtlr_cu_sweep", "rtlr_cu_sweep_dirs", "rtlr_cu_apply",
     "rtlr_cu_rhs_core", "rtlr_cu_si_step", "rtlr_cu_dsa_solve", "rtlr_cu_dsa_correct",
     "rtlr_cu_c5_fill", "rtlr_cu_fr_options_default", "rtlr_cu_lr_options_default",
@@ -123,6 +123,7 @@ def load_library(path: str = LIB_PATH):
     L.rtlr_cu_problem_destroy.argtypes = [ctypes.c_void_p]
     L.rtlr_cu_problem_info.argtypes = [ctypes.c_void_p, _I64]
     L.rtlr_cu_problem_get.argtypes = [ctypes.c_void_p, ctypes.c_char_p, _D]
+    L.rtlr_cu_problem_degree.argtypes = [ctypes.c_void_p, ctypes.POINTER(ctypes.c_int), ctypes.POINTER(ctypes.c_int)]
     L.rtlr_cu_problem_set_stream.argtypes = [ctypes.c_void_p, ctypes.c_void_p]
     L.rtlr_cu_problem_set_option.argtypes = [ctypes.c_void_p, ctypes.c_char_p, ctypes.c_double]
     L.rtlr_cu_synchronize.argtypes = [ctypes.c_void_p]
@@ -384,19 +385,23 @@ class Problem:
         self.nx, self.ny, self.n_theta, self.n_omega_z, self.n, self.n_omega = (int(v) for v in info[:6])
         self.n_unique = int(info[6])
         self.sigma_t_uniform = bool(info[7])
-        self.ncell = self.n // 4
+        k, spc = ctypes.c_int(), ctypes.c_int()
+        _check(L.rtlr_cu_problem_degree(self.h, ctypes.byref(k), ctypes.byref(spc)))
+        self.degree, self.dofs_per_cell = k.value, spc.value  # DG degree K, (K+1)^2
+        self.ncell = self.n // self.dofs_per_cell
 
     # ---- inputs (host copies) ----
     def get(self, what: str) -> np.ndarray:
+        s = self.dofs_per_cell
         sizes = {"dirs": 3 * self.n_omega, "weights": self.n_omega, "source": self.n,
-                 "sigma_t_blocks": 16 * self.ncell, "sigma_s_blocks": 16 * self.ncell,
-                 "sigma_a_blocks": 16 * self.ncell, "sip_bsr": 80 * self.ncell, "stream_blocks": 128}
+                 "sigma_t_blocks": s * s * self.ncell, "sigma_s_blocks": s * s * self.ncell,
+                 "sigma_a_blocks": s * s * self.ncell, "sip_bsr": 80 * self.ncell, "stream_blocks": 8 * s * s}
         out = np.zeros(sizes[what])
         _check(load_library().rtlr_cu_problem_get(self.h, what.encode(), out.ctypes.data_as(_D)))
         if what == "dirs":
             return out.reshape(self.n_omega, 3)
         if what.endswith("_blocks") and what != "stream_blocks":
-            return out.reshape(self.ncell, 4, 4).transpose(0, 2, 1).copy()
+            return out.reshape(self.ncell, s, s).transpose(0, 2, 1).copy()
         if what == "sip_bsr":
             return out.reshape(self.ncell, 5, 4, 4).transpose(0, 1, 3, 2).copy()
         return out
@@ -588,6 +593,7 @@ def _problem_from_handle(cls, h):
     self.nx, self.ny, self.n_theta, self.n_omega_z, self.n, self.n_omega = (int(v) for v in info[:6])
     self.n_unique = int(info[6])
     self.sigma_t_uniform = bool(info[7])
+    self.degree, self.dofs_per_cell = 1, 4  # caller-assembled problems are K = 1
     self.ncell = self.n // 4
     return self
 

@@ -219,6 +219,14 @@ int rtlr_cu_problem_info(const rtlr_cu_problem* p, int64_t info[8]) {
   });
 }
 
+int rtlr_cu_problem_degree(const rtlr_cu_problem* p, int* degree, int* dofs_per_cell) {
+  return guard([&] {
+    need(p && degree && dofs_per_cell, "problem: null argument");
+    *degree = p->p->host().degree;
+    *dofs_per_cell = p->p->host().spc;
+  });
+}
+
 int rtlr_cu_problem_get(const rtlr_cu_problem* p, const char* what, double* out) {
   return guard([&] {
     need(p && what && out, "problem: null argument");
@@ -231,6 +239,7 @@ int rtlr_cu_problem_get(const rtlr_cu_problem* p, const char* what, double* out)
     else if (w == "sigma_s_blocks") put_vec(h.sigma_s, out);
     else if (w == "sigma_a_blocks") put_vec(h.sigma_a, out);
     else if (w == "sip_bsr") put_vec(h.sip, out);
+    else if (w == "stream_blocks" && h.degree != 1) put_vec(h.kblocks, out);
     else if (w == "stream_blocks") {
       const double* m[8] = {h.sc.ax_minus, h.sc.ax_plus, h.sc.ay_minus, h.sc.ay_plus,
                             h.sc.bx_minus, h.sc.bx_plus, h.sc.by_minus, h.sc.by_plus};
@@ -254,9 +263,10 @@ int rtlr_cu_problem_set_option(rtlr_cu_problem* p, const char* key, double v) {
     else if (k == "pcg_max_iters") p->p->pcg_max_iters = static_cast<int>(v);
     else if (k == "pcg_multigrid") p->p->pcg_multigrid = v != 0.0;
     else if (k == "sweep_kernel") {
-      need(v == 0.0 || v == 1.0 || v == 2.0 || v == 3.0 || v == 4.0 || v == 5.0,
+      need(v == 0.0 || v == 1.0 || v == 2.0 || v == 3.0 || v == 4.0 || v == 5.0 || v == 6.0,
            "sweep_kernel: 0 (auto), 1 (skewed wavefront), 2 (row scan), 3 (row scan, prefactored blocks), "
-           "4 (cluster wavefront), 5 (direction groups, heterogeneous media, shared right-hand side)");
+           "4 (cluster wavefront), 5 (direction groups, heterogeneous media, shared right-hand side), "
+           "6 (general-degree diagonal wavefront)");
       p->p->sweep_kernel = static_cast<int>(v);
     } else throw std::invalid_argument("unknown option '" + k + "'");
   });

@@ -532,8 +532,10 @@ void detect_uniform(HostProblem& hp) {  // every Sigma_t block bitwise identical
 void assemble(const ProblemConfig& cfg, HostProblem& hp) {
   const auto t0 = std::chrono::steady_clock::now();
   validate_config(cfg);
-  if (cfg.degree != 1)
-    throw std::invalid_argument("rtlr::cuda: only DG degree K = 1 is supported on the GPU path");
+  if (cfg.degree != 1) {  // sweep / streaming operator only (host_dgk.cpp)
+    assemble_general(cfg, hp);
+    return;
+  }
   hp.cfg = cfg;
   hp.nx = cfg.nx;
   hp.ny = cfg.ny;

@@ -5,8 +5,9 @@
 // expression by expression so the inputs are bitwise identical to what the
 // reference's solver sees (quadrature, cell indexing, cross-section blocks,
 // source projection, SIP-DG diffusion matrix); tests/ check this against
-// the oracle restatement.  DG degree K = 1 only (s = 4 DOFs per cell);
-// other degrees are rejected with std::invalid_argument.
+// the oracle restatement.  The solvers run DG degree K = 1 (s = 4 DOFs per
+// cell); K = 0 and 2..4 assemble for the sweep and the streaming operator
+// (host_dgk.cpp).
 #pragma once
 
 #include <cstdint>
@@ -82,7 +83,18 @@ struct HostProblem {
   std::vector<double> sip;  // ncell x 5 x 16
   bool sigma_t_uniform = false;  // every sigma_t block bitwise identical
   double assembly_seconds = 0.0;
+  // DG degree K and DOFs per cell s = (K+1)^2.  K != 1 (host_dgk.cpp): the
+  // sigma blocks are ncell x s^2 and kblocks holds the streaming blocks
+  // ax-, ax+, ay-, ay+, bx-, bx+, by-, by+ (s x s column-major each); only
+  // the sweep and the streaming operator run on such a problem.
+  int degree = 1, spc = 4;
+  std::vector<double> kblocks;
 };
+
+constexpr int kMaxDegree = 4;  // K <= 4 (s <= 25) on the GPU path
+// Assembly for DG degree K != 1 (operators.cpp:13-281 for any K).
+void assemble_general(const ProblemConfig& cfg, HostProblem& out);
+void boundary_vector_general(const HostProblem& hp, const Field& g, int angle, double* out);
 
 void assemble(const ProblemConfig& cfg, HostProblem& out);
 

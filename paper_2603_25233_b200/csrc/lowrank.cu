@@ -533,6 +533,7 @@ int g1(long long n) {
 }  // namespace
 
 LowRankEngine::LowRankEngine(Problem& P, const LowRankParams& prm) : P_(P), prm_(prm), hp_(P.hp_) {
+  P.require_k1("LowRankBasis");
   s_ = P.stream_;
   n_ = hp_.ndof;
   nomega_ = hp_.n_omega;
@@ -1447,6 +1448,7 @@ double Problem::psi_difference(const double* d_psi, const double* d_X, const dou
 
 // proj/src/low_rank.cpp:436-492
 SolveReport Problem::solve_low_rank(const LowRankOptions& o) {
+  require_k1("solve_low_rank");
   if (o.use_dsa && sip_.get() == nullptr)
     throw std::invalid_argument("solve_low_rank: DSA requested but no diffusion system");
   const size_t n = hp_.ndof;

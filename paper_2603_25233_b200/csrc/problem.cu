@@ -149,9 +149,28 @@ void Problem::set_stream(cudaStream_t s) {
   own_stream_ = false;
 }
 
+void Problem::require_k1(const char* what) const {
+  if (hp_.degree != 1)
+    throw std::invalid_argument(std::string(what) + ": DG degree K = " + std::to_string(hp_.degree) +
+                                " runs the sweep and the streaming operator only on the GPU path (the solvers, "
+                                "rhs_core and the DSA are K = 1)");
+}
+
 void Problem::upload() {
   const HostProblem& h = hp_;
   cudaStream_t s = stream_;
+  if (h.degree != 1) {  // general degree: sweep / apply inputs only
+    dirs_.upload(h.dirs.data(), h.dirs.size(), s);
+    weights_.upload(h.weights.data(), h.weights.size(), s);
+    sigma_t_.upload(h.sigma_t.data(), h.sigma_t.size(), s);
+    source_.upload(h.source.data(), h.source.size(), s);
+    kblocks_.upload(h.kblocks.data(), h.kblocks.size(), s);
+    if (h.bc_any) bc_.upload(h.bc.data(), h.bc.size(), s);
+    err_.ensure(1);
+    RTLR_CUDA(cudaMemsetAsync(err_.get(), 0, sizeof(int), s));
+    RTLR_CUDA(cudaStreamSynchronize(s));
+    return;
+  }
   std::memcpy(sc_.ax_minus, h.sc.ax_minus, sizeof sc_.ax_minus);
   std::memcpy(sc_.ax_plus, h.sc.ax_plus, sizeof sc_.ax_plus);
   std::memcpy(sc_.ay_minus, h.sc.ay_minus, sizeof sc_.ay_minus);
@@ -278,6 +297,32 @@ void Problem::allreduce_max(int* d_buf, int n) {
 void Problem::sweep(const int* d_angles, int n, const double* d_rhs, long long rhs_stride,
                     double* d_psi, long long psi_stride, bool use_bc, const double* d_dirs) {
   if (n <= 0) return;
+  if (hp_.degree != 1 || sweep_kernel == 6) {  // general-degree kernel (sweep_dgk.cu)
+    DgkSweepArgs g{};
+    g.nx = hp_.nx;
+    g.ny = hp_.ny;
+    g.n = n;
+    g.dirs = d_dirs ? d_dirs : dirs_.get();
+    g.angles = d_angles;
+    g.rhs = d_rhs;
+    g.rhs_stride = rhs_stride;
+    g.bc = (use_bc && hp_.bc_any && !d_dirs) ? bc_.get() : nullptr;
+    g.bc_stride = hp_.ndof;
+    g.psi = d_psi;
+    g.psi_stride = psi_stride;
+    g.sigma_t = sigma_t_.get();
+    if (hp_.degree == 1 && kblocks_.size() == 0) {  // K = 1 through the general kernel (cross-check)
+      const double* k1[8] = {hp_.sc.ax_minus, hp_.sc.ax_plus, hp_.sc.ay_minus, hp_.sc.ay_plus,
+                             hp_.sc.bx_minus, hp_.sc.bx_plus, hp_.sc.by_minus, hp_.sc.by_plus};
+      std::vector<double> kb(8 * 16);
+      for (int b = 0; b < 8; ++b) std::copy(k1[b], k1[b] + 16, kb.begin() + 16 * b);
+      kblocks_.upload(kb.data(), kb.size(), stream_);
+    }
+    g.blocks = kblocks_.get();
+    g.err = err_.get();
+    sweep_dgk(hp_.degree, g, stream_);
+    return;
+  }
   SweepArgs a{};
   a.nx = hp_.nx;
   a.ny = hp_.ny;
@@ -359,6 +404,7 @@ bool Problem::het_applies(int n) const {
 
 bool Problem::sweep_het(const std::vector<int>& angles, const std::vector<double>* weights, const double* d_rhs,
                         double* d_psi, long long psi_stride, double* d_phi, bool use_bc) {
+  if (hp_.degree != 1) return false;
   const int n = static_cast<int>(angles.size());
   if (!het_applies(n)) return false;
   const int nx = hp_.nx, ny = hp_.ny;
@@ -491,11 +537,16 @@ void Problem::sweep_host(const int* h_angles, int n, const double* h_rhs, long l
 }
 
 void Problem::apply(double omx, double omy, const double* d_v, double* d_out) {
+  if (hp_.degree != 1) {
+    apply_dgk(hp_.degree, hp_.nx, hp_.ny, sigma_t_.get(), kblocks_.get(), omx, omy, d_v, d_out, stream_);
+    return;
+  }
   StencilArgs a{hp_.nx, hp_.ny, hp_.ncell, sigma_t_.get(), sc_};
   launch_stream_apply(a, omx, omy, d_v, d_out, stream_);
 }
 
 void Problem::rhs_core(const double* d_phi, double* d_out) {
+  require_k1("rhs_core");
   sigma_apply(hp_.ndof, sigma_s_.get(), d_phi, nullptr, source_.get(), d_out, stream_);
 }
 
@@ -531,6 +582,7 @@ PcgArgs Problem::pcg_args(const double* b, double* x) {
 }
 
 int Problem::dsa_solve(const double* d_rhs, double* d_x) {
+  require_k1("dsa_solve");
   if (sip_.get() == nullptr) throw std::invalid_argument("dsa: problem assembled without a diffusion system");
   // the iteration runs on resident vectors (so its captured graph is reused
   // across calls); the solution is copied out
@@ -541,6 +593,7 @@ int Problem::dsa_solve(const double* d_rhs, double* d_x) {
 }
 
 int Problem::dsa_correct(const double* d_phi_star, const double* d_phi_prev, double* d_delta) {
+  require_k1("dsa_correct");
   // rhs = Sigma_s (phi* - phi_prev)  (diffusion.cpp:210-213)
   double* rhs = pcg_vec_.get() + 4 * static_cast<size_t>(hp_.ndof);
   sigma_apply(hp_.ndof, sigma_s_.get(), d_phi_star, d_phi_prev, nullptr, rhs, stream_);
@@ -548,6 +601,7 @@ int Problem::dsa_correct(const double* d_phi_star, const double* d_phi_prev, dou
 }
 
 void Problem::si_step(const double* d_phi_prev, double* d_phi_star, double* d_psi_or_null) {
+  require_k1("si_step");
   const size_t n = hp_.ndof;
   const int nu = static_cast<int>(uniq_rep_.size());
   double* rc = scratch_.ensure(n + n * static_cast<size_t>(nu));
@@ -567,6 +621,7 @@ void Problem::si_step(const double* d_phi_prev, double* d_phi_star, double* d_ps
 
 // proj/src/full_rank.cpp:60-122
 SolveReport Problem::solve_full_rank(const FullRankOptions& o) {
+  require_k1("solve_full_rank");
   if (o.use_dsa && sip_.get() == nullptr)
     throw std::invalid_argument("solve_full_rank: DSA requested but no diffusion system");
   const size_t n = hp_.ndof;

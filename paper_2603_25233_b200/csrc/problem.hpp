@@ -12,6 +12,7 @@
 #include "host.hpp"
 #include "linalg.cuh"
 #include "mg.cuh"
+#include "sweep_dgk.cuh"
 #include "sweep_het.cuh"
 
 namespace rtlr {
@@ -159,6 +160,10 @@ class Problem {
   double psi_difference(const double* d_psi, const double* d_X, const double* d_S, const double* d_V, int rank);
 
   void check_error();  // throws runtime_error("sweep: singular local block")
+  // DG degree K != 1 problems run the sweep and the streaming operator only;
+  // the K = 1 entry points throw invalid_argument naming `what`.
+  int degree() const { return hp_.degree; }
+  void require_k1(const char* what) const;
 
   // Direction sharding over ranks (one process per GPU): this rank sweeps
   // its share of the unique directions and the scalar-flux partials are
@@ -200,7 +205,7 @@ class Problem {
   cudaStream_t stream_ = nullptr;
   bool own_stream_ = true;
   StreamDev sc_{};
-  DBuf<double> dirs_, weights_, sigma_t_, sigma_s_, source_, bc_, sip_, jac_;
+  DBuf<double> dirs_, weights_, sigma_t_, sigma_s_, source_, bc_, sip_, jac_, kblocks_;
   DBuf<int> err_, angle_idx_;
   DBuf<double> line_, norm_work_, pcg_vec_, pcg_part_, uniq_w_, scratch_, hin_[3], hout_[3], pref_;
   DBuf<int> hang_;

@@ -90,9 +90,25 @@ def test_quadrature_bitwise_all_baseline_rules():
         assert p.n_unique == nt * nz // 2  # mirror pairs collapse
 
 
-def test_degree_other_than_one_rejected():
+@pytest.mark.parametrize("degree", [0, 2, 3, 4])
+@pytest.mark.parametrize("name,ov", [("pin_cell", {"nx": 9, "ny": 7}), ("C4", {"nx": 24, "ny": 20}),
+                                     ("homogeneous(1,1)", {"nx": 5, "ny": 6, "boundary_const": 0.5})])
+def test_general_degree_inputs_bitwise(name, ov, degree):
+    """K != 1 assembly (host_dgk.cpp): streaming blocks, (K+2)^2-point cross
+    sections and source projection bitwise equal to the oracle's general-K
+    restatement of operators.cpp."""
+    o = O.Problem(name, degree=degree, use_dsa=0, **ov)
+    p = P.Problem(name, device=-1, degree=degree, use_dsa=0, **ov)
+    assert (p.degree, p.dofs_per_cell, p.n) == (degree, (degree + 1) ** 2, o.n)
+    assert np.array_equal(p.get("source"), o.get("source"))
+    for blk in ("sigma_t_blocks", "sigma_s_blocks", "sigma_a_blocks"):
+        assert np.array_equal(p.get(blk), o.get(blk)), blk
+    assert np.array_equal(p.get("stream_blocks"), o.get("stream_blocks"))
+
+
+def test_degree_above_four_rejected():
     with pytest.raises(P.InvalidArgument, match="degree"):
-        P.Problem("homogeneous(1,1)", device=-1, degree=2)
+        P.Problem("homogeneous(1,1)", device=-1, degree=5)
 
 
 def test_config_errors_map_to_config_error():  # problem.cpp:95-107
