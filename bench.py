@@ -274,11 +274,50 @@ def solver_leg(P, local, rank, world, dist):
                  "sharding": "angles" if world > 1 else "none"}
         if method == "lowrank":
             entry["final_rank"] = int(rep.history("rank")[-1])
+            if world == 1:
+                entry["phases"] = lowrank_phases(sp)
         if world == 1 and (name, method) in CPU_REFERENCE_JOBS:
             entry["cpu_reference"] = cpu_solver_reference(name, method, rep)
         out[f"{name}_{method}"] = entry
         del sp
         torch.cuda.synchronize()
+    return out
+
+
+def load_fp64_peak():
+    """fp64 tensor-pipe (DMMA) peak measured on this pool's B200s by
+    tools/dmma_peak (register-only mma.sync.m8n8k4.f64 loop; cuBLAS DGEMM
+    8192^3 beside it), committed under profiles/round2/."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "round2", "dmma_peak.json")) as f:
+            d = json.load(f)
+        return float(d["dmma_loop_tflops"]), "measured (tools/dmma_peak)"
+    except Exception:
+        return 37.0, "fallback"
+
+
+def lowrank_phases(sp):
+    """One more low-rank solve with the phases timed (the problem option
+    profile_phases synchronises at each phase boundary, so this run is not the
+    time-to-tol one): per phase the wall seconds, the algorithmic HBM bytes
+    and flops the solver counted from each call's shapes (DESIGN.md,
+    per-phase roofline), the achieved GB/s and TFLOP/s and their fractions of
+    the measured HBM bandwidth and fp64 tensor (DMMA) peak."""
+    hbm, hbm_kind = load_peaks()
+    dmma, dmma_kind = load_fp64_peak()
+    sp.set_option("profile_phases", 1)
+    rep = sp.solve_low_rank(build_factors=0)
+    sp.set_option("profile_phases", 0)
+    out = {"peaks": {"hbm_gbs": hbm, "hbm_kind": hbm_kind, "fp64_tensor_tflops": dmma, "fp64_kind": dmma_kind},
+           "profiled_solve_s": float(rep.get("solve_seconds", 1)[0])}
+    for name, w in rep.phase_work().items():
+        t = w["seconds"] or 0.0
+        gbs = w["bytes"] / t / 1e9 if t > 0 else None
+        tfs = w["flops"] / t / 1e12 if t > 0 else None
+        out[name] = {"seconds": t, "calls": w["calls"], "GB": w["bytes"] / 1e9, "GFLOP": w["flops"] / 1e9,
+                     "GB_per_s": gbs, "TFLOP_per_s": tfs,
+                     "frac_hbm": gbs / hbm if gbs is not None else None,
+                     "frac_fp64_tensor": tfs / dmma if tfs is not None else None}
     return out
 
 

@@ -104,7 +104,8 @@ int rtlr_cu_problem_degree(const rtlr_cu_problem* p, int* degree, int* dofs_per_
 int rtlr_cu_problem_get(const rtlr_cu_problem* p, const char* what, double* out);
 /* Launch work on an external cudaStream_t (NULL: the problem's own stream). */
 int rtlr_cu_problem_set_stream(rtlr_cu_problem* p, void* cuda_stream);
-/* "pcg_rtol", "pcg_max_iters", "pcg_multigrid" (0: block-Jacobi PCG), "sweep_kernel"
+/* "pcg_rtol", "pcg_max_iters", "pcg_multigrid" (0: block-Jacobi PCG), "profile_phases"
+ * (1: time the low-rank phases, synchronising at their boundaries), "sweep_kernel"
  * (0 auto, 1 skewed wavefront, 2 row scan, 3 row scan on prefactored cell blocks,
  * 4 cluster wavefront for a few directions, 5 direction groups with a fused
  * scalar-flux epilogue: heterogeneous media, one shared right-hand side,
@@ -175,7 +176,11 @@ int rtlr_cu_solve_low_rank(rtlr_cu_problem* p, const rtlr_cu_lr_options* o, rtlr
 int rtlr_cu_report_info(const rtlr_cu_report* r, int64_t info[8]);
 /* "phi", "psi", "S", "X", "V", "solve_seconds", or a per-outer-iteration
  * history column: "diff_two_norm", "diff_inf_norm", "rank", "oversampling",
- * "inner_iterations", "sampled_count", "fullrank_fallback", "dsa_iterations". */
+ * "inner_iterations", "sampled_count", "fullrank_fallback", "dsa_iterations".
+ * Low-rank reports also carry "phase_work": 9 x 4 doubles (seconds, algorithmic
+ * HBM bytes, flops, calls) for the phases sweep, cgs, projections, galerkin_q,
+ * residual_q, build_C, verify, svd, dsa; seconds are -1 unless the problem
+ * option "profile_phases" (or RTLR_PROFILE=1) timed them. */
 int rtlr_cu_report_get(const rtlr_cu_report* r, const char* what, double* out);
 int rtlr_cu_report_sampled(const rtlr_cu_report* r, int* counts, int* flat);
 void rtlr_cu_report_destroy(rtlr_cu_report* r);

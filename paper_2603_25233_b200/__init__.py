@@ -297,6 +297,15 @@ class Report:
     def history(self, what: str) -> np.ndarray:
         return self.get(what, self.n_history)
 
+    PHASES = ("sweep", "cgs", "projections", "galerkin_q", "residual_q", "build_C", "verify", "svd", "dsa")
+
+    def phase_work(self) -> dict:
+        """Low-rank phases: {name: {"seconds" (None unless profile_phases),
+        "bytes" (algorithmic HBM bytes), "flops", "calls"}}."""
+        w = self.get("phase_work", 4 * len(self.PHASES)).reshape(-1, 4)
+        return {name: {"seconds": None if row[0] < 0 else float(row[0]), "bytes": float(row[1]),
+                       "flops": float(row[2]), "calls": int(row[3])} for name, row in zip(self.PHASES, w)}
+
     def sampled_log(self):
         counts = np.zeros(max(1, self.n_history), dtype=np.int32)
         flat = np.zeros(max(1, self._sampled_total), dtype=np.int32)

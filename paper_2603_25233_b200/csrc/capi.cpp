@@ -262,6 +262,7 @@ int rtlr_cu_problem_set_option(rtlr_cu_problem* p, const char* key, double v) {
     if (k == "pcg_rtol") p->p->pcg_rtol = v;
     else if (k == "pcg_max_iters") p->p->pcg_max_iters = static_cast<int>(v);
     else if (k == "pcg_multigrid") p->p->pcg_multigrid = v != 0.0;
+    else if (k == "profile_phases") p->p->profile_phases = v != 0.0;
     else if (k == "sweep_kernel") {
       need(v == 0.0 || v == 1.0 || v == 2.0 || v == 3.0 || v == 4.0 || v == 5.0 || v == 6.0,
            "sweep_kernel: 0 (auto), 1 (skewed wavefront), 2 (row scan), 3 (row scan, prefactored blocks), "
@@ -511,6 +512,10 @@ int rtlr_cu_report_get(const rtlr_cu_report* r, const char* what, double* out) {
     else if (w == "X") put_vec(s.factors.X, out);
     else if (w == "V") put_vec(s.factors.V, out);
     else if (w == "solve_seconds") out[0] = s.solve_seconds;
+    else if (w == "phase_work") {
+      need(!s.phase_work.empty(), "report_get: phase_work is a low-rank report field");
+      put_vec(s.phase_work, out);
+    }
     else
       for (size_t i = 0; i < s.history.size(); ++i) {
         const OuterRecord& h = s.history[i];

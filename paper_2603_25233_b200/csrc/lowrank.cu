@@ -565,7 +565,7 @@ LowRankEngine::LowRankEngine(Problem& P, const LowRankParams& prm) : P_(P), prm_
       static_cast<double>(n_) * rmax_ * sizeof(double) <= 0.25 * static_cast<double>(free_b))
     X_.reserve(n_, rmax_, s_);
   const char* e = std::getenv("RTLR_PROFILE");
-  pt_.on = e && e[0] == '1';
+  pt_.on = (e && e[0] == '1') || P.profile_phases;
   pt_.s = s_;
   // row slices of the tall contractions
   const char* rs = std::getenv("RTLR_LR_ROWSLICE");
@@ -768,6 +768,14 @@ bool LowRankEngine::mgs_ro_update(const double* snaps, const std::vector<int>& a
     copy_norm_parts<<<dim3(kSnapParts, p_in), 256, 0, s_>>>(n_, snaps, n_, Rm, n_, parts);
     norm_parts_finish<<<(p_in + 7) / 8, 256, 0, s_>>>(p_in, parts, nr);
     RTLR_CUDA(cudaGetLastError());
+    // the copy with norms, then the within-batch CGS: column i against the i
+    // accepted before it, twice, plus its norm and scaling
+    double wb = 3.0 * p_in, wf = 2.0 * p_in;
+    for (int i = 0; i < p_in; ++i) {
+      wb += 2.0 * (2 * i + 2);
+      wf += 8.0 * i + 4.0;
+    }
+    pt_.work(8.0 * n_ * wb, n_ * wf);
   }
   double *C1 = nullptr, *C2 = nullptr;
   if (r_old > 0) {
@@ -781,6 +789,8 @@ bool LowRankEngine::mgs_ro_update(const double* snaps, const std::vector<int>& a
     // the batches at C2-C4, and the test itself cost more than it saved)
     // (row-sliced over ranks: each rank projects and updates its rows, the
     // r_old x p blocks are allreduced, the remainders' rows all-gathered once)
+    // four passes over X_old (two projections, two updates) and the p columns
+    pt_.work(8.0 * (4.0 * n_ * r_old + 6.0 * n_ * p_in), 8.0 * n_ * r_old * p_in);
     tn_rows(r_old, p_in, X_.col(0), X_.ld, snaps, n_, C1, r_old);
     nn_rows_sub(p_in, r_old, X_.col(0), X_.ld, C1, r_old, Rm, n_, /*share=*/false);
     tn_rows(r_old, p_in, X_.col(0), X_.ld, Rm, n_, C2, r_old);
@@ -929,6 +939,11 @@ bool LowRankEngine::mgs_ro_update(const double* snaps, const std::vector<int>& a
     double* tau = tau_.ensure(r_new);
     double* qw = work(householder_qr_work(n_, r_new));
     householder_qr(n_, r_new, M, n_, tau, Q, n_, R, qw, work_.size(), s_);
+    {  // blocked Householder QR with Q formed: 4 m n^2 - 4/3 n^3 flops; per
+       // 32-column panel the trailing block is read and written (twice with Q)
+      const double rn = r_new, panels = std::ceil(rn / 32.0);
+      pt_.work(8.0 * n_ * rn * (2.0 + 2.0 * panels), 4.0 * n_ * rn * rn - 4.0 / 3.0 * rn * rn * rn);
+    }
     // batch columns: Q^T snapshots (low_rank.cpp:126-129)
     double* B = gbuf_.ensure(static_cast<size_t>(r_new) * p_in);
     tn(r_new, p_in, Q, n_, snaps, n_, B, r_new);
@@ -969,6 +984,10 @@ void LowRankEngine::update_projections(bool reorth) {
     else
       stream_products(sa_, pc, X_.col(r0 + c0), X_.ld, W, n_, s_);
     double* G = gbuf_.ensure(static_cast<size_t>(rank_) * 5 * chunk);
+    // stencil images (read pc columns with their neighbours, write 5 pc) and
+    // X^T W (read X and W): 2 n r 5pc flops on the DMMA tiles
+    pt_.work(8.0 * (static_cast<double>(n_) * pc * 11.0 + static_cast<double>(n_) * rank_),
+             2.0 * n_ * rank_ * 5.0 * pc + 40.0 * n_ * pc);
     tn_rows(rank_, 5 * pc, X_.col(0), X_.ld, W, n_, G, rank_);
     proj_border_kernel<<<g1(static_cast<long long>(rank_) * pc), 256, 0, s_>>>(r0, pn, c0, pc, G, rank_, proj_.get(),
                                                                              ldp_, ldp_ * ldp_, rank_);
@@ -1052,6 +1071,11 @@ void LowRankEngine::galerkin_solve(const std::vector<int>& angles, double* d_sol
       extra = out;
     }
     int* flags = flags_.ensure(mc);
+    {  // assembly + partial-pivot LU + two triangular solves per system: the
+       // r x (r+1) matrices are written once and factored in place
+      const double r = rank_;
+      pt_.work(8.0 * mc * r * (r + 1) * 2.0, mc * (2.0 / 3.0 * r * r * r + 2.0 * r * r + 5.0 * r * r));
+    }
     double* lw = rank_ > kSmemLuMax ? luw_.ensure(galerkin_work_doubles(rank_, mc)) : nullptr;
     galerkin_batch(rank_, mc, d_ang, dirs_, proj_.get(), ldp_, ldp_ * ldp_, prhs_.get(), extra, out, ldsol, flags, lw,
                    s_);
@@ -1110,6 +1134,10 @@ std::vector<double> LowRankEngine::residual_norms(const std::vector<int>& angles
     const int nb = std::min(block, sb.end - i0);
     std::vector<int> sub(angles.begin() + i0, angles.begin() + i0 + nb);
     double* Y = ybuf_.ensure(static_cast<size_t>(n_) * block);
+    // Y = X C (read X once per block, write Y) and the stencil residual
+    // (read Y, the Sigma_t blocks and rhs once per block): 2 n r nb flops
+    pt_.work(8.0 * (static_cast<double>(n_) * rank_ + 2.0 * n_ * nb + 16.0 * hp_.ncell + n_),
+             2.0 * n_ * rank_ * nb + 60.0 * n_ * nb);
     gemm_nn(n_, nb, rank_, X_.col(0), X_.ld, coeffs + static_cast<long long>(i0) * ldc, ldc, Y, n_, s_);
     int* d_ang = upload_ints(ang_, sub);
     launch_residual_norms(sa_, nb, d_ang, dirs_, Y, n_, rhs_core_.get(), hp_.bc_any ? P_.bc_.get() : nullptr, n_,
@@ -1169,6 +1197,8 @@ void LowRankEngine::build_full_coefficients(const std::vector<int>* cand, const 
 
 // phi = X (C w)   (low_rank.cpp:385,394)
 void LowRankEngine::phi_from_C() {
+  pt_.work(8.0 * (static_cast<double>(n_) * rank_ + static_cast<double>(rank_) * nomega_ + n_),
+           2.0 * n_ * rank_ + 2.0 * rank_ * nomega_);
   double* cw = vec_.get() + 2 * static_cast<size_t>(rmax_);
   RTLR_CUDA(cudaMemsetAsync(cw, 0, rank_ * sizeof(double), s_));
   gemv_n(rank_, nomega_, C_.get(), rank_, P_.weights_.get(), 1.0, cw, s_);
@@ -1237,6 +1267,9 @@ InnerResult LowRankEngine::inner(const double* d_phi_prev, SubsampleRng& rng) {
     {  // sharded: this rank's block of the sampled sweeps, then one all-gather
       const ShardBlock sb = blk(p_now);
       P_.sweep(d_next + sb.begin, sb.end - sb.begin, rhs_core_.get(), 0, S + static_cast<size_t>(sb.begin) * n_, n_);
+      // Sigma_t blocks + the shared rhs read once, one psi written per direction;
+      // ~150 flops per cell-direction (4x4 LU, solve, two upwind couplings)
+      pt_.work(8.0 * (16.0 * hp_.ncell + n_ + static_cast<double>(p_now) * n_), 150.0 * p_now * hp_.ncell);
       // (the singular-block flag is read with the CGS state; sharded, it is
       // max-reduced first so every rank throws together)
       if (P_.sharded()) {
@@ -1360,6 +1393,12 @@ std::vector<double> LowRankEngine::svd(bool vectors, int keep, std::vector<doubl
   int sweeps = 0;
   jacobi_svd(ncols, ncols, Mt, ncols, J, 60, &rotated, work(4096), s_, &sweeps);
   svd_sweeps_ += sweeps;
+  {  // Householder R of the N_Omega x r (or r x N_Omega) factor, then one-sided
+     // Jacobi sweeps on the n x n core (pair dots + rotations, 6 n^3 flops per sweep)
+    const double mm = static_cast<double>(mrows), nn = ncols;
+    pt_.work(8.0 * (2.0 * mm * nn + 2.0 * sweeps * nn * nn), 2.0 * mm * nn * nn - 2.0 / 3.0 * nn * nn * nn +
+                                                                  6.0 * sweeps * nn * nn * nn);
+  }
   ++svd_calls_;
   double* nr = nrm_.ensure(ncols);
   col_norms_kernel<<<ncols, 256, 0, s_>>>(ncols, ncols, Mt, ncols, nr);
@@ -1493,6 +1532,10 @@ SolveReport Problem::solve_low_rank(const LowRankOptions& o) {
     if (o.use_dsa) {
       eng.pt_.start("dsa");
       rec.dsa_iterations = dsa_correct(eng.phi(), phi, delta);
+      // per PCG iteration: the SIP SpMV (5 4x4 blocks per cell), the V-cycle
+      // (two block smoothing sweeps, transfers, coarser 5-point levels) and
+      // the vector updates: ~2.5 KB and ~1.3 kflop per cell
+      eng.pt_.work(2500.0 * hp_.ncell * rec.dsa_iterations, 1300.0 * hp_.ncell * rec.dsa_iterations);
       vadd(static_cast<int>(n), eng.phi(), delta, phi, stream_);
       eng.pt_.stop();
     } else {
@@ -1510,6 +1553,13 @@ SolveReport Problem::solve_low_rank(const LowRankOptions& o) {
                  "%d Jacobi sweeps | galerkin: %lld batches, %lld systems | verify: %lld passes, %lld angles\n",
                  eng.reorth_count_, eng.reorth_seconds_, eng.cgs_split_[0], eng.cgs_split_[3], eng.cgs_split_[1], eng.svd_calls_,
                  eng.svd_sweeps_, eng.gal_calls_, eng.gal_systems_, eng.verify_calls_, eng.verify_angles_);
+  }
+  rep.phase_work.assign(4 * kPhaseCount, 0.0);
+  for (int k = 0; k < kPhaseCount; ++k) {
+    rep.phase_work[4 * k] = eng.pt_.seconds(k);
+    rep.phase_work[4 * k + 1] = eng.pt_.bytes[k];
+    rep.phase_work[4 * k + 2] = eng.pt_.flops[k];
+    rep.phase_work[4 * k + 3] = static_cast<double>(eng.pt_.calls[k]);
   }
   rep.phi.resize(n);
   RTLR_CUDA(cudaMemcpyAsync(rep.phi.data(), phi, n * sizeof(double), cudaMemcpyDeviceToHost, stream_));

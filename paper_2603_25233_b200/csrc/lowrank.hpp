@@ -87,31 +87,59 @@ struct DMat {
   double* col(int j) const { return buf.get() + static_cast<size_t>(ld) * j; }
 };
 
-// Per-phase wall-clock accounting (RTLR_PROFILE=1, or a report's profile
-// request): synchronizes the stream at phase boundaries, so it is off by
-// default.
+// Per-phase accounting.  Algorithmic work (bytes that must cross HBM and
+// flops, from the shapes of each call: DESIGN.md "Per-phase roofline") is
+// always counted (host arithmetic only); wall time per phase needs
+// synchronisation at the phase boundaries, so it is taken only with
+// RTLR_PROFILE=1 or the problem option "profile_phases".
+constexpr int kPhaseCount = 9;
+inline const char* const* phase_names() {
+  static const char* const names[kPhaseCount] = {"sweep", "cgs", "projections", "galerkin_q", "residual_q",
+                                                 "build_C", "verify", "svd", "dsa"};
+  return names;
+}
 struct PhaseTimer {
   bool on = false;
   cudaStream_t s = nullptr;
   std::vector<std::pair<std::string, double>> acc;
   std::chrono::steady_clock::time_point t0;
   std::string cur;
+  int idx = -1;  // current phase (always tracked, for the work counters)
+  double bytes[kPhaseCount] = {}, flops[kPhaseCount] = {};
+  long long calls[kPhaseCount] = {};
   void start(const char* name) {
+    idx = -1;
+    for (int k = 0; k < kPhaseCount; ++k)
+      if (std::string(phase_names()[k]) == name) idx = k;
+    if (idx >= 0) ++calls[idx];
+    cur = name;
     if (!on) return;
     RTLR_CUDA(cudaStreamSynchronize(s));
     t0 = std::chrono::steady_clock::now();
-    cur = name;
   }
   void stop() {
-    if (!on) return;
-    RTLR_CUDA(cudaStreamSynchronize(s));
-    const double dt = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+    if (on) {
+      RTLR_CUDA(cudaStreamSynchronize(s));
+      const double dt = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+      bool found = false;
+      for (auto& e : acc)
+        if (e.first == cur) {
+          e.second += dt;
+          found = true;
+        }
+      if (!found) acc.push_back({cur, dt});
+    }
+    idx = -1;
+  }
+  void work(double b, double f) {
+    if (idx < 0) return;
+    bytes[idx] += b;
+    flops[idx] += f;
+  }
+  double seconds(int k) const {
     for (auto& e : acc)
-      if (e.first == cur) {
-        e.second += dt;
-        return;
-      }
-    acc.push_back({cur, dt});
+      if (e.first == phase_names()[k]) return e.second;
+    return on ? 0.0 : -1.0;
   }
 };
 

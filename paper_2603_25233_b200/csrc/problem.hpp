@@ -85,6 +85,9 @@ struct SolveReport {
   bool has_factors = false;
   LowRankFactors factors;
   std::vector<std::vector<int>> sampled_log;
+  // Low-rank phases (lowrank.hpp phase_names order): wall seconds (-1 when
+  // not timed), algorithmic HBM bytes, flops, calls.
+  std::vector<double> phase_work;  // kPhaseCount x 4
 };
 
 struct FullRankOptions {  // full_rank.hpp:32-37
@@ -190,6 +193,7 @@ class Problem {
   double pcg_rtol = 1e-13;
   int pcg_max_iters = 20000;
   bool pcg_multigrid = true;  // false: block-Jacobi PCG
+  bool profile_phases = false;  // time the low-rank phases (synchronises at phase boundaries)
   int sweep_kernel = 0;  // 0 auto, 1 skewed wavefront (sweep.cu), 2 row scan, 3 row scan on prefactored blocks,
                          // 4 cluster wavefront (few directions), 5 direction-group kernel (sweep_het.cu)
 
