@@ -1289,6 +1289,143 @@ __device__ __forceinline__ void jacobi_pair(long long m, int n, int npad, int t,
   }
 }
 
+// ------------------------------------------------------------ singular values
+// Singular values only (the truncation rank every outer iteration,
+// low_rank.cpp:254-266): Golub-Kahan bidiagonalisation of the m x n factor
+// (m >= n) in one cooperative launch, then bisection on the zero-diagonal
+// Golub-Kahan tridiagonal (eigenvalues +-sigma), one thread per singular
+// value.  Three grid barriers per column (left reflector applied to the
+// trailing columns, warp per column; the right reflector's row products as
+// fixed-order partials over 64-column chunks; their update), against one
+// per round of n - 1 rounds per Jacobi sweep.  Householder vectors follow
+// hh_make's conventions (Eigen's makeHouseholder); every CTA derives a
+// reflector from its own identical reduction, so the tau == 0 branches are
+// grid-uniform.
+__device__ __forceinline__ void hh_params(double c0, double tail2, double& beta, double& tau, double& denom) {
+  if (tail2 <= 2.2250738585072014e-308) {
+    tau = 0.0;
+    beta = c0;
+    denom = 0.0;
+  } else {
+    beta = sqrt(c0 * c0 + tail2);
+    if (c0 >= 0.0) beta = -beta;
+    denom = c0 - beta;
+    tau = (beta - c0) / beta;
+  }
+}
+
+__global__ void __launch_bounds__(256) bidiag_coop(int m, int n, double* __restrict__ A, long long lda,
+                                                   double* __restrict__ d, double* __restrict__ e,
+                                                   double* __restrict__ part) {
+  namespace cg = cooperative_groups;
+  cg::grid_group grid = cg::this_grid();
+  extern __shared__ double bd_sm[];
+  double* v = bd_sm;      // m: left reflector
+  double* u = bd_sm + m;  // n: right reflector
+  __shared__ double red[32];
+  const int tid = threadIdx.x, lane = tid & 31;
+  const int nwt = gridDim.x * (blockDim.x >> 5), gw = blockIdx.x * (blockDim.x >> 5) + (tid >> 5);
+  for (int k = 0; k < n; ++k) {
+    // left reflector of column k (rows k..m-1) -> d[k]
+    const double* ck = A + static_cast<long long>(k) * lda;
+    double t2 = 0.0;
+    for (int i = k + 1 + tid; i < m; i += blockDim.x) t2 += ck[i] * ck[i];
+    t2 = block_sum_all(t2, red);
+    double beta, tau, den;
+    hh_params(ck[k], t2, beta, tau, den);
+    for (int i = k + tid; i < m; i += blockDim.x) v[i] = i == k ? 1.0 : (den != 0.0 ? ck[i] / den : 0.0);
+    __syncthreads();
+    if (blockIdx.x == 0 && tid == 0) d[k] = beta;
+    if (tau != 0.0)
+      for (int j = k + 1 + gw; j < n; j += nwt) {
+        double* cj = A + static_cast<long long>(j) * lda;
+        double w = 0.0;
+        for (int i = k + lane; i < m; i += 32) w += v[i] * cj[i];
+        w = warp_sum(w);
+        const double tw = tau * w;
+        for (int i = k + lane; i < m; i += 32) cj[i] -= tw * v[i];
+      }
+    grid.sync();
+    if (k + 1 >= n) break;
+    // right reflector of row k (columns k+1..n-1) -> e[k]
+    double s2 = 0.0;
+    for (int j = k + 2 + tid; j < n; j += blockDim.x) {
+      const double x = A[k + static_cast<long long>(j) * lda];
+      s2 += x * x;
+    }
+    s2 = block_sum_all(s2, red);
+    double beta2, tau2, den2;
+    hh_params(A[k + static_cast<long long>(k + 1) * lda], s2, beta2, tau2, den2);
+    for (int j = k + 1 + tid; j < n; j += blockDim.x)
+      u[j] = j == k + 1 ? 1.0 : (den2 != 0.0 ? A[k + static_cast<long long>(j) * lda] / den2 : 0.0);
+    __syncthreads();
+    if (blockIdx.x == 0 && tid == 0) e[k] = beta2;
+    if (tau2 != 0.0) {
+      const int rows = m - k - 1, cols = n - k - 1;
+      const int nrb = (rows + 31) / 32, ncc = (cols + 63) / 64;
+      for (int it = gw; it < nrb * ncc; it += nwt) {  // row products, 64-column partials
+        const int rb = it % nrb, cc = it / nrb;
+        const int i = k + 1 + rb * 32 + lane;
+        const int j0 = k + 1 + cc * 64, j1 = min(n, j0 + 64);
+        double acc = 0.0;
+        if (i < m)
+          for (int j = j0; j < j1; ++j) acc += A[i + static_cast<long long>(j) * lda] * u[j];
+        if (i < m) part[static_cast<long long>(cc) * m + i] = acc;
+      }
+      grid.sync();
+      for (int it = gw; it < nrb * ncc; it += nwt) {  // rank-1 update
+        const int rb = it % nrb, cc = it / nrb;
+        const int i = k + 1 + rb * 32 + lane;
+        if (i >= m) continue;
+        double w = 0.0;
+        for (int c = 0; c < ncc; ++c) w += part[static_cast<long long>(c) * m + i];
+        const double tw = tau2 * w;
+        const int j0 = k + 1 + cc * 64, j1 = min(n, j0 + 64);
+        for (int j = j0; j < j1; ++j) A[i + static_cast<long long>(j) * lda] -= tw * u[j];
+      }
+    }
+    grid.sync();
+  }
+}
+
+// Number of eigenvalues of the Golub-Kahan tridiagonal (zero diagonal,
+// off-diagonals d0, e0, d1, e1, ..., d_{n-1}) below x (Sturm count, LDL^T pivots).
+__device__ int gk_count_below(int n, const double* __restrict__ d, const double* __restrict__ e, double x,
+                             double pivmin) {
+  int cnt = 0;
+  double q = -x;
+  if (q < 0.0) ++cnt;
+  for (int j = 1; j < 2 * n; ++j) {
+    const double t = (j & 1) ? d[j >> 1] : e[(j >> 1) - 1];
+    if (fabs(q) < pivmin) q = -pivmin;
+    q = -x - t * t / q;
+    if (q < 0.0) ++cnt;
+  }
+  return cnt;
+}
+
+__global__ void gk_bisect(int n, const double* __restrict__ d, const double* __restrict__ e, double* __restrict__ sv) {
+  const int k = blockIdx.x * blockDim.x + threadIdx.x;  // k-th smallest
+  if (k >= n) return;
+  double ub = 0.0, tmax = 0.0;
+  for (int j = 0; j < n; ++j) {
+    const double a = fabs(d[j]), b = j + 1 < n ? fabs(e[j]) : 0.0, c = j > 0 ? fabs(e[j - 1]) : 0.0;
+    ub = fmax(ub, fmax(a + c, a + b));
+    tmax = fmax(tmax, fmax(a, b));
+  }
+  const double pivmin = fmax(2.2250738585072014e-308, 2.2250738585072014e-308 * tmax * tmax);
+  double lo = 0.0, hi = ub * (1.0 + 4e-16) + pivmin;
+  // #(sigma < x) = count(x) - n for x > 0
+  for (int it = 0; it < 200 && hi - lo > 4e-16 * hi + pivmin; ++it) {
+    const double mid = 0.5 * (lo + hi);
+    if (gk_count_below(n, d, e, mid, pivmin) - n > k)
+      hi = mid;
+    else
+      lo = mid;
+  }
+  sv[n - 1 - k] = 0.5 * (lo + hi);  // descending
+}
+
 __global__ void __launch_bounds__(256) jacobi_round(long long m, int n, int npad, int t, double* __restrict__ w,
                                                     long long ldw, double* __restrict__ v, int* __restrict__ rotated,
                                                     double tiny) {
@@ -2346,6 +2483,38 @@ bool householder_r_coop(long long m, int n, double* a, long long lda, double* r,
   const int g = std::max(1, std::min(grid, (n + 7) / 8));
   void* args[] = {&m, &n, &a, &lda, &r};
   RTLR_CUDA(cudaLaunchCooperativeKernel(reinterpret_cast<void*>(qr_r_coop), dim3(g), dim3(256), args, 0, s));
+  return true;
+}
+
+size_t bidiag_work_doubles(long long m, int n) { return static_cast<size_t>(2 * n + 8) + static_cast<size_t>((n + 63) / 64) * m; }
+
+bool bidiag_singular_values(long long m, int n, double* a, long long lda, double* d_sv, double* work,
+                            size_t work_doubles, cudaStream_t s) {
+  if (n < 1 || m < n || m > 8192 || work_doubles < bidiag_work_doubles(m, n)) return false;
+  static const int coop_per_sm = [] {
+    int dev = 0, ok = 0, per = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&ok, cudaDevAttrCooperativeLaunch, dev);
+    const char* e = std::getenv("RTLR_SVD");
+    if (!ok || (e && std::string(e) == "jacobi")) return 0;
+    RTLR_CUDA(cudaFuncSetAttribute(bidiag_coop, cudaFuncAttributeMaxDynamicSharedMemorySize, 2 * 8192 * 8));
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, bidiag_coop, 256, 2 * 8192 * 8);
+    return std::min(per, 2);
+  }();
+  if (coop_per_sm == 0) return false;
+  int dev = 0, sms = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  double* dd = work;
+  double* de = work + n;
+  double* part = work + 2 * n + 8;
+  int mi = static_cast<int>(m);
+  const size_t smem = static_cast<size_t>(m + n) * sizeof(double);
+  void* args[] = {&mi, &n, &a, &lda, &dd, &de, &part};
+  RTLR_CUDA(cudaLaunchCooperativeKernel(reinterpret_cast<void*>(bidiag_coop), dim3(sms * coop_per_sm), dim3(256), args,
+                                        smem, s));
+  gk_bisect<<<(n + 127) / 128, 128, 0, s>>>(n, dd, de, d_sv);
+  RTLR_CUDA(cudaGetLastError());
   return true;
 }
 

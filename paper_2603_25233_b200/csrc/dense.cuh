@@ -68,6 +68,13 @@ bool householder_r_coop(long long m, int n, double* a, long long lda, double* r,
 // rotations in v (n x n) when given.  Afterwards columns of w are mutually
 // orthogonal: w = U diag(s), s = column norms.
 // work >= n + 8 doubles; sweeps_used (optional) receives the sweep count.
+// Singular values (descending, device d_sv[n]) of the m x n matrix a
+// (m >= n, destroyed): cooperative Golub-Kahan bidiagonalisation and
+// bisection on the Golub-Kahan tridiagonal.  false: not applicable (no
+// cooperative launch, m > 8192, RTLR_SVD=jacobi), nothing launched.
+size_t bidiag_work_doubles(long long m, int n);
+bool bidiag_singular_values(long long m, int n, double* a, long long lda, double* d_sv, double* work,
+                            size_t work_doubles, cudaStream_t s);
 void jacobi_svd(long long m, int n, double* w, long long ldw, double* v, int max_sweeps, int* host_rotated,
                 double* work, cudaStream_t s, int* sweeps_used = nullptr);
 

@@ -1371,6 +1371,25 @@ std::vector<double> LowRankEngine::svd(bool vectors, int keep, std::vector<doubl
   else
     RTLR_CUDA(cudaMemcpyAsync(Wm, C_.get(), static_cast<size_t>(r) * nomega_ * sizeof(double),
                               cudaMemcpyDeviceToDevice, s_));
+  if (!vectors && static_cast<double>(mrows) * ncols >= 3e5) {
+    // singular values only (every outer iteration): bidiagonalisation of W
+    // and Golub-Kahan bisection, without the QR and the Jacobi sweeps (C4
+    // 0.31 -> 0.24 s, C3 0.155 -> 0.13 s; smaller factors stay on QR +
+    // Jacobi, whose sweeps there cost less than 3 grid barriers per column)
+    double* dsv = nrm_.ensure(std::max(ncols, 128));
+    if (bidiag_singular_values(mrows, ncols, Wm, mrows, dsv, work(bidiag_work_doubles(mrows, ncols)), work_.size(),
+                               s_)) {
+      ++svd_calls_;
+      const double mm = static_cast<double>(mrows), nn = ncols;
+      // 4 m n^2 - 4/3 n^3 flops; the factor crosses HBM once each way (its
+      // per-column passes stay in L2)
+      pt_.work(8.0 * 2.0 * mm * nn, 4.0 * mm * nn * nn - 4.0 / 3.0 * nn * nn * nn);
+      std::vector<double> sv(ncols);
+      RTLR_CUDA(cudaMemcpyAsync(sv.data(), dsv, ncols * sizeof(double), cudaMemcpyDeviceToHost, s_));
+      RTLR_CUDA(cudaStreamSynchronize(s_));
+      return sv;
+    }
+  }
   double* Q = svq_.ensure(static_cast<size_t>(mrows) * ncols);
   double* R = svr_.ensure(static_cast<size_t>(ncols) * ncols);
   double* Mt = svm_.ensure(static_cast<size_t>(ncols) * ncols);

@@ -345,3 +345,33 @@ def test_cpp_facade_consumer_on_gpu():
     r = subprocess.run([B.FACADE], capture_output=True, text=True, timeout=600)
     print(r.stdout, r.stderr)
     assert r.returncode == 0, r.stdout + r.stderr
+
+
+@pytest.mark.parametrize("r,n_omega", [(40, 96), (300, 1100), (560, 540)])
+def test_singular_values_bidiagonal_path(r, n_omega, monkeypatch):
+    """The per-outer-iteration singular values (low_rank.cpp:457) of factors
+    with >= 3e5 entries come from a Golub-Kahan bidiagonalisation + bisection
+    (no vectors needed; smaller ones from QR + Jacobi); against
+    numpy's SVD and the one-sided Jacobi path (RTLR_SVD=jacobi is read once
+    per process, so the Jacobi values come from truncate_factors with
+    vectors): absolute error <= 1e-13 sigma_max (n eps: backward error of the
+    bidiagonalisation) over singular values graded
+    from 1 to 1e-13, so the truncation rank (tail sum vs eps_svd * total)
+    cannot move."""
+    g = P.Problem("homogeneous(1,1)", nx=12, ny=12, n_theta=n_omega, n_omega_z=1, use_dsa=0)
+    rng = np.random.default_rng(r)
+    k = min(r, n_omega)
+    uu, _ = np.linalg.qr(rng.standard_normal((r, k)))
+    vv, _ = np.linalg.qr(rng.standard_normal((n_omega, k)))
+    s_true = np.logspace(0, -13, k)
+    C = uu @ np.diag(s_true) @ vv.T
+    bx, _ = np.linalg.qr(rng.standard_normal((g.n, r)))
+    sv = P.svd_values(g, C, bx)
+    ref = np.linalg.svd(C, compute_uv=False)
+    assert len(sv) == k
+    assert np.max(np.abs(sv - ref)) <= 1e-13 * ref[0]
+    for eps in (1e-8, 1e-10, 1e-6):
+        assert P.truncation_rank(sv, eps) == P.truncation_rank(ref, eps)
+    _, S2, _ = P.truncate_factors(g, C, bx, 1e-12)  # the vectors path (QR + Jacobi)
+    kk = len(S2)
+    assert np.max(np.abs(np.asarray(S2) - sv[:kk])) <= 1e-13 * ref[0]
