@@ -1289,6 +1289,119 @@ __device__ __forceinline__ void jacobi_pair(long long m, int n, int npad, int t,
   }
 }
 
+// ------------------------------------------------------------ CholeskyQR2 pieces
+// Upper Cholesky G = R^T R in place (r x r, column-major, ld r; the upper
+// triangle is read, the lower zeroed), one CTA; flag[0] = 1 on a non-positive
+// pivot.  Right-looking: per step the pivot, row k of R, the symmetric
+// trailing update of the upper triangle.
+__global__ void __launch_bounds__(1024) chol_upper_kernel(int r, double* __restrict__ G, int* __restrict__ flag) {
+  __shared__ double rkk;
+  const int tid = threadIdx.x, nt = blockDim.x;
+  for (int k = 0; k < r; ++k) {
+    if (tid == 0) {
+      const double d = G[k + static_cast<size_t>(k) * r];
+      if (!(d > 0.0)) *flag = 1;
+      rkk = d > 0.0 ? sqrt(d) : 1.0;
+      G[k + static_cast<size_t>(k) * r] = rkk;
+    }
+    __syncthreads();
+    const double inv = rkk;
+    for (int j = k + 1 + tid; j < r; j += nt) G[k + static_cast<size_t>(j) * r] /= inv;
+    __syncthreads();
+    const int m = r - k - 1;  // trailing order; upper-triangle pairs (i <= j) by column
+    for (long long e = tid; e < static_cast<long long>(m) * m; e += nt) {
+      const int i = k + 1 + static_cast<int>(e % m), j = k + 1 + static_cast<int>(e / m);
+      if (i <= j) G[i + static_cast<size_t>(j) * r] -= G[k + static_cast<size_t>(i) * r] * G[k + static_cast<size_t>(j) * r];
+    }
+    __syncthreads();
+  }
+  for (long long e = tid; e < static_cast<long long>(r) * r; e += nt) {
+    const int i = static_cast<int>(e % r), j = static_cast<int>(e / r);
+    if (i > j) G[e] = 0.0;
+  }
+}
+
+// Upper Cholesky of an order-n <= 32 block in place (ld ldg), lower part
+// zeroed; flag on a non-positive pivot.
+__global__ void __launch_bounds__(32) chol_upper_small(int n, double* __restrict__ G, long long ldg,
+                                                       int* __restrict__ flag) {
+  __shared__ double A[32][33];
+  const int t = threadIdx.x;
+  for (int e = t; e < n * n; e += 32) A[e % n][e / n] = G[(e % n) + (e / n) * ldg];
+  __syncwarp();
+  for (int k = 0; k < n; ++k) {
+    const double d = A[k][k];
+    if (t == 0 && !(d > 0.0)) *flag = 1;
+    const double rkk = d > 0.0 ? sqrt(d) : 1.0;
+    __syncwarp();
+    if (t == k) A[k][k] = rkk;
+    if (t > k && t < n) A[k][t] /= rkk;
+    __syncwarp();
+    // trailing upper triangle: column t (t > k), rows k+1..t
+    if (t > k && t < n)
+      for (int i = k + 1; i <= t; ++i) A[i][t] -= A[k][i] * A[k][t];
+    __syncwarp();
+  }
+  for (int e = t; e < n * n; e += 32) {
+    const int i = e % n, c = e / n;
+    G[i + c * ldg] = i <= c ? A[i][c] : 0.0;
+  }
+}
+
+__global__ void sub_inplace_kernel(int m, int n, const double* __restrict__ t, long long ldt, double* __restrict__ a,
+                                   long long lda) {
+  for (long long e = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; e < static_cast<long long>(m) * n;
+       e += static_cast<long long>(gridDim.x) * blockDim.x) {
+    const int i = static_cast<int>(e % m), c = static_cast<int>(e / m);
+    a[i + c * lda] -= t[i + c * ldt];
+  }
+}
+
+__global__ void copy2d_kernel(int m, int n, const double* __restrict__ src, long long lds, double* __restrict__ dst,
+                              long long ldd, bool zero_src_lower_of_square) {
+  for (long long e = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; e < static_cast<long long>(m) * n;
+       e += static_cast<long long>(gridDim.x) * blockDim.x) {
+    const int i = static_cast<int>(e % m), c = static_cast<int>(e / m);
+    dst[i + c * ldd] = src[i + c * lds];
+  }
+}
+
+// Ri = R^-1 for an upper-triangular block of order n <= 32 (ld ldr / ldi):
+// the block in shared memory, one thread per column, back substitution from
+// the diagonal up.
+__global__ void __launch_bounds__(32) tri_inv_upper_small(int n, const double* __restrict__ R, long long ldr,
+                                                          double* __restrict__ Ri, long long ldi) {
+  __shared__ double Rs[32][33];
+  __shared__ double Xs[32][33];
+  const int j = threadIdx.x;
+  for (int e = j; e < n * n; e += blockDim.x) {
+    const int i = e % n, c = e / n;
+    Rs[i][c] = R[i + c * ldr];
+  }
+  __syncthreads();
+  if (j < n) {
+    for (int i = j + 1; i < n; ++i) Xs[i][j] = 0.0;
+    for (int i = j; i >= 0; --i) {
+      double s = i == j ? 1.0 : 0.0;
+      for (int l = i + 1; l <= j; ++l) s -= Rs[i][l] * Xs[l][j];
+      Xs[i][j] = s / Rs[i][i];
+    }
+  }
+  __syncthreads();
+  for (int e = j; e < n * n; e += blockDim.x) {
+    const int i = e % n, c = e / n;
+    Ri[i + c * ldi] = Xs[i][c];
+  }
+}
+
+__global__ void neg_kernel(int m, int n, double* __restrict__ a, long long lda) {
+  for (long long e = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; e < static_cast<long long>(m) * n;
+       e += static_cast<long long>(gridDim.x) * blockDim.x) {
+    const int i = static_cast<int>(e % m), c = static_cast<int>(e / m);
+    a[i + c * lda] = -a[i + c * lda];
+  }
+}
+
 // ------------------------------------------------------------ singular values
 // Singular values only (the truncation rank every outer iteration,
 // low_rank.cpp:254-266): Golub-Kahan bidiagonalisation of the m x n factor
@@ -2483,6 +2596,104 @@ bool householder_r_coop(long long m, int n, double* a, long long lda, double* r,
   const int g = std::max(1, std::min(grid, (n + 7) / 8));
   void* args[] = {&m, &n, &a, &lda, &r};
   RTLR_CUDA(cudaLaunchCooperativeKernel(reinterpret_cast<void*>(qr_r_coop), dim3(g), dim3(256), args, 0, s));
+  return true;
+}
+
+// Ri (ld n) = R^-1 for upper-triangular R (order n, ld n), recursively:
+// [[A, B], [0, C]]^-1 = [[A^-1, -A^-1 B C^-1], [0, C^-1]], the off-diagonal
+// block by two DMMA products through T (n x n scratch); blocks of <= 32 in
+// shared memory (<= 32).  Ri's strictly lower part is zeroed by the caller.
+static void tri_inv_upper_rec(int n, const double* R, long long ldr, double* Ri, long long ldi, double* T,
+                              cudaStream_t s) {
+  if (n <= 32) {
+    tri_inv_upper_small<<<1, 32, 0, s>>>(n, R, ldr, Ri, ldi);
+    return;
+  }
+  const int n1 = ((n / 2 + 31) / 32) * 32, n2 = n - n1;
+  tri_inv_upper_rec(n1, R, ldr, Ri, ldi, T, s);
+  tri_inv_upper_rec(n2, R + n1 + static_cast<long long>(n1) * ldr, ldr, Ri + n1 + static_cast<long long>(n1) * ldi,
+                    ldi, T, s);
+  // T = B C^-1 (n1 x n2), Ri_top_right = -(A^-1 T)
+  gemm_nn(n1, n2, n2, R + static_cast<long long>(n1) * ldr, ldr, Ri + n1 + static_cast<long long>(n1) * ldi, ldi, T,
+          n1, s);
+  double* tr = Ri + static_cast<long long>(n1) * ldi;
+  gemm_nn(n1, n2, n1, Ri, ldi, T, n1, tr, ldi, s);
+  neg_kernel<<<std::max(1, std::min(1024, (n1 * n2 + 255) / 256)), 256, 0, s>>>(n1, n2, tr, ldi);
+}
+
+// Upper Cholesky G = R^T R in place (order n, ld ldg; G's lower part
+// zeroed), recursively: R11 = chol(G11); R12 = R11^-T G12; R22 =
+// chol(G22 - R12^T R12), with DMMA products and R11^-1 by
+// tri_inv_upper_rec; blocks of <= 32 in shared memory.  ws: 3 n^2 doubles.
+static void chol_upper_rec(int n, double* G, long long ldg, double* ws, int* flag, cudaStream_t s) {
+  if (n <= 32) {
+    chol_upper_small<<<1, 32, 0, s>>>(n, G, ldg, flag);
+    return;
+  }
+  const int n1 = ((n / 2 + 31) / 32) * 32, n2 = n - n1;
+  double* G12 = G + static_cast<long long>(n1) * ldg;
+  double* G22 = G12 + n1;
+  chol_upper_rec(n1, G, ldg, ws, flag, s);
+  double* Ri = ws;                                       // n1 x n1
+  double* T = ws + static_cast<size_t>(n1) * n1;         // n1 x n2 (then n2 x n2)
+  double* Tr = T + static_cast<size_t>(n1) * std::max(n1, n2);  // scratch of tri_inv_upper_rec
+  RTLR_CUDA(cudaMemsetAsync(Ri, 0, static_cast<size_t>(n1) * n1 * sizeof(double), s));
+  tri_inv_upper_rec(n1, G, ldg, Ri, n1, Tr, s);
+  // R12 = Ri^T G12 -> T, copied into G12
+  double* gw = Tr;  // (gemm_tn with M = n1, K = n1: split count from the shape, partials in gw)
+  gemm_tn(n1, n2, n1, Ri, n1, G12, ldg, T, n1, gw, static_cast<size_t>(n1) * std::max(n1, n2) * 4, s);
+  const int g = std::max(1, std::min(1024, (n1 * n2 + 255) / 256));
+  copy2d_kernel<<<g, 256, 0, s>>>(n1, n2, T, n1, G12, ldg, false);
+  // G22 -= R12^T R12
+  gemm_tn(n2, n2, n1, G12, ldg, G12, ldg, T, n2, gw, static_cast<size_t>(n1) * std::max(n1, n2) * 4, s);
+  sub_inplace_kernel<<<std::max(1, std::min(1024, (n2 * n2 + 255) / 256)), 256, 0, s>>>(n2, n2, T, n2, G22, ldg);
+  chol_upper_rec(n2, G22, ldg, ws, flag, s);
+  // the lower-left block is zero
+  RTLR_CUDA(cudaMemset2DAsync(G + n1, ldg * sizeof(double), 0, n2 * sizeof(double), n1, s));
+}
+size_t cholqr2_work_doubles(long long m, int n) {
+  return std::max(gemm_tn_work(n, n, m), static_cast<size_t>(1)) + 12 * static_cast<size_t>(n) * n + 8;
+}
+
+// X (m x n, ld ldx) <- Q, R (n x n, ld n) with X_in = Q R, Q orthonormal:
+// two rounds of G = X^T X (DMMA), G = R^T R (Cholesky), X <- X R^-1
+// (DMMA), R = R2 R1.  Q buffer: m x n scratch (ld m).  For well-conditioned
+// X (the low-rank basis after the block CGS: an orthonormal block plus
+// orthonormalised new columns, losing orthogonality at the 1e-10 level that
+// triggers the rebuild); false (and X untouched) on a non-positive pivot.
+bool cholqr2_inplace(long long m, int n, double* X, long long ldx, double* R, double* Qbuf, double* work,
+                     size_t work_doubles, int* d_flag, cudaStream_t s) {
+  if (n < 1 || work_doubles < cholqr2_work_doubles(m, n)) return false;
+  const size_t nn = static_cast<size_t>(n) * n;
+  double* G = work;
+  double* Ri = work + nn;
+  double* R1 = work + 2 * nn;
+  double* T = work + 3 * nn;
+  double* cws = work + 5 * nn;  // chol_upper_rec scratch (up to ~7 n^2 with the partials)
+  double* gw = work + 12 * nn + 8;
+  const size_t gwn = work_doubles - (12 * nn + 8);
+  RTLR_CUDA(cudaMemsetAsync(d_flag, 0, sizeof(int), s));
+  auto inv = [&]() {
+    RTLR_CUDA(cudaMemsetAsync(Ri, 0, nn * sizeof(double), s));
+    tri_inv_upper_rec(n, G, n, Ri, n, T, s);
+  };
+  // round 1: X -> Qbuf
+  gemm_tn(n, n, m, X, ldx, X, ldx, G, n, gw, gwn, s);
+  chol_upper_rec(n, G, n, cws, d_flag, s);
+  inv();
+  RTLR_CUDA(cudaMemcpyAsync(R1, G, nn * sizeof(double), cudaMemcpyDeviceToDevice, s));
+  gemm_nn(m, n, n, X, ldx, Ri, n, Qbuf, m, s);
+  // round 2: Qbuf -> X
+  gemm_tn(n, n, m, Qbuf, m, Qbuf, m, G, n, gw, gwn, s);
+  chol_upper_rec(n, G, n, cws, d_flag, s);
+  inv();
+  int hflag = 0;
+  RTLR_CUDA(cudaMemcpyAsync(&hflag, d_flag, sizeof(int), cudaMemcpyDeviceToHost, s));
+  RTLR_CUDA(cudaStreamSynchronize(s));
+  if (hflag) return false;
+  gemm_nn(m, n, n, Qbuf, m, Ri, n, X, ldx, s);
+  gemm_nn(n, n, n, G, n, R1, n, R, n, s);  // R = R2 R1
+  RTLR_CUDA(cudaGetLastError());
   return true;
 }
 

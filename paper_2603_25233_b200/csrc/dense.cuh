@@ -68,6 +68,12 @@ bool householder_r_coop(long long m, int n, double* a, long long lda, double* r,
 // rotations in v (n x n) when given.  Afterwards columns of w are mutually
 // orthogonal: w = U diag(s), s = column norms.
 // work >= n + 8 doubles; sweeps_used (optional) receives the sweep count.
+// CholeskyQR2 of a well-conditioned m x n block in place: X <- Q, R (n x n,
+// ld n) with X_in = Q R.  Qbuf: m x n scratch; work >= cholqr2_work_doubles.
+// false on a non-positive Cholesky pivot (X untouched).
+size_t cholqr2_work_doubles(long long m, int n);
+bool cholqr2_inplace(long long m, int n, double* X, long long ldx, double* R, double* Qbuf, double* work,
+                     size_t work_doubles, int* d_flag, cudaStream_t s);
 // Singular values (descending, device d_sv[n]) of the m x n matrix a
 // (m >= n, destroyed): cooperative Golub-Kahan bidiagonalisation and
 // bisection on the Golub-Kahan tridiagonal.  false: not applicable (no

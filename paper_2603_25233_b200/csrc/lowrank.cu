@@ -566,6 +566,7 @@ LowRankEngine::LowRankEngine(Problem& P, const LowRankParams& prm) : P_(P), prm_
     X_.reserve(n_, rmax_, s_);
   const char* e = std::getenv("RTLR_PROFILE");
   pt_.on = (e && e[0] == '1') || P.profile_phases;
+  if (e && e[0] == '1') alloc_stats().split = true;
   pt_.s = s_;
   // row slices of the tall contractions
   const char* rs = std::getenv("RTLR_LR_ROWSLICE");
@@ -926,29 +927,54 @@ bool LowRankEngine::mgs_ro_update(const double* snaps, const std::vector<int>& a
     const auto tq0 = std::chrono::steady_clock::now();
     const int n_acc = static_cast<int>(accepted.size());
     const int r_new = prev_rank_ + n_acc;
-    double* M = qa_.ensure(static_cast<size_t>(n_) * r_new);
-    if (prev_rank_ > 0)
-      RTLR_CUDA(cudaMemcpyAsync(M, X_.col(0), static_cast<size_t>(n_) * prev_rank_ * sizeof(double),
-                                cudaMemcpyDeviceToDevice, s_));
-    for (int k = 0; k < n_acc; ++k)
-      RTLR_CUDA(cudaMemcpyAsync(M + static_cast<size_t>(n_) * (prev_rank_ + k),
-                                snaps + static_cast<size_t>(accepted[k]) * n_, n_ * sizeof(double),
-                                cudaMemcpyDeviceToDevice, s_));
-    double* Q = qq_.ensure(static_cast<size_t>(n_) * r_new);
     double* R = qr_.ensure(static_cast<size_t>(r_new) * r_new);
-    double* tau = tau_.ensure(r_new);
-    double* qw = work(householder_qr_work(n_, r_new));
-    householder_qr(n_, r_new, M, n_, tau, Q, n_, R, qw, work_.size(), s_);
-    {  // blocked Householder QR with Q formed: 4 m n^2 - 4/3 n^3 flops; per
-       // 32-column panel the trailing block is read and written (twice with Q)
-      const double rn = r_new, panels = std::ceil(rn / 32.0);
-      pt_.work(8.0 * n_ * rn * (2.0 + 2.0 * panels), 4.0 * n_ * rn * rn - 4.0 / 3.0 * rn * rn * rn);
+    // The new basis spans the same nested column spaces as the reference's
+    // Householder QR of [X_old, accepted snapshots] (low_rank.cpp:112-130):
+    // X_ already holds [X_old, the batch's CGS-orthonormalised columns], a
+    // well-conditioned block whose orthogonality slipped at the 1e-10 level
+    // the overlap test caught, so CholeskyQR2 on it (four DMMA products
+    // and two small Cholesky factorisations) gives the same Q up to column
+    // signs and rounding, and R[:, :prev] the old basis in the new one.
+    // Householder on the reference's matrix stays as the fallback (a
+    // non-positive Cholesky pivot) and behind RTLR_REBUILD=householder.
+    static const bool hh_only = [] {
+      const char* e = std::getenv("RTLR_REBUILD");
+      return e && std::string(e) == "householder";
+    }();
+    bool chol = false;
+    if (!hh_only) {
+      double* Qb = qq_.ensure(static_cast<size_t>(n_) * r_new);
+      double* cw = work(cholqr2_work_doubles(n_, r_new));
+      chol = cholqr2_inplace(n_, r_new, X_.col(0), X_.ld, R, Qb, cw, work_.size(), chol_flag_.ensure(1), s_);
+      if (chol) {  // two rounds of X^T X and X R^-1: 8 m n^2 flops, X read three times, written twice
+        const double rn = r_new;
+        pt_.work(8.0 * 5.0 * n_ * rn, 8.0 * n_ * rn * rn);
+      }
+    }
+    if (!chol) {
+      double* M = qa_.ensure(static_cast<size_t>(n_) * r_new);
+      if (prev_rank_ > 0)
+        RTLR_CUDA(cudaMemcpyAsync(M, X_.col(0), static_cast<size_t>(n_) * prev_rank_ * sizeof(double),
+                                  cudaMemcpyDeviceToDevice, s_));
+      for (int k = 0; k < n_acc; ++k)
+        RTLR_CUDA(cudaMemcpyAsync(M + static_cast<size_t>(n_) * (prev_rank_ + k),
+                                  snaps + static_cast<size_t>(accepted[k]) * n_, n_ * sizeof(double),
+                                  cudaMemcpyDeviceToDevice, s_));
+      double* Q = qq_.ensure(static_cast<size_t>(n_) * r_new);
+      double* tau = tau_.ensure(r_new);
+      double* qw = work(householder_qr_work(n_, r_new));
+      householder_qr(n_, r_new, M, n_, tau, Q, n_, R, qw, work_.size(), s_);
+      {  // blocked Householder QR with Q formed: 4 m n^2 - 4/3 n^3 flops; per
+         // 32-column panel the trailing block is read and written (twice with Q)
+        const double rn = r_new, panels = std::ceil(rn / 32.0);
+        pt_.work(8.0 * n_ * rn * (2.0 + 2.0 * panels), 4.0 * n_ * rn * rn - 4.0 / 3.0 * rn * rn * rn);
+      }
+      RTLR_CUDA(cudaMemcpyAsync(X_.col(0), Q, static_cast<size_t>(n_) * r_new * sizeof(double),
+                                cudaMemcpyDeviceToDevice, s_));
     }
     // batch columns: Q^T snapshots (low_rank.cpp:126-129)
     double* B = gbuf_.ensure(static_cast<size_t>(r_new) * p_in);
-    tn(r_new, p_in, Q, n_, snaps, n_, B, r_new);
-    RTLR_CUDA(cudaMemcpyAsync(X_.col(0), Q, static_cast<size_t>(n_) * r_new * sizeof(double),
-                              cudaMemcpyDeviceToDevice, s_));
+    tn(r_new, p_in, X_.col(0), X_.ld, snaps, n_, B, r_new);
     rank_ = r_new;
     if (m0 > 0 && prev_rank_ > 0) {
       // old record columns: R[:, :prev] old_j (low_rank.cpp:121-125), one
@@ -1569,9 +1595,13 @@ SolveReport Problem::solve_low_rank(const LowRankOptions& o) {
     for (auto& e : eng.pt_.acc) std::fprintf(stderr, " %s=%.4f", e.first.c_str(), e.second);
     std::fprintf(stderr,
                  " | reorth: %d rebuilds, %.4f s (inside cgs) | cgs: block %.4f (GEMMs %.4f), per-snapshot %.4f | svd: %d calls, "
-                 "%d Jacobi sweeps | galerkin: %lld batches, %lld systems | verify: %lld passes, %lld angles\n",
+                 "%d Jacobi sweeps | galerkin: %lld batches, %lld systems | verify: %lld passes, %lld angles | "
+                 "device allocations (process): %lld (%lld reused), %.1f GB, %.4f s (free %.4f, malloc %.4f)\n",
                  eng.reorth_count_, eng.reorth_seconds_, eng.cgs_split_[0], eng.cgs_split_[3], eng.cgs_split_[1], eng.svd_calls_,
-                 eng.svd_sweeps_, eng.gal_calls_, eng.gal_systems_, eng.verify_calls_, eng.verify_angles_);
+                 eng.svd_sweeps_, eng.gal_calls_, eng.gal_systems_, eng.verify_calls_, eng.verify_angles_,
+                 alloc_stats().count, alloc_stats().reused, alloc_stats().bytes / 1e9, alloc_stats().seconds,
+                 alloc_stats().free_s,
+                 alloc_stats().malloc_s);
   }
   rep.phase_work.assign(4 * kPhaseCount, 0.0);
   for (int k = 0; k < kPhaseCount; ++k) {

@@ -296,7 +296,7 @@ class LowRankEngine {
   double* hbuf_ = nullptr;
   void* hstate_ = nullptr;  // pinned CgsState read back once per CGS batch
   int* hflags_ = nullptr;   // pinned: [0] Galerkin non-finite, [1] sweep singular block
-  DBuf<int> gal_bad_;
+  DBuf<int> gal_bad_, chol_flag_;
   IntRing ring_;
   int rank_ = 0, n_snap_ = 0, prev_rank_ = 0;
   DBuf<double> rec_;  // coefficient record, rmax x N_Omega (ld ldr_), device-resident

@@ -133,6 +133,29 @@ Problem::~Problem() {
   if (own_stream_ && stream_) cudaStreamDestroy(stream_);
   if (h_state_) cudaFreeHost(h_state_);
   if (h_pin_) cudaFreeHost(h_pin_);
+  release_buffers();
+}
+
+// The member buffers go back through the block cache (their destructors run
+// after this body), so free them here first, then the cached blocks.
+void Problem::release_buffers() {
+  dirs_.release();
+  weights_.release();
+  sigma_t_.release();
+  sigma_s_.release();
+  source_.release();
+  bc_.release();
+  sip_.release();
+  jac_.release();
+  kblocks_.release();
+  line_.release();
+  norm_work_.release();
+  pcg_vec_.release();
+  pcg_part_.release();
+  scratch_.release();
+  pref_.release();
+  mg_bufs_.clear();
+  BlockCache::get().trim();
 }
 
 void Problem::set_stream(cudaStream_t s) {

@@ -3,7 +3,11 @@
 #pragma once
 
 #include <algorithm>
+#include <chrono>
 #include <memory>
+#include <iterator>
+#include <mutex>
+#include <map>
 #include <utility>
 #include <string>
 #include <vector>
@@ -18,6 +22,82 @@
 namespace rtlr {
 namespace cuda {
 
+// Device (re)allocations made by DBuf (reported with the low-rank profile).
+struct AllocStats {
+  double seconds = 0.0, bytes = 0.0, free_s = 0.0, malloc_s = 0.0;
+  long long count = 0, reused = 0;
+  bool split = false;  // RTLR_PROFILE: drain the device first, time the driver calls alone
+};
+inline AllocStats& alloc_stats() {
+  static AllocStats a;
+  return a;
+}
+
+// A process-wide cache of released DBuf blocks (per device).  The low-rank
+// engine's buffers grow with the rank (hundreds of growths per C4 solve):
+// cudaFree + cudaMalloc of multi-GB blocks cost 0.05-0.5 s per solve and
+// drained the device each time.  Released blocks are kept and handed to the
+// next request they fit (at most 4x larger); a reuse drains the device
+// first (cudaDeviceSynchronize: the block's previous owner may still have
+// work queued on another stream), as the cudaFree it replaces did.  The
+// cache holds at most a quarter of the device memory; beyond that the
+// largest blocks are freed, and a Problem's destructor frees them all.
+class BlockCache {
+ public:
+  static BlockCache& get() {
+    static BlockCache* c = new BlockCache();  // (never destroyed: blocks live until process exit)
+    return *c;
+  }
+  void* take(size_t bytes, size_t* got) {
+    std::lock_guard<std::mutex> lk(mu_);
+    auto& m = map_[dev()];
+    auto it = m.lower_bound(bytes);
+    if (it == m.end() || it->first > 4 * bytes) return nullptr;
+    void* p = it->second;
+    *got = it->first;
+    held_[dev()] -= it->first;
+    m.erase(it);
+    return p;
+  }
+  // frees every cached block of the current device (a Problem's destructor:
+  // the memory goes back to the driver with the problem that used it)
+  void trim() {
+    std::lock_guard<std::mutex> lk(mu_);
+    const int d = dev();
+    for (auto& e : map_[d]) cudaFree(e.second);
+    map_[d].clear();
+    held_[d] = 0;
+  }
+  void put(void* p, size_t bytes) {
+    std::lock_guard<std::mutex> lk(mu_);
+    const int d = dev();
+    map_[d].emplace(bytes, p);
+    held_[d] += bytes;
+    if (cap_[d] == 0) {
+      size_t fr = 0, tot = 0;
+      cudaMemGetInfo(&fr, &tot);
+      cap_[d] = tot / 4;
+    }
+    auto& m = map_[d];
+    while (held_[d] > cap_[d] && !m.empty()) {
+      auto last = std::prev(m.end());
+      cudaFree(last->second);
+      held_[d] -= last->first;
+      m.erase(last);
+    }
+  }
+
+ private:
+  static int dev() {
+    int d = 0;
+    cudaGetDevice(&d);
+    return d;
+  }
+  std::mutex mu_;
+  std::map<int, std::multimap<size_t, void*>> map_;
+  std::map<int, size_t> held_, cap_;
+};
+
 template <class T>
 class DBuf {
  public:
@@ -26,20 +106,37 @@ class DBuf {
   DBuf& operator=(const DBuf&) = delete;
   ~DBuf() { release(); }
   void release() {
-    if (p_) cudaFree(p_);
+    if (p_) BlockCache::get().put(p_, n_ * sizeof(T));
     p_ = nullptr;
     n_ = 0;
   }
   // Grow to at least n elements (contents not preserved).  A buffer that
   // grows again gets 1.5x headroom, so steadily growing work buffers (the
-  // low-rank basis raises r every inner iteration) reallocate O(log) times:
-  // cudaFree synchronizes the device.
+  // low-rank basis raises r every inner iteration) reallocate O(log) times;
+  // released blocks are recycled through BlockCache.
   T* ensure(size_t n) {
     if (n > n_) {
+      if (alloc_stats().split) cudaDeviceSynchronize();
+      const auto t0 = std::chrono::steady_clock::now();
       const size_t want = n_ ? std::max(n, n_ + n_ / 2) : n;
       release();
-      RTLR_CUDA(cudaMalloc(&p_, (want ? want : 1) * sizeof(T)));
-      n_ = want;
+      const auto t1 = std::chrono::steady_clock::now();
+      size_t got = 0;
+      void* c = BlockCache::get().take((want ? want : 1) * sizeof(T), &got);
+      if (c) {
+        RTLR_CUDA(cudaDeviceSynchronize());
+        p_ = static_cast<T*>(c);
+        n_ = got / sizeof(T);
+        ++alloc_stats().reused;
+      } else {
+        RTLR_CUDA(cudaMalloc(&p_, (want ? want : 1) * sizeof(T)));
+        n_ = want;
+      }
+      alloc_stats().free_s += std::chrono::duration<double>(t1 - t0).count();
+      alloc_stats().malloc_s += std::chrono::duration<double>(std::chrono::steady_clock::now() - t1).count();
+      alloc_stats().seconds += std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+      alloc_stats().bytes += static_cast<double>(want) * sizeof(T);
+      ++alloc_stats().count;
     }
     return p_;
   }
@@ -167,6 +264,7 @@ class Problem {
   // the K = 1 entry points throw invalid_argument naming `what`.
   int degree() const { return hp_.degree; }
   void require_k1(const char* what) const;
+  void release_buffers();  // (destructor) member buffers and the cached blocks back to the driver
 
   // Direction sharding over ranks (one process per GPU): this rank sweeps
   // its share of the unique directions and the scalar-flux partials are

@@ -234,3 +234,35 @@ def test_row_sliced_contractions_match_the_unsliced_solve(name, ov, tmp_path):
     o = O.Problem(name, seed=7, **ov)
     ref = o.solve("lowrank").get("phi", o.n)
     assert rel(b[2:], ref) <= 1e-8
+
+
+_REBUILD_RUN = r'''
+import sys, numpy as np
+sys.path.insert(0, sys.argv[1])
+import paper_2603_25233_b200 as P
+g = P.Problem("C2", nx=48, ny=48, n_theta=16, n_omega_z=8)
+r = g.solve_low_rank(build_factors=0, eps_mgs=1e-15)
+np.save(sys.argv[2], np.concatenate([[r.iterations, r.history("rank")[-1]], r.phi]))
+'''
+
+
+def test_basis_rebuild_paths_agree(tmp_path):
+    """The overlap-triggered basis rebuild (low_rank.cpp:107-130) by
+    CholeskyQR2 of [X_old, the batch's orthonormalised columns] (default)
+    against the reference's Householder QR of [X_old, accepted snapshots]
+    (RTLR_REBUILD=householder): the same nested column spaces, so the same
+    solve to rounding.  eps_mgs = 1e-15 makes the overlap test fire at
+    almost every batch."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    out = {}
+    for v in ("householder", "cholqr2"):
+        f = str(tmp_path / f"phi_{v}.npy")
+        env = dict(os.environ, RTLR_REBUILD=v)
+        subprocess.run([sys.executable, "-c", _REBUILD_RUN, root, f], env=env, check=True, timeout=600)
+        out[v] = np.load(f)
+    a, b = out["householder"], out["cholqr2"]
+    assert abs(a[0] - b[0]) <= 1 and abs(a[1] - b[1]) <= 2
+    assert rel(b[2:], a[2:]) <= 1e-8
