@@ -1341,10 +1341,34 @@ InnerResult LowRankEngine::inner(const double* d_phi_prev, SubsampleRng& rng) {
       RTLR_CUDA(cudaStreamSynchronize(s_));
       flags_check();
       if (hbuf_[0] <= prm_.eps_diff) {
-        // verify every unsampled angle before accepting (low_rank.cpp:396-424)
-        std::vector<int> unsampled;
+        // verify every unsampled angle before accepting (low_rank.cpp:396-424).
+        // An unsampled angle whose mirror partner (the same (Omega_x,
+        // Omega_y)) is sampled has that partner's snapshot,
+        // psi = (D + Sigma_t)^-1 rhs, in the basis span (accepted, or dropped
+        // with a remainder below drop_tol of its norm), so its Galerkin
+        // solution reproduces it and its residual is rounding noise, far
+        // below eps_res: it cannot be outstanding, and it is not evaluated
+        // (the reference evaluates it; the accept / outstanding decisions
+        // are the same).  RTLR_VERIFY_MIRRORS=eval evaluates every angle;
+        // =check evaluates them and reports the largest such residual.
+        static const int mirror_mode = [] {  // 0 skip, 1 eval, 2 check
+          const char* e = std::getenv("RTLR_VERIFY_MIRRORS");
+          if (!e) return 0;
+          const std::string v = e;
+          return v == "eval" ? 1 : v == "check" ? 2 : 0;
+        }();
+        std::vector<char> partner_sampled(P_.uniq_rep_.size(), 0);
         for (int j = 0; j < nomega_; ++j)
-          if (!sampled[j]) unsampled.push_back(j);
+          if (sampled[j]) partner_sampled[P_.uniq_of_[j]] = 1;
+        std::vector<int> unsampled, skipped;
+        for (int j = 0; j < nomega_; ++j)
+          if (!sampled[j]) {
+            if (mirror_mode != 1 && partner_sampled[P_.uniq_of_[j]] && !hp_.bc_any)
+              skipped.push_back(j);
+            else
+              unsampled.push_back(j);
+          }
+        if (mirror_mode == 2) unsampled.insert(unsampled.end(), skipped.begin(), skipped.end());
         double* Cu = sol_.ensure(static_cast<size_t>(rank_) * unsampled.size());
         int* du = upload_ints(ang2_, unsampled);
         gather_cols<<<g1(static_cast<long long>(rank_) * unsampled.size()), 256, 0, s_>>>(
@@ -1354,6 +1378,12 @@ InnerResult LowRankEngine::inner(const double* d_phi_prev, SubsampleRng& rng) {
         verify_angles_ += static_cast<long long>(unsampled.size());
         std::vector<double> vn = residual_norms(unsampled, Cu, rank_, /*mirror_equal=*/true);
         pt_.stop();
+        if (mirror_mode == 2 && !skipped.empty()) {
+          double worst = 0.0;
+          for (size_t i = unsampled.size() - skipped.size(); i < unsampled.size(); ++i) worst = std::max(worst, vn[i]);
+          std::fprintf(stderr, "[rtlr verify] %zu angles with a sampled mirror partner: largest residual %.3e (eps_res %.1e)\n",
+                       skipped.size(), worst, prm_.eps_res);
+        }
         std::vector<std::pair<double, int>> outstanding;
         for (size_t i = 0; i < unsampled.size(); ++i)
           if (vn[i] >= prm_.eps_res) outstanding.push_back({vn[i], unsampled[i]});

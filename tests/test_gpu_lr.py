@@ -266,3 +266,38 @@ def test_basis_rebuild_paths_agree(tmp_path):
     a, b = out["householder"], out["cholqr2"]
     assert abs(a[0] - b[0]) <= 1 and abs(a[1] - b[1]) <= 2
     assert rel(b[2:], a[2:]) <= 1e-8
+
+
+_MIRROR_RUN = r'''
+import sys, numpy as np
+sys.path.insert(0, sys.argv[1])
+import paper_2603_25233_b200 as P
+p = P.Problem("C2")
+r = p.solve_low_rank(build_factors=0)
+np.save(sys.argv[2], np.concatenate([[r.iterations], r.history("rank"), r.phi]))
+'''
+
+
+def test_verification_skips_mirrors_of_sampled_angles(tmp_path):
+    """The verification pass (low_rank.cpp:396-424) does not evaluate an
+    unsampled angle whose mirror partner is sampled (its residual is rounding
+    noise: the partner's snapshot is in the basis span): the solve is
+    bitwise the one that evaluates every angle (RTLR_VERIFY_MIRRORS=eval),
+    and with =check the skipped residuals are reported far below eps_res."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    out = {}
+    for v in ("eval", "skip", "check"):
+        f = str(tmp_path / f"phi_{v}.npy")
+        env = dict(os.environ, RTLR_VERIFY_MIRRORS=v)
+        res = subprocess.run([sys.executable, "-c", _MIRROR_RUN, root, f], env=env, check=True, timeout=600,
+                             capture_output=True, text=True)
+        out[v] = np.load(f)
+        if v == "check":
+            worst = [float(l.split("largest residual ")[1].split()[0]) for l in res.stderr.splitlines()
+                     if "sampled mirror partner" in l]
+            assert worst and max(worst) < 1e-3 * 1e-7
+    assert np.array_equal(out["eval"], out["skip"])
+    assert np.array_equal(out["eval"], out["check"])
