@@ -1208,6 +1208,36 @@ void LowRankEngine::build_full_coefficients(const std::vector<int>* cand, const 
                                                                              r, C, r);
     }
   }
+  // An angle whose mirror partner (the same (Omega_x, Omega_y)) has a
+  // record column takes that column: the partner's snapshot is the angle's
+  // own transport solution and lies in the basis span, so the angle's
+  // Galerkin solution is that column up to rounding (the reference solves
+  // it; the verification residuals of such angles are ~1e-12 at C2-C4).
+  // RTLR_BUILDC_MIRRORS=solve solves them as the reference does.
+  static const bool copy_mirrors = [] {
+    const char* e = std::getenv("RTLR_BUILDC_MIRRORS");
+    return !(e && std::string(e) == "solve");
+  }();
+  if (copy_mirrors && !hp_.bc_any && n_snap_ > 0) {
+    std::vector<int> src_of(P_.uniq_rep_.size(), -1);
+    for (int i = 0; i < n_snap_; ++i) src_of[P_.uniq_of_[sampled_[i]]] = sampled_[i];
+    std::vector<int> to, from;
+    for (int j = 0; j < nomega_; ++j)
+      if (!done[j] && src_of[P_.uniq_of_[j]] >= 0) {
+        to.push_back(j);
+        from.push_back(src_of[P_.uniq_of_[j]]);
+        done[j] = 1;
+      }
+    if (!to.empty()) {
+      double* tmpc = ybuf_.ensure(static_cast<size_t>(r) * to.size());
+      int* df = upload_ints(ang_, from);
+      gather_cols<<<g1(static_cast<long long>(r) * from.size()), 256, 0, s_>>>(r, static_cast<int>(from.size()), df, C,
+                                                                              r, tmpc, r);
+      int* dt = upload_ints(ang2_, to);
+      scatter_cols<<<g1(static_cast<long long>(r) * to.size()), 256, 0, s_>>>(r, static_cast<int>(to.size()), dt, tmpc,
+                                                                             r, C, r);
+    }
+  }
   std::vector<int> rest;
   for (int j = 0; j < nomega_; ++j)
     if (!done[j]) rest.push_back(j);
