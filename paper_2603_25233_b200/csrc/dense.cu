@@ -2339,8 +2339,13 @@ void gemm_nn(long long M, int N, int K, const double* A, long long lda, const do
     const char* e = std::getenv("RTLR_NN_NT");
     return e && e[0] == '0';
   }();
-  // (N = 8 with the pipeline's alignment — the CGS block updates — takes the DMMA tiles below)
-  if ((N <= 8 && !(pipe_ok && !nt_off && N == 8)) || (N <= kSkinny && !pipe_ok)) {
+  // (4 <= N <= 8, e.g. C2's p = 4 CGS updates: the FFMA skinny kernel's 512-row CTAs left the
+  // GPU under-filled at N_x = 65536: 65 -> 25 us at r = 220, C2 LR ~3% faster)
+  static const int nt_min_n = [] {  // RTLR_NN_NT_MIN=n: narrowest N on the DMMA tiles (A/B timing)
+    const char* e = std::getenv("RTLR_NN_NT_MIN");
+    return e && std::atoi(e) > 0 ? std::atoi(e) : 4;
+  }();
+  if ((N <= 8 && !(pipe_ok && !nt_off && N >= nt_min_n)) || (N <= kSkinny && !pipe_ok)) {
     if (aligned16(A) && lda % 2 == 0) {
       const unsigned grid = static_cast<unsigned>((M + 511) / 512);
       if (N == 1) gemm_nn_skinny2<1><<<grid, 256, 0, s>>>(M, N, K, A, lda, B, ldb, C, ldc, subtract);
