@@ -2434,16 +2434,29 @@ void stream_products(const StencilArgs& a, int p, const double* P, long long ldp
   RTLR_CUDA(cudaGetLastError());
 }
 
+int lu_smem_max(int m) {
+  static const int small_max = [] {  // RTLR_LU_SMEM_SMALL=n: the threshold for small batches (A/B timing)
+    const char* e = std::getenv("RTLR_LU_SMEM_SMALL");
+    return e ? std::max(0, std::min(kSmemLuMax, std::atoi(e))) : kSmemLuMaxSmall;
+  }();
+  return m <= kSmemLuSmallBatch ? small_max : kSmemLuMax;
+}
+
+size_t galerkin_work_per_system(int r) {
+  return static_cast<size_t>(r) * (r + 1) + r + (kPermInts + 1) / 2 + 1;
+}
+
 size_t galerkin_work_doubles(int r, int m) {
-  if (r <= kSmemLuMax) return 0;
-  return static_cast<size_t>(m) * (static_cast<size_t>(r) * (r + 1) + r + (kPermInts + 1) / 2 + 1);
+  if (r <= lu_smem_max(m)) return 0;
+  return static_cast<size_t>(m) * galerkin_work_per_system(r);
 }
 
 void galerkin_batch(int r, int m, const int* angles, const double* dirs, const double* proj, long long ldp,
                     long long proj_stride, const double* prhs, const double* extra, double* sol, long long ldsol,
                     int* flags, double* work, cudaStream_t s) {
   if (m <= 0 || r <= 0) return;
-  if (r > kSmemLuMax) {
+  const int smem_max = lu_smem_max(m);
+  if (r > smem_max) {
     double* M = work;
     int* piv = reinterpret_cast<int*>(work + static_cast<size_t>(m) * r * (r + 1));
     int* perm = reinterpret_cast<int*>(work + static_cast<size_t>(m) * (r * static_cast<size_t>(r + 1) + r));
@@ -2499,7 +2512,7 @@ void galerkin_batch(int r, int m, const int* angles, const double* dirs, const d
     RTLR_CUDA(cudaGetLastError());
     return;
   }
-  const bool in_smem = r <= kSmemLuMax;
+  const bool in_smem = r <= smem_max;
   const size_t smem = in_smem ? static_cast<size_t>(r) * r * sizeof(double) : 0;
   if (in_smem)
     RTLR_CUDA(cudaFuncSetAttribute(galerkin_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,

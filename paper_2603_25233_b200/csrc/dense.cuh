@@ -45,7 +45,15 @@ void stream_products(const StencilArgs& a, int p, const double* P, long long ldp
 // sol: r x m (ldsol); extra optional r x m (Xt g_j).  flags[j] = 1 if the
 // solution is not finite.  work >= m * r * r doubles for r > kSmemLuMax.
 constexpr int kSmemLuMax = 96;
+// Small batches (m <= 64, the greedy candidates) switch to the blocked path
+// above r = 64 (tools/lu_bench, 16 systems: the one-CTA shared-memory LU is
+// faster up to r = 40, equal at 64, 13% slower at 80, 30% at 96, 2.2x at
+// 160); larger batches switch at 96.
+constexpr int kSmemLuMaxSmall = 64, kSmemLuSmallBatch = 64;
+// (RTLR_LU_SMEM_SMALL=0: 96 for every batch)
+int lu_smem_max(int m);
 size_t galerkin_work_doubles(int r, int m);
+size_t galerkin_work_per_system(int r);  // the blocked path's workspace per system
 void galerkin_batch(int r, int m, const int* angles, const double* dirs, const double* proj, long long ldp,
                     long long proj_stride, const double* prhs, const double* extra, double* sol,
                     long long ldsol, int* flags, double* work, cudaStream_t s);

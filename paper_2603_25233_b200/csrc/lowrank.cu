@@ -1070,7 +1070,7 @@ void LowRankEngine::galerkin_solve(const std::vector<int>& angles, double* d_sol
     const char* e = std::getenv("RTLR_GAL_CHUNK_MB");
     return (e && std::atoll(e) > 0 ? std::atoll(e) : 4096LL) << 20;
   }();
-  const long long per_system = static_cast<long long>(galerkin_work_doubles(rank_, 1)) * sizeof(double);
+  const long long per_system = static_cast<long long>(galerkin_work_per_system(rank_)) * sizeof(double);
   const int chunk = rank_ > kSmemLuMax
                         ? static_cast<int>(std::min<long long>(65535, std::max<long long>(1, budget_bytes / per_system)))
                         : 4096;
@@ -1102,7 +1102,8 @@ void LowRankEngine::galerkin_solve(const std::vector<int>& angles, double* d_sol
       const double r = rank_;
       pt_.work(8.0 * mc * r * (r + 1) * 2.0, mc * (2.0 / 3.0 * r * r * r + 2.0 * r * r + 5.0 * r * r));
     }
-    double* lw = rank_ > kSmemLuMax ? luw_.ensure(galerkin_work_doubles(rank_, mc)) : nullptr;
+    const size_t lwn = galerkin_work_doubles(rank_, mc);
+    double* lw = lwn ? luw_.ensure(lwn) : nullptr;
     galerkin_batch(rank_, mc, d_ang, dirs_, proj_.get(), ldp_, ldp_ * ldp_, prhs_.get(), extra, out, ldsol, flags, lw,
                    s_);
     or_flags_kernel<<<1, 256, 0, s_>>>(mc, flags, gal_bad_.get());
