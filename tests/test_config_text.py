@@ -110,3 +110,15 @@ def test_cli_reports_config_errors(tmp_path):
     assert r.returncode == 3
     r = subprocess.run([cli, "presets"], capture_output=True, text=True, timeout=120)
     assert r.returncode == 0 and "pin_cell" in r.stdout and "C4" in r.stdout
+
+
+def test_degree_key_assembles_a_general_degree_problem():
+    """`space.degree = 2` in a config file (the reference's DG degree key,
+    problem.cpp) assembles the quadratic-element problem the keyword
+    override does (host_dgk.cpp)."""
+    text = "preset = pin_cell\nmesh.nx = 6\nmesh.ny = 5\nspace.degree = 2\n"
+    a = P.Problem(config_text=text, device=-1)
+    b = P.Problem("pin_cell", device=-1, nx=6, ny=5, degree=2)
+    assert (a.degree, a.dofs_per_cell, a.n) == (2, 9, 9 * 30)
+    for w in ("dirs", "weights", "source", "sigma_t_blocks", "sigma_s_blocks", "sigma_a_blocks", "stream_blocks"):
+        assert np.array_equal(a.get(w), b.get(w)), w
