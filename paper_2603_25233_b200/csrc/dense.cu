@@ -1501,6 +1501,165 @@ __global__ void __launch_bounds__(256) bidiag_coop(int m, int n, double* __restr
   }
 }
 
+// The same bidiagonalisation with the reflector applications laid out for
+// memory-level parallelism (bidiag_coop's loops carried one dependent L2
+// load per iteration: ~90 us per column at 2048 x 600).  Left reflector: a
+// team of T warps per trailing column, each lane holding its <= 32 rows of
+// the column in registers between the dot product and the update (one load
+// round).  Right reflector: a CTA per 8-row block, its 32 column groups
+// keeping the row block's entries in registers, the row products reduced in
+// shared memory, so no partials cross CTAs: two grid barriers per column
+// (bidiag_coop: three).  n <= 1024 and m <= 8192 (one register round each).
+constexpr int kBdRegs = 32, kBdRows = 8;
+__global__ void __launch_bounds__(256, 2) bidiag_coop2(int m, int n, double* __restrict__ A, long long lda,
+                                                       double* __restrict__ d, double* __restrict__ e) {
+  namespace cg = cooperative_groups;
+  cg::grid_group grid = cg::this_grid();
+  extern __shared__ double bd_sm[];
+  double* v = bd_sm;      // m: left reflector
+  double* u = bd_sm + m;  // n: right reflector
+  __shared__ double red[32];
+  __shared__ double part[256];  // left: one partial per warp; right: [column group][row]
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  const int nwarps = gridDim.x * 8;
+  for (int k = 0; k < n; ++k) {
+    // ---- left reflector of column k (rows k..m-1), applied to columns k+1..n-1
+    const double* ck = A + static_cast<long long>(k) * lda;
+    double t2 = 0.0;
+    for (int i = k + 1 + tid; i < m; i += blockDim.x) t2 += ck[i] * ck[i];
+    t2 = block_sum_all(t2, red);
+    double beta, tau, den;
+    hh_params(ck[k], t2, beta, tau, den);
+    for (int i = k + tid; i < m; i += blockDim.x) v[i] = i == k ? 1.0 : (den != 0.0 ? ck[i] / den : 0.0);
+    __syncthreads();
+    if (blockIdx.x == 0 && tid == 0) d[k] = beta;
+    const int ncols = n - k - 1;
+    if (tau != 0.0 && ncols > 0) {
+      int T = 8;  // warps per column: as many as the grid holds, at least enough for one register round
+      while (T > 1 && ncols * T > nwarps) T >>= 1;
+      while (T < 8 && m - k > 32 * kBdRegs * T) T <<= 1;
+      const int per_cta = 8 / T, ngroups = (ncols + per_cta - 1) / per_cta;
+      const int slot = wid / T, t = wid % T;
+      for (int g = blockIdx.x; g < ngroups; g += gridDim.x) {
+        const int j = k + 1 + g * per_cta + slot;
+        const bool live = j < n;
+        double* cj = A + static_cast<long long>(live ? j : k) * lda;
+        double c[kBdRegs];
+        double w = 0.0;
+#pragma unroll
+        for (int s = 0; s < kBdRegs; ++s) {
+          const int i = k + lane + 32 * (t + T * s);
+          c[s] = (live && i < m) ? cj[i] : 0.0;
+        }
+#pragma unroll
+        for (int s = 0; s < kBdRegs; ++s) {
+          const int i = k + lane + 32 * (t + T * s);
+          if (i < m) w += v[i] * c[s];
+        }
+        w = warp_sum(w);
+        if (lane == 0) part[wid] = w;
+        __syncthreads();
+        double wt = 0.0;
+        for (int q = 0; q < T; ++q) wt += part[slot * T + q];  // fixed order
+        const double tw = tau * wt;
+        if (live) {
+#pragma unroll
+          for (int s = 0; s < kBdRegs; ++s) {
+            const int i = k + lane + 32 * (t + T * s);
+            if (i < m) cj[i] = c[s] - tw * v[i];
+          }
+        }
+        __syncthreads();
+      }
+    }
+    grid.sync();
+    if (k + 1 >= n) break;
+    // ---- right reflector of row k (columns k+1..n-1), applied to rows k+1..m-1
+    double s2 = 0.0;
+    for (int j = k + 2 + tid; j < n; j += blockDim.x) {
+      const double x = A[k + static_cast<long long>(j) * lda];
+      s2 += x * x;
+    }
+    s2 = block_sum_all(s2, red);
+    double beta2, tau2, den2;
+    hh_params(A[k + static_cast<long long>(k + 1) * lda], s2, beta2, tau2, den2);
+    for (int j = k + 1 + tid; j < n; j += blockDim.x)
+      u[j] = j == k + 1 ? 1.0 : (den2 != 0.0 ? A[k + static_cast<long long>(j) * lda] / den2 : 0.0);
+    __syncthreads();
+    if (blockIdx.x == 0 && tid == 0) e[k] = beta2;
+    if (tau2 != 0.0) {
+      const int rows = m - k - 1, nrb = (rows + kBdRows - 1) / kBdRows;
+      const int ro = tid % kBdRows, grp = tid / kBdRows;  // 32 column groups
+      for (int rb = blockIdx.x; rb < nrb; rb += gridDim.x) {
+        const int i = k + 1 + rb * kBdRows + ro;
+        const bool live = i < m;
+        double c[kBdRegs];
+        double acc = 0.0;
+#pragma unroll
+        for (int s = 0; s < kBdRegs; ++s) {
+          const int j = k + 1 + grp + 32 * s;
+          c[s] = (live && j < n) ? A[i + static_cast<long long>(j) * lda] : 0.0;
+        }
+#pragma unroll
+        for (int s = 0; s < kBdRegs; ++s) {
+          const int j = k + 1 + grp + 32 * s;
+          if (j < n) acc += c[s] * u[j];
+        }
+        part[tid] = acc;  // = part[grp * kBdRows + ro]
+        __syncthreads();
+        double y = 0.0;
+        for (int q = 0; q < 32; ++q) y += part[q * kBdRows + ro];  // fixed order
+        const double ty = tau2 * y;
+        if (live) {
+#pragma unroll
+          for (int s = 0; s < kBdRegs; ++s) {
+            const int j = k + 1 + grp + 32 * s;
+            if (j < n) A[i + static_cast<long long>(j) * lda] = c[s] - ty * u[j];
+          }
+        }
+        __syncthreads();
+      }
+    }
+    grid.sync();
+  }
+}
+
+// The k-th smallest singular value by multisection of the Golub-Kahan
+// tridiagonal's Sturm counts: one warp per value, 32 points per round
+// (~11 rounds to full precision against ~60 bisection steps of a thread).
+__device__ int gk_count_below(int n, const double* __restrict__ d, const double* __restrict__ e, double x,
+                             double pivmin);
+__global__ void gk_multisect(int n, const double* __restrict__ d, const double* __restrict__ e,
+                             double* __restrict__ sv) {
+  const int lane = threadIdx.x & 31;
+  const int k = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;  // k-th smallest
+  if (k >= n) return;
+  double ub = 0.0, tmax = 0.0;
+  for (int j = lane; j < n; j += 32) {
+    const double a = fabs(d[j]), b = j + 1 < n ? fabs(e[j]) : 0.0, c = j > 0 ? fabs(e[j - 1]) : 0.0;
+    ub = fmax(ub, fmax(a + c, a + b));
+    tmax = fmax(tmax, fmax(a, b));
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    ub = fmax(ub, __shfl_xor_sync(0xffffffffu, ub, o));
+    tmax = fmax(tmax, __shfl_xor_sync(0xffffffffu, tmax, o));
+  }
+  const double pivmin = fmax(2.2250738585072014e-308, 2.2250738585072014e-308 * tmax * tmax);
+  double lo = 0.0, hi = ub * (1.0 + 4e-16) + pivmin;
+  for (int it = 0; it < 40 && hi - lo > 4e-16 * hi + pivmin; ++it) {
+    const double x = lo + (hi - lo) * ((lane + 1) / 33.0);
+    const bool above = gk_count_below(n, d, e, x, pivmin) - n > k;  // sigma_k < x
+    const unsigned mask = __ballot_sync(0xffffffffu, above);
+    const int first = mask ? __ffs(mask) - 1 : 32;  // first point above sigma_k
+    const double nhi = first < 32 ? __shfl_sync(0xffffffffu, x, first) : hi;
+    const double nlo = first > 0 ? __shfl_sync(0xffffffffu, x, first > 0 ? first - 1 : 0) : lo;
+    lo = nlo;
+    hi = nhi;
+  }
+  if (lane == 0) sv[n - 1 - k] = 0.5 * (lo + hi);  // descending
+}
+
 // Number of eigenvalues of the Golub-Kahan tridiagonal (zero diagonal,
 // off-diagonals d0, e0, d1, e1, ..., d_{n-1}) below x (Sturm count, LDL^T pivots).
 __device__ int gk_count_below(int n, const double* __restrict__ d, const double* __restrict__ e, double x,
@@ -1796,16 +1955,23 @@ template <int RPT>
 __global__ void __launch_bounds__(256, 1) lu_panel_reg(int r, int k0, int jb, double* __restrict__ M,
                                                        int* __restrict__ piv, int* __restrict__ perm) {
   constexpr int NT = 256, NW = NT / 32;
-  extern __shared__ double P[];  // rows x kNbMax finished entries (ld rows), then rows ints
+  extern __shared__ double P[];  // rows x kNbMax L entries (ld rows, by row tag), then rows ints
   __shared__ __align__(16) double cand[2][NW][kNbMax];
   __shared__ __align__(16) double rowj[2][kNbMax];
+  __shared__ double Ub[kNbMax][kNbMax + 1];  // the pivot rows' U parts, by final row
   __shared__ double shv[2][NW];
-  __shared__ int shi[2][NW];
+  __shared__ int shi[2][NW], candtag[2][NW], rowjtag[2];
   double* A = M + static_cast<size_t>(blockIdx.x) * r * (r + 1);
   int* pv = piv + static_cast<size_t>(blockIdx.x) * r;
   const int rows = r - k0, tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
-  // active parts; columns >= jb are zero and stay zero (the pivot row's are)
+  int* tag_at = reinterpret_cast<int*>(P + static_cast<size_t>(rows) * kNbMax);
+  // active parts; columns >= jb are zero and stay zero (the pivot row's are).
+  // tag: the panel row a slot's row started as; L entries are stored by tag,
+  // so a row swap moves no finished entries (they follow the tag at the end)
   double a[RPT][kNbMax];
+  int tag[RPT];
+#pragma unroll
+  for (int q = 0; q < RPT; ++q) tag[q] = tid + NT * q;
 #pragma unroll
   for (int c = 0; c < kNbMax; ++c)
 #pragma unroll
@@ -1846,11 +2012,13 @@ __global__ void __launch_bounds__(256, 1) lu_panel_reg(int r, int k0, int jb, do
         double2* dst = reinterpret_cast<double2*>(cand[buf][wid]);
 #pragma unroll
         for (int c = 0; c < kNbMax; c += 2) dst[c / 2] = make_double2(a[q][c], a[q][c + 1]);
+        candtag[buf][wid] = tag[q];
       }
       if (i == j) {
         double2* dst = reinterpret_cast<double2*>(rowj[buf]);
 #pragma unroll
         for (int c = 0; c < kNbMax; c += 2) dst[c / 2] = make_double2(a[q][c], a[q][c + 1]);
+        rowjtag[buf] = tag[q];
       }
     }
   };
@@ -1885,23 +2053,20 @@ __global__ void __launch_bounds__(256, 1) lu_panel_reg(int r, int k0, int jb, do
           a[q][c] = v.x;
           a[q][c + 1] = v.y;
         }
-      } else if (p != j && i == p) {  // row p <- row j, with the L parts swapped in P
+        tag[q] = candtag[buf][bw];
+      } else if (p != j && i == p) {  // row p <- row j (its L part follows the tag)
 #pragma unroll
         for (int c = 0; c < kNbMax; c += 2) {
           const double2 v = R2[c / 2];
           a[q][c] = v.x;
           a[q][c + 1] = v.y;
         }
-        for (int c = 0; c < j; ++c) {
-          const double t = P[j + c * rows];
-          P[j + c * rows] = P[p + c * rows];
-          P[p + c * rows] = t;
-        }
+        tag[q] = rowjtag[buf];
       }
       if (i == j)  // the pivot row's U part is final
 #pragma unroll
         for (int c = 0; c < kNbMax; ++c)
-          if (c < jb - j) P[j + (j + c) * rows] = a[q][c];
+          if (c < jb - j) Ub[j][j + c] = a[q][c];
     }
     const double d = U2[0].x;
     // rank-1 update of the rows below j (column order), then shift left
@@ -1910,7 +2075,7 @@ __global__ void __launch_bounds__(256, 1) lu_panel_reg(int r, int k0, int jb, do
       const int i = tid + NT * q;
       if (i > j && i < rows) {
         const double l = d != 0.0 ? a[q][0] / d : a[q][0];
-        P[i + j * rows] = l;
+        P[tag[q] + j * rows] = l;
 #pragma unroll
         for (int c = 2; c < kNbMax; c += 2) {
           const double2 u = U2[c / 2];
@@ -1926,12 +2091,132 @@ __global__ void __launch_bounds__(256, 1) lu_panel_reg(int r, int k0, int jb, do
     if (j + 1 < jb) publish(j + 1);
     __syncthreads();
   }
-  for (int e = tid; e < rows * jb; e += NT) {
-    const int i = e % rows, c = e / rows;
-    A[k0 + i + static_cast<size_t>(k0 + c) * r] = P[e];
+#pragma unroll
+  for (int q = 0; q < RPT; ++q) {
+    const int i = tid + NT * q;
+    if (i < rows) tag_at[i] = tag[q];
   }
-  lu_panel_perm(rows, k0, jb, pv, reinterpret_cast<int*>(P + static_cast<size_t>(rows) * kNbMax),
-                perm + static_cast<size_t>(blockIdx.x) * kPermInts);
+  __syncthreads();
+  for (int c = 0; c < jb; ++c)
+    for (int i = tid; i < rows; i += NT)
+      A[k0 + i + static_cast<size_t>(k0 + c) * r] = i <= c ? Ub[i][c] : P[tag_at[i] + c * rows];
+  __syncthreads();
+  lu_panel_perm(rows, k0, jb, pv, tag_at, perm + static_cast<size_t>(blockIdx.x) * kPermInts);
+}
+
+// Small batches (the q greedy candidates) up to r = kCtaLuMax: one CTA of
+// 1024 threads per system with [A | b] in shared memory.  Warp w owns the
+// columns j = w (mod 32), lane l the rows i = l (mod 32), so the rank-1
+// update walks static index sets (no division) and column k + 1 is one
+// warp's: its argmax is a shuffle reduction right after that warp updates
+// it.  Two barriers per column: (1) the pivot row moves to row k (staged in
+// prow) and the multipliers are formed; (2) the rank-1 update of the rows
+// below, the right-hand side included as column r.  L is not stored (the
+// forward substitution is the update of column r).  Back substitution by
+// 32 x 32 diagonal blocks (shuffle solve in warp 0, then one warp per row
+// above).  Pivot rule, all-zero column and singular-flag behaviour as
+// lu_solve_block.
+constexpr int kCtaLuMax = 160;
+__global__ void __launch_bounds__(1024, 1) galerkin_cta_lu(int r, const int* __restrict__ angles,
+                                                           const double* __restrict__ dirs,
+                                                           const double* __restrict__ proj, long long ldp,
+                                                           long long pstride, const double* __restrict__ prhs,
+                                                           const double* __restrict__ extra, double* __restrict__ sol,
+                                                           long long ldsol, int* __restrict__ flags) {
+  extern __shared__ double Am[];  // r x (r + 1), column-major, ld r
+  __shared__ double prow[kCtaLuMax + 1], lcol[kCtaLuMax];
+  __shared__ int sp;
+  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+  const int jb = blockIdx.x;
+  const int ang = angles[jb];
+  const double omx = dirs[3 * ang], omy = dirs[3 * ang + 1];
+  const double* px = proj + (omx >= 0.0 ? 0 : 1) * pstride;
+  const double* py = proj + (omy >= 0.0 ? 2 : 3) * pstride;
+  const double* pt = proj + 4 * pstride;
+  // reduced_streaming (low_rank.cpp:176-183): omx*Px + omy*Py + Pt, then the rhs column
+  for (int j = w; j < r; j += 32)
+    for (int i = lane; i < r; i += 32)
+      Am[i + j * r] = omx * px[i + j * ldp] + omy * py[i + j * ldp] + pt[i + j * ldp];
+  if (w == 0)
+    for (int i = lane; i < r; i += 32) Am[i + r * r] = prhs[i] + (extra ? extra[i + jb * ldsol] : 0.0);
+  __syncthreads();
+  auto argmax_col = [&](int c) {  // warp c % 32: first maximum of |A[i, c]|, i >= c
+    double best = -1.0;
+    int bi = r;
+    for (int i = c + ((lane - c) & 31); i < r; i += 32) {  // ascending rows of this lane >= c
+      const double v = fabs(Am[i + c * r]);
+      if (v > best) {
+        best = v;
+        bi = i;
+      }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) argmax_merge(best, bi, __shfl_xor_sync(0xffffffffu, best, o),
+                                                  __shfl_xor_sync(0xffffffffu, bi, o));
+    if (lane == 0) sp = best > 0.0 ? bi : c;  // all-zero column: no swap
+  };
+  if (w == 0) argmax_col(0);
+  __syncthreads();
+  for (int k = 0; k < r; ++k) {
+    const int p = sp;
+    const double d = Am[p + k * r];
+    // (1) pivot row -> row k (columns > k; prow keeps it), old row k -> row p;
+    // multipliers from column k as the swap leaves it (column k is not written here)
+    for (int j = k + 1 + tid; j <= r; j += 1024) {
+      const double pr = Am[p + j * r];
+      prow[j] = pr;
+      if (p != k) {
+        Am[p + j * r] = Am[k + j * r];
+        Am[k + j * r] = pr;
+      }
+    }
+    for (int i = k + 1 + tid; i < r; i += 1024) {
+      const double a = i == p ? Am[k + k * r] : Am[i + k * r];
+      lcol[i] = d != 0.0 ? a / d : a;
+    }
+    __syncthreads();
+    if (tid == 0) Am[k + k * r] = d;
+    // (2) rank-1 update of rows > k, columns > k (column r: the forward substitution)
+    const int j0 = w + 32 * ((k + 1 - w + 31) >> 5);  // first column of this warp > k
+    const int i0 = lane + 32 * ((k + 1 - lane + 31) >> 5);
+    for (int j = j0; j <= r; j += 32) {
+      const double u = prow[j];
+      for (int i = i0; i < r; i += 32) Am[i + j * r] -= lcol[i] * u;
+    }
+    if (k + 1 < r && w == ((k + 1) & 31)) {
+      __syncwarp();
+      argmax_col(k + 1);
+    }
+    __syncthreads();
+  }
+  // back substitution: y = column r, U upper (diagonal in place)
+  double* y = Am + static_cast<size_t>(r) * r;
+  for (int b0 = ((r - 1) / 32) * 32; b0 >= 0; b0 -= 32) {
+    const int bs = min(32, r - b0);
+    if (w == 0) {
+      double x = lane < bs ? y[b0 + lane] : 0.0;
+      for (int i = bs - 1; i >= 0; --i) {
+        const double xi = __shfl_sync(0xffffffffu, x, i) / Am[b0 + i + (b0 + i) * r];
+        if (lane == i) x = xi;
+        if (lane < i) x -= xi * Am[b0 + lane + (b0 + i) * r];
+      }
+      if (lane < bs) y[b0 + lane] = x;
+    }
+    __syncthreads();
+    for (int row = w; row < b0; row += 32) {
+      double v = lane < bs ? Am[row + (b0 + lane) * r] * y[b0 + lane] : 0.0;
+      v = warp_sum(v);
+      if (lane == 0) y[row] -= v;
+    }
+    __syncthreads();
+  }
+  int bad = 0;
+  for (int i = tid; i < r; i += 1024) {
+    sol[i + jb * ldsol] = y[i];
+    if (!isfinite(y[i])) bad = 1;
+  }
+  bad = __syncthreads_or(bad);
+  if (tid == 0) flags[jb] = bad;
 }
 
 // For one 64-column tile of the trailing columns (k0+jb .. r, the last one
@@ -2129,6 +2414,72 @@ __global__ void __launch_bounds__(256) lu_backsolve_cta(int r, const double* __r
   const int sys = blockIdx.x;
   const double* A = M + static_cast<size_t>(sys) * r * (r + 1);
   for (int i = tid; i < r; i += blockDim.x) xs[i] = A[i + static_cast<size_t>(r) * r];
+  if (r > 64) {
+    // Look-ahead form for long solves: warp 0 updates the next diagonal
+    // block's 32 rows first and solves that block (reciprocal pivots, formed
+    // off the chain) while warps 1-7 update the rows above it; the next
+    // diagonal block is staged by warps 1-7 too.  One barrier per block.
+    double* ub2 = ub + 32 * 33;  // double buffer of the diagonal block
+    double* rinv = ub2 + 32 * 33;  // 2 x 32 reciprocal pivots
+    const int nb = (r + 31) / 32;
+    auto stage = [&](int b, int t0, int nt) {  // diagonal block b and its reciprocals
+      const int i0 = b * 32, bs = min(32, r - i0);
+      double* u = (b & 1) ? ub2 : ub;
+      for (int e = t0; e < bs * bs; e += nt) {
+        const int j = e % bs, i = e / bs;
+        u[j * 33 + i] = A[i0 + j + static_cast<size_t>(i0 + i) * r];
+      }
+      for (int i = t0; i < bs; i += nt) rinv[(b & 1) * 32 + i] = 1.0 / A[i0 + i + static_cast<size_t>(i0 + i) * r];
+    };
+    auto solve_diag = [&](int b) {  // warp 0
+      const int i0 = b * 32, bs = min(32, r - i0);
+      const double* u = (b & 1) ? ub2 : ub;
+      const double ri = lane < bs ? rinv[(b & 1) * 32 + lane] : 0.0;
+      double x = lane < bs ? xs[i0 + lane] : 0.0;
+      for (int i = bs - 1; i >= 0; --i) {
+        const double xi = __shfl_sync(0xffffffffu, x * ri, i);
+        if (lane == i) x = xi;
+        if (lane < i) x -= xi * u[lane * 33 + i];
+      }
+      if (lane < bs) xs[i0 + lane] = x;
+    };
+    auto update_rows = [&](int row_beg, int row_end, int b, int t0, int nt) {  // rows -= U[rows][block b] x_b
+      const int i0 = b * 32, bs = min(32, r - i0);
+      const double* xb = xs + i0;
+      for (int row = row_beg + t0; row < row_end; row += nt) {
+        const double* ar = A + row + static_cast<size_t>(i0) * r;
+        double acc = 0.0;
+        if (bs == 32) {
+          double v[32];
+#pragma unroll
+          for (int l = 0; l < 32; ++l) v[l] = ar[static_cast<size_t>(l) * r];
+#pragma unroll
+          for (int l = 0; l < 32; ++l) acc += v[l] * xb[l];
+        } else {
+          for (int l = 0; l < bs; ++l) acc += ar[static_cast<size_t>(l) * r] * xb[l];
+        }
+        xs[row] -= acc;
+      }
+    };
+    stage(nb - 1, tid, blockDim.x);
+    __syncthreads();
+    if (warp == 0) solve_diag(nb - 1);
+    __syncthreads();
+    for (int b = nb - 1; b > 0; --b) {
+      const int i0 = b * 32, n0 = i0 - 32;  // block b - 1 holds rows n0 .. i0 - 1
+      if (warp == 0) {
+        __syncwarp();
+        update_rows(n0, i0, b, lane, 32);
+        __syncwarp();
+      } else {
+        stage(b - 1, tid - 32, blockDim.x - 32);
+        update_rows(0, n0, b, tid - 32, blockDim.x - 32);
+      }
+      __syncthreads();  // block b - 1 staged, its rows and the rows above updated with x_b
+      if (warp == 0) solve_diag(b - 1);
+      __syncthreads();
+    }
+  } else
   for (int i0 = ((r - 1) / 32) * 32; i0 >= 0; i0 -= 32) {
     const int bs = min(32, r - i0);
     __syncthreads();
@@ -2455,6 +2806,22 @@ void galerkin_batch(int r, int m, const int* angles, const double* dirs, const d
                     long long proj_stride, const double* prhs, const double* extra, double* sol, long long ldsol,
                     int* flags, double* work, cudaStream_t s) {
   if (m <= 0 || r <= 0) return;
+  static const bool cta_lu = [] {  // RTLR_GAL_CTA=0: the shared-memory / blocked kernels for small batches (A/B)
+    const char* e = std::getenv("RTLR_GAL_CTA");
+    return !(e && std::string(e) == "0");
+  }();
+  if (cta_lu && m <= kSmemLuSmallBatch && r <= kCtaLuMax) {
+    const size_t smem = static_cast<size_t>(r) * (r + 1) * sizeof(double);
+    static const bool attr = [] {
+      RTLR_CUDA(cudaFuncSetAttribute(galerkin_cta_lu, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     kCtaLuMax * (kCtaLuMax + 1) * 8));
+      return true;
+    }();
+    (void)attr;
+    galerkin_cta_lu<<<m, 1024, smem, s>>>(r, angles, dirs, proj, ldp, proj_stride, prhs, extra, sol, ldsol, flags);
+    RTLR_CUDA(cudaGetLastError());
+    return;
+  }
   const int smem_max = lu_smem_max(m);
   if (r > smem_max) {
     double* M = work;
@@ -2496,7 +2863,7 @@ void galerkin_batch(int r, int m, const int* angles, const double* dirs, const d
     // One CTA per system while the systems do not fill the GPU with warps;
     // beyond that one warp per system (8 per CTA) has the parallelism.
     if (m < 8 * 148) {
-      const size_t smem = (static_cast<size_t>(r) + 32 * 33) * sizeof(double);
+      const size_t smem = (static_cast<size_t>(r) + 2 * 32 * 33 + 64) * sizeof(double);
       if (smem > 48 * 1024)
         RTLR_CUDA(cudaFuncSetAttribute(lu_backsolve_cta, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        static_cast<int>(smem)));
@@ -2720,7 +3087,13 @@ size_t bidiag_work_doubles(long long m, int n) { return static_cast<size_t>(2 * 
 bool bidiag_singular_values(long long m, int n, double* a, long long lda, double* d_sv, double* work,
                             size_t work_doubles, cudaStream_t s) {
   if (n < 1 || m < n || m > 8192 || work_doubles < bidiag_work_doubles(m, n)) return false;
-  static const int coop_per_sm = [] {
+  // RTLR_SVD=bidiag1: the three-barrier kernel and thread-per-value bisection (A/B)
+  static const int variant = [] {
+    const char* e = std::getenv("RTLR_SVD");
+    return e && std::string(e) == "bidiag1" ? 1 : 2;
+  }();
+  const bool v2 = variant == 2 && n <= 32 * kBdRegs;
+  static const int coop_per_sm[2] = {[] {
     int dev = 0, ok = 0, per = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&ok, cudaDevAttrCooperativeLaunch, dev);
@@ -2729,8 +3102,19 @@ bool bidiag_singular_values(long long m, int n, double* a, long long lda, double
     RTLR_CUDA(cudaFuncSetAttribute(bidiag_coop, cudaFuncAttributeMaxDynamicSharedMemorySize, 2 * 8192 * 8));
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, bidiag_coop, 256, 2 * 8192 * 8);
     return std::min(per, 2);
-  }();
-  if (coop_per_sm == 0) return false;
+  }(), [] {
+    int dev = 0, ok = 0, per = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&ok, cudaDevAttrCooperativeLaunch, dev);
+    const char* e = std::getenv("RTLR_SVD");
+    if (!ok || (e && std::string(e) == "jacobi")) return 0;
+    const int bytes = (8192 + 32 * kBdRegs) * 8;
+    RTLR_CUDA(cudaFuncSetAttribute(bidiag_coop2, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, bidiag_coop2, 256, bytes);
+    return std::min(per, 2);
+  }()};
+  const int per_sm = coop_per_sm[v2 ? 1 : 0];
+  if (per_sm == 0) return false;
   int dev = 0, sms = 0;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
@@ -2739,10 +3123,17 @@ bool bidiag_singular_values(long long m, int n, double* a, long long lda, double
   double* part = work + 2 * n + 8;
   int mi = static_cast<int>(m);
   const size_t smem = static_cast<size_t>(m + n) * sizeof(double);
-  void* args[] = {&mi, &n, &a, &lda, &dd, &de, &part};
-  RTLR_CUDA(cudaLaunchCooperativeKernel(reinterpret_cast<void*>(bidiag_coop), dim3(sms * coop_per_sm), dim3(256), args,
-                                        smem, s));
-  gk_bisect<<<(n + 127) / 128, 128, 0, s>>>(n, dd, de, d_sv);
+  if (v2) {
+    void* args[] = {&mi, &n, &a, &lda, &dd, &de};
+    RTLR_CUDA(cudaLaunchCooperativeKernel(reinterpret_cast<void*>(bidiag_coop2), dim3(sms * per_sm), dim3(256), args,
+                                          smem, s));
+    gk_multisect<<<(n + 7) / 8, 256, 0, s>>>(n, dd, de, d_sv);
+  } else {
+    void* args[] = {&mi, &n, &a, &lda, &dd, &de, &part};
+    RTLR_CUDA(cudaLaunchCooperativeKernel(reinterpret_cast<void*>(bidiag_coop), dim3(sms * per_sm), dim3(256), args,
+                                          smem, s));
+    gk_bisect<<<(n + 127) / 128, 128, 0, s>>>(n, dd, de, d_sv);
+  }
   RTLR_CUDA(cudaGetLastError());
   return true;
 }

@@ -1458,14 +1458,19 @@ std::vector<double> LowRankEngine::svd(bool vectors, int keep, std::vector<doubl
   else
     RTLR_CUDA(cudaMemcpyAsync(Wm, C_.get(), static_cast<size_t>(r) * nomega_ * sizeof(double),
                               cudaMemcpyDeviceToDevice, s_));
-  if (!vectors && static_cast<double>(mrows) * ncols >= 3e5) {
+  static const double bidiag_min = [] {  // RTLR_SVD_BIDIAG_MIN: smallest factor (entries) on the bidiagonal path
+    const char* e = std::getenv("RTLR_SVD_BIDIAG_MIN");
+    return e ? std::atof(e) : 0.0;
+  }();
+  if (!vectors && static_cast<double>(mrows) * ncols >= bidiag_min) {
     // singular values only (every outer iteration): bidiagonalisation of W
-    // and Golub-Kahan bisection, without the QR and the Jacobi sweeps (C4
-    // 0.31 -> 0.24 s, C3 0.155 -> 0.13 s; smaller factors stay on QR +
-    // Jacobi, whose sweeps there cost less than 3 grid barriers per column)
+    // and Golub-Kahan multisection, without the QR and the Jacobi sweeps
+    // (bidiag_coop2 + gk_multisect, tools/svd_time.py: 2048 x 600 56 -> 18.5
+    // ms, 1152 x 403 28.5 -> 9.3, 512 x 178 8.6 -> 4.0, 128 x 64 3.0 -> 1.7;
+    // RTLR_SVD_BIDIAG_MIN raises the size below which QR + Jacobi run)
     double* dsv = nrm_.ensure(std::max(ncols, 128));
-    if (bidiag_singular_values(mrows, ncols, Wm, mrows, dsv, work(bidiag_work_doubles(mrows, ncols)), work_.size(),
-                               s_)) {
+    double* bw = work(bidiag_work_doubles(mrows, ncols));  // before work_.size(): argument order is unspecified
+    if (bidiag_singular_values(mrows, ncols, Wm, mrows, dsv, bw, work_.size(), s_)) {
       ++svd_calls_;
       const double mm = static_cast<double>(mrows), nn = ncols;
       // 4 m n^2 - 4/3 n^3 flops; the factor crosses HBM once each way (its
