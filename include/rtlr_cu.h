@@ -208,6 +208,16 @@ int rtlr_cu_psi_difference(rtlr_cu_problem* p, const double* psi_full, const dou
  * orthonormal columns, r n x n upper triangular (Eigen sign conventions). */
 int rtlr_cu_dense_qr(int device, int64_t m, int n, const double* a, double* q, double* r);
 
+/* The batched Galerkin solve (low_rank.cpp:176-200) two ways, for tests and
+ * tools: m <= 64 systems A_j = omx Px- + omy Py- + Pt (sign-selected among
+ * the 5 projections proj[5][r][r], column-major, r = r0 + k) with right-hand
+ * side prhs: sol_full by the partial-pivot LU at rank r; sol_border by the
+ * rank-r0 factors finished with the k <= 8 border columns (the low-rank
+ * loop's prefactored candidates).  Both r x m, column-major. */
+int rtlr_cu_dense_galerkin_border(int device, int r0, int k, int m, const int* angles, int n_omega,
+                                  const double* dirs, const double* proj, const double* prhs, double* sol_full,
+                                  double* sol_border);
+
 /* ---- caller-assembled problems.  The reference's solvers take assembled
  * objects, not a config: solve_full_rank(ops, quad, bc, source, dsa, opts)
  * (full_rank.hpp:41-43), solve_low_rank(...) (low_rank.hpp:156-158),

@@ -40,7 +40,7 @@ EXPORTS = [
     "rtlr_cu_report_get", "rtlr_cu_report_sampled", "rtlr_cu_report_destroy",
     "rtlr_cu_partition_angles", "rtlr_cu_problem_fr_options", "rtlr_cu_problem_lr_options",
     "rtlr_cu_sweep_async", "rtlr_cu_check", "rtlr_cu_nccl_unique_id", "rtlr_cu_problem_set_comm",
-    "rtlr_cu_shard_block", "rtlr_cu_dense_qr", "rtlr_cu_psi_difference",
+    "rtlr_cu_shard_block", "rtlr_cu_dense_qr", "rtlr_cu_dense_galerkin_border", "rtlr_cu_psi_difference",
     "rtlr_cu_config_parse", "rtlr_cu_config_load", "rtlr_cu_config_set_mode", "rtlr_cu_run",
     "rtlr_cu_problem_upload", "rtlr_cu_lr_params_default", "rtlr_cu_rng_create", "rtlr_cu_rng_destroy",
     "rtlr_cu_rng_draw_below", "rtlr_cu_rng_sample", "rtlr_cu_lr_basis_create", "rtlr_cu_lr_basis_destroy",
@@ -162,6 +162,9 @@ def load_library(path: str = LIB_PATH):
     L.rtlr_cu_partition_angles.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int, _I, _I]
     _ip = ctypes.POINTER(ctypes.c_int)
     L.rtlr_cu_shard_block.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.c_int, _ip, _ip, _ip]
+    L.rtlr_cu_dense_galerkin_border.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_void_p,
+                                                ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p,
+                                                ctypes.c_void_p, ctypes.c_void_p]
     L.rtlr_cu_dense_qr.argtypes = [ctypes.c_int, ctypes.c_int64, ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p,
                                    ctypes.c_void_p]
     V, Vp, Dp = ctypes.c_void_p, ctypes.POINTER(ctypes.c_void_p), _D
@@ -247,6 +250,25 @@ def dense_qr(a: np.ndarray, device: int = 0):
     r = np.zeros((n, n), dtype=np.float64, order="F")
     _check(load_library().rtlr_cu_dense_qr(device, m, n, _dp(a), _dp(q), _dp(r)))
     return q, r
+
+
+def dense_galerkin_border(r0: int, k: int, angles, dirs: np.ndarray, proj: np.ndarray, prhs: np.ndarray,
+                          device: int = 0):
+    """(sol_full, sol_border): the Galerkin systems of `angles` solved at rank
+    r0 + k by the pivoted LU and by the rank-r0 factors plus the k border
+    columns.  proj: (5, r, r) with proj[q][:, :] the q-th projection (stored
+    column-major on the device), dirs (n_omega, 3), prhs (r,)."""
+    angles = np.ascontiguousarray(angles, dtype=np.int32)
+    dirs = np.ascontiguousarray(dirs, dtype=np.float64)
+    r = r0 + k
+    pj = np.ascontiguousarray(np.stack([np.asfortranarray(proj[q]).T for q in range(5)]), dtype=np.float64)
+    prhs = np.ascontiguousarray(prhs, dtype=np.float64)
+    m = len(angles)
+    s1 = np.zeros((r, m), dtype=np.float64, order="F")
+    s2 = np.zeros((r, m), dtype=np.float64, order="F")
+    _check(load_library().rtlr_cu_dense_galerkin_border(device, r0, k, m, angles.ctypes.data_as(ctypes.c_void_p),
+                                                        dirs.shape[0], _dp(dirs), _dp(pj), _dp(prhs), _dp(s1), _dp(s2)))
+    return s1, s2
 
 
 def compare_runs(full, low, problem=None) -> dict:

@@ -585,6 +585,40 @@ int rtlr_cu_dense_qr(int device, int64_t m, int n, const double* a, double* q, d
   });
 }
 
+int rtlr_cu_dense_galerkin_border(int device, int r0, int k, int m, const int* angles, int n_omega,
+                                  const double* dirs, const double* proj, const double* prhs, double* sol_full,
+                                  double* sol_border) {
+  return guard([&] {
+    need(r0 >= 1 && k >= 0 && m >= 1 && m <= 64 && angles && dirs && proj && prhs && sol_full && sol_border,
+         "dense_galerkin_border: bad argument");
+    need(galerkin_border_fits(r0, k), "dense_galerkin_border: rank or border out of range");
+    RTLR_CUDA(cudaSetDevice(device));
+    cudaStream_t s;
+    RTLR_CUDA(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+    const int r = r0 + k;
+    const size_t rr = static_cast<size_t>(r) * r;
+    DBuf<double> dd, dp, dr, w1, w2, s1, s2;
+    DBuf<int> da, fl;
+    dd.upload(dirs, 3 * static_cast<size_t>(n_omega), s);
+    dp.upload(proj, 5 * rr, s);
+    dr.upload(prhs, r, s);
+    da.upload(angles, m, s);
+    fl.ensure(2 * m);
+    s1.ensure(static_cast<size_t>(r) * m);
+    s2.ensure(static_cast<size_t>(r) * m);
+    const size_t lw = galerkin_work_doubles(r, m);
+    galerkin_batch(r, m, da.get(), dd.get(), dp.get(), r, rr, dr.get(), nullptr, s1.get(), r, fl.get(),
+                   lw ? w1.ensure(lw) : nullptr, s);
+    double* pw = w2.ensure(static_cast<size_t>(m) * galerkin_work_per_system(r0));
+    galerkin_prefactor(r0, m, da.get(), dd.get(), dp.get(), r, rr, dr.get(), pw, s);
+    galerkin_border_solve(r0, k, m, da.get(), dd.get(), dp.get(), r, rr, dr.get(), pw, s2.get(), r, fl.get() + m, s);
+    RTLR_CUDA(cudaMemcpyAsync(sol_full, s1.get(), static_cast<size_t>(r) * m * sizeof(double), cudaMemcpyDeviceToHost, s));
+    RTLR_CUDA(cudaMemcpyAsync(sol_border, s2.get(), static_cast<size_t>(r) * m * sizeof(double), cudaMemcpyDeviceToHost, s));
+    RTLR_CUDA(cudaStreamSynchronize(s));
+    RTLR_CUDA(cudaStreamDestroy(s));
+  });
+}
+
 int rtlr_cu_shard_block(int m, int nranks, int rank, int* begin, int* end, int* bsz) {
   return guard([&] {
     need(begin != nullptr && end != nullptr && bsz != nullptr, "shard_block: null argument");

@@ -2405,15 +2405,13 @@ __global__ void __launch_bounds__(256) lu_backsolve_warp(int r, int m, const dou
 // together).  Per element the same operations in the same order as
 // lu_backsolve_warp, so the solutions are bitwise identical; a few systems
 // (the q greedy candidates) no longer leave the GPU with one warp each.
-__global__ void __launch_bounds__(256) lu_backsolve_cta(int r, const double* __restrict__ M,
-                                                        double* __restrict__ sol, long long ldsol,
-                                                        int* __restrict__ flags) {
-  extern __shared__ double xs[];
-  double* ub = xs + r;  // 32 x 33 diagonal block, ub[j * 33 + i] = U[i0 + j][i0 + i]
+// (the body: A the factored r x (r + 1) system, xs the right-hand side in
+// shared memory -- loaded from column r when load_rhs -- and the solution on
+// return; ub 2 x 32 x 33 + 64 doubles of scratch; every thread of the CTA)
+__device__ void lu_backsolve_cta_body(int r, const double* __restrict__ A, double* xs, double* ub, bool load_rhs) {
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int sys = blockIdx.x;
-  const double* A = M + static_cast<size_t>(sys) * r * (r + 1);
-  for (int i = tid; i < r; i += blockDim.x) xs[i] = A[i + static_cast<size_t>(r) * r];
+  if (load_rhs)
+    for (int i = tid; i < r; i += blockDim.x) xs[i] = A[i + static_cast<size_t>(r) * r];
   if (r > 64) {
     // Look-ahead form for long solves: warp 0 updates the next diagonal
     // block's 32 rows first and solves that block (reciprocal pivots, formed
@@ -2515,10 +2513,275 @@ __global__ void __launch_bounds__(256) lu_backsolve_cta(int r, const double* __r
     }
   }
   __syncthreads();
+}
+
+__global__ void __launch_bounds__(256) lu_backsolve_cta(int r, const double* __restrict__ M,
+                                                        double* __restrict__ sol, long long ldsol,
+                                                        int* __restrict__ flags) {
+  extern __shared__ double xs[];
+  double* ub = xs + r;  // 32 x 33 diagonal block, ub[j * 33 + i] = U[i0 + j][i0 + i]
+  const int tid = threadIdx.x;
+  const int sys = blockIdx.x;
+  lu_backsolve_cta_body(r, M + static_cast<size_t>(sys) * r * (r + 1), xs, ub, true);
   int bad = 0;
   for (int i = tid; i < r; i += blockDim.x) {
     sol[i + static_cast<long long>(sys) * ldsol] = xs[i];
     if (!isfinite(xs[i])) bad = 1;
+  }
+  bad = __syncthreads_or(bad);
+  if (tid == 0) flags[sys] = bad;
+}
+
+// ---------------------------------------------------------------------------
+// Bordered finish of a prefactored Galerkin system.  The greedy candidates of
+// an inner iteration are known before that iteration's sweep (the pool and
+// the RNG state are), and the basis of the previous iteration is the leading
+// block of this one's, so P A00 = L U (r0 x r0, with y0 = L^-1 P b0 in column
+// r0) is factored on a second stream while the sweep, the CGS and the
+// projection update run.  With the k <= kBorderMax new basis columns in:
+//   [A00 A01] [x0]   [b0]      U01 = L^-1 P A01,  L10 = A10 U^-1,
+//   [A10 A11] [x1] = [b1]      S = A11 - L10 U01, x1 = S^-1 (b1 - L10 y0),
+//                              x0 = U^-1 (y0 - U01 x1).
+// One CTA of 512 threads per system: threads 0-255 replay the panels on the
+// new columns (the panel's row swaps, the unit-lower 32 x 32 solve in a
+// warp's lanes, the rows below; two named barriers per panel) while threads
+// 256-511 solve the new rows against U (right-looking over 32-column
+// blocks); then the k x k Schur system (partial pivoting) and the blocked
+// back substitution of lu_backsolve_cta.  The factorisation pivots within
+// the leading block first (the reference pivots over the whole column): the
+// reduced operators' symmetric part is positive definite (Sigma_t > 0 plus
+// the upwind flux terms), so the leading block is as well conditioned as the
+// whole, and the solutions agree to rounding (tests/test_gpu_lr.py).
+constexpr int kBorderMax = 8;
+constexpr int kBorderScratch = 2 * 32 * 33 + 64 + 16 * 72 + 72 + 8;
+size_t border_smem_bytes(int r0) {
+  return (static_cast<size_t>(r0) * (2 * kBorderMax + 1) + kBorderScratch) * sizeof(double);
+}
+__device__ __forceinline__ void bar_group(int id) { asm volatile("bar.sync %0, 256;" ::"r"(id) : "memory"); }
+
+__global__ void __launch_bounds__(512, 1) galerkin_border_kernel(int r0, int k, const int* __restrict__ angles,
+                                                                 const double* __restrict__ dirs,
+                                                                 const double* __restrict__ proj, long long ldp,
+                                                                 long long pstride, const double* __restrict__ prhs,
+                                                                 const double* __restrict__ Fall,
+                                                                 const int* __restrict__ pivall,
+                                                                 double* __restrict__ sol, long long ldsol,
+                                                                 int* __restrict__ flags) {
+  extern __shared__ __align__(16) double bsm[];
+  double* Vt = bsm;                                  // r0 x 8: A01 -> U01 (row i: its 8 columns)
+  double* Wt = Vt + static_cast<size_t>(r0) * 8;     // r0 x 8: A10^T -> L10^T
+  double* ys = Wt + static_cast<size_t>(r0) * 8;     // y0 -> y0 - U01 x1 -> x0
+  double* ub = ys + r0;                              // back substitution scratch
+  double* red = ub + 2 * 32 * 33 + 64;               // 16 x 72 partial sums
+  double* Ss = red + 16 * 72;                        // 8 x 9: [S | y1]
+  double* x1 = Ss + 72;
+  const int tid = threadIdx.x, lane = tid & 31;
+  const int sys = blockIdx.x;
+  const double* F = Fall + static_cast<size_t>(sys) * r0 * (r0 + 1);
+  const int* pv = pivall + static_cast<size_t>(sys) * r0;
+  const int ang = angles[sys];
+  const double omx = dirs[3 * ang], omy = dirs[3 * ang + 1];
+  const double* px = proj + (omx >= 0.0 ? 0 : 1) * pstride;
+  const double* py = proj + (omy >= 0.0 ? 2 : 3) * pstride;
+  const double* pt = proj + 4 * pstride;
+  auto a_at = [&](int i, int j) {  // reduced_streaming (low_rank.cpp:176-183)
+    const long long e = i + j * ldp;
+    return omx * px[e] + omy * py[e] + pt[e];
+  };
+  if (tid < 256) {
+    const int gt = tid, gw = gt >> 5;
+    for (int t = 0; t < kBorderMax; ++t)
+      for (int i = gt; i < r0; i += 256) Vt[i * 8 + t] = t < k ? a_at(i, r0 + t) : 0.0;
+    for (int i = gt; i < r0; i += 256) ys[i] = F[i + static_cast<size_t>(r0) * r0];
+    bar_group(1);
+    for (int k0 = 0; k0 < r0;) {
+      const int jb = lu_panel_width(r0, k0);
+      if (gw < k) {  // warp gw: column gw through the panel's swaps and its unit-lower block
+        const int t = gw;
+        const int pvl = lane < jb ? pv[k0 + lane] : 0;
+        double v = lane < jb ? Vt[(k0 + lane) * 8 + t] : 0.0;
+        double Lr[32];
+#pragma unroll
+        for (int l = 0; l < 32; ++l)
+          Lr[l] = (lane < jb && l < lane) ? F[k0 + lane + static_cast<size_t>(k0 + l) * r0] : 0.0;
+        for (int j = 0; j < jb; ++j) {
+          const int b = __shfl_sync(0xffffffffu, pvl, j);
+          if (b == k0 + j) continue;
+          const double vj = __shfl_sync(0xffffffffu, v, j);
+          if (b < k0 + jb) {
+            const double vb = __shfl_sync(0xffffffffu, v, b - k0);
+            if (lane == j) v = vb;
+            if (lane == b - k0) v = vj;
+          } else {
+            if (lane == j) {
+              v = Vt[b * 8 + t];
+              Vt[b * 8 + t] = vj;
+            }
+            __syncwarp();
+          }
+        }
+#pragma unroll
+        for (int l = 0; l < 31; ++l) {
+          const double vl = __shfl_sync(0xffffffffu, v, l);
+          if (lane > l) v -= Lr[l] * vl;
+        }
+        if (lane < jb) Vt[(k0 + lane) * 8 + t] = v;
+      }
+      bar_group(1);
+      for (int i = k0 + jb + gt; i < r0; i += 256) {
+        const double* Li = F + i + static_cast<size_t>(k0) * r0;
+        double acc[8] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
+#pragma unroll 8
+        for (int l = 0; l < jb; ++l) {
+          const double lv = Li[static_cast<size_t>(l) * r0];
+          const double2* vr = reinterpret_cast<const double2*>(Vt + (k0 + l) * 8);
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            const double2 vv = vr[q];
+            acc[2 * q] += lv * vv.x;
+            acc[2 * q + 1] += lv * vv.y;
+          }
+        }
+        double2* vo = reinterpret_cast<double2*>(Vt + i * 8);
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          double2 vv = vo[q];
+          vv.x -= acc[2 * q];
+          vv.y -= acc[2 * q + 1];
+          vo[q] = vv;
+        }
+      }
+      bar_group(1);
+      k0 += jb;
+    }
+  } else {
+    const int gt = tid - 256, gw = gt >> 5;
+    for (int j = gt; j < r0; j += 256)
+#pragma unroll
+      for (int u = 0; u < kBorderMax; ++u) Wt[j * 8 + u] = u < k ? a_at(r0 + u, j) : 0.0;
+    bar_group(2);
+    for (int c0 = 0; c0 < r0; c0 += 32) {
+      const int bs = min(32, r0 - c0);
+      if (gw < k) {  // warp gw: new row gw against the upper 32 x 32 diagonal block
+        const int u = gw;
+        double sv = lane < bs ? Wt[(c0 + lane) * 8 + u] : 0.0;
+        const double rinv = lane < bs ? 1.0 / F[c0 + lane + static_cast<size_t>(c0 + lane) * r0] : 1.0;
+        double Uc[32];  // U[c0 + i][c0 + lane], i < lane
+#pragma unroll
+        for (int i = 0; i < 32; ++i)
+          Uc[i] = (lane < bs && i < lane) ? F[c0 + i + static_cast<size_t>(c0 + lane) * r0] : 0.0;
+#pragma unroll
+        for (int i = 0; i < 32; ++i) {
+          const double xi = __shfl_sync(0xffffffffu, sv * rinv, i);
+          if (lane == i) sv = xi;
+          if (lane > i) sv -= xi * Uc[i];
+        }
+        if (lane < bs) Wt[(c0 + lane) * 8 + u] = sv;
+      }
+      bar_group(2);
+      for (int j = c0 + bs + gt; j < r0; j += 256) {
+        const double* Uj = F + c0 + static_cast<size_t>(j) * r0;
+        double acc[8] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
+#pragma unroll 8
+        for (int i = 0; i < bs; ++i) {
+          const double uv = Uj[i];
+          const double2* wr = reinterpret_cast<const double2*>(Wt + (c0 + i) * 8);
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            const double2 ww = wr[q];
+            acc[2 * q] += uv * ww.x;
+            acc[2 * q + 1] += uv * ww.y;
+          }
+        }
+        double2* wo = reinterpret_cast<double2*>(Wt + j * 8);
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          double2 ww = wo[q];
+          ww.x -= acc[2 * q];
+          ww.y -= acc[2 * q + 1];
+          wo[q] = ww;
+        }
+      }
+      bar_group(2);
+    }
+  }
+  __syncthreads();
+  {  // [L10 U01 | L10 y0]: warp w sums rows w, w + 16, ...; a lane holds pairs lane, lane + 32, lane + 64
+    const int w = tid >> 5;
+    double acc[3] = {0.0, 0.0, 0.0};
+    for (int i = w; i < r0; i += 16) {
+#pragma unroll
+      for (int q = 0; q < 3; ++q) {
+        const int pr = lane + 32 * q;
+        if (pr < 72) {
+          const int u = pr / 9, t = pr - 9 * u;
+          acc[q] += Wt[i * 8 + u] * (t < 8 ? Vt[i * 8 + t] : ys[i]);
+        }
+      }
+    }
+#pragma unroll
+    for (int q = 0; q < 3; ++q)
+      if (lane + 32 * q < 72) red[w * 72 + lane + 32 * q] = acc[q];
+  }
+  __syncthreads();
+  if (tid < 72) {
+    double sum = 0.0;
+    for (int w = 0; w < 16; ++w) sum += red[w * 72 + tid];
+    const int u = tid / 9, t = tid - 9 * u;
+    double base;  // identity padding past k
+    if (u < k && t < k)
+      base = a_at(r0 + u, r0 + t);
+    else if (u < k && t == 8)
+      base = prhs[r0 + u];
+    else
+      base = (t == u) ? 1.0 : 0.0;
+    Ss[tid] = base - sum;
+  }
+  __syncthreads();
+  if (tid == 0) {  // 8 x 8 partial-pivot elimination of [S | y1]
+    for (int c = 0; c < 8; ++c) {
+      int p = c;
+      double best = fabs(Ss[c * 9 + c]);
+      for (int i = c + 1; i < 8; ++i)
+        if (fabs(Ss[i * 9 + c]) > best) {
+          best = fabs(Ss[i * 9 + c]);
+          p = i;
+        }
+      if (p != c)
+        for (int j = c; j < 9; ++j) {
+          const double tmp = Ss[c * 9 + j];
+          Ss[c * 9 + j] = Ss[p * 9 + j];
+          Ss[p * 9 + j] = tmp;
+        }
+      const double d = Ss[c * 9 + c];
+      for (int i = c + 1; i < 8; ++i) {
+        const double mlt = Ss[i * 9 + c] / d;
+        for (int j = c + 1; j < 9; ++j) Ss[i * 9 + j] -= mlt * Ss[c * 9 + j];
+      }
+    }
+    for (int i = 7; i >= 0; --i) {
+      double x = Ss[i * 9 + 8];
+      for (int j = i + 1; j < 8; ++j) x -= Ss[i * 9 + j] * x1[j];
+      x1[i] = x / Ss[i * 9 + i];
+    }
+  }
+  __syncthreads();
+  for (int i = tid; i < r0; i += 512) {
+    double z = ys[i];
+#pragma unroll
+    for (int t = 0; t < 8; ++t) z -= Vt[i * 8 + t] * x1[t];
+    ys[i] = z;
+  }
+  __syncthreads();
+  lu_backsolve_cta_body(r0, F, ys, ub, false);
+  int bad = 0;
+  for (int i = tid; i < r0; i += 512) {
+    sol[i + static_cast<long long>(sys) * ldsol] = ys[i];
+    if (!isfinite(ys[i])) bad = 1;
+  }
+  if (tid < k) {
+    sol[r0 + tid + static_cast<long long>(sys) * ldsol] = x1[tid];
+    if (!isfinite(x1[tid])) bad = 1;
   }
   bad = __syncthreads_or(bad);
   if (tid == 0) flags[sys] = bad;
@@ -2802,6 +3065,43 @@ size_t galerkin_work_doubles(int r, int m) {
   return static_cast<size_t>(m) * galerkin_work_per_system(r);
 }
 
+// The blocked right-looking factorisation of m assembled r x (r + 1)
+// systems in place (panel, then swaps + TRSM + DMMA update of the trailing
+// columns, the right-hand side among them).
+static void lu_factor_blocked(int r, int m, double* M, int* piv, int* perm, cudaStream_t s) {
+  constexpr int kPanelThreads = 256;
+  RTLR_CUDA(cudaFuncSetAttribute(lu_panel_smem<kPanelThreads>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 kPanelSmemBytes));
+  RTLR_CUDA(cudaFuncSetAttribute(lu_trail, cudaFuncAttributeMaxDynamicSharedMemorySize, kTrailSmem));
+  static const int reg_panel = [] {  // RTLR_LU_PANEL=smem: the shared-memory panel only
+    const char* e = std::getenv("RTLR_LU_PANEL");
+    if (e && std::string(e) == "smem") return 0;
+    const int bytes = 512 * static_cast<int>(kNbMax * sizeof(double) + sizeof(int));
+    RTLR_CUDA(cudaFuncSetAttribute(lu_panel_reg<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
+    RTLR_CUDA(cudaFuncSetAttribute(lu_panel_reg<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
+    return 1;
+  }();
+  for (int k0 = 0; k0 < r;) {
+    const int jb = lu_panel_width(r, k0);
+    const int rows = r - k0;
+    const size_t slot_bytes = static_cast<size_t>(rows) * (kNbMax * sizeof(double) + sizeof(int));
+    // (small batches only: at one CTA per SM the register panel loses to
+    // the shared-memory one once the batch fills the GPU; 3 rows per
+    // thread spill)
+    const bool small = reg_panel && m <= 64 && jb == kNbMax;
+    if (small && rows <= 256)
+      lu_panel_reg<1><<<m, 256, slot_bytes, s>>>(r, k0, jb, M, piv, perm);
+    else if (small && rows <= 512)
+      lu_panel_reg<2><<<m, 256, slot_bytes, s>>>(r, k0, jb, M, piv, perm);
+    else
+      lu_panel_smem<kPanelThreads><<<m, kPanelThreads, static_cast<size_t>(rows) * (jb * sizeof(double) + 4), s>>>(
+          r, k0, jb, M, piv, perm);
+    const int ntrail = r + 1 - (k0 + jb);
+    if (ntrail > 0) lu_trail<<<dim3((ntrail + BN - 1) / BN, m), 256, kTrailSmem, s>>>(r, k0, jb, M, perm);
+    k0 += jb;
+  }
+}
+
 void galerkin_batch(int r, int m, const int* angles, const double* dirs, const double* proj, long long ldp,
                     long long proj_stride, const double* prhs, const double* extra, double* sol, long long ldsol,
                     int* flags, double* work, cudaStream_t s) {
@@ -2829,37 +3129,7 @@ void galerkin_batch(int r, int m, const int* angles, const double* dirs, const d
     int* perm = reinterpret_cast<int*>(work + static_cast<size_t>(m) * (r * static_cast<size_t>(r + 1) + r));
     lu_assemble<<<dim3(std::max(1, std::min(64, (r * (r + 1) + 255) / 256)), m), 256, 0, s>>>(
         r, angles, dirs, proj, ldp, proj_stride, prhs, extra, ldsol, M);
-    constexpr int kPanelThreads = 256;
-    RTLR_CUDA(cudaFuncSetAttribute(lu_panel_smem<kPanelThreads>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                   kPanelSmemBytes));
-    RTLR_CUDA(cudaFuncSetAttribute(lu_trail, cudaFuncAttributeMaxDynamicSharedMemorySize, kTrailSmem));
-    static const int reg_panel = [] {  // RTLR_LU_PANEL=smem: the shared-memory panel only
-      const char* e = std::getenv("RTLR_LU_PANEL");
-      if (e && std::string(e) == "smem") return 0;
-      const int bytes = 512 * static_cast<int>(kNbMax * sizeof(double) + sizeof(int));
-      RTLR_CUDA(cudaFuncSetAttribute(lu_panel_reg<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
-      RTLR_CUDA(cudaFuncSetAttribute(lu_panel_reg<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
-      return 1;
-    }();
-    for (int k0 = 0; k0 < r;) {
-      const int jb = lu_panel_width(r, k0);
-      const int rows = r - k0;
-      const size_t slot_bytes = static_cast<size_t>(rows) * (kNbMax * sizeof(double) + sizeof(int));
-      // (small batches only: at one CTA per SM the register panel loses to
-      // the shared-memory one once the batch fills the GPU; 3 rows per
-      // thread spill)
-      const bool small = reg_panel && m <= 64 && jb == kNbMax;
-      if (small && rows <= 256)
-        lu_panel_reg<1><<<m, 256, slot_bytes, s>>>(r, k0, jb, M, piv, perm);
-      else if (small && rows <= 512)
-        lu_panel_reg<2><<<m, 256, slot_bytes, s>>>(r, k0, jb, M, piv, perm);
-      else
-        lu_panel_smem<kPanelThreads><<<m, kPanelThreads, static_cast<size_t>(rows) * (jb * sizeof(double) + 4), s>>>(
-            r, k0, jb, M, piv, perm);
-      const int ntrail = r + 1 - (k0 + jb);
-      if (ntrail > 0) lu_trail<<<dim3((ntrail + BN - 1) / BN, m), 256, kTrailSmem, s>>>(r, k0, jb, M, perm);
-      k0 += jb;
-    }
+    lu_factor_blocked(r, m, M, piv, perm, s);
     // One CTA per system while the systems do not fill the GPU with warps;
     // beyond that one warp per system (8 per CTA) has the parallelism.
     if (m < 8 * 148) {
@@ -2886,6 +3156,43 @@ void galerkin_batch(int r, int m, const int* angles, const double* dirs, const d
                                    kSmemLuMax * kSmemLuMax * 8));
   galerkin_kernel<<<m, 256, smem, s>>>(r, angles, dirs, proj, ldp, proj_stride, prhs, extra, sol, ldsol, flags,
                                        work, in_smem);
+  RTLR_CUDA(cudaGetLastError());
+}
+
+// Prefactor: assemble [A | prhs] at rank r for the m angles and factor it in
+// place (no back substitution); work as galerkin_batch's blocked path.
+void galerkin_prefactor(int r, int m, const int* angles, const double* dirs, const double* proj, long long ldp,
+                        long long proj_stride, const double* prhs, double* work, cudaStream_t s,
+                        cudaEvent_t assembled) {
+  if (m <= 0 || r <= 0) return;
+  double* M = work;
+  int* piv = reinterpret_cast<int*>(work + static_cast<size_t>(m) * r * (r + 1));
+  int* perm = reinterpret_cast<int*>(work + static_cast<size_t>(m) * (r * static_cast<size_t>(r + 1) + r));
+  lu_assemble<<<dim3(std::max(1, std::min(64, (r * (r + 1) + 255) / 256)), m), 256, 0, s>>>(
+      r, angles, dirs, proj, ldp, proj_stride, prhs, nullptr, 0, M);
+  if (assembled) RTLR_CUDA(cudaEventRecord(assembled, s));  // proj and prhs are not read past this point
+  lu_factor_blocked(r, m, M, piv, perm, s);
+  RTLR_CUDA(cudaGetLastError());
+}
+
+bool galerkin_border_fits(int r0, int k) {
+  return r0 >= 1 && k >= 0 && k <= kBorderMax && border_smem_bytes(r0) <= 227 * 1024;
+}
+
+// The solutions at rank r0 + k from the rank-r0 factors galerkin_prefactor left in work.
+void galerkin_border_solve(int r0, int k, int m, const int* angles, const double* dirs, const double* proj,
+                           long long ldp, long long proj_stride, const double* prhs, const double* work, double* sol,
+                           long long ldsol, int* flags, cudaStream_t s) {
+  if (m <= 0) return;
+  if (!galerkin_border_fits(r0, k)) throw std::invalid_argument("galerkin_border_solve: rank or border out of range");
+  static const bool attr = [] {
+    RTLR_CUDA(cudaFuncSetAttribute(galerkin_border_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
+    return true;
+  }();
+  (void)attr;
+  const int* piv = reinterpret_cast<const int*>(work + static_cast<size_t>(m) * r0 * (r0 + 1));
+  galerkin_border_kernel<<<m, 512, border_smem_bytes(r0), s>>>(r0, k, angles, dirs, proj, ldp, proj_stride, prhs, work,
+                                                               piv, sol, ldsol, flags);
   RTLR_CUDA(cudaGetLastError());
 }
 

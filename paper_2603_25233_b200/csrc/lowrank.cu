@@ -555,6 +555,17 @@ LowRankEngine::LowRankEngine(Problem& P, const LowRankParams& prm) : P_(P), prm_
   gal_bad_.ensure(1);
   RTLR_CUDA(cudaMemsetAsync(gal_bad_.get(), 0, sizeof(int), s_));
   ring_.init(s_);
+  {
+    const char* pe = std::getenv("RTLR_LU_PREFACTOR");
+    prefactor_on_ = !(pe && pe[0] == '0');
+    int least = 0, greatest = 0;
+    RTLR_CUDA(cudaDeviceGetStreamPriorityRange(&least, &greatest));
+    RTLR_CUDA(cudaStreamCreateWithPriority(&s2_, cudaStreamNonBlocking, greatest));
+    RTLR_CUDA(cudaEventCreateWithFlags(&ev_fork_, cudaEventDisableTiming));
+    RTLR_CUDA(cudaEventCreateWithFlags(&ev_asm_, cudaEventDisableTiming));
+    RTLR_CUDA(cudaEventCreateWithFlags(&ev_done_, cudaEventDisableTiming));
+    RTLR_CUDA(cudaMallocHost(&pf_hang_, 256 * sizeof(int)));
+  }
   ldr_ = rmax_;
   // The basis grows every inner iteration; reserving it for the largest
   // possible rank up front (when that takes at most a quarter of the free
@@ -643,6 +654,14 @@ void LowRankEngine::nn_rows_sub(int p, int r, const double* Xm, long long ldx, c
 
 LowRankEngine::~LowRankEngine() {
   cudaStreamSynchronize(s_);
+  if (s2_) {
+    cudaStreamSynchronize(s2_);
+    cudaStreamDestroy(s2_);
+    cudaEventDestroy(ev_fork_);
+    cudaEventDestroy(ev_asm_);
+    cudaEventDestroy(ev_done_);
+    cudaFreeHost(pf_hang_);
+  }
   cudaFreeHost(hbuf_);
   cudaFreeHost(hstate_);
   cudaFreeHost(hflags_);
@@ -1267,17 +1286,127 @@ void LowRankEngine::phi_from_C() {
 // partial Fisher-Yates over the ascending pool), their Galerkin solutions
 // (kept in cand_), full-space residual norms, the p largest (ties by angle).
 GreedyOutcome LowRankEngine::greedy_subsample(const std::vector<char>& sampled, int p, int q, SubsampleRng& rng) {
-  GreedyOutcome g;
   std::vector<int> pool;
   for (int j = 0; j < nomega_; ++j)
     if (!sampled[j]) pool.push_back(j);
-  g.candidates = rng.sample_without_replacement(std::move(pool), q);
+  return greedy_evaluate(rng.sample_without_replacement(std::move(pool), q), p, /*use_prefactor=*/false);
+}
+
+// The candidates of the inner iteration that sweeps `next`, drawn now: that
+// iteration marks `next` sampled and then draws from the unsampled pool
+// (low_rank.cpp:217-226), and nothing in between touches the RNG, so the
+// draw is the same one.  None when no angle would remain (the loop then ends
+// as exhausted without a draw).  The distinct candidate systems are factored
+// at the current rank on s2_ (not for inflow problems, whose right-hand
+// sides are per angle, nor sharded, nor while the one-CTA solve is faster).
+void LowRankEngine::predraw(const std::vector<char>& sampled, const std::vector<int>& next, int q,
+                            SubsampleRng& rng) {
+  pf_.have_cands = pf_.factored = false;
+  if (!prefactor_on_) return;
+  std::vector<char> mark(sampled);
+  for (int j : next) mark[j] = 1;
+  std::vector<int> pool;
+  for (int j = 0; j < nomega_; ++j)
+    if (!mark[j]) pool.push_back(j);
+  if (pool.empty()) return;
+  pf_.cands = rng.sample_without_replacement(std::move(pool), q);
+  pf_.have_cands = true;
+  static const int min_rank = [] {
+    const char* e = std::getenv("RTLR_LU_PREFACTOR_MIN");
+    return e ? std::atoi(e) : 64;
+  }();
+  const int m = static_cast<int>(pf_.cands.size());
+  if (hp_.bc_any || P_.sharded() || nslice_ > 1 || rank_ <= min_rank || m == 0 || m > 256 ||
+      static_cast<int>(next.size()) > 8 || !galerkin_border_fits(rank_, 8))
+    return;
+  pf_.reps.clear();
+  pf_.pos.assign(m, 0);
+  std::vector<int> seen(P_.uniq_rep_.size(), -1);
+  for (int k = 0; k < m; ++k) {
+    const int u = P_.uniq_of_[pf_.cands[k]];
+    if (seen[u] < 0) {
+      seen[u] = static_cast<int>(pf_.reps.size());
+      pf_.reps.push_back(pf_.cands[k]);
+    }
+    pf_.pos[k] = seen[u];
+  }
+  const int mr = static_cast<int>(pf_.reps.size());
+  const size_t need = static_cast<size_t>(mr) * galerkin_work_per_system(rank_);
+  if (pfw_.size() < need) {
+    RTLR_CUDA(cudaStreamSynchronize(s2_));
+    pfw_.ensure(static_cast<size_t>(mr) * galerkin_work_per_system(std::min<int>(rmax_, rank_ + 64)));
+  }
+  std::memcpy(pf_hang_, pf_.reps.data(), mr * sizeof(int));
+  RTLR_CUDA(cudaMemcpyAsync(pf_ang_.ensure(256), pf_hang_, mr * sizeof(int), cudaMemcpyHostToDevice, s_));
+  RTLR_CUDA(cudaEventRecord(ev_fork_, s_));
+  RTLR_CUDA(cudaStreamWaitEvent(s2_, ev_fork_, 0));
+  galerkin_prefactor(rank_, mr, pf_ang_.get(), dirs_, proj_.get(), ldp_, ldp_ * ldp_, prhs_.get(), pfw_.get(), s2_,
+                     ev_asm_);
+  RTLR_CUDA(cudaEventRecord(ev_done_, s2_));
+  pf_.r0 = rank_;
+  pf_.factored = true;
+}
+
+// The candidates' Galerkin solutions (kept in cand_), full-space residual
+// norms, the p largest (ties by angle) (low_rank.cpp:227-252).
+GreedyOutcome LowRankEngine::greedy_evaluate(std::vector<int> cands_in, int p, bool use_prefactor) {
+  GreedyOutcome g;
+  g.candidates = std::move(cands_in);
   const std::vector<int>& cands = g.candidates;
   const int m = static_cast<int>(cands.size());
   if (m == 0) return g;
   double* csol = cand_.ensure(static_cast<size_t>(rank_) * padded(m));
   pt_.start("galerkin_q");
-  galerkin(cands, csol, rank_);
+  const int k_new = rank_ - pf_.r0;
+  if (use_prefactor && pf_.factored && pf_.r0 == prev_rank_ && k_new >= 0 && galerkin_border_fits(pf_.r0, k_new)) {
+    const int mr = static_cast<int>(pf_.reps.size());
+    ++gal_calls_;
+    gal_systems_ += mr;
+    ++pf_used_;
+    {  // on the critical path: the border's three triangular solves per system
+      const double r = rank_;
+      pt_.work(8.0 * mr * 1.5 * r * r, mr * (3.0 * r * r * (k_new + 1)));
+    }
+    RTLR_CUDA(cudaStreamWaitEvent(s_, ev_done_, 0));
+    double* tmp = mr < m ? gsol_.ensure(static_cast<size_t>(rank_) * mr) : csol;
+    int* flags = flags_.ensure(mr);
+    galerkin_border_solve(pf_.r0, k_new, mr, pf_ang_.get(), dirs_, proj_.get(), ldp_, ldp_ * ldp_, prhs_.get(),
+                          pfw_.get(), tmp, rank_, flags, s_);
+    or_flags_kernel<<<1, 256, 0, s_>>>(mr, flags, gal_bad_.get());
+    if (mr < m) {
+      int* dpos = upload_ints(pos_, pf_.pos);
+      gather_cols<<<g1(static_cast<long long>(rank_) * m), 256, 0, s_>>>(rank_, m, dpos, tmp, rank_, csol, rank_);
+    }
+    RTLR_CUDA(cudaGetLastError());
+    static const bool check = [] {  // RTLR_LU_PREFACTOR=check: against the full pivoted LU, worst column reported
+      const char* e = std::getenv("RTLR_LU_PREFACTOR");
+      return e && std::string(e) == "check";
+    }();
+    if (check) {
+      std::vector<double> a(static_cast<size_t>(rank_) * m), b(a.size());
+      RTLR_CUDA(cudaMemcpyAsync(a.data(), csol, a.size() * sizeof(double), cudaMemcpyDeviceToHost, s_));
+      RTLR_CUDA(cudaStreamSynchronize(s_));
+      DBuf<double> full;
+      galerkin(cands, full.ensure(a.size()), rank_);
+      RTLR_CUDA(cudaMemcpyAsync(b.data(), full.get(), b.size() * sizeof(double), cudaMemcpyDeviceToHost, s_));
+      RTLR_CUDA(cudaStreamSynchronize(s_));
+      double worst = 0.0;
+      for (int c = 0; c < m; ++c) {
+        double d2 = 0.0, n2 = 0.0;
+        for (int i = 0; i < rank_; ++i) {
+          const double x = a[i + static_cast<size_t>(c) * rank_], y = b[i + static_cast<size_t>(c) * rank_];
+          d2 += (x - y) * (x - y);
+          n2 += y * y;
+        }
+        worst = std::max(worst, std::sqrt(d2 / std::max(n2, 1e-300)));
+      }
+      pf_check_worst_ = std::max(pf_check_worst_, worst);
+    }
+  } else {
+    if (pf_.factored) ++pf_missed_;
+    galerkin(cands, csol, rank_);
+  }
+  pf_.factored = false;
   pt_.stop();
   pt_.start("residual_q");
   g.residual_norms = residual_norms(cands, csol, rank_, /*mirror_equal=*/true);
@@ -1310,6 +1439,7 @@ void LowRankEngine::load_factors(const double* d_C, const double* d_X, int r) {
 InnerResult LowRankEngine::inner(const double* d_phi_prev, SubsampleRng& rng) {
   if (prm_.p < 1 || prm_.q < prm_.p) throw std::invalid_argument("low_rank_si: need 1 <= p <= q");
   reset(d_phi_prev);
+  pf_.have_cands = pf_.factored = false;
   std::vector<char> sampled(nomega_, 0);
   InnerResult out;
   std::vector<int> all(nomega_);
@@ -1339,6 +1469,9 @@ InnerResult LowRankEngine::inner(const double* d_phi_prev, SubsampleRng& rng) {
       sampled[j] = 1;
       out.sampled_order.push_back(j);
     }
+    // (the prefactor's assembly reads the projections at the old rank:
+    // it precedes this iteration's growth and border writes)
+    if (pf_.factored) RTLR_CUDA(cudaStreamWaitEvent(s_, ev_asm_, 0));
     pt_.start("cgs");
     const bool reorth = mgs_ro_update(S, next);
     pt_.stop();
@@ -1353,7 +1486,13 @@ InnerResult LowRankEngine::inner(const double* d_phi_prev, SubsampleRng& rng) {
       phi_from_C();
       break;
     }
-    const GreedyOutcome g = greedy_subsample(sampled, prm_.p, prm_.q, rng);
+    GreedyOutcome g;
+    if (pf_.have_cands) {
+      pf_.have_cands = false;
+      g = greedy_evaluate(std::move(pf_.cands), prm_.p, /*use_prefactor=*/!reorth);
+    } else {
+      g = greedy_subsample(sampled, prm_.p, prm_.q, rng);
+    }
     const std::vector<int>& cands = g.candidates;
     const double* csol = cand_.get();
     const double max_residual = g.max_residual;
@@ -1429,7 +1568,9 @@ InnerResult LowRankEngine::inner(const double* d_phi_prev, SubsampleRng& rng) {
       }
       RTLR_CUDA(cudaMemcpyAsync(phi_old_.get(), phi_.get(), n_ * sizeof(double), cudaMemcpyDeviceToDevice, s_));
     }
+    predraw(sampled, next, prm_.q, rng);
   }
+  pf_.have_cands = pf_.factored = false;
   flags_enqueue();
   RTLR_CUDA(cudaStreamSynchronize(s_));
   flags_check();
@@ -1656,15 +1797,18 @@ SolveReport Problem::solve_low_rank(const LowRankOptions& o) {
   }
   if (!rep.converged)
     RTLR_CUDA(cudaMemcpyAsync(phi, eng.phi(), n * sizeof(double), cudaMemcpyDeviceToDevice, stream_));
+  if (eng.pf_check_worst_ > 0.0)
+    std::fprintf(stderr, "[rtlr prefactor] bordered vs full pivoted LU over %lld candidate batches: worst relative difference of a solution %.3e\n",
+                 eng.pf_used_, eng.pf_check_worst_);
   if (eng.pt_.on) {
     std::fprintf(stderr, "[rtlr profile] low-rank phases (s):");
     for (auto& e : eng.pt_.acc) std::fprintf(stderr, " %s=%.4f", e.first.c_str(), e.second);
     std::fprintf(stderr,
                  " | reorth: %d rebuilds, %.4f s (inside cgs) | cgs: block %.4f (GEMMs %.4f), per-snapshot %.4f | svd: %d calls, "
-                 "%d Jacobi sweeps | galerkin: %lld batches, %lld systems | verify: %lld passes, %lld angles | "
+                 "%d Jacobi sweeps | galerkin: %lld batches, %lld systems (prefactored %lld, fell back %lld) | verify: %lld passes, %lld angles | "
                  "device allocations (process): %lld (%lld reused), %.1f GB, %.4f s (free %.4f, malloc %.4f)\n",
                  eng.reorth_count_, eng.reorth_seconds_, eng.cgs_split_[0], eng.cgs_split_[3], eng.cgs_split_[1], eng.svd_calls_,
-                 eng.svd_sweeps_, eng.gal_calls_, eng.gal_systems_, eng.verify_calls_, eng.verify_angles_,
+                 eng.svd_sweeps_, eng.gal_calls_, eng.gal_systems_, eng.pf_used_, eng.pf_missed_, eng.verify_calls_, eng.verify_angles_,
                  alloc_stats().count, alloc_stats().reused, alloc_stats().bytes / 1e9, alloc_stats().seconds,
                  alloc_stats().free_s,
                  alloc_stats().malloc_s);

@@ -173,6 +173,8 @@ class LowRankEngine {
   int svd_sweeps_ = 0, svd_calls_ = 0;
   long long gal_calls_ = 0, gal_systems_ = 0;
   long long verify_calls_ = 0, verify_angles_ = 0;
+  double pf_check_worst_ = 0.0;  // RTLR_LU_PREFACTOR=check
+  long long pf_used_ = 0, pf_missed_ = 0;  // prefactored candidate batches finished by bordering / redone in full
   double reorth_seconds_ = 0.0;  // their wall time (meaningful with RTLR_PROFILE=1)
   double cgs_split_[4] = {0, 0, 0, 0};  // RTLR_PROFILE: block GEMMs + host / per-snapshot loop / overlap / GEMMs only
   void lap(int slot, std::chrono::steady_clock::time_point& t) {
@@ -299,6 +301,24 @@ class LowRankEngine {
   DBuf<int> gal_bad_, chol_flag_;
   IntRing ring_;
   int rank_ = 0, n_snap_ = 0, prev_rank_ = 0;
+  // The greedy candidates one inner iteration ahead (lowrank.cu predraw):
+  // drawn as soon as the next batch of angles is fixed (the pool and the
+  // RNG state are then what greedy_subsample will see), their systems
+  // factored at the current rank on s2_ while the next sweep, CGS and
+  // projection update run, finished by bordering (dense.cu).
+  struct Prefactor {
+    bool have_cands = false, factored = false;
+    int r0 = 0;
+    std::vector<int> cands, reps, pos;
+  } pf_;
+  bool prefactor_on_ = true;
+  cudaStream_t s2_ = nullptr;
+  cudaEvent_t ev_fork_ = nullptr, ev_asm_ = nullptr, ev_done_ = nullptr;
+  DBuf<double> pfw_;
+  DBuf<int> pf_ang_;
+  int* pf_hang_ = nullptr;  // pinned staging of the distinct candidates
+  void predraw(const std::vector<char>& sampled, const std::vector<int>& next, int q, SubsampleRng& rng);
+  GreedyOutcome greedy_evaluate(std::vector<int> cands, int p, bool use_prefactor);
   DBuf<double> rec_;  // coefficient record, rmax x N_Omega (ld ldr_), device-resident
   long long ldr_ = 0;
   int rec_cols_ = 0;

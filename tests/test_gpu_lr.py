@@ -301,3 +301,40 @@ def test_verification_skips_mirrors_of_sampled_angles(tmp_path):
             assert worst and max(worst) < 1e-3 * 1e-7
     assert np.array_equal(out["eval"], out["skip"])
     assert np.array_equal(out["eval"], out["check"])
+
+
+def _coercive_projections(r, rng):
+    """Five r x r matrices shaped like the reduced operators: upwind
+    derivative projections (skew part plus a positive semidefinite flux
+    part) and a positive definite Sigma_t projection."""
+    out = []
+    for _ in range(4):
+        g = rng.standard_normal((r, r)) / np.sqrt(r)
+        h = rng.standard_normal((r, r)) / np.sqrt(r)
+        out.append(g - g.T + 0.3 * h @ h.T)
+    h = rng.standard_normal((r, r)) / np.sqrt(r)
+    out.append(np.eye(r) + 0.2 * h @ h.T)
+    return out
+
+
+@pytest.mark.parametrize("r0,k,m", [(65, 8, 16), (100, 4, 16), (160, 8, 7), (257, 8, 16), (300, 0, 3), (333, 5, 16),
+                                    (600, 8, 16), (40, 3, 5), (31, 8, 2)])
+def test_bordered_galerkin_solve(r0, k, m):
+    """The greedy candidates' prefactored systems (rank r0 factors finished
+    with k border columns, dense.cu galerkin_border_kernel) against the
+    pivoted LU at rank r0 + k and against LAPACK."""
+    rng = np.random.default_rng(1000 * r0 + k)
+    r = r0 + k
+    proj = _coercive_projections(r, rng)
+    nd = 24
+    th = rng.uniform(0, 2 * np.pi, nd)
+    dirs = np.stack([np.cos(th), np.sin(th), rng.uniform(0.1, 0.9, nd)], axis=1)
+    angles = rng.choice(nd, size=m, replace=False)
+    prhs = rng.standard_normal(r)
+    full, bord = P.dense_galerkin_border(r0, k, angles, dirs, proj, prhs)
+    for c, j in enumerate(angles):
+        ox, oy = dirs[j, 0], dirs[j, 1]
+        a = ox * proj[0 if ox >= 0 else 1] + oy * proj[2 if oy >= 0 else 3] + proj[4]
+        ref = np.linalg.solve(a, prhs)
+        assert np.linalg.norm(full[:, c] - ref) <= 1e-11 * np.linalg.norm(ref)
+        assert np.linalg.norm(bord[:, c] - ref) <= 1e-11 * np.linalg.norm(ref), (r0, k, c)
