@@ -296,6 +296,8 @@ class LowRankEngine {
   DBuf<int> ang_, ang2_, flags_, pos_, rfrom_;
   DBuf<double> tpart_, gath_, npart_;
   double* hbuf_ = nullptr;
+  double* hnorm_ = nullptr;  // pinned: residual norms read back per greedy step / verification pass
+  size_t hnorm_cap_ = 0;
   void* hstate_ = nullptr;  // pinned CgsState read back once per CGS batch
   int* hflags_ = nullptr;   // pinned: [0] Galerkin non-finite, [1] sweep singular block
   DBuf<int> gal_bad_, chol_flag_;
