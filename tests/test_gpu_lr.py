@@ -338,3 +338,44 @@ def test_bordered_galerkin_solve(r0, k, m):
         ref = np.linalg.solve(a, prhs)
         assert np.linalg.norm(full[:, c] - ref) <= 1e-11 * np.linalg.norm(ref)
         assert np.linalg.norm(bord[:, c] - ref) <= 1e-11 * np.linalg.norm(ref), (r0, k, c)
+
+
+_PREFACTOR_RUN = r'''
+import sys, numpy as np
+sys.path.insert(0, sys.argv[1])
+import paper_2603_25233_b200 as P
+g = P.Problem("C3", nx=48, ny=48, n_theta=24, n_omega_z=8)
+r = g.solve_low_rank(build_factors=0)
+np.save(sys.argv[2], np.concatenate([[r.iterations, sum(r.history("inner_iterations"))], r.history("rank"), r.phi]))
+'''
+
+
+def test_prefactored_candidates_keep_the_solve(tmp_path):
+    """The greedy candidates' systems factored one inner iteration ahead on
+    the second stream and finished by bordering (lowrank.cu predraw,
+    dense.cu galerkin_border_kernel), from rank 8 up here: every bordered
+    batch equals the full pivoted LU to rounding (the check mode compares
+    them in situ), the solve is reproducible run to run, and against the
+    solve without the look-ahead the outer iterations and ranks are equal
+    and phi agrees far inside the low-rank tolerance."""
+    import os
+    import re
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    out, err = {}, {}
+    for tag, v in (("on", "1"), ("on2", "1"), ("off", "0"), ("check", "check")):
+        f = str(tmp_path / f"pf_{tag}.npy")
+        env = dict(os.environ, RTLR_LU_PREFACTOR=v, RTLR_LU_PREFACTOR_MIN="8")
+        res = subprocess.run([sys.executable, "-c", _PREFACTOR_RUN, root, f], env=env, check=True, timeout=600,
+                             capture_output=True, text=True)
+        out[tag], err[tag] = np.load(f), res.stderr
+    assert np.array_equal(out["on"], out["on2"])
+    assert np.array_equal(out["on"], out["check"])
+    m = re.search(r"over (\d+) candidate batches: worst relative difference of a solution ([0-9.e+-]+)", err["check"])
+    assert m, err["check"][-400:]
+    assert int(m.group(1)) >= 20 and float(m.group(2)) <= 1e-12, m.group(0)
+    nit = int(out["off"][0])
+    assert out["on"][0] == out["off"][0]
+    assert np.array_equal(out["on"][2:2 + nit], out["off"][2:2 + nit])  # ranks per outer iteration
+    assert rel(out["on"][2 + nit:], out["off"][2 + nit:]) <= 1e-9
