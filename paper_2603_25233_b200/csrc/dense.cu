@@ -2552,14 +2552,25 @@ __global__ void __launch_bounds__(256) lu_backsolve_cta(int r, const double* __r
 // reduced operators' symmetric part is positive definite (Sigma_t > 0 plus
 // the upwind flux terms), so the leading block is as well conditioned as the
 // whole, and the solutions agree to rounding (tests/test_gpu_lr.py).
-constexpr int kBorderMax = 8;
-constexpr int kBorderScratch = 2 * 32 * 33 + 64 + 16 * 72 + 72 + 8;
-size_t border_smem_bytes(int r0) {
-  return (static_cast<size_t>(r0) * (2 * kBorderMax + 1) + kBorderScratch) * sizeof(double);
+constexpr int kBorderMax = 16;  // widest border (the template's KB is 8 or 16)
+template <int KB>
+constexpr int border_scratch() {
+  return 2 * 32 * 33 + 64 + 16 * KB * (KB + 1) + KB * (KB + 1) + KB;
+}
+size_t border_smem_bytes(int r0, int kb) {
+  const int scratch = kb <= 8 ? border_scratch<8>() : border_scratch<16>();
+  const int w = kb <= 8 ? 8 : 16;
+  return (static_cast<size_t>(r0) * (2 * w + 1) + scratch) * sizeof(double);
 }
 __device__ __forceinline__ void bar_group(int id) { asm volatile("bar.sync %0, 256;" ::"r"(id) : "memory"); }
 
+// KB: the border's column capacity (8: the greedy candidates, one inner
+// iteration ahead; 16: build_full_coefficients' systems reused over two
+// iterations).  sysidx (optional): CTA b finishes stored system sysidx[b]
+// (its angle angles[sysidx[b]]) into solution column b.
+template <int KB>
 __global__ void __launch_bounds__(512, 1) galerkin_border_kernel(int r0, int k, const int* __restrict__ angles,
+                                                                 const int* __restrict__ sysidx,
                                                                  const double* __restrict__ dirs,
                                                                  const double* __restrict__ proj, long long ldp,
                                                                  long long pstride, const double* __restrict__ prhs,
@@ -2567,16 +2578,18 @@ __global__ void __launch_bounds__(512, 1) galerkin_border_kernel(int r0, int k, 
                                                                  const int* __restrict__ pivall,
                                                                  double* __restrict__ sol, long long ldsol,
                                                                  int* __restrict__ flags) {
+  constexpr int NP = KB * (KB + 1);  // entries of [S | y1]
+  constexpr int NQ = (NP + 31) / 32;
   extern __shared__ __align__(16) double bsm[];
-  double* Vt = bsm;                                  // r0 x 8: A01 -> U01 (row i: its 8 columns)
-  double* Wt = Vt + static_cast<size_t>(r0) * 8;     // r0 x 8: A10^T -> L10^T
-  double* ys = Wt + static_cast<size_t>(r0) * 8;     // y0 -> y0 - U01 x1 -> x0
-  double* ub = ys + r0;                              // back substitution scratch
-  double* red = ub + 2 * 32 * 33 + 64;               // 16 x 72 partial sums
-  double* Ss = red + 16 * 72;                        // 8 x 9: [S | y1]
-  double* x1 = Ss + 72;
+  double* Vt = bsm;                                   // r0 x KB: A01 -> U01 (row i: its KB columns)
+  double* Wt = Vt + static_cast<size_t>(r0) * KB;     // r0 x KB: A10^T -> L10^T
+  double* ys = Wt + static_cast<size_t>(r0) * KB;     // y0 -> y0 - U01 x1 -> x0
+  double* ub = ys + r0;                               // back substitution scratch
+  double* red = ub + 2 * 32 * 33 + 64;                // 16 x NP partial sums
+  double* Ss = red + 16 * NP;                         // KB x (KB + 1): [S | y1]
+  double* x1 = Ss + NP;
   const int tid = threadIdx.x, lane = tid & 31;
-  const int sys = blockIdx.x;
+  const int sys = sysidx ? sysidx[blockIdx.x] : blockIdx.x;
   const double* F = Fall + static_cast<size_t>(sys) * r0 * (r0 + 1);
   const int* pv = pivall + static_cast<size_t>(sys) * r0;
   const int ang = angles[sys];
@@ -2599,16 +2612,15 @@ __global__ void __launch_bounds__(512, 1) galerkin_border_kernel(int r0, int k, 
   }
   if (tid < 256) {
     const int gt = tid, gw = gt >> 5;
-    for (int t = 0; t < kBorderMax; ++t)
-      for (int i = gt; i < r0; i += 256) Vt[i * 8 + t] = t < k ? a_at(i, r0 + t) : 0.0;
+    for (int t = 0; t < KB; ++t)
+      for (int i = gt; i < r0; i += 256) Vt[i * KB + t] = t < k ? a_at(i, r0 + t) : 0.0;
     for (int i = gt; i < r0; i += 256) ys[i] = F[i + static_cast<size_t>(r0) * r0];
     bar_group(1);
     for (int k0 = 0; k0 < r0;) {
       const int jb = lu_panel_width(r0, k0);
-      if (gw < k) {  // warp gw: column gw through the panel's swaps and its unit-lower block
-        const int t = gw;
+      for (int t = gw; t < k; t += 8) {  // a warp: column t through the panel's swaps and its unit-lower block
         const int pvl = lane < jb ? pv[k0 + lane] : 0;
-        double v = lane < jb ? Vt[(k0 + lane) * 8 + t] : 0.0;
+        double v = lane < jb ? Vt[(k0 + lane) * KB + t] : 0.0;
         double Lr[32];
 #pragma unroll
         for (int l = 0; l < 32; ++l)
@@ -2623,8 +2635,8 @@ __global__ void __launch_bounds__(512, 1) galerkin_border_kernel(int r0, int k, 
             if (lane == b - k0) v = vj;
           } else {
             if (lane == j) {
-              v = Vt[b * 8 + t];
-              Vt[b * 8 + t] = vj;
+              v = Vt[b * KB + t];
+              Vt[b * KB + t] = vj;
             }
             __syncwarp();
           }
@@ -2634,30 +2646,34 @@ __global__ void __launch_bounds__(512, 1) galerkin_border_kernel(int r0, int k, 
           const double vl = __shfl_sync(0xffffffffu, v, l);
           if (lane > l) v -= Lr[l] * vl;
         }
-        if (lane < jb) Vt[(k0 + lane) * 8 + t] = v;
+        if (lane < jb) Vt[(k0 + lane) * KB + t] = v;
       }
       bar_group(1);
       for (int i = k0 + jb + gt; i < r0; i += 256) {
         const double* Li = F + i + static_cast<size_t>(k0) * r0;
-        double acc[8] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
+#pragma unroll
+        for (int hb = 0; hb < KB; hb += 8) {  // 8 columns at a time (registers)
+          if (hb >= k) break;
+          double acc[8] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
 #pragma unroll 8
-        for (int l = 0; l < jb; ++l) {
-          const double lv = Li[static_cast<size_t>(l) * r0];
-          const double2* vr = reinterpret_cast<const double2*>(Vt + (k0 + l) * 8);
+          for (int l = 0; l < jb; ++l) {
+            const double lv = Li[static_cast<size_t>(l) * r0];
+            const double2* vr = reinterpret_cast<const double2*>(Vt + (k0 + l) * KB + hb);
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+              const double2 vv = vr[q];
+              acc[2 * q] += lv * vv.x;
+              acc[2 * q + 1] += lv * vv.y;
+            }
+          }
+          double2* vo = reinterpret_cast<double2*>(Vt + i * KB + hb);
 #pragma unroll
           for (int q = 0; q < 4; ++q) {
-            const double2 vv = vr[q];
-            acc[2 * q] += lv * vv.x;
-            acc[2 * q + 1] += lv * vv.y;
+            double2 vv = vo[q];
+            vv.x -= acc[2 * q];
+            vv.y -= acc[2 * q + 1];
+            vo[q] = vv;
           }
-        }
-        double2* vo = reinterpret_cast<double2*>(Vt + i * 8);
-#pragma unroll
-        for (int q = 0; q < 4; ++q) {
-          double2 vv = vo[q];
-          vv.x -= acc[2 * q];
-          vv.y -= acc[2 * q + 1];
-          vo[q] = vv;
         }
       }
       bar_group(1);
@@ -2667,13 +2683,12 @@ __global__ void __launch_bounds__(512, 1) galerkin_border_kernel(int r0, int k, 
     const int gt = tid - 256, gw = gt >> 5;
     for (int j = gt; j < r0; j += 256)
 #pragma unroll
-      for (int u = 0; u < kBorderMax; ++u) Wt[j * 8 + u] = u < k ? a_at(r0 + u, j) : 0.0;
+      for (int u = 0; u < KB; ++u) Wt[j * KB + u] = u < k ? a_at(r0 + u, j) : 0.0;
     bar_group(2);
     for (int c0 = 0; c0 < r0; c0 += 32) {
       const int bs = min(32, r0 - c0);
-      if (gw < k) {  // warp gw: new row gw against the upper 32 x 32 diagonal block
-        const int u = gw;
-        double sv = lane < bs ? Wt[(c0 + lane) * 8 + u] : 0.0;
+      for (int u = gw; u < k; u += 8) {  // a warp: new row u against the upper 32 x 32 diagonal block
+        double sv = lane < bs ? Wt[(c0 + lane) * KB + u] : 0.0;
         const double rinv = lane < bs ? 1.0 / F[c0 + lane + static_cast<size_t>(c0 + lane) * r0] : 1.0;
         double Uc[32];  // U[c0 + i][c0 + lane], i < lane
 #pragma unroll
@@ -2685,115 +2700,129 @@ __global__ void __launch_bounds__(512, 1) galerkin_border_kernel(int r0, int k, 
           if (lane == i) sv = xi;
           if (lane > i) sv -= xi * Uc[i];
         }
-        if (lane < bs) Wt[(c0 + lane) * 8 + u] = sv;
+        if (lane < bs) Wt[(c0 + lane) * KB + u] = sv;
       }
       bar_group(2);
       for (int j = c0 + bs + gt; j < r0; j += 256) {
         const double* Uj = F + c0 + static_cast<size_t>(j) * r0;
-        double acc[8] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
+#pragma unroll
+        for (int hb = 0; hb < KB; hb += 8) {
+          if (hb >= k) break;
+          double acc[8] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
 #pragma unroll 8
-        for (int i = 0; i < bs; ++i) {
-          const double uv = Uj[i];
-          const double2* wr = reinterpret_cast<const double2*>(Wt + (c0 + i) * 8);
+          for (int i = 0; i < bs; ++i) {
+            const double uv = Uj[i];
+            const double2* wr = reinterpret_cast<const double2*>(Wt + (c0 + i) * KB + hb);
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+              const double2 ww = wr[q];
+              acc[2 * q] += uv * ww.x;
+              acc[2 * q + 1] += uv * ww.y;
+            }
+          }
+          double2* wo = reinterpret_cast<double2*>(Wt + j * KB + hb);
 #pragma unroll
           for (int q = 0; q < 4; ++q) {
-            const double2 ww = wr[q];
-            acc[2 * q] += uv * ww.x;
-            acc[2 * q + 1] += uv * ww.y;
+            double2 ww = wo[q];
+            ww.x -= acc[2 * q];
+            ww.y -= acc[2 * q + 1];
+            wo[q] = ww;
           }
-        }
-        double2* wo = reinterpret_cast<double2*>(Wt + j * 8);
-#pragma unroll
-        for (int q = 0; q < 4; ++q) {
-          double2 ww = wo[q];
-          ww.x -= acc[2 * q];
-          ww.y -= acc[2 * q + 1];
-          wo[q] = ww;
         }
       }
       bar_group(2);
     }
   }
   __syncthreads();
-  {  // [L10 U01 | L10 y0]: warp w sums rows w, w + 16, ...; a lane holds pairs lane, lane + 32, lane + 64
+  {  // [L10 U01 | L10 y0]: warp w sums rows w, w + 16, ...; a lane holds pairs lane, lane + 32, ...
     const int w = tid >> 5;
-    double acc[3] = {0.0, 0.0, 0.0};
+    double acc[NQ];
+#pragma unroll
+    for (int q = 0; q < NQ; ++q) acc[q] = 0.0;
     for (int i = w; i < r0; i += 16) {
 #pragma unroll
-      for (int q = 0; q < 3; ++q) {
+      for (int q = 0; q < NQ; ++q) {
         const int pr = lane + 32 * q;
-        if (pr < 72) {
-          const int u = pr / 9, t = pr - 9 * u;
-          acc[q] += Wt[i * 8 + u] * (t < 8 ? Vt[i * 8 + t] : ys[i]);
+        if (pr < NP) {
+          const int u = pr / (KB + 1), t = pr - (KB + 1) * u;
+          acc[q] += Wt[i * KB + u] * (t < KB ? Vt[i * KB + t] : ys[i]);
         }
       }
     }
 #pragma unroll
-    for (int q = 0; q < 3; ++q)
-      if (lane + 32 * q < 72) red[w * 72 + lane + 32 * q] = acc[q];
+    for (int q = 0; q < NQ; ++q)
+      if (lane + 32 * q < NP) red[w * NP + lane + 32 * q] = acc[q];
   }
   __syncthreads();
-  if (tid < 72) {
+  if (tid < NP) {
     double sum = 0.0;
-    for (int w = 0; w < 16; ++w) sum += red[w * 72 + tid];
-    const int u = tid / 9, t = tid - 9 * u;
+    for (int w = 0; w < 16; ++w) sum += red[w * NP + tid];
+    const int u = tid / (KB + 1), t = tid - (KB + 1) * u;
     double base;  // identity padding past k
     if (u < k && t < k)
       base = a_at(r0 + u, r0 + t);
-    else if (u < k && t == 8)
+    else if (u < k && t == KB)
       base = prhs[r0 + u];
     else
       base = (t == u) ? 1.0 : 0.0;
     Ss[tid] = base - sum;
   }
   __syncthreads();
-  if (tid == 0) {  // 8 x 8 partial-pivot elimination of [S | y1]
-    for (int c = 0; c < 8; ++c) {
-      int p = c;
-      double best = fabs(Ss[c * 9 + c]);
-      for (int i = c + 1; i < 8; ++i)
-        if (fabs(Ss[i * 9 + c]) > best) {
-          best = fabs(Ss[i * 9 + c]);
-          p = i;
+  if (tid < 32) {  // KB x KB partial-pivot elimination of [S | y1]: lane = row
+    constexpr int LD = KB + 1;
+    for (int c = 0; c < KB; ++c) {
+      double av = (lane >= c && lane < KB) ? fabs(Ss[lane * LD + c]) : -1.0;
+      int ai = lane;
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        const double ov = __shfl_xor_sync(0xffffffffu, av, o);
+        const int oi = __shfl_xor_sync(0xffffffffu, ai, o);
+        if (ov > av || (ov == av && oi < ai)) {
+          av = ov;
+          ai = oi;
         }
-      if (p != c)
-        for (int j = c; j < 9; ++j) {
-          const double tmp = Ss[c * 9 + j];
-          Ss[c * 9 + j] = Ss[p * 9 + j];
-          Ss[p * 9 + j] = tmp;
-        }
-      const double d = Ss[c * 9 + c];
-      for (int i = c + 1; i < 8; ++i) {
-        const double mlt = Ss[i * 9 + c] / d;
-        for (int j = c + 1; j < 9; ++j) Ss[i * 9 + j] -= mlt * Ss[c * 9 + j];
       }
+      const int p = ai;  // first row of largest magnitude
+      if (p != c && lane <= KB) {  // lane = column: swap rows c and p
+        const double tmp = Ss[c * LD + lane];
+        Ss[c * LD + lane] = Ss[p * LD + lane];
+        Ss[p * LD + lane] = tmp;
+      }
+      __syncwarp();
+      if (lane > c && lane < KB) {
+        const double mlt = Ss[lane * LD + c] / Ss[c * LD + c];
+        for (int j = c + 1; j <= KB; ++j) Ss[lane * LD + j] -= mlt * Ss[c * LD + j];
+      }
+      __syncwarp();
     }
-    for (int i = 7; i >= 0; --i) {
-      double x = Ss[i * 9 + 8];
-      for (int j = i + 1; j < 8; ++j) x -= Ss[i * 9 + j] * x1[j];
-      x1[i] = x / Ss[i * 9 + i];
-    }
+    if (lane == 0)
+      for (int i = KB - 1; i >= 0; --i) {
+        double x = Ss[i * LD + KB];
+        for (int j = i + 1; j < KB; ++j) x -= Ss[i * LD + j] * x1[j];
+        x1[i] = x / Ss[i * LD + i];
+      }
   }
   __syncthreads();
   for (int i = tid; i < r0; i += 512) {
     double z = ys[i];
 #pragma unroll
-    for (int t = 0; t < 8; ++t) z -= Vt[i * 8 + t] * x1[t];
+    for (int t = 0; t < KB; ++t) z -= Vt[i * KB + t] * x1[t];
     ys[i] = z;
   }
   __syncthreads();
   lu_backsolve_cta_body(r0, F, ys, ub, false);
   int bad = 0;
+  const long long col = static_cast<long long>(blockIdx.x) * ldsol;
   for (int i = tid; i < r0; i += 512) {
-    sol[i + static_cast<long long>(sys) * ldsol] = ys[i];
+    sol[i + col] = ys[i];
     if (!isfinite(ys[i])) bad = 1;
   }
   if (tid < k) {
-    sol[r0 + tid + static_cast<long long>(sys) * ldsol] = x1[tid];
+    sol[r0 + tid + col] = x1[tid];
     if (!isfinite(x1[tid])) bad = 1;
   }
   bad = __syncthreads_or(bad);
-  if (tid == 0) flags[sys] = bad;
+  if (tid == 0) flags[blockIdx.x] = bad;
 }
 
 // R of a Householder QR (Eigen's makeHouseholder conventions, as hh_make)
@@ -3111,6 +3140,27 @@ static void lu_factor_blocked(int r, int m, double* M, int* piv, int* perm, cuda
   }
 }
 
+// Back substitution of m factored systems (column r: the forward-substituted
+// right-hand side) into sol.
+static void lu_backsolve(int r, int m, const double* M, double* sol, long long ldsol, int* flags, cudaStream_t s) {
+  // One CTA per system while the systems do not fill the GPU with warps;
+  // beyond that one warp per system (8 per CTA) has the parallelism.
+  if (m < 8 * 148) {
+    const size_t smem = (static_cast<size_t>(r) + 2 * 32 * 33 + 64) * sizeof(double);
+    if (smem > 48 * 1024)
+      RTLR_CUDA(cudaFuncSetAttribute(lu_backsolve_cta, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     static_cast<int>(smem)));
+    lu_backsolve_cta<<<m, 256, smem, s>>>(r, M, sol, ldsol, flags);
+  } else {
+    const int per = 8;  // systems (warps) per CTA
+    const size_t smem = static_cast<size_t>(per) * (r + 32 * 33) * sizeof(double);
+    if (smem > 48 * 1024)
+      RTLR_CUDA(cudaFuncSetAttribute(lu_backsolve_warp, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     static_cast<int>(smem)));
+    lu_backsolve_warp<<<(m + per - 1) / per, 32 * per, smem, s>>>(r, m, M, sol, ldsol, flags);
+  }
+}
+
 void galerkin_batch(int r, int m, const int* angles, const double* dirs, const double* proj, long long ldp,
                     long long proj_stride, const double* prhs, const double* extra, double* sol, long long ldsol,
                     int* flags, double* work, cudaStream_t s) {
@@ -3139,22 +3189,7 @@ void galerkin_batch(int r, int m, const int* angles, const double* dirs, const d
     lu_assemble<<<dim3(std::max(1, std::min(64, (r * (r + 1) + 255) / 256)), m), 256, 0, s>>>(
         r, angles, dirs, proj, ldp, proj_stride, prhs, extra, ldsol, M);
     lu_factor_blocked(r, m, M, piv, perm, s);
-    // One CTA per system while the systems do not fill the GPU with warps;
-    // beyond that one warp per system (8 per CTA) has the parallelism.
-    if (m < 8 * 148) {
-      const size_t smem = (static_cast<size_t>(r) + 2 * 32 * 33 + 64) * sizeof(double);
-      if (smem > 48 * 1024)
-        RTLR_CUDA(cudaFuncSetAttribute(lu_backsolve_cta, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       static_cast<int>(smem)));
-      lu_backsolve_cta<<<m, 256, smem, s>>>(r, M, sol, ldsol, flags);
-    } else {
-      const int per = 8;  // systems (warps) per CTA
-      const size_t smem = static_cast<size_t>(per) * (r + 32 * 33) * sizeof(double);
-      if (smem > 48 * 1024)
-        RTLR_CUDA(cudaFuncSetAttribute(lu_backsolve_warp, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       static_cast<int>(smem)));
-      lu_backsolve_warp<<<(m + per - 1) / per, 32 * per, smem, s>>>(r, m, M, sol, ldsol, flags);
-    }
+    lu_backsolve(r, m, M, sol, ldsol, flags, s);
     RTLR_CUDA(cudaGetLastError());
     return;
   }
@@ -3184,24 +3219,39 @@ void galerkin_prefactor(int r, int m, const int* angles, const double* dirs, con
   RTLR_CUDA(cudaGetLastError());
 }
 
-bool galerkin_border_fits(int r0, int k) {
-  return r0 >= 1 && k >= 0 && k <= kBorderMax && border_smem_bytes(r0) <= 227 * 1024;
+// The solutions of the systems galerkin_prefactor left in work (rank r, no border).
+void galerkin_factored_solve(int r, int m, const double* work, double* sol, long long ldsol, int* flags,
+                             cudaStream_t s) {
+  if (m <= 0 || r <= 0) return;
+  lu_backsolve(r, m, work, sol, ldsol, flags, s);
+  RTLR_CUDA(cudaGetLastError());
 }
 
-// The solutions at rank r0 + k from the rank-r0 factors galerkin_prefactor left in work.
+bool galerkin_border_fits(int r0, int k) {
+  return r0 >= 1 && k >= 0 && k <= kBorderMax && border_smem_bytes(r0, k) <= 227 * 1024;
+}
+
+// The solutions at rank r0 + k from the rank-r0 factors galerkin_prefactor
+// left in work (m_stored systems); with sysidx, only the m listed systems.
 void galerkin_border_solve(int r0, int k, int m, const int* angles, const double* dirs, const double* proj,
                            long long ldp, long long proj_stride, const double* prhs, const double* work, double* sol,
-                           long long ldsol, int* flags, cudaStream_t s) {
+                           long long ldsol, int* flags, cudaStream_t s, const int* sysidx, int m_stored) {
   if (m <= 0) return;
   if (!galerkin_border_fits(r0, k)) throw std::invalid_argument("galerkin_border_solve: rank or border out of range");
   static const bool attr = [] {
-    RTLR_CUDA(cudaFuncSetAttribute(galerkin_border_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
+    RTLR_CUDA(cudaFuncSetAttribute(galerkin_border_kernel<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
+    RTLR_CUDA(cudaFuncSetAttribute(galerkin_border_kernel<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
     return true;
   }();
   (void)attr;
-  const int* piv = reinterpret_cast<const int*>(work + static_cast<size_t>(m) * r0 * (r0 + 1));
-  galerkin_border_kernel<<<m, 512, border_smem_bytes(r0), s>>>(r0, k, angles, dirs, proj, ldp, proj_stride, prhs, work,
-                                                               piv, sol, ldsol, flags);
+  if (m_stored < 0) m_stored = m;
+  const int* piv = reinterpret_cast<const int*>(work + static_cast<size_t>(m_stored) * r0 * (r0 + 1));
+  if (k <= 8)
+    galerkin_border_kernel<8><<<m, 512, border_smem_bytes(r0, k), s>>>(r0, k, angles, sysidx, dirs, proj, ldp,
+                                                                      proj_stride, prhs, work, piv, sol, ldsol, flags);
+  else
+    galerkin_border_kernel<16><<<m, 512, border_smem_bytes(r0, k), s>>>(r0, k, angles, sysidx, dirs, proj, ldp,
+                                                                       proj_stride, prhs, work, piv, sol, ldsol, flags);
   RTLR_CUDA(cudaGetLastError());
 }
 

@@ -60,15 +60,17 @@ void galerkin_batch(int r, int m, const int* angles, const double* dirs, const d
 
 // The greedy candidates' systems factored one inner iteration ahead (at the
 // rank r0 the basis had then, on another stream) and finished by bordering
-// once the k <= 8 new basis columns' projections exist (dense.cu).  work:
+// once the k <= 16 new basis columns' projections exist (dense.cu).  work:
 // m * galerkin_work_per_system(r0) doubles, shared by the two calls.
 void galerkin_prefactor(int r, int m, const int* angles, const double* dirs, const double* proj, long long ldp,
                         long long proj_stride, const double* prhs, double* work, cudaStream_t s,
                         cudaEvent_t assembled = nullptr);
+void galerkin_factored_solve(int r, int m, const double* work, double* sol, long long ldsol, int* flags,
+                             cudaStream_t s);
 bool galerkin_border_fits(int r0, int k);
 void galerkin_border_solve(int r0, int k, int m, const int* angles, const double* dirs, const double* proj,
                            long long ldp, long long proj_stride, const double* prhs, const double* work, double* sol,
-                           long long ldsol, int* flags, cudaStream_t s);
+                           long long ldsol, int* flags, cudaStream_t s, const int* sysidx = nullptr, int m_stored = -1);
 
 // Householder QR of an m x n (m >= n) column-major matrix (lda), in place;
 // tau (n).  Q formed explicitly into q (m x n).  r (n x n) upper.  Blocked

@@ -318,7 +318,8 @@ def _coercive_projections(r, rng):
 
 
 @pytest.mark.parametrize("r0,k,m", [(65, 8, 16), (100, 4, 16), (160, 8, 7), (257, 8, 16), (300, 0, 3), (333, 5, 16),
-                                    (600, 8, 16), (40, 3, 5), (31, 8, 2)])
+                                    (600, 8, 16), (40, 3, 5), (31, 8, 2), (100, 12, 16), (300, 9, 4), (600, 16, 16),
+                                    (130, 16, 3)])
 def test_bordered_galerkin_solve(r0, k, m):
     """The greedy candidates' prefactored systems (rank r0 factors finished
     with k border columns, dense.cu galerkin_border_kernel) against the
