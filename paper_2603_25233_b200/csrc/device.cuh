@@ -68,6 +68,10 @@ struct SweepArgs {
   // (structure of arrays; see launch_sweep_prefactor).
   const double* pref = nullptr;
   long long pref_stride = 0;
+  // Wide kernel: psi leaves through the consumed source tile (shared memory)
+  // so that each store instruction of a warp covers 1 KB contiguous (set by
+  // the launcher; RTLR_SCAN_STOUT=0 keeps the lanes' own 128-byte runs).
+  int stage_out = 0;
 };
 
 // Per (direction, cell): M^-1 (16, column-major), Qc = -M^-1 K_x (8), G = T_x Qc (4)

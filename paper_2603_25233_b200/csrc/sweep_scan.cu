@@ -233,6 +233,9 @@ __device__ __forceinline__ void tma_load_tile(unsigned dst, const CUtensorMap* m
       "l"(map), "r"(bar), "r"(0), "r"(row)
       : "memory");
 }
+__device__ __forceinline__ void st_shared_v2(unsigned addr, double x, double y) {
+  asm volatile("st.shared.v2.f64 [%0], {%1, %2};" ::"r"(addr), "d"(x), "d"(y) : "memory");
+}
 __device__ __forceinline__ void ld_shared_v2(unsigned addr, double& x, double& y) {
   asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];" : "=d"(x), "=d"(y) : "r"(addr) : "memory");
 }
@@ -302,6 +305,7 @@ struct Dir {
   unsigned ring, bars;      // wide: this warp's ring tiles and mbarriers (shared memory)
   long long src_row0;       // wide: first tensor row of this direction's sources
   int stages;               // wide: ring depth
+  bool stage_out;           // wide: psi through the consumed source tile, 1 KB contiguous per store
   int nx, ny, W, w, pw, nchunk, nrows, pitch;
   int rw, rW;         // row interleave: rows rw, rw + rW, ... (kRows: w, W; else 0, 1)
   int kbeg, kend;     // this warp's chunk range within a row
@@ -839,9 +843,38 @@ __device__ __forceinline__ void sweep_dir_wide(const Dir& d) {
         ti1 = n1;
       }
     }
+    if (d.stage_out) {
+      // psi through the consumed source tile: the lanes write their four
+      // cells where they read the sources (swizzled, conflict free), then
+      // store instruction q takes memory-order cells 32 q + lane, 1 KB
+      // contiguous per instruction instead of 32-byte pieces 128 B apart
+      // (ncu: 52 L1 wavefronts per store instruction, two thirds of the
+      // kernel's L1 data-pipe load, against 8 + the staging's 16).
+      const unsigned tile = d.ring + st * kWTileBytes;
 #pragma unroll
-    for (int c = 0; c < C; ++c)
-      if (act[c]) st_cell256(d.psi + 4 * (cell + kDx * c), ps[c]);
+      for (int c = 0; c < C; ++c) {
+        st_shared_v2(tile + unit(c, 0), ps[c][0], ps[c][1]);
+        st_shared_v2(tile + unit(c, 1), ps[c][2], ps[c][3]);
+      }
+      __syncwarp();
+      const long long gstart = XU ? cell - c0 : cell + c0 - (kWChunk - 1);  // the chunk's first cell in memory
+      const unsigned rsw = static_cast<unsigned>((lane >> 2) & 7);
+      const unsigned lb0 = static_cast<unsigned>((lane >> 2) * 128) + (((2u * (lane & 3)) ^ rsw) << 4);
+      const unsigned lb1 = static_cast<unsigned>((lane >> 2) * 128) + (((2u * (lane & 3) + 1u) ^ rsw) << 4);
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const int m = 32 * q + lane;  // memory-order cell of the tile
+        double o[4];
+        ld_shared_v2(tile + 1024u * q + lb0, o[0], o[1]);
+        ld_shared_v2(tile + 1024u * q + lb1, o[2], o[3]);
+        const int j = XU ? m : kWChunk - 1 - m;  // its sweep-order column within the chunk
+        if (k * kWChunk + j < nx) st_cell256(d.psi + 4 * (gstart + m), o);
+      }
+    } else {
+#pragma unroll
+      for (int c = 0; c < C; ++c)
+        if (act[c]) st_cell256(d.psi + 4 * (cell + kDx * c), ps[c]);
+    }
     if (act[0]) {  // y-outflow traces (per x-mode) for the next row
       double* q0 = d.my_line + wide_line_idx(col - colbase);
 #pragma unroll
@@ -854,7 +887,12 @@ __device__ __forceinline__ void sweep_dir_wide(const Dir& d) {
       }
     }
     __syncwarp();  // (own line: the next row reads what this row wrote; the tile is consumed)
-    if (lane == 0) tma_issue();  // refill the stage this step consumed
+    if (lane == 0) {
+      // (the staged psi was written to the tile through the generic proxy:
+      // ordered before the TMA engine's refill of it)
+      if (d.stage_out) asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      tma_issue();  // refill the stage this step consumed
+    }
     if (++st == S) st = 0, ph ^= 1u;
     if (MULTI && lane == 0) publish_progress(d.prod + d.w, t + 1);
     if (SPLIT && last && d.w + 1 < d.W) {
@@ -993,6 +1031,7 @@ __global__ void __launch_bounds__(256, UNIFORM ? 1 : 2)
   d.bars = smem_u32(tma_bars) + (WIDE ? 8u * kMaxStages * wib : 0u);
   d.src_row0 = static_cast<long long>(slot) * a.rhs_stride / 16;
   d.stages = stages;
+  d.stage_out = a.stage_out != 0;
   if (WIDE) {
     if (lane == 0) {
       for (int u = 0; u < stages; ++u) mbar_init(d.bars + 8u * u, 1);
@@ -1412,7 +1451,13 @@ bool make_source_map(const SweepArgs& a, CUtensorMap* m) {
 
 }  // namespace
 
-void launch_sweep_scan(const SweepArgs& a, bool uniform, cudaStream_t s) {
+void launch_sweep_scan(const SweepArgs& a_in, bool uniform, cudaStream_t s) {
+  SweepArgs a = a_in;
+  static const int stage_out = [] {  // RTLR_SCAN_STOUT=0: the lanes store their own cells (A/B)
+    const char* e = std::getenv("RTLR_SCAN_STOUT");
+    return (e && e[0] == '0') ? 0 : 1;
+  }();
+  a.stage_out = stage_out;
   if (a.n <= 0) return;
   // Launch plan for a chunk width (64 cells, or 128 for the wide kernel).
   struct Plan {
