@@ -68,9 +68,10 @@ struct SweepArgs {
   // (structure of arrays; see launch_sweep_prefactor).
   const double* pref = nullptr;
   long long pref_stride = 0;
-  // Wide kernel: psi leaves through the consumed source tile (shared memory)
-  // so that each store instruction of a warp covers 1 KB contiguous (set by
-  // the launcher; RTLR_SCAN_STOUT=0 keeps the lanes' own 128-byte runs).
+  // Wide kernel: psi leaves through the consumed source tile (shared memory):
+  // 2 one TMA store per whole chunk, 1 a coalesced read-back with 1 KB
+  // contiguous per store instruction, 0 the lanes' own 128-byte runs (set by
+  // the launcher, RTLR_SCAN_STOUT).
   int stage_out = 0;
 };
 

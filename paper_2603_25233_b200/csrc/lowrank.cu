@@ -1335,7 +1335,7 @@ GreedyOutcome LowRankEngine::greedy_subsample(const std::vector<char>& sampled, 
 // draw is the same one.  None when no angle would remain (the loop then ends
 // as exhausted without a draw).  The distinct candidate systems are factored
 // at the current rank on s2_ (not for inflow problems, whose right-hand
-// sides are per angle, nor sharded, nor while the one-CTA solve is faster).
+// sides are per angle, nor while the one-CTA solve is faster).
 void LowRankEngine::predraw(const std::vector<char>& sampled, const std::vector<int>& next, int q,
                             SubsampleRng& rng) {
   pf_.have_cands = pf_.factored = false;
@@ -1353,7 +1353,10 @@ void LowRankEngine::predraw(const std::vector<char>& sampled, const std::vector<
     return e ? std::atoi(e) : 64;
   }();
   const int m = static_cast<int>(pf_.cands.size());
-  if (hp_.bc_any || P_.sharded() || nslice_ > 1 || rank_ <= min_rank || m == 0 || m > 256 ||
+  // (With a communicator every rank factors and finishes all the candidates
+  // itself: the projections are replicated, the work is off the critical
+  // path, and the solutions then need no all-gather.)
+  if (hp_.bc_any || rank_ <= min_rank || m == 0 || m > 256 ||
       static_cast<int>(next.size()) > 8 || !galerkin_border_fits(rank_, 8))
     return;
   pf_.reps.clear();

@@ -233,6 +233,14 @@ __device__ __forceinline__ void tma_load_tile(unsigned dst, const CUtensorMap* m
       "l"(map), "r"(bar), "r"(0), "r"(row)
       : "memory");
 }
+// One 4 KB tile (32 tensor rows of 128 B) from shared memory to the tensor,
+// as a bulk-group store (the TMA engine reads the tile asynchronously).
+__device__ __forceinline__ void tma_store_tile(const CUtensorMap* map, int row, unsigned src) {
+  asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.tile.bulk_group [%0, {%2, %3}], [%1];" ::"l"(map), "r"(src),
+               "r"(0), "r"(row)
+               : "memory");
+  asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+}
 __device__ __forceinline__ void st_shared_v2(unsigned addr, double x, double y) {
   asm volatile("st.shared.v2.f64 [%0], {%1, %2};" ::"r"(addr), "d"(x), "d"(y) : "memory");
 }
@@ -305,7 +313,9 @@ struct Dir {
   unsigned ring, bars;      // wide: this warp's ring tiles and mbarriers (shared memory)
   long long src_row0;       // wide: first tensor row of this direction's sources
   int stages;               // wide: ring depth
-  bool stage_out;           // wide: psi through the consumed source tile, 1 KB contiguous per store
+  int stage_out;            // wide: psi through the consumed source tile: 1 coalesced read-back + stores, 2 TMA store
+  const CUtensorMap* pmap;  // wide, stage_out == 2: the psi tensor (rows of 128 B)
+  long long psi_row0;       // wide: first tensor row of this direction's psi
   int nx, ny, W, w, pw, nchunk, nrows, pitch;
   int rw, rW;         // row interleave: rows rw, rw + rW, ... (kRows: w, W; else 0, 1)
   int kbeg, kend;     // this warp's chunk range within a row
@@ -713,6 +723,10 @@ __device__ __forceinline__ void sweep_dir_wide(const Dir& d) {
       if (++trow < nrows) trow0 = row0_of(trow);
     }
   };
+  // (TMA-store mode refills a slot one step after it was consumed, once the
+  // store that reads it has let go of it)
+  const bool tst = d.stage_out == 2;
+  bool owe = false;
   if (lane == 0)
     for (int u = 0; u < S; ++u) tma_issue();
   // this lane's cells in a tile: memory index m -> 128-B row m / 4 (the same
@@ -843,6 +857,7 @@ __device__ __forceinline__ void sweep_dir_wide(const Dir& d) {
         ti1 = n1;
       }
     }
+    const bool full_chunk = (k + 1) * kWChunk <= nx;
     if (d.stage_out) {
       // psi through the consumed source tile: the lanes write their four
       // cells where they read the sources (swizzled, conflict free), then
@@ -856,8 +871,14 @@ __device__ __forceinline__ void sweep_dir_wide(const Dir& d) {
         st_shared_v2(tile + unit(c, 0), ps[c][0], ps[c][1]);
         st_shared_v2(tile + unit(c, 1), ps[c][2], ps[c][3]);
       }
+      if (tst) asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // the writers' side of the TMA store
       __syncwarp();
       const long long gstart = XU ? cell - c0 : cell + c0 - (kWChunk - 1);  // the chunk's first cell in memory
+      if (tst && full_chunk) {
+        // a whole chunk: one TMA store of the tile (no read-back, no store
+        // instructions of the lanes); the engine un-swizzles it
+        if (lane == 0) tma_store_tile(d.pmap, static_cast<int>(d.psi_row0 + gstart / 4), tile);
+      } else {
       const unsigned rsw = static_cast<unsigned>((lane >> 2) & 7);
       const unsigned lb0 = static_cast<unsigned>((lane >> 2) * 128) + (((2u * (lane & 3)) ^ rsw) << 4);
       const unsigned lb1 = static_cast<unsigned>((lane >> 2) * 128) + (((2u * (lane & 3) + 1u) ^ rsw) << 4);
@@ -869,6 +890,7 @@ __device__ __forceinline__ void sweep_dir_wide(const Dir& d) {
         ld_shared_v2(tile + 1024u * q + lb1, o[2], o[3]);
         const int j = XU ? m : kWChunk - 1 - m;  // its sweep-order column within the chunk
         if (k * kWChunk + j < nx) st_cell256(d.psi + 4 * (gstart + m), o);
+      }
       }
     } else {
 #pragma unroll
@@ -888,10 +910,23 @@ __device__ __forceinline__ void sweep_dir_wide(const Dir& d) {
     }
     __syncwarp();  // (own line: the next row reads what this row wrote; the tile is consumed)
     if (lane == 0) {
-      // (the staged psi was written to the tile through the generic proxy:
-      // ordered before the TMA engine's refill of it)
-      if (d.stage_out) asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-      tma_issue();  // refill the stage this step consumed
+      if (tst) {
+        // refill the previous step's slot once its store has read it (the
+        // newest store may still be reading this step's slot)
+        if (owe) {
+          if (full_chunk)
+            asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+          else  // (no store was issued this step: the newest group is the previous slot's)
+            asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+          tma_issue();
+        }
+        owe = true;
+      } else {
+        // (the staged psi was written to the tile through the generic proxy:
+        // ordered before the TMA engine's refill of it)
+        if (d.stage_out) asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        tma_issue();  // refill the stage this step consumed
+      }
     }
     if (++st == S) st = 0, ph ^= 1u;
     if (MULTI && lane == 0) publish_progress(d.prod + d.w, t + 1);
@@ -912,6 +947,7 @@ __device__ __forceinline__ void sweep_dir_wide(const Dir& d) {
       ++k;
     }
   }
+  if (tst && lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");  // the tiles stay until read
 }
 
 // Per-direction constants (kConsts layout above), written by one warp.
@@ -981,7 +1017,7 @@ __device__ __forceinline__ void dir_consts(const SweepArgs& a, double omx, doubl
 template <bool UNIFORM, int MODE, bool HAS_BC, bool WIDE>
 __global__ void __launch_bounds__(256, UNIFORM ? 1 : 2)
     sweep_scan_kernel(const SweepArgs a, int W, bool smem_lines, int nck, int stages,
-                      const __grid_constant__ CUtensorMap tmap) {
+                      const __grid_constant__ CUtensorMap tmap, const __grid_constant__ CUtensorMap pmap) {
   static_assert(!WIDE || UNIFORM, "the wide kernel is for uniform media");
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   __shared__ __align__(8) unsigned long long tma_bars[WIDE ? kWarps * kMaxStages : 1];
@@ -1031,7 +1067,9 @@ __global__ void __launch_bounds__(256, UNIFORM ? 1 : 2)
   d.bars = smem_u32(tma_bars) + (WIDE ? 8u * kMaxStages * wib : 0u);
   d.src_row0 = static_cast<long long>(slot) * a.rhs_stride / 16;
   d.stages = stages;
-  d.stage_out = a.stage_out != 0;
+  d.stage_out = a.stage_out;
+  d.pmap = &pmap;
+  d.psi_row0 = static_cast<long long>(slot) * a.psi_stride / 16;
   if (WIDE) {
     if (lane == 0) {
       for (int u = 0; u < stages; ++u) mbar_init(d.bars + 8u * u, 1);
@@ -1449,13 +1487,31 @@ bool make_source_map(const SweepArgs& a, CUtensorMap* m) {
              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
+// psi of all n directions as the same kind of tensor (for the TMA store).
+bool make_psi_map(const SweepArgs& a, CUtensorMap* m) {
+  const EncodeTiled enc = encode_tiled();
+  if (!enc || a.psi_stride % 16 != 0 || reinterpret_cast<uintptr_t>(a.psi) % 16 != 0) return false;
+  const unsigned long long total = static_cast<unsigned long long>(a.n - 1) * a.psi_stride +
+                                   4ull * static_cast<unsigned long long>(a.nx) * a.ny;
+  if (total % 16 != 0) return false;  // (a box past the last row would be clipped: keep whole rows)
+  const cuuint64_t dims[2] = {16, total / 16};
+  const cuuint64_t strides[1] = {128};
+  const cuuint32_t box[2] = {16, static_cast<cuuint32_t>(kWChunk / 4)};
+  const cuuint32_t estr[2] = {1, 1};
+  return enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, a.psi, dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+             CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) ==
+         CUDA_SUCCESS;
+}
+
 }  // namespace
 
 void launch_sweep_scan(const SweepArgs& a_in, bool uniform, cudaStream_t s) {
   SweepArgs a = a_in;
-  static const int stage_out = [] {  // RTLR_SCAN_STOUT=0: the lanes store their own cells (A/B)
+  // RTLR_SCAN_STOUT: 0 the lanes store their own cells, 1 read-back and
+  // coalesced stores, 2 TMA stores of whole chunks (A/B)
+  static const int stage_out = [] {
     const char* e = std::getenv("RTLR_SCAN_STOUT");
-    return (e && e[0] == '0') ? 0 : 1;
+    return e ? std::max(0, std::min(2, std::atoi(e))) : 2;
   }();
   a.stage_out = stage_out;
   if (a.n <= 0) return;
@@ -1557,6 +1613,9 @@ void launch_sweep_scan(const SweepArgs& a_in, bool uniform, cudaStream_t s) {
                        4LL * a.n * pl.W >= 3LL * sm_count() * kWarps;
     wide = fills && pl.smem_lines && stages >= 2 && make_source_map(a, &tmap);
   }
+  CUtensorMap pmap;
+  std::memset(&pmap, 0, sizeof(pmap));
+  if (wide && a.stage_out == 2 && !(stages >= 3 && make_psi_map(a, &pmap))) a.stage_out = 1;
   size_t smem;
   if (wide) {
     smem = pl.smem + 1024 + static_cast<size_t>(kWarps) * stages * kWTileBytes;
@@ -1570,7 +1629,7 @@ void launch_sweep_scan(const SweepArgs& a_in, bool uniform, cudaStream_t s) {
   const int blocks = (a.n + groups - 1) / groups;
   auto go = [&](auto kern) {
     RTLR_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kScanSmemMax)));
-    kern<<<blocks, kWarps * 32, smem, s>>>(a, W, smem_lines, nck, stages, tmap);
+    kern<<<blocks, kWarps * 32, smem, s>>>(a, W, smem_lines, nck, stages, tmap, pmap);
   };
   const bool bc = a.bc != nullptr;
 #define RTLR_SCAN_GO(U, M)                                                                        \

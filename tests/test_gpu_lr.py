@@ -380,3 +380,33 @@ def test_prefactored_candidates_keep_the_solve(tmp_path):
     assert out["on"][0] == out["off"][0]
     assert np.array_equal(out["on"][2:2 + nit], out["off"][2:2 + nit])  # ranks per outer iteration
     assert rel(out["on"][2 + nit:], out["off"][2 + nit:]) <= 1e-9
+
+
+_PREFACTOR_SHARDED_RUN = r'''
+import sys, numpy as np
+sys.path.insert(0, sys.argv[1])
+import paper_2603_25233_b200 as P
+g = P.Problem("C3", nx=48, ny=48, n_theta=24, n_omega_z=8)
+if sys.argv[3] == "1":
+    g.set_comm(1, 0, P.nccl_unique_id())
+r = g.solve_low_rank(build_factors=0)
+np.save(sys.argv[2], np.concatenate([[r.iterations, sum(r.history("inner_iterations"))], r.history("rank"), r.phi]))
+'''
+
+
+def test_prefactored_candidates_with_a_communicator(tmp_path):
+    """With a communicator every rank factors and finishes all the greedy
+    candidates itself (replicated projections, no all-gather of their
+    solutions): a single-rank NCCL solve is bitwise the unsharded one with
+    the look-ahead active from rank 8 up."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    out = {}
+    for tag in ("0", "1"):
+        f = str(tmp_path / f"pfs_{tag}.npy")
+        env = dict(os.environ, RTLR_LU_PREFACTOR_MIN="8")
+        subprocess.run([sys.executable, "-c", _PREFACTOR_SHARDED_RUN, root, f, tag], env=env, check=True, timeout=600)
+        out[tag] = np.load(f)
+    assert np.array_equal(out["0"], out["1"])
