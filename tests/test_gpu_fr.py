@@ -225,3 +225,42 @@ def test_sharded_full_rank_single_rank_nccl():
     rb = b.solve_full_rank(store_psi=0)
     assert rb.iterations == ra.iterations
     assert rel(rb.phi, ra.phi) <= 1e-13
+
+
+_STOUT_RUN = r'''
+import sys, numpy as np
+sys.path.insert(0, sys.argv[1])
+import paper_2603_25233_b200 as P
+ov = eval(sys.argv[3])
+g = P.Problem("homogeneous(1,1)", use_dsa=0, **ov)
+g.set_option("sweep_kernel", 2)
+rng = np.random.default_rng(11)
+rhs = rng.standard_normal((g.n, g.n_omega))
+np.save(sys.argv[2], g.sweep(np.arange(g.n_omega), rhs))
+'''
+
+
+@pytest.mark.parametrize("ov", [
+    {"nx": 256, "ny": 40, "n_theta": 8, "n_omega_z": 2},                          # whole chunks: TMA stores only
+    {"nx": 196, "ny": 30, "n_theta": 8, "n_omega_z": 2},                          # a chunk cut by the row end
+    {"nx": 1152, "ny": 16, "n_theta": 8, "n_omega_z": 2},                         # column-split rows
+    {"nx": 132, "ny": 20, "n_theta": 4, "n_omega_z": 2, "boundary_const": 1.0},   # inflow data
+])
+def test_wide_sweep_output_paths_are_bitwise_equal(ov, tmp_path):
+    """The wide kernel's three psi output paths (RTLR_SCAN_STOUT: 0 the
+    lanes' own stores, 1 staged tile read back for coalesced stores, 2 TMA
+    stores of whole chunks with the read-back path for chunks cut by the row
+    end) move the same values: bitwise equal psi for all four quadrants."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    out = {}
+    for v in ("0", "1", "2"):
+        f = str(tmp_path / f"stout_{v}.npy")
+        env = dict(os.environ, RTLR_SCAN_STOUT=v, RTLR_SWEEP_TMA="1")
+        subprocess.run([sys.executable, "-c", _STOUT_RUN, root, f, repr(ov)], env=env, check=True, timeout=600)
+        out[v] = np.load(f)
+    assert np.isfinite(out["0"]).all() and np.linalg.norm(out["0"]) > 0
+    assert np.array_equal(out["0"], out["1"])
+    assert np.array_equal(out["0"], out["2"])
