@@ -410,3 +410,39 @@ def test_prefactored_candidates_with_a_communicator(tmp_path):
         subprocess.run([sys.executable, "-c", _PREFACTOR_SHARDED_RUN, root, f, tag], env=env, check=True, timeout=600)
         out[tag] = np.load(f)
     assert np.array_equal(out["0"], out["1"])
+
+
+_PREDRAW_RUN = r'''
+import sys, json, numpy as np
+sys.path.insert(0, sys.argv[1])
+import paper_2603_25233_b200 as P
+g = P.Problem("C3", nx=48, ny=48, n_theta=24, n_omega_z=8)
+r = g.solve_low_rank(build_factors=0)
+np.save(sys.argv[2], r.phi)
+json.dump({"it": int(r.iterations), "inner": [int(x) for x in r.history("inner_iterations")],
+           "rank": [int(x) for x in r.history("rank")], "sampled": r.sampled_log()}, open(sys.argv[2] + ".json", "w"))
+'''
+
+
+def test_predrawn_candidates_follow_the_reference_rng_sequence(tmp_path):
+    """The candidates of an inner iteration are drawn at the end of the one
+    before (lowrank.cu predraw).  With the look-ahead factorisation out of
+    reach (threshold rank 10^6) the arithmetic is that of the solve without
+    it, so the early draw alone is tested: the sampled angles of every outer
+    iteration, the inner-iteration counts, the ranks and phi are bitwise
+    those of the solve that draws where the reference does
+    (low_rank.cpp:217-226)."""
+    import json
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    out = {}
+    for tag, env_add in (("early", {"RTLR_LU_PREFACTOR_MIN": "1000000"}), ("late", {"RTLR_LU_PREFACTOR": "0"})):
+        f = str(tmp_path / f"pd_{tag}.npy")
+        subprocess.run([sys.executable, "-c", _PREDRAW_RUN, root, f], env=dict(os.environ, **env_add), check=True,
+                       timeout=600)
+        out[tag] = (np.load(f), json.load(open(f + ".json")))
+    assert out["early"][1] == out["late"][1]
+    assert np.array_equal(out["early"][0], out["late"][0])
+    assert sum(out["early"][1]["inner"]) >= 20
