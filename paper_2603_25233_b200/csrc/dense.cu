@@ -2219,6 +2219,90 @@ __global__ void __launch_bounds__(1024, 1) galerkin_cta_lu(int r, const int* __r
   if (tid == 0) flags[jb] = bad;
 }
 
+// The same one-CTA elimination keeping the factors, for the look-ahead
+// factorisation of the greedy candidates at r <= kCtaLuMax (the blocked
+// chain's 2 r / 32 launches of ~45 + 16 us were the critical path of small
+// problems: C2's inner iteration has ~350 us of other work).  Output in the
+// blocked path's format, which galerkin_border_kernel replays: L below the
+// diagonal with a step's row exchange applied to the columns of its own
+// 32-column panel and to everything right of it (not to earlier panels), U
+// on and above, the forward-substituted right-hand side in column r, the
+// pivot rows in piv.
+// (in place on the systems lu_assemble wrote: the projections are read by
+// that short kernel only, so the main stream's wait for them stays short)
+__global__ void __launch_bounds__(1024, 1) galerkin_cta_factor(int r, double* __restrict__ Mout,
+                                                               int* __restrict__ pivout) {
+  extern __shared__ double Am[];  // r x (r + 1), column-major, ld r
+  __shared__ double prow[kCtaLuMax + 1], lcol[kCtaLuMax];
+  __shared__ int sp;
+  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+  const int jb = blockIdx.x;
+  int* pv = pivout + static_cast<size_t>(jb) * r;
+  {
+    const double* in = Mout + static_cast<size_t>(jb) * r * (r + 1);
+    for (int e = tid; e < r * (r + 1); e += 1024) Am[e] = in[e];
+  }
+  __syncthreads();
+  auto argmax_col = [&](int c) {  // warp c % 32: first maximum of |A[i, c]|, i >= c
+    double best = -1.0;
+    int bi = r;
+    for (int i = c + ((lane - c) & 31); i < r; i += 32) {
+      const double v = fabs(Am[i + c * r]);
+      if (v > best) {
+        best = v;
+        bi = i;
+      }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) argmax_merge(best, bi, __shfl_xor_sync(0xffffffffu, best, o),
+                                                  __shfl_xor_sync(0xffffffffu, bi, o));
+    if (lane == 0) sp = best > 0.0 ? bi : c;  // all-zero column: no swap
+  };
+  if (w == 0) argmax_col(0);
+  __syncthreads();
+  for (int k = 0; k < r; ++k) {
+    const int p = sp;
+    const double d = Am[p + k * r];
+    const int ps = k & ~(kNbMax - 1);  // first column of this step's panel
+    // (1) rows k and p exchanged in the panel's earlier columns (their L
+    // entries) and right of column k (prow keeps the pivot row); multipliers
+    // from column k as the exchange leaves it (column k is written in (2))
+    for (int j = ps + tid; j <= r; j += 1024) {
+      if (j == k) continue;
+      const double pr = Am[p + j * r];
+      if (j > k) prow[j] = pr;
+      if (p != k) {
+        Am[p + j * r] = Am[k + j * r];
+        Am[k + j * r] = pr;
+      }
+    }
+    for (int i = k + 1 + tid; i < r; i += 1024) {
+      const double a = i == p ? Am[k + k * r] : Am[i + k * r];
+      lcol[i] = d != 0.0 ? a / d : a;
+    }
+    __syncthreads();
+    if (tid == 0) {
+      Am[k + k * r] = d;
+      pv[k] = p;
+    }
+    // (2) L's column k stored; rank-1 update of rows > k, columns > k
+    for (int i = k + 1 + tid; i < r; i += 1024) Am[i + k * r] = lcol[i];
+    const int j0 = w + 32 * ((k + 1 - w + 31) >> 5);  // first column of this warp > k
+    const int i0 = lane + 32 * ((k + 1 - lane + 31) >> 5);
+    for (int j = j0; j <= r; j += 32) {
+      const double u = prow[j];
+      for (int i = i0; i < r; i += 32) Am[i + j * r] -= lcol[i] * u;
+    }
+    if (k + 1 < r && w == ((k + 1) & 31)) {
+      __syncwarp();
+      argmax_col(k + 1);
+    }
+    __syncthreads();
+  }
+  double* out = Mout + static_cast<size_t>(jb) * r * (r + 1);
+  for (int e = tid; e < r * (r + 1); e += 1024) out[e] = Am[e];
+}
+
 // For one 64-column tile of the trailing columns (k0+jb .. r, the last one
 // the augmented rhs): the panel's row swaps, U12 = L11^-1 A12, then
 // A22 -= L21 U12 row tile by row tile.  grid (column tiles, systems).
@@ -3212,9 +3296,24 @@ void galerkin_prefactor(int r, int m, const int* angles, const double* dirs, con
   double* M = work;
   int* piv = reinterpret_cast<int*>(work + static_cast<size_t>(m) * r * (r + 1));
   int* perm = reinterpret_cast<int*>(work + static_cast<size_t>(m) * (r * static_cast<size_t>(r + 1) + r));
+  static const bool cta_factor = [] {  // RTLR_PREFACTOR_CTA=0: the blocked chain at every rank (A/B)
+    const char* e = std::getenv("RTLR_PREFACTOR_CTA");
+    return !(e && e[0] == '0');
+  }();
   lu_assemble<<<dim3(std::max(1, std::min(64, (r * (r + 1) + 255) / 256)), m), 256, 0, s>>>(
       r, angles, dirs, proj, ldp, proj_stride, prhs, nullptr, 0, M);
   if (assembled) RTLR_CUDA(cudaEventRecord(assembled, s));  // proj and prhs are not read past this point
+  if (cta_factor && m <= kSmemLuSmallBatch && r <= kCtaLuMax) {
+    static const bool attr = [] {
+      RTLR_CUDA(cudaFuncSetAttribute(galerkin_cta_factor, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     kCtaLuMax * (kCtaLuMax + 1) * 8));
+      return true;
+    }();
+    (void)attr;
+    galerkin_cta_factor<<<m, 1024, static_cast<size_t>(r) * (r + 1) * sizeof(double), s>>>(r, M, piv);
+    RTLR_CUDA(cudaGetLastError());
+    return;
+  }
   lu_factor_blocked(r, m, M, piv, perm, s);
   RTLR_CUDA(cudaGetLastError());
 }
