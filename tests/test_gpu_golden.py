@@ -47,15 +47,22 @@ def load(tag):
 # iterations, sampled sets side by side) as well as to its full-rank run.
 C4R = {"nx": 128, "ny": 128, "n_theta": 32, "n_omega_z": 16}
 C4R_TAG = "C4_n_omega_z16_n_theta32_nx128_ny128"
+# C4m: the same medium at 256^2 cells (262,144 DOFs, rank ~229 of the 256
+# distinct directions): the largest low-rank oracle run of C4's medium that
+# fits a session (tests/golden/make_golden.py, one core).
+C4M = {"nx": 256, "ny": 256, "n_theta": 32, "n_omega_z": 16}
+C4M_TAG = "C4_n_omega_z16_n_theta32_nx256_ny256"
+TAGS = {128: C4R_TAG, 256: C4M_TAG}
 
 
 @pytest.mark.parametrize("name,method,ov", [("C1", "full", {}), ("C2", "full", {}), ("C2", "lowrank", {}),
                                             ("C3", "full", {}), ("C3", "lowrank", {}), ("C4", "full", {}),
-                                            ("C4", "full", C4R), ("C4", "lowrank", C4R)],
+                                            ("C4", "full", C4R), ("C4", "lowrank", C4R),
+                                            ("C4", "full", C4M), ("C4", "lowrank", C4M)],
                          ids=["C1-full", "C2-full", "C2-lowrank", "C3-full", "C3-lowrank", "C4-full",
-                              "C4r-full", "C4r-lowrank"])
+                              "C4r-full", "C4r-lowrank", "C4m-full", "C4m-lowrank"])
 def test_baseline_config_matches_oracle(name, method, ov):
-    g = load((C4R_TAG if ov else name) + f"_{method}")
+    g = load((TAGS[ov["nx"]] if ov else name) + f"_{method}")
     p = P.Problem(name, **ov)
     r = p.solve_full_rank(store_psi=0) if method == "full" else p.solve_low_rank(build_factors=0)
     ref = g["phi"]
