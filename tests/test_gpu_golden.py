@@ -52,15 +52,19 @@ C4R_TAG = "C4_n_omega_z16_n_theta32_nx128_ny128"
 # fits a session (tests/golden/make_golden.py, one core).
 C4M = {"nx": 256, "ny": 256, "n_theta": 32, "n_omega_z": 16}
 C4M_TAG = "C4_n_omega_z16_n_theta32_nx256_ny256"
-TAGS = {128: C4R_TAG, 256: C4M_TAG}
+# C4l: 384^2 cells (589,824 DOFs), the oracle's low-rank run ~1 h.
+C4L = {"nx": 384, "ny": 384, "n_theta": 32, "n_omega_z": 16}
+C4L_TAG = "C4_n_omega_z16_n_theta32_nx384_ny384"
+TAGS = {128: C4R_TAG, 256: C4M_TAG, 384: C4L_TAG}
 
 
 @pytest.mark.parametrize("name,method,ov", [("C1", "full", {}), ("C2", "full", {}), ("C2", "lowrank", {}),
                                             ("C3", "full", {}), ("C3", "lowrank", {}), ("C4", "full", {}),
                                             ("C4", "full", C4R), ("C4", "lowrank", C4R),
-                                            ("C4", "full", C4M), ("C4", "lowrank", C4M)],
+                                            ("C4", "full", C4M), ("C4", "lowrank", C4M),
+                                            ("C4", "full", C4L), ("C4", "lowrank", C4L)],
                          ids=["C1-full", "C2-full", "C2-lowrank", "C3-full", "C3-lowrank", "C4-full",
-                              "C4r-full", "C4r-lowrank", "C4m-full", "C4m-lowrank"])
+                              "C4r-full", "C4r-lowrank", "C4m-full", "C4m-lowrank", "C4l-full", "C4l-lowrank"])
 def test_baseline_config_matches_oracle(name, method, ov):
     g = load((TAGS[ov["nx"]] if ov else name) + f"_{method}")
     p = P.Problem(name, **ov)
